@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 blue-noise sampler optimiser (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+A step is one optimisation pass over the whole tile (all 64 colour classes: candidate counts,
+windowed distances, energy terms, decisions, commit) = L*L pixel-update evaluations.
+N = 1 runs BASELINE's metric workload C3 (128x128 tile, T = 1024, 1/4/16/64 spp).  N > 1
+(torchrun, one process per GPU) gives every rank its own independent dimension-pair tile of
+the same shape (pair j = rank, seeds XOR j; reading R13): no data-path collective, weak
+scaling, value = all ranks' evals / max-over-ranks device time.
+
+--impl reference times the CPU oracle (oracle/, single-threaded C) on bounded samples of the
+same workload; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "pixel-update evals/s per pass (128² tile, T=1024) + % HBM/FP roofline, 1–8 GPU"
+UNIT = "evals/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+# fma-pipe integer issue (IMAD/IDP4A): 16 lanes/clk/SMSP x 4 SMSP (B300_MICROARCH.md "Pipe rates"),
+# 148 SMs; one IDP.4A = 4 int8 multiply-accumulates = 8 ops.  DESIGN.md §7 derives this peak.
+SMS = 148
+DP4A_PER_CLK_SM = 64
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-classes", type=int, default=12, help="colour classes in the oracle sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def workload(cfg):
+    return {
+        "workload": f"{cfg.name}: {cfg.note}",
+        "tile": cfg.L, "T": cfg.T, "spp_levels": list(cfg.levels),
+        "mode": "redraw" if cfg.mode == 0 else "swap", "radius": 7, "sigma_i": 2.1, "sigma_s": 1.0,
+        "step": f"one optimisation pass = {cfg.L * cfg.L} pixel-update evals (64 colour classes)",
+    }
+
+
+def config_json(cfg, n):
+    c = workload(cfg)
+    c["per_rank"] = "one independent dimension-pair tile (pair j = rank, seeds xor j)"
+    c["global_tiles"] = n
+    c["l2"] = "per-pass working set ~0.5 GB (counts 2x64 MB, distances 117 MB, dE tables 117 MB) > 126 MB L2; no flush"
+    return c
+
+
+# ---------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in (self.out or "").splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), f[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        smax = max(r[1] for r in rows)
+        loaded = [r[0] for r in rows if r[0] > 0.3 * smax] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------- roofline
+def algorithmic(kernel, cfg):
+    """(units per launch, unit, bound) of each kernel class -- DESIGN.md §7."""
+    P, T, nl, R = cfg.L * cfg.L, cfg.T, len(cfg.levels), 7
+    H = 2 * R * R + 2 * R
+    if kernel == "gram":
+        # 4 int8 dot products per unordered window pair and level, T-long: 2 ops per MAC
+        return 2.0 * P * H * 4 * nl * T, "ops", "alu"
+    if kernel == "counts":
+        # one exact half-plane test = 2 int32x int32->int64 multiply-adds per (pixel, integrand, sample)
+        return 2.0 * P * T * max(cfg.levels), "imad.wide", "alu"
+    if kernel == "lut":
+        # bytes: read 4 int32 distances per (p, h, level); write 4 int128 dE terms per (p, h)
+        return float(P * H * (16 * nl + 64)), "bytes", "hbm"
+    if kernel == "decide":
+        # bytes: one int128 dE term per (candidate, window offset) across the 64 classes / 64 launches
+        return float(P * (2 * R + 1) ** 2 * 16) / 64, "bytes", "hbm"
+    return None, None, None
+
+
+def roofline(prof, cfg, peaks, sm_clock_mhz):
+    name = max(prof, key=lambda k: prof[k][0])
+    ms, n = prof[name]
+    units, kind, bound = algorithmic(name, cfg)
+    share = ms / max(1e-9, sum(v[0] for v in prof.values()))
+    out = {"kernel": name, "share_of_step": round(share, 4), "avg_launch_ms": ms / max(n, 1)}
+    if units is None:
+        out.update(bound="latency", achieved=None, peak=None, unit=None, frac=None, traffic=None)
+        return out
+    per_s = units / (ms / max(n, 1) / 1e3)
+    if bound == "hbm":
+        peak = peaks.get("hbm_gbs", 6650.0)
+        out.update(bound="hbm", achieved=per_s / 1e9, peak=peak, unit="GB/s")
+        out["peak_source"] = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
+    else:
+        clk = peaks.get("sm_max_mhz", 1965.0)
+        if kind == "ops":
+            peak = SMS * DP4A_PER_CLK_SM * 8 * clk * 1e6 / 1e12  # TOP/s (dp4a: 4 MAC = 8 ops)
+            out.update(bound="alu", achieved=per_s / 1e12, peak=peak, unit="TOP/s")
+        else:
+            peak = SMS * 64 * 0.5 * clk * 1e6 / 1e12             # T IMAD.WIDE/s (half-rate wide ops)
+            out.update(bound="alu", achieved=per_s / 1e12, peak=peak, unit="T imad.wide/s")
+        out["peak_source"] = ("derived: 148 SM x 64 lanes/clk fma-pipe x clocks.max.sm "
+                              f"{clk:.0f} MHz (DESIGN.md §7)")
+    out["frac"] = out["achieved"] / out["peak"]
+    out["traffic"] = None
+    try:
+        tr = json.load(open(TRAFFIC_FILE)).get(f"{cfg.name}:{name}")
+        if tr:
+            out["traffic"] = tr["dram_bytes_per_launch"]
+            out["traffic_source"] = tr.get("source", TRAFFIC_FILE)
+    except (OSError, ValueError):
+        pass
+    if sm_clock_mhz:
+        out["sm_mhz_during_run"] = sm_clock_mhz
+    return out
+
+
+# --------------------------------------------------------------------------- oracle sample
+def oracle_sample(cfg, pair, classes, passes_done=0, state=None):
+    """Run the CPU oracle over the first `classes` colour classes of a pass; returns
+    (evals, seconds, state).  Setup (bank, initial counts) is outside the timing."""
+    from oracle import oracle
+
+    if state is None:
+        U, (a, b, px, py) = synth.problem_inputs(cfg, pair)
+        pb = oracle.OracleProblem(cfg.L, cfg.T, cfg.levels, synth.D1, synth.D2, a, b, px, py)
+        state = [pb, U, pb.counts(U)]
+    pb, U, c = state
+    M = (cfg.L // 8) ** 2
+    t0 = time.perf_counter()
+    U, c, st, _ = pb.optimize(U, c, mode=cfg.mode, passes=1, first_pass=passes_done,
+                              seed=synth.opt_seed(cfg, pair), max_steps=classes, energy_each_pass=False)
+    dt = time.perf_counter() - t0
+    state[1], state[2] = U, c
+    return classes * M, dt, state
+
+
+def cpu_sample_desc(cfg, classes):
+    M = (cfg.L // 8) ** 2
+    return (f"oracle (single-threaded C, -O2) on {cfg.name}: first {classes} of 64 colour classes of pass 0 "
+            f"= {classes * M} pixel-update evals (full distances recomputed from counts per candidate)")
+
+
+def run_reference(args, cfg):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    state = None
+    classes = 2
+    for w in range(args.warmup):
+        _, _, state = oracle_sample(cfg, 0, classes, w, state)
+    ev = tt = 0.0
+    per = []
+    for k in range(args.steps):
+        e, dt, state = oracle_sample(cfg, 0, classes, args.warmup + k, state)
+        ev += e
+        tt += dt
+        per.append(dt)
+    v = ev / tt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": config_json(cfg, 1),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": cpu_sample_desc(cfg, classes) + " per step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------ ours
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2105_12620_b200 import bn
+
+    rank, local, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.current_stream()
+    pair = rank
+    U, (a, b, px, py) = synth.problem_inputs(cfg, pair)
+    seed = synth.opt_seed(cfg, pair)
+    s = bn.Sampler(local, stream.cuda_stream)
+    s.set_lattice(synth.D1, synth.D2, cfg.levels)
+    s.set_bank(a, b, px, py)
+    s.set_energy(2.1, 1.0, 7)
+    s.set_tile(cfg.L, U)
+    P = cfg.L * cfg.L
+
+    # warm-up passes (W >= 3 by contract)
+    s.optimize(args.warmup, seed, mode=cfg.mode, first_pass=0, stats=False)
+    barrier()
+    l0 = s.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        s.optimize(args.steps, seed, mode=cfg.mode, first_pass=args.warmup, stats=False)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = s.launch_count() - l0
+    ms_max = max_over_ranks(ms)
+    value = P * args.steps * world / (ms_max / 1e3)
+    clocks = clk.summary()
+
+    # per-kernel device time on the context stream (same passes, events around each launch)
+    s.profile_enable(True)
+    s.optimize(args.steps, seed, mode=cfg.mode, first_pass=args.warmup + args.steps, stats=False)
+    prof = s.profile()
+    s.profile_enable(False)
+    roof = roofline({k: v for k, v in prof.items() if v[1]}, cfg, peaks, clocks.get("sm_mhz"))
+
+    # end to end through the public API with host buffers: per step, H2D of the tile, one pass,
+    # D2H of the tile and the pass statistics.
+    pinned = torch.empty((P, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    pinned[:] = s.get_tile()
+    first = args.warmup + 2 * args.steps
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for k in range(args.e2e_steps):
+        s.set_tile(cfg.L, pinned)
+        st, _ = s.optimize(1, seed, mode=cfg.mode, first_pass=first + k, stats=True)
+        s.get_tile(pinned)
+    f1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+    e2e = {"value": P * args.e2e_steps * world / (e2e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": P * 8 + 24, "d2h_bytes_per_step": P * 8 + 48,
+           "path": "bn_set_tile(host) + bn_optimize(1 pass, stats) + bn_get_tile(host) per step"}
+
+    # total launches over all ranks
+    if world > 1:
+        t = torch.tensor([launches], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        launches = int(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ev, dt, _ = oracle_sample(cfg, 0, args.cpu_classes)
+        cpu = {"value": ev / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": cpu_sample_desc(cfg, args.cpu_classes), "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": config_json(cfg, world), "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
+            "roofline": roof, "cpu_baseline": cpu,
+            "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+            "final_energy": st[-1]["E"] if st else None,
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

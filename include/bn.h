@@ -1,0 +1,163 @@
+/*
+ * bn.h -- C-ABI of the B200-native blue-noise screen-space sampler optimiser
+ * (Belcour & Heitz, arXiv 2105.12620; hot path = north star of BASELINE.json).
+ *
+ * The library (paper_2105_12620_b200/libbn.so) owns all device state of ONE tile problem
+ * ("context"): the u_p tile, the integer error-vector counts, the energy look-up tables and
+ * the per-pass work buffers.  Every step of the hot path runs in hand-written sm_100a
+ * kernels; there is no CPU fallback.
+ *
+ * Conventions
+ *  - Fixed point: a value v in [0,1) is the uint32 V with v = V / 2^32.
+ *  - Pixels: p = y * L + x, 0 <= x, y < L; the tile repeats toroidally.
+ *  - Tiles:  u_xy[2p + 0] = u_p.x, u_xy[2p + 1] = u_p.y                (uint32, 8 B / pixel)
+ *  - Counts: out[(l * P + p) * Ts + i] = c_l,p,i = #{k < N_l : f_i(mod(s^k + u_p, 1)) = 1}
+ *            (uint8, level-major; Ts = t_end - t_begin of this context's bank shard).
+ *            The error vector of PAPER.md l.238-240 is e_p,i = c / N_l - I_ref,i exactly.
+ *  - Ownership: the caller owns every buffer passed in or out; inputs are copied during the
+ *    call.  Device pointers (is_device != 0) must be device memory of the context's device
+ *    (e.g. torch tensor data_ptr()).
+ *  - Streams: calls are enqueued on the context's stream.  Calls that return host data
+ *    (bn_energy, bn_optimize with stats/accept_log, host get_tile/eval_counts,
+ *    bn_get_references) synchronise that stream before returning.
+ *  - Errors: every int-returning call returns a status below; bn_last_error() returns a
+ *    human-readable message for the last failure on that context.  A failed call leaves the
+ *    context's previously committed state unchanged unless it reports BN_ECUDA.
+ *  - Threading: a context is single-stream and not thread-safe; distinct contexts are
+ *    independent (one per GPU, rank or dimension pair).
+ */
+#ifndef BN_H
+#define BN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum bn_status {
+    BN_OK = 0,
+    BN_EINVAL = 1, /* argument outside the documented domain                            */
+    BN_ECUDA = 2,  /* CUDA runtime / launch failure (message has cudaGetErrorString)     */
+    BN_ENCCL = 3,  /* NCCL failure (multi-GPU bank sharding)                             */
+    BN_ENOMEM = 4, /* device allocation failed                                          */
+    BN_ESTATE = 5  /* call order violated, or an internal invariant failed              */
+};
+
+typedef struct bn_ctx bn_ctx;
+
+/* Create a context on CUDA device `cuda_device`, enqueuing work on `cuda_stream`
+ * (a cudaStream_t cast to uintptr_t; 0 = the legacy default stream).  *out = NULL on error. */
+int bn_create(bn_ctx **out, int cuda_device, uintptr_t cuda_stream);
+void bn_destroy(bn_ctx *ctx);
+const char *bn_last_error(const bn_ctx *ctx);
+/* Library build string (arch, version); never NULL. */
+const char *bn_version(void);
+
+/* Main sequence s^k = mod(Phi(k) d, 1) (§3.2 l.258-263): rank-1 lattice with
+ * integer direction vector d = (d1, d2), van der Corput order.  spp_levels[0..n_levels) are
+ * the progressive sample counts N_l (prefixes of the vdC order): strictly ascending powers
+ * of two in [1, 128], 1 <= n_levels <= 8.  EINVAL otherwise. */
+int bn_set_lattice(bn_ctx *ctx, uint32_t d1, uint32_t d2, const uint32_t *spp_levels,
+                   uint32_t n_levels);
+
+/* Bank of T Heaviside test integrands ("randomly oriented Heavisides"):
+ *   f_i(x, y) = 1  iff  a_i (x - px_i) + b_i (y - py_i) >= 0   (exact on the 2^-32 grid)
+ * a, b: int32 [T] with |a|, |b| <= 2^15 (so the test is exact in int64); px, py: uint32 [T]
+ * fixed-point anchors.  Host arrays, copied.  This context evaluates the shard
+ * [t_begin, t_end) (0 <= t_begin < t_end <= T); the energy always uses the full-T distance
+ * (shards are summed across ranks by bn_comm_init's communicator).  EINVAL on T = 0,
+ * bad range or |a|,|b| too large. */
+int bn_set_bank(bn_ctx *ctx, uint32_t T, const int32_t *a, const int32_t *b,
+                const uint32_t *px, const uint32_t *py, uint32_t t_begin, uint32_t t_end);
+
+/* Exact references I_ref,i (area of the half-plane inside [0,1]^2; teaser l.154) of this
+ * context's shard, fp64, written to host iref[t_end - t_begin].  Computed on the device. */
+int bn_get_references(bn_ctx *ctx, double *iref);
+
+/* Blue-noise energy parameters (north star; Eq. 1 PAPER.md l.232-237 for sigma_i = 2.1):
+ *   E = sum_l sum_p sum_{o in O} q(o, D_l(p, p+o)),   O = [-R,R]^2 \ {0} (toroidal),
+ *   q(o, D) = rn_uint64( 2^64 * exp(-|o|^2 / sigma_i^2) * exp(-(sqrt(D)/N_l) / sigma_s^2) )
+ *   D_l(p,q) = sum_i (c_l,p,i - c_l,q,i)^2 = N_l^2 ||e_p - e_q||^2   (exact integer)
+ * Defaults 2.1, 1.0, 7.  radius in [1, 7] (the stride-8 colouring needs R < 8); sigmas > 0. */
+int bn_set_energy(bn_ctx *ctx, double sigma_i, double sigma_s, int32_t radius);
+
+/* Load the tile U (L*L pixels, L a power of two >= 16, L > 2R) and build its counts.
+ * u_xy: [2 L L] uint32, host (is_device = 0) or device.  Requires lattice and bank. */
+int bn_set_tile(bn_ctx *ctx, uint32_t L, const uint32_t *u_xy, int is_device);
+/* Copy the current tile out ([2 L L] uint32) to host or device memory. */
+int bn_get_tile(bn_ctx *ctx, uint32_t *u_xy, int is_device);
+
+/* Exact error-vector representation: the counts of the current tile, layout in the header
+ * comment, n_levels * L*L * (t_end - t_begin) bytes, host or device. */
+int bn_eval_counts(bn_ctx *ctx, uint8_t *out, int is_device);
+
+/* Energy of the current tile, recomputed from the counts (not incremental).
+ * E_fixed[0..1] = (low, high) 64-bit words of the exact uint128 sum; *E = E_fixed * 2^-64.
+ * Either pointer may be NULL.  Multi-GPU: collective over the communicator. */
+int bn_energy(bn_ctx *ctx, double *E, uint64_t E_fixed[2]);
+
+enum bn_mode { BN_REDRAW = 0, BN_SWAP = 1 };
+
+typedef struct {
+    uint32_t mode;       /* BN_REDRAW: re-draw u_p; BN_SWAP: swap u_p within couples        */
+    uint32_t passes;     /* number of passes to run                                       */
+    uint32_t first_pass; /* pass index t of the first pass (resume = continue counting)   */
+    uint32_t K;          /* re-draw candidates per pixel; must be 1 in this version        */
+    uint64_t seed;       /* Philox4x32-10 key of the optimiser                             */
+} bn_opt_params;
+
+typedef struct {
+    uint32_t accepted;   /* candidates (REDRAW) or couples (SWAP) accepted in the pass     */
+    uint32_t proposed;   /* candidates (= L*L) or couples (= L*L/2) evaluated              */
+    double E;            /* E_fixed * 2^-64 after the pass                                */
+    uint64_t E_fixed[2]; /* exact energy after the pass (uint128, low word first)          */
+    uint64_t dE_sum[2];  /* exact sum of the accepted dE (int128, two's complement)        */
+} bn_pass_stats;
+
+/* Run `passes` optimisation passes (§3.4 l.291-302; north star):
+ * pass t visits the 64 colour classes s = 8r + k of the stride-8 schedule
+ *   A(t,r,k) = {(x,y): y = 8b + r, x = 8a + ((delta(t,r,b) + k) & 7)}  (transposed for odd t),
+ *   delta(t,r,b) = Philox(seed; b, t, r, 2)[0] & 7,  active index m = b (L/8) + a,
+ * in order; every member of a class is window-independent of the others.  REDRAW proposes
+ * u'_p = Philox(seed; p, t, 0, 1)[0..1]; SWAP couples m with m ^ kappa,
+ * kappa = 1 + Philox(seed; s, t, 0, 3)[0] mod (M - 1), M = (L/8)^2.  A candidate (couple) is
+ * accepted iff its exact dE < 0 against the state left by the earlier classes.
+ * stats: host [passes] or NULL.  accept_log: host [passes][64][M] bytes (1 = accepted, SWAP:
+ * both members of an accepted couple) or NULL.  EINVAL on K != 1 or an unknown mode. */
+int bn_optimize(bn_ctx *ctx, const bn_opt_params *params, bn_pass_stats *stats,
+                uint8_t *accept_log);
+
+/* Multi-GPU bank sharding: join an NCCL communicator (ncclUniqueId bytes, 128 B, from rank 0
+ * via torch.distributed) of `world` ranks, one context per rank, every rank holding the same
+ * tile and its own [t_begin, t_end) shard.  The only exchange is an int32 sum over ranks of
+ * the partial window distances, once per pass.  ENCCL on failure. */
+int bn_comm_init(bn_ctx *ctx, const void *nccl_unique_id, int rank, int world);
+/* Size of ncclUniqueId (128) and a fresh id for rank 0 to broadcast. */
+int bn_comm_unique_id(void *out128);
+
+/* Kernel launches this context has issued since creation (for the bench's gpu_launches). */
+uint64_t bn_launch_count(const bn_ctx *ctx);
+
+/* Per-kernel device time, measured with CUDA events recorded on the context's stream around
+ * every launch while enabled (the bench's roofline line).  bn_profile_enable(ctx, 1) clears
+ * and starts accumulation, 0 stops it.  bn_profile_get synchronises the stream and returns the
+ * summed milliseconds and launch count of one kernel class. */
+enum bn_kernel_id {
+    BN_K_COUNTS = 0, /* candidate / tile error-vector counts          */
+    BN_K_GATHER = 1, /* SWAP candidate gather                         */
+    BN_K_GRAM = 2,   /* windowed distances (4 per neighbour pair)     */
+    BN_K_LUT = 3,    /* fixed-point energy terms, dE tables, E        */
+    BN_K_DECIDE = 4, /* colour-class decisions                        */
+    BN_K_STATS = 5,  /* exact per-pass reductions                     */
+    BN_K_COMMIT = 6, /* commit accepted rows / shifts                 */
+    BN_K_COUNT_IDS = 7
+};
+int bn_profile_enable(bn_ctx *ctx, int enable);
+int bn_profile_get(bn_ctx *ctx, uint32_t kernel_id, double *total_ms, uint64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BN_H */

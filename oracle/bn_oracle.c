@@ -132,13 +132,24 @@ uint32_t orc_count1(const orc_problem *pb, uint32_t ux, uint32_t uy, uint32_t i,
     return c;
 }
 
-/* Error-vector counts for every pixel: out[l][p][i] (level-major, as the C-ABI documents). */
+/* Error-vector counts for every pixel: out[l][p][i] (level-major, as the C-ABI documents).
+ * Same definition as orc_count1; the main sequence s^k is generated once (orc_lattice) and
+ * each pixel's samples are its shift of it. */
 void orc_counts(const orc_problem *pb, const uint32_t *U, uint32_t P, uint8_t *out) {
+    const uint32_t Nmax = pb->levels[pb->n_levels - 1];
+    uint32_t *S = malloc(sizeof(uint32_t) * 2 * Nmax);
+    orc_lattice(pb->d1, pb->d2, Nmax, S);
     for (uint32_t l = 0; l < pb->n_levels; ++l)
         for (uint32_t p = 0; p < P; ++p)
-            for (uint32_t i = 0; i < pb->T; ++i)
-                out[((size_t)l * P + p) * pb->T + i] =
-                    (uint8_t)orc_count1(pb, U[2 * p], U[2 * p + 1], i, pb->levels[l]);
+            for (uint32_t i = 0; i < pb->T; ++i) {
+                uint32_t c = 0;
+                for (uint32_t k = 0; k < pb->levels[l]; ++k) {
+                    uint32_t X = shift_mod1(S[2 * k], U[2 * p]), Y = shift_mod1(S[2 * k + 1], U[2 * p + 1]);
+                    c += (uint32_t)heaviside(pb->a[i], pb->b[i], pb->px[i], pb->py[i], X, Y);
+                }
+                out[((size_t)l * P + p) * pb->T + i] = (uint8_t)c;
+            }
+    free(S);
 }
 
 /* Exact reference I_ref,i = area of {x in [0,1]^2 : a(x-px) + b(y-py) >= 0}
@@ -416,7 +427,18 @@ int orc_optimize(const orc_problem *pb, uint32_t *U, uint8_t *c, const orc_opt *
             }
             for (uint32_t m = 0; m < M; ++m)
                 if (acc[m]) { ++accepted; dE_sum += dEs[m]; }
-            if (accept_log) memcpy(accept_log + ((size_t)pi * 64 + s) * M, acc, M);
+            if (accept_log) {
+                /* log convention (include/bn.h): SWAP marks both members of an accepted couple */
+                uint8_t *lg = accept_log + ((size_t)pi * 64 + s) * M;
+                memcpy(lg, acc, M);
+                if (opt->mode == 1) {
+                    uint32_t o4[4];
+                    philox_seed(opt->seed, s, t, 0, 3, o4);
+                    const uint32_t kappa = 1 + o4[0] % (M - 1);
+                    for (uint32_t m = 0; m < M; ++m)
+                        if (acc[m]) lg[m ^ kappa] = 1;
+                }
+            }
         }
         if (stats) {
             stats[pi].accepted = accepted;

@@ -1,0 +1,685 @@
+// bn_api.cu -- host side of the C-ABI declared in include/bn.h.
+//
+// Owns the device state of one tile problem and sequences the pass kernels of bn_kernels.cuh
+// on the context's stream.  Host code here only validates arguments, builds the two fp64
+// look-up tables of the energy (W[o], G_l[D]; libm exp/sqrt, no contraction) and moves bytes;
+// every step of the method runs on the GPU.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bn.h"
+#include "bn_kernels.cuh"
+
+using namespace bn;
+
+namespace {
+
+// ---------------------------------------------------------------------- NCCL (dlopen'ed)
+// Loaded lazily so the library has no link-time NCCL dependency (torch ships its own
+// libnccl.so.2; dlopen returns the already-loaded copy when torch is imported first).
+typedef struct { char internal[128]; } NcclUid;
+typedef void* NcclComm;
+typedef int (*nccl_get_uid_t)(NcclUid*);
+typedef int (*nccl_init_rank_t)(NcclComm*, int, NcclUid, int);
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t);
+typedef int (*nccl_destroy_t)(NcclComm);
+typedef const char* (*nccl_errstr_t)(int);
+struct NcclApi {
+    void* h = nullptr;
+    nccl_get_uid_t get_uid = nullptr;
+    nccl_init_rank_t init_rank = nullptr;
+    nccl_allreduce_t allreduce = nullptr;
+    nccl_destroy_t destroy = nullptr;
+    nccl_errstr_t errstr = nullptr;
+    bool load() {
+        if (h) return true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names)
+            if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) return false;
+        get_uid = (nccl_get_uid_t)dlsym(h, "ncclGetUniqueId");
+        init_rank = (nccl_init_rank_t)dlsym(h, "ncclCommInitRank");
+        allreduce = (nccl_allreduce_t)dlsym(h, "ncclAllReduce");
+        destroy = (nccl_destroy_t)dlsym(h, "ncclCommDestroy");
+        errstr = (nccl_errstr_t)dlsym(h, "ncclGetErrorString");
+        return get_uid && init_rank && allreduce && destroy && errstr;
+    }
+};
+NcclApi g_nccl;
+constexpr int NCCL_INT32 = 2, NCCL_SUM = 0;  // ncclInt32, ncclSum (nccl.h enums)
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t ensure(size_t count) {
+        if (count <= n && p) return cudaSuccess;
+        release();
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T) + 16);
+        if (e == cudaSuccess) n = count;
+        return e;
+    }
+};
+
+}  // namespace
+
+struct bn_ctx {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    // lattice
+    bool have_lattice = false;
+    uint32_t d1 = 1, d2 = 1, nl = 0, levels[8] = {0};
+    // bank
+    bool have_bank = false;
+    uint32_t T = 0, t0 = 0, t1 = 0, Ts = 0, Tp = 0;
+    std::vector<int32_t> a, b;
+    std::vector<uint32_t> px, py;
+    // energy
+    double sigma_i = 2.1, sigma_s = 1.0;
+    int R = 7;
+    bool lut_dirty = true;
+    // tile
+    bool have_tile = false, counts_dirty = true;
+    uint32_t L = 0, P = 0, rowB = 0;
+    // device state
+    DevBuf<uint2> S, U, Un, pxy;
+    DevBuf<int2> ab;
+    DevBuf<long long> Cc;
+    DevBuf<uint8_t> c, cn, acc, log, cexp;
+    DevBuf<int> nc, nn, derr;
+    DevBuf<int4> Dt;
+    DevBuf<longlong2> d0, d1b;
+    DevBuf<i128> dEp;
+    DevBuf<u128> Epart;
+    DevBuf<PassStatsDev> pstats;
+    DevBuf<double> W, G, iref;
+    size_t Goff[8] = {0};
+    int Dmax[8] = {0};
+    // multi-GPU
+    NcclComm comm = nullptr;
+    int rank = 0, world = 1;
+    // per-kernel event timing (bn_profile_*)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, size_t>> prof_marks;  // (kernel id, index of start event)
+    double prof_ms[BN_K_COUNT_IDS] = {0};
+    uint64_t prof_n[BN_K_COUNT_IDS] = {0};
+};
+
+namespace {
+
+int fail(bn_ctx* ctx, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                               \
+    do {                                                                                             \
+        cudaError_t e_ = (expr);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? BN_ENOMEM : BN_ECUDA, "%s: %s (%s:%d)", \
+                        #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+    } while (0)
+
+#define LAUNCHED()                                                                              \
+    do {                                                                                        \
+        ++ctx->launches;                                                                        \
+        cudaError_t e_ = cudaGetLastError();                                                    \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(ctx, BN_ECUDA, "launch failed: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                              \
+    } while (0)
+
+cudaEvent_t next_event(bn_ctx* ctx) {
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->ev_pool.push_back(e);
+    }
+    return ctx->ev_pool[ctx->ev_used++];
+}
+// Bracket a launch with events when profiling: KSTART(id) before, LAUNCHED_K() after.
+#define KSTART(id)                                                                  \
+    do {                                                                            \
+        if (ctx->prof) {                                                            \
+            if (ctx->ev_used + 2 > 4096) flush_profile(ctx);                         \
+            ctx->prof_marks.push_back({(id), ctx->ev_used});                         \
+            cudaEventRecord(next_event(ctx), ctx->stream);                          \
+        }                                                                           \
+    } while (0)
+#define LAUNCHED_K()                                                                \
+    do {                                                                            \
+        if (ctx->prof) cudaEventRecord(next_event(ctx), ctx->stream);               \
+        LAUNCHED();                                                                 \
+    } while (0)
+
+void flush_profile(bn_ctx* ctx) {
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& m : ctx->prof_marks) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev_pool[m.second], ctx->ev_pool[m.second + 1]);
+        ctx->prof_ms[m.first] += ms;
+        ctx->prof_n[m.first] += 1;
+    }
+    ctx->prof_marks.clear();
+    ctx->ev_used = 0;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+uint32_t round_up(uint32_t v, uint32_t m) { return (v + m - 1) / m * m; }
+bool pow2(uint32_t v) { return v && !(v & (v - 1)); }
+int half_count(int R) { return 2 * R * R + 2 * R; }
+int win_count(int R) { return (2 * R + 1) * (2 * R + 1) - 1; }
+
+// Energy LUTs.  W[w] = exp(-|o|^2 / sigma_i^2) in full-window order; G_l[D] =
+// exp(-(sqrt(D)/N_l) / sigma_s^2) for 0 <= D <= T N_l^2.  Host libm, -ffp-contract=off.
+int build_lut(bn_ctx* ctx) {
+    const int R = ctx->R;
+    std::vector<double> W(win_count(R));
+    for (int oy = -R; oy <= R; ++oy)
+        for (int ox = -R; ox <= R; ++ox) {
+            if (!ox && !oy) continue;
+            W[win_index(ox, oy, R)] = std::exp(-(double)(ox * ox + oy * oy) / (ctx->sigma_i * ctx->sigma_i));
+        }
+    size_t total = 0;
+    for (uint32_t l = 0; l < ctx->nl; ++l) {
+        const uint64_t dm = (uint64_t)ctx->T * ctx->levels[l] * ctx->levels[l];
+        if (dm > 0x7fffffffull) return fail(ctx, BN_EINVAL, "T * N^2 = %llu exceeds int32", (unsigned long long)dm);
+        ctx->Dmax[l] = (int)dm;
+        ctx->Goff[l] = total;
+        total += dm + 1;
+    }
+    if (total > (1ull << 28)) return fail(ctx, BN_EINVAL, "energy table of %zu entries too large", total);
+    std::vector<double> G(total);
+    const double s2 = ctx->sigma_s * ctx->sigma_s;
+    for (uint32_t l = 0; l < ctx->nl; ++l) {
+        const double N = (double)ctx->levels[l];
+        double* g = G.data() + ctx->Goff[l];
+        for (int D = 0; D <= ctx->Dmax[l]; ++D) g[D] = std::exp(-(std::sqrt((double)D) / N) / s2);
+    }
+    CUDA_TRY(ctx->W.ensure(W.size()));
+    CUDA_TRY(ctx->G.ensure(total));
+    CUDA_TRY(cudaMemcpyAsync(ctx->W.p, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->G.p, G.data(), total * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+    ctx->lut_dirty = false;
+    return BN_OK;
+}
+
+int check_ready(bn_ctx* ctx) {
+    if (!ctx->have_lattice) return fail(ctx, BN_ESTATE, "bn_set_lattice has not been called");
+    if (!ctx->have_bank) return fail(ctx, BN_ESTATE, "bn_set_bank has not been called");
+    if (!ctx->have_tile) return fail(ctx, BN_ESTATE, "bn_set_tile has not been called");
+    if (ctx->L <= (uint32_t)(2 * ctx->R))
+        return fail(ctx, BN_EINVAL, "tile side L = %u must exceed 2R = %d", ctx->L, 2 * ctx->R);
+    return BN_OK;
+}
+
+// (Re)build counts of the current tile when lattice or bank changed after bn_set_tile.
+int ensure_counts(bn_ctx* ctx) {
+    if (!ctx->counts_dirty) return BN_OK;
+    const uint32_t P = ctx->P;
+    ctx->rowB = ctx->nl * ctx->Tp;
+    CUDA_TRY(ctx->Un.ensure(P));
+    CUDA_TRY(ctx->c.ensure((size_t)P * ctx->rowB));
+    CUDA_TRY(ctx->cn.ensure((size_t)P * ctx->rowB));
+    CUDA_TRY(ctx->nc.ensure((size_t)P * ctx->nl));
+    CUDA_TRY(ctx->nn.ensure((size_t)P * ctx->nl));
+    const uint32_t Nmax = ctx->levels[ctx->nl - 1];
+    const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
+    const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
+    KSTART(BN_K_COUNTS);
+    k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->stream>>>(
+        ctx->U.p, nullptr, 0, 0, 0, P, ctx->ab.p, ctx->Cc.p, ctx->Tp, ctx->S.p, Nmax, lo, hi, ctx->nl, ctx->c.p,
+        ctx->nc.p);
+    LAUNCHED_K();
+    ctx->counts_dirty = false;
+    return BN_OK;
+}
+
+int ensure_work(bn_ctx* ctx) {
+    int rc;
+    if ((rc = check_ready(ctx))) return rc;
+    if ((rc = ensure_counts(ctx))) return rc;
+    if (ctx->lut_dirty && (rc = build_lut(ctx))) return rc;
+    const size_t P = ctx->P, H = half_count(ctx->R), WN = win_count(ctx->R);
+    CUDA_TRY(ctx->Dt.ensure(P * H * ctx->nl));
+    CUDA_TRY(ctx->d0.ensure(P * WN));
+    CUDA_TRY(ctx->d1b.ensure(P * WN));
+    CUDA_TRY(ctx->acc.ensure(P));
+    CUDA_TRY(ctx->dEp.ensure(P));
+    CUDA_TRY(ctx->Epart.ensure((P * H + 255) / 256));
+    CUDA_TRY(ctx->derr.ensure(1));
+    return BN_OK;
+}
+
+template <int R>
+int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas) {
+    const uint32_t SW = ctx->L < 32 ? ctx->L : 32;
+    dim3 grid(ctx->L / SW, ctx->L);
+    KSTART(BN_K_GRAM);
+    k_gram<R><<<grid, 32 * (R + 1), 0, ctx->stream>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, SW, ctx->Tp, ctx->nl,
+                                                      ctx->Dt.p);
+    LAUNCHED_K();
+    if (ctx->comm) {
+        const size_t n = (size_t)ctx->P * half_count(R) * ctx->nl * 4;
+        int r = g_nccl.allreduce(ctx->Dt.p, ctx->Dt.p, n, NCCL_INT32, NCCL_SUM, ctx->comm, ctx->stream);
+        if (r) return fail(ctx, BN_ENCCL, "ncclAllReduce: %s", g_nccl.errstr(r));
+    }
+    LutArgs la;
+    for (uint32_t l = 0; l < 8; ++l) {
+        la.G[l] = l < ctx->nl ? ctx->G.p + ctx->Goff[l] : nullptr;
+        la.Dmax[l] = l < ctx->nl ? ctx->Dmax[l] : 0;
+    }
+    const size_t nthr = (size_t)ctx->P * half_count(R);
+    KSTART(BN_K_LUT);
+    k_lut<R><<<(unsigned)((nthr + 255) / 256), 256, 0, ctx->stream>>>(ctx->Dt.p, ctx->L, ctx->nl, ctx->W.p, la,
+                                                                      write_deltas, ctx->d0.p, ctx->d1b.p,
+                                                                      ctx->Epart.p, ctx->derr.p);
+    LAUNCHED_K();
+    return BN_OK;
+}
+
+int gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas) {
+    switch (ctx->R) {
+        case 1: return launch_gram_lut<1>(ctx, cn, nn, write_deltas);
+        case 2: return launch_gram_lut<2>(ctx, cn, nn, write_deltas);
+        case 3: return launch_gram_lut<3>(ctx, cn, nn, write_deltas);
+        case 4: return launch_gram_lut<4>(ctx, cn, nn, write_deltas);
+        case 5: return launch_gram_lut<5>(ctx, cn, nn, write_deltas);
+        case 6: return launch_gram_lut<6>(ctx, cn, nn, write_deltas);
+        default: return launch_gram_lut<7>(ctx, cn, nn, write_deltas);
+    }
+}
+
+template <int R>
+int launch_decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, uint8_t* log) {
+    const uint32_t M = (ctx->L / 8) * (ctx->L / 8);
+    KSTART(BN_K_DECIDE);
+    k_decide<R><<<(M + 3) / 4, 128, 0, ctx->stream>>>(s, t, seed, ctx->L, mode, ctx->d0.p, ctx->d1b.p, ctx->acc.p,
+                                                      ctx->dEp.p, log);
+    LAUNCHED_K();
+    return BN_OK;
+}
+int decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, uint8_t* log) {
+    switch (ctx->R) {
+        case 1: return launch_decide<1>(ctx, s, t, seed, mode, log);
+        case 2: return launch_decide<2>(ctx, s, t, seed, mode, log);
+        case 3: return launch_decide<3>(ctx, s, t, seed, mode, log);
+        case 4: return launch_decide<4>(ctx, s, t, seed, mode, log);
+        case 5: return launch_decide<5>(ctx, s, t, seed, mode, log);
+        case 6: return launch_decide<6>(ctx, s, t, seed, mode, log);
+        default: return launch_decide<7>(ctx, s, t, seed, mode, log);
+    }
+}
+
+int read_err_flag(bn_ctx* ctx) {
+    int h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, ctx->derr.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (h) return fail(ctx, BN_ESTATE, "internal invariant failed: window distance outside [0, T N^2]");
+    return BN_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C-ABI
+extern "C" {
+
+#define BN_STR2(x) #x
+#define BN_STR(x) BN_STR2(x)
+const char* bn_version(void) {
+    return "bn-b200 0.1 (sm_100a, CUDA " BN_STR(__CUDACC_VER_MAJOR__) "." BN_STR(__CUDACC_VER_MINOR__) ")";
+}
+
+int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
+    if (!out) return BN_EINVAL;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) return BN_ECUDA;
+    bn_ctx* ctx = new bn_ctx();
+    ctx->dev = cuda_device;
+    ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    *out = ctx;
+    return BN_OK;
+}
+
+void bn_destroy(bn_ctx* ctx) {
+    if (!ctx) return;
+    {
+        DeviceGuard g(ctx->dev);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->comm && g_nccl.destroy) g_nccl.destroy(ctx->comm);
+        ctx->S.release(); ctx->U.release(); ctx->Un.release(); ctx->pxy.release(); ctx->ab.release();
+        ctx->Cc.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
+        ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->Dt.release();
+        ctx->d0.release(); ctx->d1b.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release();
+        ctx->W.release(); ctx->G.release(); ctx->iref.release();
+        for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    }
+    delete ctx;
+}
+
+const char* bn_last_error(const bn_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+uint64_t bn_launch_count(const bn_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int bn_set_lattice(bn_ctx* ctx, uint32_t d1, uint32_t d2, const uint32_t* spp_levels, uint32_t n_levels) {
+    if (!ctx) return BN_EINVAL;
+    if (!spp_levels || n_levels < 1 || n_levels > 8) return fail(ctx, BN_EINVAL, "n_levels must be in [1, 8]");
+    for (uint32_t l = 0; l < n_levels; ++l) {
+        if (!pow2(spp_levels[l]) || spp_levels[l] > 128)
+            return fail(ctx, BN_EINVAL, "spp level %u = %u is not a power of two in [1, 128]", l, spp_levels[l]);
+        if (l && spp_levels[l] <= spp_levels[l - 1]) return fail(ctx, BN_EINVAL, "spp levels must ascend");
+    }
+    DeviceGuard g(ctx->dev);
+    const uint32_t Nmax = spp_levels[n_levels - 1];
+    std::vector<uint2> S(Nmax);
+    for (uint32_t k = 0; k < Nmax; ++k) {
+        // s^k = mod(Phi(k) d, 1): Phi(k) as the bit-reversed 32-bit numerator, product mod 2^32
+        uint32_t r = 0;
+        for (int bit = 0; bit < 32; ++bit) r = (r << 1) | ((k >> bit) & 1u);
+        S[k] = make_uint2(r * d1, r * d2);
+    }
+    CUDA_TRY(ctx->S.ensure(Nmax));
+    CUDA_TRY(cudaMemcpyAsync(ctx->S.p, S.data(), Nmax * sizeof(uint2), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->d1 = d1;
+    ctx->d2 = d2;
+    ctx->nl = n_levels;
+    for (uint32_t l = 0; l < 8; ++l) ctx->levels[l] = l < n_levels ? spp_levels[l] : 0;
+    ctx->have_lattice = true;
+    ctx->counts_dirty = true;
+    ctx->lut_dirty = true;
+    return BN_OK;
+}
+
+int bn_set_bank(bn_ctx* ctx, uint32_t T, const int32_t* a, const int32_t* b, const uint32_t* px,
+                const uint32_t* py, uint32_t t_begin, uint32_t t_end) {
+    if (!ctx) return BN_EINVAL;
+    if (T == 0 || !a || !b || !px || !py) return fail(ctx, BN_EINVAL, "empty bank");
+    if (t_begin >= t_end || t_end > T) return fail(ctx, BN_EINVAL, "bad shard [%u, %u) of T = %u", t_begin, t_end, T);
+    for (uint32_t i = 0; i < T; ++i)
+        if (a[i] < -32768 || a[i] > 32768 || b[i] < -32768 || b[i] > 32768)
+            return fail(ctx, BN_EINVAL, "integrand %u normal (%d, %d) exceeds 2^15", i, a[i], b[i]);
+    DeviceGuard g(ctx->dev);
+    ctx->T = T;
+    ctx->t0 = t_begin;
+    ctx->t1 = t_end;
+    ctx->Ts = t_end - t_begin;
+    ctx->Tp = round_up(ctx->Ts, 128);
+    ctx->a.assign(a, a + T);
+    ctx->b.assign(b, b + T);
+    ctx->px.assign(px, px + T);
+    ctx->py.assign(py, py + T);
+    std::vector<int2> ab(ctx->Tp, make_int2(0, 0));
+    std::vector<long long> C(ctx->Tp, 1);  // padding integrands never count
+    std::vector<uint2> pxy(ctx->Ts);
+    for (uint32_t j = 0; j < ctx->Ts; ++j) {
+        const uint32_t i = t_begin + j;
+        ab[j] = make_int2(a[i], b[i]);
+        C[j] = (long long)a[i] * px[i] + (long long)b[i] * py[i] - ((long long)a[i] + b[i]) * (1ll << 31);
+        pxy[j] = make_uint2(px[i], py[i]);
+    }
+    CUDA_TRY(ctx->ab.ensure(ctx->Tp));
+    CUDA_TRY(ctx->Cc.ensure(ctx->Tp));
+    CUDA_TRY(ctx->pxy.ensure(ctx->Ts));
+    CUDA_TRY(cudaMemcpyAsync(ctx->ab.p, ab.data(), ctx->Tp * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->Cc.p, C.data(), ctx->Tp * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->pxy.p, pxy.data(), ctx->Ts * sizeof(uint2), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    ctx->have_bank = true;
+    ctx->counts_dirty = true;
+    ctx->lut_dirty = true;
+    return BN_OK;
+}
+
+int bn_get_references(bn_ctx* ctx, double* iref) {
+    if (!ctx) return BN_EINVAL;
+    if (!iref) return fail(ctx, BN_EINVAL, "null output");
+    if (!ctx->have_bank) return fail(ctx, BN_ESTATE, "bn_set_bank has not been called");
+    DeviceGuard g(ctx->dev);
+    CUDA_TRY(ctx->iref.ensure(ctx->Ts));
+    k_iref<<<(ctx->Ts + 127) / 128, 128, 0, ctx->stream>>>(ctx->ab.p, ctx->pxy.p, ctx->Ts, ctx->iref.p);
+    LAUNCHED();
+    CUDA_TRY(cudaMemcpyAsync(iref, ctx->iref.p, ctx->Ts * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return BN_OK;
+}
+
+int bn_set_energy(bn_ctx* ctx, double sigma_i, double sigma_s, int32_t radius) {
+    if (!ctx) return BN_EINVAL;
+    if (!(sigma_i > 0) || !(sigma_s > 0) || !std::isfinite(sigma_i) || !std::isfinite(sigma_s))
+        return fail(ctx, BN_EINVAL, "sigmas must be positive and finite");
+    if (radius < 1 || radius > 7) return fail(ctx, BN_EINVAL, "radius %d outside [1, 7]", radius);
+    ctx->sigma_i = sigma_i;
+    ctx->sigma_s = sigma_s;
+    ctx->R = radius;
+    ctx->lut_dirty = true;
+    return BN_OK;
+}
+
+int bn_set_tile(bn_ctx* ctx, uint32_t L, const uint32_t* u_xy, int is_device) {
+    if (!ctx) return BN_EINVAL;
+    if (!u_xy) return fail(ctx, BN_EINVAL, "null tile");
+    if (!pow2(L) || L < 16 || L > 4096) return fail(ctx, BN_EINVAL, "L = %u must be a power of two in [16, 4096]", L);
+    if (!ctx->have_lattice || !ctx->have_bank) return fail(ctx, BN_ESTATE, "set lattice and bank before the tile");
+    DeviceGuard g(ctx->dev);
+    ctx->L = L;
+    ctx->P = L * L;
+    CUDA_TRY(ctx->U.ensure(ctx->P));
+    CUDA_TRY(cudaMemcpyAsync(ctx->U.p, u_xy, (size_t)ctx->P * sizeof(uint2),
+                             is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+    ctx->have_tile = true;
+    ctx->counts_dirty = true;
+    int rc = ensure_counts(ctx);
+    if (rc) return rc;
+    if (!is_device) CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // host buffer may be reused
+    return BN_OK;
+}
+
+int bn_get_tile(bn_ctx* ctx, uint32_t* u_xy, int is_device) {
+    if (!ctx) return BN_EINVAL;
+    if (!u_xy) return fail(ctx, BN_EINVAL, "null output");
+    if (!ctx->have_tile) return fail(ctx, BN_ESTATE, "no tile");
+    DeviceGuard g(ctx->dev);
+    CUDA_TRY(cudaMemcpyAsync(u_xy, ctx->U.p, (size_t)ctx->P * sizeof(uint2),
+                             is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+    if (!is_device) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return BN_OK;
+}
+
+int bn_eval_counts(bn_ctx* ctx, uint8_t* out, int is_device) {
+    if (!ctx) return BN_EINVAL;
+    if (!out) return fail(ctx, BN_EINVAL, "null output");
+    int rc = check_ready(ctx);
+    if (rc) return rc;
+    DeviceGuard g(ctx->dev);
+    if ((rc = ensure_counts(ctx))) return rc;
+    const size_t n = (size_t)ctx->nl * ctx->P * ctx->Ts;
+    uint8_t* dst = out;
+    if (!is_device) {
+        CUDA_TRY(ctx->cexp.ensure(n));
+        dst = ctx->cexp.p;
+    }
+    k_counts_export<<<ctx->nl * ctx->P, 128, 0, ctx->stream>>>(ctx->c.p, ctx->P, ctx->nl, ctx->Tp, ctx->Ts, dst);
+    LAUNCHED();
+    if (!is_device) {
+        CUDA_TRY(cudaMemcpyAsync(out, dst, n, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+    return BN_OK;
+}
+
+int bn_energy(bn_ctx* ctx, double* E, uint64_t E_fixed[2]) {
+    if (!ctx) return BN_EINVAL;
+    DeviceGuard g(ctx->dev);
+    int rc = ensure_work(ctx);
+    if (rc) return rc;
+    CUDA_TRY(ctx->pstats.ensure(1));
+    CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
+    if ((rc = gram_lut(ctx, ctx->c.p, ctx->nc.p, 0))) return rc;
+    const uint32_t nE = (uint32_t)(((size_t)ctx->P * half_count(ctx->R) + 255) / 256);
+    k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, nullptr, nullptr, ctx->P, 0, ctx->pstats.p);
+    LAUNCHED();
+    PassStatsDev h;
+    CUDA_TRY(cudaMemcpyAsync(&h, ctx->pstats.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    if ((rc = read_err_flag(ctx))) return rc;
+    if (E_fixed) {
+        E_fixed[0] = h.E_before[0];
+        E_fixed[1] = h.E_before[1];
+    }
+    if (E) *E = std::ldexp((double)h.E_before[1], 0) + std::ldexp((double)h.E_before[0], -64);
+    return BN_OK;
+}
+
+int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uint8_t* accept_log) {
+    if (!ctx) return BN_EINVAL;
+    if (!prm) return fail(ctx, BN_EINVAL, "null params");
+    if (prm->mode > BN_SWAP) return fail(ctx, BN_EINVAL, "unknown mode %u", prm->mode);
+    if (prm->K != 1) return fail(ctx, BN_EINVAL, "K = %u: only K = 1 is implemented", prm->K);
+    DeviceGuard g(ctx->dev);
+    int rc = ensure_work(ctx);
+    if (rc) return rc;
+    if (prm->passes == 0) return BN_OK;
+    const uint32_t P = ctx->P, M = (ctx->L / 8) * (ctx->L / 8), nl = ctx->nl;
+    const int R = ctx->R;
+    const uint32_t nE = (uint32_t)(((size_t)P * half_count(R) + 255) / 256);
+    CUDA_TRY(ctx->pstats.ensure(prm->passes));
+    if (accept_log) CUDA_TRY(ctx->log.ensure((size_t)prm->passes * 64 * M));
+    CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
+    const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
+    const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
+    for (uint32_t pi = 0; pi < prm->passes; ++pi) {
+        const uint32_t t = prm->first_pass + pi;
+        CUDA_TRY(cudaMemsetAsync(ctx->acc.p, 0, P, ctx->stream));
+        if (prm->mode == BN_REDRAW) {
+            KSTART(BN_K_COUNTS);
+            k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->stream>>>(
+                nullptr, ctx->Un.p, 1, prm->seed, t, P, ctx->ab.p, ctx->Cc.p, ctx->Tp, ctx->S.p,
+                ctx->levels[nl - 1], lo, hi, nl, ctx->cn.p, ctx->nn.p);
+            LAUNCHED_K();
+        } else {
+            KSTART(BN_K_GATHER);
+            k_swap_gather<<<64 * M, 128, 0, ctx->stream>>>(ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p, ctx->nc.p,
+                                                          ctx->nn.p, ctx->L, prm->seed, t, ctx->rowB, nl);
+            LAUNCHED_K();
+        }
+        if ((rc = gram_lut(ctx, ctx->cn.p, ctx->nn.p, 1))) return rc;
+        uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
+        for (uint32_t s = 0; s < 64; ++s)
+            if ((rc = decide(ctx, s, t, prm->seed, (int)prm->mode, log))) return rc;
+        KSTART(BN_K_STATS);
+        k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, ctx->dEp.p, ctx->acc.p, P,
+                                                  prm->mode == BN_SWAP, ctx->pstats.p + pi);
+        LAUNCHED_K();
+        KSTART(BN_K_COMMIT);
+        k_commit<<<P, 128, 0, ctx->stream>>>(ctx->acc.p, P, ctx->rowB, nl, ctx->Un.p, ctx->U.p, ctx->cn.p, ctx->c.p,
+                                             ctx->nn.p, ctx->nc.p);
+        LAUNCHED_K();
+    }
+    if (stats || accept_log) {
+        std::vector<PassStatsDev> h(prm->passes);
+        CUDA_TRY(cudaMemcpyAsync(h.data(), ctx->pstats.p, prm->passes * sizeof(PassStatsDev), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        if (accept_log)
+            CUDA_TRY(cudaMemcpyAsync(accept_log, ctx->log.p, (size_t)prm->passes * 64 * M, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+        if ((rc = read_err_flag(ctx))) return rc;
+        for (uint32_t pi = 0; pi < prm->passes; ++pi) {
+            if (pi && (h[pi].E_before[0] != h[pi - 1].E_after[0] || h[pi].E_before[1] != h[pi - 1].E_after[1]))
+                return fail(ctx, BN_ESTATE, "internal invariant failed: E recomputed at pass %u != E + sum dE",
+                            prm->first_pass + pi);
+            if (stats) {
+                stats[pi].accepted = h[pi].accepted;
+                stats[pi].proposed = prm->mode == BN_SWAP ? P / 2 : P;
+                stats[pi].E_fixed[0] = h[pi].E_after[0];
+                stats[pi].E_fixed[1] = h[pi].E_after[1];
+                stats[pi].E = std::ldexp((double)h[pi].E_after[1], 0) + std::ldexp((double)h[pi].E_after[0], -64);
+                stats[pi].dE_sum[0] = h[pi].dE_sum[0];
+                stats[pi].dE_sum[1] = h[pi].dE_sum[1];
+            }
+        }
+    }
+    return BN_OK;
+}
+
+int bn_profile_enable(bn_ctx* ctx, int enable) {
+    if (!ctx) return BN_EINVAL;
+    DeviceGuard g(ctx->dev);
+    flush_profile(ctx);
+    if (enable)
+        for (int i = 0; i < BN_K_COUNT_IDS; ++i) ctx->prof_ms[i] = 0.0, ctx->prof_n[i] = 0;
+    ctx->prof = enable != 0;
+    return BN_OK;
+}
+
+int bn_profile_get(bn_ctx* ctx, uint32_t kernel_id, double* total_ms, uint64_t* launches) {
+    if (!ctx) return BN_EINVAL;
+    if (kernel_id >= BN_K_COUNT_IDS) return fail(ctx, BN_EINVAL, "kernel id %u", kernel_id);
+    DeviceGuard g(ctx->dev);
+    flush_profile(ctx);
+    if (total_ms) *total_ms = ctx->prof_ms[kernel_id];
+    if (launches) *launches = ctx->prof_n[kernel_id];
+    return BN_OK;
+}
+
+int bn_comm_unique_id(void* out128) {
+    if (!out128) return BN_EINVAL;
+    if (!g_nccl.load()) return BN_ENCCL;
+    NcclUid id;
+    if (g_nccl.get_uid(&id)) return BN_ENCCL;
+    memcpy(out128, &id, sizeof id);
+    return BN_OK;
+}
+
+int bn_comm_init(bn_ctx* ctx, const void* uid, int rank, int world) {
+    if (!ctx) return BN_EINVAL;
+    if (!uid || world < 1 || rank < 0 || rank >= world) return fail(ctx, BN_EINVAL, "bad rank/world");
+    if (!g_nccl.load()) return fail(ctx, BN_ENCCL, "libnccl.so.2 not loadable: %s", dlerror());
+    DeviceGuard g(ctx->dev);
+    NcclUid id;
+    memcpy(&id, uid, sizeof id);
+    NcclComm comm = nullptr;
+    int r = g_nccl.init_rank(&comm, world, id, rank);
+    if (r) return fail(ctx, BN_ENCCL, "ncclCommInitRank: %s", g_nccl.errstr(r));
+    if (ctx->comm) g_nccl.destroy(ctx->comm);
+    ctx->comm = comm;
+    ctx->rank = rank;
+    ctx->world = world;
+    return BN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,487 @@
+// bn_kernels.cuh -- sm_100a kernels of the blue-noise sampler optimiser hot path.
+//
+// Pass structure.  Within a pass every pixel p receives exactly ONE candidate
+// row cn_p (REDRAW: counts of a Philox-drawn shift; SWAP: the partner's row), and the 64 colour
+// classes are visited in order.  Hence, at any moment of the pass, pixel q is in one of two
+// states, c_q (not yet accepted) or cn_q (accepted earlier in this pass), and every energy
+// change the pass can need is a function of the four window distances
+//     D(c_p,c_q), D(cn_p,c_q), D(c_p,cn_q), D(cn_p,cn_q)          (q = p + o, o in the window).
+// The pass therefore runs as
+//   k_counts / k_swap_gather : candidate rows cn (+ norms)                      [ALU]
+//   k_gram                   : the four windowed distances for every (p, o in H)  [dominant]
+//   k_lut                    : per (p, o): delta0 = q(D(cn_p,c_q)) - q(D(c_p,c_q)),
+//                              delta1 = q(D(cn_p,cn_q)) - q(D(c_p,cn_q)) (int128, summed over
+//                              levels), and E of the pass-start state
+//   k_decide (x64 classes)   : dE_p = 2 * sum_o (accepted[q] ? delta1 : delta0); accept iff < 0
+//   k_commit, k_pass_stats   : copy accepted rows / shifts; exact per-pass sums
+// which is bit-identical to the step-by-step greedy algorithm (oracle) because distances are
+// exact integers and the fixed-point energy terms are summed exactly in int128.
+//
+// H = half window {o : oy > 0 or (oy == 0 and ox > 0)}: each unordered neighbour pair is
+// computed once and written to both (p, o) and (p + o, -o).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bn {
+
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+// ------------------------------------------------------------------------------ Philox4x32-10
+// Salmon et al. SC'11.  Written independently of the oracle; parity checked via accept logs.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k.x += 0x9E3779B9u;
+            k.y += 0xBB67AE85u;
+        }
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    return c;
+}
+__device__ __forceinline__ uint4 philox_seeded(uint64_t seed, uint32_t c0, uint32_t c1, uint32_t c2,
+                                               uint32_t c3) {
+    return philox4x32_10(make_uint4(c0, c1, c2, c3), make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+}
+
+// Pixel of active index m in colour class s = 8r + k of pass t (stride-8 staggered schedule).
+__device__ __forceinline__ uint32_t class_pixel(uint32_t L, uint64_t seed, uint32_t t, uint32_t s, uint32_t m) {
+    const uint32_t nb = L >> 3, b = m / nb, a = m - b * nb, r = s >> 3, k = s & 7;
+    const uint32_t delta = philox_seeded(seed, b, t, r, 2).x;
+    const uint32_t along = 8 * a + ((delta + k) & 7), across = 8 * b + r;
+    return (t & 1) ? along * L + across : across * L + along;
+}
+__device__ __forceinline__ uint32_t swap_kappa(uint64_t seed, uint32_t t, uint32_t s, uint32_t M) {
+    return 1u + philox_seeded(seed, s, t, 0, 3).x % (M - 1u);
+}
+
+// Window indexing.  Full window W: raster over (oy, ox) in [-R,R]^2 minus the centre.
+__host__ __device__ __forceinline__ int win_index(int ox, int oy, int R) {
+    const int w = (oy + R) * (2 * R + 1) + (ox + R), centre = R * (2 * R + 1) + R;
+    return w > centre ? w - 1 : w;
+}
+// Half window H: oy = 0, ox = 1..R first, then oy = 1..R, ox = -R..R.
+__host__ __device__ __forceinline__ int half_index(int ox, int oy, int R) {
+    return oy == 0 ? ox - 1 : R + (oy - 1) * (2 * R + 1) + (ox + R);
+}
+
+// ---------------------------------------------------------------------------- error vectors
+// Heaviside counts for every pixel of a tile (set_tile) or for the REDRAW candidates of pass t.
+//   c_l,p,i = #{k < N_l : a_i (X_k - PX_i) + b_i (Y_k - PY_i) >= 0},  X_k = S_k.x + u_p.x mod 2^32.
+// With X' = X - 2^31 as int32, the test is a_i X' + b_i Y' >= C_i,  C_i = a PX + b PY - (a+b) 2^31,
+// i.e. two 32x32->64 integer multiply-adds per (pixel, integrand, sample): exact.
+// Padding integrands (i >= Ts) use a = b = 0, C = 1, so they always count 0.
+// Layout out: [p][l][Tp] uint8; norms: [p][l] int32 = sum_i c^2.
+constexpr int COUNT_PIX = 8;  // pixels per CTA
+
+__global__ void __launch_bounds__(256) k_counts(const uint2* __restrict__ U, uint2* __restrict__ Uout, int redraw,
+                                                uint64_t seed, uint32_t pass_t, uint32_t P,
+                                                const int2* __restrict__ ab, const long long* __restrict__ Cc,
+                                                uint32_t Tp, const uint2* __restrict__ S, uint32_t Nmax,
+                                                uint4 lev_lo, uint4 lev_hi, uint32_t nl, uint8_t* __restrict__ out,
+                                                int* __restrict__ norms) {
+    __shared__ int2 sXY[COUNT_PIX][128];
+    __shared__ int sNorm[COUNT_PIX][8];
+    const uint32_t levels[8] = {lev_lo.x, lev_lo.y, lev_lo.z, lev_lo.w, lev_hi.x, lev_hi.y, lev_hi.z, lev_hi.w};
+    const uint32_t p0 = blockIdx.x * COUNT_PIX;
+    for (uint32_t j = threadIdx.x; j < COUNT_PIX * 8; j += blockDim.x) (&sNorm[0][0])[j] = 0;
+    for (uint32_t j = threadIdx.x; j < COUNT_PIX * Nmax; j += blockDim.x) {
+        const uint32_t pp = j / Nmax, k = j - pp * Nmax, p = p0 + pp;
+        if (p >= P) continue;
+        uint2 u;
+        if (redraw) {
+            const uint4 r = philox_seeded(seed, p, pass_t, 0, 1);
+            u = make_uint2(r.x, r.y);
+            if (k == 0) Uout[p] = u;
+        } else {
+            u = U[p];
+        }
+        const uint2 s = S[k];
+        sXY[pp][k] = make_int2((int)((s.x + u.x) ^ 0x80000000u), (int)((s.y + u.y) ^ 0x80000000u));
+    }
+    __syncthreads();
+    for (uint32_t q4 = threadIdx.x; q4 < Tp / 4; q4 += blockDim.x) {
+        int2 abv[4];
+        long long cv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            abv[j] = ab[4 * q4 + j];
+            cv[j] = Cc[4 * q4 + j];
+        }
+        for (int pp = 0; pp < COUNT_PIX; ++pp) {
+            const uint32_t p = p0 + pp;
+            if (p >= P) break;
+            uint32_t cnt[4] = {0, 0, 0, 0};
+            uint32_t li = 0, nsq = 0;
+            uint32_t next = levels[0];
+            for (uint32_t k = 0; k < Nmax; ++k) {
+                const int2 xy = sXY[pp][k];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const long long v = (long long)abv[j].x * xy.x + (long long)abv[j].y * xy.y - cv[j];
+                    cnt[j] += (v >= 0);
+                }
+                if (k + 1 == next) {
+                    const uint32_t packed = cnt[0] | (cnt[1] << 8) | (cnt[2] << 16) | (cnt[3] << 24);
+                    *reinterpret_cast<uint32_t*>(out + ((size_t)p * nl + li) * Tp + 4 * q4) = packed;
+                    nsq = cnt[0] * cnt[0] + cnt[1] * cnt[1] + cnt[2] * cnt[2] + cnt[3] * cnt[3];
+#pragma unroll
+                    for (int off = 16; off; off >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, off);
+                    if ((threadIdx.x & 31) == 0) atomicAdd(&sNorm[pp][li], (int)nsq);
+                    ++li;
+                    next = li < nl ? levels[li] : 0xffffffffu;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < COUNT_PIX * nl; j += blockDim.x) {
+        const uint32_t pp = j / nl, l = j - pp * nl;
+        if (p0 + pp < P) norms[(size_t)(p0 + pp) * nl + l] = sNorm[pp][l];
+    }
+}
+// NOTE: the warp-level shuffle in k_counts requires every lane of a warp to reach it together:
+// the q4 loop bound Tp/4 is a multiple of 8 lanes... callers guarantee Tp % 128 == 0.
+
+// SWAP candidates: cn_p = c_partner(p), Un_p = U_partner(p), for every (class s, index m).
+__global__ void k_swap_gather(const uint2* __restrict__ U, uint2* __restrict__ Un, const uint8_t* __restrict__ c,
+                              uint8_t* __restrict__ cn, const int* __restrict__ nc, int* __restrict__ nn,
+                              uint32_t L, uint64_t seed, uint32_t pass_t, uint32_t rowB, uint32_t nl) {
+    const uint32_t M = (L / 8) * (L / 8);
+    const uint32_t sm = blockIdx.x;  // s * M + m
+    const uint32_t s = sm / M, m = sm - s * M;
+    const uint32_t kappa = swap_kappa(seed, pass_t, s, M);
+    const uint32_t p = class_pixel(L, seed, pass_t, s, m), p2 = class_pixel(L, seed, pass_t, s, m ^ kappa);
+    const uint4* src = reinterpret_cast<const uint4*>(c + (size_t)p2 * rowB);
+    uint4* dst = reinterpret_cast<uint4*>(cn + (size_t)p * rowB);
+    for (uint32_t j = threadIdx.x; j < rowB / 16; j += blockDim.x) dst[j] = src[j];
+    if (threadIdx.x == 0) Un[p] = U[p2];
+    if (threadIdx.x < nl) nn[(size_t)p * nl + threadIdx.x] = nc[(size_t)p2 * nl + threadIdx.x];
+}
+
+// --------------------------------------------------------------------------- window distances
+// One CTA = a strip of SW <= 32 pixels of one row y; warp w handles window row oy = w (0..R),
+// lane = pixel.  Per K-chunk the CTA stages, for every oy, the neighbour strip
+// (row y+oy, columns x0-R .. x0+SW+R-1) of both c and cn in shared memory (row stride KCW+1
+// words: conflict-free), and every thread accumulates 4 dp4a dot products per offset ox:
+//   <c_p,c_q>, <cn_p,c_q>, <c_p,cn_q>, <cn_p,cn_q>.
+// D = |x|^2 + |y|^2 - 2<x,y> from the per-row norms.  Output Dt[(p*H + h)*nl + l] =
+// int4(D(c,c), D(cn,c), D(c,cn), D(cn,cn)) for h in the half window.
+constexpr int GRAM_KC = 32;               // bytes of K per stage
+constexpr int GRAM_KCW = GRAM_KC / 4;     // words
+constexpr int GRAM_STRIDE = GRAM_KCW + 1; // padded row stride (words)
+
+template <int R>
+__global__ void __launch_bounds__(32 * (R + 1)) k_gram(const uint8_t* __restrict__ c, const uint8_t* __restrict__ cn,
+                                                        const int* __restrict__ nc, const int* __restrict__ nn,
+                                                        uint32_t L, uint32_t SW, uint32_t Tp, uint32_t nl,
+                                                        int4* __restrict__ Dt) {
+    constexpr int NCOL_MAX = 32 + 2 * R;
+    constexpr int H = 2 * R * R + 2 * R;
+    __shared__ uint32_t sC[(R + 1) * NCOL_MAX * GRAM_STRIDE];
+    __shared__ uint32_t sN[(R + 1) * NCOL_MAX * GRAM_STRIDE];
+    const uint32_t ncol = SW + 2 * R;
+    const uint32_t x0 = blockIdx.x * SW, y = blockIdx.y;
+    const int oy = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rowB = nl * Tp;
+    const uint32_t nload = (R + 1) * ncol * GRAM_KCW;
+    for (uint32_t l = 0; l < nl; ++l) {
+        uint32_t acc[2 * R + 1][4];
+#pragma unroll
+        for (int i = 0; i < 2 * R + 1; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0;
+        for (uint32_t k0 = 0; k0 < Tp; k0 += GRAM_KC) {
+            for (uint32_t j = threadIdx.x; j < nload; j += blockDim.x) {
+                const uint32_t w = j % GRAM_KCW, rc = j / GRAM_KCW;  // rc = ry * ncol + col
+                const uint32_t ry = rc / ncol, col = rc - ry * ncol;
+                const uint32_t qy = (y + ry) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
+                const size_t off = (size_t)(qy * L + qx) * rowB + l * Tp + k0 + 4 * w;
+                sC[rc * GRAM_STRIDE + w] = __ldg(reinterpret_cast<const uint32_t*>(c + off));
+                sN[rc * GRAM_STRIDE + w] = __ldg(reinterpret_cast<const uint32_t*>(cn + off));
+            }
+            __syncthreads();
+            if (lane < (int)SW) {
+                const uint32_t* ownC = sC + (R + lane) * GRAM_STRIDE;
+                const uint32_t* ownN = sN + (R + lane) * GRAM_STRIDE;
+                const uint32_t* nbC = sC + (oy * ncol + lane) * GRAM_STRIDE;
+                const uint32_t* nbN = sN + (oy * ncol + lane) * GRAM_STRIDE;
+#pragma unroll
+                for (int w = 0; w < GRAM_KCW; ++w) {
+                    const uint32_t oc = ownC[w], on = ownN[w];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) {
+                        const uint32_t qc = nbC[i * GRAM_STRIDE + w], qn = nbN[i * GRAM_STRIDE + w];
+                        acc[i][0] = __dp4a(oc, qc, acc[i][0]);
+                        acc[i][1] = __dp4a(on, qc, acc[i][1]);
+                        acc[i][2] = __dp4a(oc, qn, acc[i][2]);
+                        acc[i][3] = __dp4a(on, qn, acc[i][3]);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (lane < (int)SW) {
+            const uint32_t x = x0 + lane, p = y * L + x;
+            const int ncp = nc[(size_t)p * nl + l], nnp = nn[(size_t)p * nl + l];
+#pragma unroll
+            for (int i = 0; i < 2 * R + 1; ++i) {
+                const int ox = i - R;
+                if (oy == 0 && ox <= 0) continue;
+                const uint32_t q = ((y + oy) & (L - 1)) * L + ((x + ox + L) & (L - 1));
+                const int ncq = nc[(size_t)q * nl + l], nnq = nn[(size_t)q * nl + l];
+                int4 d;
+                d.x = ncp + ncq - 2 * (int)acc[i][0];
+                d.y = nnp + ncq - 2 * (int)acc[i][1];
+                d.z = ncp + nnq - 2 * (int)acc[i][2];
+                d.w = nnp + nnq - 2 * (int)acc[i][3];
+                Dt[((size_t)p * H + half_index(ox, oy, R)) * nl + l] = d;
+            }
+        }
+    }
+}
+
+// -------------------------------------------------------------------------- energy terms
+// q(o, D) = rn_u64(2^64 * W[o] * G_l[D]); W and G are host-built fp64 tables (exp/sqrt of the
+// host libm), the product is one IEEE multiply (no contraction possible), the scaling by 2^64
+// is exact.
+__device__ __forceinline__ unsigned long long qterm(double w, const double* __restrict__ G, int D) {
+    return __double2ull_rn(__dmul_rn(__dmul_rn(w, __ldg(G + D)), 18446744073709551616.0));
+}
+
+struct LutArgs {
+    const double* G[8];  // per-level G tables
+    int Dmax[8];         // largest legal D per level (guards corrupted distances)
+};
+
+template <int R>
+__global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32_t L, uint32_t nl,
+                                             const double* __restrict__ W, LutArgs lut, int write_deltas,
+                                             longlong2* __restrict__ d0, longlong2* __restrict__ d1,
+                                             u128* __restrict__ Epart, int* __restrict__ err) {
+    constexpr int H = 2 * R * R + 2 * R;
+    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
+    const uint32_t P = L * L;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    u128 e = 0;
+    if (idx < (size_t)P * H) {
+        const uint32_t p = (uint32_t)(idx / H), h = (uint32_t)(idx - (size_t)p * H);
+        int ox, oy;
+        if (h < (uint32_t)R) {
+            oy = 0;
+            ox = (int)h + 1;
+        } else {
+            oy = 1 + (int)(h - R) / (2 * R + 1);
+            ox = (int)(h - R) % (2 * R + 1) - R;
+        }
+        const uint32_t x = p % L, y = p / L;
+        const uint32_t q = ((y + oy) & (L - 1)) * L + ((x + ox + L) & (L - 1));
+        const int wi = win_index(ox, oy, R), wm = win_index(-ox, -oy, R);
+        const double w = W[wi];
+        i128 a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+        for (uint32_t l = 0; l < nl; ++l) {
+            const int4 D = Dt[idx * nl + l];
+            const int dm = lut.Dmax[l];
+            if ((unsigned)D.x > (unsigned)dm || (unsigned)D.y > (unsigned)dm || (unsigned)D.z > (unsigned)dm ||
+                (unsigned)D.w > (unsigned)dm) {
+                atomicOr(err, 1);
+                continue;
+            }
+            const double* G = lut.G[l];
+            const unsigned long long qcc = qterm(w, G, D.x), qnc = qterm(w, G, D.y);
+            const unsigned long long qcn = qterm(w, G, D.z), qnn = qterm(w, G, D.w);
+            e += (u128)qcc;
+            a0 += (i128)qnc - (i128)qcc;  // p takes cn_p, q still c_q
+            a1 += (i128)qnn - (i128)qcn;  // p takes cn_p, q already cn_q
+            b0 += (i128)qcn - (i128)qcc;  // q takes cn_q, p still c_p
+            b1 += (i128)qnn - (i128)qnc;  // q takes cn_q, p already cn_p
+        }
+        e *= 2;  // ordered pairs (p,q) and (q,p)
+        if (write_deltas) {
+            d0[(size_t)p * WN + wi] = make_longlong2((long long)(unsigned long long)a0, (long long)(a0 >> 64));
+            d1[(size_t)p * WN + wi] = make_longlong2((long long)(unsigned long long)a1, (long long)(a1 >> 64));
+            d0[(size_t)q * WN + wm] = make_longlong2((long long)(unsigned long long)b0, (long long)(b0 >> 64));
+            d1[(size_t)q * WN + wm] = make_longlong2((long long)(unsigned long long)b1, (long long)(b1 >> 64));
+        }
+    }
+    // block reduction of e (u128) through shared memory
+    __shared__ unsigned long long slo[256], shi[256];
+    slo[threadIdx.x] = (unsigned long long)e;
+    shi[threadIdx.x] = (unsigned long long)(e >> 64);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u128 s = 0;
+        for (int j = 0; j < (int)blockDim.x; ++j) s += ((u128)shi[j] << 64) | slo[j];
+        Epart[blockIdx.x] = s;
+    }
+}
+
+// ----------------------------------------------------------------------------- decisions
+// Colour class s of pass t: one warp per active index m (SWAP: the lower index of a couple).
+// dE_p = 2 * sum_{o in W} (acc[p+o] ? d1 : d0)[p][o]; accept iff dE < 0.
+template <int R>
+__device__ __forceinline__ i128 window_sum(const longlong2* __restrict__ d0, const longlong2* __restrict__ d1,
+                                           const uint8_t* __restrict__ acc, uint32_t L, uint32_t p) {
+    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
+    const int lane = threadIdx.x & 31;
+    const uint32_t x = p % L, y = p / L;
+    i128 s = 0;
+    for (int w = lane; w < WN; w += 32) {
+        const int ww = w >= R * (2 * R + 1) + R ? w + 1 : w;
+        const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
+        const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
+        const longlong2 v = acc[q] ? d1[(size_t)p * WN + w] : d0[(size_t)p * WN + w];
+        s += ((i128)v.y << 64) | (u128)(unsigned long long)v.x;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)s, off);
+        const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(s >> 64), off);
+        s += ((i128)hi << 64) | (u128)lo;
+    }
+    return s;
+}
+
+template <int R>
+__global__ void k_decide(uint32_t s, uint32_t pass_t, uint64_t seed, uint32_t L, int mode,
+                         const longlong2* __restrict__ d0, const longlong2* __restrict__ d1, uint8_t* __restrict__ acc,
+                         i128* __restrict__ dEp, uint8_t* __restrict__ log) {
+    const uint32_t M = (L / 8) * (L / 8);
+    const uint32_t m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (m >= M) return;
+    const uint32_t p = class_pixel(L, seed, pass_t, s, m);
+    if (mode == 0) {
+        const i128 dE = 2 * window_sum<R>(d0, d1, acc, L, p);
+        if ((threadIdx.x & 31) == 0) {
+            const bool ok = dE < 0;
+            acc[p] = ok;
+            dEp[p] = ok ? dE : (i128)0;
+            if (log) log[(size_t)s * M + m] = ok;
+        }
+    } else {
+        const uint32_t mm = m ^ swap_kappa(seed, pass_t, s, M);
+        if (mm < m) return;
+        const uint32_t p2 = class_pixel(L, seed, pass_t, s, mm);
+        const i128 dE = 2 * (window_sum<R>(d0, d1, acc, L, p) + window_sum<R>(d0, d1, acc, L, p2));
+        if ((threadIdx.x & 31) == 0) {
+            const bool ok = dE < 0;
+            acc[p] = ok;
+            acc[p2] = ok;
+            dEp[p] = ok ? dE : (i128)0;
+            dEp[p2] = 0;
+            if (log) {
+                log[(size_t)s * M + m] = ok;
+                log[(size_t)s * M + mm] = ok;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------- commit
+__global__ void k_commit(const uint8_t* __restrict__ acc, uint32_t P, uint32_t rowB, uint32_t nl,
+                         const uint2* __restrict__ Un, uint2* __restrict__ U, const uint8_t* __restrict__ cn,
+                         uint8_t* __restrict__ c, const int* __restrict__ nn, int* __restrict__ nc) {
+    const uint32_t p = blockIdx.x;
+    if (!acc[p]) return;
+    const uint4* src = reinterpret_cast<const uint4*>(cn + (size_t)p * rowB);
+    uint4* dst = reinterpret_cast<uint4*>(c + (size_t)p * rowB);
+    for (uint32_t j = threadIdx.x; j < rowB / 16; j += blockDim.x) dst[j] = src[j];
+    if (threadIdx.x == 0) U[p] = Un[p];
+    if (threadIdx.x < nl) nc[(size_t)p * nl + threadIdx.x] = nn[(size_t)p * nl + threadIdx.x];
+}
+
+struct PassStatsDev {
+    unsigned long long E_before[2];
+    unsigned long long E_after[2];
+    unsigned long long dE_sum[2];
+    unsigned int accepted, pad;
+};
+
+// Single-CTA exact reductions: E_before = sum Epart, dE_sum = sum dEp, accepted = sum acc.
+__global__ void __launch_bounds__(1024) k_pass_stats(const u128* __restrict__ Epart, uint32_t nEpart,
+                                                     const i128* __restrict__ dEp, const uint8_t* __restrict__ acc,
+                                                     uint32_t P, int swap_mode, PassStatsDev* __restrict__ out) {
+    __shared__ unsigned long long s_e[1024][2], s_d[1024][2];
+    __shared__ unsigned int s_a[1024];
+    u128 e = 0;
+    i128 d = 0;
+    unsigned a = 0;
+    for (uint32_t j = threadIdx.x; j < nEpart; j += blockDim.x) e += Epart[j];
+    if (dEp)
+        for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) {
+            d += dEp[j];
+            a += acc[j];
+        }
+    s_e[threadIdx.x][0] = (unsigned long long)e;
+    s_e[threadIdx.x][1] = (unsigned long long)(e >> 64);
+    s_d[threadIdx.x][0] = (unsigned long long)(u128)d;
+    s_d[threadIdx.x][1] = (unsigned long long)((u128)d >> 64);
+    s_a[threadIdx.x] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u128 E = 0, D = 0;
+        unsigned A = 0;
+        for (int j = 0; j < (int)blockDim.x; ++j) {
+            E += ((u128)s_e[j][1] << 64) | s_e[j][0];
+            D += ((u128)s_d[j][1] << 64) | s_d[j][0];
+            A += s_a[j];
+        }
+        const u128 Ea = E + D;  // two's complement: E + dE_sum
+        out->E_before[0] = (unsigned long long)E;
+        out->E_before[1] = (unsigned long long)(E >> 64);
+        out->E_after[0] = (unsigned long long)Ea;
+        out->E_after[1] = (unsigned long long)(Ea >> 64);
+        out->dE_sum[0] = (unsigned long long)D;
+        out->dE_sum[1] = (unsigned long long)(D >> 64);
+        out->accepted = swap_mode ? A / 2 : A;
+    }
+}
+
+// --------------------------------------------------------------------------- I_ref, readback
+// Area of {(x,y) in [0,1]^2 : a(x - px) + b(y - py) >= 0}: the unit square clipped by the
+// half-plane (walk the 4 edges, keep inside vertices and edge crossings), shoelace area. fp64.
+__global__ void k_iref(const int2* __restrict__ ab, const uint2* __restrict__ pxy, uint32_t n, double* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double a = ab[i].x, b = ab[i].y;
+    const double px = pxy[i].x * 0x1p-32, py = pxy[i].y * 0x1p-32;
+    const double vx[4] = {0.0, 1.0, 1.0, 0.0}, vy[4] = {0.0, 0.0, 1.0, 1.0};
+    double fx[8], fy[8];
+    int n_out = 0;
+    for (int e = 0; e < 4; ++e) {
+        const int f = (e + 1) & 3;
+        const double s0 = __dadd_rn(__dmul_rn(a, vx[e] - px), __dmul_rn(b, vy[e] - py));
+        const double s1 = __dadd_rn(__dmul_rn(a, vx[f] - px), __dmul_rn(b, vy[f] - py));
+        if (s0 >= 0) {
+            fx[n_out] = vx[e];
+            fy[n_out] = vy[e];
+            ++n_out;
+        }
+        if ((s0 >= 0) != (s1 >= 0)) {
+            const double t = s0 / (s0 - s1);
+            fx[n_out] = __dadd_rn(vx[e], __dmul_rn(t, vx[f] - vx[e]));
+            fy[n_out] = __dadd_rn(vy[e], __dmul_rn(t, vy[f] - vy[e]));
+            ++n_out;
+        }
+    }
+    double twice = 0.0;
+    for (int j = 0; j < n_out; ++j) {
+        const int k = (j + 1) % n_out;
+        twice = __dadd_rn(twice, __dsub_rn(__dmul_rn(fx[j], fy[k]), __dmul_rn(fx[k], fy[j])));
+    }
+    out[i] = 0.5 * twice;
+}
+
+// Internal [p][l][Tp] -> C-ABI [l][p][Ts].
+__global__ void k_counts_export(const uint8_t* __restrict__ c, uint32_t P, uint32_t nl, uint32_t Tp, uint32_t Ts,
+                                uint8_t* __restrict__ out) {
+    const uint32_t lp = blockIdx.x, l = lp / P, p = lp - l * P;
+    for (uint32_t i = threadIdx.x; i < Ts; i += blockDim.x)
+        out[(size_t)lp * Ts + i] = c[((size_t)p * nl + l) * Tp + i];
+}
+
+// Accept-log scatter is written directly by k_decide.
+
+}  // namespace bn

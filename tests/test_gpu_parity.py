@@ -1,0 +1,174 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on identical seeded inputs.
+
+Bar (north star): error vectors (counts) and u_p tiles bit-exact; accept/reject
+sequences identical; exact fixed-point energies equal (which implies per-pass dE within 1e-9
+relative and final E within 1e-6 relative of the oracle's fp64 sum, also asserted).
+Sizes: the oracle finishes in seconds, shapes span several CTAs and a ragged tail (T not a
+multiple of the 128-integrand padding); full BASELINE sizes are checked on sampled outputs.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bn():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (run under gpurun)")
+    from paper_2105_12620_b200 import bn as bnmod
+
+    bnmod.load_library()
+    return bnmod
+
+
+def make(bn, oracle_mod, L, T, levels, tile_seed=1, bank_seed=2, sigma_s=1.0, radius=7, bank=None, U=None):
+    a, b, px, py = bank if bank is not None else synth.make_bank(T, bank_seed)
+    U = synth.make_tile(L, tile_seed) if U is None else U
+    s = bn.Sampler(0)
+    s.set_lattice(synth.D1, synth.D2, levels)
+    s.set_bank(a, b, px, py)
+    s.set_energy(2.1, sigma_s, radius)
+    s.set_tile(L, U)
+    o = oracle_mod.OracleProblem(L, len(a), tuple(levels), synth.D1, synth.D2, a, b, px, py,
+                                 sigma_i=2.1, sigma_s=sigma_s, radius=radius)
+    return s, o, U
+
+
+# ----------------------------------------------------------------------------- counts / I_ref
+@pytest.mark.parametrize("L,T,levels", [(16, 64, (16,)), (16, 200, (1, 4, 16, 64)), (32, 130, (4,)),
+                                        (16, 1, (128,)), (64, 256, (4,))])
+def test_counts_bit_exact(bn, oracle_mod, L, T, levels):
+    s, o, U = make(bn, oracle_mod, L, T, levels)
+    assert np.array_equal(s.eval_counts(), o.counts(U))
+
+
+def test_counts_device_output_and_lattice_cut_bank(bn, oracle_mod):
+    import torch
+
+    N = 64
+    bank = synth.axis_cut_bank(N, np.arange(N), "y")
+    s, o, U = make(bn, oracle_mod, 16, N, (N,), bank=bank)
+    out = torch.zeros((1, 256, N), dtype=torch.uint8, device="cuda")
+    s.eval_counts(out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert np.array_equal(got, o.counts(U))
+    assert np.array_equal(got[0], np.broadcast_to(N - np.arange(N), (256, N)))  # exact integral
+
+
+def test_references(bn, oracle_mod):
+    s, o, _ = make(bn, oracle_mod, 16, 300, (16,))
+    np.testing.assert_allclose(s.get_references(), o.references(), rtol=0, atol=1e-14)
+
+
+# -------------------------------------------------------------------------------- energy
+@pytest.mark.parametrize("L,T,levels,radius,sigma_s", [(16, 64, (16,), 7, 1.0), (32, 100, (1, 4, 16), 7, 1.0),
+                                                       (32, 40, (4,), 3, 0.5), (16, 20, (64,), 1, 2.0)])
+def test_energy_exact(bn, oracle_mod, L, T, levels, radius, sigma_s):
+    s, o, U = make(bn, oracle_mod, L, T, levels, radius=radius, sigma_s=sigma_s)
+    Ef, E = s.energy()
+    Eo, Ep = o.energy(o.counts(U))
+    assert Ef == Eo
+    assert abs(E - Ep) <= 1e-9 * Ep
+
+
+def test_energy_translation_invariance(bn, oracle_mod):
+    s, o, U = make(bn, oracle_mod, 32, 50, (16,))
+    Ef, _ = s.energy()
+    s.set_tile(32, np.ascontiguousarray(np.roll(U.reshape(32, 32, 2), (5, 11), (0, 1)).reshape(-1, 2)))
+    assert s.energy()[0] == Ef
+
+
+# -------------------------------------------------------------------------- optimisation
+def _check_run(s, o, U, passes, mode, seed, first_pass=0):
+    st, lg = s.optimize(passes, seed, mode=mode, first_pass=first_pass, log=True)
+    Uo, co, sto, lgo = o.optimize(U, mode=mode, passes=passes, first_pass=first_pass, seed=seed, log=True)
+    assert np.array_equal(lg, lgo), "accept/reject sequence differs"
+    assert np.array_equal(s.get_tile(), Uo), "tile differs"
+    assert np.array_equal(s.eval_counts(), co), "counts differ"
+    for g, r in zip(st, sto):
+        assert g["accepted"] == r["accepted"] and g["proposed"] == r["proposed"]
+        assert g["E_fixed"] == r["E_fixed"] and g["dE_sum"] == r["dE_sum"]
+        assert abs(g["E"] - r["E_plain"]) <= 1e-6 * r["E_plain"]
+    return st
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_c1_shape_full_run(bn, oracle_mod, mode):
+    """C1: 16x16, 16 spp, T=64, greedy; 200 passes REDRAW (40 SWAP), compared pass by pass."""
+    s, o, U = make(bn, oracle_mod, 16, 64, (16,))
+    st = _check_run(s, o, U, 200 if mode == 0 else 40, mode, seed=3)
+    assert st[-1]["E_fixed"] < st[0]["E_fixed"] + (-st[0]["dE_sum"])
+
+
+def test_c2_shape_swap(bn, oracle_mod):
+    """C2 shape (SWAP, 4 spp) at 32x32, T=100 (ragged)."""
+    s, o, U = make(bn, oracle_mod, 32, 100, (4,))
+    _check_run(s, o, U, 6, 1, seed=5)
+
+
+def test_c3_shape_progressive(bn, oracle_mod):
+    """C3 shape (1/4/16/64 progressive) at 32x32, T=130."""
+    s, o, U = make(bn, oracle_mod, 32, 130, (1, 4, 16, 64))
+    _check_run(s, o, U, 2, 0, seed=7)
+
+
+@pytest.mark.parametrize("radius", [1, 4, 6])
+def test_other_radii(bn, oracle_mod, radius):
+    s, o, U = make(bn, oracle_mod, 16, 24, (4, 16), radius=radius)
+    _check_run(s, o, U, 3, 0, seed=11)
+
+
+def test_resume_and_determinism(bn, oracle_mod):
+    s, o, U = make(bn, oracle_mod, 32, 40, (16,))
+    s.optimize(2, 9)
+    s.optimize(1, 9, first_pass=2)
+    t1 = s.get_tile()
+    s2, _, _ = make(bn, oracle_mod, 32, 40, (16,))
+    s2.optimize(3, 9)
+    assert np.array_equal(t1, s2.get_tile())
+
+
+# ------------------------------------------------------------------------ argument errors
+def test_errors(bn, oracle_mod):
+    s = bn.Sampler(0)
+    with pytest.raises(bn.BNError) as e:
+        s.set_tile(16, np.zeros((256, 2), np.uint32))
+    assert e.value.code == bn.BN_ESTATE
+    with pytest.raises(bn.BNError) as e:
+        s.set_lattice(1, 27, [4, 3])
+    assert e.value.code == bn.BN_EINVAL
+    s2, _, _ = make(bn, oracle_mod, 16, 8, (4,))
+    with pytest.raises(bn.BNError) as e:
+        s2.optimize(1, 1, K=2)
+    assert e.value.code == bn.BN_EINVAL
+    with pytest.raises(bn.BNError) as e:
+        s2.set_tile(24, np.zeros((24 * 24, 2), np.uint32))
+    assert e.value.code == bn.BN_EINVAL
+    with pytest.raises(bn.BNError):
+        s2.set_energy(2.1, 1.0, 8)
+
+
+# ------------------------------------------------------------------ full BASELINE sizes
+@pytest.mark.slow
+def test_c3_full_size_sampled(bn, oracle_mod):
+    """C3 at full size (128x128, T=1024, 1/4/16/64 spp) in the bench's launch configuration:
+    all counts bit-exact, the first colour class's accept decisions identical to the oracle,
+    and the exact-additivity / monotonicity invariants of the whole pass."""
+    cfg = synth.CONFIGS["C3"]
+    U, bank = synth.problem_inputs(cfg)
+    s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
+    co = o.counts(U)
+    assert np.array_equal(s.eval_counts(), co)          # all 64 M counts, bit-exact
+    E0, _ = s.energy()
+    st, lg = s.optimize(1, synth.opt_seed(cfg), log=True)
+    _, _, sto, lgo = o.optimize(U, co, passes=1, seed=synth.opt_seed(cfg), max_steps=2, energy_each_pass=False,
+                                log=True)
+    assert np.array_equal(lg[0, :2], lgo[0, :2])
+    assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"] and st[0]["dE_sum"] < 0
+    assert s.energy()[0] == st[0]["E_fixed"]
