@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -100,7 +101,7 @@ struct bn_ctx {
     DevBuf<int2> ab;
     DevBuf<long long> Cc;
     DevBuf<uint8_t> c, cn, acc, log, cexp;
-    DevBuf<int> nc, nn, derr;
+    DevBuf<int> nc, nn, derr, progress;
     DevBuf<int4> Dt;
     DevBuf<longlong2> d0, d1b;
     DevBuf<i128> dEp;
@@ -112,6 +113,9 @@ struct bn_ctx {
     // multi-GPU
     NcclComm comm = nullptr;
     int rank = 0, world = 1;
+    bool per_class_decide = false;  // BN_DECIDE=per_class: 64 launches instead of one persistent
+    bool simt_gram = false;         // BN_GRAM=simt: dp4a window distances instead of IMMA
+    bool gram_attr_set[8] = {false};
     // per-kernel event timing (bn_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -289,10 +293,24 @@ template <int R>
 int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas) {
     const uint32_t SW = ctx->L < 32 ? ctx->L : 32;
     dim3 grid(ctx->L / SW, ctx->L);
-    KSTART(BN_K_GRAM);
-    k_gram<R><<<grid, 32 * (R + 1), 0, ctx->stream>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, SW, ctx->Tp, ctx->nl,
-                                                      ctx->Dt.p);
-    LAUNCHED_K();
+    if (ctx->simt_gram) {
+        KSTART(BN_K_GRAM);
+        k_gram<R><<<grid, 32 * (R + 1), 0, ctx->stream>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, SW, ctx->Tp,
+                                                          ctx->nl, ctx->Dt.p);
+        LAUNCHED_K();
+    } else {
+        using S = mma_gram::Shape<R>;
+        const int smem = 2 * S::STAGE;
+        if (!ctx->gram_attr_set[R]) {
+            CUDA_TRY(cudaFuncSetAttribute(k_gram_mma<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            ctx->gram_attr_set[R] = true;
+        }
+        dim3 g2(ctx->L / mma_gram::BX, ctx->L / mma_gram::BY);
+        KSTART(BN_K_GRAM);
+        k_gram_mma<R><<<g2, 32 * mma_gram::WARPS, smem, ctx->stream>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, ctx->Tp,
+                                                                       ctx->nl, ctx->Dt.p);
+        LAUNCHED_K();
+    }
     if (ctx->comm) {
         const size_t n = (size_t)ctx->P * half_count(R) * ctx->nl * 4;
         int r = g_nccl.allreduce(ctx->Dt.p, ctx->Dt.p, n, NCCL_INT32, NCCL_SUM, ctx->comm, ctx->stream);
@@ -333,6 +351,56 @@ int launch_decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, 
     LAUNCHED_K();
     return BN_OK;
 }
+// One cooperative launch for all 64 classes (k_decide_pass); co-residency of its CTAs is
+// guaranteed by the cooperative launch, which the neighbour-progress waits require.
+template <int R>
+int launch_decide_pass(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
+    const uint32_t nb = ctx->L / 8;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
+    uint32_t G = 1;
+    while ((nb + G - 1) / G > (uint32_t)nsm / 2) G *= 2;
+    const uint32_t ncta = (nb + G - 1) / G;
+    const uint32_t nmine = G * nb;
+    const uint32_t threads = 32 * (nmine < 16 ? nmine : 16);
+    CUDA_TRY(ctx->progress.ensure(ncta));
+    CUDA_TRY(cudaMemsetAsync(ctx->progress.p, 0, ncta * sizeof(int), ctx->stream));
+    uint32_t L = ctx->L;
+    const longlong2* d0 = ctx->d0.p;
+    const longlong2* d1 = ctx->d1b.p;
+    uint8_t* acc = ctx->acc.p;
+    i128* dEp = ctx->dEp.p;
+    int* prog = ctx->progress.p;
+    void* args[] = {&t, &seed, &L, &mode, &G, &d0, &d1, &acc, &dEp, &log, &prog};
+    KSTART(BN_K_DECIDE);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_decide_pass<R>, dim3(ncta), dim3(threads), args, 0,
+                                                ctx->stream);
+    if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        if (ctx->prof) {  // drop the unmatched start mark
+            ctx->prof_marks.pop_back();
+        }
+        *done = false;
+        return BN_OK;
+    }
+    if (e != cudaSuccess) return fail(ctx, BN_ECUDA, "cooperative decide launch: %s", cudaGetErrorString(e));
+    LAUNCHED_K();
+    *done = true;
+    return BN_OK;
+}
+
+int decide_pass(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
+    switch (ctx->R) {
+        case 1: return launch_decide_pass<1>(ctx, t, seed, mode, log, done);
+        case 2: return launch_decide_pass<2>(ctx, t, seed, mode, log, done);
+        case 3: return launch_decide_pass<3>(ctx, t, seed, mode, log, done);
+        case 4: return launch_decide_pass<4>(ctx, t, seed, mode, log, done);
+        case 5: return launch_decide_pass<5>(ctx, t, seed, mode, log, done);
+        case 6: return launch_decide_pass<6>(ctx, t, seed, mode, log, done);
+        default: return launch_decide_pass<7>(ctx, t, seed, mode, log, done);
+    }
+}
+
 int decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, uint8_t* log) {
     switch (ctx->R) {
         case 1: return launch_decide<1>(ctx, s, t, seed, mode, log);
@@ -372,6 +440,10 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     bn_ctx* ctx = new bn_ctx();
     ctx->dev = cuda_device;
     ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    const char* dm = getenv("BN_DECIDE");
+    ctx->per_class_decide = dm && !strcmp(dm, "per_class");
+    const char* gm = getenv("BN_GRAM");
+    ctx->simt_gram = gm && !strcmp(gm, "simt");
     *out = ctx;
     return BN_OK;
 }
@@ -384,7 +456,7 @@ void bn_destroy(bn_ctx* ctx) {
         if (ctx->comm && g_nccl.destroy) g_nccl.destroy(ctx->comm);
         ctx->S.release(); ctx->U.release(); ctx->Un.release(); ctx->pxy.release(); ctx->ab.release();
         ctx->Cc.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
-        ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->Dt.release();
+        ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
         ctx->d0.release(); ctx->d1b.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release();
         ctx->W.release(); ctx->G.release(); ctx->iref.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -599,8 +671,11 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         }
         if ((rc = gram_lut(ctx, ctx->cn.p, ctx->nn.p, 1))) return rc;
         uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
-        for (uint32_t s = 0; s < 64; ++s)
-            if ((rc = decide(ctx, s, t, prm->seed, (int)prm->mode, log))) return rc;
+        bool done = false;
+        if (!ctx->per_class_decide && (rc = decide_pass(ctx, t, prm->seed, (int)prm->mode, log, &done))) return rc;
+        if (!done)
+            for (uint32_t s = 0; s < 64; ++s)
+                if ((rc = decide(ctx, s, t, prm->seed, (int)prm->mode, log))) return rc;
         KSTART(BN_K_STATS);
         k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, ctx->dEp.p, ctx->acc.p, P,
                                                   prm->mode == BN_SWAP, ctx->pstats.p + pi);

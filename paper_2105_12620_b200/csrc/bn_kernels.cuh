@@ -170,7 +170,8 @@ __global__ void k_swap_gather(const uint2* __restrict__ U, uint2* __restrict__ U
 // words: conflict-free), and every thread accumulates 4 dp4a dot products per offset ox:
 //   <c_p,c_q>, <cn_p,c_q>, <c_p,cn_q>, <cn_p,cn_q>.
 // D = |x|^2 + |y|^2 - 2<x,y> from the per-row norms.  Output Dt[(p*H + h)*nl + l] =
-// int4(D(c,c), D(cn,c), D(c,cn), D(cn,cn)) for h in the half window.
+// int4(D(c,c), D(cn,c), D(c,cn), D(cn,cn)) for h in the half window (layout [l][p][h]).
+// Kept as the SIMT reference path (BN_GRAM=simt); the default is k_gram_mma below.
 constexpr int GRAM_KC = 32;               // bytes of K per stage
 constexpr int GRAM_KCW = GRAM_KC / 4;     // words
 constexpr int GRAM_STRIDE = GRAM_KCW + 1; // padded row stride (words)
@@ -237,8 +238,152 @@ __global__ void __launch_bounds__(32 * (R + 1)) k_gram(const uint8_t* __restrict
                 d.y = nnp + ncq - 2 * (int)acc[i][1];
                 d.z = ncp + nnq - 2 * (int)acc[i][2];
                 d.w = nnp + nnq - 2 * (int)acc[i][3];
-                Dt[((size_t)p * H + half_index(ox, oy, R)) * nl + l] = d;
+                Dt[((size_t)l * L * L + p) * H + half_index(ox, oy, R)] = d;
             }
+        }
+    }
+}
+
+// ------------------------------------------------------------- window distances on IMMA
+// Tensor-core version of k_gram (legacy warp MMA, mma.sync.m16n8k32 u8 x u8 -> s32, exact).
+// CTA = BY x BX = 4 x 16 pixels = 8 strips of 8 pixels; 16 warps; warp w owns strip w >> 1 and
+// the window rows oy in group (w & 1).  Per strip and oy:
+//   A (16 x K)  = rows [c_p0..c_p7 ; cn_p0..cn_p7]                     (M = 16)
+//   B (48 x K)  = [c ; cn] of the NT8 * 8 neighbour pixels of row y+oy  (6 n8 tiles for R = 7)
+//   D (16 x 48) += A B^T  ->  lane (g, t) holds, for pixel g and neighbour columns 2t, 2t+1 of
+//                            every tile, all four products <c_p,c_q>, <cn_p,c_q>, <c_p,cn_q>,
+//                            <cn_p,cn_q>.
+// The CTA stages rows y0 .. y0+BY-1+R, columns x0-R .. x0-R+NCOL-1 of c and cn for a K-chunk of
+// 64 bytes in shared memory (cp.async, double buffered; row stride 80 B: ldmatrix conflict-free).
+// Output layout Dt[l][p][h] (int4), h in the half window.
+namespace mma_gram {
+constexpr int BX = 16, BY = 4, KC = 64, ROWB = KC + 16, WARPS = 16;
+template <int R>
+struct Shape {
+    static constexpr int NT8 = (8 + 2 * R + 7) / 8;  // neighbour n8 tiles per version
+    static constexpr int NCOL = 8 + 8 * NT8;         // staged columns (covers both strips)
+    static constexpr int NROW = BY + R;              // staged rows
+    static constexpr int OYG = (R + 2) / 2;          // oy values per warp (2 groups)
+    static constexpr int STAGE = 2 * NROW * NCOL * ROWB;  // bytes per pipeline stage
+    static constexpr int H = 2 * R * R + 2 * R;
+};
+}  // namespace mma_gram
+
+__device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void imma16832(int* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int R>
+__global__ void __launch_bounds__(512, 1) k_gram_mma(const uint8_t* __restrict__ c, const uint8_t* __restrict__ cn,
+                                                     const int* __restrict__ nc, const int* __restrict__ nn,
+                                                     uint32_t L, uint32_t Tp, uint32_t nl, int4* __restrict__ Dt) {
+    using namespace mma_gram;
+    using S = Shape<R>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int strip = warp >> 1, og = warp & 1;
+    const int sj = strip >> 1, xs = (strip & 1) * 8;  // strip row within the block, x offset
+    const int oy0 = og * S::OYG;
+    const uint32_t rowB = nl * Tp;
+    const int nchunk = S::NROW * S::NCOL * 2 * (KC / 16);
+    // staged row index: ((v * NROW) + r) * NCOL + col
+    auto srow = [&](int v, int r, int col) { return ((v * S::NROW) + r) * S::NCOL + col; };
+
+    for (uint32_t l = 0; l < nl; ++l) {
+        int acc[S::OYG][S::NT8][2][4];
+#pragma unroll
+        for (int a = 0; a < S::OYG; ++a)
+#pragma unroll
+            for (int t = 0; t < S::NT8; ++t)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) acc[a][t][v][0] = acc[a][t][v][1] = acc[a][t][v][2] = acc[a][t][v][3] = 0;
+        const uint32_t nstage = Tp / KC;
+        auto issue = [&](uint32_t st) {
+            const uint32_t buf = sbase + (st & 1) * S::STAGE;
+            const uint32_t k0 = l * Tp + st * KC;
+            for (int j = threadIdx.x; j < nchunk; j += blockDim.x) {
+                const int ch = j & (KC / 16 - 1), row = j / (KC / 16);
+                const int col = row % S::NCOL, vr = row / S::NCOL, r = vr % S::NROW, v = vr / S::NROW;
+                const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
+                const uint8_t* src = (v ? cn : c) + (size_t)(qy * L + qx) * rowB + k0 + 16 * ch;
+                cp_async16(buf + row * ROWB + 16 * ch, src);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        issue(0);
+        for (uint32_t st = 0; st < nstage; ++st) {
+            if (st + 1 < nstage) {
+                issue(st + 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncthreads();
+            const uint32_t buf = sbase + (st & 1) * S::STAGE;
+#pragma unroll
+            for (int kk = 0; kk < KC; kk += 32) {
+                // A fragment: matrices (c, k 0-15), (cn, k 0-15), (c, k 16-31), (cn, k 16-31)
+                uint32_t a[4];
+                {
+                    const int mi = lane >> 3, ri = lane & 7;
+                    const int v = mi & 1, kh = mi >> 1;
+                    ldsm_x4(buf + srow(v, sj, R + xs + ri) * ROWB + kk + 16 * kh, a[0], a[1], a[2], a[3]);
+                }
+#pragma unroll
+                for (int a_oy = 0; a_oy < S::OYG; ++a_oy) {
+                    const int oy = oy0 + a_oy;
+                    if (oy > R) break;
+#pragma unroll
+                    for (int t = 0; t < S::NT8; ++t) {
+                        // B fragments of tile t for both versions: matrices (c,k0-15),(c,k16-31),(cn,k0-15),(cn,k16-31)
+                        uint32_t b[4];
+                        const int mi = lane >> 3, ri = lane & 7;
+                        const int v = mi >> 1, kh = mi & 1;
+                        ldsm_x4(buf + srow(v, sj + oy, xs + 8 * t + ri) * ROWB + kk + 16 * kh, b[0], b[1], b[2], b[3]);
+                        imma16832(acc[a_oy][t][0], a, b[0], b[1]);
+                        imma16832(acc[a_oy][t][1], a, b[2], b[3]);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // epilogue: exact distances from the dot products and the row norms
+        const int g = lane >> 2, tq = lane & 3;
+        const uint32_t px = x0 + xs + g, py = y0 + sj, p = py * L + px;
+        const int ncp = nc[(size_t)p * nl + l], nnp = nn[(size_t)p * nl + l];
+        int4* out = Dt + ((size_t)l * L * L + p) * S::H;
+#pragma unroll
+        for (int a_oy = 0; a_oy < S::OYG; ++a_oy) {
+            const int oy = oy0 + a_oy;
+            if (oy > R) break;
+#pragma unroll
+            for (int t = 0; t < S::NT8; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int n = 8 * t + 2 * tq + e, ox = n - R - g;
+                    if (ox < -R || ox > R || (oy == 0 && ox <= 0)) continue;
+                    const uint32_t q = ((py + oy) & (L - 1)) * L + ((px + ox + L) & (L - 1));
+                    const int ncq = __ldg(nc + (size_t)q * nl + l), nnq = __ldg(nn + (size_t)q * nl + l);
+                    int4 d;
+                    d.x = ncp + ncq - 2 * acc[a_oy][t][0][e];
+                    d.y = nnp + ncq - 2 * acc[a_oy][t][0][2 + e];
+                    d.z = ncp + nnq - 2 * acc[a_oy][t][1][e];
+                    d.w = nnp + nnq - 2 * acc[a_oy][t][1][2 + e];
+                    out[half_index(ox, oy, R)] = d;
+                }
         }
     }
 }
@@ -282,7 +427,7 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
         const double w = W[wi];
         i128 a0 = 0, a1 = 0, b0 = 0, b1 = 0;
         for (uint32_t l = 0; l < nl; ++l) {
-            const int4 D = Dt[idx * nl + l];
+            const int4 D = Dt[(size_t)l * P * H + idx];
             const int dm = lut.Dmax[l];
             if ((unsigned)D.x > (unsigned)dm || (unsigned)D.y > (unsigned)dm || (unsigned)D.z > (unsigned)dm ||
                 (unsigned)D.w > (unsigned)dm) {
@@ -376,6 +521,127 @@ __global__ void k_decide(uint32_t s, uint32_t pass_t, uint64_t seed, uint32_t L,
                 log[(size_t)s * M + mm] = ok;
             }
         }
+    }
+}
+
+// Persistent decision kernel: all 64 colour classes of a pass in ONE cooperative launch.
+// A "band" is the 8 lines (rows for even t, columns for odd t) holding active indices
+// m = b*(L/8) + a of one b.  CTA g owns bands [g*G, (g+1)*G).  Class s of band b only depends
+// on decisions of classes < s in bands b-1, b, b+1 (window radius R < 8), so CTA g waits until
+// its neighbour CTAs have published progress >= s (no grid-wide barrier).  SWAP couples can
+// straddle far bands: both owners evaluate the couple (identical, deterministic result) and
+// each writes its own pixel's flag, after waiting on the bands around both members.
+// The dE terms of the next candidate are loaded before the wait (they do not depend on it).
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int R>
+struct WinTerms {
+    static constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
+    static constexpr int PER = (WN + 31) / 32;
+    longlong2 v0[PER], v1[PER];
+    __device__ __forceinline__ void load(const longlong2* __restrict__ d0, const longlong2* __restrict__ d1,
+                                         uint32_t p) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int w = lane + 32 * j;
+            if (w < WN) {
+                v0[j] = __ldcg(d0 + (size_t)p * WN + w);
+                v1[j] = __ldcg(d1 + (size_t)p * WN + w);
+            }
+        }
+    }
+    // sum_w (acc[p + o_w] ? d1 : d0), reduced over the warp (every lane gets the total)
+    __device__ __forceinline__ i128 sum(const uint8_t* acc, uint32_t L, uint32_t p) const {
+        const int lane = threadIdx.x & 31;
+        const uint32_t x = p % L, y = p / L;
+        uint8_t f[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int w = lane + 32 * j;
+            f[j] = 0;
+            if (w < WN) {
+                const int ww = w >= R * (2 * R + 1) + R ? w + 1 : w;
+                const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
+                const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
+                f[j] = __ldcg(acc + q);
+            }
+        }
+        i128 s = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int w = lane + 32 * j;
+            if (w < WN) {
+                const longlong2 v = f[j] ? v1[j] : v0[j];
+                s += ((i128)v.y << 64) | (u128)(unsigned long long)v.x;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)s, off);
+            const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(s >> 64), off);
+            s += ((i128)hi << 64) | (u128)lo;
+        }
+        return s;
+    }
+};
+
+template <int R>
+__global__ void __launch_bounds__(512) k_decide_pass(uint32_t pass_t, uint64_t seed, uint32_t L, int mode,
+                                                      uint32_t G, const longlong2* __restrict__ d0,
+                                                      const longlong2* __restrict__ d1, uint8_t* acc,
+                                                      i128* __restrict__ dEp, uint8_t* __restrict__ log,
+                                                      int* progress) {
+    const uint32_t nb = L / 8, M = nb * nb;
+    const uint32_t ncta = gridDim.x, g = blockIdx.x;
+    const uint32_t b_lo = g * G, b_hi = min(nb, b_lo + G);
+    const uint32_t nmine = (b_hi - b_lo) * nb;  // candidates of this CTA per class
+    const uint32_t warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t s = 0; s < 64; ++s) {
+        const uint32_t kappa = mode ? swap_kappa(seed, pass_t, s, M) : 0;
+        for (uint32_t j = warp; j < nmine; j += nwarps) {
+            const uint32_t m = b_lo * nb + j;
+            const uint32_t p = class_pixel(L, seed, pass_t, s, m);
+            const uint32_t mm = m ^ kappa, p2 = mode ? class_pixel(L, seed, pass_t, s, mm) : p;
+            WinTerms<R> A, B;
+            A.load(d0, d1, p);
+            if (mode) B.load(d0, d1, p2);
+            // wait for the CTAs owning the bands around p (and p2): progress >= s
+            if (lane == 0 && s > 0) {
+                const uint32_t bs[2] = {m / nb, mm / nb};
+                for (int t = 0; t < (mode ? 2 : 1); ++t)
+                    for (int db = -1; db <= 1; ++db) {
+                        const uint32_t bb = (bs[t] + nb + db) % nb, owner = bb / G;
+                        if (owner == g) continue;
+                        while (ld_acquire(progress + owner) < (int)s) __nanosleep(32);
+                    }
+            }
+            __syncwarp();
+            __threadfence();
+            i128 sum = A.sum(acc, L, p);
+            if (mode) sum += B.sum(acc, L, p2);
+            const i128 dE = 2 * sum;
+            if (lane == 0) {
+                const bool ok = dE < 0;
+                acc[p] = ok;
+                const bool owner_of_couple = !mode || m < mm;
+                dEp[p] = (ok && owner_of_couple) ? dE : (i128)0;
+                if (log) log[(size_t)s * M + m] = ok;
+            }
+        }
+        // intra-CTA: every warp's class-s decisions (own pixels) are visible before the next
+        // class; then publish progress for the neighbour CTAs.
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0 && ncta > 1) st_release(progress + g, (int)s + 1);
     }
 }
 
