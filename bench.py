@@ -132,16 +132,16 @@ def algorithmic(kernel, cfg):
     H = 2 * R * R + 2 * R
     if kernel == "gram":
         # 4 int8 dot products per unordered window pair and level, T-long: 2 ops per MAC
-        return 2.0 * P * H * 4 * nl * T, "ops", "alu"
+        return 2.0 * P * H * 4 * nl * T, "ops", "tensor"
     if kernel == "counts":
-        # one exact half-plane test = 2 int32x int32->int64 multiply-adds per (pixel, integrand, sample)
-        return 2.0 * P * T * max(cfg.levels), "imad.wide", "alu"
+        # one half-plane test per (pixel, integrand, sample) = 2 FFMA (fp32 filter, exact fallback)
+        return 2.0 * P * T * max(cfg.levels), "ffma", "alu"
     if kernel == "lut":
         # bytes: read 4 int32 distances per (p, h, level); write 4 int128 dE terms per (p, h)
         return float(P * H * (16 * nl + 64)), "bytes", "hbm"
     if kernel == "decide":
-        # bytes: one int128 dE term per (candidate, window offset) across the 64 classes / 64 launches
-        return float(P * (2 * R + 1) ** 2 * 16) / 64, "bytes", "hbm"
+        # bytes: both int128 dE terms per (candidate, window offset), all 64 classes in one launch
+        return float(P * ((2 * R + 1) ** 2 - 1) * 32), "bytes", "hbm"
     return None, None, None
 
 
@@ -159,16 +159,23 @@ def roofline(prof, cfg, peaks, sm_clock_mhz):
         peak = peaks.get("hbm_gbs", 6650.0)
         out.update(bound="hbm", achieved=per_s / 1e9, peak=peak, unit="GB/s")
         out["peak_source"] = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
+    elif bound == "tensor":
+        # int8 dense tensor peak = measured bf16 dense (cuBLAS) x nominal int8/bf16 ratio 4.5/2.25
+        bf16 = peaks.get("bf16_tflops", 1590.0)
+        peak = 2.0 * bf16
+        out.update(bound="tensor", achieved=per_s / 1e12, peak=peak, unit="TOP/s (int8)")
+        out["peak_source"] = ("MEASURED_PEAKS.json bf16_tflops x 2 (B200_PROFILING.md nominal int8:bf16 = 4.5:2.25)"
+                              if "bf16_tflops" in peaks else "fallback 1.59 PF bf16 x 2")
     else:
         clk = peaks.get("sm_max_mhz", 1965.0)
         if kind == "ops":
             peak = SMS * DP4A_PER_CLK_SM * 8 * clk * 1e6 / 1e12  # TOP/s (dp4a: 4 MAC = 8 ops)
             out.update(bound="alu", achieved=per_s / 1e12, peak=peak, unit="TOP/s")
         else:
-            peak = SMS * 64 * 0.5 * clk * 1e6 / 1e12             # T IMAD.WIDE/s (half-rate wide ops)
-            out.update(bound="alu", achieved=per_s / 1e12, peak=peak, unit="T imad.wide/s")
-        out["peak_source"] = ("derived: 148 SM x 64 lanes/clk fma-pipe x clocks.max.sm "
-                              f"{clk:.0f} MHz (DESIGN.md §7)")
+            peak = SMS * 128 * clk * 1e6 / 1e12                  # T FFMA/s: 128 lanes/clk/SM
+            out.update(bound="alu", achieved=per_s / 1e12, peak=peak, unit="T FFMA/s")
+        lanes = "64 dp4a" if kind == "ops" else "128 FFMA"
+        out["peak_source"] = f"derived: 148 SM x {lanes} lanes/clk x clocks.max.sm {clk:.0f} MHz (DESIGN.md §7)"
     out["frac"] = out["achieved"] / out["peak"]
     out["traffic"] = None
     try:

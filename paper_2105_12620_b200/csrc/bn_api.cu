@@ -97,11 +97,11 @@ struct bn_ctx {
     bool have_tile = false, counts_dirty = true;
     uint32_t L = 0, P = 0, rowB = 0;
     // device state
-    DevBuf<uint2> S, U, Un, pxy;
+    DevBuf<uint2> S, U, Un, Un2, pxy;
     DevBuf<int2> ab;
     DevBuf<long long> Cc;
-    DevBuf<uint8_t> c, cn, acc, log, cexp;
-    DevBuf<int> nc, nn, derr, progress;
+    DevBuf<uint8_t> c, cn, cn2, acc, log, cexp;
+    DevBuf<int> nc, nn, nn2, derr, progress;
     DevBuf<int4> Dt;
     DevBuf<longlong2> d0, d1b;
     DevBuf<i128> dEp;
@@ -113,9 +113,17 @@ struct bn_ctx {
     // multi-GPU
     NcclComm comm = nullptr;
     int rank = 0, world = 1;
+    // streams: `stream` is the caller's; `ls` is the stream the next launch goes to; `aux`
+    // (candidate prefetch) and `hp` (high-priority decisions) are internal, joined by events.
+    cudaStream_t ls = nullptr, aux = nullptr, hp = nullptr;
+    cudaEvent_t evA = nullptr, evB = nullptr, evC = nullptr;
+    bool no_overlap = false;  // BN_OVERLAP=0: no candidate prefetch on the aux stream
     bool per_class_decide = false;  // BN_DECIDE=per_class: 64 launches instead of one persistent
     bool simt_gram = false;         // BN_GRAM=simt: dp4a window distances instead of IMMA
     bool gram_attr_set[8] = {false};
+    bool decide_attr_set[8] = {false};
+    bool cluster_attr_set[8] = {false};
+    bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     // per-kernel event timing (bn_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -168,17 +176,19 @@ cudaEvent_t next_event(bn_ctx* ctx) {
         if (ctx->prof) {                                                            \
             if (ctx->ev_used + 2 > 4096) flush_profile(ctx);                         \
             ctx->prof_marks.push_back({(id), ctx->ev_used});                         \
-            cudaEventRecord(next_event(ctx), ctx->stream);                          \
+            cudaEventRecord(next_event(ctx), ctx->ls);                              \
         }                                                                           \
     } while (0)
 #define LAUNCHED_K()                                                                \
     do {                                                                            \
-        if (ctx->prof) cudaEventRecord(next_event(ctx), ctx->stream);               \
+        if (ctx->prof) cudaEventRecord(next_event(ctx), ctx->ls);                   \
         LAUNCHED();                                                                 \
     } while (0)
 
 void flush_profile(bn_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->aux) cudaStreamSynchronize(ctx->aux);
+    if (ctx->hp) cudaStreamSynchronize(ctx->hp);
     for (auto& m : ctx->prof_marks) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev_pool[m.second], ctx->ev_pool[m.second + 1]);
@@ -265,7 +275,7 @@ int ensure_counts(bn_ctx* ctx) {
     const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
     const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
     KSTART(BN_K_COUNTS);
-    k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->stream>>>(
+    k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->ls>>>(
         ctx->U.p, nullptr, 0, 0, 0, P, ctx->ab.p, ctx->Cc.p, ctx->Tp, ctx->S.p, Nmax, lo, hi, ctx->nl, ctx->c.p,
         ctx->nc.p);
     LAUNCHED_K();
@@ -295,7 +305,7 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
     dim3 grid(ctx->L / SW, ctx->L);
     if (ctx->simt_gram) {
         KSTART(BN_K_GRAM);
-        k_gram<R><<<grid, 32 * (R + 1), 0, ctx->stream>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, SW, ctx->Tp,
+        k_gram<R><<<grid, 32 * (R + 1), 0, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, SW, ctx->Tp,
                                                           ctx->nl, ctx->Dt.p);
         LAUNCHED_K();
     } else {
@@ -307,7 +317,7 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
         }
         dim3 g2(ctx->L / mma_gram::BX, ctx->L / mma_gram::BY);
         KSTART(BN_K_GRAM);
-        k_gram_mma<R><<<g2, 32 * mma_gram::WARPS, smem, ctx->stream>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, ctx->Tp,
+        k_gram_mma<R><<<g2, 32 * mma_gram::WARPS, smem, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, ctx->Tp,
                                                                        ctx->nl, ctx->Dt.p);
         LAUNCHED_K();
     }
@@ -323,7 +333,7 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
     }
     const size_t nthr = (size_t)ctx->P * half_count(R);
     KSTART(BN_K_LUT);
-    k_lut<R><<<(unsigned)((nthr + 255) / 256), 256, 0, ctx->stream>>>(ctx->Dt.p, ctx->L, ctx->nl, ctx->W.p, la,
+    k_lut<R><<<(unsigned)((nthr + 255) / 256), 256, 0, ctx->ls>>>(ctx->Dt.p, ctx->L, ctx->nl, ctx->W.p, la,
                                                                       write_deltas, ctx->d0.p, ctx->d1b.p,
                                                                       ctx->Epart.p, ctx->derr.p);
     LAUNCHED_K();
@@ -346,40 +356,100 @@ template <int R>
 int launch_decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, uint8_t* log) {
     const uint32_t M = (ctx->L / 8) * (ctx->L / 8);
     KSTART(BN_K_DECIDE);
-    k_decide<R><<<(M + 3) / 4, 128, 0, ctx->stream>>>(s, t, seed, ctx->L, mode, ctx->d0.p, ctx->d1b.p, ctx->acc.p,
+    k_decide<R><<<(M + 3) / 4, 128, 0, ctx->ls>>>(s, t, seed, ctx->L, mode, ctx->d0.p, ctx->d1b.p, ctx->acc.p,
                                                       ctx->dEp.p, log);
     LAUNCHED_K();
     return BN_OK;
 }
 // One cooperative launch for all 64 classes (k_decide_pass); co-residency of its CTAs is
 // guaranteed by the cooperative launch, which the neighbour-progress waits require.
+// Cluster launch of k_decide_cluster when the tile's candidate CTAs fit one cluster (<= 16).
+template <int R>
+int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
+    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
+    const uint32_t nb = ctx->L / 8, P = ctx->P;
+    uint32_t cpc = mode ? 8 : 16;
+    while (cpc > nb) cpc /= 2;
+    const uint32_t ncta = nb * nb / cpc;
+    *done = false;
+    if (ncta > 16 || ctx->no_cluster) return BN_OK;
+    const size_t smem = (size_t)(mode ? 2 : 1) * cpc * 2 * WN * 16 + P;
+    const void* fn = mode ? (const void*)k_decide_cluster<R, 1> : (const void*)k_decide_cluster<R, 0>;
+    if (!ctx->cluster_attr_set[R]) {
+        for (const void* f : {(const void*)k_decide_cluster<R, 0>, (const void*)k_decide_cluster<R, 1>}) {
+            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        }
+        ctx->cluster_attr_set[R] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncta);
+    cfg.blockDim = dim3(32 * cpc);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->ls;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ncta;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+        cudaGetLastError();
+        return BN_OK;  // cluster does not fit: persistent flag kernel instead
+    }
+    uint32_t L = ctx->L;
+    const longlong2* d0 = ctx->d0.p;
+    const longlong2* d1 = ctx->d1b.p;
+    uint8_t* acc = ctx->acc.p;
+    i128* dEp = ctx->dEp.p;
+    void* args[] = {&t, &seed, &L, &cpc, &d0, &d1, &acc, &dEp, &log};
+    KSTART(BN_K_DECIDE);
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess) return fail(ctx, BN_ECUDA, "cluster decide launch: %s", cudaGetErrorString(e));
+    LAUNCHED_K();
+    *done = true;
+    return BN_OK;
+}
+
 template <int R>
 int launch_decide_pass(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
+    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
+    int rc = launch_decide_cluster<R>(ctx, t, seed, mode, log, done);
+    if (rc || *done) return rc;
     const uint32_t nb = ctx->L / 8;
+    // candidates per CTA: <= 16 warps (REDRAW) / 8 (SWAP stages the partner too); divides nb
+    uint32_t cpc = mode ? 8 : 16;
+    while (cpc > nb) cpc /= 2;
+    const uint32_t ncta = nb * nb / cpc;
+    const size_t smem = (size_t)(mode ? 2 : 1) * cpc * 2 * WN * 16;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
-    uint32_t G = 1;
-    while ((nb + G - 1) / G > (uint32_t)nsm / 2) G *= 2;
-    const uint32_t ncta = (nb + G - 1) / G;
-    const uint32_t nmine = G * nb;
-    const uint32_t threads = 32 * (nmine < 16 ? nmine : 16);
+    if (ncta > (uint32_t)nsm || nb > 512) {
+        *done = false;  // not co-residable: per-class launches
+        return BN_OK;
+    }
+    const void* fn = mode ? (const void*)k_decide_pass<R, 1> : (const void*)k_decide_pass<R, 0>;
+    if (!ctx->decide_attr_set[R]) {
+        CUDA_TRY(cudaFuncSetAttribute(k_decide_pass<R, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_decide_pass<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        ctx->decide_attr_set[R] = true;
+    }
     CUDA_TRY(ctx->progress.ensure(ncta));
-    CUDA_TRY(cudaMemsetAsync(ctx->progress.p, 0, ncta * sizeof(int), ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(ctx->progress.p, 0, ncta * sizeof(int), ctx->ls));
     uint32_t L = ctx->L;
     const longlong2* d0 = ctx->d0.p;
     const longlong2* d1 = ctx->d1b.p;
     uint8_t* acc = ctx->acc.p;
     i128* dEp = ctx->dEp.p;
     int* prog = ctx->progress.p;
-    void* args[] = {&t, &seed, &L, &mode, &G, &d0, &d1, &acc, &dEp, &log, &prog};
+    void* args[] = {&t, &seed, &L, &cpc, &d0, &d1, &acc, &dEp, &log, &prog};
     KSTART(BN_K_DECIDE);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_decide_pass<R>, dim3(ncta), dim3(threads), args, 0,
-                                                ctx->stream);
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(ncta), dim3(32 * cpc), args, smem, ctx->ls);
     if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
         cudaGetLastError();
-        if (ctx->prof) {  // drop the unmatched start mark
-            ctx->prof_marks.pop_back();
-        }
+        if (ctx->prof) ctx->prof_marks.pop_back();
         *done = false;
         return BN_OK;
     }
@@ -442,6 +512,24 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
     const char* dm = getenv("BN_DECIDE");
     ctx->per_class_decide = dm && !strcmp(dm, "per_class");
+    ctx->no_cluster = dm && !strcmp(dm, "flags");
+    const char* ov = getenv("BN_OVERLAP");
+    ctx->no_overlap = ov && !strcmp(ov, "0");
+    ctx->ls = ctx->stream;
+    {
+        DeviceGuard g(cuda_device);
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, lo) != cudaSuccess ||
+            cudaStreamCreateWithPriority(&ctx->hp, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->evA, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->evB, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->evC, cudaEventDisableTiming) != cudaSuccess) {
+            delete ctx;
+            *out = nullptr;
+            return BN_ECUDA;
+        }
+    }
     const char* gm = getenv("BN_GRAM");
     ctx->simt_gram = gm && !strcmp(gm, "simt");
     *out = ctx;
@@ -460,6 +548,11 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->d0.release(); ctx->d1b.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release();
         ctx->W.release(); ctx->G.release(); ctx->iref.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+        ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release();
+        if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
+        if (ctx->hp) cudaStreamSynchronize(ctx->hp), cudaStreamDestroy(ctx->hp);
+        for (cudaEvent_t e : {ctx->evA, ctx->evB, ctx->evC})
+            if (e) cudaEventDestroy(e);
     }
     delete ctx;
 }
@@ -511,7 +604,7 @@ int bn_set_bank(bn_ctx* ctx, uint32_t T, const int32_t* a, const int32_t* b, con
     ctx->t0 = t_begin;
     ctx->t1 = t_end;
     ctx->Ts = t_end - t_begin;
-    ctx->Tp = round_up(ctx->Ts, 128);
+    ctx->Tp = round_up(ctx->Ts, 256);  // k_counts: 8 integrands/thread, whole warps
     ctx->a.assign(a, a + T);
     ctx->b.assign(b, b + T);
     ctx->px.assign(px, px + T);
@@ -654,37 +747,76 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
     const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
     const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
+    // Candidate buffers are double-buffered so that the REDRAW candidates of pass t+1 (which do
+    // not depend on pass t's decisions) are counted on the aux stream while pass t's colour
+    // classes are decided on the high-priority stream.
+    const bool overlap = prm->mode == BN_REDRAW && !ctx->no_overlap && prm->passes > 1 && !ctx->comm;
+    if (overlap) {
+        CUDA_TRY(ctx->Un2.ensure(P));
+        CUDA_TRY(ctx->cn2.ensure((size_t)P * ctx->rowB));
+        CUDA_TRY(ctx->nn2.ensure((size_t)P * nl));
+    }
+    auto buf_U = [&](uint32_t pi) { return (overlap && (pi & 1)) ? ctx->Un2.p : ctx->Un.p; };
+    auto buf_c = [&](uint32_t pi) { return (overlap && (pi & 1)) ? ctx->cn2.p : ctx->cn.p; };
+    auto buf_n = [&](uint32_t pi) { return (overlap && (pi & 1)) ? ctx->nn2.p : ctx->nn.p; };
+    auto launch_counts = [&](uint32_t pi) -> int {
+        KSTART(BN_K_COUNTS);
+        k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->ls>>>(
+            nullptr, buf_U(pi), 1, prm->seed, prm->first_pass + pi, P, ctx->ab.p, ctx->Cc.p, ctx->Tp, ctx->S.p,
+            ctx->levels[nl - 1], lo, hi, nl, buf_c(pi), buf_n(pi));
+        LAUNCHED_K();
+        return BN_OK;
+    };
     for (uint32_t pi = 0; pi < prm->passes; ++pi) {
         const uint32_t t = prm->first_pass + pi;
+        ctx->ls = ctx->stream;
         CUDA_TRY(cudaMemsetAsync(ctx->acc.p, 0, P, ctx->stream));
         if (prm->mode == BN_REDRAW) {
-            KSTART(BN_K_COUNTS);
-            k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->stream>>>(
-                nullptr, ctx->Un.p, 1, prm->seed, t, P, ctx->ab.p, ctx->Cc.p, ctx->Tp, ctx->S.p,
-                ctx->levels[nl - 1], lo, hi, nl, ctx->cn.p, ctx->nn.p);
-            LAUNCHED_K();
+            if (overlap && pi > 0) {
+                CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evC, 0));  // prefetched by pass pi-1
+            } else if ((rc = launch_counts(pi))) {
+                return rc;
+            }
         } else {
             KSTART(BN_K_GATHER);
             k_swap_gather<<<64 * M, 128, 0, ctx->stream>>>(ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p, ctx->nc.p,
                                                           ctx->nn.p, ctx->L, prm->seed, t, ctx->rowB, nl);
             LAUNCHED_K();
         }
-        if ((rc = gram_lut(ctx, ctx->cn.p, ctx->nn.p, 1))) return rc;
+        if ((rc = gram_lut(ctx, buf_c(pi), buf_n(pi), 1))) return rc;
         uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
+        if (overlap) {
+            // decisions on hp, next candidates on aux, both after this pass's energy terms
+            CUDA_TRY(cudaEventRecord(ctx->evA, ctx->stream));
+            CUDA_TRY(cudaStreamWaitEvent(ctx->hp, ctx->evA, 0));
+            ctx->ls = ctx->hp;
+        }
         bool done = false;
         if (!ctx->per_class_decide && (rc = decide_pass(ctx, t, prm->seed, (int)prm->mode, log, &done))) return rc;
         if (!done)
             for (uint32_t s = 0; s < 64; ++s)
                 if ((rc = decide(ctx, s, t, prm->seed, (int)prm->mode, log))) return rc;
+        if (overlap) {
+            CUDA_TRY(cudaEventRecord(ctx->evB, ctx->hp));
+            if (pi + 1 < prm->passes) {
+                CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->evA, 0));
+                ctx->ls = ctx->aux;
+                if ((rc = launch_counts(pi + 1))) return rc;
+                CUDA_TRY(cudaEventRecord(ctx->evC, ctx->aux));
+            }
+            ctx->ls = ctx->stream;
+            CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evB, 0));
+        }
         KSTART(BN_K_STATS);
         k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, ctx->dEp.p, ctx->acc.p, P,
                                                   prm->mode == BN_SWAP, ctx->pstats.p + pi);
         LAUNCHED_K();
         KSTART(BN_K_COMMIT);
-        k_commit<<<P, 128, 0, ctx->stream>>>(ctx->acc.p, P, ctx->rowB, nl, ctx->Un.p, ctx->U.p, ctx->cn.p, ctx->c.p,
-                                             ctx->nn.p, ctx->nc.p);
+        k_commit<<<P, 128, 0, ctx->stream>>>(ctx->acc.p, P, ctx->rowB, nl, buf_U(pi), ctx->U.p, buf_c(pi), ctx->c.p,
+                                             buf_n(pi), ctx->nc.p);
         LAUNCHED_K();
     }
+    ctx->ls = ctx->stream;
     if (stats || accept_log) {
         std::vector<PassStatsDev> h(prm->passes);
         CUDA_TRY(cudaMemcpyAsync(h.data(), ctx->pstats.p, prm->passes * sizeof(PassStatsDev), cudaMemcpyDeviceToHost,

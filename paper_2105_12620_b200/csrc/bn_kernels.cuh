@@ -58,6 +58,13 @@ __device__ __forceinline__ uint32_t class_pixel(uint32_t L, uint64_t seed, uint3
 __device__ __forceinline__ uint32_t swap_kappa(uint64_t seed, uint32_t t, uint32_t s, uint32_t M) {
     return 1u + philox_seeded(seed, s, t, 0, 3).x % (M - 1u);
 }
+// Same as class_pixel with delta(t, r, b) & 7 read from a per-pass table tab[r * nb + b].
+__device__ __forceinline__ uint32_t class_pixel_tab(const uint8_t* tab, uint32_t L, uint32_t t, uint32_t s,
+                                                    uint32_t m) {
+    const uint32_t nb = L >> 3, b = m / nb, a = m - b * nb, r = s >> 3, k = s & 7;
+    const uint32_t along = 8 * a + ((tab[r * nb + b] + k) & 7), across = 8 * b + r;
+    return (t & 1) ? along * L + across : across * L + along;
+}
 
 // Window indexing.  Full window W: raster over (oy, ox) in [-R,R]^2 minus the centre.
 __host__ __device__ __forceinline__ int win_index(int ox, int oy, int R) {
@@ -78,13 +85,53 @@ __host__ __device__ __forceinline__ int half_index(int ox, int oy, int R) {
 // Layout out: [p][l][Tp] uint8; norms: [p][l] int32 = sum_i c^2.
 constexpr int COUNT_PIX = 8;  // pixels per CTA
 
-__global__ void __launch_bounds__(256) k_counts(const uint2* __restrict__ U, uint2* __restrict__ Uout, int redraw,
+// Filtered fast test.  t = fma(a, x', fma(b, y', -C)) in fp32 with x' = fl(X'), C~ = fl(C):
+//   |x' - X'| <= 2^6, |C~ - C| <= 2^24, |a|,|b| <= 2^15, |b y' - C~| < 2^49
+//   => |t - v| <= 2^21 + 2^24 + 2^21 + 2^24 + 2^25 < 2^27
+// so sign(t) = sign(v) whenever |t| >= 2^27.  A (pixel, integrand) whose samples ever come
+// closer than that (probability ~2^-20 per test) is recounted exactly in int64.
+constexpr float COUNT_EXACT_BAND = 134217728.0f;  // 2^27
+
+template <int NI>
+__device__ __forceinline__ void count_span(const float2* __restrict__ xyf, uint32_t k0, uint32_t k1, const float* af,
+                                           const float* bf, const float* cf, uint32_t* neg, float* mn) {
+    uint32_t k = k0;
+    for (; k + 4 <= k1; k += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float2 xy = xyf[k + u];
+#pragma unroll
+            for (int j = 0; j < NI; ++j) {
+                const float t = fmaf(af[j], xy.x, fmaf(bf[j], xy.y, cf[j]));
+                neg[j] += __float_as_uint(t) >> 31;
+                mn[j] = fminf(mn[j], fabsf(t));
+            }
+        }
+    }
+    for (; k < k1; ++k) {
+        const float2 xy = xyf[k];
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+            const float t = fmaf(af[j], xy.x, fmaf(bf[j], xy.y, cf[j]));
+            neg[j] += __float_as_uint(t) >> 31;
+            mn[j] = fminf(mn[j], fabsf(t));
+        }
+    }
+}
+
+// Each thread owns NI = 8 consecutive integrands (two packed 32-bit words per level row) and
+// walks the CTA's pixels; the sample loop is split at the level boundaries N_l so that the
+// inner loop is branch-free and unrolled.
+constexpr int COUNT_NI = 8;
+__global__ void __launch_bounds__(256, 3) k_counts(const uint2* __restrict__ U, uint2* __restrict__ Uout, int redraw,
                                                 uint64_t seed, uint32_t pass_t, uint32_t P,
                                                 const int2* __restrict__ ab, const long long* __restrict__ Cc,
                                                 uint32_t Tp, const uint2* __restrict__ S, uint32_t Nmax,
                                                 uint4 lev_lo, uint4 lev_hi, uint32_t nl, uint8_t* __restrict__ out,
                                                 int* __restrict__ norms) {
+    constexpr int NI = COUNT_NI;
     __shared__ int2 sXY[COUNT_PIX][128];
+    __shared__ float2 sXYf[COUNT_PIX][128];
     __shared__ int sNorm[COUNT_PIX][8];
     const uint32_t levels[8] = {lev_lo.x, lev_lo.y, lev_lo.z, lev_lo.w, lev_hi.x, lev_hi.y, lev_hi.z, lev_hi.w};
     const uint32_t p0 = blockIdx.x * COUNT_PIX;
@@ -101,39 +148,73 @@ __global__ void __launch_bounds__(256) k_counts(const uint2* __restrict__ U, uin
             u = U[p];
         }
         const uint2 s = S[k];
-        sXY[pp][k] = make_int2((int)((s.x + u.x) ^ 0x80000000u), (int)((s.y + u.y) ^ 0x80000000u));
+        const int2 xy = make_int2((int)((s.x + u.x) ^ 0x80000000u), (int)((s.y + u.y) ^ 0x80000000u));
+        sXY[pp][k] = xy;
+        sXYf[pp][k] = make_float2(__int2float_rn(xy.x), __int2float_rn(xy.y));
     }
     __syncthreads();
-    for (uint32_t q4 = threadIdx.x; q4 < Tp / 4; q4 += blockDim.x) {
-        int2 abv[4];
-        long long cv[4];
+    // threads = (integrand group q) x (pixel subset sub): when Tp/NI < blockDim the CTA's threads
+    // split its pixels instead of idling (Tp/NI is a multiple of 32, so warps stay uniform)
+    const uint32_t qn = Tp / NI;
+    const uint32_t nsub = qn < blockDim.x ? blockDim.x / qn : 1;
+    const uint32_t sub = threadIdx.x / (blockDim.x / nsub), tq = threadIdx.x % (blockDim.x / nsub);
+    for (uint32_t q = tq; q < qn; q += blockDim.x / nsub) {
+        float af[NI], bf[NI], cf[NI];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            abv[j] = ab[4 * q4 + j];
-            cv[j] = Cc[4 * q4 + j];
+        for (int j = 0; j < NI; ++j) {
+            const int2 v = ab[NI * q + j];
+            af[j] = (float)v.x;
+            bf[j] = (float)v.y;
+            cf[j] = -__ll2float_rn(Cc[NI * q + j]);
         }
-        for (int pp = 0; pp < COUNT_PIX; ++pp) {
+        for (uint32_t pp = sub; pp < COUNT_PIX; pp += nsub) {
             const uint32_t p = p0 + pp;
             if (p >= P) break;
-            uint32_t cnt[4] = {0, 0, 0, 0};
-            uint32_t li = 0, nsq = 0;
-            uint32_t next = levels[0];
-            for (uint32_t k = 0; k < Nmax; ++k) {
-                const int2 xy = sXY[pp][k];
+            uint32_t neg[NI];
+            float mn[NI];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const long long v = (long long)abv[j].x * xy.x + (long long)abv[j].y * xy.y - cv[j];
-                    cnt[j] += (v >= 0);
+            for (int j = 0; j < NI; ++j) {
+                neg[j] = 0;
+                mn[j] = 3.0e38f;
+            }
+            uint8_t* orow = out + (size_t)p * nl * Tp + NI * q;
+            uint32_t kprev = 0;
+            for (uint32_t li = 0; li < nl; ++li) {
+                const uint32_t n1 = levels[li];
+                count_span<NI>(sXYf[pp], kprev, n1, af, bf, cf, neg, mn);
+                kprev = n1;
+                uint32_t w[NI / 4];
+                uint32_t nsq = 0;
+#pragma unroll
+                for (int h = 0; h < NI / 4; ++h) {
+                    const uint32_t c0 = n1 - neg[4 * h], c1 = n1 - neg[4 * h + 1];
+                    const uint32_t c2 = n1 - neg[4 * h + 2], c3 = n1 - neg[4 * h + 3];
+                    w[h] = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+                    nsq += c0 * c0 + c1 * c1 + c2 * c2 + c3 * c3;
                 }
-                if (k + 1 == next) {
-                    const uint32_t packed = cnt[0] | (cnt[1] << 8) | (cnt[2] << 16) | (cnt[3] << 24);
-                    *reinterpret_cast<uint32_t*>(out + ((size_t)p * nl + li) * Tp + 4 * q4) = packed;
-                    nsq = cnt[0] * cnt[0] + cnt[1] * cnt[1] + cnt[2] * cnt[2] + cnt[3] * cnt[3];
+                *reinterpret_cast<uint2*>(orow + (size_t)li * Tp) = make_uint2(w[0], w[1]);
 #pragma unroll
-                    for (int off = 16; off; off >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, off);
-                    if ((threadIdx.x & 31) == 0) atomicAdd(&sNorm[pp][li], (int)nsq);
-                    ++li;
-                    next = li < nl ? levels[li] : 0xffffffffu;
+                for (int off = 16; off; off >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, off);
+                if ((threadIdx.x & 31) == 0) atomicAdd(&sNorm[pp][li], (int)nsq);
+            }
+            // exact int64 recount of any integrand whose samples came within the error band
+#pragma unroll
+            for (int j = 0; j < NI; ++j) {
+                if (mn[j] >= COUNT_EXACT_BAND) continue;
+                const int2 abj = ab[NI * q + j];
+                const long long cj = Cc[NI * q + j];
+                uint32_t cnt = 0, lj = 0, nx = levels[0];
+                for (uint32_t k = 0; k < Nmax; ++k) {
+                    const int2 xy = sXY[pp][k];
+                    cnt += ((long long)abj.x * xy.x + (long long)abj.y * xy.y - cj) >= 0;
+                    if (k + 1 == nx) {
+                        uint8_t* cell = orow + (size_t)lj * Tp + j;
+                        const int old = *cell;
+                        *cell = (uint8_t)cnt;
+                        atomicAdd(&sNorm[pp][lj], (int)(cnt * cnt) - old * old);
+                        ++lj;
+                        nx = lj < nl ? levels[lj] : 0xffffffffu;
+                    }
                 }
             }
         }
@@ -144,8 +225,8 @@ __global__ void __launch_bounds__(256) k_counts(const uint2* __restrict__ U, uin
         if (p0 + pp < P) norms[(size_t)(p0 + pp) * nl + l] = sNorm[pp][l];
     }
 }
-// NOTE: the warp-level shuffle in k_counts requires every lane of a warp to reach it together:
-// the q4 loop bound Tp/4 is a multiple of 8 lanes... callers guarantee Tp % 128 == 0.
+// The warp shuffle in k_counts needs all 32 lanes of a warp in the q loop together: Tp / 8 must
+// be a multiple of 32, i.e. callers guarantee Tp % 256 == 0.
 
 // SWAP candidates: cn_p = c_partner(p), Un_p = U_partner(p), for every (class s, index m).
 __global__ void k_swap_gather(const uint2* __restrict__ U, uint2* __restrict__ Un, const uint8_t* __restrict__ c,
@@ -546,15 +627,15 @@ struct WinTerms {
     static constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     static constexpr int PER = (WN + 31) / 32;
     longlong2 v0[PER], v1[PER];
-    __device__ __forceinline__ void load(const longlong2* __restrict__ d0, const longlong2* __restrict__ d1,
-                                         uint32_t p) {
+    // from the shared-memory staging buffer: rows [WN] of delta0 then [WN] of delta1
+    __device__ __forceinline__ void load_smem(const longlong2* row) {
         const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int w = lane + 32 * j;
             if (w < WN) {
-                v0[j] = __ldcg(d0 + (size_t)p * WN + w);
-                v1[j] = __ldcg(d1 + (size_t)p * WN + w);
+                v0[j] = row[w];
+                v1[j] = row[WN + w];
             }
         }
     }
@@ -593,55 +674,204 @@ struct WinTerms {
     }
 };
 
+// Stage the dE-term rows (delta0, delta1) of the candidates of CTA `g` for class s into smem.
+// Slot j holds candidate m = first + j (and, for SWAP, slot cpc + j its partner's rows).
 template <int R>
-__global__ void __launch_bounds__(512) k_decide_pass(uint32_t pass_t, uint64_t seed, uint32_t L, int mode,
-                                                      uint32_t G, const longlong2* __restrict__ d0,
-                                                      const longlong2* __restrict__ d1, uint8_t* acc,
-                                                      i128* __restrict__ dEp, uint8_t* __restrict__ log,
-                                                      int* progress) {
+__device__ __forceinline__ void stage_class(uint32_t smem_base, const uint32_t* slot_pix, uint32_t nslot,
+                                            const longlong2* __restrict__ d0, const longlong2* __restrict__ d1) {
+    constexpr int WN = WinTerms<R>::WN;
+    for (uint32_t j = threadIdx.x; j < nslot * 2 * WN; j += blockDim.x) {
+        const uint32_t slot = j / (2 * WN), e = j - slot * 2 * WN, tab = e >= (uint32_t)WN, w = e - tab * WN;
+        const longlong2* src = (tab ? d1 : d0) + (size_t)slot_pix[slot] * WN + w;
+        cp_async16(smem_base + (slot * 2 * WN + e) * 16, src);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Persistent decision kernel v3: CTA g owns `cpc` consecutive active indices (a contiguous part
+// of one band).  For class s it (1) moves the staged dE terms of its candidates from smem to
+// registers, (2) immediately stages class s+1's terms with cp.async (they do not depend on any
+// decision), (3) waits until the CTAs of the neighbouring bands have published progress >= s,
+// (4) reads the neighbours' accept flags, reduces, decides, and publishes progress s+1.
+template <int R, int mode>
+__global__ void __launch_bounds__(512, 1) k_decide_pass(uint32_t pass_t, uint64_t seed, uint32_t L,
+                                                        uint32_t cpc, const longlong2* __restrict__ d0,
+                                                        const longlong2* __restrict__ d1, uint8_t* acc,
+                                                        i128* __restrict__ dEp, uint8_t* __restrict__ log,
+                                                        int* progress) {
+    constexpr int WN = WinTerms<R>::WN;
+    extern __shared__ __align__(16) uint8_t dsm[];
+    __shared__ uint8_t sDelta[8 * 512];     // delta(t, r, b) & 7, r < 8, b < nb <= 512
+    __shared__ uint32_t sKappa[64];
+    __shared__ uint32_t sSlot[2][32];       // pixels of the staged slots, double indexed by class parity
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(dsm);
+    const longlong2* srows = reinterpret_cast<const longlong2*>(dsm);
     const uint32_t nb = L / 8, M = nb * nb;
-    const uint32_t ncta = gridDim.x, g = blockIdx.x;
-    const uint32_t b_lo = g * G, b_hi = min(nb, b_lo + G);
-    const uint32_t nmine = (b_hi - b_lo) * nb;  // candidates of this CTA per class
-    const uint32_t warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const uint32_t g = blockIdx.x, ncta = gridDim.x, per_band = nb / cpc;
+    const uint32_t first = g * cpc, nslot = mode ? 2 * cpc : cpc;
+    const uint32_t warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    for (uint32_t s = 0; s < 64; ++s) {
-        const uint32_t kappa = mode ? swap_kappa(seed, pass_t, s, M) : 0;
-        for (uint32_t j = warp; j < nmine; j += nwarps) {
-            const uint32_t m = b_lo * nb + j;
-            const uint32_t p = class_pixel(L, seed, pass_t, s, m);
-            const uint32_t mm = m ^ kappa, p2 = mode ? class_pixel(L, seed, pass_t, s, mm) : p;
-            WinTerms<R> A, B;
-            A.load(d0, d1, p);
-            if (mode) B.load(d0, d1, p2);
-            // wait for the CTAs owning the bands around p (and p2): progress >= s
-            if (lane == 0 && s > 0) {
-                const uint32_t bs[2] = {m / nb, mm / nb};
-                for (int t = 0; t < (mode ? 2 : 1); ++t)
-                    for (int db = -1; db <= 1; ++db) {
-                        const uint32_t bb = (bs[t] + nb + db) % nb, owner = bb / G;
-                        if (owner == g) continue;
-                        while (ld_acquire(progress + owner) < (int)s) __nanosleep(32);
-                    }
-            }
-            __syncwarp();
-            __threadfence();
-            i128 sum = A.sum(acc, L, p);
-            if (mode) sum += B.sum(acc, L, p2);
-            const i128 dE = 2 * sum;
-            if (lane == 0) {
-                const bool ok = dE < 0;
-                acc[p] = ok;
-                const bool owner_of_couple = !mode || m < mm;
-                dEp[p] = (ok && owner_of_couple) ? dE : (i128)0;
-                if (log) log[(size_t)s * M + m] = ok;
-            }
+    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
+        sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
+    if (mode)
+        for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sKappa[j] = swap_kappa(seed, pass_t, j, M);
+    __syncthreads();
+    auto slot_pixels = [&](uint32_t s, uint32_t* out) {
+        if (threadIdx.x < nslot) {
+            const uint32_t j = threadIdx.x;
+            const uint32_t m = j < cpc ? first + j : ((first + j - cpc) ^ sKappa[s]);
+            out[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
         }
-        // intra-CTA: every warp's class-s decisions (own pixels) are visible before the next
-        // class; then publish progress for the neighbour CTAs.
+    };
+    slot_pixels(0, sSlot[0]);
+    __syncthreads();
+    stage_class<R>(sbase, sSlot[0], nslot, d0, d1);
+    for (uint32_t s = 0; s < 64; ++s) {
+        if (s + 1 < 64) slot_pixels(s + 1, sSlot[(s + 1) & 1]);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        // warp j owns candidate first + j (the launch has exactly cpc warps)
+        const uint32_t j = warp;
+        const uint32_t kappa = mode ? sKappa[s] : 0;
+        const uint32_t m = first + j, mm = m ^ kappa;
+        const uint32_t p = sSlot[s & 1][j], p2 = mode ? sSlot[s & 1][cpc + j] : p;
+        WinTerms<R> A, B;
+        A.load_smem(srows + (size_t)j * 2 * WN);
+        if (mode) B.load_smem(srows + (size_t)(cpc + j) * 2 * WN);
+        __syncthreads();
+        if (s + 1 < 64) stage_class<R>(sbase, sSlot[(s + 1) & 1], nslot, d0, d1);
+        if (lane == 0 && s > 0) {
+            const uint32_t bs[2] = {m / nb, mm / nb};
+            for (int t = 0; t < (mode ? 2 : 1); ++t)
+                for (int db = -1; db <= 1; ++db) {
+                    const uint32_t bb = (bs[t] + nb + db) % nb;
+                    for (uint32_t h = 0; h < per_band; ++h) {
+                        const uint32_t owner = bb * per_band + h;
+                        if (owner == g) continue;
+                        while (ld_acquire(progress + owner) < (int)s) __nanosleep(20);
+                    }
+                }
+        }
+        __syncwarp();
+        __threadfence();
+        i128 sum = A.sum(acc, L, p);
+        if (mode) sum += B.sum(acc, L, p2);
+        const i128 dE = 2 * sum;
+        if (lane == 0) {
+            const bool ok = dE < 0;
+            acc[p] = ok;
+            dEp[p] = (ok && (!mode || m < mm)) ? dE : (i128)0;
+            if (log) log[(size_t)s * M + m] = ok;
+        }
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0 && ncta > 1) st_release(progress + g, (int)s + 1);
+    }
+}
+
+// Cluster decision kernel (tiles with L*L/cpc <= 16 CTAs, i.e. L <= 128): the whole tile's
+// accept flags live in every CTA's shared memory; after deciding class s each CTA pushes its
+// new flags into every other CTA's copy through distributed shared memory (st.shared::cluster)
+// and the cluster barrier (arrive.release / wait.acquire) orders them before class s+1.  No
+// global-memory handshake is on the 64-class critical path.
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_u8(uint32_t local_addr, uint32_t cta, uint8_t v) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(cta));
+    asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(remote), "h"((unsigned short)v) : "memory");
+}
+
+template <int R>
+struct WinTermsLocal : WinTerms<R> {
+    // sum with the flags read from this CTA's shared-memory copy
+    __device__ __forceinline__ i128 sum_local(const uint8_t* sflags, uint32_t L, uint32_t p) const {
+        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
+        const int lane = threadIdx.x & 31;
+        const uint32_t x = p % L, y = p / L;
+        i128 s = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int w = lane + 32 * j;
+            if (w < WN) {
+                const int ww = w >= R * (2 * R + 1) + R ? w + 1 : w;
+                const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
+                const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
+                const longlong2 v = sflags[q] ? this->v1[j] : this->v0[j];
+                s += ((i128)v.y << 64) | (u128)(unsigned long long)v.x;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)s, off);
+            const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(s >> 64), off);
+            s += ((i128)hi << 64) | (u128)lo;
+        }
+        return s;
+    }
+};
+
+template <int R, int mode>
+__global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
+                                                           const longlong2* __restrict__ d0,
+                                                           const longlong2* __restrict__ d1, uint8_t* __restrict__ acc,
+                                                           i128* __restrict__ dEp, uint8_t* __restrict__ log) {
+    constexpr int WN = WinTerms<R>::WN;
+    extern __shared__ __align__(16) uint8_t dsm[];
+    __shared__ uint8_t sDelta[8 * 16];
+    __shared__ uint32_t sKappa[64];
+    __shared__ uint32_t sSlot[2][32];
+    const uint32_t nb = L / 8, M = nb * nb, P = L * L;
+    const uint32_t g = blockIdx.x, ncta = gridDim.x;
+    const uint32_t first = g * cpc, nslot = mode ? 2 * cpc : cpc;
+    const uint32_t rows_bytes = nslot * 2 * WN * 16;
+    uint8_t* sflags = dsm + rows_bytes;  // [P] accept flags of the whole tile (this pass)
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(dsm);
+    const uint32_t sflags_addr = sbase + rows_bytes;
+    const longlong2* srows = reinterpret_cast<const longlong2*>(dsm);
+    const uint32_t warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
+    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
+        sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
+    if (mode)
+        for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sKappa[j] = swap_kappa(seed, pass_t, j, M);
+    __syncthreads();
+    auto slot_pixels = [&](uint32_t s, uint32_t* out) {
+        if (threadIdx.x < nslot) {
+            const uint32_t j = threadIdx.x;
+            const uint32_t m = j < cpc ? first + j : ((first + j - cpc) ^ sKappa[s]);
+            out[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
+        }
+    };
+    slot_pixels(0, sSlot[0]);
+    __syncthreads();
+    stage_class<R>(sbase, sSlot[0], nslot, d0, d1);
+    cluster_sync_all();  // every CTA's flag copy is initialised before any remote store
+    for (uint32_t s = 0; s < 64; ++s) {
+        if (s + 1 < 64) slot_pixels(s + 1, sSlot[(s + 1) & 1]);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        const uint32_t j = warp;
+        const uint32_t kappa = mode ? sKappa[s] : 0;
+        const uint32_t m = first + j, mm = m ^ kappa;
+        const uint32_t p = sSlot[s & 1][j], p2 = mode ? sSlot[s & 1][cpc + j] : p;
+        WinTermsLocal<R> A, B;
+        A.load_smem(srows + (size_t)j * 2 * WN);
+        if (mode) B.load_smem(srows + (size_t)(cpc + j) * 2 * WN);
+        __syncthreads();
+        if (s + 1 < 64) stage_class<R>(sbase, sSlot[(s + 1) & 1], nslot, d0, d1);
+        i128 sum = A.sum_local(sflags, L, p);
+        if (mode) sum += B.sum_local(sflags, L, p2);
+        const bool ok = 2 * sum < 0;
+        if (ok && (uint32_t)lane < ncta) st_cluster_u8(sflags_addr + p, lane, 1);  // incl. own copy
+        if (lane == 0) {
+            acc[p] = ok;
+            dEp[p] = (ok && (!mode || m < mm)) ? 2 * sum : (i128)0;
+            if (log) log[(size_t)s * M + m] = ok;
+        }
+        cluster_sync_all();
     }
 }
 
