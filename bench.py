@@ -250,6 +250,7 @@ def run_ours(args, cfg):
     import torch.distributed as dist
 
     from paper_2105_12620_b200 import bn
+    from paper_2105_12620_b200.dist import max_over_ranks, pairs_of_rank, sum_over_ranks
 
     rank, local, world = dist_env()
     if world != args.gpus:
@@ -264,15 +265,8 @@ def run_ours(args, cfg):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     stream = torch.cuda.current_stream()
-    pair = rank
+    pair = pairs_of_rank(world, rank, world)[0]  # one independent pair tile per rank
     U, (a, b, px, py) = synth.problem_inputs(cfg, pair)
     seed = synth.opt_seed(cfg, pair)
     s = bn.Sampler(local, stream.cuda_stream)
@@ -325,11 +319,7 @@ def run_ours(args, cfg):
            "h2d_bytes_per_step": P * 8 + 24, "d2h_bytes_per_step": P * 8 + 48,
            "path": "bn_set_tile(host) + bn_optimize(1 pass, stats) + bn_get_tile(host) per step"}
 
-    # total launches over all ranks
-    if world > 1:
-        t = torch.tensor([launches], dtype=torch.int64, device="cuda")
-        dist.all_reduce(t)
-        launches = int(t.item())
+    launches = sum_over_ranks(launches)  # total over all ranks
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -129,6 +129,13 @@ typedef struct {
 int bn_optimize(bn_ctx *ctx, const bn_opt_params *params, bn_pass_stats *stats,
                 uint8_t *accept_log);
 
+/* Window distances of the current tile over THIS context's bank shard (no cross-rank sum):
+ * out[(l * P + p) * H + h] = D_l(p, p + o_h) restricted to integrands [t_begin, t_end),
+ * h indexing the half window {o: oy > 0 or (oy == 0 and ox > 0)} ordered oy = 0, ox = 1..R, then
+ * oy = 1..R, ox = -R..R (H = 2R^2 + 2R).  int32, host or device.  Summing the outputs of the
+ * shards of a bank gives the full-bank distances exactly (the multi-GPU decomposition). */
+int bn_window_distances(bn_ctx *ctx, int32_t *out, int is_device);
+
 /* Multi-GPU bank sharding: join an NCCL communicator (ncclUniqueId bytes, 128 B, from rank 0
  * via torch.distributed) of `world` ranks, one context per rank, every rank holding the same
  * tile and its own [t_begin, t_end) shard.  The only exchange is an int32 sum over ranks of

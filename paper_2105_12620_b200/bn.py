@@ -24,7 +24,7 @@ _STATUS = {1: "EINVAL", 2: "ECUDA", 3: "ENCCL", 4: "ENOMEM", 5: "ESTATE"}
 SYMBOLS = ("bn_create", "bn_destroy", "bn_last_error", "bn_version", "bn_set_lattice", "bn_set_bank",
            "bn_get_references", "bn_set_energy", "bn_set_tile", "bn_get_tile", "bn_eval_counts", "bn_energy",
            "bn_optimize", "bn_comm_init", "bn_comm_unique_id", "bn_launch_count", "bn_profile_enable",
-           "bn_profile_get")
+           "bn_profile_get", "bn_window_distances")
 KERNELS = ("counts", "gather", "gram", "lut", "decide", "stats", "commit")
 
 
@@ -75,6 +75,7 @@ def load_library(path: str = LIB_PATH):
         "bn_comm_unique_id": ([vp], ctypes.c_int),
         "bn_launch_count": ([vp], u64),
         "bn_profile_enable": ([vp, ctypes.c_int], ctypes.c_int),
+        "bn_window_distances": ([vp, vp, ctypes.c_int], ctypes.c_int),
         "bn_profile_get": ([vp, u32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -207,6 +208,15 @@ class Sampler:
                                 E_fixed=int(s.E_fixed[0]) | (int(s.E_fixed[1]) << 64),
                                 dE_sum=d - (1 << 128) if d >> 127 else d))
         return out, lg
+
+    def window_distances(self, radius: int = 7, out=None):
+        """Partial (this bank shard) window distances D_l(p, p+o), [levels, P, H] int32."""
+        H = 2 * radius * radius + 2 * radius
+        if out is None:
+            out = np.zeros((len(self.levels), self.L * self.L, H), np.int32)
+        ptr, dev = _ptr(out)
+        self._check(self._lib.bn_window_distances(self._ctx, ptr, dev))
+        return out
 
     def comm_init(self, uid: bytes, rank: int, world: int):
         self._check(self._lib.bn_comm_init(self._ctx, uid, rank, world))

@@ -340,6 +340,32 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
     return BN_OK;
 }
 
+template <int R>
+int launch_gram_only(bn_ctx* ctx) {
+    using S = mma_gram::Shape<R>;
+    const int smem = 2 * S::STAGE;
+    if (!ctx->gram_attr_set[R]) {
+        CUDA_TRY(cudaFuncSetAttribute(k_gram_mma<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        ctx->gram_attr_set[R] = true;
+    }
+    dim3 g2(ctx->L / mma_gram::BX, ctx->L / mma_gram::BY);
+    k_gram_mma<R><<<g2, 32 * mma_gram::WARPS, smem, ctx->stream>>>(ctx->c.p, ctx->c.p, ctx->nc.p, ctx->nc.p, ctx->L,
+                                                                   ctx->Tp, ctx->nl, ctx->Dt.p);
+    LAUNCHED();
+    return BN_OK;
+}
+int gram_only(bn_ctx* ctx) {
+    switch (ctx->R) {
+        case 1: return launch_gram_only<1>(ctx);
+        case 2: return launch_gram_only<2>(ctx);
+        case 3: return launch_gram_only<3>(ctx);
+        case 4: return launch_gram_only<4>(ctx);
+        case 5: return launch_gram_only<5>(ctx);
+        case 6: return launch_gram_only<6>(ctx);
+        default: return launch_gram_only<7>(ctx);
+    }
+}
+
 int gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas) {
     switch (ctx->R) {
         case 1: return launch_gram_lut<1>(ctx, cn, nn, write_deltas);
@@ -839,6 +865,31 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
                 stats[pi].dE_sum[1] = h[pi].dE_sum[1];
             }
         }
+    }
+    return BN_OK;
+}
+
+int bn_window_distances(bn_ctx* ctx, int32_t* out, int is_device) {
+    if (!ctx) return BN_EINVAL;
+    if (!out) return fail(ctx, BN_EINVAL, "null output");
+    DeviceGuard g(ctx->dev);
+    int rc = ensure_work(ctx);
+    if (rc) return rc;
+    if ((rc = gram_only(ctx))) return rc;
+    const size_t n = (size_t)ctx->nl * ctx->P * half_count(ctx->R);
+    int* dst = out;
+    DevBuf<int> tmp;
+    if (!is_device) {
+        CUDA_TRY(tmp.ensure(n));
+        dst = tmp.p;
+    }
+    k_dt_export<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->Dt.p, n, dst);
+    LAUNCHED();
+    if (!is_device) {
+        cudaError_t e = cudaMemcpyAsync(out, dst, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        tmp.release();
+        if (e != cudaSuccess) return fail(ctx, BN_ECUDA, "distances readback: %s", cudaGetErrorString(e));
     }
     return BN_OK;
 }

@@ -970,6 +970,12 @@ __global__ void k_iref(const int2* __restrict__ ab, const uint2* __restrict__ px
     out[i] = 0.5 * twice;
 }
 
+// cc component of Dt [l][p][H] (int4) -> int32 [l][p][H].
+__global__ void k_dt_export(const int4* __restrict__ Dt, size_t n, int* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = Dt[i].x;
+}
+
 // Internal [p][l][Tp] -> C-ABI [l][p][Ts].
 __global__ void k_counts_export(const uint8_t* __restrict__ c, uint32_t P, uint32_t nl, uint32_t Tp, uint32_t Ts,
                                 uint8_t* __restrict__ out) {

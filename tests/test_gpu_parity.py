@@ -9,7 +9,7 @@ multiple of the 128-integrand padding); full BASELINE sizes are checked on sampl
 import numpy as np
 import pytest
 
-import synth
+import synth  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -172,3 +172,32 @@ def test_c3_full_size_sampled(bn, oracle_mod):
     assert np.array_equal(lg[0, :2], lgo[0, :2])
     assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"] and st[0]["dE_sum"] < 0
     assert s.energy()[0] == st[0]["E_fixed"]
+
+
+# ------------------------------------------------------------- bank-shard decomposition (C5)
+def test_window_distances_and_shard_decomposition(bn, oracle_mod):
+    """The multi-GPU (C5) exchange sums partial window distances over bank shards.  On one GPU:
+    the full-bank distances equal the plain definition on the oracle's counts, and the shard
+    contexts' partial distances (T split 3 ways, ragged) add up to them exactly."""
+    from paper_2105_12620_b200.dist import shard_range
+    from tests.test_dist_cpu import _partial_distances
+
+    L, T, levels = 32, 301, (4, 16)
+    a, b, px, py = synth.make_bank(T, 21)
+    U = synth.make_tile(L, 22)
+    full, o, _ = make(bn, oracle_mod, L, T, levels, bank=(a, b, px, py), U=U)
+    Df = full.window_distances()
+    co = o.counts(U)
+    for li in range(len(levels)):
+        assert np.array_equal(Df[li], _partial_distances(co[li], L))
+    acc = np.zeros_like(Df)
+    for r in range(3):
+        t0, t1 = shard_range(T, r, 3)
+        s = bn.Sampler(0)
+        s.set_lattice(synth.D1, synth.D2, levels)
+        s.set_bank(a, b, px, py, t0, t1)
+        s.set_energy(2.1, 1.0, 7)
+        s.set_tile(L, U)
+        assert np.array_equal(s.eval_counts(), co[:, :, t0:t1])
+        acc += s.window_distances()
+    assert np.array_equal(acc, Df)
