@@ -675,15 +675,21 @@ struct WinTerms {
 };
 
 // Stage the dE-term rows (delta0, delta1) of the candidates of CTA `g` for class s into smem.
-// Slot j holds candidate m = first + j (and, for SWAP, slot cpc + j its partner's rows).
+// Slot j holds candidate m = first + j (and, for SWAP, slot cpc + j its partner's rows); warp w
+// copies slots w, w + nwarps, ... (row = WN delta0 terms then WN delta1 terms, 16 B each).
 template <int R>
 __device__ __forceinline__ void stage_class(uint32_t smem_base, const uint32_t* slot_pix, uint32_t nslot,
                                             const longlong2* __restrict__ d0, const longlong2* __restrict__ d1) {
     constexpr int WN = WinTerms<R>::WN;
-    for (uint32_t j = threadIdx.x; j < nslot * 2 * WN; j += blockDim.x) {
-        const uint32_t slot = j / (2 * WN), e = j - slot * 2 * WN, tab = e >= (uint32_t)WN, w = e - tab * WN;
-        const longlong2* src = (tab ? d1 : d0) + (size_t)slot_pix[slot] * WN + w;
-        cp_async16(smem_base + (slot * 2 * WN + e) * 16, src);
+    const uint32_t warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t slot = warp; slot < nslot; slot += nwarps) {
+        const size_t off = (size_t)slot_pix[slot] * WN;
+        const uint32_t dst = smem_base + slot * 2 * WN * 16;
+#pragma unroll
+        for (uint32_t w = lane; w < (uint32_t)WN; w += 32) {
+            cp_async16(dst + w * 16, d0 + off + w);
+            cp_async16(dst + (WN + w) * 16, d1 + off + w);
+        }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -783,32 +789,52 @@ __device__ __forceinline__ void st_cluster_u8(uint32_t local_addr, uint32_t cta,
     asm volatile("st.shared::cluster.u8 [%0], %1;" ::"r"(remote), "h"((unsigned short)v) : "memory");
 }
 
+// Per-lane window offsets (oy, ox) of the lane's terms w = lane + 32 j, computed once.
 template <int R>
-struct WinTermsLocal : WinTerms<R> {
-    // sum with the flags read from this CTA's shared-memory copy
-    __device__ __forceinline__ i128 sum_local(const uint8_t* sflags, uint32_t L, uint32_t p) const {
-        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
+struct LaneOffsets {
+    static constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
+    int oy[PER], ox[PER];
+    __device__ __forceinline__ void init() {
         const int lane = threadIdx.x & 31;
-        const uint32_t x = p % L, y = p / L;
-        i128 s = 0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int w = lane + 32 * j;
-            if (w < WN) {
-                const int ww = w >= R * (2 * R + 1) + R ? w + 1 : w;
-                const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
-                const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
+            const int ww = w >= R * (2 * R + 1) + R ? w + 1 : w;
+            oy[j] = w < WN ? ww / (2 * R + 1) - R : 0;
+            ox[j] = w < WN ? ww % (2 * R + 1) - R : 0;
+        }
+    }
+};
+
+template <int R>
+struct WinTermsLocal : WinTerms<R> {
+    // sum with the flags read from this CTA's shared-memory copy
+    __device__ __forceinline__ i128 sum_local(const uint8_t* sflags, uint32_t L, uint32_t p,
+                                              const LaneOffsets<R>& off) const {
+        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
+        const int lane = threadIdx.x & 31;
+        const uint32_t x = p & (L - 1), y = p / L;
+        unsigned long long lo = 0;
+        long long hi = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            if (lane + 32 * j < WN) {
+                const uint32_t q = ((y + off.oy[j]) & (L - 1)) * L + ((x + off.ox[j]) & (L - 1));
                 const longlong2 v = sflags[q] ? this->v1[j] : this->v0[j];
-                s += ((i128)v.y << 64) | (u128)(unsigned long long)v.x;
+                const unsigned long long nlo = lo + (unsigned long long)v.x;
+                hi += v.y + (nlo < lo);
+                lo = nlo;
             }
         }
 #pragma unroll
-        for (int off = 16; off; off >>= 1) {
-            const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)s, off);
-            const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(s >> 64), off);
-            s += ((i128)hi << 64) | (u128)lo;
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
+            const long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+            const unsigned long long nlo = lo + olo;
+            hi += ohi + (nlo < lo);
+            lo = nlo;
         }
-        return s;
+        return ((i128)hi << 64) | (u128)lo;
     }
 };
 
@@ -848,6 +874,8 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
     slot_pixels(0, sSlot[0]);
     __syncthreads();
     stage_class<R>(sbase, sSlot[0], nslot, d0, d1);
+    LaneOffsets<R> off;
+    off.init();
     cluster_sync_all();  // every CTA's flag copy is initialised before any remote store
     for (uint32_t s = 0; s < 64; ++s) {
         if (s + 1 < 64) slot_pixels(s + 1, sSlot[(s + 1) & 1]);
@@ -862,16 +890,17 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
         if (mode) B.load_smem(srows + (size_t)(cpc + j) * 2 * WN);
         __syncthreads();
         if (s + 1 < 64) stage_class<R>(sbase, sSlot[(s + 1) & 1], nslot, d0, d1);
-        i128 sum = A.sum_local(sflags, L, p);
-        if (mode) sum += B.sum_local(sflags, L, p2);
+        i128 sum = A.sum_local(sflags, L, p, off);
+        if (mode) sum += B.sum_local(sflags, L, p2, off);
         const bool ok = 2 * sum < 0;
         if (ok && (uint32_t)lane < ncta) st_cluster_u8(sflags_addr + p, lane, 1);  // incl. own copy
-        if (lane == 0) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        if (lane == 0) {  // bookkeeping for commit/stats: not needed by other CTAs in this kernel
             acc[p] = ok;
             dEp[p] = (ok && (!mode || m < mm)) ? 2 * sum : (i128)0;
             if (log) log[(size_t)s * M + m] = ok;
         }
-        cluster_sync_all();
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
 }
 
