@@ -107,6 +107,8 @@ struct bn_ctx {
     DevBuf<i128> dEp;
     DevBuf<u128> Epart;
     DevBuf<PassStatsDev> pstats;
+    DevBuf<FinishPart> fparts;
+    DevBuf<unsigned int> ticket;
     DevBuf<double> W, G, iref;
     size_t Goff[8] = {0};
     int Dmax[8] = {0};
@@ -333,9 +335,11 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
     }
     const size_t nthr = (size_t)ctx->P * half_count(R);
     KSTART(BN_K_LUT);
-    k_lut<R><<<(unsigned)((nthr + 255) / 256), 256, 0, ctx->ls>>>(ctx->Dt.p, ctx->L, ctx->nl, ctx->W.p, la,
-                                                                      write_deltas, ctx->d0.p, ctx->d1b.p,
-                                                                      ctx->Epart.p, ctx->derr.p);
+    {
+        auto fn = ctx->nl == 4 ? k_lut<R, 4> : ctx->nl == 1 ? k_lut<R, 1> : k_lut<R, 0>;
+        fn<<<(unsigned)((nthr + 255) / 256), 256, 0, ctx->ls>>>(ctx->Dt.p, ctx->L, ctx->nl, ctx->W.p, la, write_deltas,
+                                                              ctx->d0.p, ctx->d1b.p, ctx->Epart.p, ctx->derr.p);
+    }
     LAUNCHED_K();
     return BN_OK;
 }
@@ -571,7 +575,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->S.release(); ctx->U.release(); ctx->Un.release(); ctx->pxy.release(); ctx->ab.release();
         ctx->Cc.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
         ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
-        ctx->d0.release(); ctx->d1b.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release();
+        ctx->d0.release(); ctx->d1b.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
         ctx->W.release(); ctx->G.release(); ctx->iref.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release();
@@ -769,6 +773,14 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     const int R = ctx->R;
     const uint32_t nE = (uint32_t)(((size_t)P * half_count(R) + 255) / 256);
     CUDA_TRY(ctx->pstats.ensure(prm->passes));
+    int nsm_fin = 148;
+    cudaDeviceGetAttribute(&nsm_fin, cudaDevAttrMultiProcessorCount, ctx->dev);
+    const uint32_t nfin = (uint32_t)(2 * nsm_fin) < P / 16 ? (uint32_t)(2 * nsm_fin) : (P / 16);
+    if (!ctx->ticket.p) {
+        CUDA_TRY(ctx->ticket.ensure(1));
+        CUDA_TRY(cudaMemsetAsync(ctx->ticket.p, 0, sizeof(unsigned int), ctx->stream));
+    }
+    CUDA_TRY(ctx->fparts.ensure(nfin));
     if (accept_log) CUDA_TRY(ctx->log.ensure((size_t)prm->passes * 64 * M));
     CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
     const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
@@ -833,13 +845,11 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             ctx->ls = ctx->stream;
             CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evB, 0));
         }
-        KSTART(BN_K_STATS);
-        k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, ctx->dEp.p, ctx->acc.p, P,
-                                                  prm->mode == BN_SWAP, ctx->pstats.p + pi);
-        LAUNCHED_K();
         KSTART(BN_K_COMMIT);
-        k_commit<<<P, 128, 0, ctx->stream>>>(ctx->acc.p, P, ctx->rowB, nl, buf_U(pi), ctx->U.p, buf_c(pi), ctx->c.p,
-                                             buf_n(pi), ctx->nc.p);
+        k_finish<<<nfin, 256, 0, ctx->stream>>>(ctx->acc.p, P, ctx->rowB, nl, buf_U(pi), ctx->U.p, buf_c(pi),
+                                                 ctx->c.p, buf_n(pi), ctx->nc.p, ctx->Epart.p, nE, ctx->dEp.p,
+                                                 prm->mode == BN_SWAP, ctx->fparts.p, ctx->ticket.p,
+                                                 ctx->pstats.p + pi);
         LAUNCHED_K();
     }
     ctx->ls = ctx->stream;

@@ -482,8 +482,9 @@ struct LutArgs {
     int Dmax[8];         // largest legal D per level (guards corrupted distances)
 };
 
-template <int R>
-__global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32_t L, uint32_t nl,
+// NL > 0: compile-time level count (all distance loads issued up front); NL = 0: runtime nl.
+template <int R, int NL>
+__global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32_t L, uint32_t nl_rt,
                                              const double* __restrict__ W, LutArgs lut, int write_deltas,
                                              longlong2* __restrict__ d0, longlong2* __restrict__ d1,
                                              u128* __restrict__ Epart, int* __restrict__ err) {
@@ -507,8 +508,15 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
         const int wi = win_index(ox, oy, R), wm = win_index(-ox, -oy, R);
         const double w = W[wi];
         i128 a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+        const uint32_t nl = NL ? NL : nl_rt;
+        int4 Dv[NL ? NL : 1];
+        if (NL) {
+#pragma unroll
+            for (int l = 0; l < (NL ? NL : 1); ++l) Dv[l] = Dt[(size_t)l * P * H + idx];
+        }
+#pragma unroll
         for (uint32_t l = 0; l < nl; ++l) {
-            const int4 D = Dt[(size_t)l * P * H + idx];
+            const int4 D = NL ? Dv[NL ? l : 0] : Dt[(size_t)l * P * H + idx];
             const int dm = lut.Dmax[l];
             if ((unsigned)D.x > (unsigned)dm || (unsigned)D.y > (unsigned)dm || (unsigned)D.z > (unsigned)dm ||
                 (unsigned)D.w > (unsigned)dm) {
@@ -961,6 +969,94 @@ __global__ void __launch_bounds__(1024) k_pass_stats(const u128* __restrict__ Ep
         out->dE_sum[0] = (unsigned long long)D;
         out->dE_sum[1] = (unsigned long long)(D >> 64);
         out->accepted = swap_mode ? A / 2 : A;
+    }
+}
+
+// Pass epilogue in one grid: commit accepted rows / shifts / norms, and the exact pass sums
+// (E_before = sum Epart, dE_sum = sum dEp, accepted = sum acc) as per-block partials that the
+// last block to finish (atomic ticket) reduces into `out`; the ticket is reset for the next use.
+struct FinishPart {
+    unsigned long long e[2], d[2];
+    unsigned int a, pad[3];
+};
+__global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc, uint32_t P, uint32_t rowB,
+                                                uint32_t nl, const uint2* __restrict__ Un, uint2* __restrict__ U,
+                                                const uint8_t* __restrict__ cn, uint8_t* __restrict__ c,
+                                                const int* __restrict__ nn, int* __restrict__ nc,
+                                                const u128* __restrict__ Epart, uint32_t nEpart,
+                                                const i128* __restrict__ dEp, int swap_mode,
+                                                FinishPart* __restrict__ parts, unsigned int* __restrict__ ticket,
+                                                PassStatsDev* __restrict__ out) {
+    const uint32_t nblk = gridDim.x, b = blockIdx.x;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const uint32_t p0 = (uint32_t)((uint64_t)P * b / nblk), p1 = (uint32_t)((uint64_t)P * (b + 1) / nblk);
+    // commit: one warp per accepted pixel
+    for (uint32_t p = p0 + warp; p < p1; p += nw) {
+        if (!acc[p]) continue;
+        const uint4* src = reinterpret_cast<const uint4*>(cn + (size_t)p * rowB);
+        uint4* dst = reinterpret_cast<uint4*>(c + (size_t)p * rowB);
+        for (uint32_t j = lane; j < rowB / 16; j += 32) dst[j] = src[j];
+        if (lane == 0) U[p] = Un[p];
+        if (lane < nl) nc[(size_t)p * nl + lane] = nn[(size_t)p * nl + lane];
+    }
+    // exact partial sums
+    u128 e = 0;
+    i128 d = 0;
+    unsigned a = 0;
+    const uint32_t e0 = (uint32_t)((uint64_t)nEpart * b / nblk), e1 = (uint32_t)((uint64_t)nEpart * (b + 1) / nblk);
+    for (uint32_t j = e0 + threadIdx.x; j < e1; j += blockDim.x) e += Epart[j];
+    for (uint32_t j = p0 + threadIdx.x; j < p1; j += blockDim.x) {
+        d += dEp[j];
+        a += acc[j];
+    }
+    __shared__ unsigned long long s_e[256][2], s_d[256][2];
+    __shared__ unsigned int s_a[256];
+    __shared__ bool last;
+    s_e[threadIdx.x][0] = (unsigned long long)e;
+    s_e[threadIdx.x][1] = (unsigned long long)(e >> 64);
+    s_d[threadIdx.x][0] = (unsigned long long)(u128)d;
+    s_d[threadIdx.x][1] = (unsigned long long)((u128)d >> 64);
+    s_a[threadIdx.x] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u128 E = 0, D = 0;
+        unsigned A = 0;
+        for (int j = 0; j < (int)blockDim.x; ++j) {
+            E += ((u128)s_e[j][1] << 64) | s_e[j][0];
+            D += ((u128)s_d[j][1] << 64) | s_d[j][0];
+            A += s_a[j];
+        }
+        FinishPart fp;
+        fp.e[0] = (unsigned long long)E;
+        fp.e[1] = (unsigned long long)(E >> 64);
+        fp.d[0] = (unsigned long long)D;
+        fp.d[1] = (unsigned long long)(D >> 64);
+        fp.a = A;
+        parts[b] = fp;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == nblk - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        u128 E = 0, D = 0;
+        unsigned A = 0;
+        for (uint32_t j = 0; j < nblk; ++j) {
+            const FinishPart fp = parts[j];
+            E += ((u128)fp.e[1] << 64) | fp.e[0];
+            D += ((u128)fp.d[1] << 64) | fp.d[0];
+            A += fp.a;
+        }
+        const u128 Ea = E + D;
+        out->E_before[0] = (unsigned long long)E;
+        out->E_before[1] = (unsigned long long)(E >> 64);
+        out->E_after[0] = (unsigned long long)Ea;
+        out->E_after[1] = (unsigned long long)(Ea >> 64);
+        out->dE_sum[0] = (unsigned long long)D;
+        out->dE_sum[1] = (unsigned long long)(D >> 64);
+        out->accepted = swap_mode ? A / 2 : A;
+        *ticket = 0;
     }
 }
 
