@@ -325,7 +325,7 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
     }
     if (ctx->comm) {
         const size_t n = (size_t)ctx->P * half_count(R) * ctx->nl * 4;
-        int r = g_nccl.allreduce(ctx->Dt.p, ctx->Dt.p, n, NCCL_INT32, NCCL_SUM, ctx->comm, ctx->stream);
+        int r = g_nccl.allreduce(ctx->Dt.p, ctx->Dt.p, n, NCCL_INT32, NCCL_SUM, ctx->comm, ctx->ls);
         if (r) return fail(ctx, BN_ENCCL, "ncclAllReduce: %s", g_nccl.errstr(r));
     }
     LutArgs la;
@@ -805,52 +805,57 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         LAUNCHED_K();
         return BN_OK;
     };
+    // With overlap, the whole critical path (gram, energy terms, decisions, finish) runs on the
+    // internal highest-priority stream `hp` and only the next pass's candidate counts run on the
+    // lowest-priority `aux` stream; pending hp CTAs are dispatched first.  Both join the caller's
+    // stream at the end.
+    cudaStream_t cs = ctx->stream;
+    if (overlap) {
+        CUDA_TRY(cudaEventRecord(ctx->evA, ctx->stream));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->hp, ctx->evA, 0));
+        cs = ctx->hp;
+    }
     for (uint32_t pi = 0; pi < prm->passes; ++pi) {
         const uint32_t t = prm->first_pass + pi;
-        ctx->ls = ctx->stream;
-        CUDA_TRY(cudaMemsetAsync(ctx->acc.p, 0, P, ctx->stream));
+        ctx->ls = cs;
+        CUDA_TRY(cudaMemsetAsync(ctx->acc.p, 0, P, cs));
         if (prm->mode == BN_REDRAW) {
             if (overlap && pi > 0) {
-                CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evC, 0));  // prefetched by pass pi-1
+                CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evC, 0));  // prefetched during pass pi-1
             } else if ((rc = launch_counts(pi))) {
                 return rc;
             }
         } else {
             KSTART(BN_K_GATHER);
-            k_swap_gather<<<64 * M, 128, 0, ctx->stream>>>(ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p, ctx->nc.p,
-                                                          ctx->nn.p, ctx->L, prm->seed, t, ctx->rowB, nl);
+            k_swap_gather<<<64 * M, 128, 0, cs>>>(ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p, ctx->nc.p, ctx->nn.p,
+                                                 ctx->L, prm->seed, t, ctx->rowB, nl);
             LAUNCHED_K();
         }
         if ((rc = gram_lut(ctx, buf_c(pi), buf_n(pi), 1))) return rc;
-        uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
-        if (overlap) {
-            // decisions on hp, next candidates on aux, both after this pass's energy terms
-            CUDA_TRY(cudaEventRecord(ctx->evA, ctx->stream));
-            CUDA_TRY(cudaStreamWaitEvent(ctx->hp, ctx->evA, 0));
-            ctx->ls = ctx->hp;
+        if (overlap && pi + 1 < prm->passes) {
+            // next pass's candidates: their buffer was last read by finish(pi-1), already done on cs
+            CUDA_TRY(cudaEventRecord(ctx->evB, cs));
+            CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->evB, 0));
+            ctx->ls = ctx->aux;
+            if ((rc = launch_counts(pi + 1))) return rc;
+            CUDA_TRY(cudaEventRecord(ctx->evC, ctx->aux));
+            ctx->ls = cs;
         }
+        uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
         bool done = false;
         if (!ctx->per_class_decide && (rc = decide_pass(ctx, t, prm->seed, (int)prm->mode, log, &done))) return rc;
         if (!done)
             for (uint32_t s = 0; s < 64; ++s)
                 if ((rc = decide(ctx, s, t, prm->seed, (int)prm->mode, log))) return rc;
-        if (overlap) {
-            CUDA_TRY(cudaEventRecord(ctx->evB, ctx->hp));
-            if (pi + 1 < prm->passes) {
-                CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->evA, 0));
-                ctx->ls = ctx->aux;
-                if ((rc = launch_counts(pi + 1))) return rc;
-                CUDA_TRY(cudaEventRecord(ctx->evC, ctx->aux));
-            }
-            ctx->ls = ctx->stream;
-            CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evB, 0));
-        }
         KSTART(BN_K_COMMIT);
-        k_finish<<<nfin, 256, 0, ctx->stream>>>(ctx->acc.p, P, ctx->rowB, nl, buf_U(pi), ctx->U.p, buf_c(pi),
-                                                 ctx->c.p, buf_n(pi), ctx->nc.p, ctx->Epart.p, nE, ctx->dEp.p,
-                                                 prm->mode == BN_SWAP, ctx->fparts.p, ctx->ticket.p,
-                                                 ctx->pstats.p + pi);
+        k_finish<<<nfin, 256, 0, cs>>>(ctx->acc.p, P, ctx->rowB, nl, buf_U(pi), ctx->U.p, buf_c(pi), ctx->c.p,
+                                        buf_n(pi), ctx->nc.p, ctx->Epart.p, nE, ctx->dEp.p, prm->mode == BN_SWAP,
+                                        ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi);
         LAUNCHED_K();
+    }
+    if (overlap) {
+        CUDA_TRY(cudaEventRecord(ctx->evB, cs));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evB, 0));
     }
     ctx->ls = ctx->stream;
     if (stats || accept_log) {

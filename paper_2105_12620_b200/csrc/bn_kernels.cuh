@@ -83,7 +83,7 @@ __host__ __device__ __forceinline__ int half_index(int ox, int oy, int R) {
 // i.e. two 32x32->64 integer multiply-adds per (pixel, integrand, sample): exact.
 // Padding integrands (i >= Ts) use a = b = 0, C = 1, so they always count 0.
 // Layout out: [p][l][Tp] uint8; norms: [p][l] int32 = sum_i c^2.
-constexpr int COUNT_PIX = 8;  // pixels per CTA
+constexpr int COUNT_PIX = 4;  // pixels per CTA (short CTAs co-schedule well on the aux stream)
 
 // Filtered fast test.  t = fma(a, x', fma(b, y', -C)) in fp32 with x' = fl(X'), C~ = fl(C):
 //   |x' - X'| <= 2^6, |C~ - C| <= 2^24, |a|,|b| <= 2^15, |b y' - C~| < 2^49
@@ -93,30 +93,28 @@ constexpr int COUNT_PIX = 8;  // pixels per CTA
 constexpr float COUNT_EXACT_BAND = 134217728.0f;  // 2^27
 
 template <int NI>
+__device__ __forceinline__ void count_sample(float2 xy, const float* af, const float* bf, const float* cf,
+                                             uint32_t* neg, float* mn) {
+    float t[NI];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+        t[j] = fmaf(af[j], xy.x, fmaf(bf[j], xy.y, cf[j]));
+        neg[j] += __float_as_uint(t[j]) >> 31;  // LEA.HI
+    }
+    // running min of |t| over pairs of integrands: one FMNMX3 per two tests
+#pragma unroll
+    for (int j = 0; j < NI; j += 2) mn[j >> 1] = fminf(mn[j >> 1], fminf(fabsf(t[j]), fabsf(t[j + 1])));
+}
+
+template <int NI>
 __device__ __forceinline__ void count_span(const float2* __restrict__ xyf, uint32_t k0, uint32_t k1, const float* af,
                                            const float* bf, const float* cf, uint32_t* neg, float* mn) {
     uint32_t k = k0;
     for (; k + 4 <= k1; k += 4) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float2 xy = xyf[k + u];
-#pragma unroll
-            for (int j = 0; j < NI; ++j) {
-                const float t = fmaf(af[j], xy.x, fmaf(bf[j], xy.y, cf[j]));
-                neg[j] += __float_as_uint(t) >> 31;
-                mn[j] = fminf(mn[j], fabsf(t));
-            }
-        }
+        for (int u = 0; u < 4; ++u) count_sample<NI>(xyf[k + u], af, bf, cf, neg, mn);
     }
-    for (; k < k1; ++k) {
-        const float2 xy = xyf[k];
-#pragma unroll
-        for (int j = 0; j < NI; ++j) {
-            const float t = fmaf(af[j], xy.x, fmaf(bf[j], xy.y, cf[j]));
-            neg[j] += __float_as_uint(t) >> 31;
-            mn[j] = fminf(mn[j], fabsf(t));
-        }
-    }
+    for (; k < k1; ++k) count_sample<NI>(xyf[k], af, bf, cf, neg, mn);
 }
 
 // Each thread owns NI = 8 consecutive integrands (two packed 32-bit words per level row) and
@@ -135,19 +133,25 @@ __global__ void __launch_bounds__(256, 3) k_counts(const uint2* __restrict__ U, 
     __shared__ int sNorm[COUNT_PIX][8];
     const uint32_t levels[8] = {lev_lo.x, lev_lo.y, lev_lo.z, lev_lo.w, lev_hi.x, lev_hi.y, lev_hi.z, lev_hi.w};
     const uint32_t p0 = blockIdx.x * COUNT_PIX;
+    __shared__ uint2 sU[COUNT_PIX];
     for (uint32_t j = threadIdx.x; j < COUNT_PIX * 8; j += blockDim.x) (&sNorm[0][0])[j] = 0;
-    for (uint32_t j = threadIdx.x; j < COUNT_PIX * Nmax; j += blockDim.x) {
-        const uint32_t pp = j / Nmax, k = j - pp * Nmax, p = p0 + pp;
-        if (p >= P) continue;
+    if (threadIdx.x < COUNT_PIX && p0 + threadIdx.x < P) {  // one shift (one Philox draw) per pixel
+        const uint32_t p = p0 + threadIdx.x;
         uint2 u;
         if (redraw) {
             const uint4 r = philox_seeded(seed, p, pass_t, 0, 1);
             u = make_uint2(r.x, r.y);
-            if (k == 0) Uout[p] = u;
+            Uout[p] = u;
         } else {
             u = U[p];
         }
-        const uint2 s = S[k];
+        sU[threadIdx.x] = u;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < COUNT_PIX * Nmax; j += blockDim.x) {
+        const uint32_t pp = j / Nmax, k = j - pp * Nmax;
+        if (p0 + pp >= P) continue;
+        const uint2 u = sU[pp], s = S[k];
         const int2 xy = make_int2((int)((s.x + u.x) ^ 0x80000000u), (int)((s.y + u.y) ^ 0x80000000u));
         sXY[pp][k] = xy;
         sXYf[pp][k] = make_float2(__int2float_rn(xy.x), __int2float_rn(xy.y));
@@ -171,12 +175,11 @@ __global__ void __launch_bounds__(256, 3) k_counts(const uint2* __restrict__ U, 
             const uint32_t p = p0 + pp;
             if (p >= P) break;
             uint32_t neg[NI];
-            float mn[NI];
+            float mn[NI / 2];  // min |t| per pair of integrands
 #pragma unroll
-            for (int j = 0; j < NI; ++j) {
-                neg[j] = 0;
-                mn[j] = 3.0e38f;
-            }
+            for (int j = 0; j < NI; ++j) neg[j] = 0;
+#pragma unroll
+            for (int j = 0; j < NI / 2; ++j) mn[j] = 3.0e38f;
             uint8_t* orow = out + (size_t)p * nl * Tp + NI * q;
             uint32_t kprev = 0;
             for (uint32_t li = 0; li < nl; ++li) {
@@ -190,17 +193,15 @@ __global__ void __launch_bounds__(256, 3) k_counts(const uint2* __restrict__ U, 
                     const uint32_t c0 = n1 - neg[4 * h], c1 = n1 - neg[4 * h + 1];
                     const uint32_t c2 = n1 - neg[4 * h + 2], c3 = n1 - neg[4 * h + 3];
                     w[h] = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
-                    nsq += c0 * c0 + c1 * c1 + c2 * c2 + c3 * c3;
+                    nsq = __dp4a(w[h], w[h], nsq);  // sum of the four squared counts
                 }
                 *reinterpret_cast<uint2*>(orow + (size_t)li * Tp) = make_uint2(w[0], w[1]);
-#pragma unroll
-                for (int off = 16; off; off >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, off);
-                if ((threadIdx.x & 31) == 0) atomicAdd(&sNorm[pp][li], (int)nsq);
+                atomicAdd(&sNorm[pp][li], (int)nsq);
             }
             // exact int64 recount of any integrand whose samples came within the error band
 #pragma unroll
             for (int j = 0; j < NI; ++j) {
-                if (mn[j] >= COUNT_EXACT_BAND) continue;
+                if (mn[j >> 1] >= COUNT_EXACT_BAND) continue;  // exact recount of both of the pair
                 const int2 abj = ab[NI * q + j];
                 const long long cj = Cc[NI * q + j];
                 uint32_t cnt = 0, lj = 0, nx = levels[0];
@@ -225,8 +226,7 @@ __global__ void __launch_bounds__(256, 3) k_counts(const uint2* __restrict__ U, 
         if (p0 + pp < P) norms[(size_t)(p0 + pp) * nl + l] = sNorm[pp][l];
     }
 }
-// The warp shuffle in k_counts needs all 32 lanes of a warp in the q loop together: Tp / 8 must
-// be a multiple of 32, i.e. callers guarantee Tp % 256 == 0.
+// Tp / 8 integrand groups per pixel: callers guarantee Tp % 256 == 0 (whole warps per group).
 
 // SWAP candidates: cn_p = c_partner(p), Un_p = U_partner(p), for every (class s, index m).
 __global__ void k_swap_gather(const uint2* __restrict__ U, uint2* __restrict__ Un, const uint8_t* __restrict__ c,
@@ -441,10 +441,18 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma(const uint8_t* __restrict__
             }
             __syncthreads();
         }
-        // epilogue: exact distances from the dot products and the row norms
+        // epilogue: exact distances from the dot products and the row norms (norms of the staged
+        // neighbourhood are put in shared memory once per level; the operand buffers are free now)
+        int* snorm = reinterpret_cast<int*>(smem);  // [2][NROW][NCOL]
+        for (int j = threadIdx.x; j < 2 * S::NROW * S::NCOL; j += blockDim.x) {
+            const int col = j % S::NCOL, vr = j / S::NCOL, r = vr % S::NROW, v = vr / S::NROW;
+            const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
+            snorm[j] = (v ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
+        }
+        __syncthreads();
         const int g = lane >> 2, tq = lane & 3;
         const uint32_t px = x0 + xs + g, py = y0 + sj, p = py * L + px;
-        const int ncp = nc[(size_t)p * nl + l], nnp = nn[(size_t)p * nl + l];
+        const int ncp = snorm[sj * S::NCOL + R + xs + g], nnp = snorm[(S::NROW + sj) * S::NCOL + R + xs + g];
         int4* out = Dt + ((size_t)l * L * L + p) * S::H;
 #pragma unroll
         for (int a_oy = 0; a_oy < S::OYG; ++a_oy) {
@@ -456,8 +464,8 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma(const uint8_t* __restrict__
                 for (int e = 0; e < 2; ++e) {
                     const int n = 8 * t + 2 * tq + e, ox = n - R - g;
                     if (ox < -R || ox > R || (oy == 0 && ox <= 0)) continue;
-                    const uint32_t q = ((py + oy) & (L - 1)) * L + ((px + ox + L) & (L - 1));
-                    const int ncq = __ldg(nc + (size_t)q * nl + l), nnq = __ldg(nn + (size_t)q * nl + l);
+                    const int qc = (sj + oy) * S::NCOL + xs + n;  // staged neighbour (row, column)
+                    const int ncq = snorm[qc], nnq = snorm[S::NROW * S::NCOL + qc];
                     int4 d;
                     d.x = ncp + ncq - 2 * acc[a_oy][t][0][e];
                     d.y = nnp + ncq - 2 * acc[a_oy][t][0][2 + e];
@@ -466,6 +474,7 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma(const uint8_t* __restrict__
                     out[half_index(ox, oy, R)] = d;
                 }
         }
+        __syncthreads();  // snorm aliases the operand buffers of the next level
     }
 }
 
