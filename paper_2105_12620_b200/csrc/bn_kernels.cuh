@@ -984,10 +984,59 @@ __global__ void __launch_bounds__(1024) k_pass_stats(const u128* __restrict__ Ep
 // Pass epilogue in one grid: commit accepted rows / shifts / norms, and the exact pass sums
 // (E_before = sum Epart, dE_sum = sum dEp, accepted = sum acc) as per-block partials that the
 // last block to finish (atomic ticket) reduces into `out`; the ticket is reset for the next use.
+// Exact block-wide sums with 64-bit carries (warp shuffles, then warp 0 over the warps).
+__device__ __forceinline__ u128 warp_sum_u128(u128 v) {
+    unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
+        const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+        const unsigned long long nlo = lo + olo;
+        hi += ohi + (nlo < lo);
+        lo = nlo;
+    }
+    return ((u128)hi << 64) | lo;
+}
 struct FinishPart {
     unsigned long long e[2], d[2];
     unsigned int a, pad[3];
 };
+__device__ __forceinline__ FinishPart block_sum_parts(u128 e, u128 d, unsigned a, FinishPart* s_w) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    e = warp_sum_u128(e);
+    d = warp_sum_u128(d);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) {
+        s_w[warp].e[0] = (unsigned long long)e;
+        s_w[warp].e[1] = (unsigned long long)(e >> 64);
+        s_w[warp].d[0] = (unsigned long long)d;
+        s_w[warp].d[1] = (unsigned long long)(d >> 64);
+        s_w[warp].a = a;
+    }
+    __syncthreads();
+    FinishPart r = {};
+    if (warp == 0) {
+        u128 E = 0, D = 0;
+        unsigned A = 0;
+        if (lane < nw) {
+            E = ((u128)s_w[lane].e[1] << 64) | s_w[lane].e[0];
+            D = ((u128)s_w[lane].d[1] << 64) | s_w[lane].d[0];
+            A = s_w[lane].a;
+        }
+        E = warp_sum_u128(E);
+        D = warp_sum_u128(D);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) A += __shfl_xor_sync(0xffffffffu, A, o);
+        r.e[0] = (unsigned long long)E;
+        r.e[1] = (unsigned long long)(E >> 64);
+        r.d[0] = (unsigned long long)D;
+        r.d[1] = (unsigned long long)(D >> 64);
+        r.a = A;
+    }
+    __syncthreads();  // s_w may be reused by the caller
+    return r;
+}
 __global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc, uint32_t P, uint32_t rowB,
                                                 uint32_t nl, const uint2* __restrict__ Un, uint2* __restrict__ U,
                                                 const uint8_t* __restrict__ cn, uint8_t* __restrict__ c,
@@ -1018,53 +1067,37 @@ __global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc,
         d += dEp[j];
         a += acc[j];
     }
-    __shared__ unsigned long long s_e[256][2], s_d[256][2];
-    __shared__ unsigned int s_a[256];
+    __shared__ FinishPart s_w[32];
     __shared__ bool last;
-    s_e[threadIdx.x][0] = (unsigned long long)e;
-    s_e[threadIdx.x][1] = (unsigned long long)(e >> 64);
-    s_d[threadIdx.x][0] = (unsigned long long)(u128)d;
-    s_d[threadIdx.x][1] = (unsigned long long)((u128)d >> 64);
-    s_a[threadIdx.x] = a;
-    __syncthreads();
+    FinishPart mine = block_sum_parts(e, (u128)d, a, s_w);
     if (threadIdx.x == 0) {
-        u128 E = 0, D = 0;
-        unsigned A = 0;
-        for (int j = 0; j < (int)blockDim.x; ++j) {
-            E += ((u128)s_e[j][1] << 64) | s_e[j][0];
-            D += ((u128)s_d[j][1] << 64) | s_d[j][0];
-            A += s_a[j];
-        }
-        FinishPart fp;
-        fp.e[0] = (unsigned long long)E;
-        fp.e[1] = (unsigned long long)(E >> 64);
-        fp.d[0] = (unsigned long long)D;
-        fp.d[1] = (unsigned long long)(D >> 64);
-        fp.a = A;
-        parts[b] = fp;
+        parts[b] = mine;
         __threadfence();
         last = atomicAdd(ticket, 1u) == nblk - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
+    // the last block reduces all partials in parallel
+    u128 E = 0, D = 0;
+    unsigned A = 0;
+    for (uint32_t j = threadIdx.x; j < nblk; j += blockDim.x) {
+        const unsigned long long* q = reinterpret_cast<const unsigned long long*>(parts + j);
+        E += ((u128)__ldcg(q + 1) << 64) | __ldcg(q + 0);
+        D += ((u128)__ldcg(q + 3) << 64) | __ldcg(q + 2);
+        A += (unsigned)__ldcg(q + 4);
+    }
+    const FinishPart tot = block_sum_parts(E, D, A, s_w);
     if (threadIdx.x == 0) {
-        u128 E = 0, D = 0;
-        unsigned A = 0;
-        for (uint32_t j = 0; j < nblk; ++j) {
-            const FinishPart fp = parts[j];
-            E += ((u128)fp.e[1] << 64) | fp.e[0];
-            D += ((u128)fp.d[1] << 64) | fp.d[0];
-            A += fp.a;
-        }
-        const u128 Ea = E + D;
-        out->E_before[0] = (unsigned long long)E;
-        out->E_before[1] = (unsigned long long)(E >> 64);
+        const u128 Et = ((u128)tot.e[1] << 64) | tot.e[0], Dt = ((u128)tot.d[1] << 64) | tot.d[0];
+        const u128 Ea = Et + Dt;
+        out->E_before[0] = tot.e[0];
+        out->E_before[1] = tot.e[1];
         out->E_after[0] = (unsigned long long)Ea;
         out->E_after[1] = (unsigned long long)(Ea >> 64);
-        out->dE_sum[0] = (unsigned long long)D;
-        out->dE_sum[1] = (unsigned long long)(D >> 64);
-        out->accepted = swap_mode ? A / 2 : A;
+        out->dE_sum[0] = tot.d[0];
+        out->dE_sum[1] = tot.d[1];
+        out->accepted = swap_mode ? tot.a / 2 : tot.a;
         *ticket = 0;
     }
 }
