@@ -266,61 +266,100 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
-    pair = pairs_of_rank(world, rank, world)[0]  # one independent pair tile per rank
-    U, (a, b, px, py) = synth.problem_inputs(cfg, pair)
-    seed = synth.opt_seed(cfg, pair)
-    s = bn.Sampler(local, stream.cuda_stream)
-    s.set_lattice(synth.D1, synth.D2, cfg.levels)
-    s.set_bank(a, b, px, py)
-    s.set_energy(2.1, 1.0, 7)
-    s.set_tile(cfg.L, U)
+    # Work decomposition:
+    #  C4: the 8 independent dimension pairs are split over ranks (strong scaling, fixed total);
+    #  C5 with N > 1: one tile, bank shards + one int32 all-reduce per pass (strong scaling);
+    #  otherwise: one independent pair tile per rank (weak scaling).
+    banksharded = cfg.name == "C5" and world > 1
+    if cfg.pairs > 1:
+        pairs, scaling = pairs_of_rank(cfg.pairs, rank, world), "strong"
+    elif banksharded:
+        pairs, scaling = [0], "strong"
+    else:
+        pairs, scaling = [rank], "weak"
     P = cfg.L * cfg.L
+    samplers, streams, seeds = [], [], []
+    for j in pairs:
+        U, (a, b, px, py) = synth.problem_inputs(cfg, j)
+        st_j = torch.cuda.Stream() if len(pairs) > 1 else stream
+        s = bn.Sampler(local, st_j.cuda_stream)
+        s.set_lattice(synth.D1, synth.D2, cfg.levels)
+        if banksharded:
+            from paper_2105_12620_b200.dist import make_bank_sharded
+
+            make_bank_sharded(s, a, b, px, py, rank, world)
+        else:
+            s.set_bank(a, b, px, py)
+        s.set_energy(2.1, 1.0, 7)
+        s.set_tile(cfg.L, U)
+        samplers.append(s)
+        streams.append(st_j)
+        seeds.append(synth.opt_seed(cfg, j))
+    s = samplers[0]
+    U0 = synth.problem_inputs(cfg, pairs[0])[0]
+
+    def run_all(passes, first):
+        """Enqueue `passes` passes on every local pair (each on its own stream), joined to `stream`."""
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        for sj, stj, sd in zip(samplers, streams, seeds):
+            if stj is not stream:
+                stj.wait_event(ev)
+            sj.optimize(passes, sd, mode=cfg.mode, first_pass=first, stats=False)
+        for stj in streams:
+            if stj is not stream:
+                e = torch.cuda.Event()
+                e.record(stj)
+                stream.wait_event(e)
 
     # warm-up passes (W >= 3 by contract)
-    s.optimize(args.warmup, seed, mode=cfg.mode, first_pass=0, stats=False)
+    run_all(args.warmup, 0)
     barrier()
-    l0 = s.launch_count()
+    l0 = sum(x.launch_count() for x in samplers)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
-        s.optimize(args.steps, seed, mode=cfg.mode, first_pass=args.warmup, stats=False)
+        run_all(args.steps, args.warmup)
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1)
-    launches = s.launch_count() - l0
+    launches = sum(x.launch_count() for x in samplers) - l0
     ms_max = max_over_ranks(ms)
-    value = P * args.steps * world / (ms_max / 1e3)
+    units_per_step = P * (1 if banksharded else len(pairs) * world) if cfg.pairs == 1 else P * cfg.pairs
+    value = units_per_step * args.steps / (ms_max / 1e3)
     clocks = clk.summary()
 
-    # per-kernel device time on the context stream (same passes, events around each launch)
+    # per-kernel device time on the context stream (one pair alone, events around each launch)
     s.profile_enable(True)
-    s.optimize(args.steps, seed, mode=cfg.mode, first_pass=args.warmup + args.steps, stats=False)
+    s.optimize(args.steps, seeds[0], mode=cfg.mode, first_pass=args.warmup + args.steps, stats=False)
     prof = s.profile()
     s.profile_enable(False)
     roof = roofline({k: v for k, v in prof.items() if v[1]}, cfg, peaks, clocks.get("sm_mhz"))
 
     # end to end through the public API with host buffers: per step, H2D of the tile, one pass,
-    # D2H of the tile and the pass statistics.
+    # D2H of the tile and the pass statistics (pair 0 of every rank).
     pinned = torch.empty((P, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
     pinned[:] = s.get_tile()
     first = args.warmup + 2 * args.steps
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
+    f0.record(streams[0])
+    st = None
     for k in range(args.e2e_steps):
         s.set_tile(cfg.L, pinned)
-        st, _ = s.optimize(1, seed, mode=cfg.mode, first_pass=first + k, stats=True)
+        st, _ = s.optimize(1, seeds[0], mode=cfg.mode, first_pass=first + k, stats=True)
         s.get_tile(pinned)
-    f1.record(stream)
+    f1.record(streams[0])
     barrier()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
-    e2e = {"value": P * args.e2e_steps * world / (e2e_ms / 1e3), "unit": UNIT,
+    e2e_units = P * (1 if banksharded else world)
+    e2e = {"value": e2e_units * args.e2e_steps / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": P * 8 + 24, "d2h_bytes_per_step": P * 8 + 48,
            "path": "bn_set_tile(host) + bn_optimize(1 pass, stats) + bn_get_tile(host) per step"}
+    del U0
 
     launches = sum_over_ranks(launches)  # total over all ranks
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ev, dt, _ = oracle_sample(cfg, 0, args.cpu_classes)
@@ -328,17 +367,25 @@ def run_ours(args, cfg):
                "sample": cpu_sample_desc(cfg, args.cpu_classes), "seconds": dt}
 
     if rank == 0:
+        cfgj = config_json(cfg, world)
+        if cfg.pairs > 1:
+            cfgj["per_rank"] = f"{len(pairs)} of the {cfg.pairs} independent dimension-pair tiles, one stream each"
+            cfgj["global_tiles"] = cfg.pairs
+        elif banksharded:
+            cfgj["per_rank"] = f"bank shard {world}-way, one int32 NCCL all-reduce of window distances per pass"
+            cfgj["global_tiles"] = 1
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": config_json(cfg, world), "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
+            "scaling": scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": cfgj, "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
             "roofline": roof, "cpu_baseline": cpu,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
             "final_energy": st[-1]["E"] if st else None,
         }
         print(json.dumps(line), flush=True)
-    s.close()
+    for x in samplers:
+        x.close()
     if world > 1:
         dist.destroy_process_group()
 
