@@ -123,6 +123,8 @@ struct bn_ctx {
     bool per_class_decide = false;  // BN_DECIDE=per_class: 64 launches instead of one persistent
     bool simt_gram = false;         // BN_GRAM=simt: dp4a window distances instead of IMMA
     bool gram_attr_set[8] = {false};
+    bool gram2_attr_set[8] = {false};
+    bool imma_v1 = false;  // BN_GRAM=imma1: the one-strip-per-warp IMMA kernel
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
@@ -310,7 +312,7 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
         k_gram<R><<<grid, 32 * (R + 1), 0, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, SW, ctx->Tp,
                                                           ctx->nl, ctx->Dt.p);
         LAUNCHED_K();
-    } else {
+    } else if (ctx->imma_v1) {
         using S = mma_gram::Shape<R>;
         const int smem = 2 * S::STAGE;
         if (!ctx->gram_attr_set[R]) {
@@ -321,6 +323,18 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
         KSTART(BN_K_GRAM);
         k_gram_mma<R><<<g2, 32 * mma_gram::WARPS, smem, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, ctx->Tp,
                                                                        ctx->nl, ctx->Dt.p);
+        LAUNCHED_K();
+    } else {
+        using S = Shape2<R>;
+        const int smem = 2 * S::STAGE;
+        if (!ctx->gram2_attr_set[R]) {
+            CUDA_TRY(cudaFuncSetAttribute(k_gram_mma2<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            ctx->gram2_attr_set[R] = true;
+        }
+        dim3 g2(ctx->L / mma_gram::BX, ctx->L / mma_gram::BY);
+        KSTART(BN_K_GRAM);
+        k_gram_mma2<R><<<g2, 32 * mma_gram::WARPS, smem, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, ctx->Tp,
+                                                                        ctx->nl, ctx->Dt.p);
         LAUNCHED_K();
     }
     if (ctx->comm) {
@@ -562,6 +576,7 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     }
     const char* gm = getenv("BN_GRAM");
     ctx->simt_gram = gm && !strcmp(gm, "simt");
+    ctx->imma_v1 = gm && !strcmp(gm, "imma1");
     *out = ctx;
     return BN_OK;
 }

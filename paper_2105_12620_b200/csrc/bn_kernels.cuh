@@ -478,6 +478,141 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma(const uint8_t* __restrict__
     }
 }
 
+// IMMA window Gram v2: same staging as k_gram_mma, but warp w owns BOTH strips of block row
+// w >> 2 and the window rows oy in group (w & 3) (OYG2 of them).  The neighbour fragments of the
+// NT8 + 1 column tiles covering both strips are loaded once per (k32, oy) and shared by the two
+// strips' A fragments: 2 + OYG2 * (NT8 + 1) ldmatrix.x4 per 4 * OYG2 * NT8 mma (10 per 24 at R = 7).
+template <int R>
+struct Shape2 {
+    static constexpr int NT8 = (8 + 2 * R + 7) / 8;
+    static constexpr int NCOL = 8 + 8 * NT8;
+    static constexpr int NROW = mma_gram::BY + R;
+    static constexpr int OYG2 = (R + 4) / 4;  // oy per warp, 4 groups
+    static constexpr int STAGE = 2 * NROW * NCOL * mma_gram::ROWB;
+    static constexpr int H = 2 * R * R + 2 * R;
+};
+
+template <int R>
+__global__ void __launch_bounds__(512, 1) k_gram_mma2(const uint8_t* __restrict__ c, const uint8_t* __restrict__ cn,
+                                                      const int* __restrict__ nc, const int* __restrict__ nn,
+                                                      uint32_t L, uint32_t Tp, uint32_t nl, int4* __restrict__ Dt) {
+    using namespace mma_gram;
+    using S = Shape2<R>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+    const uint32_t x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sj = warp >> 2, og = warp & 3;  // block row, oy group
+    const int oy0 = og * S::OYG2;
+    const uint32_t rowB = nl * Tp;
+    const int nchunk = S::NROW * S::NCOL * 2 * (KC / 16);
+    auto srow = [&](int v, int r, int col) { return ((v * S::NROW) + r) * S::NCOL + col; };
+
+    for (uint32_t l = 0; l < nl; ++l) {
+        int acc[2][S::OYG2][S::NT8][2][4];
+#pragma unroll
+        for (int st2 = 0; st2 < 2; ++st2)
+#pragma unroll
+            for (int a = 0; a < S::OYG2; ++a)
+#pragma unroll
+                for (int t = 0; t < S::NT8; ++t)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v)
+                        acc[st2][a][t][v][0] = acc[st2][a][t][v][1] = acc[st2][a][t][v][2] = acc[st2][a][t][v][3] = 0;
+        const uint32_t nstage = Tp / KC;
+        auto issue = [&](uint32_t st) {
+            const uint32_t buf = sbase + (st & 1) * S::STAGE;
+            const uint32_t k0 = l * Tp + st * KC;
+            for (int j = threadIdx.x; j < nchunk; j += blockDim.x) {
+                const int ch = j & (KC / 16 - 1), row = j / (KC / 16);
+                const int col = row % S::NCOL, vr = row / S::NCOL, v = vr >= S::NROW, r = vr - v * S::NROW;
+                const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
+                const uint8_t* src = (v ? cn : c) + (size_t)(qy * L + qx) * rowB + k0 + 16 * ch;
+                cp_async16(buf + row * ROWB + 16 * ch, src);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        issue(0);
+        for (uint32_t st = 0; st < nstage; ++st) {
+            if (st + 1 < nstage) {
+                issue(st + 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncthreads();
+            const uint32_t buf = sbase + (st & 1) * S::STAGE;
+            const int mi = lane >> 3, ri = lane & 7;
+#pragma unroll
+            for (int kk = 0; kk < KC; kk += 32) {
+                uint32_t a[2][4];
+#pragma unroll
+                for (int st2 = 0; st2 < 2; ++st2) {
+                    const int v = mi & 1, kh = mi >> 1;
+                    ldsm_x4(buf + srow(v, sj, R + 8 * st2 + ri) * ROWB + kk + 16 * kh, a[st2][0], a[st2][1],
+                            a[st2][2], a[st2][3]);
+                }
+#pragma unroll
+                for (int a_oy = 0; a_oy < S::OYG2; ++a_oy) {
+                    const int oy = oy0 + a_oy;
+                    if (oy > R) break;
+#pragma unroll
+                    for (int T = 0; T <= S::NT8; ++T) {
+                        uint32_t b[4];
+                        const int v = mi >> 1, kh = mi & 1;
+                        ldsm_x4(buf + srow(v, sj + oy, 8 * T + ri) * ROWB + kk + 16 * kh, b[0], b[1], b[2], b[3]);
+                        if (T < S::NT8) {  // strip 0 uses tiles 0 .. NT8-1
+                            imma16832(acc[0][a_oy][T][0], a[0], b[0], b[1]);
+                            imma16832(acc[0][a_oy][T][1], a[0], b[2], b[3]);
+                        }
+                        if (T >= 1) {  // strip 1 uses tiles 1 .. NT8
+                            imma16832(acc[1][a_oy][T - 1][0], a[1], b[0], b[1]);
+                            imma16832(acc[1][a_oy][T - 1][1], a[1], b[2], b[3]);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        int* snorm = reinterpret_cast<int*>(smem);  // [2][NROW][NCOL]
+        for (int j = threadIdx.x; j < 2 * S::NROW * S::NCOL; j += blockDim.x) {
+            const int col = j % S::NCOL, vr = j / S::NCOL, r = vr % S::NROW, v = vr / S::NROW;
+            const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
+            snorm[j] = (v ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
+        }
+        __syncthreads();
+        const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+        for (int st2 = 0; st2 < 2; ++st2) {
+            const int xs = 8 * st2;
+            const uint32_t px = x0 + xs + g, py = y0 + sj, p = py * L + px;
+            const int ncp = snorm[sj * S::NCOL + R + xs + g], nnp = snorm[(S::NROW + sj) * S::NCOL + R + xs + g];
+            int4* out = Dt + ((size_t)l * L * L + p) * S::H;
+#pragma unroll
+            for (int a_oy = 0; a_oy < S::OYG2; ++a_oy) {
+                const int oy = oy0 + a_oy;
+                if (oy > R) break;
+#pragma unroll
+                for (int t = 0; t < S::NT8; ++t)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int n = 8 * t + 2 * tq + e, ox = n - R - g;
+                        if (ox < -R || ox > R || (oy == 0 && ox <= 0)) continue;
+                        const int qc = (sj + oy) * S::NCOL + xs + n;
+                        const int ncq = snorm[qc], nnq = snorm[S::NROW * S::NCOL + qc];
+                        int4 d;
+                        d.x = ncp + ncq - 2 * acc[st2][a_oy][t][0][e];
+                        d.y = nnp + ncq - 2 * acc[st2][a_oy][t][0][2 + e];
+                        d.z = ncp + nnq - 2 * acc[st2][a_oy][t][1][e];
+                        d.w = nnp + nnq - 2 * acc[st2][a_oy][t][1][2 + e];
+                        out[half_index(ox, oy, R)] = d;
+                    }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // -------------------------------------------------------------------------- energy terms
 // q(o, D) = rn_u64(2^64 * W[o] * G_l[D]); W and G are host-built fp64 tables (exp/sqrt of the
 // host libm), the product is one IEEE multiply (no contraction possible), the scaling by 2^64
