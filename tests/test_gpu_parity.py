@@ -201,3 +201,75 @@ def test_window_distances_and_shard_decomposition(bn, oracle_mod):
         assert np.array_equal(s.eval_counts(), co[:, :, t0:t1])
         acc += s.window_distances()
     assert np.array_equal(acc, Df)
+
+
+@pytest.mark.slow
+def test_c2_full_size_swap(bn, oracle_mod):
+    """C2 exactly (64x64, 4 spp, T=256, SWAP, seeds 1/2/3): 3 passes compared pass by pass."""
+    cfg = synth.CONFIGS["C2"]
+    U, bank = synth.problem_inputs(cfg)
+    s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
+    _check_run(s, o, U, 3, cfg.mode, seed=synth.opt_seed(cfg))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("pair", [0, 5])
+def test_c4_pair_full_size(bn, oracle_mod, pair):
+    """C4 pair j (128x128, 16 spp, T=1024, seeds xor j): all counts bit-exact, first colour class
+    decisions equal to the oracle, device invariants over a full pass."""
+    cfg = synth.CONFIGS["C4"]
+    U, bank = synth.problem_inputs(cfg, pair)
+    s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
+    co = o.counts(U)
+    assert np.array_equal(s.eval_counts(), co)
+    E0, _ = s.energy()
+    st, lg = s.optimize(1, synth.opt_seed(cfg, pair), log=True)
+    _, _, _, lgo = o.optimize(U, co, passes=1, seed=synth.opt_seed(cfg, pair), max_steps=1, energy_each_pass=False,
+                              log=True)
+    assert np.array_equal(lg[0, :1], lgo[0, :1])
+    assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"] and st[0]["dE_sum"] < 0
+
+
+def test_concurrent_contexts_match_sequential(bn, oracle_mod):
+    """Independent pair tiles on their own streams, enqueued concurrently (the C4 bench layout),
+    give bit-identical tiles to running each context alone."""
+    import torch
+
+    L, T, levels = 32, 96, (4, 16)
+    runs = []
+    for concurrent in (False, True):
+        ctxs = []
+        for j in range(3):
+            st = torch.cuda.Stream()
+            a, b, px, py = synth.make_bank(T, 40 + j)
+            s = bn.Sampler(0, st.cuda_stream)
+            s.set_lattice(synth.D1, synth.D2, levels)
+            s.set_bank(a, b, px, py)
+            s.set_energy(2.1, 1.0, 7)
+            s.set_tile(L, synth.make_tile(L, 50 + j))
+            ctxs.append(s)
+        for j, s in enumerate(ctxs):
+            s.optimize(4, 60 + j, stats=False)
+            if not concurrent:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        runs.append([s.get_tile() for s in ctxs])
+    for a_, b_ in zip(*runs):
+        assert np.array_equal(a_, b_)
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled(bn, oracle_mod):
+    """C5 (256x256, 16 spp, T=8192): all 512 M counts bit-exact and the first colour class's
+    1024 decisions equal to the oracle's (the flag-synchronised persistent decide path)."""
+    cfg = synth.CONFIGS["C5"]
+    U, bank = synth.problem_inputs(cfg)
+    s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
+    co = o.counts(U)
+    assert np.array_equal(s.eval_counts(), co)
+    E0, _ = s.energy()
+    st, lg = s.optimize(1, synth.opt_seed(cfg), log=True)
+    _, _, _, lgo = o.optimize(U, co, passes=1, seed=synth.opt_seed(cfg), max_steps=1, energy_each_pass=False,
+                              log=True)
+    assert np.array_equal(lg[0, :1], lgo[0, :1])
+    assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"]
