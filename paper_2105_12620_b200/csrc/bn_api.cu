@@ -125,6 +125,8 @@ struct bn_ctx {
     bool gram_attr_set[8] = {false};
     bool gram2_attr_set[8] = {false};
     bool imma_v1 = false;  // BN_GRAM=imma1: the one-strip-per-warp IMMA kernel
+    bool tc_gram = false;  // BN_GRAM=tc: tcgen05/TMEM window Gram (R = 7)
+    bool tc_attr_set = false;
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
@@ -304,10 +306,33 @@ int ensure_work(bn_ctx* ctx) {
 }
 
 template <int R>
+int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn);
+template <int R>
+int launch_lut_only(bn_ctx* ctx, int write_deltas);
+
+template <int R>
 int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas) {
+    int rc = launch_gram<R>(ctx, cn, nn);
+    if (rc) return rc;
+    return launch_lut_only<R>(ctx, write_deltas);
+}
+
+// Window Gram: tcgen05 (BN_GRAM=tc, R = 7), IMMA v2 (default), IMMA v1 (BN_GRAM=imma1), dp4a.
+template <int R>
+int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     const uint32_t SW = ctx->L < 32 ? ctx->L : 32;
     dim3 grid(ctx->L / SW, ctx->L);
-    if (ctx->simt_gram) {
+    if (R == 7 && ctx->tc_gram) {
+        const int smem = tc::SMEM + 1024;
+        if (!ctx->tc_attr_set) {
+            CUDA_TRY(cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            ctx->tc_attr_set = true;
+        }
+        KSTART(BN_K_GRAM);
+        k_gram_tc<<<dim3(ctx->L / 8, ctx->L / 8), tc::THREADS, smem, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L,
+                                                                                ctx->Tp, ctx->nl, ctx->Dt.p);
+        LAUNCHED_K();
+    } else if (ctx->simt_gram) {
         KSTART(BN_K_GRAM);
         k_gram<R><<<grid, 32 * (R + 1), 0, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, SW, ctx->Tp,
                                                           ctx->nl, ctx->Dt.p);
@@ -337,6 +362,11 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
                                                                         ctx->nl, ctx->Dt.p);
         LAUNCHED_K();
     }
+    return BN_OK;
+}
+
+template <int R>
+int launch_lut_only(bn_ctx* ctx, int write_deltas) {
     if (ctx->comm) {
         const size_t n = (size_t)ctx->P * half_count(R) * ctx->nl * 4;
         int r = g_nccl.allreduce(ctx->Dt.p, ctx->Dt.p, n, NCCL_INT32, NCCL_SUM, ctx->comm, ctx->ls);
@@ -360,17 +390,7 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
 
 template <int R>
 int launch_gram_only(bn_ctx* ctx) {
-    using S = mma_gram::Shape<R>;
-    const int smem = 2 * S::STAGE;
-    if (!ctx->gram_attr_set[R]) {
-        CUDA_TRY(cudaFuncSetAttribute(k_gram_mma<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        ctx->gram_attr_set[R] = true;
-    }
-    dim3 g2(ctx->L / mma_gram::BX, ctx->L / mma_gram::BY);
-    k_gram_mma<R><<<g2, 32 * mma_gram::WARPS, smem, ctx->stream>>>(ctx->c.p, ctx->c.p, ctx->nc.p, ctx->nc.p, ctx->L,
-                                                                   ctx->Tp, ctx->nl, ctx->Dt.p);
-    LAUNCHED();
-    return BN_OK;
+    return launch_gram<R>(ctx, ctx->c.p, ctx->nc.p);
 }
 int gram_only(bn_ctx* ctx) {
     switch (ctx->R) {
@@ -577,6 +597,7 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     const char* gm = getenv("BN_GRAM");
     ctx->simt_gram = gm && !strcmp(gm, "simt");
     ctx->imma_v1 = gm && !strcmp(gm, "imma1");
+    ctx->tc_gram = gm && !strcmp(gm, "tc");
     *out = ctx;
     return BN_OK;
 }

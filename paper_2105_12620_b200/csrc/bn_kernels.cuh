@@ -250,8 +250,8 @@ __global__ void k_swap_gather(const uint2* __restrict__ U, uint2* __restrict__ U
 // (row y+oy, columns x0-R .. x0+SW+R-1) of both c and cn in shared memory (row stride KCW+1
 // words: conflict-free), and every thread accumulates 4 dp4a dot products per offset ox:
 //   <c_p,c_q>, <cn_p,c_q>, <c_p,cn_q>, <cn_p,cn_q>.
-// D = |x|^2 + |y|^2 - 2<x,y> from the per-row norms.  Output Dt[(p*H + h)*nl + l] =
-// int4(D(c,c), D(cn,c), D(c,cn), D(cn,cn)) for h in the half window (layout [l][p][h]).
+// D = |x|^2 + |y|^2 - 2<x,y> from the per-row norms.  Output Dt[l][p][h] =
+// int4(D(c_p,c_q), D(c_p,cn_q), D(cn_p,c_q), D(cn_p,cn_q)), q = p + o_h, h in the half window.
 // Kept as the SIMT reference path (BN_GRAM=simt); the default is k_gram_mma below.
 constexpr int GRAM_KC = 32;               // bytes of K per stage
 constexpr int GRAM_KCW = GRAM_KC / 4;     // words
@@ -315,10 +315,10 @@ __global__ void __launch_bounds__(32 * (R + 1)) k_gram(const uint8_t* __restrict
                 const uint32_t q = ((y + oy) & (L - 1)) * L + ((x + ox + L) & (L - 1));
                 const int ncq = nc[(size_t)q * nl + l], nnq = nn[(size_t)q * nl + l];
                 int4 d;
-                d.x = ncp + ncq - 2 * (int)acc[i][0];
-                d.y = nnp + ncq - 2 * (int)acc[i][1];
-                d.z = ncp + nnq - 2 * (int)acc[i][2];
-                d.w = nnp + nnq - 2 * (int)acc[i][3];
+                d.x = ncp + ncq - 2 * (int)acc[i][0];  // D(c_p, c_q)
+                d.y = ncp + nnq - 2 * (int)acc[i][2];  // D(c_p, cn_q)
+                d.z = nnp + ncq - 2 * (int)acc[i][1];  // D(cn_p, c_q)
+                d.w = nnp + nnq - 2 * (int)acc[i][3];  // D(cn_p, cn_q)
                 Dt[((size_t)l * L * L + p) * H + half_index(ox, oy, R)] = d;
             }
         }
@@ -467,10 +467,10 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma(const uint8_t* __restrict__
                     const int qc = (sj + oy) * S::NCOL + xs + n;  // staged neighbour (row, column)
                     const int ncq = snorm[qc], nnq = snorm[S::NROW * S::NCOL + qc];
                     int4 d;
-                    d.x = ncp + ncq - 2 * acc[a_oy][t][0][e];
-                    d.y = nnp + ncq - 2 * acc[a_oy][t][0][2 + e];
-                    d.z = ncp + nnq - 2 * acc[a_oy][t][1][e];
-                    d.w = nnp + nnq - 2 * acc[a_oy][t][1][2 + e];
+                    d.x = ncp + ncq - 2 * acc[a_oy][t][0][e];      // D(c_p, c_q)
+                    d.y = ncp + nnq - 2 * acc[a_oy][t][1][e];      // D(c_p, cn_q)
+                    d.z = nnp + ncq - 2 * acc[a_oy][t][0][2 + e];  // D(cn_p, c_q)
+                    d.w = nnp + nnq - 2 * acc[a_oy][t][1][2 + e];  // D(cn_p, cn_q)
                     out[half_index(ox, oy, R)] = d;
                 }
         }
@@ -601,15 +601,226 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma2(const uint8_t* __restrict_
                         const int qc = (sj + oy) * S::NCOL + xs + n;
                         const int ncq = snorm[qc], nnq = snorm[S::NROW * S::NCOL + qc];
                         int4 d;
-                        d.x = ncp + ncq - 2 * acc[st2][a_oy][t][0][e];
-                        d.y = nnp + ncq - 2 * acc[st2][a_oy][t][0][2 + e];
-                        d.z = ncp + nnq - 2 * acc[st2][a_oy][t][1][e];
-                        d.w = nnp + nnq - 2 * acc[st2][a_oy][t][1][2 + e];
+                        d.x = ncp + ncq - 2 * acc[st2][a_oy][t][0][e];      // D(c_p, c_q)
+                        d.y = ncp + nnq - 2 * acc[st2][a_oy][t][1][e];      // D(c_p, cn_q)
+                        d.z = nnp + ncq - 2 * acc[st2][a_oy][t][0][2 + e];  // D(cn_p, c_q)
+                        d.w = nnp + nnq - 2 * acc[st2][a_oy][t][1][2 + e];  // D(cn_p, cn_q)
                         out[half_index(ox, oy, R)] = d;
                     }
             }
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------- window Gram on 5th-gen tensor cores (tcgen05)
+// UMMA version of the window Gram for R = 7.  CTA = 8 x 8 pixels; A (M = 128) =
+// [c rows of the 64 pixels ; cn rows]; the half-window neighbourhood (15 rows x 22 columns) is
+// split by neighbour rows into two TMEM chunks, ny 0..7 (B = 352 rows) and ny 8..14 (308 -> 320),
+// each accumulated over K = the level's T bytes with tcgen05.mma.kind::i8 (exact s32) into TMEM.
+// Operands are staged with cp.async in the canonical K-major SWIZZLE_128B layout (8-row, 1024-B
+// atoms), 128 B of K per stage, 3-stage ring; tcgen05.commit on a per-buffer mbarrier releases a
+// buffer.  Epilogue: tcgen05.ld 32 columns per (lane, neighbour row, version), a per-warp smem
+// scratch picks each lane's 15 window columns, D = |x|^2 + |y|^2 - 2<x,y>; lane (p, v) writes the
+// int2 (D(v_p, c_q), D(v_p, cn_q)) = .xy (v = 0) or .zw (v = 1) of Dt[l][p][h].
+namespace tc {
+constexpr int R = 7, NBC = 8 + 2 * R /*22*/, NBR = 8 + R /*15*/;
+constexpr int A_ROWS = 128, B_ROWS0 = 2 * 8 * NBC /*352*/, B_ROWS1 = 2 * 7 * NBC /*308*/;
+constexpr int N1_0 = B_ROWS0 - 256 /*96*/, N1_1 = 64; /* 308 -> 320 = 256 + 64 */
+constexpr int KB = 128;                                  // K bytes per stage (one swizzle row)
+constexpr int A_BYTES = A_ROWS * KB, B_BYTES = B_ROWS0 * KB;
+constexpr int STAGE = A_BYTES + B_BYTES;                 // 61440
+constexpr int NSTAGE = 3;
+constexpr int THREADS = 256;
+constexpr int SCR = 24;                                  // scratch ints per lane
+constexpr int SMEM = NSTAGE * STAGE + 8 * 32 * SCR * 4 + 2 * NBR * NBC * 4 + 64;
+constexpr int H = 2 * R * R + 2 * R;
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {  // K-major, SWIZZLE_128B, SBO = 1024
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__host__ __device__ constexpr uint32_t idesc_u8(int M, int N) {
+    return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);  // s32 += u8 x u8, K-major
+}
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    for (uint32_t i = 0; !mbar_try(bar, parity); ++i)
+        if (i > (1u << 26)) __trap();  // never hang the GPU on a protocol bug
+}
+__device__ __forceinline__ void ld32(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+}  // namespace tc
+
+__global__ void __launch_bounds__(tc::THREADS, 1) k_gram_tc(const uint8_t* __restrict__ c, const uint8_t* __restrict__ cn,
+                                                            const int* __restrict__ nc, const int* __restrict__ nn,
+                                                            uint32_t L, uint32_t Tp, uint32_t nl,
+                                                            int4* __restrict__ Dt) {
+    using namespace tc;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment of the operand ring (SWIZZLE_128B atoms)
+    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sring = (raw + 1023) & ~1023u;
+    uint8_t* gring = smem_raw + (sring - raw);
+    int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);          // [8 warps][32][SCR]
+    int* snorm = scratch + 8 * 32 * SCR;                                      // [2][NBR][NBC]
+    __shared__ __align__(8) uint64_t bars[NSTAGE + 1];
+    __shared__ uint32_t tmem_base_sh;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t x0 = blockIdx.x * 8, y0 = blockIdx.y * 8, P = L * L;
+    const uint32_t rowB = nl * Tp;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b <= NSTAGE; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tmem_base_sh))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base_sh;
+    uint32_t gs = 0;        // global stage counter (buffer = gs % 3, use = gs / 3)
+    uint32_t done_uses = 0; // uses of the chunk-done barrier
+    const uint32_t nk = Tp / KB;
+
+    for (uint32_t l = 0; l < nl; ++l) {
+        // norms of the neighbourhood (own pixels included) for this level
+        for (int j = threadIdx.x; j < 2 * NBR * NBC; j += blockDim.x) {
+            const int nx = j % NBC, vr = j / NBC, v = vr >= NBR, r = vr - v * NBR;
+            const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - R) & (L - 1);
+            snorm[j] = (v ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
+        }
+        for (int ch = 0; ch < 2; ++ch) {
+            const int NR = ch ? 7 : 8, nb_rows = 2 * NR * NBC, N1 = ch ? N1_1 : N1_0;
+            const int nrows = A_ROWS + nb_rows;
+            auto issue = [&](uint32_t kstage) {
+                const uint32_t b = gs % NSTAGE, use = gs / NSTAGE;
+                if (use > 0) mbar_wait(bar0 + 8 * b, (use - 1) & 1);  // MMAs of gs - 3 done with it
+                const uint32_t buf = sring + b * STAGE;
+                const uint32_t k0 = l * Tp + kstage * KB;
+                for (int j = threadIdx.x; j < nrows * 8; j += blockDim.x) {
+                    const int row = j >> 3, cc = j & 7;
+                    uint32_t pix;
+                    const uint8_t* base;
+                    uint32_t dst;
+                    if (row < A_ROWS) {
+                        const int v = row >> 6, pp = row & 63;
+                        pix = ((y0 + (pp >> 3)) & (L - 1)) * L + ((x0 + (pp & 7)) & (L - 1));
+                        base = v ? cn : c;
+                        dst = buf + (row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4);
+                    } else {
+                        const int br = row - A_ROWS, v = br >= NR * NBC, rr = br - v * NR * NBC;
+                        const int nyl = rr / NBC, nx = rr - nyl * NBC;
+                        pix = ((y0 + 8 * ch + nyl) & (L - 1)) * L + ((x0 + nx + L - R) & (L - 1));
+                        base = v ? cn : c;
+                        dst = buf + A_BYTES + (br >> 3) * 1024 + (br & 7) * 128 + ((cc ^ (br & 7)) << 4);
+                    }
+                    cp_async16(dst, base + (size_t)pix * rowB + k0 + 16 * cc);
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                ++gs;
+            };
+            const uint32_t gs_first = gs;
+            issue(0);
+            if (nk > 1) issue(1);
+            for (uint32_t ks = 0; ks < nk; ++ks) {
+                if (ks + 2 < nk) {
+                    issue(ks + 2);
+                    asm volatile("cp.async.wait_group 2;" ::: "memory");
+                } else if (ks + 1 < nk) {
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t g = gs_first + ks, b = g % NSTAGE;
+                    const uint32_t sa = sring + b * STAGE, sb = sa + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < KB / 32; ++kk) {
+                        const uint32_t acc = (ks > 0 || kk > 0) ? 1u : 0u;
+                        mma(tmem, sdesc(sa + 32 * kk), sdesc(sb + 32 * kk), idesc_u8(128, 256), acc);
+                        mma(tmem + 256, sdesc(sa + 32 * kk), sdesc(sb + 256 * 128 + 32 * kk), idesc_u8(128, N1), acc);
+                    }
+                    commit(bar0 + 8 * b);
+                    if (ks + 1 == nk) commit(bar0 + 8 * NSTAGE);  // chunk done
+                }
+            }
+            // ---- epilogue of this chunk
+            mbar_wait(bar0 + 8 * NSTAGE, done_uses & 1);
+            ++done_uses;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const int lq = warp & 3;                  // TMEM lane quarter = A rows 32 lq ..
+            const int arow = 32 * lq + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
+            const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
+            const int np = snorm[(v * NBR + dy) * NBC + dx + R];
+            int* scr = scratch + (warp * 32 + lane) * SCR;
+            int2* out2 = reinterpret_cast<int2*>(Dt + ((size_t)l * P + p) * H) + v;  // .xy (v=0) / .zw (v=1)
+            for (int nyl = (warp >> 2); nyl < NR; nyl += 2) {  // warps w and w+4 split the neighbour rows
+                const int ny = 8 * ch + nyl, oy = ny - dy;
+                uint32_t rc[32], rn[32];
+                ld32(tmem + ((uint32_t)(32 * lq) << 16) + nyl * NBC, rc);              // <v_p, c_q>
+                ld32(tmem + ((uint32_t)(32 * lq) << 16) + NR * NBC + nyl * NBC, rn);   // <v_p, cn_q>
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (oy < 0 || oy > R) continue;
+                // pick the window columns nx = dx + ox + R (lane-dependent) through the lane's scratch row
+                int dc[2 * R + 1], dn[2 * R + 1];
+#pragma unroll
+                for (int j = 0; j < NBC; ++j) scr[j] = (int)rc[j];
+#pragma unroll
+                for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + i];
+#pragma unroll
+                for (int j = 0; j < NBC; ++j) scr[j] = (int)rn[j];
+#pragma unroll
+                for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + i];
+#pragma unroll
+                for (int i = 0; i < 2 * R + 1; ++i) {
+                    const int ox = i - R, nx = dx + i;
+                    if (oy == 0 && ox <= 0) continue;
+                    const int nq_c = snorm[ny * NBC + nx], nq_n = snorm[(NBR + ny) * NBC + nx];
+                    out2[2 * half_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncthreads();  // TMEM and scratch free for the next chunk / level
+        }
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
 }
 
@@ -668,8 +879,8 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
                 continue;
             }
             const double* G = lut.G[l];
-            const unsigned long long qcc = qterm(w, G, D.x), qnc = qterm(w, G, D.y);
-            const unsigned long long qcn = qterm(w, G, D.z), qnn = qterm(w, G, D.w);
+            const unsigned long long qcc = qterm(w, G, D.x), qcn = qterm(w, G, D.y);
+            const unsigned long long qnc = qterm(w, G, D.z), qnn = qterm(w, G, D.w);
             e += (u128)qcc;
             a0 += (i128)qnc - (i128)qcc;  // p takes cn_p, q still c_q
             a1 += (i128)qnn - (i128)qcn;  // p takes cn_p, q already cn_q

@@ -273,3 +273,31 @@ def test_c5_full_size_sampled(bn, oracle_mod):
                               log=True)
     assert np.array_equal(lg[0, :1], lgo[0, :1])
     assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"]
+
+
+# ------------------------------------------------------------------ window-Gram variants
+@pytest.mark.parametrize("L,T,levels", [(16, 64, (16,)), (32, 300, (1, 4, 16, 64)), (64, 512, (4,))])
+def test_gram_variants_bit_identical(bn, oracle_mod, L, T, levels, monkeypatch):
+    """tcgen05 (UMMA/TMEM), IMMA v2, IMMA v1 and dp4a window Grams give identical distances,
+    equal to the plain definition on the oracle's counts."""
+    from tests.test_dist_cpu import _partial_distances
+
+    a, b, px, py = synth.make_bank(T, 31)
+    U = synth.make_tile(L, 32)
+    outs = {}
+    for variant in ("", "tc", "imma1", "simt"):
+        monkeypatch.setenv("BN_GRAM", variant)
+        s, o, _ = make(bn, oracle_mod, L, T, levels, bank=(a, b, px, py), U=U)
+        outs[variant] = s.window_distances()
+    co = o.counts(U)
+    for li in range(len(levels)):
+        assert np.array_equal(outs[""][li], _partial_distances(co[li], L))
+    for k in ("tc", "imma1", "simt"):
+        assert np.array_equal(outs[k], outs[""]), k
+
+
+def test_tc_gram_optimize_parity(bn, oracle_mod, monkeypatch):
+    """Full passes with the tcgen05 window Gram against the oracle (C3 shape, ragged T)."""
+    monkeypatch.setenv("BN_GRAM", "tc")
+    s, o, U = make(bn, oracle_mod, 32, 130, (1, 4, 16, 64))
+    _check_run(s, o, U, 2, 0, seed=7)
