@@ -56,6 +56,34 @@ struct NcclApi {
 NcclApi g_nccl;
 constexpr int NCCL_INT32 = 2, NCCL_SUM = 0;  // ncclInt32, ncclSum (nccl.h enums)
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda).
+typedef CUresult (*encode_tiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+encode_tiled_t get_encode_tiled() {
+    static encode_tiled_t fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (encode_tiled_t)p;
+    }
+    return fn;
+}
+// 2D map over a [P][rowB] uint8 count tensor: boxes of 8 pixel rows x 128 bytes, 128-B swizzle.
+bool make_count_map(CUtensorMap* m, const void* base, uint64_t rowB, uint64_t P) {
+    encode_tiled_t enc = get_encode_tiled();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {rowB, P};
+    cuuint64_t strides[1] = {rowB};
+    cuuint32_t box[2] = {128, 8};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -127,6 +155,10 @@ struct bn_ctx {
     bool imma_v1 = false;  // BN_GRAM=imma1: the one-strip-per-warp IMMA kernel
     bool tc_gram = false;  // BN_GRAM=tc: tcgen05/TMEM window Gram (R = 7)
     bool tc_attr_set = false;
+    bool tc2_gram = false;  // BN_GRAM=tc2: warp-specialised tcgen05 window Gram (R = 7)
+    bool tc2_attr_set = false;
+    bool tc3_gram = false;  // BN_GRAM=tc3: TMA-fed warp-specialised tcgen05 window Gram (R = 7)
+    bool tc3_attr_set = false;
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
@@ -322,7 +354,30 @@ template <int R>
 int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     const uint32_t SW = ctx->L < 32 ? ctx->L : 32;
     dim3 grid(ctx->L / SW, ctx->L);
-    if (R == 7 && ctx->tc_gram) {
+    if (R == 7 && ctx->tc3_gram) {
+        CUtensorMap mc, mn;
+        if (!make_count_map(&mc, ctx->c.p, ctx->rowB, ctx->P) || !make_count_map(&mn, cn, ctx->rowB, ctx->P))
+            return fail(ctx, BN_ECUDA, "cuTensorMapEncodeTiled failed");
+        const int smem = tc3::SMEM;
+        if (!ctx->tc3_attr_set) {
+            CUDA_TRY(cudaFuncSetAttribute(k_gram_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            ctx->tc3_attr_set = true;
+        }
+        KSTART(BN_K_GRAM);
+        k_gram_tc3<<<dim3(ctx->L / 8, ctx->L / 8, ctx->nl), tc3::THREADS, smem, ctx->ls>>>(mc, mn, ctx->nc.p, nn, ctx->L,
+                                                                                            ctx->Tp, ctx->nl, ctx->Dt.p);
+        LAUNCHED_K();
+    } else if (R == 7 && ctx->tc2_gram) {
+        const int smem = tc2::SMEM;
+        if (!ctx->tc2_attr_set) {
+            CUDA_TRY(cudaFuncSetAttribute(k_gram_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            ctx->tc2_attr_set = true;
+        }
+        KSTART(BN_K_GRAM);
+        k_gram_tc2<<<dim3(ctx->L / 8, ctx->L / 8), tc2::THREADS, smem, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn,
+                                                                                  ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
+        LAUNCHED_K();
+    } else if (R == 7 && ctx->tc_gram) {
         const int smem = tc::SMEM + 1024;
         if (!ctx->tc_attr_set) {
             CUDA_TRY(cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -598,6 +653,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->simt_gram = gm && !strcmp(gm, "simt");
     ctx->imma_v1 = gm && !strcmp(gm, "imma1");
     ctx->tc_gram = gm && !strcmp(gm, "tc");
+    ctx->tc2_gram = gm && !strcmp(gm, "tc2");
+    ctx->tc3_gram = gm && !strcmp(gm, "tc3");
     *out = ctx;
     return BN_OK;
 }

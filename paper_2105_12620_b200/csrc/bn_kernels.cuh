@@ -20,6 +20,7 @@
 // H = half window {o : oy > 0 or (oy == 0 and ox > 0)}: each unordered neighbour pair is
 // computed once and written to both (p, o) and (p + o, -o).
 #pragma once
+#include <cuda.h>  // CUtensorMap (type only; the encoder is fetched through the runtime)
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -818,6 +819,379 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_gram_tc(const uint8_t* __res
             __syncthreads();  // TMEM and scratch free for the next chunk / level
         }
     }
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// Warp-specialised tcgen05 window Gram (R = 7).  Roles: warps 0-3 epilogue (TMEM lanes 32w..),
+// warps 4-7 producers (cp.async into the SWIZZLE_128B ring), warp 8 lane 0 issues the UMMAs.
+// The half-window neighbourhood is split into three 5-row chunks (B = 220 -> N = 224 TMEM
+// columns), so two TMEM accumulators (256 columns each) let the epilogue of one chunk overlap the
+// MMAs of the next.  mbarriers: full[s] (128 producer arrivals), empty[s] (MMA commit),
+// tfull[u] (MMA commit), tempty[u] (128 epilogue arrivals).
+namespace tc2 {
+constexpr int R = 7, NBC = 8 + 2 * R, NBR = 8 + R;
+constexpr int CH_ROWS = 5, NCHUNK = 3, B_ROWS = 2 * CH_ROWS * NBC /*220*/, N = 224;
+constexpr int A_ROWS = 128, KB = 128, A_BYTES = A_ROWS * KB, B_BYTES = N * KB;
+constexpr int STAGE = A_BYTES + B_BYTES;  // 45056 = 44 KB (1024-aligned)
+constexpr int NSTAGE = 4;
+constexpr int NROWS = A_ROWS + B_ROWS;    // staged rows per stage (348)
+constexpr int THREADS = 288;
+constexpr int SCR = 24;
+constexpr int SMEM = NSTAGE * STAGE + 4 * 32 * SCR * 4 + 2 * NBR * NBC * 4 + NROWS * 8 + 1024;
+constexpr int H = 2 * R * R + 2 * R;
+}  // namespace tc2
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(tc2::THREADS, 1) k_gram_tc2(const uint8_t* __restrict__ c,
+                                                              const uint8_t* __restrict__ cn,
+                                                              const int* __restrict__ nc, const int* __restrict__ nn,
+                                                              uint32_t L, uint32_t Tp, uint32_t nl,
+                                                              int4* __restrict__ Dt) {
+    using namespace tc2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sring = (raw + 1023) & ~1023u;
+    uint8_t* gring = smem_raw + (sring - raw);
+    int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);  // [4 warps][32][SCR]
+    int* snorm = scratch + 4 * 32 * SCR;                              // [2][NBR][NBC]
+    long long* rowoff = reinterpret_cast<long long*>(snorm + 2 * NBR * NBC);  // [NROWS] (bit 0: version)
+    __shared__ __align__(8) uint64_t bars[2 * NSTAGE + 4];
+    __shared__ uint32_t tmem_sh;
+    const uint32_t b_full = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    const uint32_t b_empty = b_full + 8 * NSTAGE, b_tfull = b_full + 16 * NSTAGE, b_tempty = b_tfull + 16;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t x0 = blockIdx.x * 8, y0 = blockIdx.y * 8, P = L * L, rowB = nl * Tp;
+    const uint32_t nk = Tp / KB;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSTAGE; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_full + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_empty + 8 * i) : "memory");
+        }
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_tfull + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_tempty + 8 * i) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tmem_sh))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_sh;
+
+    if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------------------------ producers
+        const int pt = threadIdx.x - 128, cc = pt & 7;
+        uint32_t g = 0;
+        for (uint32_t l = 0; l < nl; ++l)
+            for (int ch = 0; ch < NCHUNK; ++ch) {
+                named_bar(1, 128);  // everyone done issuing from the previous row table
+                for (int row = pt; row < NROWS; row += 128) {
+                    uint32_t pix, v;
+                    if (row < A_ROWS) {
+                        v = row >> 6;
+                        const int pp = row & 63;
+                        pix = ((y0 + (pp >> 3)) & (L - 1)) * L + ((x0 + (pp & 7)) & (L - 1));
+                    } else {
+                        const int br = row - A_ROWS;
+                        v = br >= CH_ROWS * NBC;
+                        const int rr = br - (int)v * CH_ROWS * NBC, nyl = rr / NBC, nx = rr - nyl * NBC;
+                        pix = ((y0 + CH_ROWS * ch + nyl) & (L - 1)) * L + ((x0 + nx + L - R) & (L - 1));
+                    }
+                    rowoff[row] = (((long long)pix * rowB) << 1) | v;
+                }
+                named_bar(1, 128);
+                for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
+                    const uint32_t b = g % NSTAGE, use = g / NSTAGE;
+                    if (use > 0) tc::mbar_wait(b_empty + 8 * b, (use - 1) & 1);
+                    const uint32_t buf = sring + b * STAGE;
+                    const size_t k0 = (size_t)l * Tp + ks * KB + 16 * cc;
+                    for (int row = pt >> 3; row < NROWS; row += 16) {
+                        const long long ro = rowoff[row];
+                        const uint8_t* src = ((ro & 1) ? cn : c) + (ro >> 1) + k0;
+                        const uint32_t dst = row < A_ROWS
+                                                 ? buf + (row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4)
+                                                 : buf + A_BYTES + ((row - A_ROWS) >> 3) * 1024 +
+                                                       ((row - A_ROWS) & 7) * 128 + ((cc ^ ((row - A_ROWS) & 7)) << 4);
+                        cp_async16(dst, src);
+                    }
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    if (g >= 2) {  // stage g-2 has landed: publish it to the async proxy / MMA warp
+                        asm volatile("cp.async.wait_group 2;" ::: "memory");
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        mbar_arrive(b_full + 8 * ((g - 2) % NSTAGE));
+                    }
+                }
+            }
+        // drain the last two stages
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (g >= 2) mbar_arrive(b_full + 8 * ((g - 2) % NSTAGE));
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (g >= 1) mbar_arrive(b_full + 8 * ((g - 1) % NSTAGE));
+    } else if (warp == 8) {
+        // ------------------------------------------------------------------ MMA issuer
+        uint32_t g = 0, q = 0;
+        for (uint32_t l = 0; l < nl; ++l)
+            for (int ch = 0; ch < NCHUNK; ++ch, ++q) {
+                const uint32_t ub = q & 1, uu = q >> 1;
+                if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
+                    const uint32_t b = g % NSTAGE;
+                    tc::mbar_wait(b_full + 8 * b, (g / NSTAGE) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if (lane == 0) {
+                        const uint32_t sa = sring + b * STAGE, sb = sa + A_BYTES;
+#pragma unroll
+                        for (int kk = 0; kk < KB / 32; ++kk)
+                            tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk),
+                                    tc::idesc_u8(128, N), (ks > 0 || kk > 0) ? 1u : 0u);
+                        tc::commit(b_empty + 8 * b);
+                        if (ks + 1 == nk) tc::commit(b_tfull + 8 * ub);
+                    }
+                    __syncwarp();
+                }
+            }
+    } else if (warp < 4) {
+        // ------------------------------------------------------------------ epilogue
+        const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
+        const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
+        int* scr = scratch + (warp * 32 + lane) * SCR;
+        uint32_t q = 0;
+        for (uint32_t l = 0; l < nl; ++l) {
+            named_bar(2, 128);  // all epilogue threads done with the previous level's norms
+            for (int j = threadIdx.x; j < 2 * NBR * NBC; j += 128) {
+                const int nx = j % NBC, vr = j / NBC, vv = vr >= NBR, r = vr - vv * NBR;
+                const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - R) & (L - 1);
+                snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
+            }
+            named_bar(2, 128);
+            const int np = snorm[(v * NBR + dy) * NBC + dx + R];
+            int2* out2 = reinterpret_cast<int2*>(Dt + ((size_t)l * P + p) * H) + v;
+            for (int ch = 0; ch < NCHUNK; ++ch, ++q) {
+                const uint32_t ub = q & 1, uu = q >> 1;
+                tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
+                    const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
+                    uint32_t rc[32], rn[32];
+                    const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub + nyl * NBC;
+                    tc::ld32(ta, rc);                          // <v_p, c_q>
+                    tc::ld32(ta + CH_ROWS * NBC, rn);          // <v_p, cn_q>
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (oy < 0 || oy > R) continue;
+                    int dc[2 * R + 1], dn[2 * R + 1];
+#pragma unroll
+                    for (int j = 0; j < NBC; ++j) scr[j] = (int)rc[j];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + i];
+#pragma unroll
+                    for (int j = 0; j < NBC; ++j) scr[j] = (int)rn[j];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + i];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) {
+                        const int ox = i - R, nx = dx + i;
+                        if (oy == 0 && ox <= 0) continue;
+                        const int nq_c = snorm[ny * NBC + nx], nq_n = snorm[(NBR + ny) * NBC + nx];
+                        out2[2 * half_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(b_tempty + 8 * ub);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// TMA-fed, warp-specialised tcgen05 window Gram (R = 7), one CTA per (8x8 block, level).
+// Every operand group is an aligned run of 8 pixels (x0 is a multiple of 8), i.e. 8 consecutive
+// rows of the [P][levels*Tp] count tensor: one 2D TMA box of 8 rows x 128 B per group, which is
+// exactly one SWIZZLE_128B atom of the UMMA K-major layout.  Per 128-B K stage: A = 16 boxes
+// (c and cn of the 8 block rows), B = 30 boxes (c and cn of 5 neighbour rows x 3 aligned groups
+// covering x0-8 .. x0+15; N = 240, the 2 columns outside the window are ignored).  A toroidal
+// wrap only ever moves a whole group.  Warp 0-3: epilogue, warp 4 lane 0: TMA producer, warp 5
+// lane 0: UMMA issuer.  Three neighbour chunks, two TMEM accumulators of 256 columns.
+namespace tc3 {
+constexpr int R = 7, NBR = 8 + R, GRP = 3, NBX = 8 * GRP /*24*/;
+constexpr int CH_ROWS = 5, NCHUNK = 3, N = 2 * CH_ROWS * NBX /*240*/;
+constexpr int A_BYTES = 128 * 128, B_BYTES = N * 128;
+constexpr int STAGE = A_BYTES + B_BYTES;  // 47104 = 46 KB
+constexpr int NSTAGE = 4;
+constexpr int THREADS = 192;
+constexpr int SCR = 28;
+constexpr int SMEM = NSTAGE * STAGE + 4 * 32 * SCR * 4 + 2 * NBR * NBX * 4 + 1024;
+constexpr int H = 2 * R * R + 2 * R;
+}  // namespace tc3
+
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_constant__ CUtensorMap tm_c,
+                                                              const __grid_constant__ CUtensorMap tm_n,
+                                                              const int* __restrict__ nc, const int* __restrict__ nn,
+                                                              uint32_t L, uint32_t Tp, uint32_t nl,
+                                                              int4* __restrict__ Dt) {
+    using namespace tc3;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sring = (raw + 1023) & ~1023u;
+    uint8_t* gring = smem_raw + (sring - raw);
+    int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);  // [4 warps][32][SCR]
+    int* snorm = scratch + 4 * 32 * SCR;                              // [2][NBR][NBX], x from x0-8
+    __shared__ __align__(8) uint64_t bars[2 * NSTAGE + 4];
+    __shared__ uint32_t tmem_sh;
+    const uint32_t b_full = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    const uint32_t b_empty = b_full + 8 * NSTAGE, b_tfull = b_full + 16 * NSTAGE, b_tempty = b_tfull + 16;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t x0 = blockIdx.x * 8, y0 = blockIdx.y * 8, l = blockIdx.z, P = L * L;
+    const uint32_t nk = Tp / 128;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSTAGE; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_full + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_empty + 8 * i) : "memory");
+        }
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_tfull + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_tempty + 8 * i) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tmem_sh))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    // neighbourhood norms of this level (rows y0 .. y0+14, columns x0-8 .. x0+15)
+    for (int j = threadIdx.x; j < 2 * NBR * NBX; j += blockDim.x) {
+        const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;
+        const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - 8) & (L - 1);
+        snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_sh;
+
+    if (warp == 4) {
+        // --------------------------------------------------------------- TMA producer
+        if (lane == 0) {
+            uint32_t g = 0;
+            for (int ch = 0; ch < NCHUNK; ++ch)
+                for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
+                    const uint32_t b = g % NSTAGE, use = g / NSTAGE;
+                    if (use > 0) tc::mbar_wait(b_empty + 8 * b, (use - 1) & 1);
+                    const uint32_t buf = sring + b * STAGE, bar = b_full + 8 * b;
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(STAGE)
+                                 : "memory");
+                    const int kx = (int)(l * Tp + ks * 128);
+                    for (int v = 0; v < 2; ++v)
+                        for (int dy = 0; dy < 8; ++dy)
+                            tma_2d(buf + (v * 8 + dy) * 1024, v ? &tm_n : &tm_c, kx,
+                                   (int)(((y0 + dy) & (L - 1)) * L + x0), bar);
+                    for (int v = 0; v < 2; ++v)
+                        for (int nyl = 0; nyl < CH_ROWS; ++nyl)
+                            for (int gx = 0; gx < GRP; ++gx) {
+                                const uint32_t py = (y0 + CH_ROWS * ch + nyl) & (L - 1);
+                                const uint32_t px = (x0 + 8 * gx + L - 8) & (L - 1);
+                                tma_2d(buf + A_BYTES + (v * CH_ROWS * GRP + nyl * GRP + gx) * 1024,
+                                       v ? &tm_n : &tm_c, kx, (int)(py * L + px), bar);
+                            }
+                }
+        }
+    } else if (warp == 5) {
+        // --------------------------------------------------------------- UMMA issuer
+        uint32_t g = 0;
+        for (int ch = 0; ch < NCHUNK; ++ch) {
+            const uint32_t ub = ch & 1, uu = ch >> 1;
+            if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
+                const uint32_t b = g % NSTAGE;
+                tc::mbar_wait(b_full + 8 * b, (g / NSTAGE) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0) {
+                    const uint32_t sa = sring + b * STAGE, sb = sa + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk),
+                                tc::idesc_u8(128, N), (ks > 0 || kk > 0) ? 1u : 0u);
+                    tc::commit(b_empty + 8 * b);
+                    if (ks + 1 == nk) tc::commit(b_tfull + 8 * ub);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp < 4) {
+        // --------------------------------------------------------------- epilogue
+        const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
+        const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
+        int* scr = scratch + (warp * 32 + lane) * SCR;
+        const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
+        int2* out2 = reinterpret_cast<int2*>(Dt + ((size_t)l * P + p) * H) + v;
+        for (int ch = 0; ch < NCHUNK; ++ch) {
+            const uint32_t ub = ch & 1, uu = ch >> 1;
+            tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
+                const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
+                uint32_t rc[32], rn[32];
+                const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub + nyl * NBX;
+                tc::ld32(ta, rc);                       // <v_p, c_q>, q in x0-8 .. x0+23 of row ny
+                tc::ld32(ta + CH_ROWS * NBX, rn);       // <v_p, cn_q>
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (oy < 0 || oy > R) continue;
+                int dc[2 * R + 1], dn[2 * R + 1];
+#pragma unroll
+                for (int j = 0; j < NBX; ++j) scr[j] = (int)rc[j];
+#pragma unroll
+                for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + 1 + i];
+#pragma unroll
+                for (int j = 0; j < NBX; ++j) scr[j] = (int)rn[j];
+#pragma unroll
+                for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + 1 + i];
+#pragma unroll
+                for (int i = 0; i < 2 * R + 1; ++i) {
+                    const int ox = i - R, nx = dx + 1 + i;
+                    if (oy == 0 && ox <= 0) continue;
+                    const int nq_c = snorm[ny * NBX + nx], nq_n = snorm[(NBR + ny) * NBX + nx];
+                    out2[2 * half_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(b_tempty + 8 * ub);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");

@@ -285,19 +285,20 @@ def test_gram_variants_bit_identical(bn, oracle_mod, L, T, levels, monkeypatch):
     a, b, px, py = synth.make_bank(T, 31)
     U = synth.make_tile(L, 32)
     outs = {}
-    for variant in ("", "tc", "imma1", "simt"):
+    for variant in ("", "tc", "tc2", "tc3", "imma1", "simt"):
         monkeypatch.setenv("BN_GRAM", variant)
         s, o, _ = make(bn, oracle_mod, L, T, levels, bank=(a, b, px, py), U=U)
         outs[variant] = s.window_distances()
     co = o.counts(U)
     for li in range(len(levels)):
         assert np.array_equal(outs[""][li], _partial_distances(co[li], L))
-    for k in ("tc", "imma1", "simt"):
+    for k in ("tc", "tc2", "tc3", "imma1", "simt"):
         assert np.array_equal(outs[k], outs[""]), k
 
 
-def test_tc_gram_optimize_parity(bn, oracle_mod, monkeypatch):
-    """Full passes with the tcgen05 window Gram against the oracle (C3 shape, ragged T)."""
-    monkeypatch.setenv("BN_GRAM", "tc")
+@pytest.mark.parametrize("variant", ["tc", "tc2", "tc3"])
+def test_tc_gram_optimize_parity(bn, oracle_mod, monkeypatch, variant):
+    """Full passes with the tcgen05 window Grams against the oracle (C3 shape, ragged T)."""
+    monkeypatch.setenv("BN_GRAM", variant)
     s, o, U = make(bn, oracle_mod, 32, 130, (1, 4, 16, 64))
     _check_run(s, o, U, 2, 0, seed=7)
