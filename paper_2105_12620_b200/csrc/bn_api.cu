@@ -152,7 +152,7 @@ struct bn_ctx {
     bool simt_gram = false;         // BN_GRAM=simt: dp4a window distances instead of IMMA
     bool gram_attr_set[8] = {false};
     bool gram2_attr_set[8] = {false};
-    bool imma_v1 = false;  // BN_GRAM=imma1: the one-strip-per-warp IMMA kernel
+    bool imma_v1 = false;  // BN_GRAM=imma1: the one-strip-per-warp IMMA kernel (BN_GRAM=imma2: v2)
     bool tc_gram = false;  // BN_GRAM=tc: tcgen05/TMEM window Gram (R = 7)
     bool tc_attr_set = false;
     bool tc2_gram = false;  // BN_GRAM=tc2: warp-specialised tcgen05 window Gram (R = 7)
@@ -349,7 +349,8 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
     return launch_lut_only<R>(ctx, write_deltas);
 }
 
-// Window Gram: tcgen05 (BN_GRAM=tc, R = 7), IMMA v2 (default), IMMA v1 (BN_GRAM=imma1), dp4a.
+// Window Gram: TMA-fed tcgen05 k_gram_tc3 (default for R = 7, BN_GRAM=tc3), tcgen05 variants tc/tc2,
+// IMMA v2 (BN_GRAM=imma2, and every R != 7), IMMA v1 (BN_GRAM=imma1), dp4a (BN_GRAM=simt).
 template <int R>
 int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     const uint32_t SW = ctx->L < 32 ? ctx->L : 32;
@@ -654,7 +655,7 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->imma_v1 = gm && !strcmp(gm, "imma1");
     ctx->tc_gram = gm && !strcmp(gm, "tc");
     ctx->tc2_gram = gm && !strcmp(gm, "tc2");
-    ctx->tc3_gram = gm && !strcmp(gm, "tc3");
+    ctx->tc3_gram = !gm || !*gm || !strcmp(gm, "tc3");  // default window Gram (R = 7)
     *out = ctx;
     return BN_OK;
 }
