@@ -145,8 +145,14 @@ def algorithmic(kernel, cfg):
     return None, None, None
 
 
-def roofline(prof, cfg, peaks, sm_clock_mhz):
-    name = max(prof, key=lambda k: prof[k][0])
+CRITICAL = ("gram", "lut", "decide", "commit", "gather")  # counts(t+1) overlaps decide(t)
+
+
+def roofline(prof, cfg, peaks, sm_clock_mhz, name=None):
+    """Roofline line of one kernel class; default: the largest on the critical path."""
+    if name is None:
+        crit = {k: v for k, v in prof.items() if k in CRITICAL} or prof
+        name = max(crit, key=lambda k: crit[k][0])
     ms, n = prof[name]
     units, kind, bound = algorithmic(name, cfg)
     share = ms / max(1e-9, sum(v[0] for v in prof.values()))
@@ -187,6 +193,9 @@ def roofline(prof, cfg, peaks, sm_clock_mhz):
         pass
     if sm_clock_mhz:
         out["sm_mhz_during_run"] = sm_clock_mhz
+    if name == "gram" and cfg.name in ("C3", "C4", "C5"):
+        out["limiter"] = ("L2->SM operand streaming: the UMMA pipe runs at its peak MAC rate when fed, "
+                          "but a TMA-only run of the same kernel takes ~85% of its time (DESIGN.md 5.3)")
     return out
 
 
@@ -335,7 +344,12 @@ def run_ours(args, cfg):
     s.optimize(args.steps, seeds[0], mode=cfg.mode, first_pass=args.warmup + args.steps, stats=False)
     prof = s.profile()
     s.profile_enable(False)
-    roof = roofline({k: v for k, v in prof.items() if v[1]}, cfg, peaks, clocks.get("sm_mhz"))
+    active = {k: v for k, v in prof.items() if v[1]}
+    roof = roofline(active, cfg, peaks, clocks.get("sm_mhz"))
+    roof_all = {}
+    for k in active:
+        r = roofline(active, cfg, peaks, None, name=k)
+        roof_all[k] = {x: r.get(x) for x in ("bound", "achieved", "peak", "unit", "frac", "avg_launch_ms")}
 
     # end to end through the public API with host buffers: per step, H2D of the tile, one pass,
     # D2H of the tile and the pass statistics (pair 0 of every rank).
@@ -381,6 +395,7 @@ def run_ours(args, cfg):
             "config": cfgj, "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
             "roofline": roof, "cpu_baseline": cpu,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+            "roofline_per_kernel": roof_all,
             "final_energy": st[-1]["E"] if st else None,
         }
         print(json.dumps(line), flush=True)
