@@ -93,36 +93,49 @@ constexpr int COUNT_PIX = 4;  // pixels per CTA (short CTAs co-schedule well on 
 // closer than that (probability ~2^-20 per test) is recounted exactly in int64.
 constexpr float COUNT_EXACT_BAND = 134217728.0f;  // 2^27
 
+// Packed fp32x2 FMA (sm_100: FFMA2), round-to-nearest on each half exactly like fmaf.
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
+}
+
+// One sample against NI integrands held as NI/2 packed pairs: t = a x + (b y - C) per lane half.
 template <int NI>
-__device__ __forceinline__ void count_sample(float2 xy, const float* af, const float* bf, const float* cf,
+__device__ __forceinline__ void count_sample(float2 xy, const unsigned long long* ab2a,
+                                             const unsigned long long* ab2b, const unsigned long long* c2,
                                              uint32_t* neg, float* mn) {
-    float t[NI];
+    const unsigned long long xx = pack2(xy.x, xy.x), yy = pack2(xy.y, xy.y);
 #pragma unroll
-    for (int j = 0; j < NI; ++j) {
-        t[j] = fmaf(af[j], xy.x, fmaf(bf[j], xy.y, cf[j]));
-        neg[j] += __float_as_uint(t[j]) >> 31;  // LEA.HI
+    for (int h = 0; h < NI / 2; ++h) {
+        const unsigned long long t = fma2(ab2a[h], xx, fma2(ab2b[h], yy, c2[h]));
+        const uint32_t lo = (uint32_t)t, hi = (uint32_t)(t >> 32);
+        neg[2 * h] += lo >> 31;  // LEA.HI
+        neg[2 * h + 1] += hi >> 31;
+        mn[h] = fminf(mn[h], fminf(fabsf(__uint_as_float(lo)), fabsf(__uint_as_float(hi))));  // FMNMX3
     }
-    // running min of |t| over pairs of integrands: one FMNMX3 per two tests
-#pragma unroll
-    for (int j = 0; j < NI; j += 2) mn[j >> 1] = fminf(mn[j >> 1], fminf(fabsf(t[j]), fabsf(t[j + 1])));
 }
 
 template <int NI>
-__device__ __forceinline__ void count_span(const float2* __restrict__ xyf, uint32_t k0, uint32_t k1, const float* af,
-                                           const float* bf, const float* cf, uint32_t* neg, float* mn) {
+__device__ __forceinline__ void count_span(const float2* __restrict__ xyf, uint32_t k0, uint32_t k1,
+                                           const unsigned long long* a2, const unsigned long long* b2,
+                                           const unsigned long long* c2, uint32_t* neg, float* mn) {
     uint32_t k = k0;
     for (; k + 4 <= k1; k += 4) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) count_sample<NI>(xyf[k + u], af, bf, cf, neg, mn);
+        for (int u = 0; u < 4; ++u) count_sample<NI>(xyf[k + u], a2, b2, c2, neg, mn);
     }
-    for (; k < k1; ++k) count_sample<NI>(xyf[k], af, bf, cf, neg, mn);
+    for (; k < k1; ++k) count_sample<NI>(xyf[k], a2, b2, c2, neg, mn);
 }
 
 // Each thread owns NI = 8 consecutive integrands (two packed 32-bit words per level row) and
 // walks the CTA's pixels; the sample loop is split at the level boundaries N_l so that the
 // inner loop is branch-free and unrolled.
 constexpr int COUNT_NI = 8;
-__global__ void __launch_bounds__(256, 3) k_counts(const uint2* __restrict__ U, uint2* __restrict__ Uout, int redraw,
+__global__ void __launch_bounds__(256, 2) k_counts(const uint2* __restrict__ U, uint2* __restrict__ Uout, int redraw,
                                                 uint64_t seed, uint32_t pass_t, uint32_t P,
                                                 const int2* __restrict__ ab, const long long* __restrict__ Cc,
                                                 uint32_t Tp, const uint2* __restrict__ S, uint32_t Nmax,
@@ -164,13 +177,13 @@ __global__ void __launch_bounds__(256, 3) k_counts(const uint2* __restrict__ U, 
     const uint32_t nsub = qn < blockDim.x ? blockDim.x / qn : 1;
     const uint32_t sub = threadIdx.x / (blockDim.x / nsub), tq = threadIdx.x % (blockDim.x / nsub);
     for (uint32_t q = tq; q < qn; q += blockDim.x / nsub) {
-        float af[NI], bf[NI], cf[NI];
+        unsigned long long a2[NI / 2], b2[NI / 2], c2[NI / 2];  // integrand pairs (2h, 2h+1)
 #pragma unroll
-        for (int j = 0; j < NI; ++j) {
-            const int2 v = ab[NI * q + j];
-            af[j] = (float)v.x;
-            bf[j] = (float)v.y;
-            cf[j] = -__ll2float_rn(Cc[NI * q + j]);
+        for (int h = 0; h < NI / 2; ++h) {
+            const int2 v0 = ab[NI * q + 2 * h], v1 = ab[NI * q + 2 * h + 1];
+            a2[h] = pack2((float)v0.x, (float)v1.x);
+            b2[h] = pack2((float)v0.y, (float)v1.y);
+            c2[h] = pack2(-__ll2float_rn(Cc[NI * q + 2 * h]), -__ll2float_rn(Cc[NI * q + 2 * h + 1]));
         }
         for (uint32_t pp = sub; pp < COUNT_PIX; pp += nsub) {
             const uint32_t p = p0 + pp;
@@ -185,7 +198,7 @@ __global__ void __launch_bounds__(256, 3) k_counts(const uint2* __restrict__ U, 
             uint32_t kprev = 0;
             for (uint32_t li = 0; li < nl; ++li) {
                 const uint32_t n1 = levels[li];
-                count_span<NI>(sXYf[pp], kprev, n1, af, bf, cf, neg, mn);
+                count_span<NI>(sXYf[pp], kprev, n1, a2, b2, c2, neg, mn);
                 kprev = n1;
                 uint32_t w[NI / 4];
                 uint32_t nsq = 0;
