@@ -1556,6 +1556,20 @@ struct LaneOffsets {
     }
 };
 
+// Exact warp sum of an int128 (two's complement, mod 2^128) with 8 REDUX.SUM instructions:
+// split into 16-bit limbs (each warp sum < 2^21 fits 32 bits), then recombine with carries.
+__device__ __forceinline__ i128 warp_sum_i128_redux(unsigned long long lo, unsigned long long hi) {
+    uint32_t s[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[i] = __reduce_add_sync(0xffffffffu, (uint32_t)(lo >> (16 * i)) & 0xffffu);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[4 + i] = __reduce_add_sync(0xffffffffu, (uint32_t)(hi >> (16 * i)) & 0xffffu);
+    u128 r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += (u128)s[i] << (16 * i);
+    return (i128)r;
+}
+
 template <int R>
 struct WinTermsLocal : WinTerms<R> {
     // sum with the flags read from this CTA's shared-memory copy
@@ -1576,15 +1590,7 @@ struct WinTermsLocal : WinTerms<R> {
                 lo = nlo;
             }
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
-            const long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
-            const unsigned long long nlo = lo + olo;
-            hi += ohi + (nlo < lo);
-            lo = nlo;
-        }
-        return ((i128)hi << 64) | (u128)lo;
+        return warp_sum_i128_redux(lo, (unsigned long long)hi);
     }
 };
 
