@@ -131,7 +131,9 @@ struct bn_ctx {
     DevBuf<uint8_t> c, cn, cn2, acc, log, cexp;
     DevBuf<int> nc, nn, nn2, derr, progress;
     DevBuf<int4> Dt;
-    DevBuf<longlong2> d0, d1b;
+    DevBuf<long long> d0, d1b;   // int64 dE terms (DT_ESC = see escape tables)
+    DevBuf<longlong2> x0, x1;    // exact int128 escape tables (sparse writes)
+    bool force_escape = false;   // BN_DT_ESCAPE=1: every term through the escape tables (tests)
     DevBuf<i128> dEp;
     DevBuf<u128> Epart;
     DevBuf<PassStatsDev> pstats;
@@ -330,6 +332,8 @@ int ensure_work(bn_ctx* ctx) {
     CUDA_TRY(ctx->Dt.ensure(P * H * ctx->nl));
     CUDA_TRY(ctx->d0.ensure(P * WN));
     CUDA_TRY(ctx->d1b.ensure(P * WN));
+    CUDA_TRY(ctx->x0.ensure(P * WN));
+    CUDA_TRY(ctx->x1.ensure(P * WN));
     CUDA_TRY(ctx->acc.ensure(P));
     CUDA_TRY(ctx->dEp.ensure(P));
     CUDA_TRY(ctx->Epart.ensure((P * H + 255) / 256));
@@ -438,7 +442,8 @@ int launch_lut_only(bn_ctx* ctx, int write_deltas) {
     {
         auto fn = ctx->nl == 4 ? k_lut<R, 4> : ctx->nl == 1 ? k_lut<R, 1> : k_lut<R, 0>;
         fn<<<(unsigned)((nthr + 255) / 256), 256, 0, ctx->ls>>>(ctx->Dt.p, ctx->L, ctx->nl, ctx->W.p, la, write_deltas,
-                                                              ctx->d0.p, ctx->d1b.p, ctx->Epart.p, ctx->derr.p);
+                                                              ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p,
+                                                              (int)ctx->force_escape, ctx->Epart.p, ctx->derr.p);
     }
     LAUNCHED_K();
     return BN_OK;
@@ -476,8 +481,8 @@ template <int R>
 int launch_decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, uint8_t* log) {
     const uint32_t M = (ctx->L / 8) * (ctx->L / 8);
     KSTART(BN_K_DECIDE);
-    k_decide<R><<<(M + 3) / 4, 128, 0, ctx->ls>>>(s, t, seed, ctx->L, mode, ctx->d0.p, ctx->d1b.p, ctx->acc.p,
-                                                      ctx->dEp.p, log);
+    const DTabs T = {ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
+    k_decide<R><<<(M + 3) / 4, 128, 0, ctx->ls>>>(s, t, seed, ctx->L, mode, T, ctx->acc.p, ctx->dEp.p, log);
     LAUNCHED_K();
     return BN_OK;
 }
@@ -493,7 +498,7 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     const uint32_t ncta = nb * nb / cpc;
     *done = false;
     if (ncta > 16 || ctx->no_cluster) return BN_OK;
-    const size_t smem = (size_t)(mode ? 2 : 1) * cpc * 2 * WN * 16 + P;
+    const size_t smem = (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8 + P;  // double-buffered int64 rows + flags
     const void* fn = mode ? (const void*)k_decide_cluster<R, 1> : (const void*)k_decide_cluster<R, 0>;
     if (!ctx->cluster_attr_set[R]) {
         for (const void* f : {(const void*)k_decide_cluster<R, 0>, (const void*)k_decide_cluster<R, 1>}) {
@@ -520,11 +525,10 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
         return BN_OK;  // cluster does not fit: persistent flag kernel instead
     }
     uint32_t L = ctx->L;
-    const longlong2* d0 = ctx->d0.p;
-    const longlong2* d1 = ctx->d1b.p;
+    const DTabs T = {ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
     uint8_t* acc = ctx->acc.p;
     i128* dEp = ctx->dEp.p;
-    void* args[] = {&t, &seed, &L, &cpc, &d0, &d1, &acc, &dEp, &log};
+    void* args[] = {&t, &seed, &L, &cpc, (void*)&T, &acc, &dEp, &log};
     KSTART(BN_K_DECIDE);
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return fail(ctx, BN_ECUDA, "cluster decide launch: %s", cudaGetErrorString(e));
@@ -543,7 +547,7 @@ int launch_decide_pass(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t
     uint32_t cpc = mode ? 8 : 16;
     while (cpc > nb) cpc /= 2;
     const uint32_t ncta = nb * nb / cpc;
-    const size_t smem = (size_t)(mode ? 2 : 1) * cpc * 2 * WN * 16;
+    const size_t smem = (size_t)(mode ? 2 : 1) * cpc * 2 * WN * 8;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
     if (ncta > (uint32_t)nsm || nb > 512) {
@@ -559,12 +563,11 @@ int launch_decide_pass(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t
     CUDA_TRY(ctx->progress.ensure(ncta));
     CUDA_TRY(cudaMemsetAsync(ctx->progress.p, 0, ncta * sizeof(int), ctx->ls));
     uint32_t L = ctx->L;
-    const longlong2* d0 = ctx->d0.p;
-    const longlong2* d1 = ctx->d1b.p;
+    const DTabs T = {ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
     uint8_t* acc = ctx->acc.p;
     i128* dEp = ctx->dEp.p;
     int* prog = ctx->progress.p;
-    void* args[] = {&t, &seed, &L, &cpc, &d0, &d1, &acc, &dEp, &log, &prog};
+    void* args[] = {&t, &seed, &L, &cpc, (void*)&T, &acc, &dEp, &log, &prog};
     KSTART(BN_K_DECIDE);
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(ncta), dim3(32 * cpc), args, smem, ctx->ls);
     if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
@@ -650,6 +653,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
             return BN_ECUDA;
         }
     }
+    const char* esc = getenv("BN_DT_ESCAPE");
+    ctx->force_escape = esc && !strcmp(esc, "1");
     const char* gm = getenv("BN_GRAM");
     ctx->simt_gram = gm && !strcmp(gm, "simt");
     ctx->imma_v1 = gm && !strcmp(gm, "imma1");
@@ -669,7 +674,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->S.release(); ctx->U.release(); ctx->Un.release(); ctx->pxy.release(); ctx->ab.release();
         ctx->Cc.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
         ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
-        ctx->d0.release(); ctx->d1b.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
+        ctx->d0.release(); ctx->d1b.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
         ctx->W.release(); ctx->G.release(); ctx->iref.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release();

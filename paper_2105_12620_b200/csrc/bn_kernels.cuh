@@ -1219,6 +1219,31 @@ __device__ __forceinline__ unsigned long long qterm(double w, const double* __re
     return __double2ull_rn(__dmul_rn(__dmul_rn(w, __ldg(G + D)), 18446744073709551616.0));
 }
 
+// dE terms are stored as int64 when the exact int128 value fits (the common case); otherwise the
+// int64 slot holds the sentinel DT_ESC and the exact value goes to the int128 escape table at the
+// same index (written only then).  Halves the bytes the decisions stage per colour class.
+constexpr long long DT_ESC = (long long)0x8000000000000000ull;
+__device__ __forceinline__ void put_term(long long* d, longlong2* x, size_t idx, i128 v, int force) {
+    const bool fits = v > (i128)DT_ESC && v <= (i128)0x7fffffffffffffffll;
+    if (fits && !force) {
+        d[idx] = (long long)v;
+    } else {
+        d[idx] = DT_ESC;
+        x[idx] = make_longlong2((long long)(unsigned long long)v, (long long)(v >> 64));
+    }
+}
+__device__ __forceinline__ i128 get_term(long long v, const longlong2* __restrict__ x, size_t idx) {
+    if (v != DT_ESC) return (i128)v;
+    const longlong2 e = x[idx];
+    return ((i128)e.y << 64) | (u128)(unsigned long long)e.x;
+}
+struct DTabs {
+    const long long* d0;
+    const long long* d1;
+    const longlong2* x0;
+    const longlong2* x1;
+};
+
 struct LutArgs {
     const double* G[8];  // per-level G tables
     int Dmax[8];         // largest legal D per level (guards corrupted distances)
@@ -1228,7 +1253,8 @@ struct LutArgs {
 template <int R, int NL>
 __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32_t L, uint32_t nl_rt,
                                              const double* __restrict__ W, LutArgs lut, int write_deltas,
-                                             longlong2* __restrict__ d0, longlong2* __restrict__ d1,
+                                             long long* __restrict__ d0, long long* __restrict__ d1,
+                                             longlong2* __restrict__ x0, longlong2* __restrict__ x1, int force_escape,
                                              u128* __restrict__ Epart, int* __restrict__ err) {
     constexpr int H = 2 * R * R + 2 * R;
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
@@ -1276,10 +1302,10 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
         }
         e *= 2;  // ordered pairs (p,q) and (q,p)
         if (write_deltas) {
-            d0[(size_t)p * WN + wi] = make_longlong2((long long)(unsigned long long)a0, (long long)(a0 >> 64));
-            d1[(size_t)p * WN + wi] = make_longlong2((long long)(unsigned long long)a1, (long long)(a1 >> 64));
-            d0[(size_t)q * WN + wm] = make_longlong2((long long)(unsigned long long)b0, (long long)(b0 >> 64));
-            d1[(size_t)q * WN + wm] = make_longlong2((long long)(unsigned long long)b1, (long long)(b1 >> 64));
+            put_term(d0, x0, (size_t)p * WN + wi, a0, force_escape);
+            put_term(d1, x1, (size_t)p * WN + wi, a1, force_escape);
+            put_term(d0, x0, (size_t)q * WN + wm, b0, force_escape);
+            put_term(d1, x1, (size_t)q * WN + wm, b1, force_escape);
         }
     }
     // block reduction of e (u128) through shared memory
@@ -1298,8 +1324,7 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
 // Colour class s of pass t: one warp per active index m (SWAP: the lower index of a couple).
 // dE_p = 2 * sum_{o in W} (acc[p+o] ? d1 : d0)[p][o]; accept iff dE < 0.
 template <int R>
-__device__ __forceinline__ i128 window_sum(const longlong2* __restrict__ d0, const longlong2* __restrict__ d1,
-                                           const uint8_t* __restrict__ acc, uint32_t L, uint32_t p) {
+__device__ __forceinline__ i128 window_sum(const DTabs T, const uint8_t* __restrict__ acc, uint32_t L, uint32_t p) {
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     const int lane = threadIdx.x & 31;
     const uint32_t x = p % L, y = p / L;
@@ -1308,8 +1333,8 @@ __device__ __forceinline__ i128 window_sum(const longlong2* __restrict__ d0, con
         const int ww = w >= R * (2 * R + 1) + R ? w + 1 : w;
         const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
         const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
-        const longlong2 v = acc[q] ? d1[(size_t)p * WN + w] : d0[(size_t)p * WN + w];
-        s += ((i128)v.y << 64) | (u128)(unsigned long long)v.x;
+        const size_t idx = (size_t)p * WN + w;
+        s += acc[q] ? get_term(T.d1[idx], T.x1, idx) : get_term(T.d0[idx], T.x0, idx);
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
@@ -1321,15 +1346,14 @@ __device__ __forceinline__ i128 window_sum(const longlong2* __restrict__ d0, con
 }
 
 template <int R>
-__global__ void k_decide(uint32_t s, uint32_t pass_t, uint64_t seed, uint32_t L, int mode,
-                         const longlong2* __restrict__ d0, const longlong2* __restrict__ d1, uint8_t* __restrict__ acc,
-                         i128* __restrict__ dEp, uint8_t* __restrict__ log) {
+__global__ void k_decide(uint32_t s, uint32_t pass_t, uint64_t seed, uint32_t L, int mode, const DTabs T,
+                         uint8_t* __restrict__ acc, i128* __restrict__ dEp, uint8_t* __restrict__ log) {
     const uint32_t M = (L / 8) * (L / 8);
     const uint32_t m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (m >= M) return;
     const uint32_t p = class_pixel(L, seed, pass_t, s, m);
     if (mode == 0) {
-        const i128 dE = 2 * window_sum<R>(d0, d1, acc, L, p);
+        const i128 dE = 2 * window_sum<R>(T, acc, L, p);
         if ((threadIdx.x & 31) == 0) {
             const bool ok = dE < 0;
             acc[p] = ok;
@@ -1340,7 +1364,7 @@ __global__ void k_decide(uint32_t s, uint32_t pass_t, uint64_t seed, uint32_t L,
         const uint32_t mm = m ^ swap_kappa(seed, pass_t, s, M);
         if (mm < m) return;
         const uint32_t p2 = class_pixel(L, seed, pass_t, s, mm);
-        const i128 dE = 2 * (window_sum<R>(d0, d1, acc, L, p) + window_sum<R>(d0, d1, acc, L, p2));
+        const i128 dE = 2 * (window_sum<R>(T, acc, L, p) + window_sum<R>(T, acc, L, p2));
         if ((threadIdx.x & 31) == 0) {
             const bool ok = dE < 0;
             acc[p] = ok;
@@ -1376,9 +1400,9 @@ template <int R>
 struct WinTerms {
     static constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     static constexpr int PER = (WN + 31) / 32;
-    longlong2 v0[PER], v1[PER];
-    // from the shared-memory staging buffer: rows [WN] of delta0 then [WN] of delta1
-    __device__ __forceinline__ void load_smem(const longlong2* row) {
+    long long v0[PER], v1[PER];
+    // from the shared-memory staging buffer: a row of WN delta0 terms then WN delta1 terms
+    __device__ __forceinline__ void load_smem(const long long* row) {
         const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
@@ -1390,7 +1414,7 @@ struct WinTerms {
         }
     }
     // sum_w (acc[p + o_w] ? d1 : d0), reduced over the warp (every lane gets the total)
-    __device__ __forceinline__ i128 sum(const uint8_t* acc, uint32_t L, uint32_t p) const {
+    __device__ __forceinline__ i128 sum(const uint8_t* acc, uint32_t L, uint32_t p, const DTabs T) const {
         const int lane = threadIdx.x & 31;
         const uint32_t x = p % L, y = p / L;
         uint8_t f[PER];
@@ -1410,8 +1434,8 @@ struct WinTerms {
         for (int j = 0; j < PER; ++j) {
             const int w = lane + 32 * j;
             if (w < WN) {
-                const longlong2 v = f[j] ? v1[j] : v0[j];
-                s += ((i128)v.y << 64) | (u128)(unsigned long long)v.x;
+                const size_t idx = (size_t)p * WN + w;
+                s += f[j] ? get_term(v1[j], T.x1, idx) : get_term(v0[j], T.x0, idx);
             }
         }
 #pragma unroll
@@ -1426,19 +1450,19 @@ struct WinTerms {
 
 // Stage the dE-term rows (delta0, delta1) of the candidates of CTA `g` for class s into smem.
 // Slot j holds candidate m = first + j (and, for SWAP, slot cpc + j its partner's rows); warp w
-// copies slots w, w + nwarps, ... (row = WN delta0 terms then WN delta1 terms, 16 B each).
+// copies slots w, w + nwarps, ... (row = WN int64 delta0 terms then WN delta1 terms).
 template <int R>
 __device__ __forceinline__ void stage_class(uint32_t smem_base, const uint32_t* slot_pix, uint32_t nslot,
-                                            const longlong2* __restrict__ d0, const longlong2* __restrict__ d1) {
-    constexpr int WN = WinTerms<R>::WN;
+                                            const DTabs T) {
+    constexpr int WN = WinTerms<R>::WN, NC = WN / 2;  // 16-B chunks per table row
     const uint32_t warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t slot = warp; slot < nslot; slot += nwarps) {
         const size_t off = (size_t)slot_pix[slot] * WN;
-        const uint32_t dst = smem_base + slot * 2 * WN * 16;
+        const uint32_t dst = smem_base + slot * 2 * WN * 8;
 #pragma unroll
-        for (uint32_t w = lane; w < (uint32_t)WN; w += 32) {
-            cp_async16(dst + w * 16, d0 + off + w);
-            cp_async16(dst + (WN + w) * 16, d1 + off + w);
+        for (uint32_t c = lane; c < (uint32_t)NC; c += 32) {
+            cp_async16(dst + c * 16, T.d0 + off + 2 * c);
+            cp_async16(dst + (NC + c) * 16, T.d1 + off + 2 * c);
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -1451,8 +1475,7 @@ __device__ __forceinline__ void stage_class(uint32_t smem_base, const uint32_t* 
 // (4) reads the neighbours' accept flags, reduces, decides, and publishes progress s+1.
 template <int R, int mode>
 __global__ void __launch_bounds__(512, 1) k_decide_pass(uint32_t pass_t, uint64_t seed, uint32_t L,
-                                                        uint32_t cpc, const longlong2* __restrict__ d0,
-                                                        const longlong2* __restrict__ d1, uint8_t* acc,
+                                                        uint32_t cpc, const DTabs T, uint8_t* acc,
                                                         i128* __restrict__ dEp, uint8_t* __restrict__ log,
                                                         int* progress) {
     constexpr int WN = WinTerms<R>::WN;
@@ -1461,7 +1484,7 @@ __global__ void __launch_bounds__(512, 1) k_decide_pass(uint32_t pass_t, uint64_
     __shared__ uint32_t sKappa[64];
     __shared__ uint32_t sSlot[2][32];       // pixels of the staged slots, double indexed by class parity
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(dsm);
-    const longlong2* srows = reinterpret_cast<const longlong2*>(dsm);
+    const long long* srows = reinterpret_cast<const long long*>(dsm);
     const uint32_t nb = L / 8, M = nb * nb;
     const uint32_t g = blockIdx.x, ncta = gridDim.x, per_band = nb / cpc;
     const uint32_t first = g * cpc, nslot = mode ? 2 * cpc : cpc;
@@ -1481,7 +1504,7 @@ __global__ void __launch_bounds__(512, 1) k_decide_pass(uint32_t pass_t, uint64_
     };
     slot_pixels(0, sSlot[0]);
     __syncthreads();
-    stage_class<R>(sbase, sSlot[0], nslot, d0, d1);
+    stage_class<R>(sbase, sSlot[0], nslot, T);
     for (uint32_t s = 0; s < 64; ++s) {
         if (s + 1 < 64) slot_pixels(s + 1, sSlot[(s + 1) & 1]);
         asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -1495,7 +1518,7 @@ __global__ void __launch_bounds__(512, 1) k_decide_pass(uint32_t pass_t, uint64_
         A.load_smem(srows + (size_t)j * 2 * WN);
         if (mode) B.load_smem(srows + (size_t)(cpc + j) * 2 * WN);
         __syncthreads();
-        if (s + 1 < 64) stage_class<R>(sbase, sSlot[(s + 1) & 1], nslot, d0, d1);
+        if (s + 1 < 64) stage_class<R>(sbase, sSlot[(s + 1) & 1], nslot, T);
         if (lane == 0 && s > 0) {
             const uint32_t bs[2] = {m / nb, mm / nb};
             for (int t = 0; t < (mode ? 2 : 1); ++t)
@@ -1510,8 +1533,8 @@ __global__ void __launch_bounds__(512, 1) k_decide_pass(uint32_t pass_t, uint64_
         }
         __syncwarp();
         __threadfence();
-        i128 sum = A.sum(acc, L, p);
-        if (mode) sum += B.sum(acc, L, p2);
+        i128 sum = A.sum(acc, L, p, T);
+        if (mode) sum += B.sum(acc, L, p2, T);
         const i128 dE = 2 * sum;
         if (lane == 0) {
             const bool ok = dE < 0;
@@ -1573,31 +1596,34 @@ __device__ __forceinline__ i128 warp_sum_i128_redux(unsigned long long lo, unsig
 template <int R>
 struct WinTermsLocal : WinTerms<R> {
     // sum with the flags read from this CTA's shared-memory copy
-    __device__ __forceinline__ i128 sum_local(const uint8_t* sflags, uint32_t L, uint32_t p,
-                                              const LaneOffsets<R>& off) const {
+    __device__ __forceinline__ i128 sum_local(const uint8_t* sflags, uint32_t L, uint32_t p, const LaneOffsets<R>& off,
+                                              const DTabs T) const {
         constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
         const int lane = threadIdx.x & 31;
         const uint32_t x = p & (L - 1), y = p / L;
-        unsigned long long lo = 0;
-        long long hi = 0;
+        i128 acc = 0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
-            if (lane + 32 * j < WN) {
+            const int w = lane + 32 * j;
+            if (w < WN) {
                 const uint32_t q = ((y + off.oy[j]) & (L - 1)) * L + ((x + off.ox[j]) & (L - 1));
-                const longlong2 v = sflags[q] ? this->v1[j] : this->v0[j];
-                const unsigned long long nlo = lo + (unsigned long long)v.x;
-                hi += v.y + (nlo < lo);
-                lo = nlo;
+                const bool f = sflags[q];
+                const long long v = f ? this->v1[j] : this->v0[j];
+                if (v != DT_ESC) {
+                    acc += (i128)v;
+                } else {  // rare: exact int128 term from the escape table
+                    const longlong2 e = (f ? T.x1 : T.x0)[(size_t)p * WN + w];
+                    acc += ((i128)e.y << 64) | (u128)(unsigned long long)e.x;
+                }
             }
         }
-        return warp_sum_i128_redux(lo, (unsigned long long)hi);
+        return warp_sum_i128_redux((unsigned long long)acc, (unsigned long long)(acc >> 64));
     }
 };
 
 template <int R, int mode>
 __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
-                                                           const longlong2* __restrict__ d0,
-                                                           const longlong2* __restrict__ d1, uint8_t* __restrict__ acc,
+                                                           const DTabs T, uint8_t* __restrict__ acc,
                                                            i128* __restrict__ dEp, uint8_t* __restrict__ log) {
     constexpr int WN = WinTerms<R>::WN;
     extern __shared__ __align__(16) uint8_t dsm[];
@@ -1607,11 +1633,10 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
     const uint32_t nb = L / 8, M = nb * nb, P = L * L;
     const uint32_t g = blockIdx.x, ncta = gridDim.x;
     const uint32_t first = g * cpc, nslot = mode ? 2 * cpc : cpc;
-    const uint32_t rows_bytes = nslot * 2 * WN * 16;
-    uint8_t* sflags = dsm + rows_bytes;  // [P] accept flags of the whole tile (this pass)
+    const uint32_t buf_bytes = nslot * 2 * WN * 8;  // int64 delta0 + delta1 rows per slot
+    uint8_t* sflags = dsm + 2 * buf_bytes;         // [P] accept flags of the whole tile (this pass)
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(dsm);
-    const uint32_t sflags_addr = sbase + rows_bytes;
-    const longlong2* srows = reinterpret_cast<const longlong2*>(dsm);
+    const uint32_t sflags_addr = sbase + 2 * buf_bytes;
     const uint32_t warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
@@ -1629,25 +1654,34 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
     };
     slot_pixels(0, sSlot[0]);
     __syncthreads();
-    stage_class<R>(sbase, sSlot[0], nslot, d0, d1);
+    stage_class<R>(sbase, sSlot[0], nslot, T);
     LaneOffsets<R> off;
     off.init();
     cluster_sync_all();  // every CTA's flag copy is initialised before any remote store
     for (uint32_t s = 0; s < 64; ++s) {
-        if (s + 1 < 64) slot_pixels(s + 1, sSlot[(s + 1) & 1]);
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
+        // double-buffered staging: class s+1 goes to buffer (s+1)&1, last read in class s-1
+        // (the cluster barrier that ended class s-1 orders those reads before these copies)
+        if (s + 1 < 64) {
+            slot_pixels(s + 1, sSlot[(s + 1) & 1]);
+            __syncwarp();
+            __syncthreads();  // sSlot[(s+1)&1] visible to the staging warps
+            stage_class<R>(sbase + ((s + 1) & 1) * buf_bytes, sSlot[(s + 1) & 1], nslot, T);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();  // class s's staged rows visible to every warp
+        const uint32_t b = s & 1;
         const uint32_t j = warp;
         const uint32_t kappa = mode ? sKappa[s] : 0;
         const uint32_t m = first + j, mm = m ^ kappa;
-        const uint32_t p = sSlot[s & 1][j], p2 = mode ? sSlot[s & 1][cpc + j] : p;
+        const uint32_t p = sSlot[b][j], p2 = mode ? sSlot[b][cpc + j] : p;
+        const long long* rows = reinterpret_cast<const long long*>(dsm + b * buf_bytes);
         WinTermsLocal<R> A, B;
-        A.load_smem(srows + (size_t)j * 2 * WN);
-        if (mode) B.load_smem(srows + (size_t)(cpc + j) * 2 * WN);
-        __syncthreads();
-        if (s + 1 < 64) stage_class<R>(sbase, sSlot[(s + 1) & 1], nslot, d0, d1);
-        i128 sum = A.sum_local(sflags, L, p, off);
-        if (mode) sum += B.sum_local(sflags, L, p2, off);
+        A.load_smem(rows + (size_t)j * 2 * WN);
+        if (mode) B.load_smem(rows + (size_t)(cpc + j) * 2 * WN);
+        i128 sum = A.sum_local(sflags, L, p, off, T);
+        if (mode) sum += B.sum_local(sflags, L, p2, off, T);
         const bool ok = 2 * sum < 0;
         if (ok && (uint32_t)lane < ncta) st_cluster_u8(sflags_addr + p, lane, 1);  // incl. own copy
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");

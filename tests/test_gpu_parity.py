@@ -302,3 +302,15 @@ def test_tc_gram_optimize_parity(bn, oracle_mod, monkeypatch, variant):
     monkeypatch.setenv("BN_GRAM", variant)
     s, o, U = make(bn, oracle_mod, 32, 130, (1, 4, 16, 64))
     _check_run(s, o, U, 2, 0, seed=7)
+
+
+@pytest.mark.parametrize("decide", ["", "flags", "per_class"])
+def test_escape_path_all_terms(bn, oracle_mod, monkeypatch, decide):
+    """dE terms are int64 with an int128 escape; forcing every term through the escape tables
+    (BN_DT_ESCAPE=1) must give the same bit-exact passes on every decision kernel."""
+    monkeypatch.setenv("BN_DT_ESCAPE", "1")
+    monkeypatch.setenv("BN_DECIDE", decide)
+    s, o, U = make(bn, oracle_mod, 32, 100, (4, 16))
+    _check_run(s, o, U, 2, 0, seed=13)
+    s2, o2, U2 = make(bn, oracle_mod, 32, 60, (4,))
+    _check_run(s2, o2, U2, 2, 1, seed=14)
