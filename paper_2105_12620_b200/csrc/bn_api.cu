@@ -84,6 +84,23 @@ bool make_count_map(CUtensorMap* m, const void* base, uint64_t rowB, uint64_t P)
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3D map over the [y][x][levels*Tp] count tensor with a {128, bx, by} box, 128-B swizzle.
+bool make_count_map3(CUtensorMap* m, const void* base, uint64_t rowB, uint64_t L, uint32_t bx, uint32_t by) {
+    encode_tiled_t enc = get_encode_tiled();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {rowB, L, L};
+    cuuint64_t strides[2] = {rowB, L * rowB};
+    cuuint32_t box[3] = {128, bx, by};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool make_count_maps(CountMaps* m, const void* base, uint64_t rowB, uint64_t L) {
+    return make_count_map3(&m->a, base, rowB, L, 8, 8) && make_count_map3(&m->b, base, rowB, L, 24, 5) &&
+           make_count_map3(&m->s, base, rowB, L, 8, 1);
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -360,8 +377,8 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     const uint32_t SW = ctx->L < 32 ? ctx->L : 32;
     dim3 grid(ctx->L / SW, ctx->L);
     if (R == 7 && ctx->tc3_gram) {
-        CUtensorMap mc, mn;
-        if (!make_count_map(&mc, ctx->c.p, ctx->rowB, ctx->P) || !make_count_map(&mn, cn, ctx->rowB, ctx->P))
+        CountMaps mc, mn;
+        if (!make_count_maps(&mc, ctx->c.p, ctx->rowB, ctx->L) || !make_count_maps(&mn, cn, ctx->rowB, ctx->L))
             return fail(ctx, BN_ECUDA, "cuTensorMapEncodeTiled failed");
         const int smem = tc3::SMEM;
         if (!ctx->tc3_attr_set) {

@@ -1067,8 +1067,22 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int
         : "memory");
 }
 
-__global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_constant__ CUtensorMap tm_c,
-                                                              const __grid_constant__ CUtensorMap tm_n,
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
+        : "memory");
+}
+// Tensor maps over the [y][x][K] count tensor (3D, K innermost): box A = {128, 8, 8} (a whole
+// 8x8 block = 64 rows), box B = {128, 24, 5} (a whole neighbour chunk, no wrap), box S =
+// {128, 8, 1} (8 pixels of one row, used where a toroidal wrap splits a chunk).
+struct CountMaps {
+    CUtensorMap a, b, s;
+};
+
+__global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_constant__ CountMaps mc,
+                                                              const __grid_constant__ CountMaps mn,
                                                               const int* __restrict__ nc, const int* __restrict__ nn,
                                                               uint32_t L, uint32_t Tp, uint32_t nl,
                                                               int4* __restrict__ Dt) {
@@ -1126,18 +1140,22 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_const
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(STAGE)
                                  : "memory");
                     const int kx = (int)(l * Tp + ks * 128);
-                    for (int v = 0; v < 2; ++v)
-                        for (int dy = 0; dy < 8; ++dy)
-                            tma_2d(buf + (v * 8 + dy) * 1024, v ? &tm_n : &tm_c, kx,
-                                   (int)(((y0 + dy) & (L - 1)) * L + x0), bar);
-                    for (int v = 0; v < 2; ++v)
-                        for (int nyl = 0; nyl < CH_ROWS; ++nyl)
-                            for (int gx = 0; gx < GRP; ++gx) {
-                                const uint32_t py = (y0 + CH_ROWS * ch + nyl) & (L - 1);
-                                const uint32_t px = (x0 + 8 * gx + L - 8) & (L - 1);
-                                tma_2d(buf + A_BYTES + (v * CH_ROWS * GRP + nyl * GRP + gx) * 1024,
-                                       v ? &tm_n : &tm_c, kx, (int)(py * L + px), bar);
-                            }
+                    const bool whole = x0 >= 8 && x0 + 16 <= L && y0 + CH_ROWS * (ch + 1) <= L;
+                    for (int v = 0; v < 2; ++v) {
+                        const CountMaps& m = v ? mn : mc;
+                        tma_3d(buf + v * 8192, &m.a, kx, (int)x0, (int)y0, bar);  // 64 block rows
+                        const uint32_t bdst = buf + A_BYTES + v * CH_ROWS * GRP * 1024;
+                        if (whole) {
+                            tma_3d(bdst, &m.b, kx, (int)x0 - 8, (int)(y0 + CH_ROWS * ch), bar);
+                        } else {
+                            for (int nyl = 0; nyl < CH_ROWS; ++nyl)
+                                for (int gx = 0; gx < GRP; ++gx) {
+                                    const uint32_t py = (y0 + CH_ROWS * ch + nyl) & (L - 1);
+                                    const uint32_t px = (x0 + 8 * gx + L - 8) & (L - 1);
+                                    tma_3d(bdst + (nyl * GRP + gx) * 1024, &m.s, kx, (int)px, (int)py, bar);
+                                }
+                        }
+                    }
                 }
         }
     } else if (warp == 5) {
