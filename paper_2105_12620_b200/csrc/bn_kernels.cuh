@@ -1117,12 +1117,6 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_const
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    // neighbourhood norms of this level (rows y0 .. y0+14, columns x0-8 .. x0+15)
-    for (int j = threadIdx.x; j < 2 * NBR * NBX; j += blockDim.x) {
-        const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;
-        const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - 8) & (L - 1);
-        snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
-    }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1183,6 +1177,14 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_const
         }
     } else if (warp < 4) {
         // --------------------------------------------------------------- epilogue
+        // neighbourhood norms of this level (rows y0 .. y0+14, columns x0-8 .. x0+15), loaded while
+        // the producer and the MMA warp already run
+        for (int j = threadIdx.x; j < 2 * NBR * NBX; j += 128) {
+            const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;
+            const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - 8) & (L - 1);
+            snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
+        }
+        named_bar(2, 128);
         const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
         const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
         int* scr = scratch + (warp * 32 + lane) * SCR;
