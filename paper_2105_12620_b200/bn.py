@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbn.so")
+LIB_PATH = os.environ.get("BN_LIB") or os.path.join(_HERE, "libbn.so")  # BN_LIB: an experiment build
 
 BN_OK, BN_EINVAL, BN_ECUDA, BN_ENCCL, BN_ENOMEM, BN_ESTATE = range(6)
 REDRAW, SWAP = 0, 1

@@ -27,20 +27,26 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS)
-    if force or stale:
-        cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB, *SRC, "-ldl"]
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines: tuple[str, ...] = ()) -> str:
+    """Compile `out` (default: the in-tree libbn.so).  `defines` (-D...) build experiment variants
+    under another name, loaded with BN_LIB=<path>."""
+    stale = not os.path.exists(out) or any(os.path.getmtime(d) > os.path.getmtime(out) for d in DEPS)
+    if force or stale or defines:
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SRC, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc failed building libbn.so")
         if verbose:
             sys.stderr.write(r.stderr)
-        with open(os.path.join(HERE, "build_ptxas.log"), "w") as f:
-            f.write(r.stderr)
-    return LIB
+        if out == LIB:
+            with open(os.path.join(HERE, "build_ptxas.log"), "w") as f:
+                f.write(r.stderr)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = sys.argv[1:]
+    out = args[args.index("-o") + 1] if "-o" in args else LIB
+    defs = tuple(a[2:] for a in args if a.startswith("-D"))
+    print(build(force="--force" in args, verbose=True, out=out, defines=defs))

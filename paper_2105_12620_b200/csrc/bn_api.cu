@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -145,6 +146,7 @@ struct bn_ctx {
     DevBuf<uint2> S, U, Un, Un2, pxy;
     DevBuf<int2> ab;
     DevBuf<long long> Cc;
+    DevBuf<CountGroup> cgrp;  // packed fp32 operands of the filtered count test
     DevBuf<uint8_t> c, cn, cn2, acc, log, cexp;
     DevBuf<int> nc, nn, nn2, derr, progress;
     DevBuf<int4> Dt;
@@ -167,6 +169,7 @@ struct bn_ctx {
     cudaStream_t ls = nullptr, aux = nullptr, hp = nullptr;
     cudaEvent_t evA = nullptr, evB = nullptr, evC = nullptr;
     bool no_overlap = false;  // BN_OVERLAP=0: no candidate prefetch on the aux stream
+    bool prefetch_after_lut = false;  // BN_PREFETCH=lut: prefetch after the energy terms (not the Gram)
     bool per_class_decide = false;  // BN_DECIDE=per_class: 64 launches instead of one persistent
     bool simt_gram = false;         // BN_GRAM=simt: dp4a window distances instead of IMMA
     bool gram_attr_set[8] = {false};
@@ -333,7 +336,7 @@ int ensure_counts(bn_ctx* ctx) {
     const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
     KSTART(BN_K_COUNTS);
     k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->ls>>>(
-        ctx->U.p, nullptr, 0, 0, 0, P, ctx->ab.p, ctx->Cc.p, ctx->Tp, ctx->S.p, Nmax, lo, hi, ctx->nl, ctx->c.p,
+        ctx->U.p, nullptr, 0, 0, 0, P, ctx->ab.p, ctx->Cc.p, ctx->cgrp.p, ctx->Tp, ctx->S.p, Nmax, lo, hi, ctx->nl, ctx->c.p,
         ctx->nc.p);
     LAUNCHED_K();
     ctx->counts_dirty = false;
@@ -364,9 +367,11 @@ template <int R>
 int launch_lut_only(bn_ctx* ctx, int write_deltas);
 
 template <int R>
-int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas) {
+int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas,
+                    const std::function<int()>* after_gram) {
     int rc = launch_gram<R>(ctx, cn, nn);
     if (rc) return rc;
+    if (after_gram && (rc = (*after_gram)())) return rc;
     return launch_lut_only<R>(ctx, write_deltas);
 }
 
@@ -482,15 +487,17 @@ int gram_only(bn_ctx* ctx) {
     }
 }
 
-int gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas) {
+// `after_gram` (optional) is called between the Gram and the energy-term launches.
+int gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas,
+             const std::function<int()>* after_gram = nullptr) {
     switch (ctx->R) {
-        case 1: return launch_gram_lut<1>(ctx, cn, nn, write_deltas);
-        case 2: return launch_gram_lut<2>(ctx, cn, nn, write_deltas);
-        case 3: return launch_gram_lut<3>(ctx, cn, nn, write_deltas);
-        case 4: return launch_gram_lut<4>(ctx, cn, nn, write_deltas);
-        case 5: return launch_gram_lut<5>(ctx, cn, nn, write_deltas);
-        case 6: return launch_gram_lut<6>(ctx, cn, nn, write_deltas);
-        default: return launch_gram_lut<7>(ctx, cn, nn, write_deltas);
+        case 1: return launch_gram_lut<1>(ctx, cn, nn, write_deltas, after_gram);
+        case 2: return launch_gram_lut<2>(ctx, cn, nn, write_deltas, after_gram);
+        case 3: return launch_gram_lut<3>(ctx, cn, nn, write_deltas, after_gram);
+        case 4: return launch_gram_lut<4>(ctx, cn, nn, write_deltas, after_gram);
+        case 5: return launch_gram_lut<5>(ctx, cn, nn, write_deltas, after_gram);
+        case 6: return launch_gram_lut<6>(ctx, cn, nn, write_deltas, after_gram);
+        default: return launch_gram_lut<7>(ctx, cn, nn, write_deltas, after_gram);
     }
 }
 
@@ -655,6 +662,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->no_cluster = dm && !strcmp(dm, "flags");
     const char* ov = getenv("BN_OVERLAP");
     ctx->no_overlap = ov && !strcmp(ov, "0");
+    const char* pfe = getenv("BN_PREFETCH");
+    ctx->prefetch_after_lut = pfe && !strcmp(pfe, "lut");
     ctx->ls = ctx->stream;
     {
         DeviceGuard g(cuda_device);
@@ -689,7 +698,7 @@ void bn_destroy(bn_ctx* ctx) {
         cudaStreamSynchronize(ctx->stream);
         if (ctx->comm && g_nccl.destroy) g_nccl.destroy(ctx->comm);
         ctx->S.release(); ctx->U.release(); ctx->Un.release(); ctx->pxy.release(); ctx->ab.release();
-        ctx->Cc.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
+        ctx->Cc.release(); ctx->cgrp.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
         ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
         ctx->d0.release(); ctx->d1b.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
         ctx->W.release(); ctx->G.release(); ctx->iref.release();
@@ -770,6 +779,9 @@ int bn_set_bank(bn_ctx* ctx, uint32_t T, const int32_t* a, const int32_t* b, con
     CUDA_TRY(cudaMemcpyAsync(ctx->ab.p, ab.data(), ctx->Tp * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
     CUDA_TRY(cudaMemcpyAsync(ctx->Cc.p, C.data(), ctx->Tp * sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
     CUDA_TRY(cudaMemcpyAsync(ctx->pxy.p, pxy.data(), ctx->Ts * sizeof(uint2), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(ctx->cgrp.ensure(ctx->Tp / COUNT_NI));
+    k_count_prep<<<(ctx->Tp / COUNT_NI + 127) / 128, 128, 0, ctx->stream>>>(ctx->ab.p, ctx->Cc.p, ctx->Tp, ctx->cgrp.p);
+    LAUNCHED();
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     ctx->have_bank = true;
     ctx->counts_dirty = true;
@@ -916,7 +928,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     auto launch_counts = [&](uint32_t pi) -> int {
         KSTART(BN_K_COUNTS);
         k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->ls>>>(
-            nullptr, buf_U(pi), 1, prm->seed, prm->first_pass + pi, P, ctx->ab.p, ctx->Cc.p, ctx->Tp, ctx->S.p,
+            nullptr, buf_U(pi), 1, prm->seed, prm->first_pass + pi, P, ctx->ab.p, ctx->Cc.p, ctx->cgrp.p, ctx->Tp, ctx->S.p,
             ctx->levels[nl - 1], lo, hi, nl, buf_c(pi), buf_n(pi));
         LAUNCHED_K();
         return BN_OK;
@@ -947,16 +959,22 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
                                                  ctx->L, prm->seed, t, ctx->rowB, nl);
             LAUNCHED_K();
         }
-        if ((rc = gram_lut(ctx, buf_c(pi), buf_n(pi), 1))) return rc;
-        if (overlap && pi + 1 < prm->passes) {
-            // next pass's candidates: their buffer was last read by finish(pi-1), already done on cs
+        // next pass's candidates: their buffer was last read by finish(pi-1), already ordered on cs;
+        // launched once the Gram (the one SM-saturating kernel of the pass) is done, so they fill
+        // the SMs left idle by the memory-bound energy terms and the 16-SM decisions
+        const std::function<int()> prefetch = [&]() -> int {
             CUDA_TRY(cudaEventRecord(ctx->evB, cs));
             CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->evB, 0));
             ctx->ls = ctx->aux;
-            if ((rc = launch_counts(pi + 1))) return rc;
+            if (int r = launch_counts(pi + 1)) return r;
             CUDA_TRY(cudaEventRecord(ctx->evC, ctx->aux));
             ctx->ls = cs;
-        }
+            return BN_OK;
+        };
+        const bool pf = overlap && pi + 1 < prm->passes;
+        if ((rc = gram_lut(ctx, buf_c(pi), buf_n(pi), 1, pf && !ctx->prefetch_after_lut ? &prefetch : nullptr)))
+            return rc;
+        if (pf && ctx->prefetch_after_lut && (rc = prefetch())) return rc;
         uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
         bool done = false;
         if (!ctx->per_class_decide && (rc = decide_pass(ctx, t, prm->seed, (int)prm->mode, log, &done))) return rc;

@@ -84,7 +84,10 @@ __host__ __device__ __forceinline__ int half_index(int ox, int oy, int R) {
 // i.e. two 32x32->64 integer multiply-adds per (pixel, integrand, sample): exact.
 // Padding integrands (i >= Ts) use a = b = 0, C = 1, so they always count 0.
 // Layout out: [p][l][Tp] uint8; norms: [p][l] int32 = sum_i c^2.
-constexpr int COUNT_PIX = 4;  // pixels per CTA (short CTAs co-schedule well on the aux stream)
+#ifndef BN_COUNT_PIX
+#define BN_COUNT_PIX 8
+#endif
+constexpr int COUNT_PIX = BN_COUNT_PIX;  // pixels per CTA (short CTAs co-schedule well on the aux stream)
 
 // Filtered fast test.  t = fma(a, x', fma(b, y', -C)) in fp32 with x' = fl(X'), C~ = fl(C):
 //   |x' - X'| <= 2^6, |C~ - C| <= 2^24, |a|,|b| <= 2^15, |b y' - C~| < 2^49
@@ -133,58 +136,78 @@ __device__ __forceinline__ void count_span(const float2* __restrict__ xyf, uint3
 
 // Each thread owns NI = 8 consecutive integrands (two packed 32-bit words per level row) and
 // walks the CTA's pixels; the sample loop is split at the level boundaries N_l so that the
-// inner loop is branch-free and unrolled.
+// inner loop is branch-free and unrolled.  The fp32 operands of the filtered test come
+// pre-packed from k_count_prep (one 96-byte record per integrand group).
 constexpr int COUNT_NI = 8;
-__global__ void __launch_bounds__(256, 2) k_counts(const uint2* __restrict__ U, uint2* __restrict__ Uout, int redraw,
+struct CountGroup {  // integrand pairs (2h, 2h+1) of one group, h = 0..3: {a, a}, {b, b}, {-C, -C}
+    unsigned long long a2[COUNT_NI / 2], b2[COUNT_NI / 2], c2[COUNT_NI / 2];
+};
+__global__ void k_count_prep(const int2* __restrict__ ab, const long long* __restrict__ Cc, uint32_t Tp,
+                             CountGroup* __restrict__ g) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Tp / COUNT_NI) return;
+    CountGroup r;
+#pragma unroll
+    for (int h = 0; h < COUNT_NI / 2; ++h) {
+        const int2 v0 = ab[COUNT_NI * q + 2 * h], v1 = ab[COUNT_NI * q + 2 * h + 1];
+        r.a2[h] = pack2((float)v0.x, (float)v1.x);
+        r.b2[h] = pack2((float)v0.y, (float)v1.y);
+        r.c2[h] = pack2(-__ll2float_rn(Cc[COUNT_NI * q + 2 * h]), -__ll2float_rn(Cc[COUNT_NI * q + 2 * h + 1]));
+    }
+    g[q] = r;
+}
+
+#ifndef BN_COUNT_MINB
+#define BN_COUNT_MINB 2
+#endif
+__global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __restrict__ U, uint2* __restrict__ Uout, int redraw,
                                                 uint64_t seed, uint32_t pass_t, uint32_t P,
                                                 const int2* __restrict__ ab, const long long* __restrict__ Cc,
-                                                uint32_t Tp, const uint2* __restrict__ S, uint32_t Nmax,
-                                                uint4 lev_lo, uint4 lev_hi, uint32_t nl, uint8_t* __restrict__ out,
+                                                const CountGroup* __restrict__ grp, uint32_t Tp,
+                                                const uint2* __restrict__ S, uint32_t Nmax, uint4 lev_lo,
+                                                uint4 lev_hi, uint32_t nl, uint8_t* __restrict__ out,
                                                 int* __restrict__ norms) {
     constexpr int NI = COUNT_NI;
     __shared__ int2 sXY[COUNT_PIX][128];
     __shared__ float2 sXYf[COUNT_PIX][128];
     __shared__ int sNorm[COUNT_PIX][8];
-    const uint32_t levels[8] = {lev_lo.x, lev_lo.y, lev_lo.z, lev_lo.w, lev_hi.x, lev_hi.y, lev_hi.z, lev_hi.w};
+    __shared__ uint32_t levels[8];
+    if (threadIdx.x == 0) {
+        levels[0] = lev_lo.x, levels[1] = lev_lo.y, levels[2] = lev_lo.z, levels[3] = lev_lo.w;
+        levels[4] = lev_hi.x, levels[5] = lev_hi.y, levels[6] = lev_hi.z, levels[7] = lev_hi.w;
+    }
     const uint32_t p0 = blockIdx.x * COUNT_PIX;
-    __shared__ uint2 sU[COUNT_PIX];
-    for (uint32_t j = threadIdx.x; j < COUNT_PIX * 8; j += blockDim.x) (&sNorm[0][0])[j] = 0;
-    if (threadIdx.x < COUNT_PIX && p0 + threadIdx.x < P) {  // one shift (one Philox draw) per pixel
-        const uint32_t p = p0 + threadIdx.x;
-        uint2 u;
-        if (redraw) {
-            const uint4 r = philox_seeded(seed, p, pass_t, 0, 1);
-            u = make_uint2(r.x, r.y);
-            Uout[p] = u;
-        } else {
-            u = U[p];
-        }
-        sU[threadIdx.x] = u;
-    }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < COUNT_PIX * Nmax; j += blockDim.x) {
-        const uint32_t pp = j / Nmax, k = j - pp * Nmax;
-        if (p0 + pp >= P) continue;
-        const uint2 u = sU[pp], s = S[k];
-        const int2 xy = make_int2((int)((s.x + u.x) ^ 0x80000000u), (int)((s.y + u.y) ^ 0x80000000u));
-        sXY[pp][k] = xy;
-        sXYf[pp][k] = make_float2(__int2float_rn(xy.x), __int2float_rn(xy.y));
-    }
-    __syncthreads();
     // threads = (integrand group q) x (pixel subset sub): when Tp/NI < blockDim the CTA's threads
     // split its pixels instead of idling (Tp/NI is a multiple of 32, so warps stay uniform)
     const uint32_t qn = Tp / NI;
     const uint32_t nsub = qn < blockDim.x ? blockDim.x / qn : 1;
     const uint32_t sub = threadIdx.x / (blockDim.x / nsub), tq = threadIdx.x % (blockDim.x / nsub);
-    for (uint32_t q = tq; q < qn; q += blockDim.x / nsub) {
-        unsigned long long a2[NI / 2], b2[NI / 2], c2[NI / 2];  // integrand pairs (2h, 2h+1)
-#pragma unroll
-        for (int h = 0; h < NI / 2; ++h) {
-            const int2 v0 = ab[NI * q + 2 * h], v1 = ab[NI * q + 2 * h + 1];
-            a2[h] = pack2((float)v0.x, (float)v1.x);
-            b2[h] = pack2((float)v0.y, (float)v1.y);
-            c2[h] = pack2(-__ll2float_rn(Cc[NI * q + 2 * h]), -__ll2float_rn(Cc[NI * q + 2 * h + 1]));
+    // this thread's first integrand group: loads in flight while the samples are staged
+    CountGroup g0;
+    if (tq < qn) g0 = grp[tq];
+    for (uint32_t j = threadIdx.x; j < COUNT_PIX * 8; j += blockDim.x) (&sNorm[0][0])[j] = 0;
+    for (uint32_t j = threadIdx.x; j < COUNT_PIX * Nmax; j += blockDim.x) {
+        // samples X_k = S_k + u_p of pixel pp; the shift (one Philox draw per pixel) is recomputed
+        // by every thread that needs it instead of staged behind a barrier
+        const uint32_t pp = j / Nmax, k = j - pp * Nmax, p = p0 + pp;
+        if (p >= P) continue;
+        uint2 u;
+        if (redraw) {
+            const uint4 r = philox_seeded(seed, p, pass_t, 0, 1);
+            u = make_uint2(r.x, r.y);
+            if (k == 0) Uout[p] = u;
+        } else {
+            u = U[p];
         }
+        const uint2 sk = S[k];
+        const int2 xy = make_int2((int)((sk.x + u.x) ^ 0x80000000u), (int)((sk.y + u.y) ^ 0x80000000u));
+        sXY[pp][k] = xy;
+        sXYf[pp][k] = make_float2(__int2float_rn(xy.x), __int2float_rn(xy.y));
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t q = tq; q < qn; q += blockDim.x / nsub) {
+        const CountGroup gq = q == tq ? g0 : grp[q];
         for (uint32_t pp = sub; pp < COUNT_PIX; pp += nsub) {
             const uint32_t p = p0 + pp;
             if (p >= P) break;
@@ -198,7 +221,7 @@ __global__ void __launch_bounds__(256, 2) k_counts(const uint2* __restrict__ U, 
             uint32_t kprev = 0;
             for (uint32_t li = 0; li < nl; ++li) {
                 const uint32_t n1 = levels[li];
-                count_span<NI>(sXYf[pp], kprev, n1, a2, b2, c2, neg, mn);
+                count_span<NI>(sXYf[pp], kprev, n1, gq.a2, gq.b2, gq.c2, neg, mn);
                 kprev = n1;
                 uint32_t w[NI / 4];
                 uint32_t nsq = 0;
@@ -210,25 +233,51 @@ __global__ void __launch_bounds__(256, 2) k_counts(const uint2* __restrict__ U, 
                     nsq = __dp4a(w[h], w[h], nsq);  // sum of the four squared counts
                 }
                 *reinterpret_cast<uint2*>(orow + (size_t)li * Tp) = make_uint2(w[0], w[1]);
-                atomicAdd(&sNorm[pp][li], (int)nsq);
+                // a warp's lanes share the pixel (tq runs over whole warps): one REDUX, one atomic
+                nsq = __reduce_add_sync(0xffffffffu, nsq);
+                if (lane == 0) atomicAdd(&sNorm[pp][li], (int)nsq);
             }
-            // exact int64 recount of any integrand whose samples came within the error band
+            // exact int64 recount of any pair of integrands whose samples came within the error
+            // band, done by the whole warp (the pixel is warp-uniform): lane k tests samples
+            // k, k+32, ...; per-level counts are popcounts of the ballots
 #pragma unroll
-            for (int j = 0; j < NI; ++j) {
-                if (mn[j >> 1] >= COUNT_EXACT_BAND) continue;  // exact recount of both of the pair
-                const int2 abj = ab[NI * q + j];
-                const long long cj = Cc[NI * q + j];
-                uint32_t cnt = 0, lj = 0, nx = levels[0];
-                for (uint32_t k = 0; k < Nmax; ++k) {
-                    const int2 xy = sXY[pp][k];
-                    cnt += ((long long)abj.x * xy.x + (long long)abj.y * xy.y - cj) >= 0;
-                    if (k + 1 == nx) {
-                        uint8_t* cell = orow + (size_t)lj * Tp + j;
-                        const int old = *cell;
-                        *cell = (uint8_t)cnt;
-                        atomicAdd(&sNorm[pp][lj], (int)(cnt * cnt) - old * old);
-                        ++lj;
-                        nx = lj < nl ? levels[lj] : 0xffffffffu;
+            for (int h = 0; h < NI / 2; ++h) {
+                uint32_t need = __ballot_sync(0xffffffffu, mn[h] < COUNT_EXACT_BAND);
+                while (need) {
+                    const int src = __ffs(need) - 1;
+                    need &= need - 1;
+                    const uint32_t qs = __shfl_sync(0xffffffffu, q, src);
+                    for (int e = 0; e < 2; ++e) {
+                        const uint32_t i = NI * qs + 2 * h + e;
+                        const int2 abj = ab[i];
+                        const long long cj = Cc[i];
+                        uint32_t bits[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const uint32_t k = lane + 32 * r;
+                            bool pos = false;
+                            if (k < Nmax) {
+                                const int2 xy = sXY[pp][k];
+                                pos = ((long long)abj.x * xy.x + (long long)abj.y * xy.y - cj) >= 0;
+                            }
+                            bits[r] = __ballot_sync(0xffffffffu, pos);
+                        }
+                        if ((int)lane == src) {
+                            for (uint32_t lj = 0; lj < nl; ++lj) {
+                                const uint32_t n1 = levels[lj];
+                                uint32_t cnt = 0;
+#pragma unroll
+                                for (int r = 0; r < 4; ++r) {
+                                    const uint32_t lo = 32 * r;
+                                    const uint32_t m = n1 <= lo ? 0u : n1 - lo >= 32 ? 0xffffffffu : (1u << (n1 - lo)) - 1u;
+                                    cnt += __popc(bits[r] & m);
+                                }
+                                uint8_t* cell = orow + (size_t)lj * Tp + 2 * h + e;
+                                const int old = *cell;
+                                *cell = (uint8_t)cnt;
+                                atomicAdd(&sNorm[pp][lj], (int)(cnt * cnt) - old * old);
+                            }
+                        }
                     }
                 }
             }
@@ -852,7 +901,7 @@ constexpr int STAGE = A_BYTES + B_BYTES;  // 45056 = 44 KB (1024-aligned)
 constexpr int NSTAGE = 4;
 constexpr int NROWS = A_ROWS + B_ROWS;    // staged rows per stage (348)
 constexpr int THREADS = 288;
-constexpr int SCR = 24;
+constexpr int SCR = 25;  // odd row stride: conflict-free scratch writes
 constexpr int SMEM = NSTAGE * STAGE + 4 * 32 * SCR * 4 + 2 * NBR * NBC * 4 + NROWS * 8 + 1024;
 constexpr int H = 2 * R * R + 2 * R;
 }  // namespace tc2
@@ -1054,7 +1103,7 @@ constexpr int A_BYTES = 128 * 128, B_BYTES = N * 128;
 constexpr int STAGE = A_BYTES + B_BYTES;  // 47104 = 46 KB
 constexpr int NSTAGE = 4;
 constexpr int THREADS = 192;
-constexpr int SCR = 28;
+constexpr int SCR = 25;  // odd row stride: conflict-free scratch writes
 constexpr int SMEM = NSTAGE * STAGE + 4 * 32 * SCR * 4 + 2 * NBR * NBX * 4 + 1024;
 constexpr int H = 2 * R * R + 2 * R;
 }  // namespace tc3
