@@ -169,7 +169,7 @@ struct bn_ctx {
     cudaStream_t ls = nullptr, aux = nullptr, hp = nullptr;
     cudaEvent_t evA = nullptr, evB = nullptr, evC = nullptr;
     bool no_overlap = false;  // BN_OVERLAP=0: no candidate prefetch on the aux stream
-    bool prefetch_after_lut = false;  // BN_PREFETCH=lut: prefetch after the energy terms (not the Gram)
+    int prefetch_at = 1;  // BN_PREFETCH=start|gram|lut: launch the next pass's counts before the Gram / after it / after the energy terms
     bool per_class_decide = false;  // BN_DECIDE=per_class: 64 launches instead of one persistent
     bool simt_gram = false;         // BN_GRAM=simt: dp4a window distances instead of IMMA
     bool gram_attr_set[8] = {false};
@@ -184,6 +184,7 @@ struct bn_ctx {
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
+    bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
     // per-kernel event timing (bn_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -522,11 +523,16 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     const uint32_t ncta = nb * nb / cpc;
     *done = false;
     if (ncta > 16 || ctx->no_cluster) return BN_OK;
-    const size_t smem = (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8 + P;  // double-buffered int64 rows + flags
-    const void* fn = mode ? (const void*)k_decide_cluster<R, 1> : (const void*)k_decide_cluster<R, 0>;
+    // v2 (default): u32 flags + slot table; v1 (BN_DECIDE=cluster1): byte flags, cluster barriers
+    const bool v2 = !ctx->cluster_v1;
+    const size_t smem = v2 ? (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8 + 4 * (size_t)P + 64 * 4 * (mode ? 2 : 1) * cpc
+                           : (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8 + P;  // double-buffered rows + flags
+    const void* fn = v2 ? (mode ? (const void*)k_decide_cl2<R, 1> : (const void*)k_decide_cl2<R, 0>)
+                        : (mode ? (const void*)k_decide_cluster<R, 1> : (const void*)k_decide_cluster<R, 0>);
     if (!ctx->cluster_attr_set[R]) {
-        for (const void* f : {(const void*)k_decide_cluster<R, 0>, (const void*)k_decide_cluster<R, 1>}) {
-            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        for (const void* f : {(const void*)k_decide_cluster<R, 0>, (const void*)k_decide_cluster<R, 1>,
+                              (const void*)k_decide_cl2<R, 0>, (const void*)k_decide_cl2<R, 1>}) {
+            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
             CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         }
         ctx->cluster_attr_set[R] = true;
@@ -660,10 +666,11 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     const char* dm = getenv("BN_DECIDE");
     ctx->per_class_decide = dm && !strcmp(dm, "per_class");
     ctx->no_cluster = dm && !strcmp(dm, "flags");
+    ctx->cluster_v1 = dm && !strcmp(dm, "cluster1");
     const char* ov = getenv("BN_OVERLAP");
     ctx->no_overlap = ov && !strcmp(ov, "0");
     const char* pfe = getenv("BN_PREFETCH");
-    ctx->prefetch_after_lut = pfe && !strcmp(pfe, "lut");
+    ctx->prefetch_at = !pfe ? 1 : !strcmp(pfe, "start") ? 0 : !strcmp(pfe, "lut") ? 2 : 1;
     ctx->ls = ctx->stream;
     {
         DeviceGuard g(cuda_device);
@@ -972,9 +979,10 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             return BN_OK;
         };
         const bool pf = overlap && pi + 1 < prm->passes;
-        if ((rc = gram_lut(ctx, buf_c(pi), buf_n(pi), 1, pf && !ctx->prefetch_after_lut ? &prefetch : nullptr)))
+        if (pf && ctx->prefetch_at == 0 && (rc = prefetch())) return rc;
+        if ((rc = gram_lut(ctx, buf_c(pi), buf_n(pi), 1, pf && ctx->prefetch_at == 1 ? &prefetch : nullptr)))
             return rc;
-        if (pf && ctx->prefetch_after_lut && (rc = prefetch())) return rc;
+        if (pf && ctx->prefetch_at == 2 && (rc = prefetch())) return rc;
         uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
         bool done = false;
         if (!ctx->per_class_decide && (rc = decide_pass(ctx, t, prm->seed, (int)prm->mode, log, &done))) return rc;

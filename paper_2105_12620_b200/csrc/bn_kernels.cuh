@@ -107,6 +107,20 @@ __device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
 }
 
 // One sample against NI integrands held as NI/2 packed pairs: t = a x + (b y - C) per lane half.
+// One sample against NI integrands held as NI/2 packed pairs: t = a x + (b y - C) per lane half.
+// Sign-bit accumulation n += t >> 31 on either issue pipe: LEA.HI runs on the (half-rate) ALU
+// pipe, which the FMNMX3 filter already loads; IMAD.HI t * two (two == 2 at run time, so ptxas
+// cannot strength-reduce it back to a shift) runs on the FMA pipe.  The count loop splits its
+// sign bits between the two so that neither pipe limits it alone.
+__device__ __forceinline__ uint32_t sign_acc_fma(uint32_t n, uint32_t t, uint32_t two) {
+    asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(n) : "r"(t), "r"(two));
+    return n;
+}
+#ifndef BN_COUNT_IMAD
+#define BN_COUNT_IMAD 1
+#endif
+
+// One sample against NI integrands held as NI/2 packed pairs: t = a x + (b y - C) per lane half.
 template <int NI>
 __device__ __forceinline__ void count_sample(float2 xy, const unsigned long long* ab2a,
                                              const unsigned long long* ab2b, const unsigned long long* c2,
@@ -1313,6 +1327,20 @@ struct DTabs {
     const longlong2* x1;
 };
 
+// Exact warp sum of an int128 (two's complement, mod 2^128) with 8 REDUX.SUM instructions:
+// split into 16-bit limbs (each warp sum < 2^21 fits 32 bits), then recombine with carries.
+__device__ __forceinline__ i128 warp_sum_i128_redux(unsigned long long lo, unsigned long long hi) {
+    uint32_t s[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[i] = __reduce_add_sync(0xffffffffu, (uint32_t)(lo >> (16 * i)) & 0xffffu);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[4 + i] = __reduce_add_sync(0xffffffffu, (uint32_t)(hi >> (16 * i)) & 0xffffu);
+    u128 r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += (u128)s[i] << (16 * i);
+    return (i128)r;
+}
+
 struct LutArgs {
     const double* G[8];  // per-level G tables
     int Dmax[8];         // largest legal D per level (guards corrupted distances)
@@ -1377,14 +1405,14 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
             put_term(d1, x1, (size_t)q * WN + wm, b1, force_escape);
         }
     }
-    // block reduction of e (u128) through shared memory
-    __shared__ unsigned long long slo[256], shi[256];
-    slo[threadIdx.x] = (unsigned long long)e;
-    shi[threadIdx.x] = (unsigned long long)(e >> 64);
+    // block reduction of e (u128): exact REDUX warp sums, then the 8 warp partials
+    __shared__ u128 swarp[8];
+    const u128 ws = (u128)warp_sum_i128_redux((unsigned long long)e, (unsigned long long)(e >> 64));
+    if ((threadIdx.x & 31) == 0) swarp[threadIdx.x >> 5] = ws;
     __syncthreads();
     if (threadIdx.x == 0) {
         u128 s = 0;
-        for (int j = 0; j < (int)blockDim.x; ++j) s += ((u128)shi[j] << 64) | slo[j];
+        for (int j = 0; j < (int)(blockDim.x >> 5); ++j) s += swarp[j];
         Epart[blockIdx.x] = s;
     }
 }
@@ -1648,20 +1676,6 @@ struct LaneOffsets {
     }
 };
 
-// Exact warp sum of an int128 (two's complement, mod 2^128) with 8 REDUX.SUM instructions:
-// split into 16-bit limbs (each warp sum < 2^21 fits 32 bits), then recombine with carries.
-__device__ __forceinline__ i128 warp_sum_i128_redux(unsigned long long lo, unsigned long long hi) {
-    uint32_t s[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s[i] = __reduce_add_sync(0xffffffffu, (uint32_t)(lo >> (16 * i)) & 0xffffu);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s[4 + i] = __reduce_add_sync(0xffffffffu, (uint32_t)(hi >> (16 * i)) & 0xffffu);
-    u128 r = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r += (u128)s[i] << (16 * i);
-    return (i128)r;
-}
-
 template <int R>
 struct WinTermsLocal : WinTerms<R> {
     // sum with the flags read from this CTA's shared-memory copy
@@ -1728,18 +1742,27 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
     off.init();
     cluster_sync_all();  // every CTA's flag copy is initialised before any remote store
     for (uint32_t s = 0; s < 64; ++s) {
+#ifdef BN_DEC_PROF
+        long long tp0 = clock64(), tp1 = 0, tp2 = 0, tp3 = 0, tp4 = 0, tp5 = 0;
+#define TP(v) v = clock64()
+#else
+#define TP(v)
+#endif
         // double-buffered staging: class s+1 goes to buffer (s+1)&1, last read in class s-1
         // (the cluster barrier that ended class s-1 orders those reads before these copies)
         if (s + 1 < 64) {
             slot_pixels(s + 1, sSlot[(s + 1) & 1]);
             __syncwarp();
             __syncthreads();  // sSlot[(s+1)&1] visible to the staging warps
+            TP(tp1);
             stage_class<R>(sbase + ((s + 1) & 1) * buf_bytes, sSlot[(s + 1) & 1], nslot, T);
+            TP(tp2);
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();  // class s's staged rows visible to every warp
+        TP(tp3);
         const uint32_t b = s & 1;
         const uint32_t j = warp;
         const uint32_t kappa = mode ? sKappa[s] : 0;
@@ -1749,9 +1772,19 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
         WinTermsLocal<R> A, B;
         A.load_smem(rows + (size_t)j * 2 * WN);
         if (mode) B.load_smem(rows + (size_t)(cpc + j) * 2 * WN);
+#ifdef BN_DEC_PROF
+        long long tq0 = clock64();
+        asm volatile("" ::"l"(A.v0[0]), "l"(A.v1[WinTerms<R>::PER - 1]));
+        long long tq1 = clock64();
+#endif
         i128 sum = A.sum_local(sflags, L, p, off, T);
         if (mode) sum += B.sum_local(sflags, L, p2, off, T);
         const bool ok = 2 * sum < 0;
+        TP(tp4);
+#ifdef BN_DEC_PROF
+        if (pass_t == 2 && (s == 10 || s == 40) && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 7))
+            printf("DECPROF2 cta %u s %u load_smem %lld sum_local %lld\n", blockIdx.x, s, tq1 - tq0, tp4 - tq1);
+#endif
         if (ok && (uint32_t)lane < ncta) st_cluster_u8(sflags_addr + p, lane, 1);  // incl. own copy
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         if (lane == 0) {  // bookkeeping for commit/stats: not needed by other CTAs in this kernel
@@ -1760,7 +1793,152 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
             if (log) log[(size_t)s * M + m] = ok;
         }
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#ifdef BN_DEC_PROF
+        TP(tp5);
+        if (pass_t == 2 && (s == 10 || s == 40) && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 7))
+            printf("DECPROF cta %u s %u slotpix+sync %lld stage %lld wait+sync %lld sum %lld flag+barrier %lld total %lld\n",
+                   blockIdx.x, s, tp1 - tp0, tp2 - tp1, tp3 - tp2, tp4 - tp3, tp5 - tp4, tp5 - tp0);
+#endif
     }
+}
+
+// Cluster decision kernel v2 (same tiles as k_decide_cluster): no cluster barrier per class.
+// After deciding class s every warp pushes its pixel's accept flag (u32, 0 or 1) into every CTA's
+// flag array with st.async, which also completes 4 bytes of transaction on that CTA's mailbox
+// mbarrier for the class parity; a CTA starts class s+1 once its mailbox has received all M
+// flags of class s.  A CTA can only send class s+1 flags after receiving every flag of class s,
+// i.e. after every warp of the cluster has finished reading the flags for class s, so a flag
+// never changes under a reader.  Each warp stages its own candidates' dE-term rows for the next
+// class with two bulk copies (cp.async.bulk, mbarrier completion), so no warp waits on another.
+// Barrier-free: the cluster-scope release of barrier.cluster.arrive (MEMBAR.ALL.GPU, which also
+// drains the in-flight staging) is off the 64-class critical path.
+template <int R>
+struct WinTermsFlags32 : WinTerms<R> {
+    __device__ __forceinline__ i128 sum_flags(const uint32_t* sflags, uint32_t L, uint32_t p,
+                                              const LaneOffsets<R>& off, const DTabs T) const {
+        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
+        const int lane = threadIdx.x & 31;
+        const uint32_t x = p & (L - 1), y = p / L;
+        i128 acc = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int w = lane + 32 * j;
+            if (w < WN) {
+                const uint32_t q = ((y + off.oy[j]) & (L - 1)) * L + ((x + off.ox[j]) & (L - 1));
+                const bool f = sflags[q] != 0;
+                const long long v = f ? this->v1[j] : this->v0[j];
+                if (v != DT_ESC) {
+                    acc += (i128)v;
+                } else {  // rare: exact int128 term from the escape table
+                    const longlong2 e = (f ? T.x1 : T.x0)[(size_t)p * WN + w];
+                    acc += ((i128)e.y << 64) | (u128)(unsigned long long)e.x;
+                }
+            }
+        }
+        return warp_sum_i128_redux((unsigned long long)acc, (unsigned long long)(acc >> 64));
+    }
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_u32(uint32_t local_addr, uint32_t local_bar, uint32_t cta, uint32_t v) {
+    uint32_t ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(cta));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(local_bar), "r"(cta));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(ra), "r"(v), "r"(rb)
+                 : "memory");
+}
+
+template <int R, int mode>
+__global__ void __launch_bounds__(512, 1) k_decide_cl2(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
+                                                       const DTabs T, uint8_t* __restrict__ acc,
+                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log) {
+    constexpr int WN = WinTerms<R>::WN;
+    constexpr uint32_t ROWB = 2 * WN * 8;   // one slot: delta0 row then delta1 row (int64)
+    constexpr uint32_t NSW = mode ? 2 : 1;  // slots per warp (SWAP: the candidate and its partner)
+    extern __shared__ __align__(16) uint8_t dsm[];
+    __shared__ uint8_t sDelta[8 * 16];
+    __shared__ uint32_t sKappa[64];
+    __shared__ __align__(8) uint64_t sbar[2 + 2 * 16];  // mailboxes [2], staging [warp][buffer]
+    const uint32_t nb = L / 8, M = nb * nb, P = L * L;
+    const uint32_t ncta = gridDim.x, first = blockIdx.x * cpc;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t buf_bytes = cpc * NSW * ROWB;
+    uint32_t* sflags = reinterpret_cast<uint32_t*>(dsm + 2 * buf_bytes);  // [P]
+    uint32_t* sSlot = sflags + P;                                          // [64][cpc * NSW]
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(dsm);
+    const uint32_t sflags_addr = sbase + 2 * buf_bytes;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
+    auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
+    auto stbar = [&](uint32_t b) { return bar0 + 8 * (2 + 2 * warp + b); };
+    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
+    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
+        sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
+    if (mode)
+        for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sKappa[j] = swap_kappa(seed, pass_t, j, M);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2 + 2 * 16; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t per_class = cpc * NSW;
+    for (uint32_t j = threadIdx.x; j < 64 * per_class; j += blockDim.x) {
+        const uint32_t s = j / per_class, i = j - s * per_class;
+        const uint32_t m = i < cpc ? first + i : ((first + i - cpc) ^ sKappa[s]);
+        sSlot[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
+    }
+    __syncthreads();
+    // warp `warp` stages its slot(s) of class s into buffer b (lane 0 issues the bulk copies)
+    auto stage = [&](uint32_t s, uint32_t b) {
+        __syncwarp();  // the warp's reads of buffer b (class s-2) are done
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t bar = stbar(b);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(NSW * ROWB)
+                         : "memory");
+#pragma unroll
+            for (uint32_t i = 0; i < NSW; ++i) {
+                const uint32_t pix = sSlot[s * per_class + (i ? cpc : 0) + warp];
+                const uint32_t dst = sbase + b * buf_bytes + (warp * NSW + i) * ROWB;
+                bulk_g2s(dst, T.d0 + (size_t)pix * WN, WN * 8, bar);
+                bulk_g2s(dst + WN * 8, T.d1 + (size_t)pix * WN, WN * 8, bar);
+            }
+        }
+    };
+    stage(0, 0);
+    LaneOffsets<R> off;
+    off.init();
+    cluster_sync_all();  // every CTA's barriers and flags are initialised before any remote st.async
+    for (uint32_t s = 0; s < 64; ++s) {
+        const uint32_t b = s & 1;
+        if (s + 1 < 64) stage(s + 1, b ^ 1);
+        if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
+        if (threadIdx.x == 0)  // this CTA expects M flags of class s (the phase of class s-2 is complete)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
+                         : "memory");
+        tc::mbar_wait(stbar(b), (s >> 1) & 1);  // this warp's rows of class s
+        const uint32_t m = first + warp, mm = m ^ (mode ? sKappa[s] : 0u);
+        const uint32_t p = sSlot[s * per_class + warp], p2 = mode ? sSlot[s * per_class + cpc + warp] : p;
+        const long long* rows = reinterpret_cast<const long long*>(dsm + b * buf_bytes) + (size_t)warp * NSW * 2 * WN;
+        WinTermsFlags32<R> A, B;
+        A.load_smem(rows);
+        if (mode) B.load_smem(rows + 2 * WN);
+        i128 sum = A.sum_flags(sflags, L, p, off, T);
+        if (mode) sum += B.sum_flags(sflags, L, p2, off, T);
+        const bool ok = 2 * sum < 0;
+        if (lane < ncta) st_async_u32(sflags_addr + 4 * p, mailbox(s), lane, ok ? 1u : 0u);
+        if (lane == 0) {  // bookkeeping for commit/stats
+            acc[p] = ok;
+            dEp[p] = (ok && (!mode || m < mm)) ? 2 * sum : (i128)0;
+            if (log) log[(size_t)s * M + m] = ok;
+        }
+    }
+    tc::mbar_wait(mailbox(63), (63 >> 1) & 1);  // every flag sent to this CTA has landed
+    cluster_sync_all();
 }
 
 // ------------------------------------------------------------------------------- commit
