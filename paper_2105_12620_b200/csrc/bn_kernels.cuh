@@ -107,20 +107,6 @@ __device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
 }
 
 // One sample against NI integrands held as NI/2 packed pairs: t = a x + (b y - C) per lane half.
-// One sample against NI integrands held as NI/2 packed pairs: t = a x + (b y - C) per lane half.
-// Sign-bit accumulation n += t >> 31 on either issue pipe: LEA.HI runs on the (half-rate) ALU
-// pipe, which the FMNMX3 filter already loads; IMAD.HI t * two (two == 2 at run time, so ptxas
-// cannot strength-reduce it back to a shift) runs on the FMA pipe.  The count loop splits its
-// sign bits between the two so that neither pipe limits it alone.
-__device__ __forceinline__ uint32_t sign_acc_fma(uint32_t n, uint32_t t, uint32_t two) {
-    asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(n) : "r"(t), "r"(two));
-    return n;
-}
-#ifndef BN_COUNT_IMAD
-#define BN_COUNT_IMAD 1
-#endif
-
-// One sample against NI integrands held as NI/2 packed pairs: t = a x + (b y - C) per lane half.
 template <int NI>
 __device__ __forceinline__ void count_sample(float2 xy, const unsigned long long* ab2a,
                                              const unsigned long long* ab2b, const unsigned long long* c2,
@@ -141,9 +127,12 @@ __device__ __forceinline__ void count_span(const float2* __restrict__ xyf, uint3
                                            const unsigned long long* a2, const unsigned long long* b2,
                                            const unsigned long long* c2, uint32_t* neg, float* mn) {
     uint32_t k = k0;
-    for (; k + 4 <= k1; k += 4) {
+#ifndef BN_COUNT_UNROLL
+#define BN_COUNT_UNROLL 4
+#endif
+    for (; k + BN_COUNT_UNROLL <= k1; k += BN_COUNT_UNROLL) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) count_sample<NI>(xyf[k + u], a2, b2, c2, neg, mn);
+        for (int u = 0; u < BN_COUNT_UNROLL; ++u) count_sample<NI>(xyf[k + u], a2, b2, c2, neg, mn);
     }
     for (; k < k1; ++k) count_sample<NI>(xyf[k], a2, b2, c2, neg, mn);
 }
@@ -200,23 +189,25 @@ __global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __re
     CountGroup g0;
     if (tq < qn) g0 = grp[tq];
     for (uint32_t j = threadIdx.x; j < COUNT_PIX * 8; j += blockDim.x) (&sNorm[0][0])[j] = 0;
-    for (uint32_t j = threadIdx.x; j < COUNT_PIX * Nmax; j += blockDim.x) {
-        // samples X_k = S_k + u_p of pixel pp; the shift (one Philox draw per pixel) is recomputed
-        // by every thread that needs it instead of staged behind a barrier
-        const uint32_t pp = j / Nmax, k = j - pp * Nmax, p = p0 + pp;
-        if (p >= P) continue;
+    // samples X_k = S_k + u_p: warp w stages pixels w, w + 8, ...; every lane of the warp draws
+    // the pixel's shift (one Philox per pixel and lane) instead of waiting behind a barrier
+    for (uint32_t pp = threadIdx.x >> 5; pp < COUNT_PIX; pp += blockDim.x >> 5) {
+        const uint32_t p = p0 + pp;
+        if (p >= P) break;
         uint2 u;
         if (redraw) {
             const uint4 r = philox_seeded(seed, p, pass_t, 0, 1);
             u = make_uint2(r.x, r.y);
-            if (k == 0) Uout[p] = u;
+            if ((threadIdx.x & 31) == 0) Uout[p] = u;
         } else {
             u = U[p];
         }
-        const uint2 sk = S[k];
-        const int2 xy = make_int2((int)((sk.x + u.x) ^ 0x80000000u), (int)((sk.y + u.y) ^ 0x80000000u));
-        sXY[pp][k] = xy;
-        sXYf[pp][k] = make_float2(__int2float_rn(xy.x), __int2float_rn(xy.y));
+        for (uint32_t k = threadIdx.x & 31; k < Nmax; k += 32) {
+            const uint2 sk = S[k];
+            const int2 xy = make_int2((int)((sk.x + u.x) ^ 0x80000000u), (int)((sk.y + u.y) ^ 0x80000000u));
+            sXY[pp][k] = xy;
+            sXYf[pp][k] = make_float2(__int2float_rn(xy.x), __int2float_rn(xy.y));
+        }
     }
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31;
@@ -1742,27 +1733,18 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
     off.init();
     cluster_sync_all();  // every CTA's flag copy is initialised before any remote store
     for (uint32_t s = 0; s < 64; ++s) {
-#ifdef BN_DEC_PROF
-        long long tp0 = clock64(), tp1 = 0, tp2 = 0, tp3 = 0, tp4 = 0, tp5 = 0;
-#define TP(v) v = clock64()
-#else
-#define TP(v)
-#endif
         // double-buffered staging: class s+1 goes to buffer (s+1)&1, last read in class s-1
         // (the cluster barrier that ended class s-1 orders those reads before these copies)
         if (s + 1 < 64) {
             slot_pixels(s + 1, sSlot[(s + 1) & 1]);
             __syncwarp();
             __syncthreads();  // sSlot[(s+1)&1] visible to the staging warps
-            TP(tp1);
             stage_class<R>(sbase + ((s + 1) & 1) * buf_bytes, sSlot[(s + 1) & 1], nslot, T);
-            TP(tp2);
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();  // class s's staged rows visible to every warp
-        TP(tp3);
         const uint32_t b = s & 1;
         const uint32_t j = warp;
         const uint32_t kappa = mode ? sKappa[s] : 0;
@@ -1772,19 +1754,9 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
         WinTermsLocal<R> A, B;
         A.load_smem(rows + (size_t)j * 2 * WN);
         if (mode) B.load_smem(rows + (size_t)(cpc + j) * 2 * WN);
-#ifdef BN_DEC_PROF
-        long long tq0 = clock64();
-        asm volatile("" ::"l"(A.v0[0]), "l"(A.v1[WinTerms<R>::PER - 1]));
-        long long tq1 = clock64();
-#endif
         i128 sum = A.sum_local(sflags, L, p, off, T);
         if (mode) sum += B.sum_local(sflags, L, p2, off, T);
         const bool ok = 2 * sum < 0;
-        TP(tp4);
-#ifdef BN_DEC_PROF
-        if (pass_t == 2 && (s == 10 || s == 40) && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 7))
-            printf("DECPROF2 cta %u s %u load_smem %lld sum_local %lld\n", blockIdx.x, s, tq1 - tq0, tp4 - tq1);
-#endif
         if (ok && (uint32_t)lane < ncta) st_cluster_u8(sflags_addr + p, lane, 1);  // incl. own copy
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         if (lane == 0) {  // bookkeeping for commit/stats: not needed by other CTAs in this kernel
@@ -1793,12 +1765,6 @@ __global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint
             if (log) log[(size_t)s * M + m] = ok;
         }
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-#ifdef BN_DEC_PROF
-        TP(tp5);
-        if (pass_t == 2 && (s == 10 || s == 40) && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 7))
-            printf("DECPROF cta %u s %u slotpix+sync %lld stage %lld wait+sync %lld sum %lld flag+barrier %lld total %lld\n",
-                   blockIdx.x, s, tp1 - tp0, tp2 - tp1, tp3 - tp2, tp4 - tp3, tp5 - tp4, tp5 - tp0);
-#endif
     }
 }
 
