@@ -180,6 +180,7 @@ struct bn_ctx {
     bool tc2_gram = false;  // BN_GRAM=tc2: warp-specialised tcgen05 window Gram (R = 7)
     bool tc2_attr_set = false;
     bool tc3_gram = false;  // BN_GRAM=tc3: TMA-fed warp-specialised tcgen05 window Gram (R = 7)
+    bool tc4_gram = false;  // BN_GRAM=tc4 (default): persistent version of tc3
     bool tc3_attr_set = false;
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
@@ -388,12 +389,21 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
             return fail(ctx, BN_ECUDA, "cuTensorMapEncodeTiled failed");
         const int smem = tc3::SMEM;
         if (!ctx->tc3_attr_set) {
+            CUDA_TRY(cudaFuncSetAttribute(k_gram_tc4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             CUDA_TRY(cudaFuncSetAttribute(k_gram_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             ctx->tc3_attr_set = true;
         }
         KSTART(BN_K_GRAM);
-        k_gram_tc3<<<dim3(ctx->L / 8, ctx->L / 8, ctx->nl), tc3::THREADS, smem, ctx->ls>>>(mc, mn, ctx->nc.p, nn, ctx->L,
-                                                                                            ctx->Tp, ctx->nl, ctx->Dt.p);
+        if (ctx->tc4_gram) {  // persistent: one CTA per SM walks the (block, level) items
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
+            const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
+            const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
+            k_gram_tc4<<<grid, tc3::THREADS, smem, ctx->ls>>>(mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
+        } else {
+            k_gram_tc3<<<dim3(ctx->L / 8, ctx->L / 8, ctx->nl), tc3::THREADS, smem, ctx->ls>>>(
+                mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
+        }
         LAUNCHED_K();
     } else if (R == 7 && ctx->tc2_gram) {
         const int smem = tc2::SMEM;
@@ -693,7 +703,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->imma_v1 = gm && !strcmp(gm, "imma1");
     ctx->tc_gram = gm && !strcmp(gm, "tc");
     ctx->tc2_gram = gm && !strcmp(gm, "tc2");
-    ctx->tc3_gram = !gm || !*gm || !strcmp(gm, "tc3");  // default window Gram (R = 7)
+    ctx->tc4_gram = !gm || !*gm || !strcmp(gm, "tc4");  // default window Gram (R = 7): persistent
+    ctx->tc3_gram = ctx->tc4_gram || !strcmp(gm, "tc3");
     *out = ctx;
     return BN_OK;
 }

@@ -709,12 +709,20 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {  // K-major, SWIZZLE
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 __host__ __device__ constexpr uint32_t idesc_u8(int M, int N) {
+#ifdef BN_EXP_F8
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);  // f32 += e4m3 x e4m3
+#else
     return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);  // s32 += u8 x u8, K-major
+#endif
 }
 __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+#ifdef BN_EXP_F8
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+#else
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+#endif
         "l"(da), "l"(db), "r"(idesc), "r"(accum));
 }
 __device__ __forceinline__ void commit(uint32_t bar) {
@@ -1275,6 +1283,178 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_const
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(b_tempty + 8 * ub);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+// Persistent version of k_gram_tc3: one CTA per SM walks the (8x8 block, level) items
+// cta, cta + G, ...  The stage ring and the two TMEM accumulators continue across items, so the
+// TMA producer and the MMA warp run into the next item while the epilogue still drains the
+// previous one, and the per-CTA start-up (TMEM allocation, barrier set-up) and the last chunk's
+// epilogue are paid once per SM instead of once per item.  The epilogue loads the next item's
+// neighbourhood norms itself after finishing an item (the MMAs of that item are already
+// running).  Same TMA boxes, UMMA descriptors and epilogue arithmetic as k_gram_tc3.
+__global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_constant__ CountMaps mc,
+                                                              const __grid_constant__ CountMaps mn,
+                                                              const int* __restrict__ nc, const int* __restrict__ nn,
+                                                              uint32_t L, uint32_t Tp, uint32_t nl,
+                                                              int4* __restrict__ Dt) {
+    using namespace tc3;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sring = (raw + 1023) & ~1023u;
+    uint8_t* gring = smem_raw + (sring - raw);
+    int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);  // [4 warps][32][SCR]
+    int* snorm = scratch + 4 * 32 * SCR;                              // [2][NBR][NBX], x from x0-8
+    __shared__ __align__(8) uint64_t bars[2 * NSTAGE + 4];
+    __shared__ uint32_t tmem_sh;
+    const uint32_t b_full = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    const uint32_t b_empty = b_full + 8 * NSTAGE, b_tfull = b_full + 16 * NSTAGE, b_tempty = b_tfull + 16;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nbx = L / 8, nitems = nbx * nbx * nl, P = L * L;
+    const uint32_t nk = Tp / 128;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSTAGE; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_full + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_empty + 8 * i) : "memory");
+        }
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_tfull + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_tempty + 8 * i) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tmem_sh))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_sh;
+    auto item_xyl = [&](uint32_t it, uint32_t& x0, uint32_t& y0, uint32_t& l) {
+        const uint32_t bx = it % nbx, r = it / nbx;
+        x0 = 8 * bx;
+        y0 = 8 * (r % nbx);
+        l = r / nbx;
+    };
+
+    if (warp == 4) {
+        // --------------------------------------------------------------- TMA producer
+        if (lane == 0) {
+            uint32_t g = 0;
+            for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+                uint32_t x0, y0, l;
+                item_xyl(it, x0, y0, l);
+                for (int ch = 0; ch < NCHUNK; ++ch)
+                    for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
+                        const uint32_t b = g % NSTAGE, use = g / NSTAGE;
+                        if (use > 0) tc::mbar_wait(b_empty + 8 * b, (use - 1) & 1);
+                        const uint32_t buf = sring + b * STAGE, bar = b_full + 8 * b;
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(STAGE)
+                                     : "memory");
+                        const int kx = (int)(l * Tp + ks * 128);
+                        const bool whole = x0 >= 8 && x0 + 16 <= L && y0 + CH_ROWS * (ch + 1) <= L;
+                        for (int v = 0; v < 2; ++v) {
+                            const CountMaps& m = v ? mn : mc;
+                            tma_3d(buf + v * 8192, &m.a, kx, (int)x0, (int)y0, bar);  // 64 block rows
+                            const uint32_t bdst = buf + A_BYTES + v * CH_ROWS * GRP * 1024;
+                            if (whole) {
+                                tma_3d(bdst, &m.b, kx, (int)x0 - 8, (int)(y0 + CH_ROWS * ch), bar);
+                            } else {
+                                for (int nyl = 0; nyl < CH_ROWS; ++nyl)
+                                    for (int gx = 0; gx < GRP; ++gx) {
+                                        const uint32_t py = (y0 + CH_ROWS * ch + nyl) & (L - 1);
+                                        const uint32_t px = (x0 + 8 * gx + L - 8) & (L - 1);
+                                        tma_3d(bdst + (nyl * GRP + gx) * 1024, &m.s, kx, (int)px, (int)py, bar);
+                                    }
+                            }
+                        }
+                    }
+            }
+        }
+    } else if (warp == 5) {
+        // --------------------------------------------------------------- UMMA issuer
+        uint32_t g = 0, cc = 0;  // stage counter, chunk counter (accumulator ring)
+        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x)
+            for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
+                const uint32_t ub = cc & 1, uu = cc >> 1;
+                if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
+                    const uint32_t b = g % NSTAGE;
+                    tc::mbar_wait(b_full + 8 * b, (g / NSTAGE) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if (lane == 0) {
+                        const uint32_t sa = sring + b * STAGE, sb = sa + A_BYTES;
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk),
+                                    tc::idesc_u8(128, N), (ks > 0 || kk > 0) ? 1u : 0u);
+                        tc::commit(b_empty + 8 * b);
+                        if (ks + 1 == nk) tc::commit(b_tfull + 8 * ub);
+                    }
+                    __syncwarp();
+                }
+            }
+    } else if (warp < 4) {
+        // --------------------------------------------------------------- epilogue
+        const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
+        int* scr = scratch + (warp * 32 + lane) * SCR;
+        uint32_t cc = 0;
+        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+            uint32_t x0, y0, l;
+            item_xyl(it, x0, y0, l);
+            named_bar(2, 128);  // previous item's norms are no longer read
+            for (int j = threadIdx.x; j < 2 * NBR * NBX; j += 128) {
+                const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;
+                const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - 8) & (L - 1);
+                snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
+            }
+            named_bar(2, 128);
+            const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
+            const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
+            int2* out2 = reinterpret_cast<int2*>(Dt + ((size_t)l * P + p) * H) + v;
+            for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
+                const uint32_t ub = cc & 1, uu = cc >> 1;
+                tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
+                    const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
+                    uint32_t rc[32], rn[32];
+                    const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub + nyl * NBX;
+                    tc::ld32(ta, rc);                       // <v_p, c_q>, q in x0-8 .. x0+23 of row ny
+                    tc::ld32(ta + CH_ROWS * NBX, rn);       // <v_p, cn_q>
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (oy < 0 || oy > R) continue;
+                    int dc[2 * R + 1], dn[2 * R + 1];
+#pragma unroll
+                    for (int j = 0; j < NBX; ++j) scr[j] = (int)rc[j];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + 1 + i];
+#pragma unroll
+                    for (int j = 0; j < NBX; ++j) scr[j] = (int)rn[j];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + 1 + i];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) {
+                        const int ox = i - R, nx = dx + 1 + i;
+                        if (oy == 0 && ox <= 0) continue;
+                        const int nq_c = snorm[ny * NBX + nx], nq_n = snorm[(NBR + ny) * NBX + nx];
+                        out2[2 * half_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(b_tempty + 8 * ub);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
