@@ -350,8 +350,8 @@ int ensure_work(bn_ctx* ctx) {
     if ((rc = check_ready(ctx))) return rc;
     if ((rc = ensure_counts(ctx))) return rc;
     if (ctx->lut_dirty && (rc = build_lut(ctx))) return rc;
-    const size_t P = ctx->P, H = half_count(ctx->R), WN = win_count(ctx->R);
-    CUDA_TRY(ctx->Dt.ensure(P * H * ctx->nl));
+    const size_t P = ctx->P, H = half_count_padded(ctx->R), WN = win_count(ctx->R);
+    CUDA_TRY(ctx->Dt.ensure(P * H * ctx->nl));  // two int2 planes over [l][p][padded h]
     CUDA_TRY(ctx->d0.ensure(P * WN));
     CUDA_TRY(ctx->d1b.ensure(P * WN));
     CUDA_TRY(ctx->x0.ensure(P * WN));
@@ -461,7 +461,7 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
 template <int R>
 int launch_lut_only(bn_ctx* ctx, int write_deltas) {
     if (ctx->comm) {
-        const size_t n = (size_t)ctx->P * half_count(R) * ctx->nl * 4;
+        const size_t n = (size_t)ctx->P * half_count_padded(R) * ctx->nl * 4;
         int r = g_nccl.allreduce(ctx->Dt.p, ctx->Dt.p, n, NCCL_INT32, NCCL_SUM, ctx->comm, ctx->ls);
         if (r) return fail(ctx, BN_ENCCL, "ncclAllReduce: %s", g_nccl.errstr(r));
     }
@@ -470,7 +470,7 @@ int launch_lut_only(bn_ctx* ctx, int write_deltas) {
         la.G[l] = l < ctx->nl ? ctx->G.p + ctx->Goff[l] : nullptr;
         la.Dmax[l] = l < ctx->nl ? ctx->Dmax[l] : 0;
     }
-    const size_t nthr = (size_t)ctx->P * half_count(R);
+    const size_t nthr = (size_t)ctx->P * half_count_padded(R);
     KSTART(BN_K_LUT);
     {
         auto fn = ctx->nl == 4 ? k_lut<R, 4> : ctx->nl == 1 ? k_lut<R, 1> : k_lut<R, 0>;
@@ -892,7 +892,7 @@ int bn_energy(bn_ctx* ctx, double* E, uint64_t E_fixed[2]) {
     CUDA_TRY(ctx->pstats.ensure(1));
     CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
     if ((rc = gram_lut(ctx, ctx->c.p, ctx->nc.p, 0))) return rc;
-    const uint32_t nE = (uint32_t)(((size_t)ctx->P * half_count(ctx->R) + 255) / 256);
+    const uint32_t nE = (uint32_t)(((size_t)ctx->P * half_count_padded(ctx->R) + 255) / 256);
     k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, nullptr, nullptr, ctx->P, 0, ctx->pstats.p);
     LAUNCHED();
     PassStatsDev h;
@@ -917,7 +917,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     if (prm->passes == 0) return BN_OK;
     const uint32_t P = ctx->P, M = (ctx->L / 8) * (ctx->L / 8), nl = ctx->nl;
     const int R = ctx->R;
-    const uint32_t nE = (uint32_t)(((size_t)P * half_count(R) + 255) / 256);
+    const uint32_t nE = (uint32_t)(((size_t)P * half_count_padded(R) + 255) / 256);
     CUDA_TRY(ctx->pstats.ensure(prm->passes));
     int nsm_fin = 148;
     cudaDeviceGetAttribute(&nsm_fin, cudaDevAttrMultiProcessorCount, ctx->dev);
@@ -1051,7 +1051,7 @@ int bn_window_distances(bn_ctx* ctx, int32_t* out, int is_device) {
         CUDA_TRY(tmp.ensure(n));
         dst = tmp.p;
     }
-    k_dt_export<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->Dt.p, n, dst);
+    k_dt_export<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->Dt.p, ctx->P, ctx->nl, ctx->R, dst);
     LAUNCHED();
     if (!is_device) {
         cudaError_t e = cudaMemcpyAsync(out, dst, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);

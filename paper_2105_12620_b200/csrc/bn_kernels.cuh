@@ -76,6 +76,15 @@ __host__ __device__ __forceinline__ int win_index(int ox, int oy, int R) {
 __host__ __device__ __forceinline__ int half_index(int ox, int oy, int R) {
     return oy == 0 ? ox - 1 : R + (oy - 1) * (2 * R + 1) + (ox + R);
 }
+// Padded half window (the layout of the window-distance planes): row oy = 0 holds ox = 1..R in
+// ru4(R) records, rows oy = 1..R hold ox = -R..R in ru4(2R+1) records each, so every window row of
+// a pixel starts 32-byte aligned in an int2 plane and a Gram epilogue writes it with whole-sector
+// stores.  Pad records are never read.
+__host__ __device__ constexpr int ru4(int x) { return (x + 3) & ~3; }
+__host__ __device__ constexpr int half_count_padded(int R) { return ru4(R) + R * ru4(2 * R + 1); }
+__host__ __device__ __forceinline__ int hpad_index(int ox, int oy, int R) {
+    return oy == 0 ? ox - 1 : ru4(R) + (oy - 1) * ru4(2 * R + 1) + (ox + R);
+}
 
 // ---------------------------------------------------------------------------- error vectors
 // Heaviside counts for every pixel of a tile (set_tile) or for the REDRAW candidates of pass t.
@@ -312,6 +321,24 @@ __global__ void k_swap_gather(const uint2* __restrict__ U, uint2* __restrict__ U
     if (threadIdx.x < nl) nn[(size_t)p * nl + threadIdx.x] = nc[(size_t)p2 * nl + threadIdx.x];
 }
 
+// ------------------------------------------------------------------- window-distance planes
+// The window distances of every (level l, pixel p, half-window offset h) are two int2 planes over
+// the same [l][p][h] index (the int4 buffer Dt of nl*P*H records holds plane 0 in its first half,
+// plane 1 in its second):  plane 0 = (D(c_p, c_q), D(c_p, cn_q)),  plane 1 = (D(cn_p, c_q),
+// D(cn_p, cn_q)).  A Gram epilogue owning the c_p (or cn_p) row of a pixel writes whole int2
+// records of one plane, so its stores coalesce.
+__host__ __device__ __forceinline__ int2* dt_plane(int4* Dt, size_t n, int v) {
+    return reinterpret_cast<int2*>(Dt) + (size_t)v * n;
+}
+__device__ __forceinline__ void dt_put(int4* Dt, size_t n, size_t idx, int4 d) {
+    dt_plane(Dt, n, 0)[idx] = make_int2(d.x, d.y);
+    dt_plane(Dt, n, 1)[idx] = make_int2(d.z, d.w);
+}
+__device__ __forceinline__ int4 dt_get(const int4* Dt, size_t n, size_t idx) {
+    const int2 a = __ldg(reinterpret_cast<const int2*>(Dt) + idx), b = __ldg(reinterpret_cast<const int2*>(Dt) + n + idx);
+    return make_int4(a.x, a.y, b.x, b.y);
+}
+
 // --------------------------------------------------------------------------- window distances
 // One CTA = a strip of SW <= 32 pixels of one row y; warp w handles window row oy = w (0..R),
 // lane = pixel.  Per K-chunk the CTA stages, for every oy, the neighbour strip
@@ -387,7 +414,7 @@ __global__ void __launch_bounds__(32 * (R + 1)) k_gram(const uint8_t* __restrict
                 d.y = ncp + nnq - 2 * (int)acc[i][2];  // D(c_p, cn_q)
                 d.z = nnp + ncq - 2 * (int)acc[i][1];  // D(cn_p, c_q)
                 d.w = nnp + nnq - 2 * (int)acc[i][3];  // D(cn_p, cn_q)
-                Dt[((size_t)l * L * L + p) * H + half_index(ox, oy, R)] = d;
+                dt_put(Dt, (size_t)nl * L * L * half_count_padded(R), ((size_t)l * L * L + p) * half_count_padded(R) + hpad_index(ox, oy, R), d);
             }
         }
     }
@@ -521,7 +548,7 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma(const uint8_t* __restrict__
         const int g = lane >> 2, tq = lane & 3;
         const uint32_t px = x0 + xs + g, py = y0 + sj, p = py * L + px;
         const int ncp = snorm[sj * S::NCOL + R + xs + g], nnp = snorm[(S::NROW + sj) * S::NCOL + R + xs + g];
-        int4* out = Dt + ((size_t)l * L * L + p) * S::H;
+        const size_t obase = ((size_t)l * L * L + p) * half_count_padded(R), ndt = (size_t)nl * L * L * half_count_padded(R);
 #pragma unroll
         for (int a_oy = 0; a_oy < S::OYG; ++a_oy) {
             const int oy = oy0 + a_oy;
@@ -539,7 +566,7 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma(const uint8_t* __restrict__
                     d.y = ncp + nnq - 2 * acc[a_oy][t][1][e];      // D(c_p, cn_q)
                     d.z = nnp + ncq - 2 * acc[a_oy][t][0][2 + e];  // D(cn_p, c_q)
                     d.w = nnp + nnq - 2 * acc[a_oy][t][1][2 + e];  // D(cn_p, cn_q)
-                    out[half_index(ox, oy, R)] = d;
+                    dt_put(Dt, ndt, obase + hpad_index(ox, oy, R), d);
                 }
         }
         __syncthreads();  // snorm aliases the operand buffers of the next level
@@ -655,7 +682,7 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma2(const uint8_t* __restrict_
             const int xs = 8 * st2;
             const uint32_t px = x0 + xs + g, py = y0 + sj, p = py * L + px;
             const int ncp = snorm[sj * S::NCOL + R + xs + g], nnp = snorm[(S::NROW + sj) * S::NCOL + R + xs + g];
-            int4* out = Dt + ((size_t)l * L * L + p) * S::H;
+            const size_t obase = ((size_t)l * L * L + p) * half_count_padded(R), ndt = (size_t)nl * L * L * half_count_padded(R);
 #pragma unroll
             for (int a_oy = 0; a_oy < S::OYG2; ++a_oy) {
                 const int oy = oy0 + a_oy;
@@ -673,7 +700,7 @@ __global__ void __launch_bounds__(512, 1) k_gram_mma2(const uint8_t* __restrict_
                         d.y = ncp + nnq - 2 * acc[st2][a_oy][t][1][e];      // D(c_p, cn_q)
                         d.z = nnp + ncq - 2 * acc[st2][a_oy][t][0][2 + e];  // D(cn_p, c_q)
                         d.w = nnp + nnq - 2 * acc[st2][a_oy][t][1][2 + e];  // D(cn_p, cn_q)
-                        out[half_index(ox, oy, R)] = d;
+                        dt_put(Dt, ndt, obase + hpad_index(ox, oy, R), d);
                     }
             }
         }
@@ -864,7 +891,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_gram_tc(const uint8_t* __res
             const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
             const int np = snorm[(v * NBR + dy) * NBC + dx + R];
             int* scr = scratch + (warp * 32 + lane) * SCR;
-            int2* out2 = reinterpret_cast<int2*>(Dt + ((size_t)l * P + p) * H) + v;  // .xy (v=0) / .zw (v=1)
+            int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
             for (int nyl = (warp >> 2); nyl < NR; nyl += 2) {  // warps w and w+4 split the neighbour rows
                 const int ny = 8 * ch + nyl, oy = ny - dy;
                 uint32_t rc[32], rn[32];
@@ -887,7 +914,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) k_gram_tc(const uint8_t* __res
                     const int ox = i - R, nx = dx + i;
                     if (oy == 0 && ox <= 0) continue;
                     const int nq_c = snorm[ny * NBC + nx], nq_n = snorm[(NBR + ny) * NBC + nx];
-                    out2[2 * half_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
+                    out2[hpad_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1058,7 +1085,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1) k_gram_tc2(const uint8_t* __r
             }
             named_bar(2, 128);
             const int np = snorm[(v * NBR + dy) * NBC + dx + R];
-            int2* out2 = reinterpret_cast<int2*>(Dt + ((size_t)l * P + p) * H) + v;
+            int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
             for (int ch = 0; ch < NCHUNK; ++ch, ++q) {
                 const uint32_t ub = q & 1, uu = q >> 1;
                 tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
@@ -1085,7 +1112,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1) k_gram_tc2(const uint8_t* __r
                         const int ox = i - R, nx = dx + i;
                         if (oy == 0 && ox <= 0) continue;
                         const int nq_c = snorm[ny * NBC + nx], nq_n = snorm[(NBR + ny) * NBC + nx];
-                        out2[2 * half_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
+                        out2[hpad_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1251,7 +1278,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_const
         const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
         int* scr = scratch + (warp * 32 + lane) * SCR;
         const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
-        int2* out2 = reinterpret_cast<int2*>(Dt + ((size_t)l * P + p) * H) + v;
+        int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
         for (int ch = 0; ch < NCHUNK; ++ch) {
             const uint32_t ub = ch & 1, uu = ch >> 1;
             tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
@@ -1278,7 +1305,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_const
                     const int ox = i - R, nx = dx + 1 + i;
                     if (oy == 0 && ox <= 0) continue;
                     const int nq_c = snorm[ny * NBX + nx], nq_n = snorm[(NBR + ny) * NBX + nx];
-                    out2[2 * half_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
+                    out2[hpad_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1291,6 +1318,13 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
+}
+
+// 256-bit store of four int2 records {(x[0], y[0]) .. (x[3], y[3])} (one whole 32-byte sector).
+__device__ __forceinline__ void st_v8(int2* dst, const int* x, const int* y) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(x[0]), "r"(y[0]), "r"(x[1]),
+                 "r"(y[1]), "r"(x[2]), "r"(y[2]), "r"(x[3]), "r"(y[3])
+                 : "memory");
 }
 
 // Persistent version of k_gram_tc3: one CTA per SM walks the (8x8 block, level) items
@@ -1422,7 +1456,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
             named_bar(2, 128);
             const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
             const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
-            int2* out2 = reinterpret_cast<int2*>(Dt + ((size_t)l * P + p) * H) + v;
+            int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
             for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
                 const uint32_t ub = cc & 1, uu = cc >> 1;
                 tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
@@ -1444,12 +1478,23 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                     for (int j = 0; j < NBX; ++j) scr[j] = (int)rn[j];
 #pragma unroll
                     for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + 1 + i];
+                    // the row's 15 records (+1 zero pad) are 128 contiguous, 64-byte aligned bytes of
+                    // plane v: four whole-sector 256-bit stores (two for the oy = 0 row, ox = 1..R)
+                    int vx[16], vy[16];
 #pragma unroll
                     for (int i = 0; i < 2 * R + 1; ++i) {
-                        const int ox = i - R, nx = dx + 1 + i;
-                        if (oy == 0 && ox <= 0) continue;
-                        const int nq_c = snorm[ny * NBX + nx], nq_n = snorm[(NBR + ny) * NBX + nx];
-                        out2[2 * half_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
+                        const int nx = dx + 1 + i;
+                        vx[i] = np + snorm[ny * NBX + nx] - 2 * dc[i];
+                        vy[i] = np + snorm[(NBR + ny) * NBX + nx] - 2 * dn[i];
+                    }
+                    vx[15] = vy[15] = 0;
+                    if (oy > 0) {
+                        int2* o = out2 + hpad_index(-R, oy, R);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) st_v8(o + 4 * q, vx + 4 * q, vy + 4 * q);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) st_v8(out2 + 4 * q, vx + R + 1 + 4 * q, vy + R + 1 + 4 * q);
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1524,21 +1569,21 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
                                              long long* __restrict__ d0, long long* __restrict__ d1,
                                              longlong2* __restrict__ x0, longlong2* __restrict__ x1, int force_escape,
                                              u128* __restrict__ Epart, int* __restrict__ err) {
-    constexpr int H = 2 * R * R + 2 * R;
+    constexpr int HP = half_count_padded(R), R0 = ru4(R), RW = ru4(2 * R + 1);
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     const uint32_t P = L * L;
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // (p, padded offset hp)
     u128 e = 0;
-    if (idx < (size_t)P * H) {
-        const uint32_t p = (uint32_t)(idx / H), h = (uint32_t)(idx - (size_t)p * H);
-        int ox, oy;
-        if (h < (uint32_t)R) {
-            oy = 0;
-            ox = (int)h + 1;
-        } else {
-            oy = 1 + (int)(h - R) / (2 * R + 1);
-            ox = (int)(h - R) % (2 * R + 1) - R;
-        }
+    const uint32_t p = (uint32_t)(idx / HP), hp = (uint32_t)(idx - (size_t)p * HP);
+    int ox, oy;
+    if (hp < (uint32_t)R0) {
+        oy = 0;
+        ox = (int)hp + 1;
+    } else {
+        oy = 1 + (int)(hp - R0) / RW;
+        ox = (int)(hp - R0) % RW - R;
+    }
+    if (idx < (size_t)P * HP && ox <= R) {  // pads (ox > R) are skipped
         const uint32_t x = p % L, y = p / L;
         const uint32_t q = ((y + oy) & (L - 1)) * L + ((x + ox + L) & (L - 1));
         const int wi = win_index(ox, oy, R), wm = win_index(-ox, -oy, R);
@@ -1548,11 +1593,11 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
         int4 Dv[NL ? NL : 1];
         if (NL) {
 #pragma unroll
-            for (int l = 0; l < (NL ? NL : 1); ++l) Dv[l] = Dt[(size_t)l * P * H + idx];
+            for (int l = 0; l < (NL ? NL : 1); ++l) Dv[l] = dt_get(Dt, (size_t)nl * P * HP, (size_t)l * P * HP + idx);
         }
 #pragma unroll
         for (uint32_t l = 0; l < nl; ++l) {
-            const int4 D = NL ? Dv[NL ? l : 0] : Dt[(size_t)l * P * H + idx];
+            const int4 D = NL ? Dv[NL ? l : 0] : dt_get(Dt, (size_t)nl * P * HP, (size_t)l * P * HP + idx);
             const int dm = lut.Dmax[l];
             if ((unsigned)D.x > (unsigned)dm || (unsigned)D.y > (unsigned)dm || (unsigned)D.z > (unsigned)dm ||
                 (unsigned)D.w > (unsigned)dm) {
@@ -2304,9 +2349,14 @@ __global__ void k_iref(const int2* __restrict__ ab, const uint2* __restrict__ px
 }
 
 // cc component of Dt [l][p][H] (int4) -> int32 [l][p][H].
-__global__ void k_dt_export(const int4* __restrict__ Dt, size_t n, int* __restrict__ out) {
+__global__ void k_dt_export(const int4* __restrict__ Dt, uint32_t P, uint32_t nl, int R, int* __restrict__ out) {
+    const size_t H = (size_t)2 * R * R + 2 * R, HP = half_count_padded(R), n = (size_t)nl * P * H;
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = Dt[i].x;
+    if (i >= n) return;
+    const size_t lp = i / H;
+    const int h = (int)(i - lp * H);
+    const int oy = h < R ? 0 : 1 + (h - R) / (2 * R + 1), ox = h < R ? h + 1 : (h - R) % (2 * R + 1) - R;
+    out[i] = reinterpret_cast<const int2*>(Dt)[lp * HP + hpad_index(ox, oy, R)].x;  // plane 0 .x = D(c_p, c_q)
 }
 
 // Internal [p][l][Tp] -> C-ABI [l][p][Ts].
