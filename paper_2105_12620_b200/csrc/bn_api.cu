@@ -169,6 +169,12 @@ struct bn_ctx {
     cudaStream_t ls = nullptr, aux = nullptr, hp = nullptr;
     cudaEvent_t evA = nullptr, evB = nullptr, evC = nullptr;
     bool no_overlap = false;  // BN_OVERLAP=0: no candidate prefetch on the aux stream
+    // per-row publication of the next pass's candidate counts (k_counts -> k_gram_tc4 follows them)
+    DevBuf<unsigned int> rows_done;
+    uint32_t rows_L = 0, counts_epoch = 0;
+    const unsigned int* gram_rows = nullptr;  // set for the Gram of a pass whose counts may still run
+    uint32_t gram_rows_target = 0;
+    bool no_rowflags = true;  // BN_ROWFLAGS=1: the Gram follows the counts row by row (measured slower on C3)
     int prefetch_at = 1;  // BN_PREFETCH=start|gram|lut: launch the next pass's counts before the Gram / after it / after the energy terms
     bool per_class_decide = false;  // BN_DECIDE=per_class: 64 launches instead of one persistent
     bool simt_gram = false;         // BN_GRAM=simt: dp4a window distances instead of IMMA
@@ -339,7 +345,7 @@ int ensure_counts(bn_ctx* ctx) {
     KSTART(BN_K_COUNTS);
     k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->ls>>>(
         ctx->U.p, nullptr, 0, 0, 0, P, ctx->ab.p, ctx->Cc.p, ctx->cgrp.p, ctx->Tp, ctx->S.p, Nmax, lo, hi, ctx->nl, ctx->c.p,
-        ctx->nc.p);
+        ctx->nc.p, nullptr, ctx->L);
     LAUNCHED_K();
     ctx->counts_dirty = false;
     return BN_OK;
@@ -399,7 +405,8 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
             const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
             const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
-            k_gram_tc4<<<grid, tc3::THREADS, smem, ctx->ls>>>(mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
+            k_gram_tc4<<<grid, tc3::THREADS, smem, ctx->ls>>>(mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p,
+                                                              ctx->gram_rows, ctx->gram_rows_target);
         } else {
             k_gram_tc3<<<dim3(ctx->L / 8, ctx->L / 8, ctx->nl), tc3::THREADS, smem, ctx->ls>>>(
                 mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
@@ -679,6 +686,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->cluster_v1 = dm && !strcmp(dm, "cluster1");
     const char* ov = getenv("BN_OVERLAP");
     ctx->no_overlap = ov && !strcmp(ov, "0");
+    const char* rf = getenv("BN_ROWFLAGS");
+    ctx->no_rowflags = !(rf && !strcmp(rf, "1"));
     const char* pfe = getenv("BN_PREFETCH");
     ctx->prefetch_at = !pfe ? 1 : !strcmp(pfe, "start") ? 0 : !strcmp(pfe, "lut") ? 2 : 1;
     ctx->ls = ctx->stream;
@@ -686,7 +695,10 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
         DeviceGuard g(cuda_device);
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        if (cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        // BN_AUX_PRIO=hi|mid: the candidate-prefetch stream at the critical path's priority / between
+        const char* ap = getenv("BN_AUX_PRIO");
+        const int aux_prio = !ap ? lo : !strcmp(ap, "hi") ? hi : !strcmp(ap, "mid") ? (lo + hi) / 2 : lo;
+        if (cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, aux_prio) != cudaSuccess ||
             cudaStreamCreateWithPriority(&ctx->hp, cudaStreamNonBlocking, hi) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->evA, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->evB, cudaEventDisableTiming) != cudaSuccess ||
@@ -721,7 +733,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->d0.release(); ctx->d1b.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
         ctx->W.release(); ctx->G.release(); ctx->iref.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
-        ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release();
+        ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release(); ctx->rows_done.release();
         if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
         if (ctx->hp) cudaStreamSynchronize(ctx->hp), cudaStreamDestroy(ctx->hp);
         for (cudaEvent_t e : {ctx->evA, ctx->evB, ctx->evC})
@@ -943,12 +955,26 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     auto buf_U = [&](uint32_t pi) { return (overlap && (pi & 1)) ? ctx->Un2.p : ctx->Un.p; };
     auto buf_c = [&](uint32_t pi) { return (overlap && (pi & 1)) ? ctx->cn2.p : ctx->cn.p; };
     auto buf_n = [&](uint32_t pi) { return (overlap && (pi & 1)) ? ctx->nn2.p : ctx->nn.p; };
+    // Row flags: with the persistent tcgen05 Gram, pass t's Gram follows its candidate counts row by
+    // row (k_counts publishes each finished tile-row segment, k_gram_tc4 waits per item), so the
+    // counts of pass t+1 may still be finishing when the Gram of pass t+1 starts.
+    const bool rowflags = overlap && ctx->tc4_gram && ctx->R == 7 && !ctx->no_rowflags;
+    uint32_t rows_target[2] = {0, 0};
+    if (rowflags) {
+        CUDA_TRY(ctx->rows_done.ensure(ctx->L));
+        if (ctx->rows_L != ctx->L) {
+            CUDA_TRY(cudaMemsetAsync(ctx->rows_done.p, 0, ctx->L * sizeof(unsigned int), ctx->stream));
+            ctx->rows_L = ctx->L;
+            ctx->counts_epoch = 0;
+        }
+    }
     auto launch_counts = [&](uint32_t pi) -> int {
         KSTART(BN_K_COUNTS);
         k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->ls>>>(
             nullptr, buf_U(pi), 1, prm->seed, prm->first_pass + pi, P, ctx->ab.p, ctx->Cc.p, ctx->cgrp.p, ctx->Tp, ctx->S.p,
-            ctx->levels[nl - 1], lo, hi, nl, buf_c(pi), buf_n(pi));
+            ctx->levels[nl - 1], lo, hi, nl, buf_c(pi), buf_n(pi), rowflags ? ctx->rows_done.p : nullptr, ctx->L);
         LAUNCHED_K();
+        if (rowflags) rows_target[pi & 1] = ++ctx->counts_epoch * (ctx->L / COUNT_PIX);
         return BN_OK;
     };
     // With overlap, the whole critical path (gram, energy terms, decisions, finish) runs on the
@@ -967,7 +993,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         CUDA_TRY(cudaMemsetAsync(ctx->acc.p, 0, P, cs));
         if (prm->mode == BN_REDRAW) {
             if (overlap && pi > 0) {
-                CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evC, 0));  // prefetched during pass pi-1
+                if (!rowflags) CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evC, 0));  // prefetched during pass pi-1
             } else if ((rc = launch_counts(pi))) {
                 return rc;
             }
@@ -981,6 +1007,9 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         // launched once the Gram (the one SM-saturating kernel of the pass) is done, so they fill
         // the SMs left idle by the memory-bound energy terms and the 16-SM decisions
         const std::function<int()> prefetch = [&]() -> int {
+            // with row flags the Gram only waited per row: everything after it waits for the whole
+            // counts kernel of this pass (recorded in evC during pass pi-1)
+            if (rowflags && pi > 0) CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evC, 0));
             CUDA_TRY(cudaEventRecord(ctx->evB, cs));
             CUDA_TRY(cudaStreamWaitEvent(ctx->aux, ctx->evB, 0));
             ctx->ls = ctx->aux;
@@ -990,9 +1019,16 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             return BN_OK;
         };
         const bool pf = overlap && pi + 1 < prm->passes;
+        const std::function<int()> join = [&]() -> int {  // last pass: only wait for its counts
+            if (rowflags && pi > 0) CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evC, 0));
+            return BN_OK;
+        };
         if (pf && ctx->prefetch_at == 0 && (rc = prefetch())) return rc;
-        if ((rc = gram_lut(ctx, buf_c(pi), buf_n(pi), 1, pf && ctx->prefetch_at == 1 ? &prefetch : nullptr)))
-            return rc;
+        ctx->gram_rows = rowflags ? ctx->rows_done.p : nullptr;
+        ctx->gram_rows_target = rows_target[pi & 1];
+        rc = gram_lut(ctx, buf_c(pi), buf_n(pi), 1, pf && ctx->prefetch_at == 1 ? &prefetch : (rowflags ? &join : nullptr));
+        ctx->gram_rows = nullptr;
+        if (rc) return rc;
         if (pf && ctx->prefetch_at == 2 && (rc = prefetch())) return rc;
         uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
         bool done = false;

@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __re
                                                 const CountGroup* __restrict__ grp, uint32_t Tp,
                                                 const uint2* __restrict__ S, uint32_t Nmax, uint4 lev_lo,
                                                 uint4 lev_hi, uint32_t nl, uint8_t* __restrict__ out,
-                                                int* __restrict__ norms) {
+                                                int* __restrict__ norms, unsigned int* __restrict__ rows_done,
+                                                uint32_t L) {
     constexpr int NI = COUNT_NI;
     __shared__ int2 sXY[COUNT_PIX][128];
     __shared__ float2 sXYf[COUNT_PIX][128];
@@ -301,6 +302,11 @@ __global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __re
     for (uint32_t j = threadIdx.x; j < COUNT_PIX * nl; j += blockDim.x) {
         const uint32_t pp = j / nl, l = j - pp * nl;
         if (p0 + pp < P) norms[(size_t)(p0 + pp) * nl + l] = sNorm[pp][l];
+    }
+    if (rows_done) {  // publish: this CTA's segment of tile row p0 / L is complete (rows, norms, shifts)
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(rows_done + p0 / L, 1u);
     }
 }
 // Tp / 8 integrand groups per pixel: callers guarantee Tp % 256 == 0 (whole warps per group).
@@ -1338,7 +1344,9 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                                                               const __grid_constant__ CountMaps mn,
                                                               const int* __restrict__ nc, const int* __restrict__ nn,
                                                               uint32_t L, uint32_t Tp, uint32_t nl,
-                                                              int4* __restrict__ Dt) {
+                                                              int4* __restrict__ Dt,
+                                                              const unsigned int* __restrict__ rows_done,
+                                                              uint32_t rows_target) {
     using namespace tc3;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
@@ -1374,11 +1382,37 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_sh;
+    // items: blocks in raster order within a level, levels outermost (each level's count slice is
+    // an L2-resident working set); when following k_counts row by row (rows_done), the level is
+    // the fastest index instead, so the Gram sweeps the tile's block rows front to back
     auto item_xyl = [&](uint32_t it, uint32_t& x0, uint32_t& y0, uint32_t& l) {
-        const uint32_t bx = it % nbx, r = it / nbx;
-        x0 = 8 * bx;
-        y0 = 8 * (r % nbx);
-        l = r / nbx;
+        if (rows_done) {
+            l = it % nl;
+            const uint32_t b = it / nl;
+            x0 = 8 * (b % nbx);
+            y0 = 8 * (b / nbx);
+        } else {
+            const uint32_t bx = it % nbx, r = it / nbx;
+            x0 = 8 * bx;
+            y0 = 8 * (r % nbx);
+            l = r / nbx;
+        }
+    };
+    // wait until every tile row y0 .. y0 + 14 (mod L) of this pass's candidates is published by
+    // k_counts (acquire), then order the following TMA (async-proxy) reads after it
+    auto wait_rows = [&](uint32_t y0) {
+        if (!rows_done) return;
+        for (uint32_t r = 0; r < (uint32_t)NBR; ++r) {
+            const unsigned int* f = rows_done + ((y0 + r) & (L - 1));
+            for (uint32_t n = 0;; ++n) {
+                unsigned int v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                if ((int)(v - rows_target) >= 0) break;
+                if (n > (1u << 26)) __trap();  // never hang the GPU on a protocol bug
+                __nanosleep(64);
+            }
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
     };
 
     if (warp == 4) {
@@ -1388,6 +1422,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
             for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
                 uint32_t x0, y0, l;
                 item_xyl(it, x0, y0, l);
+                wait_rows(y0);
                 for (int ch = 0; ch < NCHUNK; ++ch)
                     for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
                         const uint32_t b = g % NSTAGE, use = g / NSTAGE;
@@ -1447,6 +1482,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
         for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
             uint32_t x0, y0, l;
             item_xyl(it, x0, y0, l);
+            if (threadIdx.x == 0) wait_rows(y0);  // the candidates' norms come from k_counts too
             named_bar(2, 128);  // previous item's norms are no longer read
             for (int j = threadIdx.x; j < 2 * NBR * NBX; j += 128) {
                 const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;

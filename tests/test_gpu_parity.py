@@ -325,3 +325,12 @@ def test_decide_kernels_parity(bn, oracle_mod, monkeypatch, decide, L, mode):
     monkeypatch.setenv("BN_DECIDE", decide)
     s, o, U = make(bn, oracle_mod, L, 40, (4, 16))
     _check_run(s, o, U, 2, mode, seed=21 + L + mode)
+
+
+@pytest.mark.parametrize("rowflags", ["0", "1"])
+def test_overlapped_passes_rowflags(bn, oracle_mod, monkeypatch, rowflags):
+    """Multi-pass REDRAW with the next pass's counts prefetched on the low-priority stream; with
+    BN_ROWFLAGS=1 the persistent Gram follows those counts row by row through device flags."""
+    monkeypatch.setenv("BN_ROWFLAGS", rowflags)
+    s, o, U = make(bn, oracle_mod, 32, 130, (1, 4, 16, 64))
+    _check_run(s, o, U, 5, 0, seed=9)
