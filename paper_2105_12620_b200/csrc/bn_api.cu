@@ -187,6 +187,8 @@ struct bn_ctx {
     bool tc2_attr_set = false;
     bool tc3_gram = false;  // BN_GRAM=tc3: TMA-fed warp-specialised tcgen05 window Gram (R = 7)
     bool tc4_gram = false;  // BN_GRAM=tc4 (default): persistent version of tc3
+    bool use_tc5 = false;   // BN_GRAM=tc5: the A-resident variant k_gram_tc5 (Tp <= 1024)
+    bool tc5_attr_set = false;
     bool tc3_attr_set = false;
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
@@ -400,7 +402,19 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
             ctx->tc3_attr_set = true;
         }
         KSTART(BN_K_GRAM);
-        if (ctx->tc4_gram) {  // persistent: one CTA per SM walks the (block, level) items
+        if (ctx->tc4_gram && !ctx->gram_rows && ctx->Tp <= 128u * tc5::NKMAX && ctx->use_tc5) {
+            // persistent with the A operand resident (Tp <= 1024; BN_GRAM=tc5: measured slower on C3,
+            // its 2-stage B ring keeps too few bytes in flight to hide the TMA latency)
+            if (!ctx->tc5_attr_set) {
+                CUDA_TRY(cudaFuncSetAttribute(k_gram_tc5, cudaFuncAttributeMaxDynamicSharedMemorySize, tc5::SMEM));
+                ctx->tc5_attr_set = true;
+            }
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
+            const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
+            const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
+            k_gram_tc5<<<grid, tc3::THREADS, tc5::SMEM, ctx->ls>>>(mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
+        } else if (ctx->tc4_gram) {  // persistent: one CTA per SM walks the (block, level) items
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
             const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
@@ -715,7 +729,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->imma_v1 = gm && !strcmp(gm, "imma1");
     ctx->tc_gram = gm && !strcmp(gm, "tc");
     ctx->tc2_gram = gm && !strcmp(gm, "tc2");
-    ctx->tc4_gram = !gm || !*gm || !strcmp(gm, "tc4");  // default window Gram (R = 7): persistent
+    ctx->tc4_gram = !gm || !*gm || !strcmp(gm, "tc4") || !strcmp(gm, "tc5");  // default (R = 7): persistent
+    ctx->use_tc5 = gm && !strcmp(gm, "tc5");
     ctx->tc3_gram = ctx->tc4_gram || !strcmp(gm, "tc3");
     *out = ctx;
     return BN_OK;

@@ -1546,6 +1546,213 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     }
 }
 
+// k_gram_tc5: k_gram_tc4 with the A operand resident.  For Tp <= 1024 (nk <= 8 K-slices) the
+// block's 128 A rows (c and cn of its 64 pixels) for all K fit in shared memory (8 x 16 KB), so
+// they are loaded once per item instead of once per neighbour chunk: the L2->SM operand stream
+// drops from (A + B) to B per (chunk, K-slice) after the first chunk (1104 -> 848 rows of 128 B
+// per item, -23%).  A slot ks is released by the MMA of the item's
+// last chunk on it and refilled with the next item's slice ks.  B streams through a 2-stage ring,
+// which keeps only 60 KB in flight (tc4: 184 KB): on C3 it is slower than tc4 (0.127 vs 0.120 ms),
+// so it is opt-in (BN_GRAM=tc5).
+namespace tc5 {
+constexpr int NKMAX = 8, NBST = 2;
+constexpr int A_SLOT = tc3::A_BYTES, B_STAGE = tc3::B_BYTES;  // 16 KB, 30 KB
+constexpr int SMEM = NKMAX * A_SLOT + NBST * B_STAGE + 4 * 32 * tc3::SCR * 4 + 2 * tc3::NBR * tc3::NBX * 4 + 1024;
+}  // namespace tc5
+
+__global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc5(const __grid_constant__ CountMaps mc,
+                                                              const __grid_constant__ CountMaps mn,
+                                                              const int* __restrict__ nc, const int* __restrict__ nn,
+                                                              uint32_t L, uint32_t Tp, uint32_t nl,
+                                                              int4* __restrict__ Dt) {
+    using namespace tc3;
+    using tc5::A_SLOT;
+    using tc5::B_STAGE;
+    using tc5::NBST;
+    using tc5::NKMAX;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t sbase = (raw + 1023) & ~1023u;
+    const uint32_t sA = sbase, sB = sbase + NKMAX * A_SLOT;
+    uint8_t* gbase = smem_raw + (sbase - raw);
+    int* scratch = reinterpret_cast<int*>(gbase + NKMAX * A_SLOT + NBST * B_STAGE);  // [4 warps][32][SCR]
+    int* snorm = scratch + 4 * 32 * SCR;                                              // [2][NBR][NBX]
+    __shared__ __align__(8) uint64_t bars[2 * NKMAX + 2 * NBST + 4];
+    __shared__ uint32_t tmem_sh;
+    const uint32_t a_full = (uint32_t)__cvta_generic_to_shared(&bars[0]), a_empty = a_full + 8 * NKMAX;
+    const uint32_t b_full = a_empty + 8 * NKMAX, b_empty = b_full + 8 * NBST;
+    const uint32_t b_tfull = b_empty + 8 * NBST, b_tempty = b_tfull + 16;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nbx = L / 8, nitems = nbx * nbx * nl, P = L * L;
+    const uint32_t nk = Tp / 128;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NKMAX; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a_full + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a_empty + 8 * i) : "memory");
+        }
+        for (int i = 0; i < NBST; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_full + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_empty + 8 * i) : "memory");
+        }
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_tfull + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_tempty + 8 * i) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tmem_sh))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_sh;
+    auto item_xyl = [&](uint32_t it, uint32_t& x0, uint32_t& y0, uint32_t& l) {
+        const uint32_t bx = it % nbx, r = it / nbx;
+        x0 = 8 * bx;
+        y0 = 8 * (r % nbx);
+        l = r / nbx;
+    };
+
+    if (warp == 4) {
+        // --------------------------------------------------------------- TMA producer
+        if (lane == 0) {
+            uint32_t g = 0, ii = 0;  // B stage counter, local item counter
+            for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ii) {
+                uint32_t x0, y0, l;
+                item_xyl(it, x0, y0, l);
+                for (int ch = 0; ch < NCHUNK; ++ch)
+                    for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
+                        const int kx = (int)(l * Tp + ks * 128);
+                        if (ch == 0) {  // A slice ks of this item (its slot was freed by the last item's chunk 2)
+                            if (ii > 0) tc::mbar_wait(a_empty + 8 * ks, (ii - 1) & 1);
+                            const uint32_t abar = a_full + 8 * ks, adst = sA + ks * A_SLOT;
+                            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(abar), "r"(A_SLOT)
+                                         : "memory");
+                            tma_3d(adst, &mc.a, kx, (int)x0, (int)y0, abar);
+                            tma_3d(adst + 8192, &mn.a, kx, (int)x0, (int)y0, abar);
+                        }
+                        const uint32_t b = g % NBST, use = g / NBST;
+                        if (use > 0) tc::mbar_wait(b_empty + 8 * b, (use - 1) & 1);
+                        const uint32_t bdst0 = sB + b * B_STAGE, bar = b_full + 8 * b;
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(B_STAGE)
+                                     : "memory");
+                        const bool whole = x0 >= 8 && x0 + 16 <= L && y0 + CH_ROWS * (ch + 1) <= L;
+                        for (int v = 0; v < 2; ++v) {
+                            const CountMaps& m = v ? mn : mc;
+                            const uint32_t bdst = bdst0 + v * CH_ROWS * GRP * 1024;
+                            if (whole) {
+                                tma_3d(bdst, &m.b, kx, (int)x0 - 8, (int)(y0 + CH_ROWS * ch), bar);
+                            } else {
+                                for (int nyl = 0; nyl < CH_ROWS; ++nyl)
+                                    for (int gx = 0; gx < GRP; ++gx) {
+                                        const uint32_t py = (y0 + CH_ROWS * ch + nyl) & (L - 1);
+                                        const uint32_t px = (x0 + 8 * gx + L - 8) & (L - 1);
+                                        tma_3d(bdst + (nyl * GRP + gx) * 1024, &m.s, kx, (int)px, (int)py, bar);
+                                    }
+                            }
+                        }
+                    }
+            }
+        }
+    } else if (warp == 5) {
+        // --------------------------------------------------------------- UMMA issuer
+        uint32_t g = 0, cc = 0, ii = 0;
+        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ii)
+            for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
+                const uint32_t ub = cc & 1, uu = cc >> 1;
+                if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
+                    const uint32_t b = g % NBST;
+                    if (ch == 0) tc::mbar_wait(a_full + 8 * ks, ii & 1);
+                    tc::mbar_wait(b_full + 8 * b, (g / NBST) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if (lane == 0) {
+                        const uint32_t sa = sA + ks * A_SLOT, sb = sB + b * B_STAGE;
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk),
+                                    tc::idesc_u8(128, N), (ks > 0 || kk > 0) ? 1u : 0u);
+                        tc::commit(b_empty + 8 * b);
+                        if (ch + 1 == NCHUNK) tc::commit(a_empty + 8 * ks);  // last use of A slice ks
+                        if (ks + 1 == nk) tc::commit(b_tfull + 8 * ub);
+                    }
+                    __syncwarp();
+                }
+            }
+    } else if (warp < 4) {
+        // --------------------------------------------------------------- epilogue (as k_gram_tc4)
+        const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
+        int* scr = scratch + (warp * 32 + lane) * SCR;
+        uint32_t cc = 0;
+        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+            uint32_t x0, y0, l;
+            item_xyl(it, x0, y0, l);
+            named_bar(2, 128);  // previous item's norms are no longer read
+            for (int j = threadIdx.x; j < 2 * NBR * NBX; j += 128) {
+                const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;
+                const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - 8) & (L - 1);
+                snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
+            }
+            named_bar(2, 128);
+            const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
+            const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
+            int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
+            for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
+                const uint32_t ub = cc & 1, uu = cc >> 1;
+                tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
+                    const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
+                    uint32_t rc[32], rn[32];
+                    const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub + nyl * NBX;
+                    tc::ld32(ta, rc);
+                    tc::ld32(ta + CH_ROWS * NBX, rn);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (oy < 0 || oy > R) continue;
+                    int dc[2 * R + 1], dn[2 * R + 1];
+#pragma unroll
+                    for (int j = 0; j < NBX; ++j) scr[j] = (int)rc[j];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + 1 + i];
+#pragma unroll
+                    for (int j = 0; j < NBX; ++j) scr[j] = (int)rn[j];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + 1 + i];
+                    int vx[16], vy[16];
+#pragma unroll
+                    for (int i = 0; i < 2 * R + 1; ++i) {
+                        const int nx = dx + 1 + i;
+                        vx[i] = np + snorm[ny * NBX + nx] - 2 * dc[i];
+                        vy[i] = np + snorm[(NBR + ny) * NBX + nx] - 2 * dn[i];
+                    }
+                    vx[15] = vy[15] = 0;
+                    if (oy > 0) {
+                        int2* o = out2 + hpad_index(-R, oy, R);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) st_v8(o + 4 * q, vx + 4 * q, vy + 4 * q);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) st_v8(out2 + 4 * q, vx + R + 1 + 4 * q, vy + R + 1 + 4 * q);
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(b_tempty + 8 * ub);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 // -------------------------------------------------------------------------- energy terms
 // q(o, D) = rn_u64(2^64 * W[o] * G_l[D]); W and G are host-built fp64 tables (exp/sqrt of the
 // host libm), the product is one IEEE multiply (no contraction possible), the scaling by 2^64
@@ -1591,6 +1798,20 @@ __device__ __forceinline__ i128 warp_sum_i128_redux(unsigned long long lo, unsig
 #pragma unroll
     for (int i = 0; i < 8; ++i) r += (u128)s[i] << (16 * i);
     return (i128)r;
+}
+
+// Exact warp sum of a u128 (or an int128 mod 2^128) by a 5-step shuffle butterfly.
+__device__ __forceinline__ u128 warp_sum_u128(u128 v) {
+    unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
+        const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+        const unsigned long long nlo = lo + olo;
+        hi += ohi + (nlo < lo);
+        lo = nlo;
+    }
+    return ((u128)hi << 64) | lo;
 }
 
 struct LutArgs {
@@ -2062,6 +2283,10 @@ struct WinTermsFlags32 : WinTerms<R> {
                 }
             }
         }
+#ifndef BN_DEC_RED
+#define BN_DEC_RED 1
+#endif
+        if (BN_DEC_RED) return (i128)warp_sum_u128((u128)acc);
         return warp_sum_i128_redux((unsigned long long)acc, (unsigned long long)(acc >> 64));
     }
 };
@@ -2232,18 +2457,6 @@ __global__ void __launch_bounds__(1024) k_pass_stats(const u128* __restrict__ Ep
 // (E_before = sum Epart, dE_sum = sum dEp, accepted = sum acc) as per-block partials that the
 // last block to finish (atomic ticket) reduces into `out`; the ticket is reset for the next use.
 // Exact block-wide sums with 64-bit carries (warp shuffles, then warp 0 over the warps).
-__device__ __forceinline__ u128 warp_sum_u128(u128 v) {
-    unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
-        const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
-        const unsigned long long nlo = lo + olo;
-        hi += ohi + (nlo < lo);
-        lo = nlo;
-    }
-    return ((u128)hi << 64) | lo;
-}
 struct FinishPart {
     unsigned long long e[2], d[2];
     unsigned int a, pad[3];

@@ -285,18 +285,18 @@ def test_gram_variants_bit_identical(bn, oracle_mod, L, T, levels, monkeypatch):
     a, b, px, py = synth.make_bank(T, 31)
     U = synth.make_tile(L, 32)
     outs = {}
-    for variant in ("", "tc", "tc2", "tc3", "imma2", "imma1", "simt"):
+    for variant in ("", "tc", "tc2", "tc3", "tc5", "imma2", "imma1", "simt"):
         monkeypatch.setenv("BN_GRAM", variant)
         s, o, _ = make(bn, oracle_mod, L, T, levels, bank=(a, b, px, py), U=U)
         outs[variant] = s.window_distances()
     co = o.counts(U)
     for li in range(len(levels)):
         assert np.array_equal(outs[""][li], _partial_distances(co[li], L))
-    for k in ("tc", "tc2", "tc3", "imma2", "imma1", "simt"):
+    for k in ("tc", "tc2", "tc3", "tc5", "imma2", "imma1", "simt"):
         assert np.array_equal(outs[k], outs[""]), k
 
 
-@pytest.mark.parametrize("variant", ["tc", "tc2", "tc3", "tc4"])
+@pytest.mark.parametrize("variant", ["tc", "tc2", "tc3", "tc4", "tc5"])
 def test_tc_gram_optimize_parity(bn, oracle_mod, monkeypatch, variant):
     """Full passes with the tcgen05 window Grams against the oracle (C3 shape, ragged T)."""
     monkeypatch.setenv("BN_GRAM", variant)
