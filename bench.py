@@ -137,22 +137,21 @@ def algorithmic(kernel, cfg):
         # one half-plane test per (pixel, integrand, sample) = 2 FFMA (fp32 filter, exact fallback)
         return 2.0 * P * T * max(cfg.levels), "ffma", "alu"
     if kernel == "lut":
-        # bytes: read 4 int32 distances per (p, h, level); write 4 int128 dE terms per (p, h)
-        return float(P * H * (16 * nl + 64)), "bytes", "hbm"
+        # bytes: read the 4 int32 distances per (p, h, level) (two int2 planes); write the 4 int64
+        # dE terms per (p, h) (p side and q side; the int128 escapes are rare)
+        return float(P * H * (16 * nl + 32)), "bytes", "hbm"
     if kernel == "decide":
-        # bytes: both int128 dE terms per (candidate, window offset), all 64 classes in one launch
-        return float(P * ((2 * R + 1) ** 2 - 1) * 32), "bytes", "hbm"
+        # bytes: both int64 dE terms per (candidate, window offset), all 64 classes in one launch
+        return float(P * ((2 * R + 1) ** 2 - 1) * 16), "bytes", "hbm"
     return None, None, None
 
 
-CRITICAL = ("gram", "lut", "decide", "commit", "gather")  # counts(t+1) overlaps decide(t)
-
-
 def roofline(prof, cfg, peaks, sm_clock_mhz, name=None):
-    """Roofline line of one kernel class; default: the largest on the critical path."""
+    """Roofline line of one kernel class; default: the kernel with the largest device time per
+    step (C3: k_counts, which runs beside the energy terms and decisions and, with the Gram,
+    sets the pass time -- DESIGN.md 7)."""
     if name is None:
-        crit = {k: v for k, v in prof.items() if k in CRITICAL} or prof
-        name = max(crit, key=lambda k: crit[k][0])
+        name = max(prof, key=lambda k: prof[k][0])
     ms, n = prof[name]
     units, kind, bound = algorithmic(name, cfg)
     share = ms / max(1e-9, sum(v[0] for v in prof.values()))
@@ -194,8 +193,12 @@ def roofline(prof, cfg, peaks, sm_clock_mhz, name=None):
     if sm_clock_mhz:
         out["sm_mhz_during_run"] = sm_clock_mhz
     if name == "gram" and cfg.name in ("C3", "C4", "C5"):
-        out["limiter"] = ("L2->SM operand streaming: the UMMA pipe runs at its peak MAC rate when fed, "
-                          "but a TMA-only run of the same kernel takes ~85% of its time (DESIGN.md 5.3)")
+        out["limiter"] = ("L2->SM operand streaming: the UMMA pipe runs at its peak MAC rate when fed "
+                          "(tools/umma_bench.cu), a run without the epilogue takes ~80% of the kernel "
+                          "time; 31% of the issued MACs are useful (dense 128x240 tiles, DESIGN.md 5.1)")
+    if name == "counts":
+        out["limiter"] = ("ALU-pipe issue: per test 1 FFMA2 (fma pipe) + ~1.75 half-rate ALU ops (sign "
+                          "count, |t| filter); the FFMA-lane peak is the reported denominator (DESIGN.md 5.1)")
     return out
 
 

@@ -810,7 +810,9 @@ int bn_set_bank(bn_ctx* ctx, uint32_t T, const int32_t* a, const int32_t* b, con
     ctx->px.assign(px, px + T);
     ctx->py.assign(py, py + T);
     std::vector<int2> ab(ctx->Tp, make_int2(0, 0));
-    std::vector<long long> C(ctx->Tp, 1);  // padding integrands never count
+    // padding integrands (a = b = 0) never count: t = -C is far outside the fp32 filter band, so
+    // they are never recounted either
+    std::vector<long long> C(ctx->Tp, 1ll << 62);
     std::vector<uint2> pxy(ctx->Ts);
     for (uint32_t j = 0; j < ctx->Ts; ++j) {
         const uint32_t i = t_begin + j;

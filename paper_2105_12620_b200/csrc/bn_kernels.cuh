@@ -91,7 +91,7 @@ __host__ __device__ __forceinline__ int hpad_index(int ox, int oy, int R) {
 //   c_l,p,i = #{k < N_l : a_i (X_k - PX_i) + b_i (Y_k - PY_i) >= 0},  X_k = S_k.x + u_p.x mod 2^32.
 // With X' = X - 2^31 as int32, the test is a_i X' + b_i Y' >= C_i,  C_i = a PX + b PY - (a+b) 2^31,
 // i.e. two 32x32->64 integer multiply-adds per (pixel, integrand, sample): exact.
-// Padding integrands (i >= Ts) use a = b = 0, C = 1, so they always count 0.
+// Padding integrands (i >= Ts) use a = b = 0, C = 2^62, so they always count 0 (t = -C).
 // Layout out: [p][l][Tp] uint8; norms: [p][l] int32 = sum_i c^2.
 #ifndef BN_COUNT_PIX
 #define BN_COUNT_PIX 8
