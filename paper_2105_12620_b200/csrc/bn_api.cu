@@ -194,6 +194,7 @@ struct bn_ctx {
     bool cluster_attr_set[8] = {false};
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
+    bool cluster_v2 = false;  // BN_DECIDE=cluster2: shared-memory-staged rows (v2)
     // per-kernel event timing (bn_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -555,14 +556,18 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     *done = false;
     if (ncta > 16 || ctx->no_cluster) return BN_OK;
     // v2 (default): u32 flags + slot table; v1 (BN_DECIDE=cluster1): byte flags, cluster barriers
-    const bool v2 = !ctx->cluster_v1;
-    const size_t smem = v2 ? (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8 + 4 * (size_t)P + 64 * 4 * (mode ? 2 : 1) * cpc
-                           : (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8 + P;  // double-buffered rows + flags
-    const void* fn = v2 ? (mode ? (const void*)k_decide_cl2<R, 1> : (const void*)k_decide_cl2<R, 0>)
-                        : (mode ? (const void*)k_decide_cluster<R, 1> : (const void*)k_decide_cluster<R, 0>);
+    // v3 (default): register-prefetched rows; v2 (BN_DECIDE=cluster2): rows staged in shared memory
+    // by bulk copies; v1 (BN_DECIDE=cluster1): byte flags + a cluster barrier per class
+    const int ver = ctx->cluster_v1 ? 1 : ctx->cluster_v2 ? 2 : 3;
+    const size_t rows = (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8, slots = (size_t)64 * 4 * (mode ? 2 : 1) * cpc;
+    const size_t smem = ver == 3 ? 4 * (size_t)P + slots : ver == 2 ? rows + 4 * (size_t)P + slots : rows + P;
+    const void* fn = ver == 3   ? (mode ? (const void*)k_decide_cl3<R, 1> : (const void*)k_decide_cl3<R, 0>)
+                     : ver == 2 ? (mode ? (const void*)k_decide_cl2<R, 1> : (const void*)k_decide_cl2<R, 0>)
+                                : (mode ? (const void*)k_decide_cluster<R, 1> : (const void*)k_decide_cluster<R, 0>);
     if (!ctx->cluster_attr_set[R]) {
         for (const void* f : {(const void*)k_decide_cluster<R, 0>, (const void*)k_decide_cluster<R, 1>,
-                              (const void*)k_decide_cl2<R, 0>, (const void*)k_decide_cl2<R, 1>}) {
+                              (const void*)k_decide_cl2<R, 0>, (const void*)k_decide_cl2<R, 1>,
+                              (const void*)k_decide_cl3<R, 0>, (const void*)k_decide_cl3<R, 1>}) {
             CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
             CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         }
@@ -698,6 +703,7 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->per_class_decide = dm && !strcmp(dm, "per_class");
     ctx->no_cluster = dm && !strcmp(dm, "flags");
     ctx->cluster_v1 = dm && !strcmp(dm, "cluster1");
+    ctx->cluster_v2 = dm && !strcmp(dm, "cluster2");
     const char* ov = getenv("BN_OVERLAP");
     ctx->no_overlap = ov && !strcmp(ov, "0");
     const char* rf = getenv("BN_ROWFLAGS");

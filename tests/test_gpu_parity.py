@@ -304,7 +304,7 @@ def test_tc_gram_optimize_parity(bn, oracle_mod, monkeypatch, variant):
     _check_run(s, o, U, 2, 0, seed=7)
 
 
-@pytest.mark.parametrize("decide", ["", "cluster1", "flags", "per_class"])
+@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags", "per_class"])
 def test_escape_path_all_terms(bn, oracle_mod, monkeypatch, decide):
     """dE terms are int64 with an int128 escape; forcing every term through the escape tables
     (BN_DT_ESCAPE=1) must give the same bit-exact passes on every decision kernel."""
@@ -316,7 +316,7 @@ def test_escape_path_all_terms(bn, oracle_mod, monkeypatch, decide):
     _check_run(s2, o2, U2, 2, 1, seed=14)
 
 
-@pytest.mark.parametrize("decide", ["", "cluster1", "flags"])
+@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags"])
 @pytest.mark.parametrize("L,mode", [(16, 0), (64, 1), (128, 0), (128, 1)])
 def test_decide_kernels_parity(bn, oracle_mod, monkeypatch, decide, L, mode):
     """Every persistent decision kernel (barrier-free cluster v2 = default, cluster v1 with a
