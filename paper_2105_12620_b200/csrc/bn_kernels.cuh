@@ -161,17 +161,27 @@ __device__ __forceinline__ void count_sample1(float2 p0, const unsigned long lon
     }
 }
 
-template <int NI>
-__device__ __forceinline__ void count_span(const float2* __restrict__ xyf, uint32_t k0, uint32_t k1,
+// Samples [k0, k1) of NPX pixels at once (independent accumulator chains: more ILP per warp).
+template <int NI, int NPX>
+__device__ __forceinline__ void count_span(const float2* const* xyf, uint32_t k0, uint32_t k1,
                                            const unsigned long long* a2, const unsigned long long* b2,
-                                           const unsigned long long* c2, uint32_t* acc, float* mn) {
+                                           const unsigned long long* c2, uint32_t (*acc)[NI / 2],
+                                           float (*mn)[NI / 2]) {
     uint32_t k = k0;
-    for (; k + 4 <= k1; k += 4) {
-        count_sample2<NI>(xyf[k], xyf[k + 1], a2, b2, c2, acc, mn);
-        count_sample2<NI>(xyf[k + 2], xyf[k + 3], a2, b2, c2, acc, mn);
+    constexpr uint32_t STEP = NPX == 1 ? 4 : 2;
+    for (; k + STEP <= k1; k += STEP) {
+#pragma unroll
+        for (int x = 0; x < NPX; ++x) {
+            count_sample2<NI>(xyf[x][k], xyf[x][k + 1], a2, b2, c2, acc[x], mn[x]);
+            if (NPX == 1) count_sample2<NI>(xyf[x][k + 2], xyf[x][k + 3], a2, b2, c2, acc[x], mn[x]);
+        }
     }
-    for (; k + 2 <= k1; k += 2) count_sample2<NI>(xyf[k], xyf[k + 1], a2, b2, c2, acc, mn);
-    if (k < k1) count_sample1<NI>(xyf[k], a2, b2, c2, acc, mn);
+    for (; k + 2 <= k1; k += 2)
+#pragma unroll
+        for (int x = 0; x < NPX; ++x) count_sample2<NI>(xyf[x][k], xyf[x][k + 1], a2, b2, c2, acc[x], mn[x]);
+    if (k < k1)
+#pragma unroll
+        for (int x = 0; x < NPX; ++x) count_sample1<NI>(xyf[x][k], a2, b2, c2, acc[x], mn[x]);
 }
 
 // Each thread owns NI = 8 consecutive integrands (two packed 32-bit words per level row) and
@@ -195,6 +205,102 @@ __global__ void k_count_prep(const int2* __restrict__ ab, const long long* __res
         r.c2[h] = pack2(-__ll2float_rn(Cc[COUNT_NI * q + 2 * h]), -__ll2float_rn(Cc[COUNT_NI * q + 2 * h + 1]));
     }
     g[q] = r;
+}
+
+// NPX pixels (pp, pp + nsub, ...) of the CTA against integrand group q: counts per level, row
+// norms, and the warp-cooperative exact recount of ambiguous pairs (see k_counts).
+template <int NI, int NPX>
+__device__ __forceinline__ void count_pixels(uint32_t pp0, uint32_t nsub, uint32_t p0, const CountGroup& gq, uint32_t q,
+                                             float2 (*sXYf)[128], int2 (*sXY)[128], const uint32_t* levels,
+                                             uint32_t nl, uint32_t Tp, uint32_t Nmax, uint8_t* __restrict__ out,
+                                             const int2* __restrict__ ab, const long long* __restrict__ Cc,
+                                             int (*sNorm)[8]) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t acc[NPX][NI / 2];  // packed negative-test counts per pair of integrands (sgn2)
+    float mn[NPX][NI / 2];      // min |t| per pair of integrands
+    const float2* xyf[NPX];
+#pragma unroll
+    for (int x = 0; x < NPX; ++x) {
+        xyf[x] = sXYf[pp0 + x * nsub];
+#pragma unroll
+        for (int j = 0; j < NI / 2; ++j) acc[x][j] = 0, mn[x][j] = 3.0e38f;
+    }
+    uint32_t kprev = 0;
+    for (uint32_t li = 0; li < nl; ++li) {
+        const uint32_t n1 = levels[li];
+        count_span<NI, NPX>(xyf, kprev, n1, gq.a2, gq.b2, gq.c2, acc, mn);
+        kprev = n1;
+#pragma unroll
+        for (int x = 0; x < NPX; ++x) {
+            const uint32_t pp = pp0 + x * nsub;
+            uint32_t neg[NI];
+#pragma unroll
+            for (int h = 0; h < NI / 2; ++h) sign_counts(acc[x][h], neg[2 * h], neg[2 * h + 1]);
+            uint32_t w[NI / 4];
+            uint32_t nsq = 0;
+#pragma unroll
+            for (int h = 0; h < NI / 4; ++h) {
+                const uint32_t c0 = n1 - neg[4 * h], c1 = n1 - neg[4 * h + 1];
+                const uint32_t c2 = n1 - neg[4 * h + 2], c3 = n1 - neg[4 * h + 3];
+                w[h] = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+                nsq = __dp4a(w[h], w[h], nsq);  // sum of the four squared counts
+            }
+            uint8_t* orow = out + (size_t)(p0 + pp) * nl * Tp + NI * q;
+            *reinterpret_cast<uint2*>(orow + (size_t)li * Tp) = make_uint2(w[0], w[1]);
+            // a warp's lanes share the pixel (q runs over whole warps): one REDUX, one atomic
+            nsq = __reduce_add_sync(0xffffffffu, nsq);
+            if (lane == 0) atomicAdd(&sNorm[pp][li], (int)nsq);
+        }
+    }
+    // exact int64 recount of any pair of integrands whose samples came within the error band,
+    // done by the whole warp (the pixel is warp-uniform): lane k tests samples k, k+32, ...;
+    // per-level counts are popcounts of the ballots
+#pragma unroll
+    for (int x = 0; x < NPX; ++x) {
+        const uint32_t pp = pp0 + x * nsub;
+        uint8_t* orow = out + (size_t)(p0 + pp) * nl * Tp + NI * q;
+#pragma unroll
+        for (int h = 0; h < NI / 2; ++h) {
+            uint32_t need = __ballot_sync(0xffffffffu, mn[x][h] < COUNT_EXACT_BAND);
+            while (need) {
+                const int src = __ffs(need) - 1;
+                need &= need - 1;
+                const uint32_t qs = __shfl_sync(0xffffffffu, q, src);
+                for (int e = 0; e < 2; ++e) {
+                    const uint32_t i = NI * qs + 2 * h + e;
+                    const int2 abj = ab[i];
+                    const long long cj = Cc[i];
+                    uint32_t bits[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t k = lane + 32 * r;
+                        bool pos = false;
+                        if (k < Nmax) {
+                            const int2 xy = sXY[pp][k];
+                            pos = ((long long)abj.x * xy.x + (long long)abj.y * xy.y - cj) >= 0;
+                        }
+                        bits[r] = __ballot_sync(0xffffffffu, pos);
+                    }
+                    if ((int)lane == src) {
+                        for (uint32_t lj = 0; lj < nl; ++lj) {
+                            const uint32_t n1 = levels[lj];
+                            uint32_t cnt = 0;
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) {
+                                const uint32_t lo = 32 * r;
+                                const uint32_t m = n1 <= lo ? 0u : n1 - lo >= 32 ? 0xffffffffu : (1u << (n1 - lo)) - 1u;
+                                cnt += __popc(bits[r] & m);
+                            }
+                            uint8_t* cell = orow + (size_t)lj * Tp + 2 * h + e;
+                            const int old = *cell;
+                            *cell = (uint8_t)cnt;
+                            atomicAdd(&sNorm[pp][lj], (int)(cnt * cnt) - old * old);
+                        }
+                    }
+                }
+            }
+        }
+    }
 }
 
 #ifndef BN_COUNT_MINB
@@ -251,80 +357,12 @@ __global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __re
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t q = tq; q < qn; q += blockDim.x / nsub) {
         const CountGroup gq = q == tq ? g0 : grp[q];
-        for (uint32_t pp = sub; pp < COUNT_PIX; pp += nsub) {
-            const uint32_t p = p0 + pp;
-            if (p >= P) break;
-            uint32_t acc[NI / 2];  // packed negative-test counts per pair of integrands (sgn2)
-            float mn[NI / 2];      // min |t| per pair of integrands
-#pragma unroll
-            for (int j = 0; j < NI / 2; ++j) acc[j] = 0, mn[j] = 3.0e38f;
-            uint8_t* orow = out + (size_t)p * nl * Tp + NI * q;
-            uint32_t kprev = 0;
-            for (uint32_t li = 0; li < nl; ++li) {
-                const uint32_t n1 = levels[li];
-                count_span<NI>(sXYf[pp], kprev, n1, gq.a2, gq.b2, gq.c2, acc, mn);
-                kprev = n1;
-                uint32_t neg[NI];
-#pragma unroll
-                for (int h = 0; h < NI / 2; ++h) sign_counts(acc[h], neg[2 * h], neg[2 * h + 1]);
-                uint32_t w[NI / 4];
-                uint32_t nsq = 0;
-#pragma unroll
-                for (int h = 0; h < NI / 4; ++h) {
-                    const uint32_t c0 = n1 - neg[4 * h], c1 = n1 - neg[4 * h + 1];
-                    const uint32_t c2 = n1 - neg[4 * h + 2], c3 = n1 - neg[4 * h + 3];
-                    w[h] = c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
-                    nsq = __dp4a(w[h], w[h], nsq);  // sum of the four squared counts
-                }
-                *reinterpret_cast<uint2*>(orow + (size_t)li * Tp) = make_uint2(w[0], w[1]);
-                // a warp's lanes share the pixel (tq runs over whole warps): one REDUX, one atomic
-                nsq = __reduce_add_sync(0xffffffffu, nsq);
-                if (lane == 0) atomicAdd(&sNorm[pp][li], (int)nsq);
-            }
-            // exact int64 recount of any pair of integrands whose samples came within the error
-            // band, done by the whole warp (the pixel is warp-uniform): lane k tests samples
-            // k, k+32, ...; per-level counts are popcounts of the ballots
-#pragma unroll
-            for (int h = 0; h < NI / 2; ++h) {
-                uint32_t need = __ballot_sync(0xffffffffu, mn[h] < COUNT_EXACT_BAND);
-                while (need) {
-                    const int src = __ffs(need) - 1;
-                    need &= need - 1;
-                    const uint32_t qs = __shfl_sync(0xffffffffu, q, src);
-                    for (int e = 0; e < 2; ++e) {
-                        const uint32_t i = NI * qs + 2 * h + e;
-                        const int2 abj = ab[i];
-                        const long long cj = Cc[i];
-                        uint32_t bits[4];
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const uint32_t k = lane + 32 * r;
-                            bool pos = false;
-                            if (k < Nmax) {
-                                const int2 xy = sXY[pp][k];
-                                pos = ((long long)abj.x * xy.x + (long long)abj.y * xy.y - cj) >= 0;
-                            }
-                            bits[r] = __ballot_sync(0xffffffffu, pos);
-                        }
-                        if ((int)lane == src) {
-                            for (uint32_t lj = 0; lj < nl; ++lj) {
-                                const uint32_t n1 = levels[lj];
-                                uint32_t cnt = 0;
-#pragma unroll
-                                for (int r = 0; r < 4; ++r) {
-                                    const uint32_t lo = 32 * r;
-                                    const uint32_t m = n1 <= lo ? 0u : n1 - lo >= 32 ? 0xffffffffu : (1u << (n1 - lo)) - 1u;
-                                    cnt += __popc(bits[r] & m);
-                                }
-                                uint8_t* cell = orow + (size_t)lj * Tp + 2 * h + e;
-                                const int old = *cell;
-                                *cell = (uint8_t)cnt;
-                                atomicAdd(&sNorm[pp][lj], (int)(cnt * cnt) - old * old);
-                            }
-                        }
-                    }
-                }
-            }
+        for (uint32_t pp = sub; pp < COUNT_PIX; pp += 2 * nsub) {
+            if (p0 + pp >= P) break;
+            if (pp + nsub < COUNT_PIX && p0 + pp + nsub < P)  // two of the thread's pixels at once
+                count_pixels<NI, 2>(pp, nsub, p0, gq, q, sXYf, sXY, levels, nl, Tp, Nmax, out, ab, Cc, sNorm);
+            else
+                count_pixels<NI, 1>(pp, nsub, p0, gq, q, sXYf, sXY, levels, nl, Tp, Nmax, out, ab, Cc, sNorm);
         }
     }
     __syncthreads();
