@@ -461,3 +461,95 @@ int orc_optimize(const orc_problem *pb, uint32_t *U, uint8_t *c, const orc_opt *
 uint32_t orc_active_pixel(uint32_t L, uint64_t seed, uint32_t t, uint32_t s, uint32_t m) {
     return active_pixel(L, seed, t, s / 8, s % 8, m);
 }
+
+/* ---------------------------------------------------------------------------------------
+ * Paper-verbatim parallel optimisation (§3.4 l.291-307; SURVEY §8(f) row f1;
+ * readings R11, R25-R27 in DESIGN.md §2).
+ *
+ * Couples of pass t (l.303-306: "we precompute a permutation of pixel indices that we store in
+ * a linear array.  We scramble the pixel indices using an XOR with a different seed per
+ * compute pass"):
+ *   key(t)   = Philox(seed; t, 0, 0, 5)[0] & (P - 1)          (P a power of two: a bijection)
+ *   sigma_j  = perm[j] ^ key(t)
+ *   couple c = (sigma_2c, sigma_2c+1),   c < budget / 2       (l.298: budget N/4 pixels, R11)
+ * Pixel-disjoint by construction (l.293-294 "a pixel in a swap couple is not used in another
+ * couple").  Every couple is evaluated against the tile as it stands at the start of the pass
+ * ("we evaluate the cost function with no modification", l.294-295; snapshot reading R26,
+ * SPEC.md l.250), and every couple with dE < 0 is swapped.  Concurrent swaps of nearby
+ * couples are not accounted for, so E may rise (l.295-297).
+ * --------------------------------------------------------------------------------------- */
+uint32_t orc_paper_key(uint64_t seed, uint32_t t, uint32_t P) {
+    uint32_t o4[4];
+    philox_seed(seed, t, 0, 0, 5, o4);
+    return o4[0] & (P - 1);
+}
+
+/* Couples of one pass: out[2c], out[2c+1] for c < budget/2.  -1 if P is not a power of two
+ * (the XOR would leave [0, P)) or the budget is odd / out of range. */
+int orc_paper_couples(const uint32_t *perm, uint32_t P, uint32_t key, uint32_t budget,
+                      uint32_t *out) {
+    if (P == 0 || (P & (P - 1)) || (budget & 1) || budget > P || key >= P) return -1;
+    for (uint32_t j = 0; j < budget; ++j) out[j] = perm[j] ^ key;
+    return 0;
+}
+
+/* passes of the paper-verbatim optimiser.  perm: [P] permutation of pixel indices;
+ * budget: pixels per pass (even, 2..P).  stats[pi]: accepted couples, proposed = budget/2,
+ * dE_sum = sum of the accepted couples' snapshot dE, E after the pass recomputed from scratch.
+ * accept_log: optional [passes][budget/2] bytes.  Returns 0, or -1 on bad arguments. */
+int orc_paper_optimize(const orc_problem *pb, uint32_t *U, uint8_t *c, const uint32_t *perm,
+                       uint32_t budget, uint32_t passes, uint32_t first_pass, uint64_t seed,
+                       orc_stats *stats, uint8_t *accept_log) {
+    const uint32_t L = pb->L, P = L * L, T = pb->T, nl = pb->n_levels;
+    const size_t rowlen = (size_t)nl * T;
+    if (L < 16 || (L & (L - 1)) || pb->radius < 1 || pb->radius > 7) return -1;
+    if (budget < 2 || (budget & 1) || budget > P) return -1;
+    uint8_t *seen = calloc(P, 1);
+    for (uint32_t j = 0; j < P; ++j) {
+        if (perm[j] >= P || seen[perm[j]]) { free(seen); return -1; }   /* not a permutation */
+        seen[perm[j]] = 1;
+    }
+    free(seen);
+    const uint32_t nc = budget / 2;
+    uint32_t *pix = malloc(sizeof(uint32_t) * budget);
+    i128 *dEs = malloc(sizeof(i128) * nc);
+    uint8_t *rp = malloc(rowlen), *rq = malloc(rowlen);
+    for (uint32_t pi = 0; pi < passes; ++pi) {
+        const uint32_t t = first_pass + pi;
+        orc_paper_couples(perm, P, orc_paper_key(seed, t, P), budget, pix);
+        /* 1. every couple against the snapshot (the counts are not modified in this loop) */
+        for (uint32_t k = 0; k < nc; ++k) {
+            const uint32_t p = pix[2 * k], q = pix[2 * k + 1];
+            get_rows(pb, c, p, rp);
+            get_rows(pb, c, q, rq);
+            dEs[k] = delta_replace(pb, c, p, rq, q) + delta_replace(pb, c, q, rp, p);
+        }
+        /* 2. swap every improving couple (disjoint: the order does not matter) */
+        uint32_t accepted = 0;
+        i128 dE_sum = 0;
+        for (uint32_t k = 0; k < nc; ++k) {
+            const int ok = dEs[k] < 0;
+            if (accept_log) accept_log[(size_t)pi * nc + k] = (uint8_t)ok;
+            if (!ok) continue;
+            const uint32_t p = pix[2 * k], q = pix[2 * k + 1];
+            get_rows(pb, c, p, rp);
+            get_rows(pb, c, q, rq);
+            set_rows(pb, c, p, rq);
+            set_rows(pb, c, q, rp);
+            uint32_t ux = U[2 * p], uy = U[2 * p + 1];
+            U[2 * p] = U[2 * q]; U[2 * p + 1] = U[2 * q + 1];
+            U[2 * q] = ux; U[2 * q + 1] = uy;
+            ++accepted;
+            dE_sum += dEs[k];
+        }
+        if (stats) {
+            stats[pi].accepted = accepted;
+            stats[pi].proposed = nc;
+            stats[pi].dE_sum[0] = (uint64_t)(u128)dE_sum;
+            stats[pi].dE_sum[1] = (uint64_t)((u128)dE_sum >> 64);
+            orc_energy(pb, c, stats[pi].E_fixed, &stats[pi].E_plain);
+        }
+    }
+    free(pix); free(dEs); free(rp); free(rq);
+    return 0;
+}

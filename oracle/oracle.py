@@ -102,6 +102,15 @@ def lib():
         _lib.orc_active_pixel.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                           ctypes.c_uint32]
         _lib.orc_active_pixel.restype = ctypes.c_uint32
+        _lib.orc_paper_key.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32]
+        _lib.orc_paper_key.restype = ctypes.c_uint32
+        _lib.orc_paper_couples.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                           ctypes.c_void_p]
+        _lib.orc_paper_couples.restype = ctypes.c_int
+        _lib.orc_paper_optimize.argtypes = [P(Problem), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
+                                            ctypes.c_void_p, ctypes.c_void_p]
+        _lib.orc_paper_optimize.restype = ctypes.c_int
     return _lib
 
 
@@ -141,6 +150,20 @@ def sample(d1: int, d2: int, ux: int, uy: int, k: int) -> tuple:
     o = (ctypes.c_uint32 * 2)()
     lib().orc_sample(d1, d2, ux, uy, k, o)
     return int(o[0]), int(o[1])
+
+
+def paper_key(seed: int, t: int, P: int) -> int:
+    """Per-pass XOR scramble key = Philox(seed; t,0,0,5)[0] & (P-1) (R25)."""
+    return lib().orc_paper_key(seed, t, P)
+
+
+def paper_couples(perm, key: int, budget: int) -> np.ndarray:
+    """Couples of one pass, [budget/2, 2]: (perm[2c]^key, perm[2c+1]^key)."""
+    perm = np.ascontiguousarray(perm, dtype=np.uint32)
+    out = np.zeros(budget, np.uint32)
+    if lib().orc_paper_couples(perm.ctypes.data, len(perm), key, budget, out.ctypes.data) != 0:
+        raise ValueError("oracle rejected the couple arguments")
+    return out.reshape(-1, 2)
 
 
 def iref(a: int, b: int, px: int, py: int) -> float:
@@ -231,6 +254,25 @@ class OracleProblem:
                                 acc.ctypes.data if acc is not None else None)
         if rc != 0:
             raise ValueError("oracle rejected the optimisation arguments")
+        stats = [dict(accepted=s.accepted, proposed=s.proposed, E_plain=s.E_plain,
+                      E_fixed=_u128(s.E_fixed[0], s.E_fixed[1]), dE_sum=_i128(s.dE_sum[0], s.dE_sum[1]))
+                 for s in list(st)[:passes]]
+        return U, c, stats, acc
+
+    def paper_optimize(self, U: np.ndarray, perm, *, budget: int | None = None, passes: int = 1,
+                       first_pass: int = 0, seed: int = 3, c: np.ndarray | None = None, log: bool = False):
+        """Paper-verbatim parallel swaps against the pass-start snapshot (§3.4 l.291-307).
+        Returns (U, c, stats list, accept log [passes, budget/2] or None)."""
+        U = np.array(U, dtype=np.uint32).reshape(-1, 2).copy()
+        c = self.counts(U) if c is None else np.array(c, dtype=np.uint8, copy=True)
+        perm = np.ascontiguousarray(perm, dtype=np.uint32)
+        budget = self.P // 4 if budget is None else budget
+        st = (Stats * max(passes, 1))()
+        acc = np.zeros((passes, max(budget // 2, 1)), dtype=np.uint8) if log else None
+        rc = lib().orc_paper_optimize(self.ref(), U.ctypes.data, c.ctypes.data, perm.ctypes.data, budget, passes,
+                                      first_pass, seed, st, acc.ctypes.data if acc is not None else None)
+        if rc != 0:
+            raise ValueError("oracle rejected the paper-mode arguments")
         stats = [dict(accepted=s.accepted, proposed=s.proposed, E_plain=s.E_plain,
                       E_fixed=_u128(s.E_fixed[0], s.E_fixed[1]), dE_sum=_i128(s.dE_sum[0], s.dE_sum[1]))
                  for s in list(st)[:passes]]

@@ -49,6 +49,14 @@ def make_tile(L: int, seed: int) -> np.ndarray:
     return rng.integers(0, 1 << 32, size=(L * L, 2), dtype=np.uint64).astype(np.uint32)
 
 
+def make_permutation(P: int, seed: int) -> np.ndarray:
+    """Precomputed permutation of the P pixel indices of the paper-verbatim optimiser
+    ("we precompute a permutation of pixel indices that we store in a
+    linear array"; how it is drawn is unstated -- uniform, reading R25).  uint32 [P]."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.permutation(P).astype(np.uint32)
+
+
 def axis_cut_bank(N: int, js, axis: str = "x"):
     """Lattice-aligned axis steps f = [x >= j/N] (or y): the exact-integral pin bank."""
     js = np.asarray(js, dtype=np.int64)

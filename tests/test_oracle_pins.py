@@ -320,3 +320,116 @@ def test_greedy_lowers_low_frequency_error_power(oracle_mod):
         return F[(r > 0) & (r < 0.12)].mean() / F[r > 0].mean()
 
     assert low_power(c1) < 0.8 * low_power(pb.counts(U))
+
+
+# ------------------------------------------------------- paper-verbatim parallel swaps (f1) --
+def test_paper_couples_spec_examples(oracle_mod):
+    """identity permutation, XOR key 0, budget 4 -> (0,1),(2,3); identity of 8
+    indices, key 1 -> sequence [1,0,3,2,...], couples (1,0),(3,2); non-power-of-two P rejected."""
+    ident = np.arange(8, dtype=np.uint32)
+    assert oracle_mod.paper_couples(ident, 0, 4).tolist() == [[0, 1], [2, 3]]
+    assert oracle_mod.paper_couples(ident, 1, 4).tolist() == [[1, 0], [3, 2]]
+    assert oracle_mod.paper_couples(ident, 1, 8).ravel().tolist() == [1, 0, 3, 2, 5, 4, 7, 6]
+    with pytest.raises(ValueError):
+        oracle_mod.paper_couples(np.arange(6, dtype=np.uint32), 1, 4)
+    with pytest.raises(ValueError):
+        oracle_mod.paper_couples(ident, 1, 3)              # budget must be even
+
+
+def test_paper_couples_disjoint_and_full_budget_partitions(oracle_mod):
+    """no pixel in two couples; XOR by a key < P is a bijection, so the full
+    budget P covers every pixel exactly once; the key changes from pass to pass (l.305)."""
+    P = 256
+    perm = synth.make_permutation(P, 5)
+    keys = {oracle_mod.paper_key(3, t, P) for t in range(16)}
+    assert len(keys) > 8 and all(0 <= k < P for k in keys)
+    for t in range(4):
+        cp = oracle_mod.paper_couples(perm, oracle_mod.paper_key(3, t, P), P)
+        assert sorted(cp.ravel().tolist()) == list(range(P))
+        cq = oracle_mod.paper_couples(perm, oracle_mod.paper_key(3, t, P), P // 4)
+        assert len(set(cq.ravel().tolist())) == P // 4
+
+
+def _chebyshev_torus(p, q, L):
+    dx, dy = abs(p % L - q % L), abs(p // L - q // L)
+    return max(min(dx, L - dx), min(dy, L - dy))
+
+
+def test_paper_single_couple_is_sequential_swap(oracle_mod):
+    """budget 2 (one couple per pass) reduces to the sequential optimiser:
+    the recomputed energy after each pass equals E_before + dE exactly (brute force), and E
+    never rises."""
+    pb, U = _small(oracle_mod, L=16, T=10, levels=(4, 16), seed=6)
+    perm = synth.make_permutation(256, 8)
+    E0, _ = pb.energy(pb.counts(U))
+    U1, c1, st, lg = pb.paper_optimize(U, perm, budget=2, passes=40, seed=4, log=True)
+    prev = E0
+    for s in st:
+        assert s["proposed"] == 1
+        assert s["E_fixed"] == prev + s["dE_sum"]
+        assert s["E_fixed"] <= prev
+        prev = s["E_fixed"]
+    assert 0 < sum(s["accepted"] for s in st) < 40
+    assert lg.sum() == sum(s["accepted"] for s in st)
+
+
+def test_paper_far_couples_are_additive_near_couples_need_not_be(oracle_mod):
+    """couples whose members are more than R apart from every other couple's
+    members change E by exactly the sum of their snapshot dE.  Near couples interact
+    (the pass may even raise E), so only the far passes are asserted."""
+    L, R = 64, 7
+    bank = synth.make_bank(8, 21)
+    pb = _problem(oracle_mod, L, 8, [4], bank)
+    U = synth.make_tile(L, 22)
+    perm = synth.make_permutation(L * L, 23)
+    c = pb.counts(U)
+    prev, _ = pb.energy(c)
+    far = near_diff = 0
+    for t in range(24):
+        cp = oracle_mod.paper_couples(perm, oracle_mod.paper_key(9, t, L * L), 8)
+        U, c, st, _ = pb.paper_optimize(U, perm, budget=8, passes=1, first_pass=t, seed=9, c=c)
+        s = st[0]
+        pix = cp.ravel().tolist()
+        separated = all(_chebyshev_torus(pix[i], pix[j], L) > R
+                        for i in range(8) for j in range(8) if i // 2 != j // 2)
+        if separated:
+            far += 1
+            assert s["E_fixed"] == prev + s["dE_sum"]
+        elif s["E_fixed"] != prev + s["dE_sum"]:
+            near_diff += 1
+        prev = s["E_fixed"]
+    assert far >= 3
+
+
+def test_paper_snapshot_semantics_order_independent(oracle_mod):
+    """every couple is evaluated against the pass-start snapshot, so listing
+    the same couples in another order gives the identical tile (a Gauss-Seidel evaluation
+    would not); swaps permute the tile; cache coherence."""
+    pb, U = _small(oracle_mod, L=16, T=12, levels=(16,), seed=3)
+    P, budget = 256, 64
+    perm = synth.make_permutation(P, 11)
+    rev = perm.copy()
+    head = perm[:budget].reshape(-1, 2)[::-1].ravel()
+    rev[:budget] = head
+    a = pb.paper_optimize(U, perm, budget=budget, passes=1, seed=2, log=True)
+    b = pb.paper_optimize(U, rev, budget=budget, passes=1, seed=2, log=True)
+    assert np.array_equal(a[0], b[0])
+    assert np.array_equal(a[3][0], b[3][0][::-1])
+    assert a[2][0]["accepted"] > 1
+    assert sorted(map(tuple, a[0].tolist())) == sorted(map(tuple, U.tolist()))
+    assert np.array_equal(a[1], pb.counts(a[0]))
+
+
+def test_paper_mode_lowers_energy_deterministic_resumable(oracle_mod):
+    """a fixed-seed run lowers the energy; reruns are identical; a run split
+    in two (first_pass) equals the whole run."""
+    pb, U = _small(oracle_mod, L=16, T=12, levels=(16,), seed=5)
+    perm = synth.make_permutation(256, 12)
+    E0, _ = pb.energy(pb.counts(U))
+    a = pb.paper_optimize(U, perm, passes=12, seed=6)
+    b = pb.paper_optimize(U, perm, passes=12, seed=6)
+    assert np.array_equal(a[0], b[0]) and a[2] == b[2]
+    assert a[2][-1]["E_fixed"] < E0
+    h1 = pb.paper_optimize(U, perm, passes=5, seed=6)
+    h2 = pb.paper_optimize(h1[0], perm, passes=7, first_pass=5, seed=6, c=h1[1])
+    assert np.array_equal(h2[0], a[0]) and h2[2][-1] == a[2][-1]
