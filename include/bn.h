@@ -98,19 +98,23 @@ int bn_eval_counts(bn_ctx *ctx, uint8_t *out, int is_device);
  * Either pointer may be NULL.  Multi-GPU: collective over the communicator. */
 int bn_energy(bn_ctx *ctx, double *E, uint64_t E_fixed[2]);
 
-enum bn_mode { BN_REDRAW = 0, BN_SWAP = 1 };
+enum bn_mode { BN_REDRAW = 0, BN_SWAP = 1, BN_PAPER_SWAP = 2 };
 
 typedef struct {
-    uint32_t mode;       /* BN_REDRAW: re-draw u_p; BN_SWAP: swap u_p within couples        */
+    uint32_t mode;       /* BN_REDRAW: re-draw u_p; BN_SWAP: swap u_p within couples;        */
+                         /* BN_PAPER_SWAP: the paper's snapshot couples (bn_set_permutation) */
     uint32_t passes;     /* number of passes to run                                       */
     uint32_t first_pass; /* pass index t of the first pass (resume = continue counting)   */
     uint32_t K;          /* re-draw candidates per pixel; must be 1 in this version        */
     uint64_t seed;       /* Philox4x32-10 key of the optimiser                             */
+    uint32_t budget;     /* BN_PAPER_SWAP: pixels per pass (even, 2..L*L; 0 = L*L/4, the     */
+                         /* paper's N/4); ignored by the other modes         */
+    uint32_t reserved;   /* must be 0                                                       */
 } bn_opt_params;
 
 typedef struct {
-    uint32_t accepted;   /* candidates (REDRAW) or couples (SWAP) accepted in the pass     */
-    uint32_t proposed;   /* candidates (= L*L) or couples (= L*L/2) evaluated              */
+    uint32_t accepted;   /* candidates (REDRAW) or couples (SWAP, PAPER_SWAP) accepted      */
+    uint32_t proposed;   /* candidates (= L*L), couples (= L*L/2) or budget/2 evaluated    */
     double E;            /* E_fixed * 2^-64 after the pass                                */
     uint64_t E_fixed[2]; /* exact energy after the pass (uint128, low word first)          */
     uint64_t dE_sum[2];  /* exact sum of the accepted dE (int128, two's complement)        */
@@ -125,9 +129,26 @@ typedef struct {
  * kappa = 1 + Philox(seed; s, t, 0, 3)[0] mod (M - 1), M = (L/8)^2.  A candidate (couple) is
  * accepted iff its exact dE < 0 against the state left by the earlier classes.
  * stats: host [passes] or NULL.  accept_log: host [passes][64][M] bytes (1 = accepted, SWAP:
- * both members of an accepted couple) or NULL.  EINVAL on K != 1 or an unknown mode. */
+ * both members of an accepted couple) or NULL.  EINVAL on K != 1 or an unknown mode.
+ *
+ * BN_PAPER_SWAP (§3.4 l.291-307 verbatim): pass t forms the couples
+ *   c = (perm[2c] ^ key(t), perm[2c+1] ^ key(t)),  c < budget/2,
+ *   key(t) = Philox(seed; t, 0, 0, 5)[0] & (L*L - 1)   ("XOR with a different seed per pass"),
+ * from the permutation given to bn_set_permutation; every couple's swap dE is evaluated against
+ * the tile at the start of the pass and every couple with dE < 0 is swapped.  Concurrent swaps
+ * of nearby couples are not accounted for, so E may rise (l.295-297): stats[].E is the energy
+ * recomputed after the pass (one extra energy evaluation after the last pass), dE_sum the sum of
+ * the accepted couples' snapshot dE.  accept_log[pass][c] = couple c's flag (first budget/2
+ * bytes of each pass's 64*M).  ESTATE if no permutation of L*L entries is set; EINVAL on a
+ * bad budget. */
 int bn_optimize(bn_ctx *ctx, const bn_opt_params *params, bn_pass_stats *stats,
                 uint8_t *accept_log);
+
+/* Precomputed permutation of the pixel indices used by BN_PAPER_SWAP (PAPER.md l.303-304:
+ * "we precompute a permutation of pixel indices that we store in a linear array").
+ * perm: host uint32 [n], n = L*L of the tile the optimiser will run on, every index in [0, n)
+ * exactly once (EINVAL otherwise).  Copied. */
+int bn_set_permutation(bn_ctx *ctx, const uint32_t *perm, uint32_t n);
 
 /* Window distances of the current tile over THIS context's bank shard (no cross-rank sum):
  * out[(l * P + p) * H + h] = D_l(p, p + o_h) restricted to integrands [t_begin, t_end),

@@ -17,14 +17,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BN_LIB") or os.path.join(_HERE, "libbn.so")  # BN_LIB: an experiment build
 
 BN_OK, BN_EINVAL, BN_ECUDA, BN_ENCCL, BN_ENOMEM, BN_ESTATE = range(6)
-REDRAW, SWAP = 0, 1
+REDRAW, SWAP, PAPER_SWAP = 0, 1, 2
 _STATUS = {1: "EINVAL", 2: "ECUDA", 3: "ENCCL", 4: "ENOMEM", 5: "ESTATE"}
 
 #: every entry point declared in include/bn.h (checked by tests/test_abi.py)
 SYMBOLS = ("bn_create", "bn_destroy", "bn_last_error", "bn_version", "bn_set_lattice", "bn_set_bank",
            "bn_get_references", "bn_set_energy", "bn_set_tile", "bn_get_tile", "bn_eval_counts", "bn_energy",
            "bn_optimize", "bn_comm_init", "bn_comm_unique_id", "bn_launch_count", "bn_profile_enable",
-           "bn_profile_get", "bn_window_distances")
+           "bn_profile_get", "bn_window_distances", "bn_set_permutation")
 KERNELS = ("counts", "gather", "gram", "lut", "decide", "stats", "commit")
 
 
@@ -36,7 +36,8 @@ class BNError(RuntimeError):
 
 class OptParams(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_uint32), ("passes", ctypes.c_uint32), ("first_pass", ctypes.c_uint32),
-                ("K", ctypes.c_uint32), ("seed", ctypes.c_uint64)]
+                ("K", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("budget", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
 
 
 class PassStats(ctypes.Structure):
@@ -76,6 +77,7 @@ def load_library(path: str = LIB_PATH):
         "bn_launch_count": ([vp], u64),
         "bn_profile_enable": ([vp, ctypes.c_int], ctypes.c_int),
         "bn_window_distances": ([vp, vp, ctypes.c_int], ctypes.c_int),
+        "bn_set_permutation": ([vp, vp, u32], ctypes.c_int),
         "bn_profile_get": ([vp, u32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -190,10 +192,16 @@ class Sampler:
         self._check(self._lib.bn_energy(self._ctx, ctypes.byref(E), ef))
         return int(ef[0]) | (int(ef[1]) << 64), E.value
 
+    def set_permutation(self, perm):
+        """Precomputed pixel permutation of the paper-verbatim mode."""
+        perm = np.ascontiguousarray(perm, dtype=np.uint32)
+        self._check(self._lib.bn_set_permutation(self._ctx, perm.ctypes.data, len(perm)))
+
     def optimize(self, passes: int, seed: int, mode: int = REDRAW, first_pass: int = 0, K: int = 1,
-                 stats: bool = True, log: bool = False):
-        """Run passes; returns (list of per-pass dicts or None, accept log [passes,64,M] or None)."""
-        prm = OptParams(mode, passes, first_pass, K, seed)
+                 stats: bool = True, log: bool = False, budget: int = 0):
+        """Run passes; returns (list of per-pass dicts or None, accept log or None).  The log is
+        [passes, 64, M] for REDRAW/SWAP and [passes, budget/2] (couple flags) for PAPER_SWAP."""
+        prm = OptParams(mode, passes, first_pass, K, seed, budget, 0)
         st = (PassStats * max(passes, 1))() if stats else None
         M = (self.L // 8) ** 2
         lg = np.zeros((passes, 64, M), np.uint8) if log else None
@@ -207,6 +215,9 @@ class Sampler:
                 out.append(dict(accepted=s.accepted, proposed=s.proposed, E=s.E,
                                 E_fixed=int(s.E_fixed[0]) | (int(s.E_fixed[1]) << 64),
                                 dE_sum=d - (1 << 128) if d >> 127 else d))
+        if lg is not None and mode == PAPER_SWAP:
+            ncp = (budget or self.L * self.L // 4) // 2
+            lg = lg.reshape(passes, -1)[:, :ncp].copy()
         return out, lg
 
     def window_distances(self, radius: int = 7, out=None):

@@ -149,6 +149,8 @@ struct bn_ctx {
     DevBuf<CountGroup> cgrp;  // packed fp32 operands of the filtered count test
     DevBuf<uint8_t> c, cn, cn2, acc, log, cexp;
     DevBuf<int> nc, nn, nn2, derr, progress;
+    DevBuf<uint32_t> perm, part;  // BN_PAPER_SWAP: precomputed permutation, per-pass partner map
+    uint32_t perm_n = 0;
     DevBuf<int4> Dt;
     DevBuf<long long> d0, d1b;   // int64 dE terms (DT_ESC = see escape tables)
     DevBuf<longlong2> x0, x1;    // exact int128 escape tables (sparse writes)
@@ -672,6 +674,28 @@ int decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, uint8_t
     }
 }
 
+template <int R>
+int launch_paper_decide(bn_ctx* ctx, uint32_t t, uint64_t seed, uint32_t ncp, uint8_t* log) {
+    const DTabs T{ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
+    KSTART(BN_K_DECIDE);
+    k_paper_decide<R><<<(ncp + 7) / 8, 256, 0, ctx->ls>>>(ctx->perm.p, seed, t, ctx->L, ncp, T, ctx->acc.p,
+                                                          ctx->dEp.p, log);
+    LAUNCHED_K();
+    return BN_OK;
+}
+
+int paper_decide(bn_ctx* ctx, uint32_t t, uint64_t seed, uint32_t ncp, uint8_t* log) {
+    switch (ctx->R) {
+        case 1: return launch_paper_decide<1>(ctx, t, seed, ncp, log);
+        case 2: return launch_paper_decide<2>(ctx, t, seed, ncp, log);
+        case 3: return launch_paper_decide<3>(ctx, t, seed, ncp, log);
+        case 4: return launch_paper_decide<4>(ctx, t, seed, ncp, log);
+        case 5: return launch_paper_decide<5>(ctx, t, seed, ncp, log);
+        case 6: return launch_paper_decide<6>(ctx, t, seed, ncp, log);
+        default: return launch_paper_decide<7>(ctx, t, seed, ncp, log);
+    }
+}
+
 int read_err_flag(bn_ctx* ctx) {
     int h = 0;
     CUDA_TRY(cudaMemcpyAsync(&h, ctx->derr.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -752,7 +776,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->Cc.release(); ctx->cgrp.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
         ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
         ctx->d0.release(); ctx->d1b.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
-        ctx->W.release(); ctx->G.release(); ctx->iref.release();
+        ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release(); ctx->rows_done.release();
         if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
@@ -944,7 +968,8 @@ int bn_energy(bn_ctx* ctx, double* E, uint64_t E_fixed[2]) {
 int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uint8_t* accept_log) {
     if (!ctx) return BN_EINVAL;
     if (!prm) return fail(ctx, BN_EINVAL, "null params");
-    if (prm->mode > BN_SWAP) return fail(ctx, BN_EINVAL, "unknown mode %u", prm->mode);
+    if (prm->mode > BN_PAPER_SWAP) return fail(ctx, BN_EINVAL, "unknown mode %u", prm->mode);
+    if (prm->reserved) return fail(ctx, BN_EINVAL, "bn_opt_params.reserved must be 0");
     if (prm->K != 1) return fail(ctx, BN_EINVAL, "K = %u: only K = 1 is implemented", prm->K);
     DeviceGuard g(ctx->dev);
     int rc = ensure_work(ctx);
@@ -953,7 +978,16 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     const uint32_t P = ctx->P, M = (ctx->L / 8) * (ctx->L / 8), nl = ctx->nl;
     const int R = ctx->R;
     const uint32_t nE = (uint32_t)(((size_t)P * half_count_padded(R) + 255) / 256);
-    CUDA_TRY(ctx->pstats.ensure(prm->passes));
+    const bool paper = prm->mode == BN_PAPER_SWAP;
+    const uint32_t budget = paper ? (prm->budget ? prm->budget : P / 4) : 0, ncp = budget / 2;
+    if (paper) {
+        if (!ctx->perm.p || ctx->perm_n != P)
+            return fail(ctx, BN_ESTATE, "BN_PAPER_SWAP needs bn_set_permutation with L*L = %u entries", P);
+        if (budget < 2 || (budget & 1) || budget > P)
+            return fail(ctx, BN_EINVAL, "budget %u: must be even and in [2, L*L = %u]", budget, P);
+        CUDA_TRY(ctx->part.ensure(P));
+    }
+    CUDA_TRY(ctx->pstats.ensure(prm->passes + 1));
     int nsm_fin = 148;
     cudaDeviceGetAttribute(&nsm_fin, cudaDevAttrMultiProcessorCount, ctx->dev);
     const uint32_t nfin = (uint32_t)(2 * nsm_fin) < P / 16 ? (uint32_t)(2 * nsm_fin) : (P / 16);
@@ -1014,7 +1048,18 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         const uint32_t t = prm->first_pass + pi;
         ctx->ls = cs;
         CUDA_TRY(cudaMemsetAsync(ctx->acc.p, 0, P, cs));
-        if (prm->mode == BN_REDRAW) {
+        if (paper) {
+            // couples of pass t -> partner map -> gathered partner rows; dEp is only written for
+            // couple members, so it is cleared for the exact pass sums of k_finish
+            CUDA_TRY(cudaMemsetAsync(ctx->part.p, 0xFF, (size_t)P * sizeof(uint32_t), cs));
+            CUDA_TRY(cudaMemsetAsync(ctx->dEp.p, 0, (size_t)P * sizeof(i128), cs));
+            KSTART(BN_K_GATHER);
+            k_paper_pairs<<<(ncp + 255) / 256, 256, 0, cs>>>(ctx->perm.p, prm->seed, t, P, ncp, ctx->part.p);
+            LAUNCHED();
+            k_paper_gather<<<(P + 7) / 8, 256, 0, cs>>>(ctx->part.p, ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p,
+                                                        ctx->nc.p, ctx->nn.p, P, ctx->rowB, nl);
+            LAUNCHED_K();
+        } else if (prm->mode == BN_REDRAW) {
             if (overlap && pi > 0) {
                 if (!rowflags) CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evC, 0));  // prefetched during pass pi-1
             } else if ((rc = launch_counts(pi))) {
@@ -1055,13 +1100,18 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         if (pf && ctx->prefetch_at == 2 && (rc = prefetch())) return rc;
         uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
         bool done = false;
-        if (!ctx->per_class_decide && (rc = decide_pass(ctx, t, prm->seed, (int)prm->mode, log, &done))) return rc;
+        if (paper) {
+            if ((rc = paper_decide(ctx, t, prm->seed, ncp, log))) return rc;
+            done = true;
+        }
+        if (!done && !ctx->per_class_decide && (rc = decide_pass(ctx, t, prm->seed, (int)prm->mode, log, &done)))
+            return rc;
         if (!done)
             for (uint32_t s = 0; s < 64; ++s)
                 if ((rc = decide(ctx, s, t, prm->seed, (int)prm->mode, log))) return rc;
         KSTART(BN_K_COMMIT);
         k_finish<<<nfin, 256, 0, cs>>>(ctx->acc.p, P, ctx->rowB, nl, buf_U(pi), ctx->U.p, buf_c(pi), ctx->c.p,
-                                        buf_n(pi), ctx->nc.p, ctx->Epart.p, nE, ctx->dEp.p, prm->mode == BN_SWAP,
+                                        buf_n(pi), ctx->nc.p, ctx->Epart.p, nE, ctx->dEp.p, prm->mode != BN_REDRAW,
                                         ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi);
         LAUNCHED_K();
     }
@@ -1070,21 +1120,35 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->evB, 0));
     }
     ctx->ls = ctx->stream;
+    if (paper && stats) {
+        // the paper's concurrent swaps do not add up (E may rise): the energy after pass pi is the
+        // pass-start energy of pass pi + 1, and after the last pass one more energy evaluation
+        if ((rc = gram_lut(ctx, ctx->c.p, ctx->nc.p, 0))) return rc;
+        k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, nullptr, nullptr, P, 0,
+                                                  ctx->pstats.p + prm->passes);
+        LAUNCHED();
+    }
     if (stats || accept_log) {
-        std::vector<PassStatsDev> h(prm->passes);
-        CUDA_TRY(cudaMemcpyAsync(h.data(), ctx->pstats.p, prm->passes * sizeof(PassStatsDev), cudaMemcpyDeviceToHost,
+        std::vector<PassStatsDev> h(prm->passes + (paper && stats ? 1 : 0));
+        CUDA_TRY(cudaMemcpyAsync(h.data(), ctx->pstats.p, h.size() * sizeof(PassStatsDev), cudaMemcpyDeviceToHost,
                                  ctx->stream));
         if (accept_log)
             CUDA_TRY(cudaMemcpyAsync(accept_log, ctx->log.p, (size_t)prm->passes * 64 * M, cudaMemcpyDeviceToHost,
                                      ctx->stream));
         if ((rc = read_err_flag(ctx))) return rc;
+        if (paper && stats)
+            for (uint32_t pi = 0; pi < prm->passes; ++pi) {
+                h[pi].E_after[0] = h[pi + 1].E_before[0];
+                h[pi].E_after[1] = h[pi + 1].E_before[1];
+            }
         for (uint32_t pi = 0; pi < prm->passes; ++pi) {
-            if (pi && (h[pi].E_before[0] != h[pi - 1].E_after[0] || h[pi].E_before[1] != h[pi - 1].E_after[1]))
+            if (!paper && pi &&
+                (h[pi].E_before[0] != h[pi - 1].E_after[0] || h[pi].E_before[1] != h[pi - 1].E_after[1]))
                 return fail(ctx, BN_ESTATE, "internal invariant failed: E recomputed at pass %u != E + sum dE",
                             prm->first_pass + pi);
             if (stats) {
                 stats[pi].accepted = h[pi].accepted;
-                stats[pi].proposed = prm->mode == BN_SWAP ? P / 2 : P;
+                stats[pi].proposed = paper ? ncp : prm->mode == BN_SWAP ? P / 2 : P;
                 stats[pi].E_fixed[0] = h[pi].E_after[0];
                 stats[pi].E_fixed[1] = h[pi].E_after[1];
                 stats[pi].E = std::ldexp((double)h[pi].E_after[1], 0) + std::ldexp((double)h[pi].E_after[0], -64);
@@ -1093,6 +1157,23 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             }
         }
     }
+    return BN_OK;
+}
+
+int bn_set_permutation(bn_ctx* ctx, const uint32_t* perm, uint32_t n) {
+    if (!ctx) return BN_EINVAL;
+    if (!perm || n == 0) return fail(ctx, BN_EINVAL, "empty permutation");
+    std::vector<uint8_t> seen(n, 0);
+    for (uint32_t j = 0; j < n; ++j) {
+        if (perm[j] >= n || seen[perm[j]])
+            return fail(ctx, BN_EINVAL, "not a permutation of [0, %u): entry %u = %u", n, j, perm[j]);
+        seen[perm[j]] = 1;
+    }
+    DeviceGuard g(ctx->dev);
+    CUDA_TRY(ctx->perm.ensure(n));
+    CUDA_TRY(cudaMemcpyAsync(ctx->perm.p, perm, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the caller's array may go away
+    ctx->perm_n = n;
     return BN_OK;
 }
 

@@ -2716,6 +2716,83 @@ __global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc,
     }
 }
 
+// ------------------------------------------------------ paper-verbatim parallel swaps (f1)
+// PAPER.md §3.4 l.291-307: the couples of pass t are consecutive entries of a precomputed
+// permutation of the pixel indices, XOR-scrambled with a per-pass key (l.303-306):
+//   key(t) = Philox(seed; t, 0, 0, 5)[0] & (P - 1),  couple c = (perm[2c] ^ key, perm[2c+1] ^ key).
+// Every couple is evaluated against the pass-start tile (l.294-295, snapshot reading R26) and
+// every couple with dE < 0 is swapped; the couples are pixel-disjoint (l.293-294), so the commit
+// is race-free.  The window distances of the snapshot come from the same Gram as the greedy
+// path: with cn_p = c_partner(p), delta0[p][o] = sum_l q(o, D(cn_p, c_p+o)) - q(o, D(c_p, c_p+o))
+// is exactly p's share of the couple's dE.
+__device__ __forceinline__ uint32_t paper_key(uint64_t seed, uint32_t t, uint32_t P) {
+    return philox_seeded(seed, t, 0, 0, 5).x & (P - 1u);
+}
+// part[p] = partner of p for the pixels of this pass's couples (0xFFFFFFFF elsewhere, memset).
+__global__ void k_paper_pairs(const uint32_t* __restrict__ perm, uint64_t seed, uint32_t pass_t, uint32_t P,
+                              uint32_t ncp, uint32_t* __restrict__ part) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncp) return;
+    const uint32_t key = paper_key(seed, pass_t, P);
+    const uint32_t p = __ldg(perm + 2 * c) ^ key, q = __ldg(perm + 2 * c + 1) ^ key;
+    part[p] = q;
+    part[q] = p;
+}
+// cn_p = c_part(p), Un_p = U_part(p), nn_p = nc_part(p); pixels outside every couple take their own
+// rows (their dE terms are never read, but their distances must stay in the LUT range).
+// One warp per pixel, 16-byte copies.
+__global__ void k_paper_gather(const uint32_t* __restrict__ part, const uint2* __restrict__ U, uint2* __restrict__ Un,
+                               const uint8_t* __restrict__ c, uint8_t* __restrict__ cn, const int* __restrict__ nc,
+                               int* __restrict__ nn, uint32_t P, uint32_t rowB, uint32_t nl) {
+    const uint32_t p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (p >= P) return;
+    const uint32_t q0 = __ldg(part + p), q = q0 == 0xFFFFFFFFu ? p : q0;
+    const uint4* src = reinterpret_cast<const uint4*>(c + (size_t)q * rowB);
+    uint4* dst = reinterpret_cast<uint4*>(cn + (size_t)p * rowB);
+    for (uint32_t j = lane; j < rowB / 16; j += 32) dst[j] = __ldg(src + j);
+    if (lane == 0) Un[p] = U[q];
+    if (lane < nl) nn[(size_t)p * nl + lane] = nc[(size_t)q * nl + lane];
+}
+// Snapshot window sum of p's delta0 terms, skipping the partner `skip` (its distance to p does
+// not change under the swap).  Exact int128, warp-wide.
+template <int R>
+__device__ __forceinline__ i128 window_sum_snapshot(const DTabs T, uint32_t L, uint32_t p, uint32_t skip) {
+    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
+    const int lane = threadIdx.x & 31;
+    const uint32_t x = p % L, y = p / L;
+    i128 s = 0;
+    for (int w = lane; w < WN; w += 32) {
+        const int ww = w >= R * (2 * R + 1) + R ? w + 1 : w;
+        const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
+        const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
+        if (q == skip) continue;
+        const size_t idx = (size_t)p * WN + w;
+        s += get_term(__ldg(T.d0 + idx), T.x0, idx);
+    }
+    return (i128)warp_sum_u128((u128)s);
+}
+// One warp per couple: dE = 2 (sum_o' delta0[p][o] + sum_o' delta0[q][o]); accept iff dE < 0.
+// acc marks both members (k_finish commits their gathered rows), dEp holds the couple's dE once.
+// log[c] = accept flag of couple c.
+template <int R>
+__global__ void k_paper_decide(const uint32_t* __restrict__ perm, uint64_t seed, uint32_t pass_t, uint32_t L,
+                               uint32_t ncp, const DTabs T, uint8_t* __restrict__ acc, i128* __restrict__ dEp,
+                               uint8_t* __restrict__ log) {
+    const uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (c >= ncp) return;
+    const uint32_t P = L * L, key = paper_key(seed, pass_t, P);
+    const uint32_t p = __ldg(perm + 2 * c) ^ key, q = __ldg(perm + 2 * c + 1) ^ key;
+    const i128 dE = 2 * (window_sum_snapshot<R>(T, L, p, q) + window_sum_snapshot<R>(T, L, q, p));
+    if ((threadIdx.x & 31) == 0) {
+        const bool ok = dE < 0;
+        acc[p] = ok;
+        acc[q] = ok;
+        dEp[p] = ok ? dE : (i128)0;
+        dEp[q] = 0;
+        if (log) log[c] = ok;
+    }
+}
+
 // --------------------------------------------------------------------------- I_ref, readback
 // Area of {(x,y) in [0,1]^2 : a(x - px) + b(y - py) >= 0}: the unit square clipped by the
 // half-plane (walk the 4 edges, keep inside vertices and edge crossings), shoelace area. fp64.

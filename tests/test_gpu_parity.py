@@ -334,3 +334,63 @@ def test_overlapped_passes_rowflags(bn, oracle_mod, monkeypatch, rowflags):
     monkeypatch.setenv("BN_ROWFLAGS", rowflags)
     s, o, U = make(bn, oracle_mod, 32, 130, (1, 4, 16, 64))
     _check_run(s, o, U, 5, 0, seed=9)
+
+
+# ------------------------------------------------------ paper-verbatim parallel swaps (f1)
+def _check_paper_run(s, o, U, passes, seed, budget=None, first_pass=0, perm_seed=8):
+    perm = synth.make_permutation(o.L * o.L, perm_seed)
+    s.set_permutation(perm)
+    b = budget or 0
+    st, lg = s.optimize(passes, seed, mode=bn_mod().PAPER_SWAP, first_pass=first_pass, log=True, budget=b)
+    Uo, co, sto, lgo = o.paper_optimize(U, perm, budget=budget, passes=passes, first_pass=first_pass, seed=seed,
+                                        log=True)
+    assert np.array_equal(lg, lgo), "accept/reject sequence differs"
+    assert np.array_equal(s.get_tile(), Uo), "tile differs"
+    assert np.array_equal(s.eval_counts(), co), "counts differ"
+    for g, r in zip(st, sto):
+        assert g["accepted"] == r["accepted"] and g["proposed"] == r["proposed"]
+        assert g["E_fixed"] == r["E_fixed"] and g["dE_sum"] == r["dE_sum"]
+        assert abs(g["E"] - r["E_plain"]) <= 1e-6 * r["E_plain"]
+    return st
+
+
+def bn_mod():
+    from paper_2105_12620_b200 import bn as m
+
+    return m
+
+
+@pytest.mark.parametrize("L,T,levels,budget", [(16, 64, (16,), None), (16, 64, (16,), 2), (32, 130, (1, 4, 16), None),
+                                               (64, 100, (4,), 2048), (32, 40, (4,), 1024)])
+def test_paper_mode_parity(bn, oracle_mod, L, T, levels, budget):
+    """Paper-verbatim snapshot couples (§3.4): accept flags, tiles, counts and the
+    recomputed energies after every pass equal to the oracle (default N/4 budget, the
+    single-couple degenerate case, the full budget P)."""
+    s, o, U = make(bn, oracle_mod, L, T, levels)
+    _check_paper_run(s, o, U, 6, seed=17, budget=budget)
+
+
+def test_paper_mode_resume_escape_and_errors(bn, oracle_mod, monkeypatch):
+    monkeypatch.setenv("BN_DT_ESCAPE", "1")
+    s, o, U = make(bn, oracle_mod, 32, 60, (4, 16))
+    _check_paper_run(s, o, U, 3, seed=5, first_pass=4)
+    s2, _, _ = make(bn, oracle_mod, 16, 8, (4,))
+    with pytest.raises(bn.BNError) as e:                   # no permutation yet
+        s2.optimize(1, 1, mode=bn.PAPER_SWAP)
+    assert e.value.code == bn.BN_ESTATE
+    with pytest.raises(bn.BNError) as e:                   # not a permutation
+        s2.set_permutation(np.zeros(256, np.uint32))
+    assert e.value.code == bn.BN_EINVAL
+    s2.set_permutation(synth.make_permutation(256, 1))
+    with pytest.raises(bn.BNError) as e:                   # odd budget
+        s2.optimize(1, 1, mode=bn.PAPER_SWAP, budget=3)
+    assert e.value.code == bn.BN_EINVAL
+
+
+@pytest.mark.slow
+def test_c2_full_size_paper_mode(bn, oracle_mod):
+    """C2 tile (64x64, 4 spp, T=256) with the paper's own optimiser: 2 passes, N/4 budget."""
+    cfg = synth.CONFIGS["C2"]
+    U, bank = synth.problem_inputs(cfg)
+    s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
+    _check_paper_run(s, o, U, 2, seed=synth.opt_seed(cfg))
