@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C3")
+    ap.add_argument("--mode", choices=["config", "redraw", "swap", "paper"], default="config",
+                    help="optimiser mode (default: the config's); paper = PAPER.md §3.4 snapshot couples, N/4 budget")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-classes", type=int, default=12, help="colour classes in the oracle sample")
@@ -59,12 +61,24 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
+MODES = {"redraw": 0, "swap": 1, "paper": 2}
+
+
+def evals_per_pass(cfg):
+    """Pixel-update evaluations of one pass: every pixel once (REDRAW; SWAP couples count 2);
+    the paper mode swaps a budget of P/4 pixels per pass."""
+    P = cfg.L * cfg.L
+    return P // 4 if cfg.mode == 2 else P
+
+
 def workload(cfg):
+    mode = {0: "redraw", 1: "swap", 2: "paper_swap"}[cfg.mode]
+    step = (f"one optimisation pass = {evals_per_pass(cfg)} pixel-update evals "
+            + ("(P/4-pixel budget of snapshot couples, PAPER.md §3.4)" if cfg.mode == 2 else "(64 colour classes)"))
     return {
-        "workload": f"{cfg.name}: {cfg.note}",
+        "workload": f"{cfg.name}: {cfg.note}" + (" [paper-verbatim parallel swaps]" if cfg.mode == 2 else ""),
         "tile": cfg.L, "T": cfg.T, "spp_levels": list(cfg.levels),
-        "mode": "redraw" if cfg.mode == 0 else "swap", "radius": 7, "sigma_i": 2.1, "sigma_s": 1.0,
-        "step": f"one optimisation pass = {cfg.L * cfg.L} pixel-update evals (64 colour classes)",
+        "mode": mode, "radius": 7, "sigma_i": 2.1, "sigma_s": 1.0, "step": step,
     }
 
 
@@ -141,8 +155,13 @@ def algorithmic(kernel, cfg):
         # dE terms per (p, h) (p side and q side; the int128 escapes are rare)
         return float(P * H * (16 * nl + 32)), "bytes", "hbm"
     if kernel == "decide":
+        if cfg.mode == 2:  # paper mode: the snapshot dE term (int64) of each couple member's window
+            return float(evals_per_pass(cfg) * ((2 * R + 1) ** 2 - 1) * 8), "bytes", "hbm"
         # bytes: both int64 dE terms per (candidate, window offset), all 64 classes in one launch
         return float(P * ((2 * R + 1) ** 2 - 1) * 16), "bytes", "hbm"
+    if kernel == "gather":
+        # bytes: read and write every pixel's count rows (partner rows -> candidate buffer)
+        return float(2 * P * nl * (-(-T // 256) * 256)), "bytes", "hbm"
     return None, None, None
 
 
@@ -215,8 +234,13 @@ def oracle_sample(cfg, pair, classes, passes_done=0, state=None):
     pb, U, c = state
     M = (cfg.L // 8) ** 2
     t0 = time.perf_counter()
-    U, c, st, _ = pb.optimize(U, c, mode=cfg.mode, passes=1, first_pass=passes_done,
-                              seed=synth.opt_seed(cfg, pair), max_steps=classes, energy_each_pass=False)
+    if cfg.mode == 2:   # `classes` x M pixels of snapshot couples
+        U, c, st, _ = pb.paper_optimize(U, synth.make_permutation(cfg.L * cfg.L, synth.opt_seed(cfg, pair)),
+                                        budget=classes * M, passes=1, first_pass=passes_done,
+                                        seed=synth.opt_seed(cfg, pair), c=c, energy_each_pass=False)
+    else:
+        U, c, st, _ = pb.optimize(U, c, mode=cfg.mode, passes=1, first_pass=passes_done,
+                                  seed=synth.opt_seed(cfg, pair), max_steps=classes, energy_each_pass=False)
     dt = time.perf_counter() - t0
     state[1], state[2] = U, c
     return classes * M, dt, state
@@ -224,6 +248,9 @@ def oracle_sample(cfg, pair, classes, passes_done=0, state=None):
 
 def cpu_sample_desc(cfg, classes):
     M = (cfg.L // 8) ** 2
+    if cfg.mode == 2:
+        return (f"oracle (single-threaded C, -O2) on {cfg.name}, paper mode: one pass with a budget of "
+                f"{classes * M} pixels = {classes * M} pixel-update evals (distances recomputed from counts)")
     return (f"oracle (single-threaded C, -O2) on {cfg.name}: first {classes} of 64 colour classes of pass 0 "
             f"= {classes * M} pixel-update evals (full distances recomputed from counts per candidate)")
 
@@ -304,6 +331,8 @@ def run_ours(args, cfg):
             s.set_bank(a, b, px, py)
         s.set_energy(2.1, 1.0, 7)
         s.set_tile(cfg.L, U)
+        if cfg.mode == 2:
+            s.set_permutation(synth.make_permutation(P, synth.opt_seed(cfg, j)))
         samplers.append(s)
         streams.append(st_j)
         seeds.append(synth.opt_seed(cfg, j))
@@ -338,7 +367,8 @@ def run_ours(args, cfg):
     ms = e0.elapsed_time(e1)
     launches = sum(x.launch_count() for x in samplers) - l0
     ms_max = max_over_ranks(ms)
-    units_per_step = P * (1 if banksharded else len(pairs) * world) if cfg.pairs == 1 else P * cfg.pairs
+    EP = evals_per_pass(cfg)
+    units_per_step = EP * (1 if banksharded else len(pairs) * world) if cfg.pairs == 1 else EP * cfg.pairs
     value = units_per_step * args.steps / (ms_max / 1e3)
     clocks = clk.summary()
 
@@ -370,7 +400,7 @@ def run_ours(args, cfg):
     f1.record(streams[0])
     barrier()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
-    e2e_units = P * (1 if banksharded else world)
+    e2e_units = EP * (1 if banksharded else world)
     e2e = {"value": e2e_units * args.e2e_steps / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": P * 8 + 24, "d2h_bytes_per_step": P * 8 + 48,
            "path": "bn_set_tile(host) + bn_optimize(1 pass, stats) + bn_get_tile(host) per step"}
@@ -413,6 +443,10 @@ def main():
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     cfg = synth.CONFIGS[args.config]
+    if args.mode != "config":
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, mode=MODES[args.mode])
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -260,7 +260,8 @@ class OracleProblem:
         return U, c, stats, acc
 
     def paper_optimize(self, U: np.ndarray, perm, *, budget: int | None = None, passes: int = 1,
-                       first_pass: int = 0, seed: int = 3, c: np.ndarray | None = None, log: bool = False):
+                       first_pass: int = 0, seed: int = 3, c: np.ndarray | None = None, log: bool = False,
+                       energy_each_pass: bool = True):
         """Paper-verbatim parallel swaps against the pass-start snapshot (§3.4 l.291-307).
         Returns (U, c, stats list, accept log [passes, budget/2] or None)."""
         U = np.array(U, dtype=np.uint32).reshape(-1, 2).copy()
@@ -270,7 +271,8 @@ class OracleProblem:
         st = (Stats * max(passes, 1))()
         acc = np.zeros((passes, max(budget // 2, 1)), dtype=np.uint8) if log else None
         rc = lib().orc_paper_optimize(self.ref(), U.ctypes.data, c.ctypes.data, perm.ctypes.data, budget, passes,
-                                      first_pass, seed, st, acc.ctypes.data if acc is not None else None)
+                                      first_pass, seed, st if energy_each_pass else None,
+                                      acc.ctypes.data if acc is not None else None)
         if rc != 0:
             raise ValueError("oracle rejected the paper-mode arguments")
         stats = [dict(accepted=s.accepted, proposed=s.proposed, E_plain=s.E_plain,
