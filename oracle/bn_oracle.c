@@ -119,6 +119,8 @@ typedef struct {
     double sigma_i;         /* spatial Gaussian, Eq.1: 2.1            */
     double sigma_s;         /* error-space scale (north star; reading R3)             */
     int32_t radius;         /* window radius R (reading R4)                           */
+    int32_t form;           /* 0: north-star GF energy; 1: Eq. 1 as written; 2: Eq. 1  */
+                            /* maximised (reading R1)                      */
 } orc_problem;
 
 /* Count c = #{k < N : f_i(s^k_p) = 1} (I_p,i = c / N).  Plain loop. */
@@ -192,7 +194,11 @@ static double w_of(const orc_problem *pb, int ox, int oy) {
     return exp(-(double)(ox * ox + oy * oy) / (pb->sigma_i * pb->sigma_i));
 }
 static double g_of(const orc_problem *pb, uint64_t D, uint32_t N) {
-    return exp(-(sqrt((double)D) / (double)N) / (pb->sigma_s * pb->sigma_s));
+    if (pb->form == 0) return exp(-(sqrt((double)D) / (double)N) / (pb->sigma_s * pb->sigma_s));
+    /* Eq. 1: ||I_p - I_q||^2 = D / N^2 with I = c / N; divided by T so that the
+     * fixed-point term w * g stays below 1.  Form 2 minimises 1 - that, i.e. maximises Eq. 1. */
+    double sq = (double)D / (double)((uint64_t)N * N * pb->T);
+    return pb->form == 1 ? sq : 1.0 - sq;
 }
 uint64_t orc_q(const orc_problem *pb, int ox, int oy, uint64_t D, uint32_t N) {
     double v = w_of(pb, ox, oy) * g_of(pb, D, N);

@@ -47,6 +47,7 @@ class Problem(ctypes.Structure):
         ("sigma_i", ctypes.c_double),
         ("sigma_s", ctypes.c_double),
         ("radius", ctypes.c_int32),
+        ("form", ctypes.c_int32),
     ]
 
 
@@ -187,6 +188,7 @@ class OracleProblem:
     sigma_i: float = 2.1
     sigma_s: float = 1.0
     radius: int = 7
+    form: int = 0          # 0 GF (north star), 1 Eq. 1 minimised, 2 Eq. 1 maximised
 
     def __post_init__(self):
         self.a = np.ascontiguousarray(self.a, dtype=np.int32)
@@ -196,7 +198,7 @@ class OracleProblem:
         lv = (ctypes.c_uint32 * 8)(*(list(self.levels) + [0] * (8 - len(self.levels))))
         self._s = Problem(self.L, self.T, len(self.levels), lv, self.d1, self.d2,
                           self.a.ctypes.data, self.b.ctypes.data, self.px.ctypes.data, self.py.ctypes.data,
-                          self.sigma_i, self.sigma_s, self.radius)
+                          self.sigma_i, self.sigma_s, self.radius, self.form)
 
     @property
     def P(self) -> int:

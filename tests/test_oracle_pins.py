@@ -433,3 +433,68 @@ def test_paper_mode_lowers_energy_deterministic_resumable(oracle_mod):
     h1 = pb.paper_optimize(U, perm, passes=5, seed=6)
     h2 = pb.paper_optimize(h1[0], perm, passes=7, first_pass=5, seed=6, c=h1[1])
     assert np.array_equal(h2[0], a[0]) and h2[2][-1] == a[2][-1]
+
+
+# ------------------------------------------------------- Eq. 1 energy forms --
+@pytest.mark.parametrize("form", [1, 2])
+def test_eq1_constant_tile_and_single_defect(oracle_mod, form):
+    """Eq. 1 with I = c/N: a constant tile has every ||I_p - I_q|| = 0, so
+    the minimised form is 0 and the maximised form (1 - ||.||^2/T) is levels * P * S; one
+    defect pixel adds (or removes) 2 S ||I_d - I_0||^2 / T (both ordered pairs)."""
+    T = 20
+    bank = synth.make_bank(T, 8)
+    pb = _problem(oracle_mod, 16, T, [4, 16], bank, form=form)
+    U = np.tile(synth.make_tile(1, 4), (256, 1))
+    S = _sum_w()
+    Ef, Ep = pb.energy(pb.counts(U))
+    want = 0.0 if form == 1 else 2 * 256 * S
+    assert abs(Ep - want) <= 1e-9 * max(want, 1.0) and abs(Ef / 2**64 - want) <= 1e-9 * max(want, 1.0)
+    U[37] = synth.make_tile(1, 5)[0]
+    c = pb.counts(U)
+    sq = [float((((c[li, 37].astype(int) - c[li, 0].astype(int)) / N) ** 2).sum()) for li, N in enumerate((4, 16))]
+    assert sq[1] > 0
+    defect = sum(2 * S * v / T for v in sq)
+    want = defect if form == 1 else 2 * 256 * S - defect
+    Ef, Ep = pb.energy(c)
+    assert abs(Ep - want) < 1e-12 * 2 * 256 * S and abs(Ef / 2**64 - want) < 1e-9 * 2 * 256 * S
+
+
+@pytest.mark.parametrize("form", [1, 2])
+def test_eq1_delta_equals_brute_force(oracle_mod, form):
+    T = 10
+    pb = _problem(oracle_mod, 16, T, (4, 16), synth.make_bank(T, 13), form=form)
+    U = synth.make_tile(16, 14)
+    c = pb.counts(U)
+    E0, _ = pb.energy(c)
+    rng = np.random.default_rng(2)
+    for _ in range(3):
+        p = int(rng.integers(0, 256))
+        un = rng.integers(0, TWO32, 2, dtype=np.uint64).astype(np.uint32)
+        U2 = U.copy()
+        U2[p] = un
+        assert pb.delta_replace(c, p, int(un[0]), int(un[1])) == pb.energy(pb.counts(U2))[0] - E0
+
+
+def test_eq1_minimised_is_red_maximised_is_blue(oracle_mod):
+    """SURVEY §0 / reading R1: greedy minimisation of Eq. 1 as written groups similar error vectors
+    (low-frequency error power rises: red noise); maximising it spreads them (power drops)."""
+    L, T = 32, 16
+    bank = synth.make_bank(T, 4)
+    U = synth.make_tile(L, 104)
+
+    def low_power(c):
+        e = c[0].reshape(L, L, -1).astype(float)
+        e -= e.mean((0, 1))
+        F = np.abs(np.fft.fft2(e, axes=(0, 1))) ** 2
+        f = np.fft.fftfreq(L)
+        r = np.sqrt(f[:, None] ** 2 + f[None, :] ** 2)
+        return F[(r > 0) & (r < 0.12)].mean() / F[r > 0].mean()
+
+    base = None
+    out = {}
+    for form in (1, 2):
+        pb = _problem(oracle_mod, L, T, (16,), bank, form=form)
+        base = low_power(pb.counts(U))
+        U1, c1, _, _ = pb.optimize(U, passes=6, seed=1, energy_each_pass=False)
+        out[form] = low_power(c1)
+    assert out[1] > 1.5 * base and out[2] < 0.8 * base
