@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--mode", choices=["config", "redraw", "swap", "paper"], default="config",
                     help="optimiser mode (default: the config's); paper = PAPER.md §3.4 snapshot couples, N/4 budget")
+    ap.add_argument("--energy", choices=["gf", "eq1", "eq1max"], default="gf",
+                    help="energy form: north-star GF (default), Eq. 1 as written, Eq. 1 maximised")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-classes", type=int, default=12, help="colour classes in the oracle sample")
@@ -330,6 +332,7 @@ def run_ours(args, cfg):
         else:
             s.set_bank(a, b, px, py)
         s.set_energy(2.1, 1.0, 7)
+        s.set_energy_form({"gf": 0, "eq1": 1, "eq1max": 2}[args.energy])
         s.set_tile(cfg.L, U)
         if cfg.mode == 2:
             s.set_permutation(synth.make_permutation(P, synth.opt_seed(cfg, j)))
@@ -415,6 +418,8 @@ def run_ours(args, cfg):
 
     if rank == 0:
         cfgj = config_json(cfg, world)
+        if args.energy != "gf":
+            cfgj["energy"] = {"eq1": "Eq. 1 as written (minimised)", "eq1max": "Eq. 1 maximised"}[args.energy]
         if cfg.pairs > 1:
             cfgj["per_rank"] = f"{len(pairs)} of the {cfg.pairs} independent dimension-pair tiles, one stream each"
             cfgj["global_tiles"] = cfg.pairs

@@ -83,6 +83,15 @@ int bn_get_references(bn_ctx *ctx, double *iref);
  * Defaults 2.1, 1.0, 7.  radius in [1, 7] (the stride-8 colouring needs R < 8); sigmas > 0. */
 int bn_set_energy(bn_ctx *ctx, double sigma_i, double sigma_s, int32_t radius);
 
+/* Energy form (reading R1): which g(D) the energy above uses.
+ *   BN_E_GF      g = exp(-(sqrt(D)/N_l) / sigma_s^2)   north-star Georgiev-Fajardo form (default)
+ *   BN_E_EQ1     g = D / (N_l^2 T) = ||I_p - I_q||^2 / T   Eq. 1 literally,
+ *                minimised ("reduce the following loss"); the 1/T keeps w*g < 1 for the fixed point
+ *   BN_E_EQ1_MAX g = 1 - D / (N_l^2 T): minimising it maximises Eq. 1 (the blue-noise direction)
+ * sigma_s is ignored by the Eq. 1 forms.  EINVAL on an unknown form. */
+enum bn_energy_form { BN_E_GF = 0, BN_E_EQ1 = 1, BN_E_EQ1_MAX = 2 };
+int bn_set_energy_form(bn_ctx *ctx, uint32_t form);
+
 /* Load the tile U (L*L pixels, L a power of two >= 16, L > 2R) and build its counts.
  * u_xy: [2 L L] uint32, host (is_device = 0) or device.  Requires lattice and bank. */
 int bn_set_tile(bn_ctx *ctx, uint32_t L, const uint32_t *u_xy, int is_device);

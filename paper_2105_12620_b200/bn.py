@@ -18,13 +18,15 @@ LIB_PATH = os.environ.get("BN_LIB") or os.path.join(_HERE, "libbn.so")  # BN_LIB
 
 BN_OK, BN_EINVAL, BN_ECUDA, BN_ENCCL, BN_ENOMEM, BN_ESTATE = range(6)
 REDRAW, SWAP, PAPER_SWAP = 0, 1, 2
+E_GF, E_EQ1, E_EQ1_MAX = 0, 1, 2
 _STATUS = {1: "EINVAL", 2: "ECUDA", 3: "ENCCL", 4: "ENOMEM", 5: "ESTATE"}
 
 #: every entry point declared in include/bn.h (checked by tests/test_abi.py)
 SYMBOLS = ("bn_create", "bn_destroy", "bn_last_error", "bn_version", "bn_set_lattice", "bn_set_bank",
            "bn_get_references", "bn_set_energy", "bn_set_tile", "bn_get_tile", "bn_eval_counts", "bn_energy",
            "bn_optimize", "bn_comm_init", "bn_comm_unique_id", "bn_launch_count", "bn_profile_enable",
-           "bn_profile_get", "bn_window_distances", "bn_set_permutation")
+           "bn_profile_get", "bn_window_distances", "bn_set_permutation",
+           "bn_set_energy_form")
 KERNELS = ("counts", "gather", "gram", "lut", "decide", "stats", "commit")
 
 
@@ -78,6 +80,7 @@ def load_library(path: str = LIB_PATH):
         "bn_profile_enable": ([vp, ctypes.c_int], ctypes.c_int),
         "bn_window_distances": ([vp, vp, ctypes.c_int], ctypes.c_int),
         "bn_set_permutation": ([vp, vp, u32], ctypes.c_int),
+        "bn_set_energy_form": ([vp, u32], ctypes.c_int),
         "bn_profile_get": ([vp, u32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -165,6 +168,10 @@ class Sampler:
 
     def set_energy(self, sigma_i: float = 2.1, sigma_s: float = 1.0, radius: int = 7):
         self._check(self._lib.bn_set_energy(self._ctx, sigma_i, sigma_s, radius))
+
+    def set_energy_form(self, form: int = E_GF):
+        """Energy g(D): E_GF (default), E_EQ1 (Eq. 1 as written, minimised), E_EQ1_MAX (Eq. 1 maximised)."""
+        self._check(self._lib.bn_set_energy_form(self._ctx, form))
 
     def set_tile(self, L: int, u_xy):
         ptr, dev = _ptr(u_xy)

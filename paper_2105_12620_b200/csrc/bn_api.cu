@@ -137,6 +137,7 @@ struct bn_ctx {
     std::vector<uint32_t> px, py;
     // energy
     double sigma_i = 2.1, sigma_s = 1.0;
+    uint32_t form = BN_E_GF;  // bn_set_energy_form
     int R = 7;
     bool lut_dirty = true;
     // tile
@@ -290,8 +291,9 @@ bool pow2(uint32_t v) { return v && !(v & (v - 1)); }
 int half_count(int R) { return 2 * R * R + 2 * R; }
 int win_count(int R) { return (2 * R + 1) * (2 * R + 1) - 1; }
 
-// Energy LUTs.  W[w] = exp(-|o|^2 / sigma_i^2) in full-window order; G_l[D] =
-// exp(-(sqrt(D)/N_l) / sigma_s^2) for 0 <= D <= T N_l^2.  Host libm, -ffp-contract=off.
+// Energy LUTs.  W[w] = exp(-|o|^2 / sigma_i^2) in full-window order; G_l[D] for 0 <= D <= T N_l^2:
+// exp(-(sqrt(D)/N_l) / sigma_s^2) (BN_E_GF), D / (N_l^2 T) (BN_E_EQ1) or 1 - D / (N_l^2 T)
+// (BN_E_EQ1_MAX).  Host libm, -ffp-contract=off.
 int build_lut(bn_ctx* ctx) {
     const int R = ctx->R;
     std::vector<double> W(win_count(R));
@@ -313,8 +315,17 @@ int build_lut(bn_ctx* ctx) {
     const double s2 = ctx->sigma_s * ctx->sigma_s;
     for (uint32_t l = 0; l < ctx->nl; ++l) {
         const double N = (double)ctx->levels[l];
+        // Eq. 1 forms: ||I_p - I_q||^2 = D / N^2, normalised by 1/T so that w * g < 1 (fixed point)
+        const double den = (double)((uint64_t)ctx->levels[l] * ctx->levels[l] * ctx->T);
         double* g = G.data() + ctx->Goff[l];
-        for (int D = 0; D <= ctx->Dmax[l]; ++D) g[D] = std::exp(-(std::sqrt((double)D) / N) / s2);
+        for (int D = 0; D <= ctx->Dmax[l]; ++D) {
+            if (ctx->form == BN_E_GF)
+                g[D] = std::exp(-(std::sqrt((double)D) / N) / s2);
+            else if (ctx->form == BN_E_EQ1)
+                g[D] = (double)D / den;
+            else
+                g[D] = 1.0 - (double)D / den;
+        }
     }
     CUDA_TRY(ctx->W.ensure(W.size()));
     CUDA_TRY(ctx->G.ensure(total));
@@ -876,6 +887,14 @@ int bn_get_references(bn_ctx* ctx, double* iref) {
     LAUNCHED();
     CUDA_TRY(cudaMemcpyAsync(iref, ctx->iref.p, ctx->Ts * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return BN_OK;
+}
+
+int bn_set_energy_form(bn_ctx* ctx, uint32_t form) {
+    if (!ctx) return BN_EINVAL;
+    if (form > BN_E_EQ1_MAX) return fail(ctx, BN_EINVAL, "unknown energy form %u", form);
+    ctx->form = form;
+    ctx->lut_dirty = true;
     return BN_OK;
 }
 

@@ -26,16 +26,18 @@ def bn():
     return bnmod
 
 
-def make(bn, oracle_mod, L, T, levels, tile_seed=1, bank_seed=2, sigma_s=1.0, radius=7, bank=None, U=None):
+def make(bn, oracle_mod, L, T, levels, tile_seed=1, bank_seed=2, sigma_s=1.0, radius=7, bank=None, U=None, form=0):
     a, b, px, py = bank if bank is not None else synth.make_bank(T, bank_seed)
     U = synth.make_tile(L, tile_seed) if U is None else U
     s = bn.Sampler(0)
     s.set_lattice(synth.D1, synth.D2, levels)
     s.set_bank(a, b, px, py)
     s.set_energy(2.1, sigma_s, radius)
+    if form:
+        s.set_energy_form(form)
     s.set_tile(L, U)
     o = oracle_mod.OracleProblem(L, len(a), tuple(levels), synth.D1, synth.D2, a, b, px, py,
-                                 sigma_i=2.1, sigma_s=sigma_s, radius=radius)
+                                 sigma_i=2.1, sigma_s=sigma_s, radius=radius, form=form)
     return s, o, U
 
 
@@ -394,3 +396,18 @@ def test_c2_full_size_paper_mode(bn, oracle_mod):
     U, bank = synth.problem_inputs(cfg)
     s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
     _check_paper_run(s, o, U, 2, seed=synth.opt_seed(cfg))
+
+
+# ------------------------------------------------------------ Eq. 1 energy forms (f4)
+@pytest.mark.parametrize("form", [1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_eq1_forms_parity(bn, oracle_mod, form, mode):
+    """Eq. 1 as written (minimised) and maximised: energies and passes bit-exact in every mode."""
+    s, o, U = make(bn, oracle_mod, 32, 100, (4, 16), form=form)
+    assert s.energy()[0] == o.energy(o.counts(U))[0]
+    if mode == 2:
+        _check_paper_run(s, o, U, 3, seed=19)
+    else:
+        _check_run(s, o, U, 3, mode, seed=19)
+    with pytest.raises(bn.BNError):
+        s.set_energy_form(3)
