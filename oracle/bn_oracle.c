@@ -559,3 +559,115 @@ int orc_paper_optimize(const orc_problem *pb, uint32_t *U, uint8_t *c, const uin
     free(pix); free(dEs); free(rp); free(rq);
     return 0;
 }
+
+/* ---------------------------------------------------------------------------------------
+ * Evaluation criterion (§3.3 l.270-284, teaser (c) l.154 "||(I_N (*) k_sigma) - I_ref||";
+ * SURVEY §8 row f2; readings R29-R31 in DESIGN.md).  Plain definitions, O(P * taps) and O(P^2):
+ *   e_i(p)    = c[l][p][i] / N_l - I_ref,i                     error image of integrand i
+ *   k_sigma   = exp(-(dx^2 + dy^2) / (2 sigma^2)) on [-r, r]^2, r = ceil(4 sigma), / its sum
+ *   rmse(s)   = 1/T sum_i sqrt( 1/P sum_p ( sum_d k_s(d) c[l][p+d][i]/N_l - I_ref,i )^2 )
+ *               (toroidal: the tile repeats over the screen, so taps wrap
+ *               mod L however large the kernel)
+ *   S(f)      = 1/T sum_i | sum_p (e_i(p) - mean_i) exp(-2 pi i f.p / L) |^2   (DC = 0)
+ *   profile_j = mean of S over the frequencies f (signed, |fx|,|fy| <= L/2) with
+ *               floor(|f|) = j + 1, j = 0 .. L/2 - 1 (DC excluded)
+ * --------------------------------------------------------------------------------------- */
+static double gauss_unnormalised(double sigma, int r, double *k) {
+    double Z = 0.0;
+    for (int dy = -r; dy <= r; ++dy)
+        for (int dx = -r; dx <= r; ++dx) {
+            double v = exp(-(double)(dx * dx + dy * dy) / (2.0 * sigma * sigma));
+            k[(dy + r) * (2 * r + 1) + (dx + r)] = v;
+            Z += v;
+        }
+    return Z;
+}
+
+/* Normalised Gaussian kernel of radius ceil(4 sigma): k[(dy+r)(2r+1) + dx+r], returns r (or -1). */
+int orc_gauss_kernel(double sigma, double *k, int kmax) {
+    if (!(sigma > 0)) return -1;
+    int r = (int)ceil(4.0 * sigma);
+    if ((2 * r + 1) * (2 * r + 1) > kmax) return -1;
+    double Z = gauss_unnormalised(sigma, r, k);
+    for (int j = 0; j < (2 * r + 1) * (2 * r + 1); ++j) k[j] /= Z;
+    return r;
+}
+
+int orc_denoised_rmse(const orc_problem *pb, const uint8_t *c, uint32_t l, const double *sigmas,
+                      uint32_t n_sigmas, double *rmse) {
+    const uint32_t L = pb->L, P = L * L, T = pb->T, N = pb->levels[l];
+    if (l >= pb->n_levels) return -1;
+    const uint8_t *cl = c + (size_t)l * P * T;
+    for (uint32_t s = 0; s < n_sigmas; ++s) {
+        int r = (int)ceil(4.0 * sigmas[s]);
+        int kw = 2 * r + 1;
+        double *k = malloc(sizeof(double) * kw * kw);
+        if (orc_gauss_kernel(sigmas[s], k, kw * kw) < 0) { free(k); return -1; }
+        double acc = 0.0;
+        for (uint32_t i = 0; i < T; ++i) {
+            const double ref = orc_iref(pb->a[i], pb->b[i], pb->px[i], pb->py[i]);
+            double ss = 0.0;
+            for (uint32_t y = 0; y < L; ++y)
+                for (uint32_t x = 0; x < L; ++x) {
+                    double v = 0.0;   /* (I_N (*) k_sigma)(p) */
+                    for (int dy = -r; dy <= r; ++dy)
+                        for (int dx = -r; dx <= r; ++dx) {
+                            uint32_t q = wrap((int64_t)y + dy, L) * L + wrap((int64_t)x + dx, L);
+                            v += k[(dy + r) * kw + (dx + r)] * ((double)cl[(size_t)q * T + i] / (double)N);
+                        }
+                    ss += (v - ref) * (v - ref);
+                }
+            acc += sqrt(ss / (double)P);
+        }
+        rmse[s] = acc / (double)T;
+        free(k);
+    }
+    return 0;
+}
+
+int orc_error_spectrum(const orc_problem *pb, const uint8_t *c, uint32_t l, double *S /* [ky][kx] */,
+                       double *profile /* [L/2] */) {
+    const uint32_t L = pb->L, P = L * L, T = pb->T, N = pb->levels[l];
+    if (l >= pb->n_levels) return -1;
+    const uint8_t *cl = c + (size_t)l * P * T;
+    const double two_pi = 6.283185307179586476925286766559;
+    double *e = malloc(sizeof(double) * P);
+    memset(S, 0, sizeof(double) * P);
+    for (uint32_t i = 0; i < T; ++i) {
+        const double ref = orc_iref(pb->a[i], pb->b[i], pb->px[i], pb->py[i]);
+        double mean = 0.0;
+        for (uint32_t p = 0; p < P; ++p) {
+            e[p] = (double)cl[(size_t)p * T + i] / (double)N - ref;
+            mean += e[p];
+        }
+        mean /= (double)P;
+        for (uint32_t ky = 0; ky < L; ++ky)
+            for (uint32_t kx = 0; kx < L; ++kx) {
+                double re = 0.0, im = 0.0;
+                for (uint32_t y = 0; y < L; ++y)
+                    for (uint32_t x = 0; x < L; ++x) {
+                        double ph = -two_pi * (double)((kx * x + ky * y) % L) / (double)L;
+                        re += (e[y * L + x] - mean) * cos(ph);
+                        im += (e[y * L + x] - mean) * sin(ph);
+                    }
+                S[ky * L + kx] += (re * re + im * im) / (double)T;
+            }
+    }
+    free(e);
+    if (profile) {
+        double *sum = calloc(L / 2, sizeof(double));
+        uint32_t *cnt = calloc(L / 2, sizeof(uint32_t));
+        for (uint32_t ky = 0; ky < L; ++ky)
+            for (uint32_t kx = 0; kx < L; ++kx) {
+                int fx = kx <= L / 2 ? (int)kx : (int)kx - (int)L;
+                int fy = ky <= L / 2 ? (int)ky : (int)ky - (int)L;
+                int j = (int)floor(sqrt((double)(fx * fx + fy * fy)));
+                if (j < 1 || j > (int)L / 2) continue;
+                sum[j - 1] += S[ky * L + kx];
+                cnt[j - 1] += 1;
+            }
+        for (uint32_t j = 0; j < L / 2; ++j) profile[j] = cnt[j] ? sum[j] / cnt[j] : 0.0;
+        free(sum); free(cnt);
+    }
+    return 0;
+}

@@ -103,6 +103,14 @@ def lib():
         _lib.orc_active_pixel.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                           ctypes.c_uint32]
         _lib.orc_active_pixel.restype = ctypes.c_uint32
+        _lib.orc_gauss_kernel.argtypes = [ctypes.c_double, ctypes.c_void_p, ctypes.c_int]
+        _lib.orc_gauss_kernel.restype = ctypes.c_int
+        _lib.orc_denoised_rmse.argtypes = [P(Problem), ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
+                                           ctypes.c_uint32, ctypes.c_void_p]
+        _lib.orc_denoised_rmse.restype = ctypes.c_int
+        _lib.orc_error_spectrum.argtypes = [P(Problem), ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
+                                            ctypes.c_void_p]
+        _lib.orc_error_spectrum.restype = ctypes.c_int
         _lib.orc_paper_key.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32]
         _lib.orc_paper_key.restype = ctypes.c_uint32
         _lib.orc_paper_couples.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
@@ -165,6 +173,15 @@ def paper_couples(perm, key: int, budget: int) -> np.ndarray:
     if lib().orc_paper_couples(perm.ctypes.data, len(perm), key, budget, out.ctypes.data) != 0:
         raise ValueError("oracle rejected the couple arguments")
     return out.reshape(-1, 2)
+
+
+def gauss_kernel(sigma: float) -> np.ndarray:
+    """Normalised Gaussian kernel, radius ceil(4 sigma) (SPEC gaussian_kernel)."""
+    r = int(np.ceil(4 * sigma))
+    k = np.zeros((2 * r + 1) ** 2, np.float64)
+    if lib().orc_gauss_kernel(sigma, k.ctypes.data, k.size) < 0:
+        raise ValueError("bad sigma")
+    return k.reshape(2 * r + 1, 2 * r + 1)
 
 
 def iref(a: int, b: int, px: int, py: int) -> float:
@@ -240,6 +257,25 @@ class OracleProblem:
         d = (ctypes.c_uint64 * 2)()
         lib().orc_delta_replace(self.ref(), c.ctypes.data, p, ux, uy, d)
         return _i128(d[0], d[1])
+
+    # -- evaluation criterion (§3.3) ------------------------------------------------
+    def denoised_rmse(self, c: np.ndarray, level: int, sigmas) -> np.ndarray:
+        """RMSE of the Gaussian-denoised test-integrand tiles, averaged over integrands (teaser (c))."""
+        c = np.ascontiguousarray(c, dtype=np.uint8)
+        sg = np.ascontiguousarray(sigmas, dtype=np.float64)
+        out = np.zeros(len(sg), np.float64)
+        if lib().orc_denoised_rmse(self.ref(), c.ctypes.data, level, sg.ctypes.data, len(sg), out.ctypes.data):
+            raise ValueError("bad arguments")
+        return out
+
+    def error_spectrum(self, c: np.ndarray, level: int):
+        """(S [L, L] mean power spectrum of the mean-subtracted error, radial profile [L/2])."""
+        c = np.ascontiguousarray(c, dtype=np.uint8)
+        S = np.zeros((self.L, self.L), np.float64)
+        prof = np.zeros(self.L // 2, np.float64)
+        if lib().orc_error_spectrum(self.ref(), c.ctypes.data, level, S.ctypes.data, prof.ctypes.data):
+            raise ValueError("bad arguments")
+        return S, prof
 
     # -- optimisation ----------------------------------------------------------------------
     def optimize(self, U: np.ndarray, c: np.ndarray | None = None, *, mode: int = 0, passes: int = 1,
