@@ -153,6 +153,20 @@ typedef struct {
 int bn_optimize(bn_ctx *ctx, const bn_opt_params *params, bn_pass_stats *stats,
                 uint8_t *accept_log);
 
+/* Evaluation criterion (§3.3 l.270-284, teaser (c) "||(I_N (*) k_sigma) - I_ref||";
+ * SURVEY §8 f2) of the current tile at progressive level `level`, over this context's integrand
+ * shard [t_begin, t_end) (Ts integrands), error images e_i(p) = c_l,p,i / N_l - I_ref,i:
+ *   rmse[s]   = 1/Ts sum_i sqrt( 1/P sum_p ((k_s (*) e_i)(p))^2 ),  s < n_sigmas (<= 64), with
+ *               k_s the Gaussian exp(-(dx^2+dy^2)/(2 sigma_s^2)), |dx|,|dy| <= ceil(4 sigma_s),
+ *               normalised to sum 1 and applied toroidally (the tile repeats; taps wrap mod L)
+ *   spectrum  [L*L] (index ky*L + kx, DC first) = 1/Ts sum_i |DFT(e_i - mean e_i)|^2, or NULL
+ *   profile   [L/2]: mean of the spectrum over the frequencies with floor(|f|) = j + 1 (signed
+ *               frequencies, DC excluded), or NULL
+ * fp64, through the 2D DFT of every error image (Parseval); host outputs; synchronises.
+ * EINVAL on level >= n_levels, a sigma outside (0, 1e4], n_sigmas > 64 or L > 256. */
+int bn_eval_quality(bn_ctx *ctx, uint32_t level, const double *sigmas, uint32_t n_sigmas,
+                    double *rmse, double *spectrum, double *profile);
+
 /* Precomputed permutation of the pixel indices used by BN_PAPER_SWAP (PAPER.md l.303-304:
  * "we precompute a permutation of pixel indices that we store in a linear array").
  * perm: host uint32 [n], n = L*L of the tile the optimiser will run on, every index in [0, n)

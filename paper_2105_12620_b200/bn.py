@@ -26,7 +26,7 @@ SYMBOLS = ("bn_create", "bn_destroy", "bn_last_error", "bn_version", "bn_set_lat
            "bn_get_references", "bn_set_energy", "bn_set_tile", "bn_get_tile", "bn_eval_counts", "bn_energy",
            "bn_optimize", "bn_comm_init", "bn_comm_unique_id", "bn_launch_count", "bn_profile_enable",
            "bn_profile_get", "bn_window_distances", "bn_set_permutation",
-           "bn_set_energy_form")
+           "bn_set_energy_form", "bn_eval_quality")
 KERNELS = ("counts", "gather", "gram", "lut", "decide", "stats", "commit")
 
 
@@ -81,6 +81,7 @@ def load_library(path: str = LIB_PATH):
         "bn_window_distances": ([vp, vp, ctypes.c_int], ctypes.c_int),
         "bn_set_permutation": ([vp, vp, u32], ctypes.c_int),
         "bn_set_energy_form": ([vp, u32], ctypes.c_int),
+        "bn_eval_quality": ([vp, u32, vp, u32, vp, vp, vp], ctypes.c_int),
         "bn_profile_get": ([vp, u32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -226,6 +227,20 @@ class Sampler:
             ncp = (budget or self.L * self.L // 4) // 2
             lg = lg.reshape(passes, -1)[:, :ncp].copy()
         return out, lg
+
+    def eval_quality(self, level: int = 0, sigmas=None, spectrum: bool = True):
+        """Paper's evaluation criterion (§3.3): (denoised RMSE per sigma, mean error power
+        spectrum [L, L] or None, radial profile [L/2] or None).  Default sigmas: 16 log-spaced in
+        [0.25, 20]."""
+        sg = np.geomspace(0.25, 20.0, 16) if sigmas is None else np.ascontiguousarray(sigmas, dtype=np.float64)
+        sg = np.ascontiguousarray(sg, dtype=np.float64)
+        r = np.zeros(len(sg), np.float64)
+        S = np.zeros((self.L, self.L), np.float64) if spectrum else None
+        prof = np.zeros(self.L // 2, np.float64) if spectrum else None
+        self._check(self._lib.bn_eval_quality(self._ctx, level, sg.ctypes.data, len(sg), r.ctypes.data,
+                                              S.ctypes.data if S is not None else None,
+                                              prof.ctypes.data if prof is not None else None))
+        return r, S, prof
 
     def window_distances(self, radius: int = 7, out=None):
         """Partial (this bank shard) window distances D_l(p, p+o), [levels, P, H] int32."""

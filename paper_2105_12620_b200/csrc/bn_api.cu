@@ -150,7 +150,9 @@ struct bn_ctx {
     DevBuf<CountGroup> cgrp;  // packed fp32 operands of the filtered count test
     DevBuf<uint8_t> c, cn, cn2, acc, log, cexp;
     DevBuf<int> nc, nn, nn2, derr, progress;
-    DevBuf<uint32_t> perm, part;  // BN_PAPER_SWAP: precomputed permutation, per-pass partner map
+    DevBuf<uint32_t> perm, part;
+    DevBuf<double2> ev_tw, ev_X1;  // bn_eval_quality work buffers
+    DevBuf<double> ev_h, ev_rm, ev_sp, ev_out;  // BN_PAPER_SWAP: precomputed permutation, per-pass partner map
     uint32_t perm_n = 0;
     DevBuf<int4> Dt;
     DevBuf<long long> d0, d1b;   // int64 dE terms (DT_ESC = see escape tables)
@@ -788,6 +790,8 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
         ctx->d0.release(); ctx->d1b.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
         ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release();
+        ctx->ev_tw.release(); ctx->ev_X1.release(); ctx->ev_h.release(); ctx->ev_rm.release(); ctx->ev_sp.release();
+        ctx->ev_out.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release(); ctx->rows_done.release();
         if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
@@ -1176,6 +1180,84 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             }
         }
     }
+    return BN_OK;
+}
+
+int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t ns, double* rmse, double* spectrum,
+                    double* profile) {
+    if (!ctx) return BN_EINVAL;
+    int rc;
+    if ((rc = check_ready(ctx))) return rc;
+    if (level >= ctx->nl) return fail(ctx, BN_EINVAL, "level %u >= %u levels", level, ctx->nl);
+    if (ns > 64 || (ns && (!sigmas || !rmse))) return fail(ctx, BN_EINVAL, "bad sigma list (at most 64)");
+    for (uint32_t s = 0; s < ns; ++s)
+        if (!(sigmas[s] > 0) || !std::isfinite(sigmas[s]) || sigmas[s] > 1e4)
+            return fail(ctx, BN_EINVAL, "sigma[%u] = %g outside (0, 1e4]", s, sigmas[s]);
+    const uint32_t L = ctx->L, P = ctx->P, Ts = ctx->Ts;
+    if (L > 256) return fail(ctx, BN_EINVAL, "bn_eval_quality supports L <= 256 (L = %u)", L);
+    DeviceGuard g(ctx->dev);
+    if ((rc = ensure_counts(ctx))) return rc;
+    CUDA_TRY(ctx->iref.ensure(Ts));
+    k_iref<<<(Ts + 127) / 128, 128, 0, ctx->stream>>>(ctx->ab.p, ctx->pxy.p, Ts, ctx->iref.p);
+    LAUNCHED();
+    // twiddles w^m = exp(-2 pi i m / L) and the 1D kernel spectra h_s(k) = sum_d g(d) cos(2 pi k d / L) / sum_d g(d)
+    // (g = exp(-d^2 / (2 sigma^2)), |d| <= ceil(4 sigma)): host libm, like the energy tables
+    const double two_pi = 6.283185307179586476925286766559;
+    std::vector<double2> tw(L);
+    for (uint32_t m = 0; m < L; ++m) tw[m] = make_double2(std::cos(two_pi * m / L), -std::sin(two_pi * m / L));
+    const uint32_t nsk = ns ? ns : 1;
+    std::vector<double> h((size_t)nsk * L, 0.0);
+    for (uint32_t s = 0; s < ns; ++s) {
+        const int r = (int)std::ceil(4.0 * sigmas[s]);
+        double Z = 0.0;
+        for (int d = -r; d <= r; ++d) Z += std::exp(-(double)d * d / (2.0 * sigmas[s] * sigmas[s]));
+        for (uint32_t k = 0; k < L; ++k) {
+            double acc = 0.0;
+            for (int d = -r; d <= r; ++d)
+                acc += std::exp(-(double)d * d / (2.0 * sigmas[s] * sigmas[s])) *
+                       std::cos(two_pi * (double)(((int64_t)k * d % (int64_t)L + L) % L) / L);
+            h[(size_t)s * L + k] = acc / Z;
+        }
+    }
+    const uint32_t chunk = 1024, ngroups = (Ts + EV_II - 1) / EV_II;
+    CUDA_TRY(ctx->ev_tw.ensure(L));
+    CUDA_TRY(ctx->ev_h.ensure(h.size()));
+    CUDA_TRY(ctx->ev_X1.ensure((size_t)std::min(chunk, Ts) * P));
+    CUDA_TRY(ctx->ev_rm.ensure((size_t)Ts * L * nsk));
+    CUDA_TRY(ctx->ev_sp.ensure((size_t)ngroups * P));
+    CUDA_TRY(ctx->ev_out.ensure(64 + P + L / 2));
+    CUDA_TRY(cudaMemcpyAsync(ctx->ev_tw.p, tw.data(), L * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->ev_h.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    const size_t sm1 = (size_t)L * EV_II * 8 + L * 16, sm2 = (size_t)L * EV_II * 16 + L * 16 + (size_t)L * EV_II * 8;
+    CUDA_TRY(cudaFuncSetAttribute(k_ev_dft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+    CUDA_TRY(cudaFuncSetAttribute(k_ev_dft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+    const double invN = 1.0 / (double)ctx->levels[level];
+    for (uint32_t i0 = 0; i0 < Ts; i0 += chunk) {
+        const uint32_t ci = std::min(chunk, Ts - i0);
+        const dim3 grid(L, (ci + EV_II - 1) / EV_II);
+        k_ev_dft_rows<<<grid, 256, sm1, ctx->stream>>>(ctx->c.p, L, ctx->rowB, level * ctx->Tp, invN, ctx->iref.p, i0,
+                                                        ci, ctx->ev_tw.p, ctx->ev_X1.p);
+        LAUNCHED();
+        k_ev_dft_cols<<<grid, 256, sm2, ctx->stream>>>(ctx->ev_X1.p, L, i0, ci, ctx->ev_tw.p, ctx->ev_h.p, nsk,
+                                                        ctx->ev_rm.p, ctx->ev_sp.p);
+        LAUNCHED();
+    }
+    double* dr = ctx->ev_out.p;
+    double* dS = dr + 64;
+    double* dprof = dS + P;
+    if (ns) {
+        k_ev_rmse<<<ns, 256, 0, ctx->stream>>>(ctx->ev_rm.p, L, Ts, nsk, dr);
+        LAUNCHED();
+        CUDA_TRY(cudaMemcpyAsync(rmse, dr, ns * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (spectrum || profile) {
+        k_ev_spectrum<<<1, 256, 0, ctx->stream>>>(ctx->ev_sp.p, L, ngroups, Ts, dS, dprof);
+        LAUNCHED();
+        if (spectrum) CUDA_TRY(cudaMemcpyAsync(spectrum, dS, (size_t)P * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (profile)
+            CUDA_TRY(cudaMemcpyAsync(profile, dprof, (L / 2) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return BN_OK;
 }
 

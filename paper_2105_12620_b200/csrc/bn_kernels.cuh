@@ -2793,6 +2793,139 @@ __global__ void k_paper_decide(const uint32_t* __restrict__ perm, uint64_t seed,
     }
 }
 
+// --------------------------------------------------- evaluation criterion
+// PAPER.md §3.3 l.270-284 / teaser (c): RMSE of the test-integrand tiles after Gaussian
+// denoising, for a range of kernel widths, and the error power spectrum.  Computed through the
+// 2D DFT of every integrand's error image e_i(p) = c_i(p)/N - I_ref,i (fp64): the toroidal
+// convolution is a product in frequency space, so by Parseval
+//   rmse_i(sigma)^2 = 1/P^2 sum_f |E_i(f)|^2 K_sigma(f)^2,   K_sigma(kx,ky) = h(kx) h(ky)
+// (h = DFT of the periodised, normalised 1D Gaussian; real and even), and the spectrum is
+// |E_i(f)|^2 with the DC bin (the mean) removed.  Row DFT -> column DFT -> per-(integrand, kx)
+// partial sums, reduced in a fixed order (deterministic).
+constexpr int EV_II = 32;  // integrands per CTA
+// X1[ii][kx][y] = sum_x e_ii(x, y) w^(kx x), w = exp(-2 pi i / L); one CTA per (row y, 32 integrands).
+__global__ void __launch_bounds__(256) k_ev_dft_rows(const uint8_t* __restrict__ c, uint32_t L, uint32_t rowB,
+                                                     uint32_t loff, double invN, const double* __restrict__ iref,
+                                                     uint32_t i0, uint32_t ni, const double2* __restrict__ tw,
+                                                     double2* __restrict__ X1) {
+    extern __shared__ double ev_smem[];
+    double* E = ev_smem;                                         // [L][EV_II]
+    double2* w = reinterpret_cast<double2*>(E + (size_t)L * EV_II);  // [L]
+    const uint32_t y = blockIdx.x, ic = blockIdx.y * EV_II;      // chunk-local integrand base
+    for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) w[j] = tw[j];
+    for (uint32_t j = threadIdx.x; j < L * EV_II; j += blockDim.x) {
+        const uint32_t x = j / EV_II, ii = j % EV_II, i = ic + ii;
+        E[j] = i < ni ? (double)c[(size_t)(y * L + x) * rowB + loff + i0 + i] * invN - iref[i0 + i] : 0.0;
+    }
+    __syncthreads();
+    for (uint32_t o = threadIdx.x; o < L * EV_II; o += blockDim.x) {
+        const uint32_t kx = o / EV_II, ii = o % EV_II, i = ic + ii;
+        double re = 0.0, im = 0.0;
+        for (uint32_t x = 0; x < L; ++x) {
+            const double2 t = w[(kx * x) & (L - 1)];
+            const double e = E[x * EV_II + ii];
+            re = fma(e, t.x, re);
+            im = fma(e, t.y, im);
+        }
+        if (i < ni) X1[((size_t)i * L + kx) * L + y] = make_double2(re, im);
+    }
+}
+// Column DFT of X1 for one kx and 32 integrands, power |E(kx, ky)|^2, then
+//   rm[i][kx][s] = sum_ky |E|^2 K_s(kx, ky)^2       (partial Parseval sums)
+//   sp[cta][ky][kx] = sum_{ii in CTA} |E|^2          (DC excluded; partial spectrum)
+__global__ void __launch_bounds__(256) k_ev_dft_cols(const double2* __restrict__ X1, uint32_t L, uint32_t i0,
+                                                     uint32_t ni, const double2* __restrict__ tw,
+                                                     const double* __restrict__ h /* [ns][L] */, uint32_t ns,
+                                                     double* __restrict__ rm, double* __restrict__ sp) {
+    extern __shared__ double ev_smem[];
+    double2* X = reinterpret_cast<double2*>(ev_smem);            // [L][EV_II]
+    double2* w = X + (size_t)L * EV_II;                           // [L]
+    double* pw = reinterpret_cast<double*>(w + L);                // [L][EV_II]
+    const uint32_t kx = blockIdx.x, ic = blockIdx.y * EV_II;
+    for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) w[j] = tw[j];
+    for (uint32_t j = threadIdx.x; j < L * EV_II; j += blockDim.x) {
+        const uint32_t ii = j / L, y = j % L, i = ic + ii;
+        X[y * EV_II + ii] = i < ni ? X1[((size_t)i * L + kx) * L + y] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    for (uint32_t o = threadIdx.x; o < L * EV_II; o += blockDim.x) {
+        const uint32_t ky = o / EV_II, ii = o % EV_II;
+        double re = 0.0, im = 0.0;
+        for (uint32_t y = 0; y < L; ++y) {
+            const double2 t = w[(ky * y) & (L - 1)], v = X[y * EV_II + ii];
+            re = fma(v.x, t.x, re);
+            re = fma(-v.y, t.y, re);
+            im = fma(v.x, t.y, im);
+            im = fma(v.y, t.x, im);
+        }
+        pw[ky * EV_II + ii] = re * re + im * im;
+    }
+    __syncthreads();
+    // Parseval partials: one thread per (integrand, sigma), fixed ky order
+    for (uint32_t o = threadIdx.x; o < EV_II * ns; o += blockDim.x) {
+        const uint32_t ii = o / ns, sg = o % ns, i = ic + ii;
+        if (i >= ni) continue;
+        const double hx = h[(size_t)sg * L + kx];
+        double acc = 0.0;
+        for (uint32_t ky = 0; ky < L; ++ky) {
+            const double k2 = hx * h[(size_t)sg * L + ky];
+            acc = fma(pw[ky * EV_II + ii], k2 * k2, acc);
+        }
+        rm[((size_t)(i0 + i) * L + kx) * ns + sg] = acc;
+    }
+    // spectrum partial over this CTA's integrands, fixed ii order
+    for (uint32_t ky = threadIdx.x; ky < L; ky += blockDim.x) {
+        double acc = 0.0;
+        if (kx != 0 || ky != 0)
+            for (uint32_t ii = 0; ii < EV_II; ++ii) acc += pw[ky * EV_II + ii];
+        sp[((size_t)((i0 + ic) / EV_II) * L + ky) * L + kx] = acc;
+    }
+}
+// rmse[s] = 1/Ts sum_i sqrt(sum_kx rm[i][kx][s]) / P  -- one CTA per sigma, exact fixed order per
+// integrand, then a fixed-order block sum.
+__global__ void __launch_bounds__(256) k_ev_rmse(const double* __restrict__ rm, uint32_t L, uint32_t Ts, uint32_t ns,
+                                                 double* __restrict__ out) {
+    __shared__ double part[256];
+    const uint32_t sg = blockIdx.x;
+    double acc = 0.0;
+    for (uint32_t i = threadIdx.x; i < Ts; i += blockDim.x) {
+        double s = 0.0;
+        for (uint32_t kx = 0; kx < L; ++kx) s += rm[((size_t)i * L + kx) * ns + sg];
+        acc += sqrt(s) / ((double)L * L);
+    }
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int j = 0; j < (int)blockDim.x; ++j) t += part[j];
+        out[sg] = t / Ts;
+    }
+}
+// spectrum[f] = 1/Ts sum_chunks sp[chunk][f]; profile[j] = mean of spectrum over floor(|f|) = j + 1.
+__global__ void __launch_bounds__(256) k_ev_spectrum(const double* __restrict__ sp, uint32_t L, uint32_t nchunk,
+                                                     uint32_t Ts, double* __restrict__ S, double* __restrict__ prof) {
+    const uint32_t P = L * L;
+    for (uint32_t f = threadIdx.x; f < P; f += blockDim.x) {
+        double acc = 0.0;
+        for (uint32_t k = 0; k < nchunk; ++k) acc += sp[(size_t)k * P + f];
+        S[f] = acc / Ts;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < L / 2; j += blockDim.x) {
+        double sum = 0.0;
+        uint32_t n = 0;
+        for (uint32_t f = 0; f < P; ++f) {
+            const int kx = (int)(f % L), ky = (int)(f / L);
+            const int fx = kx <= (int)L / 2 ? kx : kx - (int)L, fy = ky <= (int)L / 2 ? ky : ky - (int)L;
+            if ((uint32_t)floor(sqrt((double)(fx * fx + fy * fy))) == j + 1) {
+                sum += S[f];
+                ++n;
+            }
+        }
+        prof[j] = n ? sum / n : 0.0;
+    }
+}
+
 // --------------------------------------------------------------------------- I_ref, readback
 // Area of {(x,y) in [0,1]^2 : a(x - px) + b(y - py) >= 0}: the unit square clipped by the
 // half-plane (walk the 4 edges, keep inside vertices and edge crossings), shoelace area. fp64.

@@ -411,3 +411,36 @@ def test_eq1_forms_parity(bn, oracle_mod, form, mode):
         _check_run(s, o, U, 3, mode, seed=19)
     with pytest.raises(bn.BNError):
         s.set_energy_form(3)
+
+
+# ----------------------------------------------------- evaluation criterion (f2, §3.3)
+@pytest.mark.parametrize("L,T,levels,level", [(16, 40, (4, 16), 1), (32, 70, (16,), 0), (16, 33, (1, 4), 0)])
+def test_eval_quality_parity(bn, oracle_mod, L, T, levels, level):
+    """Denoised-RMSE curve (16 log-spaced sigmas in [0.25, 20], kernels larger than the tile wrap),
+    error power spectrum and radial profile: the GPU's DFT/Parseval route against the oracle's plain
+    convolution and plain DFT, fp64 (relative 1e-9 of the largest value)."""
+    s, o, U = make(bn, oracle_mod, L, T, levels)
+    sig = np.geomspace(0.25, 20.0, 16)
+    r, S, prof = s.eval_quality(level, sig)
+    c = o.counts(U)
+    ro = o.denoised_rmse(c, level, sig)
+    So, profo = o.error_spectrum(c, level)
+    np.testing.assert_allclose(r, ro, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(S, So, rtol=0, atol=1e-9 * So.max())
+    np.testing.assert_allclose(prof, profo, rtol=1e-9, atol=1e-12 * profo.max())
+
+
+def test_eval_quality_after_gpu_passes(bn, oracle_mod):
+    """The criterion on GPU-optimised tiles (SWAP and paper mode) equals the oracle's on the same
+    tile, and shows the paper's ordering: lower denoised RMSE than the random tile at sigma = 2."""
+    s, o, U = make(bn, oracle_mod, 32, 48, (16,))
+    r0, _, _ = s.eval_quality(0, [2.0], spectrum=False)
+    s.optimize(6, 1, mode=1, stats=False)
+    r1, S1, _ = s.eval_quality(0, [2.0])
+    c1 = o.counts(s.get_tile())
+    np.testing.assert_allclose(r1, o.denoised_rmse(c1, 0, [2.0]), rtol=1e-9)
+    assert r1[0] < 0.8 * r0[0]
+    with pytest.raises(bn.BNError):
+        s.eval_quality(1, [2.0])
+    with pytest.raises(bn.BNError):
+        s.eval_quality(0, [0.0])
