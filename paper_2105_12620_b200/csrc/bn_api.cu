@@ -200,6 +200,7 @@ struct bn_ctx {
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
     bool cluster_v2 = false;  // BN_DECIDE=cluster2: shared-memory-staged rows (v2)
+    bool swap_v3 = false;     // BN_DECIDE=swap3: SWAP on k_decide_cl3 (one warp per couple) instead of k_decide_swap
     // per-kernel event timing (bn_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -565,8 +566,9 @@ template <int R>
 int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     const uint32_t nb = ctx->L / 8, P = ctx->P;
-    uint32_t cpc = mode ? 8 : 16;
-    while (cpc > nb) cpc /= 2;
+    const bool swap_v4 = mode && !ctx->cluster_v1 && !ctx->cluster_v2 && !ctx->swap_v3;
+    uint32_t cpc = mode && !swap_v4 ? 8 : 16;
+    while (cpc > nb * nb / (swap_v4 ? 1 : nb)) cpc /= 2;  // at most M slots (SWAP v4) / nb per CTA
     const uint32_t ncta = nb * nb / cpc;
     *done = false;
     if (ncta > 16 || ctx->no_cluster) return BN_OK;
@@ -575,14 +577,17 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     // by bulk copies; v1 (BN_DECIDE=cluster1): byte flags + a cluster barrier per class
     const int ver = ctx->cluster_v1 ? 1 : ctx->cluster_v2 ? 2 : 3;
     const size_t rows = (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8, slots = (size_t)64 * 4 * (mode ? 2 : 1) * cpc;
-    const size_t smem = ver == 3 ? 4 * (size_t)P + slots : ver == 2 ? rows + 4 * (size_t)P + slots : rows + P;
-    const void* fn = ver == 3   ? (mode ? (const void*)k_decide_cl3<R, 1> : (const void*)k_decide_cl3<R, 0>)
+    const size_t smem = swap_v4  ? 4 * (size_t)P + (size_t)64 * cpc * 6
+                        : ver == 3 ? 4 * (size_t)P + slots : ver == 2 ? rows + 4 * (size_t)P + slots : rows + P;
+    const void* fn = swap_v4    ? (const void*)k_decide_swap<R>
+                     : ver == 3 ? (mode ? (const void*)k_decide_cl3<R, 1> : (const void*)k_decide_cl3<R, 0>)
                      : ver == 2 ? (mode ? (const void*)k_decide_cl2<R, 1> : (const void*)k_decide_cl2<R, 0>)
                                 : (mode ? (const void*)k_decide_cluster<R, 1> : (const void*)k_decide_cluster<R, 0>);
     if (!ctx->cluster_attr_set[R]) {
         for (const void* f : {(const void*)k_decide_cluster<R, 0>, (const void*)k_decide_cluster<R, 1>,
                               (const void*)k_decide_cl2<R, 0>, (const void*)k_decide_cl2<R, 1>,
-                              (const void*)k_decide_cl3<R, 0>, (const void*)k_decide_cl3<R, 1>}) {
+                              (const void*)k_decide_cl3<R, 0>, (const void*)k_decide_cl3<R, 1>,
+                              (const void*)k_decide_swap<R>}) {
             CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
             CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         }
@@ -741,6 +746,7 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->no_cluster = dm && !strcmp(dm, "flags");
     ctx->cluster_v1 = dm && !strcmp(dm, "cluster1");
     ctx->cluster_v2 = dm && !strcmp(dm, "cluster2");
+    ctx->swap_v3 = dm && !strcmp(dm, "swap3");
     const char* ov = getenv("BN_OVERLAP");
     ctx->no_overlap = ov && !strcmp(ov, "0");
     const char* rf = getenv("BN_ROWFLAGS");

@@ -2547,6 +2547,85 @@ __global__ void __launch_bounds__(mode ? 256 : 512, 1) k_decide_cl3(uint32_t pas
     cluster_sync_all();
 }
 
+// SWAP cluster decision kernel: one warp per couple MEMBER (not per couple), so SWAP decisions
+// run with the same 16 warps x 16 CTAs shape and register budget as REDRAW.  The couples
+// {m, m ^ kappa} of class s are listed by their lower member (bit h = msb(kappa) of m clear), two
+// consecutive slots per couple, so both members of a couple sit in the same CTA, in warps 2j and
+// 2j+1: each warp sums its own member's window (acc-dependent terms, as in v3), the pair exchanges
+// the two int128 sums through shared memory under a 64-thread named barrier, and both decide on
+// the identical total.  Flags are broadcast exactly as in v3 (one st.async per member).
+__device__ __forceinline__ uint32_t couple_member(uint32_t c, uint32_t kappa, uint32_t upper) {
+    const uint32_t h = 31u - __clz(kappa);
+    const uint32_t m = ((c >> h) << (h + 1)) | (c & ((1u << h) - 1u));
+    return upper ? m ^ kappa : m;
+}
+template <int R>
+__global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
+                                                        const DTabs T, uint8_t* __restrict__ acc,
+                                                        i128* __restrict__ dEp, uint8_t* __restrict__ log) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    __shared__ uint8_t sDelta[8 * 16];
+    __shared__ __align__(8) uint64_t sbar[2];
+    __shared__ __align__(16) unsigned long long sPart[16][2];
+    const uint32_t nb = L / 8, M = nb * nb, P = L * L;
+    const uint32_t ncta = gridDim.x, first = blockIdx.x * cpc;  // first slot of this CTA
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* sflags = reinterpret_cast<uint32_t*>(dsm);        // [P]
+    uint32_t* sSlot = sflags + P;                                // [64][cpc] pixels
+    uint16_t* sIdx = reinterpret_cast<uint16_t*>(sSlot + 64 * cpc);  // [64][cpc] active indices m
+    const uint32_t sflags_addr = (uint32_t)__cvta_generic_to_shared(dsm);
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
+    auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
+    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
+    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
+        sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < 64 * cpc; j += blockDim.x) {
+        const uint32_t s = j / cpc, i = first + (j - s * cpc);
+        const uint32_t m = couple_member(i >> 1, swap_kappa(seed, pass_t, s, M), i & 1);
+        sSlot[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
+        sIdx[j] = (uint16_t)m;
+    }
+    __syncthreads();
+    WinTermsFlags32<R> A, An;
+    A.load_global(T, sSlot[warp]);
+    LaneOffsets<R> off;
+    off.init();
+    cluster_sync_all();  // every CTA's barriers and flags are initialised before any remote st.async
+    const uint32_t upper = (first + warp) & 1, pair_bar = 1 + (warp >> 1);
+    for (uint32_t s = 0; s < 64; ++s) {
+        if (s + 1 < 64) An.load_global(T, sSlot[(s + 1) * cpc + warp]);
+        if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
+        if (threadIdx.x == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
+                         : "memory");
+        const uint32_t p = sSlot[s * cpc + warp];
+        const i128 mine = A.sum_flags(sflags, L, p, off, T);
+        if (lane == 0) {
+            sPart[warp][0] = (unsigned long long)mine;
+            sPart[warp][1] = (unsigned long long)((u128)mine >> 64);
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+        const uint32_t o = warp ^ 1;
+        const i128 other = (i128)(((u128)sPart[o][1] << 64) | sPart[o][0]);
+        const i128 sum = upper ? other + mine : mine + other;
+        const bool ok = 2 * sum < 0;
+        if (lane < ncta) st_async_u32(sflags_addr + 4 * p, mailbox(s), lane, ok ? 1u : 0u);
+        if (lane == 0) {
+            acc[p] = ok;
+            dEp[p] = (ok && !upper) ? 2 * sum : (i128)0;
+            if (log) log[(size_t)s * M + sIdx[s * cpc + warp]] = ok;
+        }
+        A = An;
+    }
+    tc::mbar_wait(mailbox(63), (63 >> 1) & 1);
+    cluster_sync_all();
+}
+
 // ------------------------------------------------------------------------------- commit
 __global__ void k_commit(const uint8_t* __restrict__ acc, uint32_t P, uint32_t rowB, uint32_t nl,
                          const uint2* __restrict__ Un, uint2* __restrict__ U, const uint8_t* __restrict__ cn,

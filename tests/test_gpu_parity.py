@@ -306,7 +306,7 @@ def test_tc_gram_optimize_parity(bn, oracle_mod, monkeypatch, variant):
     _check_run(s, o, U, 2, 0, seed=7)
 
 
-@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags", "per_class"])
+@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags", "per_class", "swap3"])
 def test_escape_path_all_terms(bn, oracle_mod, monkeypatch, decide):
     """dE terms are int64 with an int128 escape; forcing every term through the escape tables
     (BN_DT_ESCAPE=1) must give the same bit-exact passes on every decision kernel."""
@@ -318,12 +318,13 @@ def test_escape_path_all_terms(bn, oracle_mod, monkeypatch, decide):
     _check_run(s2, o2, U2, 2, 1, seed=14)
 
 
-@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags"])
-@pytest.mark.parametrize("L,mode", [(16, 0), (64, 1), (128, 0), (128, 1)])
+@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags", "swap3"])
+@pytest.mark.parametrize("L,mode", [(16, 0), (16, 1), (32, 1), (64, 1), (128, 0), (128, 1)])
 def test_decide_kernels_parity(bn, oracle_mod, monkeypatch, decide, L, mode):
-    """Every persistent decision kernel (barrier-free cluster v2 = default, cluster v1 with a
-    cluster barrier per class, cooperative flag kernel) against the oracle, both modes, tile sides
-    from 2 to 16 active indices per band."""
+    """Every persistent decision kernel (register-prefetched cluster v3 = default, SWAP per-member
+    cluster kernel = default for SWAP, v3 one-warp-per-couple SWAP (swap3), shared-memory-staged v2,
+    cluster v1 with a cluster barrier per class, cooperative flag kernel) against the oracle, both
+    modes, tile sides from 2 to 16 active indices per band."""
     monkeypatch.setenv("BN_DECIDE", decide)
     s, o, U = make(bn, oracle_mod, L, 40, (4, 16))
     _check_run(s, o, U, 2, mode, seed=21 + L + mode)
