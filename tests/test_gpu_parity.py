@@ -158,19 +158,20 @@ def test_errors(bn, oracle_mod):
 
 # ------------------------------------------------------------------ full BASELINE sizes
 @pytest.mark.slow
-def test_c3_full_size_sampled(bn, oracle_mod):
-    """C3 at full size (128x128, T=1024, 1/4/16/64 spp) in the bench's launch configuration:
-    all counts bit-exact, the first colour class's accept decisions identical to the oracle,
-    and the exact-additivity / monotonicity invariants of the whole pass."""
+@pytest.mark.parametrize("mode", [1, 0])
+def test_c3_full_size_sampled(bn, oracle_mod, mode):
+    """C3 at full size (128x128, T=1024, 1/4/16/64 spp) in the bench's launch configuration (SWAP,
+    and REDRAW): all counts bit-exact, the first colour classes' accept decisions identical to the
+    oracle, and the exact-additivity / monotonicity invariants of the whole pass."""
     cfg = synth.CONFIGS["C3"]
     U, bank = synth.problem_inputs(cfg)
     s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
     co = o.counts(U)
     assert np.array_equal(s.eval_counts(), co)          # all 64 M counts, bit-exact
     E0, _ = s.energy()
-    st, lg = s.optimize(1, synth.opt_seed(cfg), log=True)
-    _, _, sto, lgo = o.optimize(U, co, passes=1, seed=synth.opt_seed(cfg), max_steps=2, energy_each_pass=False,
-                                log=True)
+    st, lg = s.optimize(1, synth.opt_seed(cfg), mode=mode, log=True)
+    _, _, sto, lgo = o.optimize(U, co, mode=mode, passes=1, seed=synth.opt_seed(cfg), max_steps=2,
+                                energy_each_pass=False, log=True)
     assert np.array_equal(lg[0, :2], lgo[0, :2])
     assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"] and st[0]["dE_sum"] < 0
     assert s.energy()[0] == st[0]["E_fixed"]
