@@ -200,6 +200,7 @@ struct bn_ctx {
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
     bool cluster_v2 = false;  // BN_DECIDE=cluster2: shared-memory-staged rows (v2)
+    bool old_swap_gather = false;  // BN_GATHER=old: k_swap_gather (one Philox per copying thread)
     bool swap_v3 = false;     // BN_DECIDE=swap3: SWAP on k_decide_cl3 (one warp per couple) instead of k_decide_swap
     // per-kernel event timing (bn_profile_*)
     bool prof = false;
@@ -747,6 +748,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->cluster_v1 = dm && !strcmp(dm, "cluster1");
     ctx->cluster_v2 = dm && !strcmp(dm, "cluster2");
     ctx->swap_v3 = dm && !strcmp(dm, "swap3");
+    const char* gth = getenv("BN_GATHER");
+    ctx->old_swap_gather = gth && !strcmp(gth, "old");
     const char* ov = getenv("BN_OVERLAP");
     ctx->no_overlap = ov && !strcmp(ov, "0");
     const char* rf = getenv("BN_ROWFLAGS");
@@ -1014,8 +1017,8 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             return fail(ctx, BN_ESTATE, "BN_PAPER_SWAP needs bn_set_permutation with L*L = %u entries", P);
         if (budget < 2 || (budget & 1) || budget > P)
             return fail(ctx, BN_EINVAL, "budget %u: must be even and in [2, L*L = %u]", budget, P);
-        CUDA_TRY(ctx->part.ensure(P));
     }
+    if (prm->mode != BN_REDRAW) CUDA_TRY(ctx->part.ensure(P));
     CUDA_TRY(ctx->pstats.ensure(prm->passes + 1));
     int nsm_fin = 148;
     cudaDeviceGetAttribute(&nsm_fin, cudaDevAttrMultiProcessorCount, ctx->dev);
@@ -1096,8 +1099,15 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             }
         } else {
             KSTART(BN_K_GATHER);
-            k_swap_gather<<<64 * M, 128, 0, cs>>>(ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p, ctx->nc.p, ctx->nn.p,
-                                                 ctx->L, prm->seed, t, ctx->rowB, nl);
+            if (ctx->old_swap_gather) {
+                k_swap_gather<<<64 * M, 128, 0, cs>>>(ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p, ctx->nc.p, ctx->nn.p,
+                                                     ctx->L, prm->seed, t, ctx->rowB, nl);
+            } else {
+                k_swap_pairs<<<(64 * M + 255) / 256, 256, 0, cs>>>(ctx->L, prm->seed, t, ctx->part.p);
+                LAUNCHED();
+                k_paper_gather<<<(P + 7) / 8, 256, 0, cs>>>(ctx->part.p, ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p,
+                                                            ctx->nc.p, ctx->nn.p, P, ctx->rowB, nl);
+            }
             LAUNCHED_K();
         }
         // next pass's candidates: their buffer was last read by finish(pi-1), already ordered on cs;

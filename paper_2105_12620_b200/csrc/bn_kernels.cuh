@@ -394,6 +394,18 @@ __global__ void k_swap_gather(const uint2* __restrict__ U, uint2* __restrict__ U
     if (threadIdx.x < nl) nn[(size_t)p * nl + threadIdx.x] = nc[(size_t)p2 * nl + threadIdx.x];
 }
 
+// SWAP partner map of pass t: part[p] = p2 for every couple member (one thread per (class, index);
+// 3 Philox draws per thread instead of per copying thread).  The rows are then gathered by
+// k_paper_gather (one warp per pixel, 16-byte copies).
+__global__ void k_swap_pairs(uint32_t L, uint64_t seed, uint32_t pass_t, uint32_t* __restrict__ part) {
+    const uint32_t M = (L / 8) * (L / 8);
+    const uint32_t sm = blockIdx.x * blockDim.x + threadIdx.x;  // s * M + m
+    if (sm >= 64 * M) return;
+    const uint32_t s = sm / M, m = sm - s * M;
+    const uint32_t kappa = swap_kappa(seed, pass_t, s, M);
+    part[class_pixel(L, seed, pass_t, s, m)] = class_pixel(L, seed, pass_t, s, m ^ kappa);
+}
+
 // ------------------------------------------------------------------- window-distance planes
 // The window distances of every (level l, pixel p, half-window offset h) are two int2 planes over
 // the same [l][p][h] index (the int4 buffer Dt of nl*P*H records holds plane 0 in its first half,

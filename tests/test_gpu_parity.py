@@ -108,8 +108,11 @@ def test_c1_shape_full_run(bn, oracle_mod, mode):
     assert st[-1]["E_fixed"] < st[0]["E_fixed"] + (-st[0]["dE_sum"])
 
 
-def test_c2_shape_swap(bn, oracle_mod):
-    """C2 shape (SWAP, 4 spp) at 32x32, T=100 (ragged)."""
+@pytest.mark.parametrize("gather", ["", "old"])
+def test_c2_shape_swap(bn, oracle_mod, monkeypatch, gather):
+    """C2 shape (SWAP, 4 spp) at 32x32, T=100 (ragged); partner map + warp gather (default) and the
+    one-CTA-per-pixel gather (BN_GATHER=old)."""
+    monkeypatch.setenv("BN_GATHER", gather)
     s, o, U = make(bn, oracle_mod, 32, 100, (4,))
     _check_run(s, o, U, 6, 1, seed=5)
 
