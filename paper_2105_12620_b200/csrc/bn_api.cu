@@ -200,7 +200,6 @@ struct bn_ctx {
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
     bool cluster_v2 = false;  // BN_DECIDE=cluster2: shared-memory-staged rows (v2)
-    bool no_split = true;          // BN_SPLIT=1: class-pipelined window sums (measured slower)
     bool old_swap_gather = false;  // BN_GATHER=old: k_swap_gather (one Philox per copying thread)
     bool swap_v3 = false;     // BN_DECIDE=swap3: SWAP on k_decide_cl3 (one warp per couple) instead of k_decide_swap
     // per-kernel event timing (bn_profile_*)
@@ -579,8 +578,8 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     // by bulk copies; v1 (BN_DECIDE=cluster1): byte flags + a cluster barrier per class
     const int ver = ctx->cluster_v1 ? 1 : ctx->cluster_v2 ? 2 : 3;
     const size_t rows = (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8, slots = (size_t)64 * 4 * (mode ? 2 : 1) * cpc;
-    const size_t smem = swap_v4  ? 4 * (size_t)P + (size_t)64 * cpc * 6 + P
-                        : ver == 3 ? 4 * (size_t)P + slots + P : ver == 2 ? rows + 4 * (size_t)P + slots : rows + P;
+    const size_t smem = swap_v4  ? 4 * (size_t)P + (size_t)64 * cpc * 6
+                        : ver == 3 ? 4 * (size_t)P + slots : ver == 2 ? rows + 4 * (size_t)P + slots : rows + P;
     const void* fn = swap_v4    ? (const void*)k_decide_swap<R>
                      : ver == 3 ? (mode ? (const void*)k_decide_cl3<R, 1> : (const void*)k_decide_cl3<R, 0>)
                      : ver == 2 ? (mode ? (const void*)k_decide_cl2<R, 1> : (const void*)k_decide_cl2<R, 0>)
@@ -616,11 +615,9 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     const DTabs T = {ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
     uint8_t* acc = ctx->acc.p;
     i128* dEp = ctx->dEp.p;
-    int split = ctx->no_split ? 0 : 1;
-    void* args3[] = {&t, &seed, &L, &cpc, (void*)&T, &acc, &dEp, &log, &split};
     void* args[] = {&t, &seed, &L, &cpc, (void*)&T, &acc, &dEp, &log};
     KSTART(BN_K_DECIDE);
-    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, (swap_v4 || ver == 3) ? args3 : args);
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) return fail(ctx, BN_ECUDA, "cluster decide launch: %s", cudaGetErrorString(e));
     LAUNCHED_K();
     *done = true;
@@ -753,8 +750,6 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->swap_v3 = dm && !strcmp(dm, "swap3");
     const char* gth = getenv("BN_GATHER");
     ctx->old_swap_gather = gth && !strcmp(gth, "old");
-    const char* spl = getenv("BN_SPLIT");
-    ctx->no_split = !(spl && !strcmp(spl, "1"));
     const char* ov = getenv("BN_OVERLAP");
     ctx->no_overlap = ov && !strcmp(ov, "0");
     const char* rf = getenv("BN_ROWFLAGS");

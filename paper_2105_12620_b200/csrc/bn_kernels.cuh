@@ -2383,65 +2383,7 @@ struct WinTermsFlags32 : WinTerms<R> {
         if (BN_DEC_RED) return (i128)warp_sum_u128((u128)acc);
         return warp_sum_i128_redux((unsigned long long)acc, (unsigned long long)(acc >> 64));
     }
-    __device__ __forceinline__ i128 term(int j, bool f, uint32_t p, const DTabs T) const {
-        constexpr int WN = WinTerms<R>::WN;
-        const long long v = f ? this->v1[j] : this->v0[j];
-        if (v != DT_ESC) return (i128)v;
-        const longlong2 e = (f ? T.x1 : T.x0)[(size_t)p * WN + (threadIdx.x & 31) + 32 * j];
-        return ((i128)e.y << 64) | (u128)(unsigned long long)e.x;
-    }
-    // Split window sum for the class-pipelined decisions.  Phase 1 (before the flags of class
-    // `late` have arrived): the warp-reduced sum of every term whose neighbour is not in class
-    // `late` (its flag is final: decided earlier, or undecided = 0), plus the delta0 term of the
-    // `late` neighbours; `mask` marks the late terms of this lane.  Phase 2 (after the wait):
-    // the correction sum_{late, accepted} (delta1 - delta0), warp-reduced only if any lane has one.
-    __device__ __forceinline__ i128 sum_known(const uint32_t* sflags, const uint8_t* scls, uint32_t late, uint32_t L,
-                                              uint32_t p, const LaneOffsets<R>& off, const DTabs T,
-                                              uint32_t& mask) const {
-        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
-        const int lane = threadIdx.x & 31;
-        const uint32_t x = p & (L - 1), y = p / L;
-        i128 acc = 0;
-        mask = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const int w = lane + 32 * j;
-            if (w < WN) {
-                const uint32_t q = ((y + off.oy[j]) & (L - 1)) * L + ((x + off.ox[j]) & (L - 1));
-                const bool lt = scls[q] == late;
-                const bool f = !lt && sflags[q] != 0;
-                if (lt) mask |= 1u << j;
-                acc += term(j, f, p, T);
-            }
-        }
-        return (i128)warp_sum_u128((u128)acc);
-    }
-    __device__ __forceinline__ i128 sum_late(const uint32_t* sflags, uint32_t L, uint32_t p, const LaneOffsets<R>& off,
-                                             const DTabs T, uint32_t mask) const {
-        constexpr int PER = WinTerms<R>::PER;
-        const uint32_t x = p & (L - 1), y = p / L;
-        i128 c = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j)
-            if (mask & (1u << j)) {
-                const uint32_t q = ((y + off.oy[j]) & (L - 1)) * L + ((x + off.ox[j]) & (L - 1));
-                if (sflags[q] != 0) c += term(j, true, p, T) - term(j, false, p, T);
-            }
-        if (!__any_sync(0xffffffffu, c != 0)) return 0;
-        return (i128)warp_sum_u128((u128)c);
-    }
 };
-
-// Colour class of every pixel in pass t (the inverse of class_pixel): scls[p] = 8 r + k.
-__device__ __forceinline__ void fill_classes(uint8_t* scls, const uint8_t* sDelta, uint32_t L, uint32_t pass_t) {
-    const uint32_t nb = L >> 3, P = L * L;
-    for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) {
-        const uint32_t x = p & (L - 1), y = p / L;
-        const uint32_t along = (pass_t & 1) ? y : x, across = (pass_t & 1) ? x : y;
-        const uint32_t r = across & 7, b = across >> 3;
-        scls[p] = (uint8_t)(8 * r + ((along - sDelta[r * nb + b]) & 7));
-    }
-}
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -2553,7 +2495,7 @@ __global__ void __launch_bounds__(512, 1) k_decide_cl2(uint32_t pass_t, uint64_t
 template <int R, int mode>
 __global__ void __launch_bounds__(mode ? 256 : 512, 1) k_decide_cl3(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
                                                        const DTabs T, uint8_t* __restrict__ acc,
-                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log, int split) {
+                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log) {
     constexpr uint32_t NSW = mode ? 2 : 1;  // candidates per warp (SWAP: the candidate and its partner)
     extern __shared__ __align__(16) uint8_t dsm[];
     __shared__ uint8_t sDelta[8 * 16];
@@ -2564,7 +2506,6 @@ __global__ void __launch_bounds__(mode ? 256 : 512, 1) k_decide_cl3(uint32_t pas
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* sflags = reinterpret_cast<uint32_t*>(dsm);  // [P]
     uint32_t* sSlot = sflags + P;                          // [64][cpc * NSW]
-    uint8_t* scls = reinterpret_cast<uint8_t*>(sSlot + 64 * cpc * NSW);  // [P] class of every pixel
     const uint32_t sflags_addr = (uint32_t)__cvta_generic_to_shared(dsm);
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
     auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
@@ -2578,7 +2519,6 @@ __global__ void __launch_bounds__(mode ? 256 : 512, 1) k_decide_cl3(uint32_t pas
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (split) fill_classes(scls, sDelta, L, pass_t);
     const uint32_t per_class = cpc * NSW;
     for (uint32_t j = threadIdx.x; j < 64 * per_class; j += blockDim.x) {
         const uint32_t s = j / per_class, i = j - s * per_class;
@@ -2597,25 +2537,14 @@ __global__ void __launch_bounds__(mode ? 256 : 512, 1) k_decide_cl3(uint32_t pas
             An.load_global(T, sSlot[(s + 1) * per_class + warp]);
             if (mode) Bn.load_global(T, sSlot[(s + 1) * per_class + cpc + warp]);
         }
+        if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
+        if (threadIdx.x == 0)  // this CTA expects M flags of class s (the phase of class s-2 is complete)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
+                         : "memory");
         const uint32_t m = first + warp, mm = m ^ (mode ? sKappa[s] : 0u);
         const uint32_t p = sSlot[s * per_class + warp], p2 = mode ? sSlot[s * per_class + cpc + warp] : p;
-        i128 sum;
-        if (split && !mode) {  // everything but class s-1's neighbours while its flags are in flight
-            uint32_t mask;
-            sum = A.sum_known(sflags, scls, s - 1, L, p, off, T, mask);
-            if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);
-            if (threadIdx.x == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
-                             : "memory");
-            sum += A.sum_late(sflags, L, p, off, T, mask);
-        } else {
-            if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
-            if (threadIdx.x == 0)  // this CTA expects M flags of class s (the phase of class s-2 is complete)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
-                             : "memory");
-            sum = A.sum_flags(sflags, L, p, off, T);
-            if (mode) sum += B.sum_flags(sflags, L, p2, off, T);
-        }
+        i128 sum = A.sum_flags(sflags, L, p, off, T);
+        if (mode) sum += B.sum_flags(sflags, L, p2, off, T);
         const bool ok = 2 * sum < 0;
         if (lane < ncta) st_async_u32(sflags_addr + 4 * p, mailbox(s), lane, ok ? 1u : 0u);
         if (lane == 0) {  // bookkeeping for commit/stats
@@ -2645,7 +2574,7 @@ __device__ __forceinline__ uint32_t couple_member(uint32_t c, uint32_t kappa, ui
 template <int R>
 __global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
                                                         const DTabs T, uint8_t* __restrict__ acc,
-                                                        i128* __restrict__ dEp, uint8_t* __restrict__ log, int split) {
+                                                        i128* __restrict__ dEp, uint8_t* __restrict__ log) {
     extern __shared__ __align__(16) uint8_t dsm[];
     __shared__ uint8_t sDelta[8 * 16];
     __shared__ __align__(8) uint64_t sbar[2];
@@ -2656,7 +2585,6 @@ __global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_
     uint32_t* sflags = reinterpret_cast<uint32_t*>(dsm);        // [P]
     uint32_t* sSlot = sflags + P;                                // [64][cpc] pixels
     uint16_t* sIdx = reinterpret_cast<uint16_t*>(sSlot + 64 * cpc);  // [64][cpc] active indices m
-    uint8_t* scls = reinterpret_cast<uint8_t*>(sIdx + 64 * cpc);      // [P] class of every pixel
     const uint32_t sflags_addr = (uint32_t)__cvta_generic_to_shared(dsm);
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
     auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
@@ -2668,7 +2596,6 @@ __global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (split) fill_classes(scls, sDelta, L, pass_t);
     for (uint32_t j = threadIdx.x; j < 64 * cpc; j += blockDim.x) {
         const uint32_t s = j / cpc, i = first + (j - s * cpc);
         const uint32_t m = couple_member(i >> 1, swap_kappa(seed, pass_t, s, M), i & 1);
@@ -2684,23 +2611,12 @@ __global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_
     const uint32_t upper = (first + warp) & 1, pair_bar = 1 + (warp >> 1);
     for (uint32_t s = 0; s < 64; ++s) {
         if (s + 1 < 64) An.load_global(T, sSlot[(s + 1) * cpc + warp]);
+        if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
+        if (threadIdx.x == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
+                         : "memory");
         const uint32_t p = sSlot[s * cpc + warp];
-        i128 mine;
-        if (split) {  // everything but class s-1's neighbours while its flags are in flight
-            uint32_t mask;
-            mine = A.sum_known(sflags, scls, s - 1, L, p, off, T, mask);
-            if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);
-            if (threadIdx.x == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
-                             : "memory");
-            mine += A.sum_late(sflags, L, p, off, T, mask);
-        } else {
-            if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
-            if (threadIdx.x == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
-                             : "memory");
-            mine = A.sum_flags(sflags, L, p, off, T);
-        }
+        const i128 mine = A.sum_flags(sflags, L, p, off, T);
         if (lane == 0) {
             sPart[warp][0] = (unsigned long long)mine;
             sPart[warp][1] = (unsigned long long)((u128)mine >> 64);

@@ -322,7 +322,7 @@ def test_escape_path_all_terms(bn, oracle_mod, monkeypatch, decide):
     _check_run(s2, o2, U2, 2, 1, seed=14)
 
 
-@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags", "swap3", "split"])
+@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags", "swap3"])
 @pytest.mark.parametrize("L,mode", [(16, 0), (16, 1), (32, 1), (64, 1), (128, 0), (128, 1)])
 def test_decide_kernels_parity(bn, oracle_mod, monkeypatch, decide, L, mode):
     """Every persistent decision kernel (register-prefetched cluster v3 = default, SWAP per-member
@@ -330,7 +330,6 @@ def test_decide_kernels_parity(bn, oracle_mod, monkeypatch, decide, L, mode):
     cluster v1 with a cluster barrier per class, cooperative flag kernel) against the oracle, both
     modes, tile sides from 2 to 16 active indices per band."""
     monkeypatch.setenv("BN_DECIDE", decide)
-    monkeypatch.setenv("BN_SPLIT", "1" if decide == "split" else "0")
     s, o, U = make(bn, oracle_mod, L, 40, (4, 16))
     _check_run(s, o, U, 2, mode, seed=21 + L + mode)
 
