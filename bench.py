@@ -39,6 +39,7 @@ TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 # 148 SMs; one IDP.4A = 4 int8 multiply-accumulates = 8 ops.  DESIGN.md §7 derives this peak.
 SMS = 148
 DP4A_PER_CLK_SM = 64
+L2_PEAK_GBS = 15037.0  # measured L2-resident read bandwidth, tools/l2bw.cu
 
 
 def parse():
@@ -217,6 +218,14 @@ def roofline(prof, cfg, peaks, sm_clock_mhz, name=None):
         out["limiter"] = ("L2->SM operand streaming: the UMMA pipe runs at its peak MAC rate when fed "
                           "(tools/umma_bench.cu), a run without the epilogue takes ~80% of the kernel "
                           "time; 31% of the issued MACs are useful (dense 128x240 tiles, DESIGN.md 5.1)")
+        # TMA operand bytes per launch: every (8x8 block, level) item streams 3 neighbour chunks x Tp/128
+        # K-slices of one 46 KB stage (A: 128 rows, B: 240 rows of 128 B)
+        items = (cfg.L // 8) ** 2 * len(cfg.levels)
+        stream = items * 3 * (-(-cfg.T // 256) * 256 // 128) * (128 + 240) * 128
+        gbs = stream / (ms / max(n, 1) / 1e3) / 1e9
+        out["operand_stream"] = {"bytes_per_launch": stream, "achieved_GBs": gbs, "l2_read_peak_GBs": L2_PEAK_GBS,
+                                 "frac": gbs / L2_PEAK_GBS,
+                                 "peak_source": "tools/l2bw.cu on this pool (L2-resident 48 MB, 16-B loads, all SMs)"}
     if name == "counts":
         out["limiter"] = ("ALU-pipe issue: per test 1 FFMA2 (fma pipe) + ~1.75 half-rate ALU ops (sign "
                           "count, |t| filter); the FFMA-lane peak is the reported denominator (DESIGN.md 5.1)")
