@@ -78,7 +78,7 @@ int bn_get_references(bn_ctx *ctx, double *iref);
 
 /* Blue-noise energy parameters (north star; Eq. 1 PAPER.md l.232-237 for sigma_i = 2.1):
  *   E = sum_l sum_p sum_{o in O} q(o, D_l(p, p+o)),   O = [-R,R]^2 \ {0} (toroidal),
- *   q(o, D) = rn_uint64( 2^64 * exp(-|o|^2 / sigma_i^2) * exp(-(sqrt(D)/N_l) / sigma_s^2) )
+ *   q(o, D) = rn_uint64( 2^52 * exp(-|o|^2 / sigma_i^2) * exp(-(sqrt(D)/N_l) / sigma_s^2) )
  *   D_l(p,q) = sum_i (c_l,p,i - c_l,q,i)^2 = N_l^2 ||e_p - e_q||^2   (exact integer)
  * Defaults 2.1, 1.0, 7.  radius in [1, 7] (the stride-8 colouring needs R < 8); sigmas > 0. */
 int bn_set_energy(bn_ctx *ctx, double sigma_i, double sigma_s, int32_t radius);
@@ -103,7 +103,7 @@ int bn_get_tile(bn_ctx *ctx, uint32_t *u_xy, int is_device);
 int bn_eval_counts(bn_ctx *ctx, uint8_t *out, int is_device);
 
 /* Energy of the current tile, recomputed from the counts (not incremental).
- * E_fixed[0..1] = (low, high) 64-bit words of the exact uint128 sum; *E = E_fixed * 2^-64.
+ * E_fixed[0..1] = (low, high) 64-bit words of the exact uint128 sum; *E = E_fixed * 2^-52.
  * Either pointer may be NULL.  Multi-GPU: collective over the communicator. */
 int bn_energy(bn_ctx *ctx, double *E, uint64_t E_fixed[2]);
 
@@ -124,7 +124,7 @@ typedef struct {
 typedef struct {
     uint32_t accepted;   /* candidates (REDRAW) or couples (SWAP, PAPER_SWAP) accepted      */
     uint32_t proposed;   /* candidates (= L*L), couples (= L*L/2) or budget/2 evaluated    */
-    double E;            /* E_fixed * 2^-64 after the pass                                */
+    double E;            /* E_fixed * 2^-52 after the pass                                */
     uint64_t E_fixed[2]; /* exact energy after the pass (uint128, low word first)          */
     uint64_t dE_sum[2];  /* exact sum of the accepted dE (int128, two's complement)        */
 } bn_pass_stats;

@@ -187,7 +187,7 @@ double orc_iref(int32_t a, int32_t b, uint32_t PX, uint32_t PY) {
  *   w(o)   = exp(-|o|^2 / sigma_i^2)
  *   g_N(D) = exp(-(sqrt(D) / N) / sigma_s^2),   ||e_p - e_q|| = sqrt(D)/N exactly, because
  *            e = c/N - I_ref and I_ref cancels;  D = sum_i (c_p,i - c_q,i)^2  (integer)
- *   q(o,D) = round-to-nearest( 2^64 * (w(o) * g_N(D)) )           (uint64 fixed point)
+ *   q(o,D) = round-to-nearest( 2^52 * (w(o) * g_N(D)) )           (uint64 fixed point, R15)
  *   E_fix  = sum_l sum_p sum_{o in O} q(o, D_l(p, p+o mod L))      (uint128, exact)
  * --------------------------------------------------------------------------------------- */
 static double w_of(const orc_problem *pb, int ox, int oy) {
@@ -202,7 +202,7 @@ static double g_of(const orc_problem *pb, uint64_t D, uint32_t N) {
 }
 uint64_t orc_q(const orc_problem *pb, int ox, int oy, uint64_t D, uint32_t N) {
     double v = w_of(pb, ox, oy) * g_of(pb, D, N);
-    return (uint64_t)nearbyint(ldexp(v, 64));
+    return (uint64_t)nearbyint(ldexp(v, 52));
 }
 
 /* D_l(p,q) from two count rows of length T (the plain definition). */
@@ -217,7 +217,7 @@ static uint64_t dist2(const uint8_t *cp, const uint8_t *cq, uint32_t T) {
 
 static uint32_t wrap(int64_t v, uint32_t L) { return (uint32_t)(((v % (int64_t)L) + L) % L); }
 
-/* E over counts c[l][p][i]; Efix as (lo, hi) of a uint128; Eplain: the same sum in fp64,
+/* E over counts c[l][p][i]; Efix as (lo, hi) of a uint128 (E = Efix * 2^-52); Eplain: the same sum in fp64,
  * accumulated sequentially in raster x window order. */
 void orc_energy(const orc_problem *pb, const uint8_t *c, uint64_t Efix[2], double *Eplain) {
     const uint32_t L = pb->L, P = L * L, T = pb->T;

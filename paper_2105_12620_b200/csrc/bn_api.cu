@@ -157,7 +157,6 @@ struct bn_ctx {
     DevBuf<int4> Dt;
     DevBuf<long long> d0, d1b;   // int64 dE terms (DT_ESC = see escape tables)
     DevBuf<longlong2> x0, x1;    // exact int128 escape tables (sparse writes)
-    bool force_escape = false;   // BN_DT_ESCAPE=1: every term through the escape tables (tests)
     DevBuf<i128> dEp;
     DevBuf<u128> Epart;
     DevBuf<PassStatsDev> pstats;
@@ -380,8 +379,6 @@ int ensure_work(bn_ctx* ctx) {
     CUDA_TRY(ctx->Dt.ensure(P * H * ctx->nl));  // two int2 planes over [l][p][padded h]
     CUDA_TRY(ctx->d0.ensure(P * WN));
     CUDA_TRY(ctx->d1b.ensure(P * WN));
-    CUDA_TRY(ctx->x0.ensure(P * WN));
-    CUDA_TRY(ctx->x1.ensure(P * WN));
     CUDA_TRY(ctx->acc.ensure(P));
     CUDA_TRY(ctx->dEp.ensure(P));
     CUDA_TRY(ctx->Epart.ensure((P * H + 255) / 256));
@@ -514,8 +511,7 @@ int launch_lut_only(bn_ctx* ctx, int write_deltas) {
     {
         auto fn = ctx->nl == 4 ? k_lut<R, 4> : ctx->nl == 1 ? k_lut<R, 1> : k_lut<R, 0>;
         fn<<<(unsigned)((nthr + 255) / 256), 256, 0, ctx->ls>>>(ctx->Dt.p, ctx->L, ctx->nl, ctx->W.p, la, write_deltas,
-                                                              ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p,
-                                                              (int)ctx->force_escape, ctx->Epart.p, ctx->derr.p);
+                                                              ctx->d0.p, ctx->d1b.p, ctx->Epart.p, ctx->derr.p);
     }
     LAUNCHED_K();
     return BN_OK;
@@ -719,7 +715,8 @@ int read_err_flag(bn_ctx* ctx) {
     int h = 0;
     CUDA_TRY(cudaMemcpyAsync(&h, ctx->derr.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (h) return fail(ctx, BN_ESTATE, "internal invariant failed: window distance outside [0, T N^2]");
+    if (h & 1) return fail(ctx, BN_ESTATE, "internal invariant failed: window distance outside [0, T N^2]");
+    if (h) return fail(ctx, BN_ESTATE, "internal invariant failed: dE term outside +-2^55");
     return BN_OK;
 }
 
@@ -774,8 +771,6 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
             return BN_ECUDA;
         }
     }
-    const char* esc = getenv("BN_DT_ESCAPE");
-    ctx->force_escape = esc && !strcmp(esc, "1");
     const char* gm = getenv("BN_GRAM");
     ctx->simt_gram = gm && !strcmp(gm, "simt");
     ctx->imma_v1 = gm && !strcmp(gm, "imma1");
@@ -993,7 +988,7 @@ int bn_energy(bn_ctx* ctx, double* E, uint64_t E_fixed[2]) {
         E_fixed[0] = h.E_before[0];
         E_fixed[1] = h.E_before[1];
     }
-    if (E) *E = std::ldexp((double)h.E_before[1], 0) + std::ldexp((double)h.E_before[0], -64);
+    if (E) *E = std::ldexp((double)h.E_before[1], 64 - BN_FIX_BITS) + std::ldexp((double)h.E_before[0], -BN_FIX_BITS);
     return BN_OK;
 }
 
@@ -1190,7 +1185,8 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
                 stats[pi].proposed = paper ? ncp : prm->mode == BN_SWAP ? P / 2 : P;
                 stats[pi].E_fixed[0] = h[pi].E_after[0];
                 stats[pi].E_fixed[1] = h[pi].E_after[1];
-                stats[pi].E = std::ldexp((double)h[pi].E_after[1], 0) + std::ldexp((double)h[pi].E_after[0], -64);
+                stats[pi].E = std::ldexp((double)h[pi].E_after[1], 64 - BN_FIX_BITS) +
+                             std::ldexp((double)h[pi].E_after[0], -BN_FIX_BITS);
                 stats[pi].dE_sum[0] = h[pi].dE_sum[0];
                 stats[pi].dE_sum[1] = h[pi].dE_sum[1];
             }

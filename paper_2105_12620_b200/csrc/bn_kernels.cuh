@@ -1833,25 +1833,24 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc5(const __grid_const
 }
 
 // -------------------------------------------------------------------------- energy terms
-// q(o, D) = rn_u64(2^64 * W[o] * G_l[D]); W and G are host-built fp64 tables (exp/sqrt of the
-// host libm), the product is one IEEE multiply (no contraction possible), the scaling by 2^64
-// is exact.
+// q(o, D) = rn_u64(2^52 * W[o] * G_l[D]); W and G are host-built fp64 tables (exp/sqrt of the
+// host libm), the product is one IEEE multiply (no contraction possible), the scaling by 2^52
+// is exact (reading R15).  With q < 2^52, every dE term (a sum over <= 8 levels of differences of
+// two q's) satisfies |term| < 2^55, and every window sum of <= 224 terms |sum| < 2^63: int64 is
+// exact throughout the decisions.
+constexpr int BN_FIX_BITS = 52;  // E = E_fixed * 2^-52
 __device__ __forceinline__ unsigned long long qterm(double w, const double* __restrict__ G, int D) {
-    return __double2ull_rn(__dmul_rn(__dmul_rn(w, __ldg(G + D)), 18446744073709551616.0));
+    return __double2ull_rn(__dmul_rn(__dmul_rn(w, __ldg(G + D)), 4503599627370496.0));
 }
 
-// dE terms are stored as int64 when the exact int128 value fits (the common case); otherwise the
-// int64 slot holds the sentinel DT_ESC and the exact value goes to the int128 escape table at the
-// same index (written only then).  Halves the bytes the decisions stage per colour class.
+// dE terms are int64 (exact, see above).  The int128 escape machinery of earlier versions (a
+// sentinel plus a side table for terms beyond int64) is unreachable with the 2^52 scale; the
+// invariant |term| < 2^55 is checked here (err flag 2).
 constexpr long long DT_ESC = (long long)0x8000000000000000ull;
-__device__ __forceinline__ void put_term(long long* d, longlong2* x, size_t idx, i128 v, int force) {
-    const bool fits = v > (i128)DT_ESC && v <= (i128)0x7fffffffffffffffll;
-    if (fits && !force) {
-        d[idx] = (long long)v;
-    } else {
-        d[idx] = DT_ESC;
-        x[idx] = make_longlong2((long long)(unsigned long long)v, (long long)(v >> 64));
-    }
+constexpr long long TERM_MAX = 1ll << 55;
+__device__ __forceinline__ void put_term(long long* d, size_t idx, i128 v, int* err) {
+    if (v >= (i128)TERM_MAX || v <= -(i128)TERM_MAX) atomicOr(err, 2);
+    d[idx] = (long long)v;
 }
 __device__ __forceinline__ i128 get_term(long long v, const longlong2* __restrict__ x, size_t idx) {
     if (v != DT_ESC) return (i128)v;
@@ -1903,7 +1902,6 @@ template <int R, int NL>
 __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32_t L, uint32_t nl_rt,
                                              const double* __restrict__ W, LutArgs lut, int write_deltas,
                                              long long* __restrict__ d0, long long* __restrict__ d1,
-                                             longlong2* __restrict__ x0, longlong2* __restrict__ x1, int force_escape,
                                              u128* __restrict__ Epart, int* __restrict__ err) {
     constexpr int HP = half_count_padded(R), R0 = ru4(R), RW = ru4(2 * R + 1);
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
@@ -1951,10 +1949,10 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
         }
         e *= 2;  // ordered pairs (p,q) and (q,p)
         if (write_deltas) {
-            put_term(d0, x0, (size_t)p * WN + wi, a0, force_escape);
-            put_term(d1, x1, (size_t)p * WN + wi, a1, force_escape);
-            put_term(d0, x0, (size_t)q * WN + wm, b0, force_escape);
-            put_term(d1, x1, (size_t)q * WN + wm, b1, force_escape);
+            put_term(d0, (size_t)p * WN + wi, a0, err);
+            put_term(d1, (size_t)p * WN + wi, a1, err);
+            put_term(d0, (size_t)q * WN + wm, b0, err);
+            put_term(d1, (size_t)q * WN + wm, b1, err);
         }
     }
     // block reduction of e (u128): exact REDUX warp sums, then the 8 warp partials
@@ -2356,32 +2354,24 @@ struct WinTermsFlags32 : WinTerms<R> {
             }
         }
     }
+    // exact int64 window sum (|term| < 2^55, <= 224 terms: |sum| < 2^63), warp-reduced in int64
     __device__ __forceinline__ i128 sum_flags(const uint32_t* sflags, uint32_t L, uint32_t p,
                                               const LaneOffsets<R>& off, const DTabs T) const {
         constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
         const int lane = threadIdx.x & 31;
-        const uint32_t x = p & (L - 1), y = p / L;
-        i128 acc = 0;
+        const uint32_t x = p & (L - 1), y = p & ~(L - 1);
+        long long acc = 0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int w = lane + 32 * j;
             if (w < WN) {
-                const uint32_t q = ((y + off.oy[j]) & (L - 1)) * L + ((x + off.ox[j]) & (L - 1));
-                const bool f = sflags[q] != 0;
-                const long long v = f ? this->v1[j] : this->v0[j];
-                if (v != DT_ESC) {
-                    acc += (i128)v;
-                } else {  // rare: exact int128 term from the escape table
-                    const longlong2 e = (f ? T.x1 : T.x0)[(size_t)p * WN + w];
-                    acc += ((i128)e.y << 64) | (u128)(unsigned long long)e.x;
-                }
+                const uint32_t q = ((y + (uint32_t)off.oy[j] * L) & (L * L - 1)) + ((x + off.ox[j]) & (L - 1));
+                acc += sflags[q] != 0 ? this->v1[j] : this->v0[j];
             }
         }
-#ifndef BN_DEC_RED
-#define BN_DEC_RED 1
-#endif
-        if (BN_DEC_RED) return (i128)warp_sum_u128((u128)acc);
-        return warp_sum_i128_redux((unsigned long long)acc, (unsigned long long)(acc >> 64));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        return (i128)acc;
     }
 };
 

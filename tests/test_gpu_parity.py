@@ -311,18 +311,6 @@ def test_tc_gram_optimize_parity(bn, oracle_mod, monkeypatch, variant):
 
 
 @pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags", "per_class", "swap3"])
-def test_escape_path_all_terms(bn, oracle_mod, monkeypatch, decide):
-    """dE terms are int64 with an int128 escape; forcing every term through the escape tables
-    (BN_DT_ESCAPE=1) must give the same bit-exact passes on every decision kernel."""
-    monkeypatch.setenv("BN_DT_ESCAPE", "1")
-    monkeypatch.setenv("BN_DECIDE", decide)
-    s, o, U = make(bn, oracle_mod, 32, 100, (4, 16))
-    _check_run(s, o, U, 2, 0, seed=13)
-    s2, o2, U2 = make(bn, oracle_mod, 32, 60, (4,))
-    _check_run(s2, o2, U2, 2, 1, seed=14)
-
-
-@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags", "swap3"])
 @pytest.mark.parametrize("L,mode", [(16, 0), (16, 1), (32, 1), (64, 1), (128, 0), (128, 1)])
 def test_decide_kernels_parity(bn, oracle_mod, monkeypatch, decide, L, mode):
     """Every persistent decision kernel (register-prefetched cluster v3 = default, SWAP per-member
@@ -377,8 +365,7 @@ def test_paper_mode_parity(bn, oracle_mod, L, T, levels, budget):
     _check_paper_run(s, o, U, 6, seed=17, budget=budget)
 
 
-def test_paper_mode_resume_escape_and_errors(bn, oracle_mod, monkeypatch):
-    monkeypatch.setenv("BN_DT_ESCAPE", "1")
+def test_paper_mode_resume_and_errors(bn, oracle_mod):
     s, o, U = make(bn, oracle_mod, 32, 60, (4, 16))
     _check_paper_run(s, o, U, 3, seed=5, first_pass=4)
     s2, _, _ = make(bn, oracle_mod, 16, 8, (4,))

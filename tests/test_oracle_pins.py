@@ -14,6 +14,7 @@ import synth
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 TWO32 = 1 << 32
+FIX = 2**52          # fixed-point scale of the energy terms (reading R15)
 
 
 # --------------------------------------------------------------------------------- Philox --
@@ -183,7 +184,7 @@ def test_energy_constant_tile(oracle_mod):
     Ef, Ep = pb.energy(pb.counts(U))
     want = 2 * 256 * _sum_w()
     assert abs(Ep - want) < 1e-9 * want
-    assert abs(Ef / 2**64 - want) < 1e-9 * want
+    assert abs(Ef / FIX - want) < 1e-9 * want
     assert abs(_sum_w() - 12.854416027) < 1e-8          # SURVEY §8c value for R=7
 
 
@@ -203,7 +204,7 @@ def test_energy_single_defect_closed_form(oracle_mod):
     want = (256 - 2) * S + 2 * S * g
     Ef, Ep = pb.energy(c)
     assert abs(Ep - want) < 1e-12 * want
-    assert abs(Ef / 2**64 - want) < 1e-12 * want
+    assert abs(Ef / FIX - want) < 1e-12 * want
 
 
 def test_energy_translation_invariant_and_fixed_point(oracle_mod):
@@ -214,7 +215,7 @@ def test_energy_translation_invariant_and_fixed_point(oracle_mod):
     Ut = np.roll(U.reshape(16, 16, 2), (3, -5), axis=(0, 1)).reshape(-1, 2)
     Ef2, Ep2 = pb.energy(pb.counts(Ut))
     assert Ef == Ef2                                       # toroidal window (reading R5)
-    assert abs(Ef / 2**64 - Ep) < 256 * 224 * 2 * 2**-64 + 1e-12 * Ep
+    assert abs(Ef / FIX - Ep) < 256 * 224 * 2 * 2.0**-53 + 1e-12 * Ep
 
 
 # ------------------------------------------------------------------------------ delta E --
@@ -448,7 +449,7 @@ def test_eq1_constant_tile_and_single_defect(oracle_mod, form):
     S = _sum_w()
     Ef, Ep = pb.energy(pb.counts(U))
     want = 0.0 if form == 1 else 2 * 256 * S
-    assert abs(Ep - want) <= 1e-9 * max(want, 1.0) and abs(Ef / 2**64 - want) <= 1e-9 * max(want, 1.0)
+    assert abs(Ep - want) <= 1e-9 * max(want, 1.0) and abs(Ef / FIX - want) <= 1e-9 * max(want, 1.0)
     U[37] = synth.make_tile(1, 5)[0]
     c = pb.counts(U)
     sq = [float((((c[li, 37].astype(int) - c[li, 0].astype(int)) / N) ** 2).sum()) for li, N in enumerate((4, 16))]
@@ -456,7 +457,7 @@ def test_eq1_constant_tile_and_single_defect(oracle_mod, form):
     defect = sum(2 * S * v / T for v in sq)
     want = defect if form == 1 else 2 * 256 * S - defect
     Ef, Ep = pb.energy(c)
-    assert abs(Ep - want) < 1e-12 * 2 * 256 * S and abs(Ef / 2**64 - want) < 1e-9 * 2 * 256 * S
+    assert abs(Ep - want) < 1e-12 * 2 * 256 * S and abs(Ef / FIX - want) < 1e-9 * 2 * 256 * S
 
 
 @pytest.mark.parametrize("form", [1, 2])
