@@ -1848,9 +1848,9 @@ __device__ __forceinline__ unsigned long long qterm(double w, const double* __re
 // invariant |term| < 2^55 is checked here (err flag 2).
 constexpr long long DT_ESC = (long long)0x8000000000000000ull;
 constexpr long long TERM_MAX = 1ll << 55;
-__device__ __forceinline__ void put_term(long long* d, size_t idx, i128 v, int* err) {
-    if (v >= (i128)TERM_MAX || v <= -(i128)TERM_MAX) atomicOr(err, 2);
-    d[idx] = (long long)v;
+__device__ __forceinline__ void put_term(long long* d, size_t idx, long long v, int* err) {
+    if (v >= TERM_MAX || v <= -TERM_MAX) atomicOr(err, 2);
+    d[idx] = v;
 }
 __device__ __forceinline__ i128 get_term(long long v, const longlong2* __restrict__ x, size_t idx) {
     if (v != DT_ESC) return (i128)v;
@@ -1907,7 +1907,7 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     const uint32_t P = L * L;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // (p, padded offset hp)
-    u128 e = 0;
+    unsigned long long e = 0;  // < 2 * 8 * 2^52 = 2^56 per thread, < 2^61 per warp
     const uint32_t p = (uint32_t)(idx / HP), hp = (uint32_t)(idx - (size_t)p * HP);
     int ox, oy;
     if (hp < (uint32_t)R0) {
@@ -1922,7 +1922,8 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
         const uint32_t q = ((y + oy) & (L - 1)) * L + ((x + ox + L) & (L - 1));
         const int wi = win_index(ox, oy, R), wm = win_index(-ox, -oy, R);
         const double w = W[wi];
-        i128 a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+        // q < 2^52: per-level differences and their sums over <= 8 levels are exact in int64 (R15)
+        long long a0 = 0, a1 = 0, b0 = 0, b1 = 0;
         const uint32_t nl = NL ? NL : nl_rt;
         int4 Dv[NL ? NL : 1];
         if (NL) {
@@ -1939,13 +1940,13 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
                 continue;
             }
             const double* G = lut.G[l];
-            const unsigned long long qcc = qterm(w, G, D.x), qcn = qterm(w, G, D.y);
-            const unsigned long long qnc = qterm(w, G, D.z), qnn = qterm(w, G, D.w);
-            e += (u128)qcc;
-            a0 += (i128)qnc - (i128)qcc;  // p takes cn_p, q still c_q
-            a1 += (i128)qnn - (i128)qcn;  // p takes cn_p, q already cn_q
-            b0 += (i128)qcn - (i128)qcc;  // q takes cn_q, p still c_p
-            b1 += (i128)qnn - (i128)qnc;  // q takes cn_q, p already cn_p
+            const long long qcc = (long long)qterm(w, G, D.x), qcn = (long long)qterm(w, G, D.y);
+            const long long qnc = (long long)qterm(w, G, D.z), qnn = (long long)qterm(w, G, D.w);
+            e += (unsigned long long)qcc;
+            a0 += qnc - qcc;  // p takes cn_p, q still c_q
+            a1 += qnn - qcn;  // p takes cn_p, q already cn_q
+            b0 += qcn - qcc;  // q takes cn_q, p still c_p
+            b1 += qnn - qnc;  // q takes cn_q, p already cn_p
         }
         e *= 2;  // ordered pairs (p,q) and (q,p)
         if (write_deltas) {
@@ -1955,15 +1956,18 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
             put_term(d1, (size_t)q * WN + wm, b1, err);
         }
     }
-    // block reduction of e (u128): exact REDUX warp sums, then the 8 warp partials
-    __shared__ u128 swarp[8];
-    const u128 ws = (u128)warp_sum_i128_redux((unsigned long long)e, (unsigned long long)(e >> 64));
+    // block reduction of e: exact warp sums of 16-bit limbs (REDUX), then the 8 warp partials
+    __shared__ unsigned long long swarp[8];
+    unsigned long long ws = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        ws += (unsigned long long)__reduce_add_sync(0xffffffffu, (uint32_t)(e >> (16 * i)) & 0xffffu) << (16 * i);
     if ((threadIdx.x & 31) == 0) swarp[threadIdx.x >> 5] = ws;
     __syncthreads();
     if (threadIdx.x == 0) {
-        u128 s = 0;
-        for (int j = 0; j < (int)(blockDim.x >> 5); ++j) s += swarp[j];
-        Epart[blockIdx.x] = s;
+        u128 t = 0;
+        for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += swarp[j];
+        Epart[blockIdx.x] = t;
     }
 }
 
