@@ -15,5 +15,5 @@ python bench.py --config C5 --steps 5 --warmup 3 --cpu-classes 1 --e2e-steps 2 >
 python bench.py --config C5 --mode swap --steps 5 --warmup 3 --cpu-classes 1 --e2e-steps 2 >> $out 2> gpurun_out/bench_C5s.err; echo C5s rc=$?
 python bench.py --impl reference --steps 5 --warmup 3 >> $out 2> gpurun_out/bench_ref.err; echo ref rc=$?
 nproc; lscpu | grep "Model name"
-bash tools/gpu_ncu_multi.sh r01s k_gram_tc4 k_decide_swap k_lut k_paper_gather k_swap_gather k_finish
+bash tools/gpu_ncu_multi.sh r01t k_gram_tc4 k_decide_swap k_lut k_paper_gather k_finish
 ls gpurun_out
