@@ -289,6 +289,19 @@ struct DeviceGuard {
     }
 };
 
+// Launch through cudaLaunchKernelEx (typed arguments).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bn_ctx* ctx, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    (void)ctx;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 uint32_t round_up(uint32_t v, uint32_t m) { return (v + m - 1) / m * m; }
 bool pow2(uint32_t v) { return v && !(v & (v - 1)); }
 int half_count(int R) { return 2 * R * R + 2 * R; }
@@ -434,8 +447,8 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
             const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
             const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
-            k_gram_tc4<<<grid, tc3::THREADS, smem, ctx->ls>>>(mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p,
-                                                              ctx->gram_rows, ctx->gram_rows_target);
+            CUDA_TRY(launch_k(ctx, k_gram_tc4, dim3(grid), dim3(tc3::THREADS), smem, ctx->ls, mc, mn, ctx->nc.p, nn, ctx->L,
+                              ctx->Tp, ctx->nl, ctx->Dt.p, ctx->gram_rows, ctx->gram_rows_target));
         } else {
             k_gram_tc3<<<dim3(ctx->L / 8, ctx->L / 8, ctx->nl), tc3::THREADS, smem, ctx->ls>>>(
                 mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
@@ -510,8 +523,8 @@ int launch_lut_only(bn_ctx* ctx, int write_deltas) {
     KSTART(BN_K_LUT);
     {
         auto fn = ctx->nl == 4 ? k_lut<R, 4> : ctx->nl == 1 ? k_lut<R, 1> : k_lut<R, 0>;
-        fn<<<(unsigned)((nthr + 255) / 256), 256, 0, ctx->ls>>>(ctx->Dt.p, ctx->L, ctx->nl, ctx->W.p, la, write_deltas,
-                                                              ctx->d0.p, ctx->d1b.p, ctx->Epart.p, ctx->derr.p);
+        CUDA_TRY(launch_k(ctx, fn, dim3((unsigned)((nthr + 255) / 256)), dim3(256), 0, ctx->ls, ctx->Dt.p, ctx->L, ctx->nl,
+                          ctx->W.p, la, write_deltas, ctx->d0.p, ctx->d1b.p, ctx->Epart.p, ctx->derr.p));
     }
     LAUNCHED_K();
     return BN_OK;
@@ -1025,6 +1038,8 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     CUDA_TRY(ctx->fparts.ensure(nfin));
     if (accept_log) CUDA_TRY(ctx->log.ensure((size_t)prm->passes * 64 * M));
     CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
+    // accept flags start at zero; k_finish clears them again after every pass
+    CUDA_TRY(cudaMemsetAsync(ctx->acc.p, 0, P, ctx->stream));
     const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
     const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
     // Candidate buffers are double-buffered so that the REDRAW candidates of pass t+1 (which do
@@ -1074,7 +1089,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     for (uint32_t pi = 0; pi < prm->passes; ++pi) {
         const uint32_t t = prm->first_pass + pi;
         ctx->ls = cs;
-        CUDA_TRY(cudaMemsetAsync(ctx->acc.p, 0, P, cs));
+
         if (paper) {
             // couples of pass t -> partner map -> gathered partner rows; dEp is only written for
             // couple members, so it is cleared for the exact pass sums of k_finish
@@ -1098,10 +1113,12 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
                 k_swap_gather<<<64 * M, 128, 0, cs>>>(ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p, ctx->nc.p, ctx->nn.p,
                                                      ctx->L, prm->seed, t, ctx->rowB, nl);
             } else {
-                k_swap_pairs<<<(64 * M + 255) / 256, 256, 0, cs>>>(ctx->L, prm->seed, t, ctx->part.p);
+                CUDA_TRY(launch_k(ctx, k_swap_pairs, dim3((64 * M + 255) / 256), dim3(256), 0, cs, ctx->L, prm->seed, t,
+                                  ctx->part.p));
                 LAUNCHED();
-                k_paper_gather<<<(P + 7) / 8, 256, 0, cs>>>(ctx->part.p, ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p,
-                                                            ctx->nc.p, ctx->nn.p, P, ctx->rowB, nl);
+                CUDA_TRY(launch_k(ctx, k_paper_gather, dim3((P + 7) / 8), dim3(256), 0, cs, (const uint32_t*)ctx->part.p,
+                                  (const uint2*)ctx->U.p, ctx->Un.p, (const uint8_t*)ctx->c.p, ctx->cn.p,
+                                  (const int*)ctx->nc.p, ctx->nn.p, P, ctx->rowB, nl));
             }
             LAUNCHED_K();
         }
@@ -1144,9 +1161,10 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             for (uint32_t s = 0; s < 64; ++s)
                 if ((rc = decide(ctx, s, t, prm->seed, (int)prm->mode, log))) return rc;
         KSTART(BN_K_COMMIT);
-        k_finish<<<nfin, 256, 0, cs>>>(ctx->acc.p, P, ctx->rowB, nl, buf_U(pi), ctx->U.p, buf_c(pi), ctx->c.p,
-                                        buf_n(pi), ctx->nc.p, ctx->Epart.p, nE, ctx->dEp.p, prm->mode != BN_REDRAW,
-                                        ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi);
+        CUDA_TRY(launch_k(ctx, k_finish, dim3(nfin), dim3(256), 0, cs, (const uint8_t*)ctx->acc.p, P, ctx->rowB, nl,
+                          (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
+                          ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, (int)(prm->mode != BN_REDRAW),
+                          ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi));
         LAUNCHED_K();
     }
     if (overlap) {

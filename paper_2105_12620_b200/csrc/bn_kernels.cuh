@@ -2768,7 +2768,11 @@ __global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc,
     }
     __shared__ FinishPart s_w[32];
     __shared__ bool last;
-    FinishPart mine = block_sum_parts(e, (u128)d, a, s_w);
+    FinishPart mine = block_sum_parts(e, (u128)d, a, s_w);  // (contains __syncthreads: commit reads done)
+    // the next pass starts from all-zero accept flags (the per-class / flag-kernel decisions read
+    // undecided neighbours' flags from acc)
+    uint8_t* accw = const_cast<uint8_t*>(acc);
+    for (uint32_t j = p0 + threadIdx.x; j < p1; j += blockDim.x) accw[j] = 0;
     if (threadIdx.x == 0) {
         parts[b] = mine;
         __threadfence();
