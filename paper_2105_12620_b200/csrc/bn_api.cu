@@ -199,6 +199,7 @@ struct bn_ctx {
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
     bool cluster_v2 = false;  // BN_DECIDE=cluster2: shared-memory-staged rows (v2)
+    bool no_fuse = false;          // BN_FUSE=0: separate SWAP commit (k_finish) and gather kernels
     bool old_swap_gather = false;  // BN_GATHER=old: k_swap_gather (one Philox per copying thread)
     bool swap_v3 = false;     // BN_DECIDE=swap3: SWAP on k_decide_cl3 (one warp per couple) instead of k_decide_swap
     // per-kernel event timing (bn_profile_*)
@@ -758,6 +759,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->cluster_v1 = dm && !strcmp(dm, "cluster1");
     ctx->cluster_v2 = dm && !strcmp(dm, "cluster2");
     ctx->swap_v3 = dm && !strcmp(dm, "swap3");
+    const char* fu = getenv("BN_FUSE");
+    ctx->no_fuse = fu && !strcmp(fu, "0");
     const char* gth = getenv("BN_GATHER");
     ctx->old_swap_gather = gth && !strcmp(gth, "old");
     const char* ov = getenv("BN_OVERLAP");
@@ -1051,9 +1054,18 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         CUDA_TRY(ctx->cn2.ensure((size_t)P * ctx->rowB));
         CUDA_TRY(ctx->nn2.ensure((size_t)P * nl));
     }
-    auto buf_U = [&](uint32_t pi) { return (overlap && (pi & 1)) ? ctx->Un2.p : ctx->Un.p; };
-    auto buf_c = [&](uint32_t pi) { return (overlap && (pi & 1)) ? ctx->cn2.p : ctx->cn.p; };
-    auto buf_n = [&](uint32_t pi) { return (overlap && (pi & 1)) ? ctx->nn2.p : ctx->nn.p; };
+    // SWAP: the commit of pass t and the gather of pass t+1 run as one kernel (k_finish_gather), which
+    // writes the next candidates into the other buffer of the pair
+    const bool fuse = prm->mode == BN_SWAP && !ctx->no_fuse && !ctx->old_swap_gather && prm->passes > 1;
+    if (fuse) {
+        CUDA_TRY(ctx->Un2.ensure(P));
+        CUDA_TRY(ctx->cn2.ensure((size_t)P * ctx->rowB));
+        CUDA_TRY(ctx->nn2.ensure((size_t)P * nl));
+    }
+    const bool dbl = overlap || fuse;
+    auto buf_U = [&](uint32_t pi) { return (dbl && (pi & 1)) ? ctx->Un2.p : ctx->Un.p; };
+    auto buf_c = [&](uint32_t pi) { return (dbl && (pi & 1)) ? ctx->cn2.p : ctx->cn.p; };
+    auto buf_n = [&](uint32_t pi) { return (dbl && (pi & 1)) ? ctx->nn2.p : ctx->nn.p; };
     // Row flags: with the persistent tcgen05 Gram, pass t's Gram follows its candidate counts row by
     // row (k_counts publishes each finished tile-row segment, k_gram_tc4 waits per item), so the
     // counts of pass t+1 may still be finishing when the Gram of pass t+1 starts.
@@ -1107,6 +1119,8 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             } else if ((rc = launch_counts(pi))) {
                 return rc;
             }
+        } else if (fuse && pi > 0) {
+            // candidates gathered by k_finish_gather of pass pi - 1
         } else {
             KSTART(BN_K_GATHER);
             if (ctx->old_swap_gather) {
@@ -1117,8 +1131,8 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
                                   ctx->part.p));
                 LAUNCHED();
                 CUDA_TRY(launch_k(ctx, k_paper_gather, dim3((P + 7) / 8), dim3(256), 0, cs, (const uint32_t*)ctx->part.p,
-                                  (const uint2*)ctx->U.p, ctx->Un.p, (const uint8_t*)ctx->c.p, ctx->cn.p,
-                                  (const int*)ctx->nc.p, ctx->nn.p, P, ctx->rowB, nl));
+                                  (const uint2*)ctx->U.p, buf_U(pi), (const uint8_t*)ctx->c.p, buf_c(pi),
+                                  (const int*)ctx->nc.p, buf_n(pi), P, ctx->rowB, nl));
             }
             LAUNCHED_K();
         }
@@ -1160,6 +1174,19 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         if (!done)
             for (uint32_t s = 0; s < 64; ++s)
                 if ((rc = decide(ctx, s, t, prm->seed, (int)prm->mode, log))) return rc;
+        if (fuse && pi + 1 < prm->passes) {
+            CUDA_TRY(launch_k(ctx, k_swap_pairs, dim3((64 * M + 255) / 256), dim3(256), 0, cs, ctx->L, prm->seed, t + 1,
+                              ctx->part.p));
+            LAUNCHED();
+            KSTART(BN_K_COMMIT);
+            CUDA_TRY(launch_k(ctx, k_finish_gather, dim3(nfin), dim3(1024), 0, cs, ctx->acc.p, P, ctx->rowB, nl,
+                              (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
+                              ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, ctx->fparts.p,
+                              ctx->ticket.p, ctx->pstats.p + pi, (const uint32_t*)ctx->part.p, buf_U(pi + 1),
+                              buf_c(pi + 1), buf_n(pi + 1)));
+            LAUNCHED_K();
+            continue;
+        }
         KSTART(BN_K_COMMIT);
         CUDA_TRY(launch_k(ctx, k_finish, dim3(nfin), dim3(256), 0, cs, (const uint8_t*)ctx->acc.p, P, ctx->rowB, nl,
                           (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),

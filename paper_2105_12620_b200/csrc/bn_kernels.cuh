@@ -3015,6 +3015,90 @@ __global__ void __launch_bounds__(256) k_ev_spectrum(const double* __restrict__ 
     }
 }
 
+// SWAP pass epilogue fused with the next pass's gather: one warp per pixel p
+//   commit:  acc[p] -> c_p <- cn_p, U_p <- Un_p, nc_p <- nn_p                    (this pass)
+//   gather:  cn2_p <- row of src = part_next[p] in its post-commit state          (next pass)
+//            = acc[src] ? cn_src : c_src  (c_src is only written here when acc[src], so every read
+//            sees either an untouched c row or the candidate row: no ordering between warps needed)
+// plus the exact pass sums of k_finish (per-block partials, last-block reduction), which also
+// clears the accept flags once every block has read them.
+__global__ void __launch_bounds__(1024) k_finish_gather(uint8_t* __restrict__ acc, uint32_t P, uint32_t rowB,
+                                                       uint32_t nl, const uint2* __restrict__ Un, uint2* __restrict__ U,
+                                                       const uint8_t* __restrict__ cn, uint8_t* __restrict__ c,
+                                                       const int* __restrict__ nn, int* __restrict__ nc,
+                                                       const u128* __restrict__ Epart, uint32_t nEpart,
+                                                       const i128* __restrict__ dEp,
+                                                       FinishPart* __restrict__ parts, unsigned int* __restrict__ ticket,
+                                                       PassStatsDev* __restrict__ out,
+                                                       const uint32_t* __restrict__ part_next, uint2* __restrict__ Un2,
+                                                       uint8_t* __restrict__ cn2, int* __restrict__ nn2) {
+    const uint32_t nblk = gridDim.x, b = blockIdx.x;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const uint32_t n16 = rowB / 16;
+    const uint32_t p0 = (uint32_t)((uint64_t)P * b / nblk), p1 = (uint32_t)((uint64_t)P * (b + 1) / nblk);
+    for (uint32_t p = p0 + warp; p < p1; p += nw) {
+        if (acc[p]) {
+            const uint4* src = reinterpret_cast<const uint4*>(cn + (size_t)p * rowB);
+            uint4* dst = reinterpret_cast<uint4*>(c + (size_t)p * rowB);
+            for (uint32_t j = lane; j < n16; j += 32) dst[j] = src[j];
+            if (lane == 0) U[p] = Un[p];
+            if (lane < nl) nc[(size_t)p * nl + lane] = nn[(size_t)p * nl + lane];
+        }
+        const uint32_t q = part_next[p];
+        const bool a = acc[q] != 0;
+        const uint4* src = reinterpret_cast<const uint4*>((a ? cn : c) + (size_t)q * rowB);
+        uint4* dst = reinterpret_cast<uint4*>(cn2 + (size_t)p * rowB);
+        for (uint32_t j = lane; j < n16; j += 32) dst[j] = src[j];
+        if (lane == 0) Un2[p] = a ? Un[q] : U[q];
+        if (lane < nl) nn2[(size_t)p * nl + lane] = a ? nn[(size_t)q * nl + lane] : nc[(size_t)q * nl + lane];
+    }
+    // exact partial sums (this block's pixels, its share of Epart)
+    u128 e = 0;
+    i128 d = 0;
+    unsigned na = 0;
+    const uint32_t e0 = (uint32_t)((uint64_t)nEpart * b / nblk), e1 = (uint32_t)((uint64_t)nEpart * (b + 1) / nblk);
+    for (uint32_t j = e0 + threadIdx.x; j < e1; j += blockDim.x) e += Epart[j];
+    for (uint32_t j = p0 + threadIdx.x; j < p1; j += blockDim.x) {
+        d += dEp[j];
+        na += acc[j];
+    }
+    __shared__ FinishPart s_w[32];
+    __shared__ bool last;
+    FinishPart mine = block_sum_parts(e, (u128)d, na, s_w);
+    if (threadIdx.x == 0) {
+        parts[b] = mine;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == nblk - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    u128 E = 0, D = 0;
+    unsigned A = 0;
+    for (uint32_t j = threadIdx.x; j < nblk; j += blockDim.x) {
+        const unsigned long long* qq = reinterpret_cast<const unsigned long long*>(parts + j);
+        E += ((u128)__ldcg(qq + 1) << 64) | __ldcg(qq + 0);
+        D += ((u128)__ldcg(qq + 3) << 64) | __ldcg(qq + 2);
+        A += (unsigned)__ldcg(qq + 4);
+    }
+    const FinishPart tot = block_sum_parts(E, D, A, s_w);
+    // every block has read its accept flags (and every gather its sources'): clear them for the
+    // next pass's decisions (uint4 stores; P is a multiple of 256)
+    for (uint32_t j = threadIdx.x; j < P / 16; j += blockDim.x) reinterpret_cast<uint4*>(acc)[j] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        const u128 Et = ((u128)tot.e[1] << 64) | tot.e[0], Dt = ((u128)tot.d[1] << 64) | tot.d[0];
+        const u128 Ea = Et + Dt;
+        out->E_before[0] = tot.e[0];
+        out->E_before[1] = tot.e[1];
+        out->E_after[0] = (unsigned long long)Ea;
+        out->E_after[1] = (unsigned long long)(Ea >> 64);
+        out->dE_sum[0] = tot.d[0];
+        out->dE_sum[1] = tot.d[1];
+        out->accepted = tot.a / 2;
+        *ticket = 0;
+    }
+}
+
 // --------------------------------------------------------------------------- I_ref, readback
 // Area of {(x,y) in [0,1]^2 : a(x - px) + b(y - py) >= 0}: the unit square clipped by the
 // half-plane (walk the 4 edges, keep inside vertices and edge crossings), shoelace area. fp64.

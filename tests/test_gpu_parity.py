@@ -108,11 +108,13 @@ def test_c1_shape_full_run(bn, oracle_mod, mode):
     assert st[-1]["E_fixed"] < st[0]["E_fixed"] + (-st[0]["dE_sum"])
 
 
-@pytest.mark.parametrize("gather", ["", "old"])
+@pytest.mark.parametrize("gather", ["", "old", "nofuse"])
 def test_c2_shape_swap(bn, oracle_mod, monkeypatch, gather):
-    """C2 shape (SWAP, 4 spp) at 32x32, T=100 (ragged); partner map + warp gather (default) and the
-    one-CTA-per-pixel gather (BN_GATHER=old)."""
-    monkeypatch.setenv("BN_GATHER", gather)
+    """C2 shape (SWAP, 4 spp) at 32x32, T=100 (ragged): commit fused with the next pass's partner
+    gather (default), separate partner-map gather + commit (BN_FUSE=0), one-CTA-per-pixel gather
+    (BN_GATHER=old)."""
+    monkeypatch.setenv("BN_GATHER", "old" if gather == "old" else "")
+    monkeypatch.setenv("BN_FUSE", "0" if gather == "nofuse" else "1")
     s, o, U = make(bn, oracle_mod, 32, 100, (4,))
     _check_run(s, o, U, 6, 1, seed=5)
 
