@@ -2064,7 +2064,8 @@ struct WinTerms {
             }
         }
     }
-    // sum_w (acc[p + o_w] ? d1 : d0), reduced over the warp (every lane gets the total)
+    // sum_w (acc[p + o_w] ? d1 : d0), reduced over the warp (every lane gets the total); exact in
+    // int64 (R15: |term| < 2^55, |sum| < 2^63)
     __device__ __forceinline__ i128 sum(const uint8_t* acc, uint32_t L, uint32_t p, const DTabs T) const {
         const int lane = threadIdx.x & 31;
         const uint32_t x = p % L, y = p / L;
@@ -2080,22 +2081,15 @@ struct WinTerms {
                 f[j] = __ldcg(acc + q);
             }
         }
-        i128 s = 0;
+        long long s = 0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int w = lane + 32 * j;
-            if (w < WN) {
-                const size_t idx = (size_t)p * WN + w;
-                s += f[j] ? get_term(v1[j], T.x1, idx) : get_term(v0[j], T.x0, idx);
-            }
+            if (w < WN) s += f[j] ? v1[j] : v0[j];
         }
 #pragma unroll
-        for (int off = 16; off; off >>= 1) {
-            const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)s, off);
-            const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(s >> 64), off);
-            s += ((i128)hi << 64) | (u128)lo;
-        }
-        return s;
+        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        return (i128)s;
     }
 };
 
