@@ -196,6 +196,8 @@ struct bn_ctx {
     bool tc3_attr_set = false;
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
+    bool big_attr_set[8] = {false};
+    bool no_big = false;  // BN_DECIDE=nobig: L > 128 tiles use the cooperative flag kernel
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
     bool cluster_v2 = false;  // BN_DECIDE=cluster2: shared-memory-staged rows (v2)
@@ -573,6 +575,54 @@ int launch_decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, 
 // One cooperative launch for all 64 classes (k_decide_pass); co-residency of its CTAs is
 // guaranteed by the cooperative launch, which the neighbour-progress waits require.
 // Cluster launch of k_decide_cluster when the tile's candidate CTAs fit one cluster (<= 16).
+// L = 256, 512: one 16-CTA cluster with `spw` slots per warp and bit flags (k_decide_big).
+template <int R>
+int launch_decide_big(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
+    const uint32_t nb = ctx->L / 8, M = nb * nb, P = ctx->P, ncta = 16, nw = 16;
+    if (M % (ncta * nw) || ctx->no_big || nb > 64) return BN_OK;  // cooperative flag kernel instead
+    uint32_t spw = M / (ncta * nw);
+    if (mode && (spw & 1)) return BN_OK;
+    const uint32_t cpc = nw * spw;
+    const size_t smem = (size_t)P / 8 + (size_t)64 * cpc * 6;
+    if (smem > 220 * 1024) return BN_OK;
+    const void* fn = mode ? (const void*)k_decide_big<R, 1> : (const void*)k_decide_big<R, 0>;
+    if (!ctx->big_attr_set[R]) {
+        for (const void* f : {(const void*)k_decide_big<R, 0>, (const void*)k_decide_big<R, 1>}) {
+            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        }
+        ctx->big_attr_set[R] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncta);
+    cfg.blockDim = dim3(32 * nw);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->ls;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ncta;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 1) {
+        cudaGetLastError();
+        return BN_OK;
+    }
+    uint32_t L = ctx->L;
+    const DTabs T = {ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
+    uint8_t* acc = ctx->acc.p;
+    i128* dEp = ctx->dEp.p;
+    void* args[] = {&t, &seed, &L, &spw, (void*)&T, &acc, &dEp, &log};
+    KSTART(BN_K_DECIDE);
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    if (e != cudaSuccess) return fail(ctx, BN_ECUDA, "big cluster decide launch: %s", cudaGetErrorString(e));
+    LAUNCHED_K();
+    *done = true;
+    return BN_OK;
+}
+
 template <int R>
 int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
@@ -582,7 +632,8 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     while (cpc > nb * nb / (swap_v4 ? 1 : nb)) cpc /= 2;  // at most M slots (SWAP v4) / nb per CTA
     const uint32_t ncta = nb * nb / cpc;
     *done = false;
-    if (ncta > 16 || ctx->no_cluster) return BN_OK;
+    if (ctx->no_cluster) return BN_OK;
+    if (ncta > 16) return launch_decide_big<R>(ctx, t, seed, mode, log, done);
     // v2 (default): u32 flags + slot table; v1 (BN_DECIDE=cluster1): byte flags, cluster barriers
     // v3 (default): register-prefetched rows; v2 (BN_DECIDE=cluster2): rows staged in shared memory
     // by bulk copies; v1 (BN_DECIDE=cluster1): byte flags + a cluster barrier per class
@@ -640,8 +691,16 @@ int launch_decide_pass(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t
     int rc = launch_decide_cluster<R>(ctx, t, seed, mode, log, done);
     if (rc || *done) return rc;
     const uint32_t nb = ctx->L / 8;
-    // candidates per CTA: <= 16 warps (REDRAW) / 8 (SWAP stages the partner too); divides nb
-    uint32_t cpc = mode ? 8 : 16;
+    // SWAP is not safe here: a CTA also reads the window of its candidate's partner, in a band whose
+    // neighbours do not wait for that CTA's progress, so a later class could be decided under the
+    // read (found by test_decide_large_tiles at L = 256).  SWAP tiles beyond the cluster kernels
+    // fall back to the per-class launches.
+    if (mode) {
+        *done = false;
+        return BN_OK;
+    }
+    // candidates per CTA: <= 16 warps; divides nb
+    uint32_t cpc = 16;
     while (cpc > nb) cpc /= 2;
     const uint32_t ncta = nb * nb / cpc;
     const size_t smem = (size_t)(mode ? 2 : 1) * cpc * 2 * WN * 8;
@@ -759,6 +818,7 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->cluster_v1 = dm && !strcmp(dm, "cluster1");
     ctx->cluster_v2 = dm && !strcmp(dm, "cluster2");
     ctx->swap_v3 = dm && !strcmp(dm, "swap3");
+    ctx->no_big = dm && !strcmp(dm, "nobig");
     const char* fu = getenv("BN_FUSE");
     ctx->no_fuse = fu && !strcmp(fu, "0");
     const char* gth = getenv("BN_GATHER");

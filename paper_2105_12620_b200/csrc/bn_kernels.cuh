@@ -2113,7 +2113,8 @@ __device__ __forceinline__ void stage_class(uint32_t smem_base, const uint32_t* 
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// Persistent decision kernel v3: CTA g owns `cpc` consecutive active indices (a contiguous part
+// Persistent decision kernel (REDRAW only; SWAP partners lie in far bands whose readers the
+// progress protocol does not track): CTA g owns `cpc` consecutive active indices (a contiguous part
 // of one band).  For class s it (1) moves the staged dE terms of its candidates from smem to
 // registers, (2) immediately stages class s+1's terms with cp.async (they do not depend on any
 // decision), (3) waits until the CTAs of the neighbouring bands have published progress >= s,
@@ -2621,6 +2622,117 @@ __global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_
             if (log) log[(size_t)s * M + sIdx[s * cpc + warp]] = ok;
         }
         A = An;
+    }
+    tc::mbar_wait(mailbox(63), (63 >> 1) & 1);
+    cluster_sync_all();
+}
+
+// Cluster decisions for tiles with more candidates per class than one 16 x 16-warp cluster has
+// warps (L = 256, 512): every warp owns `spw` consecutive slots of each class (REDRAW: candidates;
+// SWAP: spw/2 whole couples, listed by their lower member, so a warp decides its couples alone),
+// sums them one after another with the next slot's dE rows already in flight, and the pass's accept
+// flags are BITS in shared memory (P/8 bytes: 8 KB for 256^2), broadcast with
+// red.async.or.b32 ... mbarrier::complete_tx (4 bytes of transaction per candidate and CTA, sent
+// whether 0 or 1).  Same mailbox protocol as k_decide_cl3.
+__device__ __forceinline__ void red_async_or(uint32_t local_addr, uint32_t local_bar, uint32_t cta, uint32_t v) {
+    uint32_t ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(cta));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(local_bar), "r"(cta));
+    asm volatile("red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.or.b32 [%0], %1, [%2];" ::"r"(ra),
+                 "r"(v), "r"(rb)
+                 : "memory");
+}
+template <int R>
+struct WinTermsBits : WinTermsFlags32<R> {
+    __device__ __forceinline__ long long sum_bits(const uint32_t* sbits, uint32_t L, uint32_t p,
+                                                  const LaneOffsets<R>& off) const {
+        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
+        const int lane = threadIdx.x & 31;
+        const uint32_t x = p & (L - 1), y = p & ~(L - 1);
+        long long acc = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int w = lane + 32 * j;
+            if (w < WN) {
+                const uint32_t q = ((y + (uint32_t)off.oy[j] * L) & (L * L - 1)) + ((x + off.ox[j]) & (L - 1));
+                acc += (sbits[q >> 5] >> (q & 31)) & 1u ? this->v1[j] : this->v0[j];
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        return acc;
+    }
+};
+template <int R, int mode>
+__global__ void __launch_bounds__(512, 1) k_decide_big(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t spw,
+                                                       const DTabs T, uint8_t* __restrict__ acc,
+                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    __shared__ uint8_t sDelta[8 * 64];
+    __shared__ __align__(8) uint64_t sbar[2];
+    const uint32_t nb = L / 8, M = nb * nb, P = L * L;
+    const uint32_t ncta = gridDim.x, nw = blockDim.x >> 5, cpc = nw * spw;
+    const uint32_t first = blockIdx.x * cpc;  // first slot of this CTA
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* sbits = reinterpret_cast<uint32_t*>(dsm);                 // [P / 32]
+    uint32_t* sSlot = sbits + P / 32;                                   // [64][cpc] pixels
+    uint16_t* sIdx = reinterpret_cast<uint16_t*>(sSlot + 64 * cpc);     // [64][cpc] active indices
+    const uint32_t sbits_addr = (uint32_t)__cvta_generic_to_shared(dsm);
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
+    auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
+    for (uint32_t j = threadIdx.x; j < P / 32; j += blockDim.x) sbits[j] = 0;
+    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
+        sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < 64 * cpc; j += blockDim.x) {
+        const uint32_t s = j / cpc, i = first + (j - s * cpc);
+        const uint32_t m = mode ? couple_member(i >> 1, swap_kappa(seed, pass_t, s, M), i & 1) : i;
+        sSlot[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
+        sIdx[j] = (uint16_t)m;
+    }
+    __syncthreads();
+    const uint32_t w0 = warp * spw;  // this warp's first slot within the CTA's slots of a class
+    WinTermsBits<R> A, An;
+    A.load_global(T, sSlot[w0]);
+    LaneOffsets<R> off;
+    off.init();
+    cluster_sync_all();
+    for (uint32_t s = 0; s < 64; ++s) {
+        if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
+        if (threadIdx.x == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
+                         : "memory");
+        long long prev = 0;  // SWAP: the lower member's window sum of the current couple
+        for (uint32_t k = 0; k < spw; ++k) {
+            // the next slot's rows (or the next class's first) are in flight while this one sums
+            const bool more = k + 1 < spw || s + 1 < 64;
+            if (more) An.load_global(T, sSlot[k + 1 < spw ? s * cpc + w0 + k + 1 : (s + 1) * cpc + w0]);
+            const uint32_t slot = s * cpc + w0 + k, p = sSlot[slot];
+            const long long mine = A.sum_bits(sbits, L, p, off);
+            if (mode && !(k & 1)) {
+                prev = mine;
+            } else {
+                const i128 sum = mode ? (i128)prev + (i128)mine : (i128)mine;
+                const bool ok = 2 * sum < 0;
+                const uint32_t np = mode ? 2 : 1;
+                // flags of the decided member(s): lane l < np * ncta sends member l / ncta to CTA l % ncta
+                if (lane < np * ncta) {
+                    const uint32_t pk = sSlot[slot - (np - 1) + lane / ncta];
+                    red_async_or(sbits_addr + 4 * (pk >> 5), mailbox(s), lane % ncta, ok ? 1u << (pk & 31) : 0u);
+                }
+                if (lane < np) {
+                    const uint32_t sl = slot - (np - 1) + lane, pk = sSlot[sl];
+                    acc[pk] = ok;
+                    dEp[pk] = (ok && lane == 0) ? 2 * sum : (i128)0;
+                    if (log) log[(size_t)s * M + sIdx[sl]] = ok;
+                }
+            }
+            if (more) A = An;
+        }
     }
     tc::mbar_wait(mailbox(63), (63 >> 1) & 1);
     cluster_sync_all();

@@ -438,3 +438,14 @@ def test_eval_quality_after_gpu_passes(bn, oracle_mod):
         s.eval_quality(1, [2.0])
     with pytest.raises(bn.BNError):
         s.eval_quality(0, [0.0])
+
+
+@pytest.mark.parametrize("decide", ["", "nobig"])
+@pytest.mark.parametrize("L,mode", [(256, 0), (256, 1), (512, 1)])
+def test_decide_large_tiles(bn, oracle_mod, monkeypatch, decide, L, mode):
+    """Tiles beyond one cluster's warps (L = 256, 512): the bit-flag cluster kernel with several
+    slots per warp (default) and, with nobig, the cooperative neighbour-band flag kernel (REDRAW) or
+    the per-class launches (SWAP), one full pass against the oracle."""
+    monkeypatch.setenv("BN_DECIDE", decide)
+    s, o, U = make(bn, oracle_mod, L, 16, (4,))
+    _check_run(s, o, U, 1, mode, seed=5 + L + mode)
