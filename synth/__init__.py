@@ -100,13 +100,14 @@ CONFIGS = {
                  note="16x16 tile, 2D rank-1 lattice, 16 spp, T=64 step integrands, 200 greedy passes"),
     "C2": Config("C2", 64, (4,), 256, 1, 100,
                  note="64x64 tile, 2D, 4 spp, T=256 integrands, swap-based optimisation, 1 GPU"),
-    # C3 runs the SWAP (pixel-permuting) optimiser: the paper's own (§3.4), and
-    # the one that lowers the denoised error (R32; REDRAW stays available, --mode redraw)
+    # C3, C4 and C5 run the SWAP (pixel-permuting) optimiser: the paper's own (PAPER.md l.228-229,
+    # §3.4), and the one that lowers the denoised error (R32; REDRAW stays available,
+    # bench.py --mode redraw)
     "C3": Config("C3", 128, (1, 4, 16, 64), 1024, 1, 100,
                  note="128x128 tile, 2D, 1/4/16/64 spp progressive, T=1024 integrands, 1 GPU"),
-    "C4": Config("C4", 128, (16,), 1024, 0, 100, pairs=8,
+    "C4": Config("C4", 128, (16,), 1024, 1, 100, pairs=8,
                  note="128x128 tile, 8 independent dimension pairs (16D sampler), one pair per GPU"),
-    "C5": Config("C5", 256, (16,), 8192, 0, 20,
+    "C5": Config("C5", 256, (16,), 8192, 1, 20,
                  note="256x256 tile, 2D, 16 spp, T=8192 integrands sharded across GPUs"),
 }
 

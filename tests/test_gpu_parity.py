@@ -223,19 +223,24 @@ def test_c2_full_size_swap(bn, oracle_mod):
 @pytest.mark.slow
 @pytest.mark.parametrize("pair", [0, 5])
 def test_c4_pair_full_size(bn, oracle_mod, pair):
-    """C4 pair j (128x128, 16 spp, T=1024, seeds xor j): all counts bit-exact, first colour class
-    decisions equal to the oracle, device invariants over a full pass."""
+    """C4 pair j (128x128, 16 spp, T=1024, seeds xor j): all counts bit-exact; for the bench's mode
+    (SWAP) and REDRAW, the first colour class's decisions equal to the oracle and the device
+    invariants over a full pass."""
     cfg = synth.CONFIGS["C4"]
     U, bank = synth.problem_inputs(cfg, pair)
-    s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
-    co = o.counts(U)
-    assert np.array_equal(s.eval_counts(), co)
-    E0, _ = s.energy()
-    st, lg = s.optimize(1, synth.opt_seed(cfg, pair), log=True)
-    _, _, _, lgo = o.optimize(U, co, passes=1, seed=synth.opt_seed(cfg, pair), max_steps=1, energy_each_pass=False,
-                              log=True)
-    assert np.array_equal(lg[0, :1], lgo[0, :1])
-    assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"] and st[0]["dE_sum"] < 0
+    co = None
+    for mode in (cfg.mode, 1 - cfg.mode):
+        s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
+        if co is None:
+            co = o.counts(U)
+            assert np.array_equal(s.eval_counts(), co)
+        E0, _ = s.energy()
+        st, lg = s.optimize(1, synth.opt_seed(cfg, pair), mode=mode, log=True)
+        _, _, _, lgo = o.optimize(U, co, mode=mode, passes=1, seed=synth.opt_seed(cfg, pair), max_steps=1,
+                                  energy_each_pass=False, log=True)
+        assert np.array_equal(lg[0, :1], lgo[0, :1])
+        assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"] and st[0]["dE_sum"] < 0
+        s.close()
 
 
 def test_concurrent_contexts_match_sequential(bn, oracle_mod):
@@ -268,19 +273,24 @@ def test_concurrent_contexts_match_sequential(bn, oracle_mod):
 
 @pytest.mark.slow
 def test_c5_full_size_sampled(bn, oracle_mod):
-    """C5 (256x256, 16 spp, T=8192): all 512 M counts bit-exact and the first colour class's
-    1024 decisions equal to the oracle's (the flag-synchronised persistent decide path)."""
+    """C5 (256x256, 16 spp, T=8192): all 512 M counts bit-exact and, for SWAP (the bench's mode) and
+    REDRAW, the first colour class's 1024 decisions equal to the oracle's (the L = 256 cluster
+    kernel with bit flags)."""
     cfg = synth.CONFIGS["C5"]
     U, bank = synth.problem_inputs(cfg)
-    s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
-    co = o.counts(U)
-    assert np.array_equal(s.eval_counts(), co)
-    E0, _ = s.energy()
-    st, lg = s.optimize(1, synth.opt_seed(cfg), log=True)
-    _, _, _, lgo = o.optimize(U, co, passes=1, seed=synth.opt_seed(cfg), max_steps=1, energy_each_pass=False,
-                              log=True)
-    assert np.array_equal(lg[0, :1], lgo[0, :1])
-    assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"]
+    co = None
+    for mode in (cfg.mode, 1 - cfg.mode):
+        s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
+        if co is None:
+            co = o.counts(U)
+            assert np.array_equal(s.eval_counts(), co)
+        E0, _ = s.energy()
+        st, lg = s.optimize(1, synth.opt_seed(cfg), mode=mode, log=True)
+        _, _, _, lgo = o.optimize(U, co, mode=mode, passes=1, seed=synth.opt_seed(cfg), max_steps=1,
+                                  energy_each_pass=False, log=True)
+        assert np.array_equal(lg[0, :1], lgo[0, :1])
+        assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"]
+        s.close()
 
 
 # ------------------------------------------------------------------ window-Gram variants

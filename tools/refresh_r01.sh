@@ -10,10 +10,11 @@ python bench.py --config C1 --mode swap --steps 200 --warmup 5 --cpu-classes 64 
 python bench.py --config C2 --steps 50 --warmup 5 --cpu-classes 16 >> $out 2> gpurun_out/bench_C2.err; echo C2 rc=$?
 python bench.py --config C2 --mode paper --steps 50 --warmup 5 --cpu-classes 16 >> $out 2> gpurun_out/bench_C2p.err; echo C2p rc=$?
 python bench.py --config C4 --steps 10 --warmup 3 --cpu-classes 8 >> $out 2> gpurun_out/bench_C4.err; echo C4 rc=$?
-python bench.py --config C4 --mode swap --steps 10 --warmup 3 --cpu-classes 8 >> $out 2> gpurun_out/bench_C4s.err; echo C4s rc=$?
+python bench.py --config C4 --mode redraw --steps 10 --warmup 3 --cpu-classes 8 >> $out 2> gpurun_out/bench_C4r.err; echo C4r rc=$?
 python bench.py --config C5 --steps 5 --warmup 3 --cpu-classes 1 --e2e-steps 2 >> $out 2> gpurun_out/bench_C5.err; echo C5 rc=$?
-python bench.py --config C5 --mode swap --steps 5 --warmup 3 --cpu-classes 1 --e2e-steps 2 >> $out 2> gpurun_out/bench_C5s.err; echo C5s rc=$?
+python bench.py --config C5 --mode redraw --steps 5 --warmup 3 --cpu-classes 1 --e2e-steps 2 >> $out 2> gpurun_out/bench_C5r.err; echo C5r rc=$?
 python bench.py --impl reference --steps 5 --warmup 3 >> $out 2> gpurun_out/bench_ref.err; echo ref rc=$?
 nproc; lscpu | grep "Model name"
-bash tools/gpu_ncu_multi.sh r01t k_gram_tc4 k_decide_swap k_lut k_paper_gather k_finish
+bash tools/gpu_ncu_multi.sh r01u k_gram_tc4 k_decide_swap k_lut k_paper_gather k_finish_gather
+bash tools/gpu_ncu_c5.sh
 ls gpurun_out
