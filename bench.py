@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--mode", choices=["config", "redraw", "swap", "paper"], default="config",
                     help="optimiser mode (default: the config's); paper = PAPER.md §3.4 snapshot couples, N/4 budget")
+    ap.add_argument("--K", type=int, default=1, help="best-of-K re-draws (REDRAW only; K candidates per pixel)")
     ap.add_argument("--energy", choices=["gf", "eq1", "eq1max"], default="gf",
                     help="energy form: north-star GF (default), Eq. 1 as written, Eq. 1 maximised")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -68,15 +69,17 @@ MODES = {"redraw": 0, "swap": 1, "paper": 2}
 
 
 def evals_per_pass(cfg):
-    """Pixel-update evaluations of one pass: every pixel once (REDRAW; SWAP couples count 2);
-    the paper mode swaps a budget of P/4 pixels per pass."""
+    """Pixel-update evaluations of one pass: every pixel once (REDRAW, x K for best-of-K; SWAP
+    couples count 2); the paper mode swaps a budget of P/4 pixels per pass."""
     P = cfg.L * cfg.L
-    return P // 4 if cfg.mode == 2 else P
+    return P // 4 if cfg.mode == 2 else P * cfg.extra.get("K", 1)
 
 
 def workload(cfg):
-    mode = {0: "redraw", 1: "swap", 2: "paper_swap"}[cfg.mode]
+    K = cfg.extra.get("K", 1)
+    mode = {0: "redraw" if K == 1 else f"redraw_best_of_{K}", 1: "swap", 2: "paper_swap"}[cfg.mode]
     step = (f"one optimisation pass = {evals_per_pass(cfg)} pixel-update evals "
+            + (f"(best of K = {K} re-draws per pixel, 64 per-class launches) " if K > 1 else "")
             + ("(P/4-pixel budget of snapshot couples, PAPER.md §3.4)" if cfg.mode == 2 else "(64 colour classes)"))
     return {
         "workload": f"{cfg.name}: {cfg.note}" + (" [paper-verbatim parallel swaps]" if cfg.mode == 2 else ""),
@@ -251,10 +254,11 @@ def oracle_sample(cfg, pair, classes, passes_done=0, state=None):
                                         seed=synth.opt_seed(cfg, pair), c=c, energy_each_pass=False)
     else:
         U, c, st, _ = pb.optimize(U, c, mode=cfg.mode, passes=1, first_pass=passes_done,
-                                  seed=synth.opt_seed(cfg, pair), max_steps=classes, energy_each_pass=False)
+                                  seed=synth.opt_seed(cfg, pair), max_steps=classes, energy_each_pass=False,
+                                  K=cfg.extra.get("K", 1))
     dt = time.perf_counter() - t0
     state[1], state[2] = U, c
-    return classes * M, dt, state
+    return classes * M * cfg.extra.get("K", 1), dt, state
 
 
 def cpu_sample_desc(cfg, classes):
@@ -262,8 +266,9 @@ def cpu_sample_desc(cfg, classes):
     if cfg.mode == 2:
         return (f"oracle (single-threaded C, -O2) on {cfg.name}, paper mode: one pass with a budget of "
                 f"{classes * M} pixels = {classes * M} pixel-update evals (distances recomputed from counts)")
+    K = cfg.extra.get("K", 1)
     return (f"oracle (single-threaded C, -O2) on {cfg.name}: first {classes} of 64 colour classes of pass 0 "
-            f"= {classes * M} pixel-update evals (full distances recomputed from counts per candidate)")
+            f"= {classes * M * K} pixel-update evals (full distances recomputed from counts per candidate)")
 
 
 def run_reference(args, cfg):
@@ -358,7 +363,7 @@ def run_ours(args, cfg):
         for sj, stj, sd in zip(samplers, streams, seeds):
             if stj is not stream:
                 stj.wait_event(ev)
-            sj.optimize(passes, sd, mode=cfg.mode, first_pass=first, stats=False)
+            sj.optimize(passes, sd, mode=cfg.mode, first_pass=first, stats=False, K=cfg.extra.get("K", 1))
         for stj in streams:
             if stj is not stream:
                 e = torch.cuda.Event()
@@ -386,7 +391,8 @@ def run_ours(args, cfg):
 
     # per-kernel device time on the context stream (one pair alone, events around each launch)
     s.profile_enable(True)
-    s.optimize(args.steps, seeds[0], mode=cfg.mode, first_pass=args.warmup + args.steps, stats=False)
+    s.optimize(args.steps, seeds[0], mode=cfg.mode, first_pass=args.warmup + args.steps, stats=False,
+               K=cfg.extra.get("K", 1))
     prof = s.profile()
     s.profile_enable(False)
     active = {k: v for k, v in prof.items() if v[1]}
@@ -407,7 +413,7 @@ def run_ours(args, cfg):
     st = None
     for k in range(args.e2e_steps):
         s.set_tile(cfg.L, pinned)
-        st, _ = s.optimize(1, seeds[0], mode=cfg.mode, first_pass=first + k, stats=True)
+        st, _ = s.optimize(1, seeds[0], mode=cfg.mode, first_pass=first + k, stats=True, K=cfg.extra.get("K", 1))
         s.get_tile(pinned)
     f1.record(streams[0])
     barrier()
@@ -461,6 +467,12 @@ def main():
         import dataclasses
 
         cfg = dataclasses.replace(cfg, mode=MODES[args.mode])
+    if args.K > 1:
+        import dataclasses
+
+        if cfg.mode != 0:
+            raise SystemExit("--K > 1 needs --mode redraw")
+        cfg = dataclasses.replace(cfg, extra=dict(cfg.extra, K=args.K))
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

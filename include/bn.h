@@ -114,7 +114,7 @@ typedef struct {
                          /* BN_PAPER_SWAP: the paper's snapshot couples (bn_set_permutation) */
     uint32_t passes;     /* number of passes to run                                       */
     uint32_t first_pass; /* pass index t of the first pass (resume = continue counting)   */
-    uint32_t K;          /* re-draw candidates per pixel; must be 1 in this version        */
+    uint32_t K;          /* re-draw candidates per pixel: 1, or 2..8 for best-of-K REDRAW  */
     uint64_t seed;       /* Philox4x32-10 key of the optimiser                             */
     uint32_t budget;     /* BN_PAPER_SWAP: pixels per pass (even, 2..L*L; 0 = L*L/4, the     */
                          /* paper's N/4); ignored by the other modes         */
@@ -138,7 +138,13 @@ typedef struct {
  * kappa = 1 + Philox(seed; s, t, 0, 3)[0] mod (M - 1), M = (L/8)^2.  A candidate (couple) is
  * accepted iff its exact dE < 0 against the state left by the earlier classes.
  * stats: host [passes] or NULL.  accept_log: host [passes][64][M] bytes (1 = accepted, SWAP:
- * both members of an accepted couple) or NULL.  EINVAL on K != 1 or an unknown mode.
+ * both members of an accepted couple) or NULL.  EINVAL on an unknown mode, K outside [1, 8] or
+ * K > 1 with a mode other than BN_REDRAW.
+ *
+ * Best-of-K REDRAW (K > 1): pixel p of class s draws K candidates
+ * u'_j = Philox(seed; p, t, j, 1)[0..1], j < K, takes the one with the lowest exact dE against the
+ * state left by the earlier classes (ties to the lowest j) and accepts it iff dE < 0.  Runs step by
+ * step (one launch per class); single-GPU only (EINVAL with a communicator).
  *
  * BN_PAPER_SWAP (§3.4 l.291-307 verbatim): pass t forms the couples
  *   c = (perm[2c] ^ key(t), perm[2c+1] ^ key(t)),  c < budget/2,

@@ -151,6 +151,9 @@ struct bn_ctx {
     DevBuf<uint8_t> c, cn, cn2, acc, log, cexp;
     DevBuf<int> nc, nn, nn2, derr, progress;
     DevBuf<uint32_t> perm, part;
+    DevBuf<uint8_t> cnK;   // best-of-K candidates [K][P][rowB]
+    DevBuf<uint2> UnK;
+    DevBuf<int> nnK;
     DevBuf<double2> ev_tw, ev_X1;  // bn_eval_quality work buffers
     DevBuf<double> ev_h, ev_rm, ev_sp, ev_out;  // BN_PAPER_SWAP: precomputed permutation, per-pass partner map
     uint32_t perm_n = 0;
@@ -197,6 +200,7 @@ struct bn_ctx {
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
     bool big_attr_set[8] = {false};
+    bool best_attr_set[8] = {false};
     bool no_big = false;  // BN_DECIDE=nobig: L > 128 tiles use the cooperative flag kernel
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
@@ -793,6 +797,100 @@ int read_err_flag(bn_ctx* ctx) {
     return BN_OK;
 }
 
+template <int R>
+int launch_class_best(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, uint32_t K, const LutArgs& la, uint8_t* log) {
+    const uint32_t M = (ctx->L / 8) * (ctx->L / 8);
+    const size_t smem = (size_t)(K + 1) * ctx->rowB;
+    if (!ctx->best_attr_set[R]) {
+        CUDA_TRY(cudaFuncSetAttribute(k_class_best<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        ctx->best_attr_set[R] = true;
+    }
+    if (smem > 200 * 1024) return fail(ctx, BN_EINVAL, "best-of-K rows (%zu B) exceed shared memory", smem);
+    k_class_best<R><<<M, 256, smem, ctx->ls>>>(s, t, seed, ctx->L, K, ctx->c.p, ctx->cnK.p, ctx->nc.p, ctx->nnK.p,
+                                               ctx->U.p, ctx->UnK.p, ctx->rowB, ctx->Tp, ctx->nl, ctx->W.p, la,
+                                               ctx->acc.p, ctx->dEp.p, log, ctx->derr.p);
+    LAUNCHED();
+    return BN_OK;
+}
+
+// Best-of-K REDRAW (K > 1): K candidate count sets per pass, then 64 per-class launches that decide
+// and commit step by step (k_class_best); exact pass sums from the running energy (k_kstats).
+int optimize_best_of_k(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uint8_t* accept_log) {
+    const uint32_t P = ctx->P, M = (ctx->L / 8) * (ctx->L / 8), nl = ctx->nl, K = prm->K;
+    if (ctx->comm) return fail(ctx, BN_EINVAL, "best-of-K is single-GPU (no bank sharding)");
+    int rc;
+    CUDA_TRY(ctx->cnK.ensure((size_t)K * P * ctx->rowB));
+    CUDA_TRY(ctx->UnK.ensure((size_t)K * P));
+    CUDA_TRY(ctx->nnK.ensure((size_t)K * P * nl));
+    CUDA_TRY(ctx->pstats.ensure(prm->passes + 1));
+    if (accept_log) CUDA_TRY(ctx->log.ensure((size_t)prm->passes * 64 * M));
+    CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
+    ctx->ls = ctx->stream;
+    // exact energy of the starting tile (slot `passes`), then E_after = E_before + sum dE per pass
+    if ((rc = gram_lut(ctx, ctx->c.p, ctx->nc.p, 0))) return rc;
+    const uint32_t nE = (uint32_t)(((size_t)P * half_count_padded(ctx->R) + 255) / 256);
+    k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, nullptr, nullptr, P, 0, ctx->pstats.p + prm->passes);
+    LAUNCHED();
+    LutArgs la;
+    for (uint32_t l = 0; l < 8; ++l) {
+        la.G[l] = l < nl ? ctx->G.p + ctx->Goff[l] : nullptr;
+        la.Dmax[l] = l < nl ? ctx->Dmax[l] : 0;
+    }
+    const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
+    const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
+    for (uint32_t pi = 0; pi < prm->passes; ++pi) {
+        const uint32_t t = prm->first_pass + pi;
+        for (uint32_t j = 0; j < K; ++j) {
+            KSTART(BN_K_COUNTS);
+            k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->stream>>>(
+                nullptr, ctx->UnK.p + (size_t)j * P, (int)(1 + j), prm->seed, t, P, ctx->ab.p, ctx->Cc.p, ctx->cgrp.p,
+                ctx->Tp, ctx->S.p, ctx->levels[nl - 1], lo, hi, nl, ctx->cnK.p + (size_t)j * P * ctx->rowB,
+                ctx->nnK.p + (size_t)j * P * nl, nullptr, ctx->L);
+            LAUNCHED_K();
+        }
+        uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
+        KSTART(BN_K_DECIDE);
+        for (uint32_t s = 0; s < 64; ++s) {
+            switch (ctx->R) {
+                case 1: rc = launch_class_best<1>(ctx, s, t, prm->seed, K, la, log); break;
+                case 2: rc = launch_class_best<2>(ctx, s, t, prm->seed, K, la, log); break;
+                case 3: rc = launch_class_best<3>(ctx, s, t, prm->seed, K, la, log); break;
+                case 4: rc = launch_class_best<4>(ctx, s, t, prm->seed, K, la, log); break;
+                case 5: rc = launch_class_best<5>(ctx, s, t, prm->seed, K, la, log); break;
+                case 6: rc = launch_class_best<6>(ctx, s, t, prm->seed, K, la, log); break;
+                default: rc = launch_class_best<7>(ctx, s, t, prm->seed, K, la, log); break;
+            }
+            if (rc) return rc;
+        }
+        if (ctx->prof) cudaEventRecord(next_event(ctx), ctx->ls);  // closes the BN_K_DECIDE bracket
+        const unsigned long long* Ein = pi == 0 ? ctx->pstats.p[prm->passes].E_before : ctx->pstats.p[pi - 1].E_after;
+        KSTART(BN_K_STATS);
+        k_kstats<<<1, 1024, 0, ctx->stream>>>(ctx->dEp.p, ctx->acc.p, P, Ein, ctx->pstats.p + pi);
+        LAUNCHED_K();
+    }
+    if (stats || accept_log) {
+        std::vector<PassStatsDev> h(prm->passes);
+        CUDA_TRY(cudaMemcpyAsync(h.data(), ctx->pstats.p, prm->passes * sizeof(PassStatsDev), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        if (accept_log)
+            CUDA_TRY(cudaMemcpyAsync(accept_log, ctx->log.p, (size_t)prm->passes * 64 * M, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+        if ((rc = read_err_flag(ctx))) return rc;
+        if (stats)
+            for (uint32_t pi = 0; pi < prm->passes; ++pi) {
+                stats[pi].accepted = h[pi].accepted;
+                stats[pi].proposed = P;
+                stats[pi].E_fixed[0] = h[pi].E_after[0];
+                stats[pi].E_fixed[1] = h[pi].E_after[1];
+                stats[pi].E = std::ldexp((double)h[pi].E_after[1], 64 - BN_FIX_BITS) +
+                              std::ldexp((double)h[pi].E_after[0], -BN_FIX_BITS);
+                stats[pi].dE_sum[0] = h[pi].dE_sum[0];
+                stats[pi].dE_sum[1] = h[pi].dE_sum[1];
+            }
+    }
+    return BN_OK;
+}
+
 }  // namespace
 
 // ============================================================================ C-ABI
@@ -869,7 +967,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->Cc.release(); ctx->cgrp.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
         ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
         ctx->d0.release(); ctx->d1b.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
-        ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release();
+        ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release(); ctx->cnK.release(); ctx->UnK.release(); ctx->nnK.release();
         ctx->ev_tw.release(); ctx->ev_X1.release(); ctx->ev_h.release(); ctx->ev_rm.release(); ctx->ev_sp.release();
         ctx->ev_out.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1073,11 +1171,13 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     if (!prm) return fail(ctx, BN_EINVAL, "null params");
     if (prm->mode > BN_PAPER_SWAP) return fail(ctx, BN_EINVAL, "unknown mode %u", prm->mode);
     if (prm->reserved) return fail(ctx, BN_EINVAL, "bn_opt_params.reserved must be 0");
-    if (prm->K != 1) return fail(ctx, BN_EINVAL, "K = %u: only K = 1 is implemented", prm->K);
+    if (prm->K < 1 || prm->K > KBEST_MAX || (prm->K > 1 && prm->mode != BN_REDRAW))
+        return fail(ctx, BN_EINVAL, "K = %u: must be 1, or 2..%d with BN_REDRAW", prm->K, KBEST_MAX);
     DeviceGuard g(ctx->dev);
     int rc = ensure_work(ctx);
     if (rc) return rc;
     if (prm->passes == 0) return BN_OK;
+    if (prm->K > 1) return optimize_best_of_k(ctx, prm, stats, accept_log);
     const uint32_t P = ctx->P, M = (ctx->L / 8) * (ctx->L / 8), nl = ctx->nl;
     const int R = ctx->R;
     const uint32_t nE = (uint32_t)(((size_t)P * half_count_padded(R) + 255) / 256);

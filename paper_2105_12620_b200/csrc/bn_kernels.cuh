@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __re
         const uint32_t p = p0 + pp;
         if (p >= P) break;
         uint2 u;
-        if (redraw) {
-            const uint4 r = philox_seeded(seed, p, pass_t, 0, 1);
+        if (redraw) {  // candidate j = redraw - 1 (best-of-K draws j = 0 .. K-1)
+            const uint4 r = philox_seeded(seed, p, pass_t, (uint32_t)(redraw - 1), 1);
             u = make_uint2(r.x, r.y);
             if ((threadIdx.x & 31) == 0) Uout[p] = u;
         } else {
@@ -3202,6 +3202,136 @@ __global__ void __launch_bounds__(1024) k_finish_gather(uint8_t* __restrict__ ac
         out->dE_sum[1] = tot.d[1];
         out->accepted = tot.a / 2;
         *ticket = 0;
+    }
+}
+
+// Best-of-K REDRAW (K > 1, reading R19): one launch per colour class, one CTA per
+// candidate pixel p of the class, step by step (the 4-Gram formulation of the K = 1 path would need
+// (K+1)^2 window Grams).  The CTA stages p's current row and its K candidate rows in shared memory,
+// each warp streams a share of the 224 neighbours' current rows (committed by the earlier classes)
+// and forms the K+1 exact dot products per level with dp4a, every lane holding all of them after a
+// butterfly; lane j < K accumulates dE_j = sum_l sum_o q(o, D(cn^j_p, c_q)) - q(o, D(c_p, c_q)) in
+// int64 (R15).  The best candidate (lowest dE, ties to the lowest j, as the oracle) is accepted iff
+// 2 dE < 0 and committed by the same CTA: members of a class are window-independent.
+constexpr int KBEST_MAX = 8;
+template <int R>
+__global__ void __launch_bounds__(256) k_class_best(uint32_t s, uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t K,
+                                                    uint8_t* __restrict__ c, const uint8_t* __restrict__ cnK,
+                                                    int* __restrict__ nc, const int* __restrict__ nnK,
+                                                    uint2* __restrict__ U, const uint2* __restrict__ UnK,
+                                                    uint32_t rowB, uint32_t Tp, uint32_t nl,
+                                                    const double* __restrict__ W, LutArgs lut,
+                                                    uint8_t* __restrict__ acc, i128* __restrict__ dEp,
+                                                    uint8_t* __restrict__ log, int* __restrict__ err) {
+    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
+    extern __shared__ __align__(16) uint8_t xrows[];  // [K + 1][rowB]: c_p, cn^0_p .. cn^{K-1}_p
+    __shared__ long long sdE[8][KBEST_MAX];
+    __shared__ int sbest;
+    const uint32_t M = (L / 8) * (L / 8), P = L * L, m = blockIdx.x;
+    const uint32_t p = class_pixel(L, seed, pass_t, s, m);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t n16 = rowB / 16;
+    for (uint32_t j = threadIdx.x; j < (K + 1) * n16; j += blockDim.x) {
+        const uint32_t v = j / n16, cidx = j - v * n16;
+        const uint4* src = reinterpret_cast<const uint4*>(v == 0 ? c + (size_t)p * rowB
+                                                                 : cnK + ((size_t)(v - 1) * P + p) * rowB);
+        reinterpret_cast<uint4*>(xrows)[j] = src[cidx];
+    }
+    __syncthreads();
+    const uint32_t x = p % L, y = p / L;
+    long long dE = 0;  // lane j < K: candidate j's sum over this warp's neighbours
+    for (uint32_t w = warp; w < (uint32_t)WN; w += blockDim.x >> 5) {
+        const int ww = w >= (uint32_t)(R * (2 * R + 1) + R) ? (int)w + 1 : (int)w;
+        const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
+        const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
+        const double wt = W[w];
+        const uint4* cq = reinterpret_cast<const uint4*>(c + (size_t)q * rowB);
+        for (uint32_t l = 0; l < nl; ++l) {
+            unsigned dot[KBEST_MAX + 1];  // counts are unsigned bytes: dp4a.u32.u32
+#pragma unroll
+            for (int v = 0; v <= KBEST_MAX; ++v) dot[v] = 0;
+            for (uint32_t ci = l * (Tp / 16) + lane; ci < (l + 1) * (Tp / 16); ci += 32) {
+                const uint4 b = __ldg(cq + ci);
+#pragma unroll
+                for (int v = 0; v <= KBEST_MAX; ++v)
+                    if (v <= (int)K) {
+                        const uint4 a = reinterpret_cast<const uint4*>(xrows)[(size_t)v * n16 + ci];
+                        dot[v] = __dp4a(a.x, b.x, dot[v]);
+                        dot[v] = __dp4a(a.y, b.y, dot[v]);
+                        dot[v] = __dp4a(a.z, b.z, dot[v]);
+                        dot[v] = __dp4a(a.w, b.w, dot[v]);
+                    }
+            }
+#pragma unroll
+            for (int v = 0; v <= KBEST_MAX; ++v)
+#pragma unroll
+                for (int o = 16; o; o >>= 1) dot[v] += __shfl_xor_sync(0xffffffffu, dot[v], o);
+            const int nq = nc[(size_t)q * nl + l];
+            const int D0 = nc[(size_t)p * nl + l] + nq - 2 * (int)dot[0];
+            const int dm = lut.Dmax[l];
+            if (lane < K) {
+                int Dj = 0;
+#pragma unroll
+                for (int v = 1; v <= KBEST_MAX; ++v)
+                    if (v == (int)lane + 1) Dj = nnK[((size_t)lane * P + p) * nl + l] + nq - 2 * (int)dot[v];
+                if ((unsigned)D0 > (unsigned)dm || (unsigned)Dj > (unsigned)dm) {
+                    atomicOr(err, 1);
+                } else {
+                    dE += (long long)qterm(wt, lut.G[l], Dj) - (long long)qterm(wt, lut.G[l], D0);
+                }
+            }
+        }
+    }
+    if (lane < K) sdE[warp][lane] = dE;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int best = -1;
+        long long bv = 0;
+        for (uint32_t j = 0; j < K; ++j) {
+            long long t = 0;
+            for (uint32_t wq = 0; wq < (blockDim.x >> 5); ++wq) t += sdE[wq][j];
+            if (best < 0 || t < bv) {
+                bv = t;
+                best = (int)j;
+            }
+        }
+        const i128 d = 2 * (i128)bv;
+        const bool ok = d < 0;
+        sbest = ok ? best : -1;
+        acc[p] = ok;
+        dEp[p] = ok ? d : (i128)0;
+        if (log) log[(size_t)s * M + m] = ok;
+    }
+    __syncthreads();
+    const int jb = sbest;
+    if (jb < 0) return;
+    const uint4* src = reinterpret_cast<const uint4*>(xrows) + (size_t)(jb + 1) * n16;
+    uint4* dst = reinterpret_cast<uint4*>(c + (size_t)p * rowB);
+    for (uint32_t j = threadIdx.x; j < n16; j += blockDim.x) dst[j] = src[j];
+    if (threadIdx.x == 0) U[p] = UnK[(size_t)jb * P + p];
+    if (threadIdx.x < nl) nc[(size_t)p * nl + threadIdx.x] = nnK[((size_t)jb * P + p) * nl + threadIdx.x];
+}
+// Pass sums of the best-of-K path: E_after = E_in + sum dEp (exact), accepted = sum acc.
+__global__ void __launch_bounds__(1024) k_kstats(const i128* __restrict__ dEp, const uint8_t* __restrict__ acc,
+                                                 uint32_t P, const unsigned long long* __restrict__ E_in,
+                                                 PassStatsDev* __restrict__ out) {
+    __shared__ FinishPart s_w[32];
+    i128 d = 0;
+    unsigned a = 0;
+    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) {
+        d += dEp[j];
+        a += acc[j];
+    }
+    const FinishPart tot = block_sum_parts(0, (u128)d, a, s_w);
+    if (threadIdx.x == 0) {
+        const u128 E = ((u128)E_in[1] << 64) | E_in[0], D = ((u128)tot.d[1] << 64) | tot.d[0], Ea = E + D;
+        out->E_before[0] = E_in[0];
+        out->E_before[1] = E_in[1];
+        out->E_after[0] = (unsigned long long)Ea;
+        out->E_after[1] = (unsigned long long)(Ea >> 64);
+        out->dE_sum[0] = tot.d[0];
+        out->dE_sum[1] = tot.d[1];
+        out->accepted = tot.a;
     }
 }
 

@@ -87,9 +87,9 @@ def test_energy_translation_invariance(bn, oracle_mod):
 
 
 # -------------------------------------------------------------------------- optimisation
-def _check_run(s, o, U, passes, mode, seed, first_pass=0):
-    st, lg = s.optimize(passes, seed, mode=mode, first_pass=first_pass, log=True)
-    Uo, co, sto, lgo = o.optimize(U, mode=mode, passes=passes, first_pass=first_pass, seed=seed, log=True)
+def _check_run(s, o, U, passes, mode, seed, first_pass=0, K=1):
+    st, lg = s.optimize(passes, seed, mode=mode, first_pass=first_pass, log=True, K=K)
+    Uo, co, sto, lgo = o.optimize(U, mode=mode, passes=passes, first_pass=first_pass, seed=seed, log=True, K=K)
     assert np.array_equal(lg, lgo), "accept/reject sequence differs"
     assert np.array_equal(s.get_tile(), Uo), "tile differs"
     assert np.array_equal(s.eval_counts(), co), "counts differ"
@@ -152,7 +152,10 @@ def test_errors(bn, oracle_mod):
     assert e.value.code == bn.BN_EINVAL
     s2, _, _ = make(bn, oracle_mod, 16, 8, (4,))
     with pytest.raises(bn.BNError) as e:
-        s2.optimize(1, 1, K=2)
+        s2.optimize(1, 1, K=2, mode=bn.SWAP)
+    assert e.value.code == bn.BN_EINVAL
+    with pytest.raises(bn.BNError) as e:
+        s2.optimize(1, 1, K=9)
     assert e.value.code == bn.BN_EINVAL
     with pytest.raises(bn.BNError) as e:
         s2.set_tile(24, np.zeros((24 * 24, 2), np.uint32))
@@ -459,3 +462,20 @@ def test_decide_large_tiles(bn, oracle_mod, monkeypatch, decide, L, mode):
     monkeypatch.setenv("BN_DECIDE", decide)
     s, o, U = make(bn, oracle_mod, L, 16, (4,))
     _check_run(s, o, U, 1, mode, seed=5 + L + mode)
+
+
+# --------------------------------------------------------------- best-of-K REDRAW (f3, K > 1)
+@pytest.mark.parametrize("L,T,levels,K,radius", [(16, 64, (16,), 2, 7), (32, 130, (1, 4, 16), 4, 7),
+                                                 (16, 40, (4, 16), 8, 5), (64, 100, (4,), 3, 7)])
+def test_best_of_k_parity(bn, oracle_mod, L, T, levels, K, radius):
+    """Best-of-K re-draws (lowest exact dE of K Philox candidates, ties to the lowest j): accept
+    logs, tiles, counts and exact energies equal to the oracle pass by pass."""
+    s, o, U = make(bn, oracle_mod, L, T, levels, radius=radius)
+    st = _check_run(s, o, U, 3, 0, seed=23, K=K)
+    assert s.energy()[0] == st[-1]["E_fixed"]            # running energy == recomputed energy
+
+
+def test_best_of_k_resume(bn, oracle_mod):
+    s, o, U = make(bn, oracle_mod, 32, 48, (16,))
+    s.optimize(2, 4, K=3, stats=False)
+    _check_run(s, o, o.optimize(U, passes=2, seed=4, K=3)[0], 2, 0, seed=4, first_pass=2, K=3)
