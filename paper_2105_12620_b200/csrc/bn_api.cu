@@ -154,6 +154,8 @@ struct bn_ctx {
     DevBuf<uint8_t> cnK;   // best-of-K candidates [K][P][rowB]
     DevBuf<uint2> UnK;
     DevBuf<int> nnK;
+    DevBuf<unsigned long long> kpart;  // best-of-K partial window sums [M][8]
+    DevBuf<unsigned int> kticket;
     DevBuf<double2> ev_tw, ev_X1;  // bn_eval_quality work buffers
     DevBuf<double> ev_h, ev_rm, ev_sp, ev_out;  // BN_PAPER_SWAP: precomputed permutation, per-pass partner map
     uint32_t perm_n = 0;
@@ -200,7 +202,6 @@ struct bn_ctx {
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
     bool big_attr_set[8] = {false};
-    bool best_attr_set[8] = {false};
     bool no_big = false;  // BN_DECIDE=nobig: L > 128 tiles use the cooperative flag kernel
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
@@ -797,20 +798,23 @@ int read_err_flag(bn_ctx* ctx) {
     return BN_OK;
 }
 
-template <int R>
-int launch_class_best(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, uint32_t K, const LutArgs& la, uint8_t* log) {
+template <int R, int NV>
+int launch_class_best_nv(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, uint32_t K, const LutArgs& la, uint8_t* log) {
     const uint32_t M = (ctx->L / 8) * (ctx->L / 8);
     const size_t smem = (size_t)(K + 1) * ctx->rowB;
-    if (!ctx->best_attr_set[R]) {
-        CUDA_TRY(cudaFuncSetAttribute(k_class_best<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        ctx->best_attr_set[R] = true;
-    }
     if (smem > 200 * 1024) return fail(ctx, BN_EINVAL, "best-of-K rows (%zu B) exceed shared memory", smem);
-    k_class_best<R><<<M, 256, smem, ctx->ls>>>(s, t, seed, ctx->L, K, ctx->c.p, ctx->cnK.p, ctx->nc.p, ctx->nnK.p,
-                                               ctx->U.p, ctx->UnK.p, ctx->rowB, ctx->Tp, ctx->nl, ctx->W.p, la,
-                                               ctx->acc.p, ctx->dEp.p, log, ctx->derr.p);
+    CUDA_TRY(cudaFuncSetAttribute(k_class_best<R, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    k_class_best<R, NV><<<dim3(M, KBEST_SPLIT), 256, smem, ctx->ls>>>(
+        s, t, seed, ctx->L, K, ctx->c.p, ctx->cnK.p, ctx->nc.p, ctx->nnK.p, ctx->U.p, ctx->UnK.p, ctx->rowB, ctx->Tp,
+        ctx->nl, ctx->W.p, la, ctx->acc.p, ctx->dEp.p, log, ctx->derr.p, ctx->kpart.p, ctx->kticket.p);
     LAUNCHED();
     return BN_OK;
+}
+template <int R>
+int launch_class_best(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, uint32_t K, const LutArgs& la, uint8_t* log) {
+    if (K + 1 <= 3) return launch_class_best_nv<R, 3>(ctx, s, t, seed, K, la, log);
+    if (K + 1 <= 5) return launch_class_best_nv<R, 5>(ctx, s, t, seed, K, la, log);
+    return launch_class_best_nv<R, KBEST_MAX + 1>(ctx, s, t, seed, K, la, log);
 }
 
 // Best-of-K REDRAW (K > 1): K candidate count sets per pass, then 64 per-class launches that decide
@@ -822,6 +826,10 @@ int optimize_best_of_k(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* sta
     CUDA_TRY(ctx->cnK.ensure((size_t)K * P * ctx->rowB));
     CUDA_TRY(ctx->UnK.ensure((size_t)K * P));
     CUDA_TRY(ctx->nnK.ensure((size_t)K * P * nl));
+    CUDA_TRY(ctx->kpart.ensure((size_t)M * KBEST_MAX));
+    CUDA_TRY(ctx->kticket.ensure(M));
+    CUDA_TRY(cudaMemsetAsync(ctx->kpart.p, 0, (size_t)M * KBEST_MAX * sizeof(unsigned long long), ctx->stream));
+    CUDA_TRY(cudaMemsetAsync(ctx->kticket.p, 0, (size_t)M * sizeof(unsigned int), ctx->stream));
     CUDA_TRY(ctx->pstats.ensure(prm->passes + 1));
     if (accept_log) CUDA_TRY(ctx->log.ensure((size_t)prm->passes * 64 * M));
     CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
@@ -967,7 +975,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->Cc.release(); ctx->cgrp.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
         ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
         ctx->d0.release(); ctx->d1b.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
-        ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release(); ctx->cnK.release(); ctx->UnK.release(); ctx->nnK.release();
+        ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release(); ctx->cnK.release(); ctx->UnK.release(); ctx->nnK.release(); ctx->kpart.release(); ctx->kticket.release();
         ctx->ev_tw.release(); ctx->ev_X1.release(); ctx->ev_h.release(); ctx->ev_rm.release(); ctx->ev_sp.release();
         ctx->ev_out.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);

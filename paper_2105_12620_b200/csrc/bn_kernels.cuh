@@ -3214,7 +3214,11 @@ __global__ void __launch_bounds__(1024) k_finish_gather(uint8_t* __restrict__ ac
 // int64 (R15).  The best candidate (lowest dE, ties to the lowest j, as the oracle) is accepted iff
 // 2 dE < 0 and committed by the same CTA: members of a class are window-independent.
 constexpr int KBEST_MAX = 8;
-template <int R>
+constexpr int KBEST_SPLIT = 4;  // CTAs per candidate (each sums a quarter of the window)
+// grid (M, KBEST_SPLIT): CTA (m, sp) sums the neighbours w = sp, sp + KBEST_SPLIT, ... of candidate m
+// into the exact int64 partials part[m][j] (integer atomics: order-independent); the last CTA of the
+// candidate (ticket) decides, commits, and resets the partials and its ticket for the next class.
+template <int R, int NV>
 __global__ void __launch_bounds__(256) k_class_best(uint32_t s, uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t K,
                                                     uint8_t* __restrict__ c, const uint8_t* __restrict__ cnK,
                                                     int* __restrict__ nc, const int* __restrict__ nnK,
@@ -3222,14 +3226,15 @@ __global__ void __launch_bounds__(256) k_class_best(uint32_t s, uint32_t pass_t,
                                                     uint32_t rowB, uint32_t Tp, uint32_t nl,
                                                     const double* __restrict__ W, LutArgs lut,
                                                     uint8_t* __restrict__ acc, i128* __restrict__ dEp,
-                                                    uint8_t* __restrict__ log, int* __restrict__ err) {
+                                                    uint8_t* __restrict__ log, int* __restrict__ err,
+                                                    unsigned long long* __restrict__ part, unsigned int* __restrict__ tickets) {
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     extern __shared__ __align__(16) uint8_t xrows[];  // [K + 1][rowB]: c_p, cn^0_p .. cn^{K-1}_p
     __shared__ long long sdE[8][KBEST_MAX];
-    __shared__ int sbest;
-    const uint32_t M = (L / 8) * (L / 8), P = L * L, m = blockIdx.x;
+    __shared__ bool slast;
+    const uint32_t M = (L / 8) * (L / 8), P = L * L, m = blockIdx.x, sp = blockIdx.y;
     const uint32_t p = class_pixel(L, seed, pass_t, s, m);
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
     const uint32_t n16 = rowB / 16;
     for (uint32_t j = threadIdx.x; j < (K + 1) * n16; j += blockDim.x) {
         const uint32_t v = j / n16, cidx = j - v * n16;
@@ -3240,20 +3245,20 @@ __global__ void __launch_bounds__(256) k_class_best(uint32_t s, uint32_t pass_t,
     __syncthreads();
     const uint32_t x = p % L, y = p / L;
     long long dE = 0;  // lane j < K: candidate j's sum over this warp's neighbours
-    for (uint32_t w = warp; w < (uint32_t)WN; w += blockDim.x >> 5) {
+    for (uint32_t w = sp + KBEST_SPLIT * warp; w < (uint32_t)WN; w += KBEST_SPLIT * nwarp) {
         const int ww = w >= (uint32_t)(R * (2 * R + 1) + R) ? (int)w + 1 : (int)w;
         const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
         const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
         const double wt = W[w];
         const uint4* cq = reinterpret_cast<const uint4*>(c + (size_t)q * rowB);
         for (uint32_t l = 0; l < nl; ++l) {
-            unsigned dot[KBEST_MAX + 1];  // counts are unsigned bytes: dp4a.u32.u32
+            unsigned dot[NV];  // counts are unsigned bytes: dp4a.u32.u32
 #pragma unroll
-            for (int v = 0; v <= KBEST_MAX; ++v) dot[v] = 0;
+            for (int v = 0; v < NV; ++v) dot[v] = 0;
             for (uint32_t ci = l * (Tp / 16) + lane; ci < (l + 1) * (Tp / 16); ci += 32) {
                 const uint4 b = __ldg(cq + ci);
 #pragma unroll
-                for (int v = 0; v <= KBEST_MAX; ++v)
+                for (int v = 0; v < NV; ++v)
                     if (v <= (int)K) {
                         const uint4 a = reinterpret_cast<const uint4*>(xrows)[(size_t)v * n16 + ci];
                         dot[v] = __dp4a(a.x, b.x, dot[v]);
@@ -3263,7 +3268,7 @@ __global__ void __launch_bounds__(256) k_class_best(uint32_t s, uint32_t pass_t,
                     }
             }
 #pragma unroll
-            for (int v = 0; v <= KBEST_MAX; ++v)
+            for (int v = 0; v < NV; ++v)
 #pragma unroll
                 for (int o = 16; o; o >>= 1) dot[v] += __shfl_xor_sync(0xffffffffu, dot[v], o);
             const int nq = nc[(size_t)q * nl + l];
@@ -3272,7 +3277,7 @@ __global__ void __launch_bounds__(256) k_class_best(uint32_t s, uint32_t pass_t,
             if (lane < K) {
                 int Dj = 0;
 #pragma unroll
-                for (int v = 1; v <= KBEST_MAX; ++v)
+                for (int v = 1; v < NV; ++v)
                     if (v == (int)lane + 1) Dj = nnK[((size_t)lane * P + p) * nl + l] + nq - 2 * (int)dot[v];
                 if ((unsigned)D0 > (unsigned)dm || (unsigned)Dj > (unsigned)dm) {
                     atomicOr(err, 1);
@@ -3284,17 +3289,30 @@ __global__ void __launch_bounds__(256) k_class_best(uint32_t s, uint32_t pass_t,
     }
     if (lane < K) sdE[warp][lane] = dE;
     __syncthreads();
+    if (threadIdx.x < K) {
+        long long t = 0;
+        for (uint32_t wq = 0; wq < nwarp; ++wq) t += sdE[wq][threadIdx.x];
+        atomicAdd(part + (size_t)m * KBEST_MAX + threadIdx.x, (unsigned long long)t);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) slast = atomicAdd(tickets + m, 1u) == KBEST_SPLIT - 1;
+    __syncthreads();
+    if (!slast) return;
+    __threadfence();
+    __shared__ int sbest;
     if (threadIdx.x == 0) {
         int best = -1;
         long long bv = 0;
         for (uint32_t j = 0; j < K; ++j) {
-            long long t = 0;
-            for (uint32_t wq = 0; wq < (blockDim.x >> 5); ++wq) t += sdE[wq][j];
+            const long long t = (long long)__ldcg(part + (size_t)m * KBEST_MAX + j);
+            part[(size_t)m * KBEST_MAX + j] = 0;
             if (best < 0 || t < bv) {
                 bv = t;
                 best = (int)j;
             }
         }
+        tickets[m] = 0;
         const i128 d = 2 * (i128)bv;
         const bool ok = d < 0;
         sbest = ok ? best : -1;
