@@ -2738,19 +2738,7 @@ __global__ void __launch_bounds__(512, 1) k_decide_big(uint32_t pass_t, uint64_t
     cluster_sync_all();
 }
 
-// ------------------------------------------------------------------------------- commit
-__global__ void k_commit(const uint8_t* __restrict__ acc, uint32_t P, uint32_t rowB, uint32_t nl,
-                         const uint2* __restrict__ Un, uint2* __restrict__ U, const uint8_t* __restrict__ cn,
-                         uint8_t* __restrict__ c, const int* __restrict__ nn, int* __restrict__ nc) {
-    const uint32_t p = blockIdx.x;
-    if (!acc[p]) return;
-    const uint4* src = reinterpret_cast<const uint4*>(cn + (size_t)p * rowB);
-    uint4* dst = reinterpret_cast<uint4*>(c + (size_t)p * rowB);
-    for (uint32_t j = threadIdx.x; j < rowB / 16; j += blockDim.x) dst[j] = src[j];
-    if (threadIdx.x == 0) U[p] = Un[p];
-    if (threadIdx.x < nl) nc[(size_t)p * nl + threadIdx.x] = nn[(size_t)p * nl + threadIdx.x];
-}
-
+// ------------------------------------------------------------------------------- pass sums
 struct PassStatsDev {
     unsigned long long E_before[2];
     unsigned long long E_after[2];
