@@ -1343,15 +1343,13 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             for (uint32_t s = 0; s < 64; ++s)
                 if ((rc = decide(ctx, s, t, prm->seed, (int)prm->mode, log))) return rc;
         if (fuse && pi + 1 < prm->passes) {
-            CUDA_TRY(launch_k(ctx, k_swap_pairs, dim3((64 * M + 255) / 256), dim3(256), 0, cs, ctx->L, prm->seed, t + 1,
-                              ctx->part.p));
-            LAUNCHED();
+            // the next pass's partners are computed in k_finish_gather itself (swap_partner)
             KSTART(BN_K_COMMIT);
             CUDA_TRY(launch_k(ctx, k_finish_gather, dim3(nfin), dim3(1024), 0, cs, ctx->acc.p, P, ctx->rowB, nl,
                               (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
                               ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, ctx->fparts.p,
-                              ctx->ticket.p, ctx->pstats.p + pi, (const uint32_t*)ctx->part.p, buf_U(pi + 1),
-                              buf_c(pi + 1), buf_n(pi + 1)));
+                              ctx->ticket.p, ctx->pstats.p + pi, (const uint32_t*)nullptr, buf_U(pi + 1),
+                              buf_c(pi + 1), buf_n(pi + 1), ctx->L, prm->seed, t + 1));
             LAUNCHED_K();
             continue;
         }

@@ -59,6 +59,16 @@ __device__ __forceinline__ uint32_t class_pixel(uint32_t L, uint64_t seed, uint3
 __device__ __forceinline__ uint32_t swap_kappa(uint64_t seed, uint32_t t, uint32_t s, uint32_t M) {
     return 1u + philox_seeded(seed, s, t, 0, 3).x % (M - 1u);
 }
+// SWAP partner of pixel p in pass t: invert class_pixel (class s = 8r + k, active index m), then
+// the pixel of m ^ kappa(t, s) in the same class.
+__device__ __forceinline__ uint32_t swap_partner(uint32_t L, uint64_t seed, uint32_t t, uint32_t p) {
+    const uint32_t nb = L >> 3, M = nb * nb, x = p & (L - 1), y = p / L;
+    const uint32_t along = (t & 1) ? y : x, across = (t & 1) ? x : y;
+    const uint32_t r = across & 7, b = across >> 3;
+    const uint32_t delta = philox_seeded(seed, b, t, r, 2).x & 7;
+    const uint32_t s = 8 * r + ((along - delta) & 7), m = b * nb + (along >> 3);
+    return class_pixel(L, seed, t, s, m ^ swap_kappa(seed, t, s, M));
+}
 // Same as class_pixel with delta(t, r, b) & 7 read from a per-pass table tab[r * nb + b].
 __device__ __forceinline__ uint32_t class_pixel_tab(const uint8_t* tab, uint32_t L, uint32_t t, uint32_t s,
                                                     uint32_t m) {
@@ -3125,7 +3135,8 @@ __global__ void __launch_bounds__(1024) k_finish_gather(uint8_t* __restrict__ ac
                                                        FinishPart* __restrict__ parts, unsigned int* __restrict__ ticket,
                                                        PassStatsDev* __restrict__ out,
                                                        const uint32_t* __restrict__ part_next, uint2* __restrict__ Un2,
-                                                       uint8_t* __restrict__ cn2, int* __restrict__ nn2) {
+                                                       uint8_t* __restrict__ cn2, int* __restrict__ nn2, uint32_t L,
+                                                       uint64_t seed, uint32_t pass_next) {
     const uint32_t nblk = gridDim.x, b = blockIdx.x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const uint32_t n16 = rowB / 16;
@@ -3138,7 +3149,9 @@ __global__ void __launch_bounds__(1024) k_finish_gather(uint8_t* __restrict__ ac
             if (lane == 0) U[p] = Un[p];
             if (lane < nl) nc[(size_t)p * nl + lane] = nn[(size_t)p * nl + lane];
         }
-        const uint32_t q = part_next[p];
+        uint32_t q = 0;
+        if (lane == 0) q = part_next ? part_next[p] : swap_partner(L, seed, pass_next, p);
+        q = __shfl_sync(0xffffffffu, q, 0);
         const bool a = acc[q] != 0;
         const uint4* src = reinterpret_cast<const uint4*>((a ? cn : c) + (size_t)q * rowB);
         uint4* dst = reinterpret_cast<uint4*>(cn2 + (size_t)p * rowB);
