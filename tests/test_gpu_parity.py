@@ -479,3 +479,39 @@ def test_best_of_k_resume(bn, oracle_mod):
     s, o, U = make(bn, oracle_mod, 32, 48, (16,))
     s.optimize(2, 4, K=3, stats=False)
     _check_run(s, o, o.optimize(U, passes=2, seed=4, K=3)[0], 2, 0, seed=4, first_pass=2, K=3)
+
+
+# ------------------------------------------------------------------------------- edge cases
+def test_edge_cases_empty_and_degenerate(bn, oracle_mod):
+    """Empty and degenerate inputs: T = 0 and out-of-range shards rejected; zero passes is a no-op;
+    a constant tile (every error vector equal, every D = 0: the energy maximum) optimises exactly
+    like the oracle; |a|, |b| beyond 2^15 rejected."""
+    s = bn.Sampler(0)
+    s.set_lattice(synth.D1, synth.D2, [16])
+    with pytest.raises(bn.BNError) as e:
+        s.set_bank(np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+    assert e.value.code == bn.BN_EINVAL
+    a, b, px, py = synth.make_bank(8, 3)
+    with pytest.raises(bn.BNError) as e:
+        s.set_bank(a, b, px, py, 5, 5)
+    assert e.value.code == bn.BN_EINVAL
+    with pytest.raises(bn.BNError) as e:
+        s.set_bank(np.full(8, 1 << 16, np.int32), b, px, py)
+    assert e.value.code == bn.BN_EINVAL
+    U = np.tile(synth.make_tile(1, 4), (256, 1))
+    s2, o, _ = make(bn, oracle_mod, 16, 24, (4, 16), U=U)
+    E0 = s2.energy()[0]
+    st, _ = s2.optimize(0, 1)
+    assert st == [] and s2.energy()[0] == E0 and np.array_equal(s2.get_tile(), U)
+    assert E0 == o.energy(o.counts(U))[0]
+    for mode in (0, 1):
+        s3, o3, _ = make(bn, oracle_mod, 16, 24, (4, 16), U=U)
+        _check_run(s3, o3, U, 3, mode, seed=31)
+
+
+def test_max_levels_and_spp(bn, oracle_mod):
+    """Eight progressive levels up to the maximum 128 spp (uint8 counts reach 128), ragged T."""
+    s, o, U = make(bn, oracle_mod, 16, 21, (1, 2, 4, 8, 16, 32, 64, 128))
+    assert np.array_equal(s.eval_counts(), o.counts(U))
+    _check_run(s, o, U, 2, 0, seed=33)
+    _check_run(s, o, s.get_tile(), 2, 1, seed=34, first_pass=2)
