@@ -1902,6 +1902,25 @@ __device__ __forceinline__ u128 warp_sum_u128(u128 v) {
     return ((u128)hi << 64) | lo;
 }
 
+// Exact warp sum of int64 partials whose total fits int64: four independent REDUX.SUM over 16-bit
+// limbs of the two's-complement value (each limb sum < 2^21), recombined mod 2^64.
+#ifndef BN_I64_REDUX
+#define BN_I64_REDUX 1  // 0: 5-step shuffle butterfly (C3 decide 0.073 vs 0.070 ms, C2 0.068 vs 0.058)
+#endif
+__device__ __forceinline__ long long warp_sum_i64(long long v) {
+    if (BN_I64_REDUX) {
+        const unsigned long long u = (unsigned long long)v;
+        unsigned long long r = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            r += (unsigned long long)__reduce_add_sync(0xffffffffu, (uint32_t)(u >> (16 * i)) & 0xffffu) << (16 * i);
+        return (long long)r;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 struct LutArgs {
     const double* G[8];  // per-level G tables
     int Dmax[8];         // largest legal D per level (guards corrupted distances)
@@ -2378,9 +2397,7 @@ struct WinTermsFlags32 : WinTerms<R> {
                 acc += sflags[q] != 0 ? this->v1[j] : this->v0[j];
             }
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        return (i128)acc;
+        return (i128)warp_sum_i64(acc);
     }
 };
 
@@ -2668,9 +2685,7 @@ struct WinTermsBits : WinTermsFlags32<R> {
                 acc += (sbits[q >> 5] >> (q & 31)) & 1u ? this->v1[j] : this->v0[j];
             }
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        return acc;
+        return warp_sum_i64(acc);
     }
 };
 template <int R, int mode>
