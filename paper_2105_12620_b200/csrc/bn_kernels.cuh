@@ -2968,16 +2968,15 @@ __device__ __forceinline__ i128 window_sum_snapshot(const DTabs T, uint32_t L, u
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     const int lane = threadIdx.x & 31;
     const uint32_t x = p % L, y = p / L;
-    i128 s = 0;
+    long long s = 0;  // exact: every term < 2^55, every window sum < 2^63 (R15)
     for (int w = lane; w < WN; w += 32) {
         const int ww = w >= R * (2 * R + 1) + R ? w + 1 : w;
         const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
         const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
         if (q == skip) continue;
-        const size_t idx = (size_t)p * WN + w;
-        s += get_term(__ldg(T.d0 + idx), T.x0, idx);
+        s += __ldg(T.d0 + (size_t)p * WN + w);
     }
-    return (i128)warp_sum_u128((u128)s);
+    return (i128)warp_sum_i64(s);
 }
 // One warp per couple: dE = 2 (sum_o' delta0[p][o] + sum_o' delta0[q][o]); accept iff dE < 0.
 // acc marks both members (k_finish commits their gathered rows), dEp holds the couple's dE once.
