@@ -150,7 +150,7 @@ struct bn_ctx {
     DevBuf<CountGroup> cgrp;  // packed fp32 operands of the filtered count test
     DevBuf<uint8_t> c, cn, cn2, acc, log, cexp;
     DevBuf<int> nc, nn, nn2, derr, progress;
-    DevBuf<uint32_t> perm, part;
+    DevBuf<uint32_t> perm, part, invperm;
     DevBuf<uint8_t> cnK;   // best-of-K candidates [K][P][rowB]
     DevBuf<uint2> UnK;
     DevBuf<int> nnK;
@@ -975,7 +975,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->Cc.release(); ctx->cgrp.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
         ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
         ctx->d0.release(); ctx->d1b.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
-        ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release(); ctx->cnK.release(); ctx->UnK.release(); ctx->nnK.release(); ctx->kpart.release(); ctx->kticket.release();
+        ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release(); ctx->invperm.release(); ctx->cnK.release(); ctx->UnK.release(); ctx->nnK.release(); ctx->kpart.release(); ctx->kticket.release();
         ctx->ev_tw.release(); ctx->ev_X1.release(); ctx->ev_h.release(); ctx->ev_rm.release(); ctx->ev_sp.release();
         ctx->ev_out.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1224,7 +1224,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     }
     // SWAP: the commit of pass t and the gather of pass t+1 run as one kernel (k_finish_gather), which
     // writes the next candidates into the other buffer of the pair
-    const bool fuse = prm->mode == BN_SWAP && !ctx->no_fuse && !ctx->old_swap_gather && prm->passes > 1;
+    const bool fuse = (prm->mode == BN_SWAP || paper) && !ctx->no_fuse && !ctx->old_swap_gather && prm->passes > 1;
     if (fuse) {
         CUDA_TRY(ctx->Un2.ensure(P));
         CUDA_TRY(ctx->cn2.ensure((size_t)P * ctx->rowB));
@@ -1270,16 +1270,17 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         const uint32_t t = prm->first_pass + pi;
         ctx->ls = cs;
 
-        if (paper) {
-            // couples of pass t -> partner map -> gathered partner rows; dEp is only written for
-            // couple members, so it is cleared for the exact pass sums of k_finish
-            CUDA_TRY(cudaMemsetAsync(ctx->part.p, 0xFF, (size_t)P * sizeof(uint32_t), cs));
-            CUDA_TRY(cudaMemsetAsync(ctx->dEp.p, 0, (size_t)P * sizeof(i128), cs));
+        if (paper && fuse && pi > 0) {
+            // candidates gathered by k_finish_gather of pass pi - 1
+        } else if (paper) {
+            // partner of every pixel from the inverse permutation, gathered partner rows (dEp is only
+            // written for couple members: the finish kernels leave it cleared after each pass)
+            if (pi == 0) CUDA_TRY(cudaMemsetAsync(ctx->dEp.p, 0, (size_t)P * sizeof(i128), cs));
             KSTART(BN_K_GATHER);
-            k_paper_pairs<<<(ncp + 255) / 256, 256, 0, cs>>>(ctx->perm.p, prm->seed, t, P, ncp, ctx->part.p);
-            LAUNCHED();
-            k_paper_gather<<<(P + 7) / 8, 256, 0, cs>>>(ctx->part.p, ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p,
-                                                        ctx->nc.p, ctx->nn.p, P, ctx->rowB, nl);
+            CUDA_TRY(launch_k(ctx, k_paper_gather, dim3((P + 7) / 8), dim3(256), 0, cs, (const uint32_t*)nullptr,
+                              (const uint2*)ctx->U.p, buf_U(pi), (const uint8_t*)ctx->c.p, buf_c(pi), (const int*)ctx->nc.p,
+                              buf_n(pi), P, ctx->rowB, nl, (const uint32_t*)ctx->perm.p, (const uint32_t*)ctx->invperm.p,
+                              prm->seed, t, budget));
             LAUNCHED_K();
         } else if (prm->mode == BN_REDRAW) {
             if (overlap && pi > 0) {
@@ -1300,7 +1301,8 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
                 LAUNCHED();
                 CUDA_TRY(launch_k(ctx, k_paper_gather, dim3((P + 7) / 8), dim3(256), 0, cs, (const uint32_t*)ctx->part.p,
                                   (const uint2*)ctx->U.p, buf_U(pi), (const uint8_t*)ctx->c.p, buf_c(pi),
-                                  (const int*)ctx->nc.p, buf_n(pi), P, ctx->rowB, nl));
+                                  (const int*)ctx->nc.p, buf_n(pi), P, ctx->rowB, nl, (const uint32_t*)nullptr,
+                                  (const uint32_t*)nullptr, (uint64_t)0, 0u, 0u));
             }
             LAUNCHED_K();
         }
@@ -1349,7 +1351,9 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
                               (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
                               ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, ctx->fparts.p,
                               ctx->ticket.p, ctx->pstats.p + pi, (const uint32_t*)nullptr, buf_U(pi + 1),
-                              buf_c(pi + 1), buf_n(pi + 1), ctx->L, prm->seed, t + 1));
+                              buf_c(pi + 1), buf_n(pi + 1), ctx->L, prm->seed, t + 1,
+                              paper ? (const uint32_t*)ctx->perm.p : (const uint32_t*)nullptr,
+                              paper ? (const uint32_t*)ctx->invperm.p : (const uint32_t*)nullptr, budget));
             LAUNCHED_K();
             continue;
         }
@@ -1357,7 +1361,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         CUDA_TRY(launch_k(ctx, k_finish, dim3(nfin), dim3(256), 0, cs, (const uint8_t*)ctx->acc.p, P, ctx->rowB, nl,
                           (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
                           ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, (int)(prm->mode != BN_REDRAW),
-                          ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi));
+                          ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi, (int)paper));
         LAUNCHED_K();
     }
     if (overlap) {
@@ -1494,9 +1498,13 @@ int bn_set_permutation(bn_ctx* ctx, const uint32_t* perm, uint32_t n) {
         seen[perm[j]] = 1;
     }
     DeviceGuard g(ctx->dev);
+    std::vector<uint32_t> inv(n);
+    for (uint32_t j = 0; j < n; ++j) inv[perm[j]] = j;
     CUDA_TRY(ctx->perm.ensure(n));
+    CUDA_TRY(ctx->invperm.ensure(n));
     CUDA_TRY(cudaMemcpyAsync(ctx->perm.p, perm, (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the caller's array may go away
+    CUDA_TRY(cudaMemcpyAsync(ctx->invperm.p, inv.data(), (size_t)n * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the caller's array and `inv` may go away
     ctx->perm_n = n;
     return BN_OK;
 }

@@ -2862,7 +2862,7 @@ __global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc,
                                                 const u128* __restrict__ Epart, uint32_t nEpart,
                                                 const i128* __restrict__ dEp, int swap_mode,
                                                 FinishPart* __restrict__ parts, unsigned int* __restrict__ ticket,
-                                                PassStatsDev* __restrict__ out) {
+                                                PassStatsDev* __restrict__ out, int clear_dEp) {
     const uint32_t nblk = gridDim.x, b = blockIdx.x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const uint32_t p0 = (uint32_t)((uint64_t)P * b / nblk), p1 = (uint32_t)((uint64_t)P * (b + 1) / nblk);
@@ -2881,8 +2881,10 @@ __global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc,
     unsigned a = 0;
     const uint32_t e0 = (uint32_t)((uint64_t)nEpart * b / nblk), e1 = (uint32_t)((uint64_t)nEpart * (b + 1) / nblk);
     for (uint32_t j = e0 + threadIdx.x; j < e1; j += blockDim.x) e += Epart[j];
+    i128* dEpw = const_cast<i128*>(dEp);  // the paper mode only rewrites its couples: clear after reading
     for (uint32_t j = p0 + threadIdx.x; j < p1; j += blockDim.x) {
         d += dEp[j];
+        if (clear_dEp) dEpw[j] = 0;
         a += acc[j];
     }
     __shared__ FinishPart s_w[32];
@@ -2936,6 +2938,13 @@ __global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc,
 __device__ __forceinline__ uint32_t paper_key(uint64_t seed, uint32_t t, uint32_t P) {
     return philox_seeded(seed, t, 0, 0, 5).x & (P - 1u);
 }
+// Partner of pixel p in pass t's couples (p itself if p is in none): p sits at position
+// j = invperm[p ^ key] of the scrambled sequence, and couples are consecutive positions.
+__device__ __forceinline__ uint32_t paper_partner(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ invperm,
+                                                  uint32_t key, uint32_t budget, uint32_t p) {
+    const uint32_t j = __ldg(invperm + (p ^ key));
+    return j < budget ? __ldg(perm + (j ^ 1u)) ^ key : p;
+}
 // part[p] = partner of p for the pixels of this pass's couples (0xFFFFFFFF elsewhere, memset).
 __global__ void k_paper_pairs(const uint32_t* __restrict__ perm, uint64_t seed, uint32_t pass_t, uint32_t P,
                               uint32_t ncp, uint32_t* __restrict__ part) {
@@ -2951,10 +2960,20 @@ __global__ void k_paper_pairs(const uint32_t* __restrict__ perm, uint64_t seed, 
 // One warp per pixel, 16-byte copies.
 __global__ void k_paper_gather(const uint32_t* __restrict__ part, const uint2* __restrict__ U, uint2* __restrict__ Un,
                                const uint8_t* __restrict__ c, uint8_t* __restrict__ cn, const int* __restrict__ nc,
-                               int* __restrict__ nn, uint32_t P, uint32_t rowB, uint32_t nl) {
+                               int* __restrict__ nn, uint32_t P, uint32_t rowB, uint32_t nl,
+                               const uint32_t* __restrict__ perm = nullptr, const uint32_t* __restrict__ invperm = nullptr,
+                               uint64_t seed = 0, uint32_t pass_t = 0, uint32_t budget = 0) {
     const uint32_t p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (p >= P) return;
-    const uint32_t q0 = __ldg(part + p), q = q0 == 0xFFFFFFFFu ? p : q0;
+    uint32_t q;
+    if (part) {
+        const uint32_t q0 = __ldg(part + p);
+        q = q0 == 0xFFFFFFFFu ? p : q0;
+    } else {  // paper mode: partner from the inverse permutation
+        q = 0;
+        if (lane == 0) q = paper_partner(perm, invperm, paper_key(seed, pass_t, P), budget, p);
+        q = __shfl_sync(0xffffffffu, q, 0);
+    }
     const uint4* src = reinterpret_cast<const uint4*>(c + (size_t)q * rowB);
     uint4* dst = reinterpret_cast<uint4*>(cn + (size_t)p * rowB);
     for (uint32_t j = lane; j < rowB / 16; j += 32) dst[j] = __ldg(src + j);
@@ -3150,7 +3169,9 @@ __global__ void __launch_bounds__(1024) k_finish_gather(uint8_t* __restrict__ ac
                                                        PassStatsDev* __restrict__ out,
                                                        const uint32_t* __restrict__ part_next, uint2* __restrict__ Un2,
                                                        uint8_t* __restrict__ cn2, int* __restrict__ nn2, uint32_t L,
-                                                       uint64_t seed, uint32_t pass_next) {
+                                                       uint64_t seed, uint32_t pass_next,
+                                                       const uint32_t* __restrict__ perm,
+                                                       const uint32_t* __restrict__ invperm, uint32_t budget) {
     const uint32_t nblk = gridDim.x, b = blockIdx.x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const uint32_t n16 = rowB / 16;
@@ -3164,7 +3185,10 @@ __global__ void __launch_bounds__(1024) k_finish_gather(uint8_t* __restrict__ ac
             if (lane < nl) nc[(size_t)p * nl + lane] = nn[(size_t)p * nl + lane];
         }
         uint32_t q = 0;
-        if (lane == 0) q = part_next ? part_next[p] : swap_partner(L, seed, pass_next, p);
+        if (lane == 0)
+            q = part_next ? part_next[p]
+                : perm    ? paper_partner(perm, invperm, paper_key(seed, pass_next, P), budget, p)
+                          : swap_partner(L, seed, pass_next, p);
         q = __shfl_sync(0xffffffffu, q, 0);
         const bool a = acc[q] != 0;
         const uint4* src = reinterpret_cast<const uint4*>((a ? cn : c) + (size_t)q * rowB);
@@ -3179,8 +3203,10 @@ __global__ void __launch_bounds__(1024) k_finish_gather(uint8_t* __restrict__ ac
     unsigned na = 0;
     const uint32_t e0 = (uint32_t)((uint64_t)nEpart * b / nblk), e1 = (uint32_t)((uint64_t)nEpart * (b + 1) / nblk);
     for (uint32_t j = e0 + threadIdx.x; j < e1; j += blockDim.x) e += Epart[j];
+    i128* dEpw = const_cast<i128*>(dEp);  // the paper mode only rewrites its couples: clear after reading
     for (uint32_t j = p0 + threadIdx.x; j < p1; j += blockDim.x) {
         d += dEp[j];
+        if (perm) dEpw[j] = 0;
         na += acc[j];
     }
     __shared__ FinishPart s_w[32];
