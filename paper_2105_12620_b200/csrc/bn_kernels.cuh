@@ -2945,16 +2945,6 @@ __device__ __forceinline__ uint32_t paper_partner(const uint32_t* __restrict__ p
     const uint32_t j = __ldg(invperm + (p ^ key));
     return j < budget ? __ldg(perm + (j ^ 1u)) ^ key : p;
 }
-// part[p] = partner of p for the pixels of this pass's couples (0xFFFFFFFF elsewhere, memset).
-__global__ void k_paper_pairs(const uint32_t* __restrict__ perm, uint64_t seed, uint32_t pass_t, uint32_t P,
-                              uint32_t ncp, uint32_t* __restrict__ part) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncp) return;
-    const uint32_t key = paper_key(seed, pass_t, P);
-    const uint32_t p = __ldg(perm + 2 * c) ^ key, q = __ldg(perm + 2 * c + 1) ^ key;
-    part[p] = q;
-    part[q] = p;
-}
 // cn_p = c_part(p), Un_p = U_part(p), nn_p = nc_part(p); pixels outside every couple take their own
 // rows (their dE terms are never read, but their distances must stay in the LUT range).
 // One warp per pixel, 16-byte copies.
