@@ -1474,8 +1474,14 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     // items: blocks in raster order within a level, levels outermost (each level's count slice is
     // an L2-resident working set); when following k_counts row by row (rows_done), the level is
     // the fastest index instead, so the Gram sweeps the tile's block rows front to back
+// Items block-major (the levels of a block consecutive) so that the window distances written last
+// are whole pixels' rows, which k_lut (BN_LUT_REVERSE) reads first while they are still in L2
+// (C3 lut 0.061 -> 0.058 ms, Gram unchanged).
+#ifndef BN_GRAM_BLOCK_MAJOR
+#define BN_GRAM_BLOCK_MAJOR 1
+#endif
     auto item_xyl = [&](uint32_t it, uint32_t& x0, uint32_t& y0, uint32_t& l) {
-        if (rows_done) {
+        if (rows_done || BN_GRAM_BLOCK_MAJOR) {
             l = it % nl;
             const uint32_t b = it / nl;
             x0 = 8 * (b % nbx);
@@ -1935,7 +1941,12 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
     constexpr int HP = half_count_padded(R), R0 = ru4(R), RW = ru4(2 * R + 1);
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     const uint32_t P = L * L;
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // (p, padded offset hp)
+#ifndef BN_LUT_REVERSE
+#define BN_LUT_REVERSE 1
+#endif
+    // (p, padded offset hp); BN_LUT_REVERSE: last-written window distances first (still in L2)
+    const size_t idx = BN_LUT_REVERSE ? (size_t)(gridDim.x - 1 - blockIdx.x) * blockDim.x + threadIdx.x
+                                      : (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long e = 0;  // < 2 * 8 * 2^52 = 2^56 per thread, < 2^61 per warp
     const uint32_t p = (uint32_t)(idx / HP), hp = (uint32_t)(idx - (size_t)p * HP);
     int ox, oy;
