@@ -429,7 +429,14 @@ __device__ __forceinline__ void dt_put(int4* Dt, size_t n, size_t idx, int4 d) {
     dt_plane(Dt, n, 0)[idx] = make_int2(d.x, d.y);
     dt_plane(Dt, n, 1)[idx] = make_int2(d.z, d.w);
 }
+#ifndef BN_DT_LDCS
+#define BN_DT_LDCS 1  // C3 decide 0.0695 -> 0.066 ms: the dE tables written by k_lut stay in L2
+#endif
 __device__ __forceinline__ int4 dt_get(const int4* Dt, size_t n, size_t idx) {
+    if (BN_DT_LDCS) {  // streaming loads: read once, keep the freshly written dE tables in L2 instead
+        const int2 a = __ldcs(reinterpret_cast<const int2*>(Dt) + idx), b = __ldcs(reinterpret_cast<const int2*>(Dt) + n + idx);
+        return make_int4(a.x, a.y, b.x, b.y);
+    }
     const int2 a = __ldg(reinterpret_cast<const int2*>(Dt) + idx), b = __ldg(reinterpret_cast<const int2*>(Dt) + n + idx);
     return make_int4(a.x, a.y, b.x, b.y);
 }
