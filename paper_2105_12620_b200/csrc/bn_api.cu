@@ -160,7 +160,7 @@ struct bn_ctx {
     DevBuf<double> ev_h, ev_rm, ev_sp, ev_out;  // BN_PAPER_SWAP: precomputed permutation, per-pass partner map
     uint32_t perm_n = 0;
     DevBuf<int4> Dt;
-    DevBuf<long long> d0, d1b;   // int64 dE terms (DT_ESC = see escape tables)
+    DevBuf<longlong2> d0;        // int64 dE terms {delta0, delta1} per (pixel, offset) (DT_ESC = see escape tables)
     DevBuf<longlong2> x0, x1;    // exact int128 escape tables (sparse writes)
     DevBuf<i128> dEp;
     DevBuf<u128> Epart;
@@ -399,7 +399,6 @@ int ensure_work(bn_ctx* ctx) {
     const size_t P = ctx->P, H = half_count_padded(ctx->R), WN = win_count(ctx->R);
     CUDA_TRY(ctx->Dt.ensure(P * H * ctx->nl));  // two int2 planes over [l][p][padded h]
     CUDA_TRY(ctx->d0.ensure(P * WN));
-    CUDA_TRY(ctx->d1b.ensure(P * WN));
     CUDA_TRY(ctx->acc.ensure(P));
     CUDA_TRY(ctx->dEp.ensure(P));
     CUDA_TRY(ctx->Epart.ensure((P * H + 255) / 256));
@@ -532,7 +531,7 @@ int launch_lut_only(bn_ctx* ctx, int write_deltas) {
     {
         auto fn = ctx->nl == 4 ? k_lut<R, 4> : ctx->nl == 1 ? k_lut<R, 1> : k_lut<R, 0>;
         CUDA_TRY(launch_k(ctx, fn, dim3((unsigned)((nthr + 255) / 256)), dim3(256), 0, ctx->ls, ctx->Dt.p, ctx->L, ctx->nl,
-                          ctx->W.p, la, write_deltas, ctx->d0.p, ctx->d1b.p, ctx->Epart.p, ctx->derr.p));
+                          ctx->W.p, la, write_deltas, ctx->d0.p, ctx->Epart.p, ctx->derr.p));
     }
     LAUNCHED_K();
     return BN_OK;
@@ -572,7 +571,7 @@ template <int R>
 int launch_decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, uint8_t* log) {
     const uint32_t M = (ctx->L / 8) * (ctx->L / 8);
     KSTART(BN_K_DECIDE);
-    const DTabs T = {ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
+    const DTabs T = {ctx->d0.p, ctx->x0.p, ctx->x1.p};
     k_decide<R><<<(M + 3) / 4, 128, 0, ctx->ls>>>(s, t, seed, ctx->L, mode, T, ctx->acc.p, ctx->dEp.p, log);
     LAUNCHED_K();
     return BN_OK;
@@ -616,7 +615,7 @@ int launch_decide_big(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t*
         return BN_OK;
     }
     uint32_t L = ctx->L;
-    const DTabs T = {ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
+    const DTabs T = {ctx->d0.p, ctx->x0.p, ctx->x1.p};
     uint8_t* acc = ctx->acc.p;
     i128* dEp = ctx->dEp.p;
     void* args[] = {&t, &seed, &L, &spw, (void*)&T, &acc, &dEp, &log};
@@ -678,7 +677,7 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
         return BN_OK;  // cluster does not fit: persistent flag kernel instead
     }
     uint32_t L = ctx->L;
-    const DTabs T = {ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
+    const DTabs T = {ctx->d0.p, ctx->x0.p, ctx->x1.p};
     uint8_t* acc = ctx->acc.p;
     i128* dEp = ctx->dEp.p;
     void* args[] = {&t, &seed, &L, &cpc, (void*)&T, &acc, &dEp, &log};
@@ -724,7 +723,7 @@ int launch_decide_pass(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t
     CUDA_TRY(ctx->progress.ensure(ncta));
     CUDA_TRY(cudaMemsetAsync(ctx->progress.p, 0, ncta * sizeof(int), ctx->ls));
     uint32_t L = ctx->L;
-    const DTabs T = {ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
+    const DTabs T = {ctx->d0.p, ctx->x0.p, ctx->x1.p};
     uint8_t* acc = ctx->acc.p;
     i128* dEp = ctx->dEp.p;
     int* prog = ctx->progress.p;
@@ -769,7 +768,7 @@ int decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, uint8_t
 
 template <int R>
 int launch_paper_decide(bn_ctx* ctx, uint32_t t, uint64_t seed, uint32_t ncp, uint8_t* log) {
-    const DTabs T{ctx->d0.p, ctx->d1b.p, ctx->x0.p, ctx->x1.p};
+    const DTabs T{ctx->d0.p, ctx->x0.p, ctx->x1.p};
     KSTART(BN_K_DECIDE);
     k_paper_decide<R><<<(ncp + 7) / 8, 256, 0, ctx->ls>>>(ctx->perm.p, seed, t, ctx->L, ncp, T, ctx->acc.p,
                                                           ctx->dEp.p, log);
@@ -974,7 +973,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->S.release(); ctx->U.release(); ctx->Un.release(); ctx->pxy.release(); ctx->ab.release();
         ctx->Cc.release(); ctx->cgrp.release(); ctx->c.release(); ctx->cn.release(); ctx->acc.release(); ctx->log.release();
         ctx->cexp.release(); ctx->nc.release(); ctx->nn.release(); ctx->derr.release(); ctx->progress.release(); ctx->Dt.release();
-        ctx->d0.release(); ctx->d1b.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
+        ctx->d0.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
         ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release(); ctx->invperm.release(); ctx->cnK.release(); ctx->UnK.release(); ctx->nnK.release(); ctx->kpart.release(); ctx->kticket.release();
         ctx->ev_tw.release(); ctx->ev_X1.release(); ctx->ev_h.release(); ctx->ev_rm.release(); ctx->ev_sp.release();
         ctx->ev_out.release();

@@ -1871,9 +1871,9 @@ __device__ __forceinline__ unsigned long long qterm(double w, const double* __re
 // invariant |term| < 2^55 is checked here (err flag 2).
 constexpr long long DT_ESC = (long long)0x8000000000000000ull;
 constexpr long long TERM_MAX = 1ll << 55;
-__device__ __forceinline__ void put_term(long long* d, size_t idx, long long v, int* err) {
-    if (v >= TERM_MAX || v <= -TERM_MAX) atomicOr(err, 2);
-    d[idx] = v;
+__device__ __forceinline__ void put_terms(longlong2* d, size_t idx, long long v0, long long v1, int* err) {
+    if (v0 >= TERM_MAX || v0 <= -TERM_MAX || v1 >= TERM_MAX || v1 <= -TERM_MAX) atomicOr(err, 2);
+    d[idx] = make_longlong2(v0, v1);
 }
 __device__ __forceinline__ i128 get_term(long long v, const longlong2* __restrict__ x, size_t idx) {
     if (v != DT_ESC) return (i128)v;
@@ -1881,8 +1881,7 @@ __device__ __forceinline__ i128 get_term(long long v, const longlong2* __restric
     return ((i128)e.y << 64) | (u128)(unsigned long long)e.x;
 }
 struct DTabs {
-    const long long* d0;
-    const long long* d1;
+    const longlong2* d;  // {delta0, delta1} interleaved per (pixel, offset): one 16-B access per term
     const longlong2* x0;
     const longlong2* x1;
 };
@@ -1943,8 +1942,7 @@ struct LutArgs {
 template <int R, int NL>
 __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32_t L, uint32_t nl_rt,
                                              const double* __restrict__ W, LutArgs lut, int write_deltas,
-                                             long long* __restrict__ d0, long long* __restrict__ d1,
-                                             u128* __restrict__ Epart, int* __restrict__ err) {
+                                             longlong2* __restrict__ d, u128* __restrict__ Epart, int* __restrict__ err) {
     constexpr int HP = half_count_padded(R), R0 = ru4(R), RW = ru4(2 * R + 1);
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     const uint32_t P = L * L;
@@ -1997,10 +1995,8 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
         }
         e *= 2;  // ordered pairs (p,q) and (q,p)
         if (write_deltas) {
-            put_term(d0, (size_t)p * WN + wi, a0, err);
-            put_term(d1, (size_t)p * WN + wi, a1, err);
-            put_term(d0, (size_t)q * WN + wm, b0, err);
-            put_term(d1, (size_t)q * WN + wm, b1, err);
+            put_terms(d, (size_t)p * WN + wi, a0, a1, err);
+            put_terms(d, (size_t)q * WN + wm, b0, b1, err);
         }
     }
     // block reduction of e: exact warp sums of 16-bit limbs (REDUX), then the 8 warp partials
@@ -2032,7 +2028,8 @@ __device__ __forceinline__ i128 window_sum(const DTabs T, const uint8_t* __restr
         const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
         const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
         const size_t idx = (size_t)p * WN + w;
-        s += acc[q] ? get_term(T.d1[idx], T.x1, idx) : get_term(T.d0[idx], T.x0, idx);
+        const longlong2 t = T.d[idx];
+        s += acc[q] ? get_term(t.y, T.x1, idx) : get_term(t.x, T.x0, idx);
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
@@ -2099,15 +2096,16 @@ struct WinTerms {
     static constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     static constexpr int PER = (WN + 31) / 32;
     long long v0[PER], v1[PER];
-    // from the shared-memory staging buffer: a row of WN delta0 terms then WN delta1 terms
+    // from the shared-memory staging buffer: a row of WN {delta0, delta1} pairs
     __device__ __forceinline__ void load_smem(const long long* row) {
         const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int w = lane + 32 * j;
             if (w < WN) {
-                v0[j] = row[w];
-                v1[j] = row[WN + w];
+                const longlong2 t = reinterpret_cast<const longlong2*>(row)[w];
+                v0[j] = t.x;
+                v1[j] = t.y;
             }
         }
     }
@@ -2142,19 +2140,18 @@ struct WinTerms {
 
 // Stage the dE-term rows (delta0, delta1) of the candidates of CTA `g` for class s into smem.
 // Slot j holds candidate m = first + j (and, for SWAP, slot cpc + j its partner's rows); warp w
-// copies slots w, w + nwarps, ... (row = WN int64 delta0 terms then WN delta1 terms).
+// copies slots w, w + nwarps, ... (row = WN {delta0, delta1} int64 pairs).
 template <int R>
 __device__ __forceinline__ void stage_class(uint32_t smem_base, const uint32_t* slot_pix, uint32_t nslot,
                                             const DTabs T) {
-    constexpr int WN = WinTerms<R>::WN, NC = WN / 2;  // 16-B chunks per table row
+    constexpr int WN = WinTerms<R>::WN, NC = WN;  // 16-B chunks ({delta0, delta1} pairs) per table row
     const uint32_t warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t slot = warp; slot < nslot; slot += nwarps) {
         const size_t off = (size_t)slot_pix[slot] * WN;
         const uint32_t dst = smem_base + slot * 2 * WN * 8;
 #pragma unroll
         for (uint32_t c = lane; c < (uint32_t)NC; c += 32) {
-            cp_async16(dst + c * 16, T.d0 + off + 2 * c);
-            cp_async16(dst + (NC + c) * 16, T.d1 + off + 2 * c);
+            cp_async16(dst + c * 16, T.d + off + c);
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -2389,15 +2386,14 @@ struct WinTermsFlags32 : WinTerms<R> {
     __device__ __forceinline__ void load_global(const DTabs T, uint32_t pix) {
         constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
         const int lane = threadIdx.x & 31;
-        const long long* r0 = T.d0 + (size_t)pix * WN;
-        const long long* r1 = T.d1 + (size_t)pix * WN;
+        const longlong2* r = T.d + (size_t)pix * WN;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int w = lane + 32 * j;
-            if (w < WN) {
-                asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(this->v0[j]) : "l"(r0 + w));
-                asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(this->v1[j]) : "l"(r1 + w));
-            }
+            if (w < WN)
+                asm volatile("ld.global.nc.L1::no_allocate.v2.b64 {%0, %1}, [%2];"
+                             : "=l"(this->v0[j]), "=l"(this->v1[j])
+                             : "l"(r + w));
         }
     }
     // exact int64 window sum (|term| < 2^55, <= 224 terms: |sum| < 2^63), warp-reduced in int64
@@ -2437,7 +2433,7 @@ __global__ void __launch_bounds__(512, 1) k_decide_cl2(uint32_t pass_t, uint64_t
                                                        const DTabs T, uint8_t* __restrict__ acc,
                                                        i128* __restrict__ dEp, uint8_t* __restrict__ log) {
     constexpr int WN = WinTerms<R>::WN;
-    constexpr uint32_t ROWB = 2 * WN * 8;   // one slot: delta0 row then delta1 row (int64)
+    constexpr uint32_t ROWB = 2 * WN * 8;   // one slot: WN {delta0, delta1} int64 pairs
     constexpr uint32_t NSW = mode ? 2 : 1;  // slots per warp (SWAP: the candidate and its partner)
     extern __shared__ __align__(16) uint8_t dsm[];
     __shared__ uint8_t sDelta[8 * 16];
@@ -2484,8 +2480,7 @@ __global__ void __launch_bounds__(512, 1) k_decide_cl2(uint32_t pass_t, uint64_t
             for (uint32_t i = 0; i < NSW; ++i) {
                 const uint32_t pix = sSlot[s * per_class + (i ? cpc : 0) + warp];
                 const uint32_t dst = sbase + b * buf_bytes + (warp * NSW + i) * ROWB;
-                bulk_g2s(dst, T.d0 + (size_t)pix * WN, WN * 8, bar);
-                bulk_g2s(dst + WN * 8, T.d1 + (size_t)pix * WN, WN * 8, bar);
+                bulk_g2s(dst, T.d + (size_t)pix * WN, 2 * WN * 8, bar);
             }
         }
     };
@@ -3001,7 +2996,7 @@ __device__ __forceinline__ i128 window_sum_snapshot(const DTabs T, uint32_t L, u
         const int oy = ww / (2 * R + 1) - R, ox = ww % (2 * R + 1) - R;
         const uint32_t q = ((y + oy + L) & (L - 1)) * L + ((x + ox + L) & (L - 1));
         if (q == skip) continue;
-        s += __ldg(T.d0 + (size_t)p * WN + w);
+        s += __ldg(reinterpret_cast<const long long*>(T.d) + 2 * ((size_t)p * WN + w));  // delta0
     }
     return (i128)warp_sum_i64(s);
 }
