@@ -1201,11 +1201,12 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     int nsm_fin = 148;
     cudaDeviceGetAttribute(&nsm_fin, cudaDevAttrMultiProcessorCount, ctx->dev);
     const uint32_t nfin = (uint32_t)(2 * nsm_fin) < P / 16 ? (uint32_t)(2 * nsm_fin) : (P / 16);
+    const uint32_t nfin_g = (uint32_t)(BN_FG_BPS * nsm_fin) < P / 16 ? (uint32_t)(BN_FG_BPS * nsm_fin) : (P / 16);
     if (!ctx->ticket.p) {
         CUDA_TRY(ctx->ticket.ensure(1));
         CUDA_TRY(cudaMemsetAsync(ctx->ticket.p, 0, sizeof(unsigned int), ctx->stream));
     }
-    CUDA_TRY(ctx->fparts.ensure(nfin));
+    CUDA_TRY(ctx->fparts.ensure(nfin > nfin_g ? nfin : nfin_g));
     if (accept_log) CUDA_TRY(ctx->log.ensure((size_t)prm->passes * 64 * M));
     CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
     // accept flags start at zero; k_finish clears them again after every pass
@@ -1346,7 +1347,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         if (fuse && pi + 1 < prm->passes) {
             // the next pass's partners are computed in k_finish_gather itself (swap_partner)
             KSTART(BN_K_COMMIT);
-            CUDA_TRY(launch_k(ctx, k_finish_gather, dim3(nfin), dim3(1024), 0, cs, ctx->acc.p, P, ctx->rowB, nl,
+            CUDA_TRY(launch_k(ctx, k_finish_gather, dim3(nfin_g), dim3(BN_FG_THREADS), 0, cs, ctx->acc.p, P, ctx->rowB, nl,
                               (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
                               ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, ctx->fparts.p,
                               ctx->ticket.p, ctx->pstats.p + pi, (const uint32_t*)nullptr, buf_U(pi + 1),

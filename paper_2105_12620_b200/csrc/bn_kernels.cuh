@@ -3162,7 +3162,16 @@ __global__ void __launch_bounds__(256) k_ev_spectrum(const double* __restrict__ 
 //            sees either an untouched c row or the candidate row: no ordering between warps needed)
 // plus the exact pass sums of k_finish (per-block partials, last-block reduction), which also
 // clears the accept flags once every block has read them.
-__global__ void __launch_bounds__(1024) k_finish_gather(uint8_t* __restrict__ acc, uint32_t P, uint32_t rowB,
+#ifndef BN_FG_THREADS
+#define BN_FG_THREADS 1024  // k_finish_gather block size
+#endif
+#ifndef BN_FG_MINB
+#define BN_FG_MINB 1  // resident blocks per SM requested from ptxas
+#endif
+#ifndef BN_FG_BPS
+#define BN_FG_BPS 1  // k_finish_gather blocks per SM in the grid (one wave: C3 commit 0.0395 -> 0.036 ms vs 2)
+#endif
+__global__ void __launch_bounds__(BN_FG_THREADS, BN_FG_MINB) k_finish_gather(uint8_t* __restrict__ acc, uint32_t P, uint32_t rowB,
                                                        uint32_t nl, const uint2* __restrict__ Un, uint2* __restrict__ U,
                                                        const uint8_t* __restrict__ cn, uint8_t* __restrict__ c,
                                                        const int* __restrict__ nn, int* __restrict__ nc,
