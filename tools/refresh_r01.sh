@@ -16,6 +16,6 @@ python bench.py --config C5 --mode redraw --steps 5 --warmup 3 --cpu-classes 1 -
 python bench.py --config C3 --mode redraw --K 4 --steps 5 --warmup 3 --cpu-classes 2 --e2e-steps 2 >> $out 2> gpurun_out/bench_C3k4.err; echo C3k4 rc=$?
 python bench.py --impl reference --steps 5 --warmup 3 >> $out 2> gpurun_out/bench_ref.err; echo ref rc=$?
 nproc; lscpu | grep "Model name"
-bash tools/gpu_ncu_multi.sh r01y k_gram_tc4 k_decide_swap k_lut k_finish_gather
+bash tools/gpu_ncu_multi.sh r01z k_gram_tc4 k_decide_swap k_lut k_finish_gather
 bash tools/gpu_ncu_c5.sh
 ls gpurun_out
