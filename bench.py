@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--K", type=int, default=1, help="best-of-K re-draws (REDRAW only; K candidates per pixel)")
     ap.add_argument("--energy", choices=["gf", "eq1", "eq1max"], default="gf",
                     help="energy form: north-star GF (default), Eq. 1 as written, Eq. 1 maximised")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--e2e-tiles", type=int, default=2, help="independent tiles (contexts, streams) in flight in the e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-classes", type=int, default=12, help="colour classes in the oracle sample")
     return ap.parse_args()
@@ -408,21 +409,26 @@ def run_ours(args, cfg):
     # alternate, and step k+1 is enqueued before step k's result is read, so one tile's upload and
     # count rebuild overlap the other's pass -- a serving loop over a stream of tiles.
     U_e2e, (ea, eb, epx, epy) = synth.problem_inputs(cfg, pairs[0])
-    e_stream = torch.cuda.Stream()
-    s_b = bn.Sampler(local, e_stream.cuda_stream)
-    s_b.set_lattice(synth.D1, synth.D2, cfg.levels)
-    if banksharded:
-        from paper_2105_12620_b200.dist import make_bank_sharded
+    NT = max(2, args.e2e_tiles)
+    e_streams, extra = [], []
+    for _ in range(NT - 1):
+        e_stream = torch.cuda.Stream()
+        s_b = bn.Sampler(local, e_stream.cuda_stream)
+        s_b.set_lattice(synth.D1, synth.D2, cfg.levels)
+        if banksharded:
+            from paper_2105_12620_b200.dist import make_bank_sharded
 
-        make_bank_sharded(s_b, ea, eb, epx, epy, rank, world)
-    else:
-        s_b.set_bank(ea, eb, epx, epy)
-    s_b.set_energy(2.1, 1.0, 7)
-    s_b.set_energy_form({"gf": 0, "eq1": 1, "eq1max": 2}[args.energy])
-    s_b.set_tile(cfg.L, U_e2e)
-    if cfg.mode == 2:
-        s_b.set_permutation(synth.make_permutation(P, seeds[0]))
-    ctxs = [s, s_b]
+            make_bank_sharded(s_b, ea, eb, epx, epy, rank, world)
+        else:
+            s_b.set_bank(ea, eb, epx, epy)
+        s_b.set_energy(2.1, 1.0, 7)
+        s_b.set_energy_form({"gf": 0, "eq1": 1, "eq1max": 2}[args.energy])
+        s_b.set_tile(cfg.L, U_e2e)
+        if cfg.mode == 2:
+            s_b.set_permutation(synth.make_permutation(P, seeds[0]))
+        e_streams.append(e_stream)
+        extra.append(s_b)
+    ctxs = [s] + extra
     pins = []
     for c_ in ctxs:
         pb = torch.empty((P, 2), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
@@ -432,36 +438,40 @@ def run_ours(args, cfg):
     K_ = cfg.extra.get("K", 1)
 
     def enqueue(k):
-        c_ = ctxs[k % 2]
-        c_.set_tile(cfg.L, pins[k % 2])
-        c_.optimize(1, seeds[0], mode=cfg.mode, first_pass=first + k // 2, stats=False, K=K_)
+        c_ = ctxs[k % NT]
+        c_.set_tile(cfg.L, pins[k % NT])
+        c_.optimize(1, seeds[0], mode=cfg.mode, first_pass=first + k // NT, stats=False, K=K_)
 
-    for k in range(4):  # warm-up of the second context (its work buffers are allocated on first use)
+    for k in range(2 * NT):  # warm-up of the other contexts (their work buffers are allocated on first use)
         enqueue(k)
-        ctxs[k % 2].get_tile(pins[k % 2])
+        ctxs[k % NT].get_tile(pins[k % NT])
     first += 2
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(streams[0])
-    e_stream.wait_event(f0)
-    enqueue(0)
+    for es in e_streams:
+        es.wait_event(f0)
+    for k in range(min(NT - 1, args.e2e_steps)):
+        enqueue(k)
     for k in range(args.e2e_steps):
-        if k + 1 < args.e2e_steps:
-            enqueue(k + 1)
-        ctxs[k % 2].get_tile(pins[k % 2])  # D2H of step k's result (synchronises its stream)
-    ej = torch.cuda.Event()
-    ej.record(e_stream)
-    streams[0].wait_event(ej)
+        if k + NT - 1 < args.e2e_steps:
+            enqueue(k + NT - 1)
+        ctxs[k % NT].get_tile(pins[k % NT])  # D2H of step k's result (synchronises its stream)
+    for es in e_streams:
+        ej = torch.cuda.Event()
+        ej.record(es)
+        streams[0].wait_event(ej)
     f1.record(streams[0])
     barrier()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
     E_after = s.energy()[1]
-    s_b.close()
+    for s_b in extra:
+        s_b.close()
     e2e_units = EP * (1 if banksharded else world)
     e2e = {"value": e2e_units * args.e2e_steps / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": P * 8, "d2h_bytes_per_step": P * 8,
            "path": ("per step: bn_set_tile(pinned host tile) + bn_optimize(1 pass) + bn_get_tile(pinned host), "
-                    "two independent tiles on two streams, step k+1 enqueued before step k's result is read")}
+                    f"{NT} independent tiles on {NT} streams, steps up to k+{NT - 1} enqueued before step k's result is read")}
     del U0
 
     launches = sum_over_ranks(launches)  # total over all ranks
