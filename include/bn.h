@@ -159,6 +159,13 @@ typedef struct {
 int bn_optimize(bn_ctx *ctx, const bn_opt_params *params, bn_pass_stats *stats,
                 uint8_t *accept_log);
 
+/* Synchronise the context's stream and report the device invariant flag: every launch since the
+ * flag was last read ORs into it (window distance outside [0, T N_l^2]; an exact dE term outside
+ * +-2^55 (reading R15); a pass whose recomputed start energy differs from the previous pass's
+ * E + sum dE).  bn_optimize with stats/accept_log and bn_energy read it too; reading clears it.
+ * BN_OK if clean, BN_ESTATE (message in bn_last_error) if an invariant failed. */
+int bn_check(bn_ctx *ctx);
+
 /* Evaluation criterion (§3.3 l.270-284, teaser (c) "||(I_N (*) k_sigma) - I_ref||";
  * SURVEY §8 f2) of the current tile at progressive level `level`, over this context's integrand
  * shard [t_begin, t_end) (Ts integrands), error images e_i(p) = c_l,p,i / N_l - I_ref,i:

@@ -26,7 +26,7 @@ SYMBOLS = ("bn_create", "bn_destroy", "bn_last_error", "bn_version", "bn_set_lat
            "bn_get_references", "bn_set_energy", "bn_set_tile", "bn_get_tile", "bn_eval_counts", "bn_energy",
            "bn_optimize", "bn_comm_init", "bn_comm_unique_id", "bn_launch_count", "bn_profile_enable",
            "bn_profile_get", "bn_window_distances", "bn_set_permutation",
-           "bn_set_energy_form", "bn_eval_quality")
+           "bn_set_energy_form", "bn_eval_quality", "bn_check")
 KERNELS = ("counts", "gather", "gram", "lut", "decide", "stats", "commit")
 
 
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH):
         "bn_optimize": ([vp, ctypes.POINTER(OptParams), vp, vp], ctypes.c_int),
         "bn_comm_init": ([vp, vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "bn_comm_unique_id": ([vp], ctypes.c_int),
+        "bn_check": ([vp], ctypes.c_int),
         "bn_launch_count": ([vp], u64),
         "bn_profile_enable": ([vp, ctypes.c_int], ctypes.c_int),
         "bn_window_distances": ([vp, vp, ctypes.c_int], ctypes.c_int),
@@ -92,17 +93,25 @@ def load_library(path: str = LIB_PATH):
     return lib
 
 
-def _ptr(x):
-    """(pointer, is_device) of a numpy array or torch tensor (contiguous)."""
+def _ptr(x, n: int | None = None, dtype=None):
+    """(pointer, is_device) of a numpy array or torch tensor (contiguous).  With `n` / `dtype`,
+    the buffer must hold exactly n elements of that numpy dtype (the C side trusts the size)."""
     if isinstance(x, np.ndarray):
         if not x.flags["C_CONTIGUOUS"]:
             raise ValueError("array must be C-contiguous")
-        return x.ctypes.data, 0
-    if hasattr(x, "data_ptr"):
+        got_dt, got_n, ptr, dev = x.dtype, x.size, x.ctypes.data, 0
+    elif hasattr(x, "data_ptr"):
         if not x.is_contiguous():
             raise ValueError("tensor must be contiguous")
-        return x.data_ptr(), int(x.is_cuda)
-    raise TypeError(f"unsupported buffer type {type(x)}")
+        got_dt = np.dtype(str(x.dtype).replace("torch.", ""))
+        got_n, ptr, dev = x.numel(), x.data_ptr(), int(x.is_cuda)
+    else:
+        raise TypeError(f"unsupported buffer type {type(x)}")
+    if dtype is not None and got_dt != np.dtype(dtype):
+        raise TypeError(f"buffer dtype {got_dt}, expected {np.dtype(dtype)}")
+    if n is not None and got_n != n:
+        raise ValueError(f"buffer holds {got_n} elements, expected {n}")
+    return ptr, dev
 
 
 def comm_unique_id() -> bytes:
@@ -131,6 +140,7 @@ class Sampler:
         self.device, self.stream = device, stream
         self.L = self.T = self.Ts = 0
         self.levels: tuple = ()
+        self.radius = 7
 
     def close(self):
         if getattr(self, "_ctx", None) and self._ctx.value:
@@ -169,27 +179,28 @@ class Sampler:
 
     def set_energy(self, sigma_i: float = 2.1, sigma_s: float = 1.0, radius: int = 7):
         self._check(self._lib.bn_set_energy(self._ctx, sigma_i, sigma_s, radius))
+        self.radius = radius
 
     def set_energy_form(self, form: int = E_GF):
         """Energy g(D): E_GF (default), E_EQ1 (Eq. 1 as written, minimised), E_EQ1_MAX (Eq. 1 maximised)."""
         self._check(self._lib.bn_set_energy_form(self._ctx, form))
 
     def set_tile(self, L: int, u_xy):
-        ptr, dev = _ptr(u_xy)
+        ptr, dev = _ptr(u_xy, 2 * L * L, np.uint32)
         self._check(self._lib.bn_set_tile(self._ctx, L, ptr, dev))
         self.L = L
 
     def get_tile(self, out=None):
         if out is None:
             out = np.zeros((self.L * self.L, 2), np.uint32)
-        ptr, dev = _ptr(out)
+        ptr, dev = _ptr(out, 2 * self.L * self.L, np.uint32)
         self._check(self._lib.bn_get_tile(self._ctx, ptr, dev))
         return out
 
     def eval_counts(self, out=None):
         if out is None:
             out = np.zeros((len(self.levels), self.L * self.L, self.Ts), np.uint8)
-        ptr, dev = _ptr(out)
+        ptr, dev = _ptr(out, len(self.levels) * self.L * self.L * self.Ts, np.uint8)
         self._check(self._lib.bn_eval_counts(self._ctx, ptr, dev))
         return out
 
@@ -242,14 +253,20 @@ class Sampler:
                                               prof.ctypes.data if prof is not None else None))
         return r, S, prof
 
-    def window_distances(self, radius: int = 7, out=None):
-        """Partial (this bank shard) window distances D_l(p, p+o), [levels, P, H] int32."""
-        H = 2 * radius * radius + 2 * radius
+    def window_distances(self, out=None):
+        """Partial (this bank shard) window distances D_l(p, p+o), [levels, P, H] int32,
+        H = 2R^2 + 2R for the radius of the last set_energy."""
+        H = 2 * self.radius * self.radius + 2 * self.radius
+        n = len(self.levels) * self.L * self.L * H
         if out is None:
             out = np.zeros((len(self.levels), self.L * self.L, H), np.int32)
-        ptr, dev = _ptr(out)
+        ptr, dev = _ptr(out, n, np.int32)
         self._check(self._lib.bn_window_distances(self._ctx, ptr, dev))
         return out
+
+    def check(self):
+        """Synchronise and raise BNError(BN_ESTATE) if any device invariant failed since the last read."""
+        self._check(self._lib.bn_check(self._ctx))
 
     def comm_init(self, uid: bytes, rank: int, world: int):
         self._check(self._lib.bn_comm_init(self._ctx, uid, rank, world))

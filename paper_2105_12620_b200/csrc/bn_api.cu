@@ -402,7 +402,10 @@ int ensure_work(bn_ctx* ctx) {
     CUDA_TRY(ctx->acc.ensure(P));
     CUDA_TRY(ctx->dEp.ensure(P));
     CUDA_TRY(ctx->Epart.ensure((P * H + 255) / 256));
-    CUDA_TRY(ctx->derr.ensure(1));
+    if (!ctx->derr.p) {  // the device error flag is sticky: cleared only when read (read_err_flag)
+        CUDA_TRY(ctx->derr.ensure(1));
+        CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
+    }
     return BN_OK;
 }
 
@@ -788,13 +791,19 @@ int paper_decide(bn_ctx* ctx, uint32_t t, uint64_t seed, uint32_t ncp, uint8_t* 
     }
 }
 
+// The device error flag accumulates every invariant failure of every launch since it was last
+// read (bits: 1 window distance outside [0, T N^2], 2 dE term outside +-2^55, 4 a pass's
+// recomputed start energy != the previous pass's E + sum dE); reading it clears it.
 int read_err_flag(bn_ctx* ctx) {
+    if (!ctx->derr.p) return BN_OK;
     int h = 0;
     CUDA_TRY(cudaMemcpyAsync(&h, ctx->derr.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (!h) return BN_OK;
+    CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
     if (h & 1) return fail(ctx, BN_ESTATE, "internal invariant failed: window distance outside [0, T N^2]");
-    if (h) return fail(ctx, BN_ESTATE, "internal invariant failed: dE term outside +-2^55");
-    return BN_OK;
+    if (h & 2) return fail(ctx, BN_ESTATE, "internal invariant failed: dE term outside +-2^55");
+    return fail(ctx, BN_ESTATE, "internal invariant failed: E recomputed at a pass start != E + sum dE");
 }
 
 template <int R, int NV>
@@ -831,7 +840,6 @@ int optimize_best_of_k(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* sta
     CUDA_TRY(cudaMemsetAsync(ctx->kticket.p, 0, (size_t)M * sizeof(unsigned int), ctx->stream));
     CUDA_TRY(ctx->pstats.ensure(prm->passes + 1));
     if (accept_log) CUDA_TRY(ctx->log.ensure((size_t)prm->passes * 64 * M));
-    CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
     ctx->ls = ctx->stream;
     // exact energy of the starting tile (slot `passes`), then E_after = E_before + sum dE per pass
     if ((rc = gram_lut(ctx, ctx->c.p, ctx->nc.p, 0))) return rc;
@@ -1157,7 +1165,6 @@ int bn_energy(bn_ctx* ctx, double* E, uint64_t E_fixed[2]) {
     int rc = ensure_work(ctx);
     if (rc) return rc;
     CUDA_TRY(ctx->pstats.ensure(1));
-    CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
     if ((rc = gram_lut(ctx, ctx->c.p, ctx->nc.p, 0))) return rc;
     const uint32_t nE = (uint32_t)(((size_t)ctx->P * half_count_padded(ctx->R) + 255) / 256);
     k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, nullptr, nullptr, ctx->P, 0, ctx->pstats.p);
@@ -1208,7 +1215,6 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     }
     CUDA_TRY(ctx->fparts.ensure(nfin > nfin_g ? nfin : nfin_g));
     if (accept_log) CUDA_TRY(ctx->log.ensure((size_t)prm->passes * 64 * M));
-    CUDA_TRY(cudaMemsetAsync(ctx->derr.p, 0, sizeof(int), ctx->stream));
     // accept flags start at zero; k_finish clears them again after every pass
     CUDA_TRY(cudaMemsetAsync(ctx->acc.p, 0, P, ctx->stream));
     const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
@@ -1353,7 +1359,8 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
                               ctx->ticket.p, ctx->pstats.p + pi, (const uint32_t*)nullptr, buf_U(pi + 1),
                               buf_c(pi + 1), buf_n(pi + 1), ctx->L, prm->seed, t + 1,
                               paper ? (const uint32_t*)ctx->perm.p : (const uint32_t*)nullptr,
-                              paper ? (const uint32_t*)ctx->invperm.p : (const uint32_t*)nullptr, budget));
+                              paper ? (const uint32_t*)ctx->invperm.p : (const uint32_t*)nullptr, budget,
+                              (int)(!paper && pi > 0), ctx->derr.p));
             LAUNCHED_K();
             continue;
         }
@@ -1361,7 +1368,8 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         CUDA_TRY(launch_k(ctx, k_finish, dim3(nfin), dim3(256), 0, cs, (const uint8_t*)ctx->acc.p, P, ctx->rowB, nl,
                           (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
                           ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, (int)(prm->mode != BN_REDRAW),
-                          ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi, (int)paper));
+                          ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi, (int)paper, (int)(!paper && pi > 0),
+                          ctx->derr.p));
         LAUNCHED_K();
     }
     if (overlap) {
@@ -1408,6 +1416,12 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         }
     }
     return BN_OK;
+}
+
+int bn_check(bn_ctx* ctx) {
+    if (!ctx) return BN_EINVAL;
+    DeviceGuard g(ctx->dev);
+    return read_err_flag(ctx);
 }
 
 int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t ns, double* rmse, double* spectrum,

@@ -2875,7 +2875,8 @@ __global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc,
                                                 const u128* __restrict__ Epart, uint32_t nEpart,
                                                 const i128* __restrict__ dEp, int swap_mode,
                                                 FinishPart* __restrict__ parts, unsigned int* __restrict__ ticket,
-                                                PassStatsDev* __restrict__ out, int clear_dEp) {
+                                                PassStatsDev* __restrict__ out, int clear_dEp,
+                                                int check_prev, int* __restrict__ err) {
     const uint32_t nblk = gridDim.x, b = blockIdx.x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const uint32_t p0 = (uint32_t)((uint64_t)P * b / nblk), p1 = (uint32_t)((uint64_t)P * (b + 1) / nblk);
@@ -2935,6 +2936,10 @@ __global__ void __launch_bounds__(256) k_finish(const uint8_t* __restrict__ acc,
         out->dE_sum[0] = tot.d[0];
         out->dE_sum[1] = tot.d[1];
         out->accepted = swap_mode ? tot.a / 2 : tot.a;
+        // exact energy chain: this pass's recomputed start energy equals the previous pass's
+        // E_before + sum dE (greedy modes; the paper mode's snapshot swaps do not add up)
+        if (check_prev && (__ldcg(&out[-1].E_after[0]) != tot.e[0] || __ldcg(&out[-1].E_after[1]) != tot.e[1]))
+            atomicOr(err, 4);
         *ticket = 0;
     }
 }
@@ -3183,7 +3188,8 @@ __global__ void __launch_bounds__(BN_FG_THREADS, BN_FG_MINB) k_finish_gather(uin
                                                        uint8_t* __restrict__ cn2, int* __restrict__ nn2, uint32_t L,
                                                        uint64_t seed, uint32_t pass_next,
                                                        const uint32_t* __restrict__ perm,
-                                                       const uint32_t* __restrict__ invperm, uint32_t budget) {
+                                                       const uint32_t* __restrict__ invperm, uint32_t budget,
+                                                       int check_prev, int* __restrict__ err) {
     const uint32_t nblk = gridDim.x, b = blockIdx.x;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const uint32_t n16 = rowB / 16;
@@ -3254,6 +3260,8 @@ __global__ void __launch_bounds__(BN_FG_THREADS, BN_FG_MINB) k_finish_gather(uin
         out->dE_sum[0] = tot.d[0];
         out->dE_sum[1] = tot.d[1];
         out->accepted = tot.a / 2;
+        if (check_prev && (__ldcg(&out[-1].E_after[0]) != tot.e[0] || __ldcg(&out[-1].E_after[1]) != tot.e[1]))
+            atomicOr(err, 4);
         *ticket = 0;
     }
 }

@@ -165,24 +165,7 @@ def test_errors(bn, oracle_mod):
 
 
 # ------------------------------------------------------------------ full BASELINE sizes
-@pytest.mark.slow
-@pytest.mark.parametrize("mode", [1, 0])
-def test_c3_full_size_sampled(bn, oracle_mod, mode):
-    """C3 at full size (128x128, T=1024, 1/4/16/64 spp) in the bench's launch configuration (SWAP,
-    and REDRAW): all counts bit-exact, the first colour classes' accept decisions identical to the
-    oracle, and the exact-additivity / monotonicity invariants of the whole pass."""
-    cfg = synth.CONFIGS["C3"]
-    U, bank = synth.problem_inputs(cfg)
-    s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
-    co = o.counts(U)
-    assert np.array_equal(s.eval_counts(), co)          # all 64 M counts, bit-exact
-    E0, _ = s.energy()
-    st, lg = s.optimize(1, synth.opt_seed(cfg), mode=mode, log=True)
-    _, _, sto, lgo = o.optimize(U, co, mode=mode, passes=1, seed=synth.opt_seed(cfg), max_steps=2,
-                                energy_each_pass=False, log=True)
-    assert np.array_equal(lg[0, :2], lgo[0, :2])
-    assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"] and st[0]["dE_sum"] < 0
-    assert s.energy()[0] == st[0]["E_fixed"]
+# complete passes at every BASELINE size: tests/test_gpu_fullsize.py (oracle goldens)
 
 
 # ------------------------------------------------------------- bank-shard decomposition (C5)
@@ -214,38 +197,6 @@ def test_window_distances_and_shard_decomposition(bn, oracle_mod):
     assert np.array_equal(acc, Df)
 
 
-@pytest.mark.slow
-def test_c2_full_size_swap(bn, oracle_mod):
-    """C2 exactly (64x64, 4 spp, T=256, SWAP, seeds 1/2/3): 3 passes compared pass by pass."""
-    cfg = synth.CONFIGS["C2"]
-    U, bank = synth.problem_inputs(cfg)
-    s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
-    _check_run(s, o, U, 3, cfg.mode, seed=synth.opt_seed(cfg))
-
-
-@pytest.mark.slow
-@pytest.mark.parametrize("pair", [0, 5])
-def test_c4_pair_full_size(bn, oracle_mod, pair):
-    """C4 pair j (128x128, 16 spp, T=1024, seeds xor j): all counts bit-exact; for the bench's mode
-    (SWAP) and REDRAW, the first colour class's decisions equal to the oracle and the device
-    invariants over a full pass."""
-    cfg = synth.CONFIGS["C4"]
-    U, bank = synth.problem_inputs(cfg, pair)
-    co = None
-    for mode in (cfg.mode, 1 - cfg.mode):
-        s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
-        if co is None:
-            co = o.counts(U)
-            assert np.array_equal(s.eval_counts(), co)
-        E0, _ = s.energy()
-        st, lg = s.optimize(1, synth.opt_seed(cfg, pair), mode=mode, log=True)
-        _, _, _, lgo = o.optimize(U, co, mode=mode, passes=1, seed=synth.opt_seed(cfg, pair), max_steps=1,
-                                  energy_each_pass=False, log=True)
-        assert np.array_equal(lg[0, :1], lgo[0, :1])
-        assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"] and st[0]["dE_sum"] < 0
-        s.close()
-
-
 def test_concurrent_contexts_match_sequential(bn, oracle_mod):
     """Independent pair tiles on their own streams, enqueued concurrently (the C4 bench layout),
     give bit-identical tiles to running each context alone."""
@@ -272,28 +223,6 @@ def test_concurrent_contexts_match_sequential(bn, oracle_mod):
         runs.append([s.get_tile() for s in ctxs])
     for a_, b_ in zip(*runs):
         assert np.array_equal(a_, b_)
-
-
-@pytest.mark.slow
-def test_c5_full_size_sampled(bn, oracle_mod):
-    """C5 (256x256, 16 spp, T=8192): all 512 M counts bit-exact and, for SWAP (the bench's mode) and
-    REDRAW, the first colour class's 1024 decisions equal to the oracle's (the L = 256 cluster
-    kernel with bit flags)."""
-    cfg = synth.CONFIGS["C5"]
-    U, bank = synth.problem_inputs(cfg)
-    co = None
-    for mode in (cfg.mode, 1 - cfg.mode):
-        s, o, _ = make(bn, oracle_mod, cfg.L, cfg.T, cfg.levels, bank=bank, U=U)
-        if co is None:
-            co = o.counts(U)
-            assert np.array_equal(s.eval_counts(), co)
-        E0, _ = s.energy()
-        st, lg = s.optimize(1, synth.opt_seed(cfg), mode=mode, log=True)
-        _, _, _, lgo = o.optimize(U, co, mode=mode, passes=1, seed=synth.opt_seed(cfg), max_steps=1,
-                                  energy_each_pass=False, log=True)
-        assert np.array_equal(lg[0, :1], lgo[0, :1])
-        assert st[0]["E_fixed"] == E0 + st[0]["dE_sum"]
-        s.close()
 
 
 # ------------------------------------------------------------------ window-Gram variants
