@@ -384,6 +384,8 @@ def run_ours(args, cfg):
         barrier()
     ms = e0.elapsed_time(e1)
     launches = sum(x.launch_count() for x in samplers) - l0
+    for x in samplers:  # every device invariant of the timed passes held (exact E chain, ranges)
+        x.check()
     ms_max = max_over_ranks(ms)
     EP = evals_per_pass(cfg)
     units_per_step = EP * (1 if banksharded else len(pairs) * world) if cfg.pairs == 1 else EP * cfg.pairs
