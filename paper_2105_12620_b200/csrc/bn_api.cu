@@ -72,34 +72,29 @@ encode_tiled_t get_encode_tiled() {
     }
     return fn;
 }
-// 2D map over a [P][rowB] uint8 count tensor: boxes of 8 pixel rows x 128 bytes, 128-B swizzle.
-bool make_count_map(CUtensorMap* m, const void* base, uint64_t rowB, uint64_t P) {
+// 3D map over the [y][x][row] count tensor restricted to one level: the level's elements start at
+// byte `lb` of each row (`rowB` bytes), `elems` of them in format `fmt` (u8, or the TMA-unpacked
+// 16U4 / 16U6 narrow types); box {128 elements, bx, by}, 128-B swizzle.
+bool make_level_map(CUtensorMap* m, const void* base, uint64_t rowB, uint64_t lb, uint64_t elems, uint32_t fmt,
+                    uint64_t L, uint32_t bx, uint32_t by) {
     encode_tiled_t enc = get_encode_tiled();
     if (!enc) return false;
-    cuuint64_t dims[2] = {rowB, P};
-    cuuint64_t strides[1] = {rowB};
-    cuuint32_t box[2] = {128, 8};
-    cuuint32_t es[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// 3D map over the [y][x][levels*Tp] count tensor with a {128, bx, by} box, 128-B swizzle.
-bool make_count_map3(CUtensorMap* m, const void* base, uint64_t rowB, uint64_t L, uint32_t bx, uint32_t by) {
-    encode_tiled_t enc = get_encode_tiled();
-    if (!enc) return false;
-    cuuint64_t dims[3] = {rowB, L, L};
+    const CUtensorMapDataType dt = fmt == BN_FMT_U8     ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                   : fmt == BN_FMT_E2M1 ? CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B
+                                                        : CU_TENSOR_MAP_DATA_TYPE_16U6_ALIGN16B;
+    cuuint64_t dims[3] = {elems, L, L};
     cuuint64_t strides[2] = {rowB, L * rowB};
     cuuint32_t box[3] = {128, bx, by};
     cuuint32_t es[3] = {1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+    return enc(m, dt, 3, const_cast<uint8_t*>(static_cast<const uint8_t*>(base) + lb), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-bool make_count_maps(CountMaps* m, const void* base, uint64_t rowB, uint64_t L) {
-    return make_count_map3(&m->a, base, rowB, L, 8, 8) && make_count_map3(&m->b, base, rowB, L, 24, 5) &&
-           make_count_map3(&m->s, base, rowB, L, 8, 1);
+bool make_level_maps(CountMaps* m, const void* base, uint64_t rowB, uint64_t lb, uint64_t elems, uint32_t fmt,
+                     uint64_t L) {
+    return make_level_map(&m->a, base, rowB, lb, elems, fmt, L, 8, 8) &&
+           make_level_map(&m->b, base, rowB, lb, elems, fmt, L, 24, 5) &&
+           make_level_map(&m->s, base, rowB, lb, elems, fmt, L, 8, 1);
 }
 
 template <class T>
@@ -186,29 +181,26 @@ struct bn_ctx {
     bool no_rowflags = true;  // BN_ROWFLAGS=1: the Gram follows the counts row by row (measured slower on C3)
     int prefetch_at = 1;  // BN_PREFETCH=start|gram|lut: launch the next pass's counts before the Gram / after it / after the energy terms
     bool per_class_decide = false;  // BN_DECIDE=per_class: 64 launches instead of one persistent
-    bool simt_gram = false;         // BN_GRAM=simt: dp4a window distances instead of IMMA
-    bool gram_attr_set[8] = {false};
-    bool gram2_attr_set[8] = {false};
-    bool imma_v1 = false;  // BN_GRAM=imma1: the one-strip-per-warp IMMA kernel (BN_GRAM=imma2: v2)
-    bool tc_gram = false;  // BN_GRAM=tc: tcgen05/TMEM window Gram (R = 7)
-    bool tc_attr_set = false;
-    bool tc2_gram = false;  // BN_GRAM=tc2: warp-specialised tcgen05 window Gram (R = 7)
-    bool tc2_attr_set = false;
-    bool tc3_gram = false;  // BN_GRAM=tc3: TMA-fed warp-specialised tcgen05 window Gram (R = 7)
-    bool tc4_gram = false;  // BN_GRAM=tc4 (default): persistent version of tc3
-    bool use_tc5 = false;   // BN_GRAM=tc5: the A-resident variant k_gram_tc5 (Tp <= 1024)
-    bool tc5_attr_set = false;
-    bool tc3_attr_set = false;
+    bool gram_attr_set[8] = {false};  // k_gram_tc4<R> shared-memory attribute
     bool decide_attr_set[8] = {false};
     bool cluster_attr_set[8] = {false};
     bool big_attr_set[8] = {false};
     bool no_big = false;  // BN_DECIDE=nobig: L > 128 tiles use the cooperative flag kernel
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
-    bool cluster_v1 = false;  // BN_DECIDE=cluster1: barrier-per-class cluster kernel (v1)
-    bool cluster_v2 = false;  // BN_DECIDE=cluster2: shared-memory-staged rows (v2)
     bool no_fuse = false;          // BN_FUSE=0: separate SWAP commit (k_finish) and gather kernels
-    bool old_swap_gather = false;  // BN_GATHER=old: k_swap_gather (one Philox per copying thread)
     bool swap_v3 = false;     // BN_DECIDE=swap3: SWAP on k_decide_cl3 (one warp per couple) instead of k_decide_swap
+    // narrow count rows: in the SWAP / paper modes, where a pass only
+    // permutes rows, the rows are stored as packed deltas c - round(N I_ref) (e2m1 / e3m2 per level,
+    // chosen from the tile's measured range); every other consumer unpacks them first (ensure_u8)
+    int narrow_mode = -1;  // BN_NARROW: -1 auto (default), 0 off, 1 force e2m1, 2 force e3m2, 3 force u8 layout
+    bool packed = false;   // c holds narrow rows (layout fmt / lb / rowBn)
+    uint32_t fmt[8] = {0}, lb[8] = {0}, rowBn = 0;
+    DevBuf<uint8_t> noff;  // offsets [l][Tp]
+    bool noff_dirty = true;
+    DevBuf<int> nrng;      // per-level max |delta|
+    uint32_t layout_epoch = 0;  // bumped whenever the row layout changes (tensor-map cache)
+    struct MapEntry { const void* base; uint32_t epoch; CountMaps m[8]; };
+    std::vector<MapEntry> map_cache;
     // per-kernel event timing (bn_profile_*)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -388,6 +380,8 @@ int ensure_counts(bn_ctx* ctx) {
         ctx->nc.p, nullptr, ctx->L);
     LAUNCHED_K();
     ctx->counts_dirty = false;
+    ctx->packed = false;
+    ++ctx->layout_epoch;
     return BN_OK;
 }
 
@@ -423,97 +417,131 @@ int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_del
     return launch_lut_only<R>(ctx, write_deltas);
 }
 
-// Window Gram: TMA-fed tcgen05 k_gram_tc3 (default for R = 7, BN_GRAM=tc3), tcgen05 variants tc/tc2,
-// IMMA v2 (BN_GRAM=imma2, and every R != 7), IMMA v1 (BN_GRAM=imma1), dp4a (BN_GRAM=simt).
+uint32_t row_bytes(const bn_ctx* ctx) { return ctx->packed ? ctx->rowBn : ctx->rowB; }
+
+// Tensor maps of the rows at `base` in the current layout, cached per (buffer, layout epoch): the
+// candidate buffers alternate between a few pointers, and encoding 3 maps per level per launch
+// would cost tens of microseconds of host time per pass.
+bool level_maps(bn_ctx* ctx, const void* base, CountMaps* out) {
+    for (const auto& e : ctx->map_cache)
+        if (e.base == base && e.epoch == ctx->layout_epoch) {
+            for (uint32_t l = 0; l < ctx->nl; ++l) out[l] = e.m[l];
+            return true;
+        }
+    bn_ctx::MapEntry ent;
+    ent.base = base;
+    ent.epoch = ctx->layout_epoch;
+    for (uint32_t l = 0; l < ctx->nl; ++l) {
+        const uint32_t f = ctx->packed ? ctx->fmt[l] : BN_FMT_U8;
+        const uint64_t lb = ctx->packed ? ctx->lb[l] : (uint64_t)l * ctx->Tp;
+        if (!make_level_maps(&ent.m[l], base, row_bytes(ctx), lb, ctx->Tp, f, ctx->L)) return false;
+        out[l] = ent.m[l];
+    }
+    if (ctx->map_cache.size() >= 8) ctx->map_cache.erase(ctx->map_cache.begin());
+    ctx->map_cache.push_back(ent);
+    return true;
+}
+
+// Window Gram: the TMA-fed persistent tcgen05 kernel k_gram_tc4<R> (one CTA per SM), every R <= 7
+// (the R = 7 neighbourhood tiles are a superset), u8 or narrow rows.
 template <int R>
 int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
-    const uint32_t SW = ctx->L < 32 ? ctx->L : 32;
-    dim3 grid(ctx->L / SW, ctx->L);
-    if (R == 7 && ctx->tc3_gram) {
-        CountMaps mc, mn;
-        if (!make_count_maps(&mc, ctx->c.p, ctx->rowB, ctx->L) || !make_count_maps(&mn, cn, ctx->rowB, ctx->L))
-            return fail(ctx, BN_ECUDA, "cuTensorMapEncodeTiled failed");
-        const int smem = tc3::SMEM;
-        if (!ctx->tc3_attr_set) {
-            CUDA_TRY(cudaFuncSetAttribute(k_gram_tc4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            CUDA_TRY(cudaFuncSetAttribute(k_gram_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            ctx->tc3_attr_set = true;
-        }
-        KSTART(BN_K_GRAM);
-        if (ctx->tc4_gram && !ctx->gram_rows && ctx->Tp <= 128u * tc5::NKMAX && ctx->use_tc5) {
-            // persistent with the A operand resident (Tp <= 1024; BN_GRAM=tc5: measured slower on C3,
-            // its 2-stage B ring keeps too few bytes in flight to hide the TMA latency)
-            if (!ctx->tc5_attr_set) {
-                CUDA_TRY(cudaFuncSetAttribute(k_gram_tc5, cudaFuncAttributeMaxDynamicSharedMemorySize, tc5::SMEM));
-                ctx->tc5_attr_set = true;
-            }
-            int nsm = 148;
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
-            const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
-            const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
-            k_gram_tc5<<<grid, tc3::THREADS, tc5::SMEM, ctx->ls>>>(mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
-        } else if (ctx->tc4_gram) {  // persistent: one CTA per SM walks the (block, level) items
-            int nsm = 148;
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
-            const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
-            const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
-            CUDA_TRY(launch_k(ctx, k_gram_tc4, dim3(grid), dim3(tc3::THREADS), smem, ctx->ls, mc, mn, ctx->nc.p, nn, ctx->L,
-                              ctx->Tp, ctx->nl, ctx->Dt.p, ctx->gram_rows, ctx->gram_rows_target));
-        } else {
-            k_gram_tc3<<<dim3(ctx->L / 8, ctx->L / 8, ctx->nl), tc3::THREADS, smem, ctx->ls>>>(
-                mc, mn, ctx->nc.p, nn, ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
-        }
-        LAUNCHED_K();
-    } else if (R == 7 && ctx->tc2_gram) {
-        const int smem = tc2::SMEM;
-        if (!ctx->tc2_attr_set) {
-            CUDA_TRY(cudaFuncSetAttribute(k_gram_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            ctx->tc2_attr_set = true;
-        }
-        KSTART(BN_K_GRAM);
-        k_gram_tc2<<<dim3(ctx->L / 8, ctx->L / 8), tc2::THREADS, smem, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn,
-                                                                                  ctx->L, ctx->Tp, ctx->nl, ctx->Dt.p);
-        LAUNCHED_K();
-    } else if (R == 7 && ctx->tc_gram) {
-        const int smem = tc::SMEM + 1024;
-        if (!ctx->tc_attr_set) {
-            CUDA_TRY(cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            ctx->tc_attr_set = true;
-        }
-        KSTART(BN_K_GRAM);
-        k_gram_tc<<<dim3(ctx->L / 8, ctx->L / 8), tc::THREADS, smem, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L,
-                                                                                ctx->Tp, ctx->nl, ctx->Dt.p);
-        LAUNCHED_K();
-    } else if (ctx->simt_gram) {
-        KSTART(BN_K_GRAM);
-        k_gram<R><<<grid, 32 * (R + 1), 0, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, SW, ctx->Tp,
-                                                          ctx->nl, ctx->Dt.p);
-        LAUNCHED_K();
-    } else if (ctx->imma_v1) {
-        using S = mma_gram::Shape<R>;
-        const int smem = 2 * S::STAGE;
-        if (!ctx->gram_attr_set[R]) {
-            CUDA_TRY(cudaFuncSetAttribute(k_gram_mma<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            ctx->gram_attr_set[R] = true;
-        }
-        dim3 g2(ctx->L / mma_gram::BX, ctx->L / mma_gram::BY);
-        KSTART(BN_K_GRAM);
-        k_gram_mma<R><<<g2, 32 * mma_gram::WARPS, smem, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, ctx->Tp,
-                                                                       ctx->nl, ctx->Dt.p);
-        LAUNCHED_K();
-    } else {
-        using S = Shape2<R>;
-        const int smem = 2 * S::STAGE;
-        if (!ctx->gram2_attr_set[R]) {
-            CUDA_TRY(cudaFuncSetAttribute(k_gram_mma2<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            ctx->gram2_attr_set[R] = true;
-        }
-        dim3 g2(ctx->L / mma_gram::BX, ctx->L / mma_gram::BY);
-        KSTART(BN_K_GRAM);
-        k_gram_mma2<R><<<g2, 32 * mma_gram::WARPS, smem, ctx->ls>>>(ctx->c.p, cn, ctx->nc.p, nn, ctx->L, ctx->Tp,
-                                                                        ctx->nl, ctx->Dt.p);
-        LAUNCHED_K();
+    GramMaps gm;
+    memset(&gm, 0, sizeof gm);
+    if (!level_maps(ctx, ctx->c.p, gm.c) || !level_maps(ctx, cn, gm.n))
+        return fail(ctx, BN_ECUDA, "cuTensorMapEncodeTiled failed");
+    for (uint32_t l = 0; l < 8; ++l) gm.fmt[l] = ctx->packed && l < ctx->nl ? ctx->fmt[l] : BN_FMT_U8;
+    const int smem = tc3::SMEM;
+    if (!ctx->gram_attr_set[R]) {
+        CUDA_TRY(cudaFuncSetAttribute(k_gram_tc4<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        ctx->gram_attr_set[R] = true;
     }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
+    const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
+    const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
+    KSTART(BN_K_GRAM);
+    CUDA_TRY(launch_k(ctx, k_gram_tc4<R>, dim3(grid), dim3(tc3::THREADS), smem, ctx->ls, gm, ctx->nc.p, nn, ctx->L,
+                      ctx->Tp, ctx->nl, ctx->Dt.p, ctx->gram_rows, ctx->gram_rows_target));
+    LAUNCHED_K();
+    return BN_OK;
+}
+
+// ---------------------------------------------------------------- narrow rows
+// The current rows as u8 counts without changing the stored layout: c itself, or (narrow rows) c
+// unpacked into the candidate buffer cn (free between bn_optimize calls).
+const uint8_t* u8_rows(bn_ctx* ctx) {
+    if (!ctx->packed) return ctx->c.p;
+    const uint32_t P = ctx->P;
+    NarrowLayout lay;
+    for (uint32_t l = 0; l < 8; ++l) lay.fmt[l] = ctx->fmt[l], lay.lb[l] = ctx->lb[l];
+    k_narrow_unpack<<<(P + 7) / 8, 256, 0, ctx->stream>>>(ctx->c.p, P, ctx->Tp, ctx->nl, ctx->noff.p, lay, ctx->rowBn,
+                                                         ctx->cn.p, ctx->nn.p);
+    ++ctx->launches;
+    return ctx->cn.p;
+}
+// u8 rows: unpack the narrow rows of c (norms |c|^2) if they are packed.
+int ensure_u8(bn_ctx* ctx) {
+    if (!ctx->packed) return BN_OK;
+    const uint32_t P = ctx->P;
+    NarrowLayout lay;
+    for (uint32_t l = 0; l < 8; ++l) lay.fmt[l] = ctx->fmt[l], lay.lb[l] = ctx->lb[l];
+    k_narrow_unpack<<<(P + 7) / 8, 256, 0, ctx->stream>>>(ctx->c.p, P, ctx->Tp, ctx->nl, ctx->noff.p, lay, ctx->rowBn,
+                                                         ctx->cn.p, ctx->nn.p);
+    LAUNCHED();
+    std::swap(ctx->c, ctx->cn);
+    std::swap(ctx->nc, ctx->nn);
+    ctx->packed = false;
+    ++ctx->layout_epoch;
+    return BN_OK;
+}
+
+// Narrow rows for the permuting modes: per level, the tile's max |c - round(N I_ref)| selects e2m1
+// (<= 4), e3m2 (<= 8) or u8; the rows are packed into that layout (norms |delta|^2).  One host
+// synchronisation (the range) per new tile.
+int ensure_narrow(bn_ctx* ctx) {
+    if (ctx->packed || ctx->narrow_mode == 0) return BN_OK;
+    const uint32_t P = ctx->P, nl = ctx->nl, Tp = ctx->Tp;
+    const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
+    const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
+    if (ctx->noff_dirty) {
+        CUDA_TRY(ctx->iref.ensure(ctx->Ts));
+        k_iref<<<(ctx->Ts + 127) / 128, 128, 0, ctx->stream>>>(ctx->ab.p, ctx->pxy.p, ctx->Ts, ctx->iref.p);
+        LAUNCHED();
+        CUDA_TRY(ctx->noff.ensure((size_t)nl * Tp));
+        k_narrow_offsets<<<(Tp + 255) / 256, 256, 0, ctx->stream>>>(ctx->iref.p, ctx->Ts, Tp, lo, hi, nl, ctx->noff.p);
+        LAUNCHED();
+        ctx->noff_dirty = false;
+    }
+    CUDA_TRY(ctx->nrng.ensure(8));
+    CUDA_TRY(cudaMemsetAsync(ctx->nrng.p, 0, 8 * sizeof(int), ctx->stream));
+    k_narrow_range<<<(P + 7) / 8, 256, 0, ctx->stream>>>(ctx->c.p, P, Tp, nl, ctx->noff.p, ctx->nrng.p);
+    LAUNCHED();
+    int rng[8];
+    CUDA_TRY(cudaMemcpyAsync(rng, ctx->nrng.p, sizeof rng, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    NarrowLayout lay;
+    uint32_t off = 0;
+    for (uint32_t l = 0; l < 8; ++l) {
+        uint32_t f = BN_FMT_U8;
+        if (l < nl) {
+            const int m = rng[l];
+            f = ctx->narrow_mode == 3 ? BN_FMT_U8
+                : m <= 4 && ctx->narrow_mode != 2 ? BN_FMT_E2M1
+                : m <= 8 ? BN_FMT_E3M2 : BN_FMT_U8;
+        }
+        ctx->fmt[l] = lay.fmt[l] = f;
+        ctx->lb[l] = lay.lb[l] = off;
+        if (l < nl) off += Tp * fmt_bits(f) / 8;
+    }
+    ctx->rowBn = off;
+    k_narrow_pack<<<(P + 7) / 8, 256, 0, ctx->stream>>>(ctx->c.p, P, Tp, nl, ctx->noff.p, lay, ctx->rowBn, ctx->cn.p,
+                                                       ctx->nn.p);
+    LAUNCHED();
+    std::swap(ctx->c, ctx->cn);
+    std::swap(ctx->nc, ctx->nn);
+    ctx->packed = true;
+    ++ctx->layout_epoch;
     return BN_OK;
 }
 
@@ -579,9 +607,6 @@ int launch_decide(bn_ctx* ctx, uint32_t s, uint32_t t, uint64_t seed, int mode, 
     LAUNCHED_K();
     return BN_OK;
 }
-// One cooperative launch for all 64 classes (k_decide_pass); co-residency of its CTAs is
-// guaranteed by the cooperative launch, which the neighbour-progress waits require.
-// Cluster launch of k_decide_cluster when the tile's candidate CTAs fit one cluster (<= 16).
 // L = 256, 512: one 16-CTA cluster with `spw` slots per warp and bit flags (k_decide_big).
 template <int R>
 int launch_decide_big(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
@@ -630,32 +655,24 @@ int launch_decide_big(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t*
     return BN_OK;
 }
 
+// L <= 128: one cluster of <= 16 CTAs decides all 64 classes (k_decide_cl3; SWAP: k_decide_swap).
 template <int R>
 int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
-    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
     const uint32_t nb = ctx->L / 8, P = ctx->P;
-    const bool swap_v4 = mode && !ctx->cluster_v1 && !ctx->cluster_v2 && !ctx->swap_v3;
+    const bool swap_v4 = mode && !ctx->swap_v3;  // SWAP: one warp per couple member (k_decide_swap)
     uint32_t cpc = mode && !swap_v4 ? 8 : 16;
     while (cpc > nb * nb / (swap_v4 ? 1 : nb)) cpc /= 2;  // at most M slots (SWAP v4) / nb per CTA
     const uint32_t ncta = nb * nb / cpc;
     *done = false;
     if (ctx->no_cluster) return BN_OK;
     if (ncta > 16) return launch_decide_big<R>(ctx, t, seed, mode, log, done);
-    // v2 (default): u32 flags + slot table; v1 (BN_DECIDE=cluster1): byte flags, cluster barriers
-    // v3 (default): register-prefetched rows; v2 (BN_DECIDE=cluster2): rows staged in shared memory
-    // by bulk copies; v1 (BN_DECIDE=cluster1): byte flags + a cluster barrier per class
-    const int ver = ctx->cluster_v1 ? 1 : ctx->cluster_v2 ? 2 : 3;
-    const size_t rows = (size_t)2 * (mode ? 2 : 1) * cpc * 2 * WN * 8, slots = (size_t)64 * 4 * (mode ? 2 : 1) * cpc;
-    const size_t smem = swap_v4  ? 4 * (size_t)P + (size_t)64 * cpc * 6
-                        : ver == 3 ? 4 * (size_t)P + slots : ver == 2 ? rows + 4 * (size_t)P + slots : rows + P;
-    const void* fn = swap_v4    ? (const void*)k_decide_swap<R>
-                     : ver == 3 ? (mode ? (const void*)k_decide_cl3<R, 1> : (const void*)k_decide_cl3<R, 0>)
-                     : ver == 2 ? (mode ? (const void*)k_decide_cl2<R, 1> : (const void*)k_decide_cl2<R, 0>)
-                                : (mode ? (const void*)k_decide_cluster<R, 1> : (const void*)k_decide_cluster<R, 0>);
+    // u32 flags in every CTA's shared memory + the slot table of the 64 classes (+ member indices)
+    const size_t slots = (size_t)64 * 4 * (mode ? 2 : 1) * cpc;
+    const size_t smem = swap_v4 ? 4 * (size_t)P + (size_t)64 * cpc * 6 : 4 * (size_t)P + slots;
+    const void* fn = swap_v4 ? (const void*)k_decide_swap<R>
+                             : (mode ? (const void*)k_decide_cl3<R, 1> : (const void*)k_decide_cl3<R, 0>);
     if (!ctx->cluster_attr_set[R]) {
-        for (const void* f : {(const void*)k_decide_cluster<R, 0>, (const void*)k_decide_cluster<R, 1>,
-                              (const void*)k_decide_cl2<R, 0>, (const void*)k_decide_cl2<R, 1>,
-                              (const void*)k_decide_cl3<R, 0>, (const void*)k_decide_cl3<R, 1>,
+        for (const void* f : {(const void*)k_decide_cl3<R, 0>, (const void*)k_decide_cl3<R, 1>,
                               (const void*)k_decide_swap<R>}) {
             CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
             CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -692,6 +709,8 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     return BN_OK;
 }
 
+// Larger tiles (REDRAW): one cooperative launch for all 64 classes (k_decide_pass); co-residency of
+// its CTAs is guaranteed by the cooperative launch, which the neighbour-progress waits require.
 template <int R>
 int launch_decide_pass(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint8_t* log, bool* done) {
     constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
@@ -928,14 +947,13 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     const char* dm = getenv("BN_DECIDE");
     ctx->per_class_decide = dm && !strcmp(dm, "per_class");
     ctx->no_cluster = dm && !strcmp(dm, "flags");
-    ctx->cluster_v1 = dm && !strcmp(dm, "cluster1");
-    ctx->cluster_v2 = dm && !strcmp(dm, "cluster2");
     ctx->swap_v3 = dm && !strcmp(dm, "swap3");
     ctx->no_big = dm && !strcmp(dm, "nobig");
     const char* fu = getenv("BN_FUSE");
     ctx->no_fuse = fu && !strcmp(fu, "0");
-    const char* gth = getenv("BN_GATHER");
-    ctx->old_swap_gather = gth && !strcmp(gth, "old");
+    const char* nw = getenv("BN_NARROW");
+    ctx->narrow_mode = !nw || !*nw || !strcmp(nw, "auto") ? -1 : !strcmp(nw, "0") ? 0 : !strcmp(nw, "e2m1") ? 1
+                     : !strcmp(nw, "e3m2") ? 2 : !strcmp(nw, "u8") ? 3 : -1;
     const char* ov = getenv("BN_OVERLAP");
     ctx->no_overlap = ov && !strcmp(ov, "0");
     const char* rf = getenv("BN_ROWFLAGS");
@@ -960,14 +978,6 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
             return BN_ECUDA;
         }
     }
-    const char* gm = getenv("BN_GRAM");
-    ctx->simt_gram = gm && !strcmp(gm, "simt");
-    ctx->imma_v1 = gm && !strcmp(gm, "imma1");
-    ctx->tc_gram = gm && !strcmp(gm, "tc");
-    ctx->tc2_gram = gm && !strcmp(gm, "tc2");
-    ctx->tc4_gram = !gm || !*gm || !strcmp(gm, "tc4") || !strcmp(gm, "tc5");  // default (R = 7): persistent
-    ctx->use_tc5 = gm && !strcmp(gm, "tc5");
-    ctx->tc3_gram = ctx->tc4_gram || !strcmp(gm, "tc3");
     *out = ctx;
     return BN_OK;
 }
@@ -987,6 +997,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->ev_out.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release(); ctx->rows_done.release();
+        ctx->noff.release(); ctx->nrng.release();
         if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
         if (ctx->hp) cudaStreamSynchronize(ctx->hp), cudaStreamDestroy(ctx->hp);
         for (cudaEvent_t e : {ctx->evA, ctx->evB, ctx->evC})
@@ -1025,6 +1036,7 @@ int bn_set_lattice(bn_ctx* ctx, uint32_t d1, uint32_t d2, const uint32_t* spp_le
     for (uint32_t l = 0; l < 8; ++l) ctx->levels[l] = l < n_levels ? spp_levels[l] : 0;
     ctx->have_lattice = true;
     ctx->counts_dirty = true;
+    ctx->noff_dirty = true;
     ctx->lut_dirty = true;
     return BN_OK;
 }
@@ -1070,6 +1082,7 @@ int bn_set_bank(bn_ctx* ctx, uint32_t T, const int32_t* a, const int32_t* b, con
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     ctx->have_bank = true;
     ctx->counts_dirty = true;
+    ctx->noff_dirty = true;
     ctx->lut_dirty = true;
     return BN_OK;
 }
@@ -1150,7 +1163,8 @@ int bn_eval_counts(bn_ctx* ctx, uint8_t* out, int is_device) {
         CUDA_TRY(ctx->cexp.ensure(n));
         dst = ctx->cexp.p;
     }
-    k_counts_export<<<ctx->nl * ctx->P, 128, 0, ctx->stream>>>(ctx->c.p, ctx->P, ctx->nl, ctx->Tp, ctx->Ts, dst);
+    const uint8_t* rows = u8_rows(ctx);
+    k_counts_export<<<ctx->nl * ctx->P, 128, 0, ctx->stream>>>(rows, ctx->P, ctx->nl, ctx->Tp, ctx->Ts, dst);
     LAUNCHED();
     if (!is_device) {
         CUDA_TRY(cudaMemcpyAsync(out, dst, n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1191,7 +1205,10 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     int rc = ensure_work(ctx);
     if (rc) return rc;
     if (prm->passes == 0) return BN_OK;
+    // rows: narrow packed deltas for the permuting modes, u8 counts where new counts are drawn
+    if ((rc = prm->mode == BN_REDRAW ? ensure_u8(ctx) : ensure_narrow(ctx))) return rc;
     if (prm->K > 1) return optimize_best_of_k(ctx, prm, stats, accept_log);
+    const uint32_t rb = row_bytes(ctx);
     const uint32_t P = ctx->P, M = (ctx->L / 8) * (ctx->L / 8), nl = ctx->nl;
     const int R = ctx->R;
     const uint32_t nE = (uint32_t)(((size_t)P * half_count_padded(R) + 255) / 256);
@@ -1230,7 +1247,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     }
     // SWAP: the commit of pass t and the gather of pass t+1 run as one kernel (k_finish_gather), which
     // writes the next candidates into the other buffer of the pair
-    const bool fuse = (prm->mode == BN_SWAP || paper) && !ctx->no_fuse && !ctx->old_swap_gather && prm->passes > 1;
+    const bool fuse = (prm->mode == BN_SWAP || paper) && !ctx->no_fuse && prm->passes > 1;
     if (fuse) {
         CUDA_TRY(ctx->Un2.ensure(P));
         CUDA_TRY(ctx->cn2.ensure((size_t)P * ctx->rowB));
@@ -1243,7 +1260,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     // Row flags: with the persistent tcgen05 Gram, pass t's Gram follows its candidate counts row by
     // row (k_counts publishes each finished tile-row segment, k_gram_tc4 waits per item), so the
     // counts of pass t+1 may still be finishing when the Gram of pass t+1 starts.
-    const bool rowflags = overlap && ctx->tc4_gram && ctx->R == 7 && !ctx->no_rowflags;
+    const bool rowflags = overlap && !ctx->no_rowflags;
     uint32_t rows_target[2] = {0, 0};
     if (rowflags) {
         CUDA_TRY(ctx->rows_done.ensure(ctx->L));
@@ -1285,7 +1302,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             KSTART(BN_K_GATHER);
             CUDA_TRY(launch_k(ctx, k_paper_gather, dim3((P + 7) / 8), dim3(256), 0, cs, (const uint32_t*)nullptr,
                               (const uint2*)ctx->U.p, buf_U(pi), (const uint8_t*)ctx->c.p, buf_c(pi), (const int*)ctx->nc.p,
-                              buf_n(pi), P, ctx->rowB, nl, (const uint32_t*)ctx->perm.p, (const uint32_t*)ctx->invperm.p,
+                              buf_n(pi), P, rb, nl, (const uint32_t*)ctx->perm.p, (const uint32_t*)ctx->invperm.p,
                               prm->seed, t, budget));
             LAUNCHED_K();
         } else if (prm->mode == BN_REDRAW) {
@@ -1298,18 +1315,13 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             // candidates gathered by k_finish_gather of pass pi - 1
         } else {
             KSTART(BN_K_GATHER);
-            if (ctx->old_swap_gather) {
-                k_swap_gather<<<64 * M, 128, 0, cs>>>(ctx->U.p, ctx->Un.p, ctx->c.p, ctx->cn.p, ctx->nc.p, ctx->nn.p,
-                                                     ctx->L, prm->seed, t, ctx->rowB, nl);
-            } else {
-                CUDA_TRY(launch_k(ctx, k_swap_pairs, dim3((64 * M + 255) / 256), dim3(256), 0, cs, ctx->L, prm->seed, t,
-                                  ctx->part.p));
-                LAUNCHED();
-                CUDA_TRY(launch_k(ctx, k_paper_gather, dim3((P + 7) / 8), dim3(256), 0, cs, (const uint32_t*)ctx->part.p,
-                                  (const uint2*)ctx->U.p, buf_U(pi), (const uint8_t*)ctx->c.p, buf_c(pi),
-                                  (const int*)ctx->nc.p, buf_n(pi), P, ctx->rowB, nl, (const uint32_t*)nullptr,
-                                  (const uint32_t*)nullptr, (uint64_t)0, 0u, 0u));
-            }
+            CUDA_TRY(launch_k(ctx, k_swap_pairs, dim3((64 * M + 255) / 256), dim3(256), 0, cs, ctx->L, prm->seed, t,
+                              ctx->part.p));
+            LAUNCHED();
+            CUDA_TRY(launch_k(ctx, k_paper_gather, dim3((P + 7) / 8), dim3(256), 0, cs, (const uint32_t*)ctx->part.p,
+                              (const uint2*)ctx->U.p, buf_U(pi), (const uint8_t*)ctx->c.p, buf_c(pi),
+                              (const int*)ctx->nc.p, buf_n(pi), P, rb, nl, (const uint32_t*)nullptr,
+                              (const uint32_t*)nullptr, (uint64_t)0, 0u, 0u));
             LAUNCHED_K();
         }
         // next pass's candidates: their buffer was last read by finish(pi-1), already ordered on cs;
@@ -1353,7 +1365,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         if (fuse && pi + 1 < prm->passes) {
             // the next pass's partners are computed in k_finish_gather itself (swap_partner)
             KSTART(BN_K_COMMIT);
-            CUDA_TRY(launch_k(ctx, k_finish_gather, dim3(nfin_g), dim3(BN_FG_THREADS), 0, cs, ctx->acc.p, P, ctx->rowB, nl,
+            CUDA_TRY(launch_k(ctx, k_finish_gather, dim3(nfin_g), dim3(BN_FG_THREADS), 0, cs, ctx->acc.p, P, rb, nl,
                               (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
                               ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, ctx->fparts.p,
                               ctx->ticket.p, ctx->pstats.p + pi, (const uint32_t*)nullptr, buf_U(pi + 1),
@@ -1365,7 +1377,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             continue;
         }
         KSTART(BN_K_COMMIT);
-        CUDA_TRY(launch_k(ctx, k_finish, dim3(nfin), dim3(256), 0, cs, (const uint8_t*)ctx->acc.p, P, ctx->rowB, nl,
+        CUDA_TRY(launch_k(ctx, k_finish, dim3(nfin), dim3(256), 0, cs, (const uint8_t*)ctx->acc.p, P, rb, nl,
                           (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
                           ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, (int)(prm->mode != BN_REDRAW),
                           ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi, (int)paper, (int)(!paper && pi > 0),
@@ -1438,6 +1450,7 @@ int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t 
     if (L > 256) return fail(ctx, BN_EINVAL, "bn_eval_quality supports L <= 256 (L = %u)", L);
     DeviceGuard g(ctx->dev);
     if ((rc = ensure_counts(ctx))) return rc;
+    const uint8_t* rows = u8_rows(ctx);
     CUDA_TRY(ctx->iref.ensure(Ts));
     k_iref<<<(Ts + 127) / 128, 128, 0, ctx->stream>>>(ctx->ab.p, ctx->pxy.p, Ts, ctx->iref.p);
     LAUNCHED();
@@ -1476,7 +1489,7 @@ int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t 
     for (uint32_t i0 = 0; i0 < Ts; i0 += chunk) {
         const uint32_t ci = std::min(chunk, Ts - i0);
         const dim3 grid(L, (ci + EV_II - 1) / EV_II);
-        k_ev_dft_rows<<<grid, 256, sm1, ctx->stream>>>(ctx->c.p, L, ctx->rowB, level * ctx->Tp, invN, ctx->iref.p, i0,
+        k_ev_dft_rows<<<grid, 256, sm1, ctx->stream>>>(rows, L, ctx->rowB, level * ctx->Tp, invN, ctx->iref.p, i0,
                                                         ci, ctx->ev_tw.p, ctx->ev_X1.p);
         LAUNCHED();
         k_ev_dft_cols<<<grid, 256, sm2, ctx->stream>>>(ctx->ev_X1.p, L, i0, ci, ctx->ev_tw.p, ctx->ev_h.p, nsk,

@@ -388,22 +388,6 @@ __global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __re
 }
 // Tp / 8 integrand groups per pixel: callers guarantee Tp % 256 == 0 (whole warps per group).
 
-// SWAP candidates: cn_p = c_partner(p), Un_p = U_partner(p), for every (class s, index m).
-__global__ void k_swap_gather(const uint2* __restrict__ U, uint2* __restrict__ Un, const uint8_t* __restrict__ c,
-                              uint8_t* __restrict__ cn, const int* __restrict__ nc, int* __restrict__ nn,
-                              uint32_t L, uint64_t seed, uint32_t pass_t, uint32_t rowB, uint32_t nl) {
-    const uint32_t M = (L / 8) * (L / 8);
-    const uint32_t sm = blockIdx.x;  // s * M + m
-    const uint32_t s = sm / M, m = sm - s * M;
-    const uint32_t kappa = swap_kappa(seed, pass_t, s, M);
-    const uint32_t p = class_pixel(L, seed, pass_t, s, m), p2 = class_pixel(L, seed, pass_t, s, m ^ kappa);
-    const uint4* src = reinterpret_cast<const uint4*>(c + (size_t)p2 * rowB);
-    uint4* dst = reinterpret_cast<uint4*>(cn + (size_t)p * rowB);
-    for (uint32_t j = threadIdx.x; j < rowB / 16; j += blockDim.x) dst[j] = src[j];
-    if (threadIdx.x == 0) Un[p] = U[p2];
-    if (threadIdx.x < nl) nn[(size_t)p * nl + threadIdx.x] = nc[(size_t)p2 * nl + threadIdx.x];
-}
-
 // SWAP partner map of pass t: part[p] = p2 for every couple member (one thread per (class, index);
 // 3 Philox draws per thread instead of per copying thread).  The rows are then gathered by
 // k_paper_gather (one warp per pixel, 16-byte copies).
@@ -441,417 +425,25 @@ __device__ __forceinline__ int4 dt_get(const int4* Dt, size_t n, size_t idx) {
     return make_int4(a.x, a.y, b.x, b.y);
 }
 
-// --------------------------------------------------------------------------- window distances
-// One CTA = a strip of SW <= 32 pixels of one row y; warp w handles window row oy = w (0..R),
-// lane = pixel.  Per K-chunk the CTA stages, for every oy, the neighbour strip
-// (row y+oy, columns x0-R .. x0+SW+R-1) of both c and cn in shared memory (row stride KCW+1
-// words: conflict-free), and every thread accumulates 4 dp4a dot products per offset ox:
-//   <c_p,c_q>, <cn_p,c_q>, <c_p,cn_q>, <cn_p,cn_q>.
-// D = |x|^2 + |y|^2 - 2<x,y> from the per-row norms.  Output Dt[l][p][h] =
-// int4(D(c_p,c_q), D(c_p,cn_q), D(cn_p,c_q), D(cn_p,cn_q)), q = p + o_h, h in the half window.
-// Kept as the SIMT reference path (BN_GRAM=simt); the default is k_gram_mma below.
-constexpr int GRAM_KC = 32;               // bytes of K per stage
-constexpr int GRAM_KCW = GRAM_KC / 4;     // words
-constexpr int GRAM_STRIDE = GRAM_KCW + 1; // padded row stride (words)
-
-template <int R>
-__global__ void __launch_bounds__(32 * (R + 1)) k_gram(const uint8_t* __restrict__ c, const uint8_t* __restrict__ cn,
-                                                        const int* __restrict__ nc, const int* __restrict__ nn,
-                                                        uint32_t L, uint32_t SW, uint32_t Tp, uint32_t nl,
-                                                        int4* __restrict__ Dt) {
-    constexpr int NCOL_MAX = 32 + 2 * R;
-    constexpr int H = 2 * R * R + 2 * R;
-    __shared__ uint32_t sC[(R + 1) * NCOL_MAX * GRAM_STRIDE];
-    __shared__ uint32_t sN[(R + 1) * NCOL_MAX * GRAM_STRIDE];
-    const uint32_t ncol = SW + 2 * R;
-    const uint32_t x0 = blockIdx.x * SW, y = blockIdx.y;
-    const int oy = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rowB = nl * Tp;
-    const uint32_t nload = (R + 1) * ncol * GRAM_KCW;
-    for (uint32_t l = 0; l < nl; ++l) {
-        uint32_t acc[2 * R + 1][4];
-#pragma unroll
-        for (int i = 0; i < 2 * R + 1; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0;
-        for (uint32_t k0 = 0; k0 < Tp; k0 += GRAM_KC) {
-            for (uint32_t j = threadIdx.x; j < nload; j += blockDim.x) {
-                const uint32_t w = j % GRAM_KCW, rc = j / GRAM_KCW;  // rc = ry * ncol + col
-                const uint32_t ry = rc / ncol, col = rc - ry * ncol;
-                const uint32_t qy = (y + ry) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
-                const size_t off = (size_t)(qy * L + qx) * rowB + l * Tp + k0 + 4 * w;
-                sC[rc * GRAM_STRIDE + w] = __ldg(reinterpret_cast<const uint32_t*>(c + off));
-                sN[rc * GRAM_STRIDE + w] = __ldg(reinterpret_cast<const uint32_t*>(cn + off));
-            }
-            __syncthreads();
-            if (lane < (int)SW) {
-                const uint32_t* ownC = sC + (R + lane) * GRAM_STRIDE;
-                const uint32_t* ownN = sN + (R + lane) * GRAM_STRIDE;
-                const uint32_t* nbC = sC + (oy * ncol + lane) * GRAM_STRIDE;
-                const uint32_t* nbN = sN + (oy * ncol + lane) * GRAM_STRIDE;
-#pragma unroll
-                for (int w = 0; w < GRAM_KCW; ++w) {
-                    const uint32_t oc = ownC[w], on = ownN[w];
-#pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) {
-                        const uint32_t qc = nbC[i * GRAM_STRIDE + w], qn = nbN[i * GRAM_STRIDE + w];
-                        acc[i][0] = __dp4a(oc, qc, acc[i][0]);
-                        acc[i][1] = __dp4a(on, qc, acc[i][1]);
-                        acc[i][2] = __dp4a(oc, qn, acc[i][2]);
-                        acc[i][3] = __dp4a(on, qn, acc[i][3]);
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        if (lane < (int)SW) {
-            const uint32_t x = x0 + lane, p = y * L + x;
-            const int ncp = nc[(size_t)p * nl + l], nnp = nn[(size_t)p * nl + l];
-#pragma unroll
-            for (int i = 0; i < 2 * R + 1; ++i) {
-                const int ox = i - R;
-                if (oy == 0 && ox <= 0) continue;
-                const uint32_t q = ((y + oy) & (L - 1)) * L + ((x + ox + L) & (L - 1));
-                const int ncq = nc[(size_t)q * nl + l], nnq = nn[(size_t)q * nl + l];
-                int4 d;
-                d.x = ncp + ncq - 2 * (int)acc[i][0];  // D(c_p, c_q)
-                d.y = ncp + nnq - 2 * (int)acc[i][2];  // D(c_p, cn_q)
-                d.z = nnp + ncq - 2 * (int)acc[i][1];  // D(cn_p, c_q)
-                d.w = nnp + nnq - 2 * (int)acc[i][3];  // D(cn_p, cn_q)
-                dt_put(Dt, (size_t)nl * L * L * half_count_padded(R), ((size_t)l * L * L + p) * half_count_padded(R) + hpad_index(ox, oy, R), d);
-            }
-        }
-    }
-}
-
-// ------------------------------------------------------------- window distances on IMMA
-// Tensor-core version of k_gram (legacy warp MMA, mma.sync.m16n8k32 u8 x u8 -> s32, exact).
-// CTA = BY x BX = 4 x 16 pixels = 8 strips of 8 pixels; 16 warps; warp w owns strip w >> 1 and
-// the window rows oy in group (w & 1).  Per strip and oy:
-//   A (16 x K)  = rows [c_p0..c_p7 ; cn_p0..cn_p7]                     (M = 16)
-//   B (48 x K)  = [c ; cn] of the NT8 * 8 neighbour pixels of row y+oy  (6 n8 tiles for R = 7)
-//   D (16 x 48) += A B^T  ->  lane (g, t) holds, for pixel g and neighbour columns 2t, 2t+1 of
-//                            every tile, all four products <c_p,c_q>, <cn_p,c_q>, <c_p,cn_q>,
-//                            <cn_p,cn_q>.
-// The CTA stages rows y0 .. y0+BY-1+R, columns x0-R .. x0-R+NCOL-1 of c and cn for a K-chunk of
-// 64 bytes in shared memory (cp.async, double buffered; row stride 80 B: ldmatrix conflict-free).
-// Output layout Dt[l][p][h] (int4), h in the half window.
-namespace mma_gram {
-constexpr int BX = 16, BY = 4, KC = 64, ROWB = KC + 16, WARPS = 16;
-template <int R>
-struct Shape {
-    static constexpr int NT8 = (8 + 2 * R + 7) / 8;  // neighbour n8 tiles per version
-    static constexpr int NCOL = 8 + 8 * NT8;         // staged columns (covers both strips)
-    static constexpr int NROW = BY + R;              // staged rows
-    static constexpr int OYG = (R + 2) / 2;          // oy values per warp (2 groups)
-    static constexpr int STAGE = 2 * NROW * NCOL * ROWB;  // bytes per pipeline stage
-    static constexpr int H = 2 * R * R + 2 * R;
-};
-}  // namespace mma_gram
-
 __device__ __forceinline__ void cp_async16(uint32_t smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void imma16832(int* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
-    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%0,%1,%2,%3};"
-                 : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-template <int R>
-__global__ void __launch_bounds__(512, 1) k_gram_mma(const uint8_t* __restrict__ c, const uint8_t* __restrict__ cn,
-                                                     const int* __restrict__ nc, const int* __restrict__ nn,
-                                                     uint32_t L, uint32_t Tp, uint32_t nl, int4* __restrict__ Dt) {
-    using namespace mma_gram;
-    using S = Shape<R>;
-    extern __shared__ __align__(128) uint8_t smem[];
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-    const uint32_t x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int strip = warp >> 1, og = warp & 1;
-    const int sj = strip >> 1, xs = (strip & 1) * 8;  // strip row within the block, x offset
-    const int oy0 = og * S::OYG;
-    const uint32_t rowB = nl * Tp;
-    const int nchunk = S::NROW * S::NCOL * 2 * (KC / 16);
-    // staged row index: ((v * NROW) + r) * NCOL + col
-    auto srow = [&](int v, int r, int col) { return ((v * S::NROW) + r) * S::NCOL + col; };
-
-    for (uint32_t l = 0; l < nl; ++l) {
-        int acc[S::OYG][S::NT8][2][4];
-#pragma unroll
-        for (int a = 0; a < S::OYG; ++a)
-#pragma unroll
-            for (int t = 0; t < S::NT8; ++t)
-#pragma unroll
-                for (int v = 0; v < 2; ++v) acc[a][t][v][0] = acc[a][t][v][1] = acc[a][t][v][2] = acc[a][t][v][3] = 0;
-        const uint32_t nstage = Tp / KC;
-        auto issue = [&](uint32_t st) {
-            const uint32_t buf = sbase + (st & 1) * S::STAGE;
-            const uint32_t k0 = l * Tp + st * KC;
-            for (int j = threadIdx.x; j < nchunk; j += blockDim.x) {
-                const int ch = j & (KC / 16 - 1), row = j / (KC / 16);
-                const int col = row % S::NCOL, vr = row / S::NCOL, r = vr % S::NROW, v = vr / S::NROW;
-                const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
-                const uint8_t* src = (v ? cn : c) + (size_t)(qy * L + qx) * rowB + k0 + 16 * ch;
-                cp_async16(buf + row * ROWB + 16 * ch, src);
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        issue(0);
-        for (uint32_t st = 0; st < nstage; ++st) {
-            if (st + 1 < nstage) {
-                issue(st + 1);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-            } else {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-            }
-            __syncthreads();
-            const uint32_t buf = sbase + (st & 1) * S::STAGE;
-#pragma unroll
-            for (int kk = 0; kk < KC; kk += 32) {
-                // A fragment: matrices (c, k 0-15), (cn, k 0-15), (c, k 16-31), (cn, k 16-31)
-                uint32_t a[4];
-                {
-                    const int mi = lane >> 3, ri = lane & 7;
-                    const int v = mi & 1, kh = mi >> 1;
-                    ldsm_x4(buf + srow(v, sj, R + xs + ri) * ROWB + kk + 16 * kh, a[0], a[1], a[2], a[3]);
-                }
-#pragma unroll
-                for (int a_oy = 0; a_oy < S::OYG; ++a_oy) {
-                    const int oy = oy0 + a_oy;
-                    if (oy > R) break;
-#pragma unroll
-                    for (int t = 0; t < S::NT8; ++t) {
-                        // B fragments of tile t for both versions: matrices (c,k0-15),(c,k16-31),(cn,k0-15),(cn,k16-31)
-                        uint32_t b[4];
-                        const int mi = lane >> 3, ri = lane & 7;
-                        const int v = mi >> 1, kh = mi & 1;
-                        ldsm_x4(buf + srow(v, sj + oy, xs + 8 * t + ri) * ROWB + kk + 16 * kh, b[0], b[1], b[2], b[3]);
-                        imma16832(acc[a_oy][t][0], a, b[0], b[1]);
-                        imma16832(acc[a_oy][t][1], a, b[2], b[3]);
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        // epilogue: exact distances from the dot products and the row norms (norms of the staged
-        // neighbourhood are put in shared memory once per level; the operand buffers are free now)
-        int* snorm = reinterpret_cast<int*>(smem);  // [2][NROW][NCOL]
-        for (int j = threadIdx.x; j < 2 * S::NROW * S::NCOL; j += blockDim.x) {
-            const int col = j % S::NCOL, vr = j / S::NCOL, r = vr % S::NROW, v = vr / S::NROW;
-            const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
-            snorm[j] = (v ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
-        }
-        __syncthreads();
-        const int g = lane >> 2, tq = lane & 3;
-        const uint32_t px = x0 + xs + g, py = y0 + sj, p = py * L + px;
-        const int ncp = snorm[sj * S::NCOL + R + xs + g], nnp = snorm[(S::NROW + sj) * S::NCOL + R + xs + g];
-        const size_t obase = ((size_t)l * L * L + p) * half_count_padded(R), ndt = (size_t)nl * L * L * half_count_padded(R);
-#pragma unroll
-        for (int a_oy = 0; a_oy < S::OYG; ++a_oy) {
-            const int oy = oy0 + a_oy;
-            if (oy > R) break;
-#pragma unroll
-            for (int t = 0; t < S::NT8; ++t)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int n = 8 * t + 2 * tq + e, ox = n - R - g;
-                    if (ox < -R || ox > R || (oy == 0 && ox <= 0)) continue;
-                    const int qc = (sj + oy) * S::NCOL + xs + n;  // staged neighbour (row, column)
-                    const int ncq = snorm[qc], nnq = snorm[S::NROW * S::NCOL + qc];
-                    int4 d;
-                    d.x = ncp + ncq - 2 * acc[a_oy][t][0][e];      // D(c_p, c_q)
-                    d.y = ncp + nnq - 2 * acc[a_oy][t][1][e];      // D(c_p, cn_q)
-                    d.z = nnp + ncq - 2 * acc[a_oy][t][0][2 + e];  // D(cn_p, c_q)
-                    d.w = nnp + nnq - 2 * acc[a_oy][t][1][2 + e];  // D(cn_p, cn_q)
-                    dt_put(Dt, ndt, obase + hpad_index(ox, oy, R), d);
-                }
-        }
-        __syncthreads();  // snorm aliases the operand buffers of the next level
-    }
-}
-
-// IMMA window Gram v2: same staging as k_gram_mma, but warp w owns BOTH strips of block row
-// w >> 2 and the window rows oy in group (w & 3) (OYG2 of them).  The neighbour fragments of the
-// NT8 + 1 column tiles covering both strips are loaded once per (k32, oy) and shared by the two
-// strips' A fragments: 2 + OYG2 * (NT8 + 1) ldmatrix.x4 per 4 * OYG2 * NT8 mma (10 per 24 at R = 7).
-template <int R>
-struct Shape2 {
-    static constexpr int NT8 = (8 + 2 * R + 7) / 8;
-    static constexpr int NCOL = 8 + 8 * NT8;
-    static constexpr int NROW = mma_gram::BY + R;
-    static constexpr int OYG2 = (R + 4) / 4;  // oy per warp, 4 groups
-    static constexpr int STAGE = 2 * NROW * NCOL * mma_gram::ROWB;
-    static constexpr int H = 2 * R * R + 2 * R;
-};
-
-template <int R>
-__global__ void __launch_bounds__(512, 1) k_gram_mma2(const uint8_t* __restrict__ c, const uint8_t* __restrict__ cn,
-                                                      const int* __restrict__ nc, const int* __restrict__ nn,
-                                                      uint32_t L, uint32_t Tp, uint32_t nl, int4* __restrict__ Dt) {
-    using namespace mma_gram;
-    using S = Shape2<R>;
-    extern __shared__ __align__(128) uint8_t smem[];
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-    const uint32_t x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sj = warp >> 2, og = warp & 3;  // block row, oy group
-    const int oy0 = og * S::OYG2;
-    const uint32_t rowB = nl * Tp;
-    const int nchunk = S::NROW * S::NCOL * 2 * (KC / 16);
-    auto srow = [&](int v, int r, int col) { return ((v * S::NROW) + r) * S::NCOL + col; };
-
-    for (uint32_t l = 0; l < nl; ++l) {
-        int acc[2][S::OYG2][S::NT8][2][4];
-#pragma unroll
-        for (int st2 = 0; st2 < 2; ++st2)
-#pragma unroll
-            for (int a = 0; a < S::OYG2; ++a)
-#pragma unroll
-                for (int t = 0; t < S::NT8; ++t)
-#pragma unroll
-                    for (int v = 0; v < 2; ++v)
-                        acc[st2][a][t][v][0] = acc[st2][a][t][v][1] = acc[st2][a][t][v][2] = acc[st2][a][t][v][3] = 0;
-        const uint32_t nstage = Tp / KC;
-        auto issue = [&](uint32_t st) {
-            const uint32_t buf = sbase + (st & 1) * S::STAGE;
-            const uint32_t k0 = l * Tp + st * KC;
-            for (int j = threadIdx.x; j < nchunk; j += blockDim.x) {
-                const int ch = j & (KC / 16 - 1), row = j / (KC / 16);
-                const int col = row % S::NCOL, vr = row / S::NCOL, v = vr >= S::NROW, r = vr - v * S::NROW;
-                const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
-                const uint8_t* src = (v ? cn : c) + (size_t)(qy * L + qx) * rowB + k0 + 16 * ch;
-                cp_async16(buf + row * ROWB + 16 * ch, src);
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        issue(0);
-        for (uint32_t st = 0; st < nstage; ++st) {
-            if (st + 1 < nstage) {
-                issue(st + 1);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-            } else {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-            }
-            __syncthreads();
-            const uint32_t buf = sbase + (st & 1) * S::STAGE;
-            const int mi = lane >> 3, ri = lane & 7;
-#pragma unroll
-            for (int kk = 0; kk < KC; kk += 32) {
-                uint32_t a[2][4];
-#pragma unroll
-                for (int st2 = 0; st2 < 2; ++st2) {
-                    const int v = mi & 1, kh = mi >> 1;
-                    ldsm_x4(buf + srow(v, sj, R + 8 * st2 + ri) * ROWB + kk + 16 * kh, a[st2][0], a[st2][1],
-                            a[st2][2], a[st2][3]);
-                }
-#pragma unroll
-                for (int a_oy = 0; a_oy < S::OYG2; ++a_oy) {
-                    const int oy = oy0 + a_oy;
-                    if (oy > R) break;
-#pragma unroll
-                    for (int T = 0; T <= S::NT8; ++T) {
-                        uint32_t b[4];
-                        const int v = mi >> 1, kh = mi & 1;
-                        ldsm_x4(buf + srow(v, sj + oy, 8 * T + ri) * ROWB + kk + 16 * kh, b[0], b[1], b[2], b[3]);
-                        if (T < S::NT8) {  // strip 0 uses tiles 0 .. NT8-1
-                            imma16832(acc[0][a_oy][T][0], a[0], b[0], b[1]);
-                            imma16832(acc[0][a_oy][T][1], a[0], b[2], b[3]);
-                        }
-                        if (T >= 1) {  // strip 1 uses tiles 1 .. NT8
-                            imma16832(acc[1][a_oy][T - 1][0], a[1], b[0], b[1]);
-                            imma16832(acc[1][a_oy][T - 1][1], a[1], b[2], b[3]);
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        int* snorm = reinterpret_cast<int*>(smem);  // [2][NROW][NCOL]
-        for (int j = threadIdx.x; j < 2 * S::NROW * S::NCOL; j += blockDim.x) {
-            const int col = j % S::NCOL, vr = j / S::NCOL, r = vr % S::NROW, v = vr / S::NROW;
-            const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + col + L - R) & (L - 1);
-            snorm[j] = (v ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
-        }
-        __syncthreads();
-        const int g = lane >> 2, tq = lane & 3;
-#pragma unroll
-        for (int st2 = 0; st2 < 2; ++st2) {
-            const int xs = 8 * st2;
-            const uint32_t px = x0 + xs + g, py = y0 + sj, p = py * L + px;
-            const int ncp = snorm[sj * S::NCOL + R + xs + g], nnp = snorm[(S::NROW + sj) * S::NCOL + R + xs + g];
-            const size_t obase = ((size_t)l * L * L + p) * half_count_padded(R), ndt = (size_t)nl * L * L * half_count_padded(R);
-#pragma unroll
-            for (int a_oy = 0; a_oy < S::OYG2; ++a_oy) {
-                const int oy = oy0 + a_oy;
-                if (oy > R) break;
-#pragma unroll
-                for (int t = 0; t < S::NT8; ++t)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int n = 8 * t + 2 * tq + e, ox = n - R - g;
-                        if (ox < -R || ox > R || (oy == 0 && ox <= 0)) continue;
-                        const int qc = (sj + oy) * S::NCOL + xs + n;
-                        const int ncq = snorm[qc], nnq = snorm[S::NROW * S::NCOL + qc];
-                        int4 d;
-                        d.x = ncp + ncq - 2 * acc[st2][a_oy][t][0][e];      // D(c_p, c_q)
-                        d.y = ncp + nnq - 2 * acc[st2][a_oy][t][1][e];      // D(c_p, cn_q)
-                        d.z = nnp + ncq - 2 * acc[st2][a_oy][t][0][2 + e];  // D(cn_p, c_q)
-                        d.w = nnp + nnq - 2 * acc[st2][a_oy][t][1][2 + e];  // D(cn_p, cn_q)
-                        dt_put(Dt, ndt, obase + hpad_index(ox, oy, R), d);
-                    }
-            }
-        }
-        __syncthreads();
-    }
-}
 
 // ------------------------------------------------- window Gram on 5th-gen tensor cores (tcgen05)
-// UMMA version of the window Gram for R = 7.  CTA = 8 x 8 pixels; A (M = 128) =
-// [c rows of the 64 pixels ; cn rows]; the half-window neighbourhood (15 rows x 22 columns) is
-// split by neighbour rows into two TMEM chunks, ny 0..7 (B = 352 rows) and ny 8..14 (308 -> 320),
-// each accumulated over K = the level's T bytes with tcgen05.mma.kind::i8 (exact s32) into TMEM.
-// Operands are staged with cp.async in the canonical K-major SWIZZLE_128B layout (8-row, 1024-B
-// atoms), 128 B of K per stage, 3-stage ring; tcgen05.commit on a per-buffer mbarrier releases a
-// buffer.  Epilogue: tcgen05.ld 32 columns per (lane, neighbour row, version), a per-warp smem
-// scratch picks each lane's 15 window columns, D = |x|^2 + |y|^2 - 2<x,y>; lane (p, v) writes the
-// int2 (D(v_p, c_q), D(v_p, cn_q)) = .xy (v = 0) or .zw (v = 1) of Dt[l][p][h].
+// tcgen05 helpers: shared-memory matrix descriptors (K-major, 128-B swizzle), instruction
+// descriptors, MMA issue / commit, mbarrier waits and TMEM loads.
 namespace tc {
-constexpr int R = 7, NBC = 8 + 2 * R /*22*/, NBR = 8 + R /*15*/;
-constexpr int A_ROWS = 128, B_ROWS0 = 2 * 8 * NBC /*352*/, B_ROWS1 = 2 * 7 * NBC /*308*/;
-constexpr int N1_0 = B_ROWS0 - 256 /*96*/, N1_1 = 64; /* 308 -> 320 = 256 + 64 */
-constexpr int KB = 128;                                  // K bytes per stage (one swizzle row)
-constexpr int A_BYTES = A_ROWS * KB, B_BYTES = B_ROWS0 * KB;
-constexpr int STAGE = A_BYTES + B_BYTES;                 // 61440
-constexpr int NSTAGE = 3;
-constexpr int THREADS = 256;
-constexpr int SCR = 24;                                  // scratch ints per lane
-constexpr int SMEM = NSTAGE * STAGE + 8 * 32 * SCR * 4 + 2 * NBR * NBC * 4 + 64;
-constexpr int H = 2 * R * R + 2 * R;
-
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {  // K-major, SWIZZLE_128B, SBO = 1024
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 __host__ __device__ constexpr uint32_t idesc_u8(int M, int N) {
-#ifdef BN_EXP_F8
-    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);  // f32 += e4m3 x e4m3
-#else
     return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);  // s32 += u8 x u8, K-major
-#endif
 }
 __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-#ifdef BN_EXP_F8
-        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-#else
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-#endif
         "l"(da), "l"(db), "r"(idesc), "r"(accum));
 }
 __device__ __forceinline__ void commit(uint32_t bar) {
@@ -882,172 +474,6 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t* r) {
 }
 }  // namespace tc
 
-__global__ void __launch_bounds__(tc::THREADS, 1) k_gram_tc(const uint8_t* __restrict__ c, const uint8_t* __restrict__ cn,
-                                                            const int* __restrict__ nc, const int* __restrict__ nn,
-                                                            uint32_t L, uint32_t Tp, uint32_t nl,
-                                                            int4* __restrict__ Dt) {
-    using namespace tc;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-B alignment of the operand ring (SWIZZLE_128B atoms)
-    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t sring = (raw + 1023) & ~1023u;
-    uint8_t* gring = smem_raw + (sring - raw);
-    int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);          // [8 warps][32][SCR]
-    int* snorm = scratch + 8 * 32 * SCR;                                      // [2][NBR][NBC]
-    __shared__ __align__(8) uint64_t bars[NSTAGE + 1];
-    __shared__ uint32_t tmem_base_sh;
-    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t x0 = blockIdx.x * 8, y0 = blockIdx.y * 8, P = L * L;
-    const uint32_t rowB = nl * Tp;
-    if (threadIdx.x == 0) {
-        for (int b = 0; b <= NSTAGE; ++b)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * b) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&tmem_base_sh))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = tmem_base_sh;
-    uint32_t gs = 0;        // global stage counter (buffer = gs % 3, use = gs / 3)
-    uint32_t done_uses = 0; // uses of the chunk-done barrier
-    const uint32_t nk = Tp / KB;
-
-    for (uint32_t l = 0; l < nl; ++l) {
-        // norms of the neighbourhood (own pixels included) for this level
-        for (int j = threadIdx.x; j < 2 * NBR * NBC; j += blockDim.x) {
-            const int nx = j % NBC, vr = j / NBC, v = vr >= NBR, r = vr - v * NBR;
-            const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - R) & (L - 1);
-            snorm[j] = (v ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
-        }
-        for (int ch = 0; ch < 2; ++ch) {
-            const int NR = ch ? 7 : 8, nb_rows = 2 * NR * NBC, N1 = ch ? N1_1 : N1_0;
-            const int nrows = A_ROWS + nb_rows;
-            auto issue = [&](uint32_t kstage) {
-                const uint32_t b = gs % NSTAGE, use = gs / NSTAGE;
-                if (use > 0) mbar_wait(bar0 + 8 * b, (use - 1) & 1);  // MMAs of gs - 3 done with it
-                const uint32_t buf = sring + b * STAGE;
-                const uint32_t k0 = l * Tp + kstage * KB;
-                for (int j = threadIdx.x; j < nrows * 8; j += blockDim.x) {
-                    const int row = j >> 3, cc = j & 7;
-                    uint32_t pix;
-                    const uint8_t* base;
-                    uint32_t dst;
-                    if (row < A_ROWS) {
-                        const int v = row >> 6, pp = row & 63;
-                        pix = ((y0 + (pp >> 3)) & (L - 1)) * L + ((x0 + (pp & 7)) & (L - 1));
-                        base = v ? cn : c;
-                        dst = buf + (row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4);
-                    } else {
-                        const int br = row - A_ROWS, v = br >= NR * NBC, rr = br - v * NR * NBC;
-                        const int nyl = rr / NBC, nx = rr - nyl * NBC;
-                        pix = ((y0 + 8 * ch + nyl) & (L - 1)) * L + ((x0 + nx + L - R) & (L - 1));
-                        base = v ? cn : c;
-                        dst = buf + A_BYTES + (br >> 3) * 1024 + (br & 7) * 128 + ((cc ^ (br & 7)) << 4);
-                    }
-                    cp_async16(dst, base + (size_t)pix * rowB + k0 + 16 * cc);
-                }
-                asm volatile("cp.async.commit_group;" ::: "memory");
-                ++gs;
-            };
-            const uint32_t gs_first = gs;
-            issue(0);
-            if (nk > 1) issue(1);
-            for (uint32_t ks = 0; ks < nk; ++ks) {
-                if (ks + 2 < nk) {
-                    issue(ks + 2);
-                    asm volatile("cp.async.wait_group 2;" ::: "memory");
-                } else if (ks + 1 < nk) {
-                    asm volatile("cp.async.wait_group 1;" ::: "memory");
-                } else {
-                    asm volatile("cp.async.wait_group 0;" ::: "memory");
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t g = gs_first + ks, b = g % NSTAGE;
-                    const uint32_t sa = sring + b * STAGE, sb = sa + A_BYTES;
-#pragma unroll
-                    for (int kk = 0; kk < KB / 32; ++kk) {
-                        const uint32_t acc = (ks > 0 || kk > 0) ? 1u : 0u;
-                        mma(tmem, sdesc(sa + 32 * kk), sdesc(sb + 32 * kk), idesc_u8(128, 256), acc);
-                        mma(tmem + 256, sdesc(sa + 32 * kk), sdesc(sb + 256 * 128 + 32 * kk), idesc_u8(128, N1), acc);
-                    }
-                    commit(bar0 + 8 * b);
-                    if (ks + 1 == nk) commit(bar0 + 8 * NSTAGE);  // chunk done
-                }
-            }
-            // ---- epilogue of this chunk
-            mbar_wait(bar0 + 8 * NSTAGE, done_uses & 1);
-            ++done_uses;
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const int lq = warp & 3;                  // TMEM lane quarter = A rows 32 lq ..
-            const int arow = 32 * lq + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
-            const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
-            const int np = snorm[(v * NBR + dy) * NBC + dx + R];
-            int* scr = scratch + (warp * 32 + lane) * SCR;
-            int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
-            for (int nyl = (warp >> 2); nyl < NR; nyl += 2) {  // warps w and w+4 split the neighbour rows
-                const int ny = 8 * ch + nyl, oy = ny - dy;
-                uint32_t rc[32], rn[32];
-                ld32(tmem + ((uint32_t)(32 * lq) << 16) + nyl * NBC, rc);              // <v_p, c_q>
-                ld32(tmem + ((uint32_t)(32 * lq) << 16) + NR * NBC + nyl * NBC, rn);   // <v_p, cn_q>
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (oy < 0 || oy > R) continue;
-                // pick the window columns nx = dx + ox + R (lane-dependent) through the lane's scratch row
-                int dc[2 * R + 1], dn[2 * R + 1];
-#pragma unroll
-                for (int j = 0; j < NBC; ++j) scr[j] = (int)rc[j];
-#pragma unroll
-                for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + i];
-#pragma unroll
-                for (int j = 0; j < NBC; ++j) scr[j] = (int)rn[j];
-#pragma unroll
-                for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + i];
-#pragma unroll
-                for (int i = 0; i < 2 * R + 1; ++i) {
-                    const int ox = i - R, nx = dx + i;
-                    if (oy == 0 && ox <= 0) continue;
-                    const int nq_c = snorm[ny * NBC + nx], nq_n = snorm[(NBR + ny) * NBC + nx];
-                    out2[hpad_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncthreads();  // TMEM and scratch free for the next chunk / level
-        }
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-    }
-}
-
-// Warp-specialised tcgen05 window Gram (R = 7).  Roles: warps 0-3 epilogue (TMEM lanes 32w..),
-// warps 4-7 producers (cp.async into the SWIZZLE_128B ring), warp 8 lane 0 issues the UMMAs.
-// The half-window neighbourhood is split into three 5-row chunks (B = 220 -> N = 224 TMEM
-// columns), so two TMEM accumulators (256 columns each) let the epilogue of one chunk overlap the
-// MMAs of the next.  mbarriers: full[s] (128 producer arrivals), empty[s] (MMA commit),
-// tfull[u] (MMA commit), tempty[u] (128 epilogue arrivals).
-namespace tc2 {
-constexpr int R = 7, NBC = 8 + 2 * R, NBR = 8 + R;
-constexpr int CH_ROWS = 5, NCHUNK = 3, B_ROWS = 2 * CH_ROWS * NBC /*220*/, N = 224;
-constexpr int A_ROWS = 128, KB = 128, A_BYTES = A_ROWS * KB, B_BYTES = N * KB;
-constexpr int STAGE = A_BYTES + B_BYTES;  // 45056 = 44 KB (1024-aligned)
-constexpr int NSTAGE = 4;
-constexpr int NROWS = A_ROWS + B_ROWS;    // staged rows per stage (348)
-constexpr int THREADS = 288;
-constexpr int SCR = 25;  // odd row stride: conflict-free scratch writes
-constexpr int SMEM = NSTAGE * STAGE + 4 * 32 * SCR * 4 + 2 * NBR * NBC * 4 + NROWS * 8 + 1024;
-constexpr int H = 2 * R * R + 2 * R;
-}  // namespace tc2
-
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -1055,195 +481,24 @@ __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(tc2::THREADS, 1) k_gram_tc2(const uint8_t* __restrict__ c,
-                                                              const uint8_t* __restrict__ cn,
-                                                              const int* __restrict__ nc, const int* __restrict__ nn,
-                                                              uint32_t L, uint32_t Tp, uint32_t nl,
-                                                              int4* __restrict__ Dt) {
-    using namespace tc2;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t sring = (raw + 1023) & ~1023u;
-    uint8_t* gring = smem_raw + (sring - raw);
-    int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);  // [4 warps][32][SCR]
-    int* snorm = scratch + 4 * 32 * SCR;                              // [2][NBR][NBC]
-    long long* rowoff = reinterpret_cast<long long*>(snorm + 2 * NBR * NBC);  // [NROWS] (bit 0: version)
-    __shared__ __align__(8) uint64_t bars[2 * NSTAGE + 4];
-    __shared__ uint32_t tmem_sh;
-    const uint32_t b_full = (uint32_t)__cvta_generic_to_shared(&bars[0]);
-    const uint32_t b_empty = b_full + 8 * NSTAGE, b_tfull = b_full + 16 * NSTAGE, b_tempty = b_tfull + 16;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t x0 = blockIdx.x * 8, y0 = blockIdx.y * 8, P = L * L, rowB = nl * Tp;
-    const uint32_t nk = Tp / KB;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < NSTAGE; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_full + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_empty + 8 * i) : "memory");
-        }
-        for (int i = 0; i < 2; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_tfull + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_tempty + 8 * i) : "memory");
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&tmem_sh))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = tmem_sh;
-
-    if (warp >= 4 && warp < 8) {
-        // ------------------------------------------------------------------ producers
-        const int pt = threadIdx.x - 128, cc = pt & 7;
-        uint32_t g = 0;
-        for (uint32_t l = 0; l < nl; ++l)
-            for (int ch = 0; ch < NCHUNK; ++ch) {
-                named_bar(1, 128);  // everyone done issuing from the previous row table
-                for (int row = pt; row < NROWS; row += 128) {
-                    uint32_t pix, v;
-                    if (row < A_ROWS) {
-                        v = row >> 6;
-                        const int pp = row & 63;
-                        pix = ((y0 + (pp >> 3)) & (L - 1)) * L + ((x0 + (pp & 7)) & (L - 1));
-                    } else {
-                        const int br = row - A_ROWS;
-                        v = br >= CH_ROWS * NBC;
-                        const int rr = br - (int)v * CH_ROWS * NBC, nyl = rr / NBC, nx = rr - nyl * NBC;
-                        pix = ((y0 + CH_ROWS * ch + nyl) & (L - 1)) * L + ((x0 + nx + L - R) & (L - 1));
-                    }
-                    rowoff[row] = (((long long)pix * rowB) << 1) | v;
-                }
-                named_bar(1, 128);
-                for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
-                    const uint32_t b = g % NSTAGE, use = g / NSTAGE;
-                    if (use > 0) tc::mbar_wait(b_empty + 8 * b, (use - 1) & 1);
-                    const uint32_t buf = sring + b * STAGE;
-                    const size_t k0 = (size_t)l * Tp + ks * KB + 16 * cc;
-                    for (int row = pt >> 3; row < NROWS; row += 16) {
-                        const long long ro = rowoff[row];
-                        const uint8_t* src = ((ro & 1) ? cn : c) + (ro >> 1) + k0;
-                        const uint32_t dst = row < A_ROWS
-                                                 ? buf + (row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4)
-                                                 : buf + A_BYTES + ((row - A_ROWS) >> 3) * 1024 +
-                                                       ((row - A_ROWS) & 7) * 128 + ((cc ^ ((row - A_ROWS) & 7)) << 4);
-                        cp_async16(dst, src);
-                    }
-                    asm volatile("cp.async.commit_group;" ::: "memory");
-                    if (g >= 2) {  // stage g-2 has landed: publish it to the async proxy / MMA warp
-                        asm volatile("cp.async.wait_group 2;" ::: "memory");
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        mbar_arrive(b_full + 8 * ((g - 2) % NSTAGE));
-                    }
-                }
-            }
-        // drain the last two stages
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (g >= 2) mbar_arrive(b_full + 8 * ((g - 2) % NSTAGE));
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (g >= 1) mbar_arrive(b_full + 8 * ((g - 1) % NSTAGE));
-    } else if (warp == 8) {
-        // ------------------------------------------------------------------ MMA issuer
-        uint32_t g = 0, q = 0;
-        for (uint32_t l = 0; l < nl; ++l)
-            for (int ch = 0; ch < NCHUNK; ++ch, ++q) {
-                const uint32_t ub = q & 1, uu = q >> 1;
-                if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
-                    const uint32_t b = g % NSTAGE;
-                    tc::mbar_wait(b_full + 8 * b, (g / NSTAGE) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    if (lane == 0) {
-                        const uint32_t sa = sring + b * STAGE, sb = sa + A_BYTES;
-#pragma unroll
-                        for (int kk = 0; kk < KB / 32; ++kk)
-                            tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk),
-                                    tc::idesc_u8(128, N), (ks > 0 || kk > 0) ? 1u : 0u);
-                        tc::commit(b_empty + 8 * b);
-                        if (ks + 1 == nk) tc::commit(b_tfull + 8 * ub);
-                    }
-                    __syncwarp();
-                }
-            }
-    } else if (warp < 4) {
-        // ------------------------------------------------------------------ epilogue
-        const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
-        const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
-        int* scr = scratch + (warp * 32 + lane) * SCR;
-        uint32_t q = 0;
-        for (uint32_t l = 0; l < nl; ++l) {
-            named_bar(2, 128);  // all epilogue threads done with the previous level's norms
-            for (int j = threadIdx.x; j < 2 * NBR * NBC; j += 128) {
-                const int nx = j % NBC, vr = j / NBC, vv = vr >= NBR, r = vr - vv * NBR;
-                const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - R) & (L - 1);
-                snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
-            }
-            named_bar(2, 128);
-            const int np = snorm[(v * NBR + dy) * NBC + dx + R];
-            int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
-            for (int ch = 0; ch < NCHUNK; ++ch, ++q) {
-                const uint32_t ub = q & 1, uu = q >> 1;
-                tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
-                    const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
-                    uint32_t rc[32], rn[32];
-                    const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub + nyl * NBC;
-                    tc::ld32(ta, rc);                          // <v_p, c_q>
-                    tc::ld32(ta + CH_ROWS * NBC, rn);          // <v_p, cn_q>
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (oy < 0 || oy > R) continue;
-                    int dc[2 * R + 1], dn[2 * R + 1];
-#pragma unroll
-                    for (int j = 0; j < NBC; ++j) scr[j] = (int)rc[j];
-#pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + i];
-#pragma unroll
-                    for (int j = 0; j < NBC; ++j) scr[j] = (int)rn[j];
-#pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + i];
-#pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) {
-                        const int ox = i - R, nx = dx + i;
-                        if (oy == 0 && ox <= 0) continue;
-                        const int nq_c = snorm[ny * NBC + nx], nq_n = snorm[(NBR + ny) * NBC + nx];
-                        out2[hpad_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
-                    }
-                }
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(b_tempty + 8 * ub);
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-    }
-}
-
-// TMA-fed, warp-specialised tcgen05 window Gram (R = 7), one CTA per (8x8 block, level).
+// TMA-fed, warp-specialised tcgen05 window Gram, one (8x8 block, level) item at a time.
 // Every operand group is an aligned run of 8 pixels (x0 is a multiple of 8), i.e. 8 consecutive
-// rows of the [P][levels*Tp] count tensor: one 2D TMA box of 8 rows x 128 B per group, which is
-// exactly one SWIZZLE_128B atom of the UMMA K-major layout.  Per 128-B K stage: A = 16 boxes
-// (c and cn of the 8 block rows), B = 30 boxes (c and cn of 5 neighbour rows x 3 aligned groups
-// covering x0-8 .. x0+15; N = 240, the 2 columns outside the window are ignored).  A toroidal
-// wrap only ever moves a whole group.  Warp 0-3: epilogue, warp 4 lane 0: TMA producer, warp 5
-// lane 0: UMMA issuer.  Three neighbour chunks, two TMEM accumulators of 256 columns.
+// rows of the [y][x][row] count tensor: one TMA box of 8 rows x 128 elements per group, which is
+// exactly one SWIZZLE_128B atom of the UMMA K-major layout.  Per 128-element K stage: A = the c and
+// cn rows of the 64 block pixels (M = 128), B = the c and cn rows of 5 neighbour rows x 3 aligned
+// groups covering x0-8 .. x0+15 (N = 240; the 2 columns outside the window are ignored).  A toroidal
+// wrap only ever moves a whole group.  Warps 0-3: epilogue, warp 4 lane 0: TMA producer, warp 5
+// lane 0: UMMA issuer.  Three neighbour chunks (the R = 7 geometry, a superset of every R <= 7),
+// two TMEM accumulators of 256 columns.
 namespace tc3 {
 constexpr int R = 7, NBR = 8 + R, GRP = 3, NBX = 8 * GRP /*24*/;
 constexpr int CH_ROWS = 5, NCHUNK = 3, N = 2 * CH_ROWS * NBX /*240*/;
 constexpr int A_BYTES = 128 * 128, B_BYTES = N * 128;
 constexpr int STAGE = A_BYTES + B_BYTES;  // 47104 = 46 KB
-constexpr int NSTAGE = 4;
+#ifndef BN_GRAM_NSTAGE
+#define BN_GRAM_NSTAGE 4
+#endif
+constexpr int NSTAGE = BN_GRAM_NSTAGE;
 constexpr int THREADS = 192;
 constexpr int SCR = 25;  // odd row stride: conflict-free scratch writes
 constexpr int SMEM = NSTAGE * STAGE + 4 * 32 * SCR * 4 + 2 * NBR * NBX * 4 + 1024;
@@ -1272,156 +527,6 @@ struct CountMaps {
     CUtensorMap a, b, s;
 };
 
-__global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc3(const __grid_constant__ CountMaps mc,
-                                                              const __grid_constant__ CountMaps mn,
-                                                              const int* __restrict__ nc, const int* __restrict__ nn,
-                                                              uint32_t L, uint32_t Tp, uint32_t nl,
-                                                              int4* __restrict__ Dt) {
-    using namespace tc3;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t sring = (raw + 1023) & ~1023u;
-    uint8_t* gring = smem_raw + (sring - raw);
-    int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);  // [4 warps][32][SCR]
-    int* snorm = scratch + 4 * 32 * SCR;                              // [2][NBR][NBX], x from x0-8
-    __shared__ __align__(8) uint64_t bars[2 * NSTAGE + 4];
-    __shared__ uint32_t tmem_sh;
-    const uint32_t b_full = (uint32_t)__cvta_generic_to_shared(&bars[0]);
-    const uint32_t b_empty = b_full + 8 * NSTAGE, b_tfull = b_full + 16 * NSTAGE, b_tempty = b_tfull + 16;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t x0 = blockIdx.x * 8, y0 = blockIdx.y * 8, l = blockIdx.z, P = L * L;
-    const uint32_t nk = Tp / 128;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < NSTAGE; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_full + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_empty + 8 * i) : "memory");
-        }
-        for (int i = 0; i < 2; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_tfull + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_tempty + 8 * i) : "memory");
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&tmem_sh))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = tmem_sh;
-
-    if (warp == 4) {
-        // --------------------------------------------------------------- TMA producer
-        if (lane == 0) {
-            uint32_t g = 0;
-            for (int ch = 0; ch < NCHUNK; ++ch)
-                for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
-                    const uint32_t b = g % NSTAGE, use = g / NSTAGE;
-                    if (use > 0) tc::mbar_wait(b_empty + 8 * b, (use - 1) & 1);
-                    const uint32_t buf = sring + b * STAGE, bar = b_full + 8 * b;
-                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(STAGE)
-                                 : "memory");
-                    const int kx = (int)(l * Tp + ks * 128);
-                    const bool whole = x0 >= 8 && x0 + 16 <= L && y0 + CH_ROWS * (ch + 1) <= L;
-                    for (int v = 0; v < 2; ++v) {
-                        const CountMaps& m = v ? mn : mc;
-                        tma_3d(buf + v * 8192, &m.a, kx, (int)x0, (int)y0, bar);  // 64 block rows
-                        const uint32_t bdst = buf + A_BYTES + v * CH_ROWS * GRP * 1024;
-                        if (whole) {
-                            tma_3d(bdst, &m.b, kx, (int)x0 - 8, (int)(y0 + CH_ROWS * ch), bar);
-                        } else {
-                            for (int nyl = 0; nyl < CH_ROWS; ++nyl)
-                                for (int gx = 0; gx < GRP; ++gx) {
-                                    const uint32_t py = (y0 + CH_ROWS * ch + nyl) & (L - 1);
-                                    const uint32_t px = (x0 + 8 * gx + L - 8) & (L - 1);
-                                    tma_3d(bdst + (nyl * GRP + gx) * 1024, &m.s, kx, (int)px, (int)py, bar);
-                                }
-                        }
-                    }
-                }
-        }
-    } else if (warp == 5) {
-        // --------------------------------------------------------------- UMMA issuer
-        uint32_t g = 0;
-        for (int ch = 0; ch < NCHUNK; ++ch) {
-            const uint32_t ub = ch & 1, uu = ch >> 1;
-            if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
-                const uint32_t b = g % NSTAGE;
-                tc::mbar_wait(b_full + 8 * b, (g / NSTAGE) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (lane == 0) {
-                    const uint32_t sa = sring + b * STAGE, sb = sa + A_BYTES;
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk),
-                                tc::idesc_u8(128, N), (ks > 0 || kk > 0) ? 1u : 0u);
-                    tc::commit(b_empty + 8 * b);
-                    if (ks + 1 == nk) tc::commit(b_tfull + 8 * ub);
-                }
-                __syncwarp();
-            }
-        }
-    } else if (warp < 4) {
-        // --------------------------------------------------------------- epilogue
-        // neighbourhood norms of this level (rows y0 .. y0+14, columns x0-8 .. x0+15), loaded while
-        // the producer and the MMA warp already run
-        for (int j = threadIdx.x; j < 2 * NBR * NBX; j += 128) {
-            const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;
-            const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - 8) & (L - 1);
-            snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
-        }
-        named_bar(2, 128);
-        const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
-        const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
-        int* scr = scratch + (warp * 32 + lane) * SCR;
-        const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
-        int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
-        for (int ch = 0; ch < NCHUNK; ++ch) {
-            const uint32_t ub = ch & 1, uu = ch >> 1;
-            tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
-                const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
-                uint32_t rc[32], rn[32];
-                const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub + nyl * NBX;
-                tc::ld32(ta, rc);                       // <v_p, c_q>, q in x0-8 .. x0+23 of row ny
-                tc::ld32(ta + CH_ROWS * NBX, rn);       // <v_p, cn_q>
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (oy < 0 || oy > R) continue;
-                int dc[2 * R + 1], dn[2 * R + 1];
-#pragma unroll
-                for (int j = 0; j < NBX; ++j) scr[j] = (int)rc[j];
-#pragma unroll
-                for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + 1 + i];
-#pragma unroll
-                for (int j = 0; j < NBX; ++j) scr[j] = (int)rn[j];
-#pragma unroll
-                for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + 1 + i];
-#pragma unroll
-                for (int i = 0; i < 2 * R + 1; ++i) {
-                    const int ox = i - R, nx = dx + 1 + i;
-                    if (oy == 0 && ox <= 0) continue;
-                    const int nq_c = snorm[ny * NBX + nx], nq_n = snorm[(NBR + ny) * NBX + nx];
-                    out2[hpad_index(ox, oy, R)] = make_int2(np + nq_c - 2 * dc[i], np + nq_n - 2 * dn[i]);
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(b_tempty + 8 * ub);
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-    }
-}
-
 // 256-bit store of four int2 records {(x[0], y[0]) .. (x[3], y[3])} (one whole 32-byte sector).
 __device__ __forceinline__ void st_v8(int2* dst, const int* x, const int* y) {
     asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(x[0]), "r"(y[0]), "r"(x[1]),
@@ -1429,21 +534,49 @@ __device__ __forceinline__ void st_v8(int2* dst, const int* x, const int* y) {
                  : "memory");
 }
 
-// Persistent version of k_gram_tc3: one CTA per SM walks the (8x8 block, level) items
-// cta, cta + G, ...  The stage ring and the two TMEM accumulators continue across items, so the
-// TMA producer and the MMA warp run into the next item while the epilogue still drains the
-// previous one, and the per-CTA start-up (TMEM allocation, barrier set-up) and the last chunk's
-// epilogue are paid once per SM instead of once per item.  The epilogue loads the next item's
-// neighbourhood norms itself after finishing an item (the MMAs of that item are already
-// running).  Same TMA boxes, UMMA descriptors and epilogue arithmetic as k_gram_tc3.
-__global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_constant__ CountMaps mc,
-                                                              const __grid_constant__ CountMaps mn,
+// Row formats of a level's count rows (SURVEY §8 f3 narrow storage).  BN_FMT_U8:
+// the counts c (uint8, kind::i8, exact s32 accumulation).  BN_FMT_E2M1 / BN_FMT_E3M2: the deltas
+// delta = c - off_i (off_i = round(N_l I_ref,i), one integer per integrand and level) packed 16 per
+// 8 (e2m1, 4-bit, |delta| <= 4 exact) or 12 bytes (e3m2, 6-bit, |delta| <= 8 exact); the TMA
+// unpacks them into the same 128-B-swizzled shared-memory layout as bytes and the tensor core
+// multiplies them with kind::f8f6f4 into fp32 (exact: |<x,y>| < 2^24; tools/narrow_mma_check.cu).
+// The offsets cancel in every distance: D = sum (c_p - c_q)^2 = sum (delta_p - delta_q)^2, and the
+// norms stored beside the rows are |delta|^2.
+enum : uint32_t { BN_FMT_U8 = 0, BN_FMT_E2M1 = 1, BN_FMT_E3M2 = 2 };
+__host__ __device__ constexpr uint32_t fmt_bits(uint32_t f) { return f == BN_FMT_U8 ? 8 : f == BN_FMT_E2M1 ? 4 : 6; }
+__host__ __device__ constexpr uint32_t idesc_f8(uint32_t f, int M, int N) {  // f32 += e2m1 / e3m2, K-major
+    return (1u << 4) | ((f == BN_FMT_E2M1 ? 5u : 4u) << 7) | ((f == BN_FMT_E2M1 ? 5u : 4u) << 10) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+// TMA maps of every level (c and cn operands) and the level's row format.
+struct GramMaps {
+    CountMaps c[8], n[8];
+    uint32_t fmt[8];
+};
+
+// Persistent window Gram: one CTA per SM walks the (8x8 block, level) items cta, cta + G, ...
+// The stage ring and the two TMEM accumulators continue across items, so the TMA producer and
+// the MMA warp run into the next item while the epilogue still drains the previous one, and the
+// per-CTA start-up (TMEM allocation, barrier set-up) is paid once per SM.  The epilogue loads the
+// next item's neighbourhood norms itself after finishing an item (its MMAs are already running),
+// forms D = |x|^2 + |y|^2 - 2<x,y> for the half-window offsets of radius R and writes each
+// (pixel, window row) run of the two int2 planes with whole-sector 256-bit stores.
+template <int R>
+__global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_constant__ GramMaps gm,
                                                               const int* __restrict__ nc, const int* __restrict__ nn,
                                                               uint32_t L, uint32_t Tp, uint32_t nl,
                                                               int4* __restrict__ Dt,
                                                               const unsigned int* __restrict__ rows_done,
                                                               uint32_t rows_target) {
-    using namespace tc3;
+    using tc3::NBR; using tc3::NBX; using tc3::GRP; using tc3::CH_ROWS; using tc3::NCHUNK; using tc3::N;
+    using tc3::A_BYTES; using tc3::STAGE; using tc3::NSTAGE; using tc3::SCR;
+    constexpr int RW = ru4(2 * R + 1), R0 = ru4(R), NV = RW > R + 1 + R0 ? RW : R + 1 + R0;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t sring = (raw + 1023) & ~1023u;
@@ -1478,27 +611,13 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_sh;
-    // items: blocks in raster order within a level, levels outermost (each level's count slice is
-    // an L2-resident working set); when following k_counts row by row (rows_done), the level is
-    // the fastest index instead, so the Gram sweeps the tile's block rows front to back
-// Items block-major (the levels of a block consecutive) so that the window distances written last
-// are whole pixels' rows, which k_lut (BN_LUT_REVERSE) reads first while they are still in L2
-// (C3 lut 0.061 -> 0.058 ms, Gram unchanged).
-#ifndef BN_GRAM_BLOCK_MAJOR
-#define BN_GRAM_BLOCK_MAJOR 1
-#endif
+    // Items block-major (the levels of a block consecutive) so that the window distances written last
+    // are whole pixels' rows, which k_lut (BN_LUT_REVERSE) reads first while they are still in L2.
     auto item_xyl = [&](uint32_t it, uint32_t& x0, uint32_t& y0, uint32_t& l) {
-        if (rows_done || BN_GRAM_BLOCK_MAJOR) {
-            l = it % nl;
-            const uint32_t b = it / nl;
-            x0 = 8 * (b % nbx);
-            y0 = 8 * (b / nbx);
-        } else {
-            const uint32_t bx = it % nbx, r = it / nbx;
-            x0 = 8 * bx;
-            y0 = 8 * (r % nbx);
-            l = r / nbx;
-        }
+        l = it % nl;
+        const uint32_t b = it / nl;
+        x0 = 8 * (b % nbx);
+        y0 = 8 * (b / nbx);
     };
     // wait until every tile row y0 .. y0 + 14 (mod L) of this pass's candidates is published by
     // k_counts (acquire), then order the following TMA (async-proxy) reads after it
@@ -1525,17 +644,23 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                 uint32_t x0, y0, l;
                 item_xyl(it, x0, y0, l);
                 wait_rows(y0);
+                // transaction bytes = the packed global bytes the boxes read (128 + 240 rows)
+                const uint32_t tx = (uint32_t)(128 + N) * 128 * fmt_bits(gm.fmt[l]) / 8;
                 for (int ch = 0; ch < NCHUNK; ++ch)
                     for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
                         const uint32_t b = g % NSTAGE, use = g / NSTAGE;
                         if (use > 0) tc::mbar_wait(b_empty + 8 * b, (use - 1) & 1);
                         const uint32_t buf = sring + b * STAGE, bar = b_full + 8 * b;
-                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(STAGE)
+#ifdef BN_GRAM_PROBE_NOTMA  // timing probe (not product): no operand loads
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+                        continue;
+#endif
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx)
                                      : "memory");
-                        const int kx = (int)(l * Tp + ks * 128);
+                        const int kx = (int)(ks * 128);
                         const bool whole = x0 >= 8 && x0 + 16 <= L && y0 + CH_ROWS * (ch + 1) <= L;
                         for (int v = 0; v < 2; ++v) {
-                            const CountMaps& m = v ? mn : mc;
+                            const CountMaps& m = v ? gm.n[l] : gm.c[l];
                             tma_3d(buf + v * 8192, &m.a, kx, (int)x0, (int)y0, bar);  // 64 block rows
                             const uint32_t bdst = buf + A_BYTES + v * CH_ROWS * GRP * 1024;
                             if (whole) {
@@ -1555,7 +680,11 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     } else if (warp == 5) {
         // --------------------------------------------------------------- UMMA issuer
         uint32_t g = 0, cc = 0;  // stage counter, chunk counter (accumulator ring)
-        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x)
+        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+            uint32_t x0, y0, l;
+            item_xyl(it, x0, y0, l);
+            const uint32_t f = gm.fmt[l];
+            const uint32_t idesc = f == BN_FMT_U8 ? tc::idesc_u8(128, N) : idesc_f8(f, 128, N);
             for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
                 const uint32_t ub = cc & 1, uu = cc >> 1;
                 if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
@@ -1566,16 +695,24 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     if (lane == 0) {
                         const uint32_t sa = sring + b * STAGE, sb = sa + A_BYTES;
+#ifndef BN_GRAM_PROBE_NOMMA
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk),
-                                    tc::idesc_u8(128, N), (ks > 0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < 4; ++kk) {
+                            if (f == BN_FMT_U8)
+                                tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk), idesc,
+                                        (ks > 0 || kk > 0) ? 1u : 0u);
+                            else
+                                mma_f8(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk), idesc,
+                                       (ks > 0 || kk > 0) ? 1u : 0u);
+                        }
+#endif
                         tc::commit(b_empty + 8 * b);
                         if (ks + 1 == nk) tc::commit(b_tfull + 8 * ub);
                     }
                     __syncwarp();
                 }
             }
+        }
     } else if (warp < 4) {
         // --------------------------------------------------------------- epilogue
         const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
@@ -1584,6 +721,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
         for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
             uint32_t x0, y0, l;
             item_xyl(it, x0, y0, l);
+            const bool fp = gm.fmt[l] != BN_FMT_U8;  // fp32 accumulator (exact integers)
             if (threadIdx.x == 0) wait_rows(y0);  // the candidates' norms come from k_counts too
             named_bar(2, 128);  // previous item's norms are no longer read
             for (int j = threadIdx.x; j < 2 * NBR * NBX; j += 128) {
@@ -1599,6 +737,13 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                 const uint32_t ub = cc & 1, uu = cc >> 1;
                 tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#ifdef BN_GRAM_PROBE_NOEPI  // timing probe (not product): no TMEM reads, no stores
+                if (true) {
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    mbar_arrive(b_tempty + 8 * ub);
+                    continue;
+                }
+#endif
                 for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
                     const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
                     uint32_t rc[32], rn[32];
@@ -1609,237 +754,33 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                     if (oy < 0 || oy > R) continue;
                     int dc[2 * R + 1], dn[2 * R + 1];
 #pragma unroll
-                    for (int j = 0; j < NBX; ++j) scr[j] = (int)rc[j];
+                    for (int j = 0; j < NBX; ++j) scr[j] = fp ? __float2int_rz(__uint_as_float(rc[j])) : (int)rc[j];
 #pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + 1 + i];
+                    for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + 8 - R + i];
 #pragma unroll
-                    for (int j = 0; j < NBX; ++j) scr[j] = (int)rn[j];
+                    for (int j = 0; j < NBX; ++j) scr[j] = fp ? __float2int_rz(__uint_as_float(rn[j])) : (int)rn[j];
 #pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + 1 + i];
-                    // the row's 15 records (+1 zero pad) are 128 contiguous, 64-byte aligned bytes of
-                    // plane v: four whole-sector 256-bit stores (two for the oy = 0 row, ox = 1..R)
-                    int vx[16], vy[16];
+                    for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + 8 - R + i];
+                    // the row's 2R+1 records (+ zero pads) are whole 32-byte sectors of plane v:
+                    // ru4(2R+1)/4 256-bit stores (ru4(R)/4 for the oy = 0 row, ox = 1..R)
+                    int vx[NV], vy[NV];
 #pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) {
-                        const int nx = dx + 1 + i;
-                        vx[i] = np + snorm[ny * NBX + nx] - 2 * dc[i];
-                        vy[i] = np + snorm[(NBR + ny) * NBX + nx] - 2 * dn[i];
+                    for (int i = 0; i < NV; ++i) {
+                        if (i < 2 * R + 1) {
+                            const int nx = dx + 8 - R + i;
+                            vx[i] = np + snorm[ny * NBX + nx] - 2 * dc[i];
+                            vy[i] = np + snorm[(NBR + ny) * NBX + nx] - 2 * dn[i];
+                        } else {
+                            vx[i] = vy[i] = 0;
+                        }
                     }
-                    vx[15] = vy[15] = 0;
                     if (oy > 0) {
                         int2* o = out2 + hpad_index(-R, oy, R);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) st_v8(o + 4 * q, vx + 4 * q, vy + 4 * q);
+                        for (int q = 0; q < RW / 4; ++q) st_v8(o + 4 * q, vx + 4 * q, vy + 4 * q);
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 2; ++q) st_v8(out2 + 4 * q, vx + R + 1 + 4 * q, vy + R + 1 + 4 * q);
-                    }
-                }
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(b_tempty + 8 * ub);
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-    }
-}
-
-// k_gram_tc5: k_gram_tc4 with the A operand resident.  For Tp <= 1024 (nk <= 8 K-slices) the
-// block's 128 A rows (c and cn of its 64 pixels) for all K fit in shared memory (8 x 16 KB), so
-// they are loaded once per item instead of once per neighbour chunk: the L2->SM operand stream
-// drops from (A + B) to B per (chunk, K-slice) after the first chunk (1104 -> 848 rows of 128 B
-// per item, -23%).  A slot ks is released by the MMA of the item's
-// last chunk on it and refilled with the next item's slice ks.  B streams through a 2-stage ring,
-// which keeps only 60 KB in flight (tc4: 184 KB): on C3 it is slower than tc4 (0.127 vs 0.120 ms),
-// so it is opt-in (BN_GRAM=tc5).
-namespace tc5 {
-constexpr int NKMAX = 8, NBST = 2;
-constexpr int A_SLOT = tc3::A_BYTES, B_STAGE = tc3::B_BYTES;  // 16 KB, 30 KB
-constexpr int SMEM = NKMAX * A_SLOT + NBST * B_STAGE + 4 * 32 * tc3::SCR * 4 + 2 * tc3::NBR * tc3::NBX * 4 + 1024;
-}  // namespace tc5
-
-__global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc5(const __grid_constant__ CountMaps mc,
-                                                              const __grid_constant__ CountMaps mn,
-                                                              const int* __restrict__ nc, const int* __restrict__ nn,
-                                                              uint32_t L, uint32_t Tp, uint32_t nl,
-                                                              int4* __restrict__ Dt) {
-    using namespace tc3;
-    using tc5::A_SLOT;
-    using tc5::B_STAGE;
-    using tc5::NBST;
-    using tc5::NKMAX;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t sbase = (raw + 1023) & ~1023u;
-    const uint32_t sA = sbase, sB = sbase + NKMAX * A_SLOT;
-    uint8_t* gbase = smem_raw + (sbase - raw);
-    int* scratch = reinterpret_cast<int*>(gbase + NKMAX * A_SLOT + NBST * B_STAGE);  // [4 warps][32][SCR]
-    int* snorm = scratch + 4 * 32 * SCR;                                              // [2][NBR][NBX]
-    __shared__ __align__(8) uint64_t bars[2 * NKMAX + 2 * NBST + 4];
-    __shared__ uint32_t tmem_sh;
-    const uint32_t a_full = (uint32_t)__cvta_generic_to_shared(&bars[0]), a_empty = a_full + 8 * NKMAX;
-    const uint32_t b_full = a_empty + 8 * NKMAX, b_empty = b_full + 8 * NBST;
-    const uint32_t b_tfull = b_empty + 8 * NBST, b_tempty = b_tfull + 16;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t nbx = L / 8, nitems = nbx * nbx * nl, P = L * L;
-    const uint32_t nk = Tp / 128;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < NKMAX; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a_full + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a_empty + 8 * i) : "memory");
-        }
-        for (int i = 0; i < NBST; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_full + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_empty + 8 * i) : "memory");
-        }
-        for (int i = 0; i < 2; ++i) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_tfull + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_tempty + 8 * i) : "memory");
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&tmem_sh))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = tmem_sh;
-    auto item_xyl = [&](uint32_t it, uint32_t& x0, uint32_t& y0, uint32_t& l) {
-        const uint32_t bx = it % nbx, r = it / nbx;
-        x0 = 8 * bx;
-        y0 = 8 * (r % nbx);
-        l = r / nbx;
-    };
-
-    if (warp == 4) {
-        // --------------------------------------------------------------- TMA producer
-        if (lane == 0) {
-            uint32_t g = 0, ii = 0;  // B stage counter, local item counter
-            for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ii) {
-                uint32_t x0, y0, l;
-                item_xyl(it, x0, y0, l);
-                for (int ch = 0; ch < NCHUNK; ++ch)
-                    for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
-                        const int kx = (int)(l * Tp + ks * 128);
-                        if (ch == 0) {  // A slice ks of this item (its slot was freed by the last item's chunk 2)
-                            if (ii > 0) tc::mbar_wait(a_empty + 8 * ks, (ii - 1) & 1);
-                            const uint32_t abar = a_full + 8 * ks, adst = sA + ks * A_SLOT;
-                            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(abar), "r"(A_SLOT)
-                                         : "memory");
-                            tma_3d(adst, &mc.a, kx, (int)x0, (int)y0, abar);
-                            tma_3d(adst + 8192, &mn.a, kx, (int)x0, (int)y0, abar);
-                        }
-                        const uint32_t b = g % NBST, use = g / NBST;
-                        if (use > 0) tc::mbar_wait(b_empty + 8 * b, (use - 1) & 1);
-                        const uint32_t bdst0 = sB + b * B_STAGE, bar = b_full + 8 * b;
-                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(B_STAGE)
-                                     : "memory");
-                        const bool whole = x0 >= 8 && x0 + 16 <= L && y0 + CH_ROWS * (ch + 1) <= L;
-                        for (int v = 0; v < 2; ++v) {
-                            const CountMaps& m = v ? mn : mc;
-                            const uint32_t bdst = bdst0 + v * CH_ROWS * GRP * 1024;
-                            if (whole) {
-                                tma_3d(bdst, &m.b, kx, (int)x0 - 8, (int)(y0 + CH_ROWS * ch), bar);
-                            } else {
-                                for (int nyl = 0; nyl < CH_ROWS; ++nyl)
-                                    for (int gx = 0; gx < GRP; ++gx) {
-                                        const uint32_t py = (y0 + CH_ROWS * ch + nyl) & (L - 1);
-                                        const uint32_t px = (x0 + 8 * gx + L - 8) & (L - 1);
-                                        tma_3d(bdst + (nyl * GRP + gx) * 1024, &m.s, kx, (int)px, (int)py, bar);
-                                    }
-                            }
-                        }
-                    }
-            }
-        }
-    } else if (warp == 5) {
-        // --------------------------------------------------------------- UMMA issuer
-        uint32_t g = 0, cc = 0, ii = 0;
-        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x, ++ii)
-            for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
-                const uint32_t ub = cc & 1, uu = cc >> 1;
-                if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
-                    const uint32_t b = g % NBST;
-                    if (ch == 0) tc::mbar_wait(a_full + 8 * ks, ii & 1);
-                    tc::mbar_wait(b_full + 8 * b, (g / NBST) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    if (lane == 0) {
-                        const uint32_t sa = sA + ks * A_SLOT, sb = sB + b * B_STAGE;
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk),
-                                    tc::idesc_u8(128, N), (ks > 0 || kk > 0) ? 1u : 0u);
-                        tc::commit(b_empty + 8 * b);
-                        if (ch + 1 == NCHUNK) tc::commit(a_empty + 8 * ks);  // last use of A slice ks
-                        if (ks + 1 == nk) tc::commit(b_tfull + 8 * ub);
-                    }
-                    __syncwarp();
-                }
-            }
-    } else if (warp < 4) {
-        // --------------------------------------------------------------- epilogue (as k_gram_tc4)
-        const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
-        int* scr = scratch + (warp * 32 + lane) * SCR;
-        uint32_t cc = 0;
-        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
-            uint32_t x0, y0, l;
-            item_xyl(it, x0, y0, l);
-            named_bar(2, 128);  // previous item's norms are no longer read
-            for (int j = threadIdx.x; j < 2 * NBR * NBX; j += 128) {
-                const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;
-                const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - 8) & (L - 1);
-                snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
-            }
-            named_bar(2, 128);
-            const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
-            const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
-            int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
-            for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
-                const uint32_t ub = cc & 1, uu = cc >> 1;
-                tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
-                    const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
-                    uint32_t rc[32], rn[32];
-                    const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub + nyl * NBX;
-                    tc::ld32(ta, rc);
-                    tc::ld32(ta + CH_ROWS * NBX, rn);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (oy < 0 || oy > R) continue;
-                    int dc[2 * R + 1], dn[2 * R + 1];
-#pragma unroll
-                    for (int j = 0; j < NBX; ++j) scr[j] = (int)rc[j];
-#pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) dc[i] = scr[dx + 1 + i];
-#pragma unroll
-                    for (int j = 0; j < NBX; ++j) scr[j] = (int)rn[j];
-#pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) dn[i] = scr[dx + 1 + i];
-                    int vx[16], vy[16];
-#pragma unroll
-                    for (int i = 0; i < 2 * R + 1; ++i) {
-                        const int nx = dx + 1 + i;
-                        vx[i] = np + snorm[ny * NBX + nx] - 2 * dc[i];
-                        vy[i] = np + snorm[(NBR + ny) * NBX + nx] - 2 * dn[i];
-                    }
-                    vx[15] = vy[15] = 0;
-                    if (oy > 0) {
-                        int2* o = out2 + hpad_index(-R, oy, R);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) st_v8(o + 4 * q, vx + 4 * q, vy + 4 * q);
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 2; ++q) st_v8(out2 + 4 * q, vx + R + 1 + 4 * q, vy + R + 1 + 4 * q);
+                        for (int q = 0; q < R0 / 4; ++q) st_v8(out2 + 4 * q, vx + R + 1 + 4 * q, vy + R + 1 + 4 * q);
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -2269,117 +1210,15 @@ struct LaneOffsets {
     }
 };
 
-template <int R>
-struct WinTermsLocal : WinTerms<R> {
-    // sum with the flags read from this CTA's shared-memory copy
-    __device__ __forceinline__ i128 sum_local(const uint8_t* sflags, uint32_t L, uint32_t p, const LaneOffsets<R>& off,
-                                              const DTabs T) const {
-        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
-        const int lane = threadIdx.x & 31;
-        const uint32_t x = p & (L - 1), y = p / L;
-        i128 acc = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const int w = lane + 32 * j;
-            if (w < WN) {
-                const uint32_t q = ((y + off.oy[j]) & (L - 1)) * L + ((x + off.ox[j]) & (L - 1));
-                const bool f = sflags[q];
-                const long long v = f ? this->v1[j] : this->v0[j];
-                if (v != DT_ESC) {
-                    acc += (i128)v;
-                } else {  // rare: exact int128 term from the escape table
-                    const longlong2 e = (f ? T.x1 : T.x0)[(size_t)p * WN + w];
-                    acc += ((i128)e.y << 64) | (u128)(unsigned long long)e.x;
-                }
-            }
-        }
-        return warp_sum_i128_redux((unsigned long long)acc, (unsigned long long)(acc >> 64));
-    }
-};
-
-template <int R, int mode>
-__global__ void __launch_bounds__(512, 1) k_decide_cluster(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
-                                                           const DTabs T, uint8_t* __restrict__ acc,
-                                                           i128* __restrict__ dEp, uint8_t* __restrict__ log) {
-    constexpr int WN = WinTerms<R>::WN;
-    extern __shared__ __align__(16) uint8_t dsm[];
-    __shared__ uint8_t sDelta[8 * 16];
-    __shared__ uint32_t sKappa[64];
-    __shared__ uint32_t sSlot[2][32];
-    const uint32_t nb = L / 8, M = nb * nb, P = L * L;
-    const uint32_t g = blockIdx.x, ncta = gridDim.x;
-    const uint32_t first = g * cpc, nslot = mode ? 2 * cpc : cpc;
-    const uint32_t buf_bytes = nslot * 2 * WN * 8;  // int64 delta0 + delta1 rows per slot
-    uint8_t* sflags = dsm + 2 * buf_bytes;         // [P] accept flags of the whole tile (this pass)
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(dsm);
-    const uint32_t sflags_addr = sbase + 2 * buf_bytes;
-    const uint32_t warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
-    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
-        sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
-    if (mode)
-        for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sKappa[j] = swap_kappa(seed, pass_t, j, M);
-    __syncthreads();
-    auto slot_pixels = [&](uint32_t s, uint32_t* out) {
-        if (threadIdx.x < nslot) {
-            const uint32_t j = threadIdx.x;
-            const uint32_t m = j < cpc ? first + j : ((first + j - cpc) ^ sKappa[s]);
-            out[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
-        }
-    };
-    slot_pixels(0, sSlot[0]);
-    __syncthreads();
-    stage_class<R>(sbase, sSlot[0], nslot, T);
-    LaneOffsets<R> off;
-    off.init();
-    cluster_sync_all();  // every CTA's flag copy is initialised before any remote store
-    for (uint32_t s = 0; s < 64; ++s) {
-        // double-buffered staging: class s+1 goes to buffer (s+1)&1, last read in class s-1
-        // (the cluster barrier that ended class s-1 orders those reads before these copies)
-        if (s + 1 < 64) {
-            slot_pixels(s + 1, sSlot[(s + 1) & 1]);
-            __syncwarp();
-            __syncthreads();  // sSlot[(s+1)&1] visible to the staging warps
-            stage_class<R>(sbase + ((s + 1) & 1) * buf_bytes, sSlot[(s + 1) & 1], nslot, T);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncthreads();  // class s's staged rows visible to every warp
-        const uint32_t b = s & 1;
-        const uint32_t j = warp;
-        const uint32_t kappa = mode ? sKappa[s] : 0;
-        const uint32_t m = first + j, mm = m ^ kappa;
-        const uint32_t p = sSlot[b][j], p2 = mode ? sSlot[b][cpc + j] : p;
-        const long long* rows = reinterpret_cast<const long long*>(dsm + b * buf_bytes);
-        WinTermsLocal<R> A, B;
-        A.load_smem(rows + (size_t)j * 2 * WN);
-        if (mode) B.load_smem(rows + (size_t)(cpc + j) * 2 * WN);
-        i128 sum = A.sum_local(sflags, L, p, off, T);
-        if (mode) sum += B.sum_local(sflags, L, p2, off, T);
-        const bool ok = 2 * sum < 0;
-        if (ok && (uint32_t)lane < ncta) st_cluster_u8(sflags_addr + p, lane, 1);  // incl. own copy
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-        if (lane == 0) {  // bookkeeping for commit/stats: not needed by other CTAs in this kernel
-            acc[p] = ok;
-            dEp[p] = (ok && (!mode || m < mm)) ? 2 * sum : (i128)0;
-            if (log) log[(size_t)s * M + m] = ok;
-        }
-        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    }
-}
-
-// Cluster decision kernel v2 (same tiles as k_decide_cluster): no cluster barrier per class.
-// After deciding class s every warp pushes its pixel's accept flag (u32, 0 or 1) into every CTA's
-// flag array with st.async, which also completes 4 bytes of transaction on that CTA's mailbox
-// mbarrier for the class parity; a CTA starts class s+1 once its mailbox has received all M
-// flags of class s.  A CTA can only send class s+1 flags after receiving every flag of class s,
-// i.e. after every warp of the cluster has finished reading the flags for class s, so a flag
-// never changes under a reader.  Each warp stages its own candidates' dE-term rows for the next
-// class with two bulk copies (cp.async.bulk, mbarrier completion), so no warp waits on another.
-// Barrier-free: the cluster-scope release of barrier.cluster.arrive (MEMBAR.ALL.GPU, which also
-// drains the in-flight staging) is off the 64-class critical path.
+// Cluster decision kernels (k_decide_cl3, k_decide_swap, k_decide_big): one 16-CTA cluster decides
+// all 64 classes of a pass with no cluster barrier per class.  After deciding class s every warp
+// pushes its pixel's accept flag (u32, 0 or 1) into every CTA's flag array with st.async, which also
+// completes 4 bytes of transaction on that CTA's mailbox mbarrier for the class parity; a CTA starts
+// class s+1 once its mailbox has received all M flags of class s.  A CTA can only send class s+1
+// flags after receiving every flag of class s, i.e. after every warp of the cluster has finished
+// reading the flags for class s, so a flag never changes under a reader.  The cluster-scope release
+// of barrier.cluster.arrive (MEMBAR.ALL.GPU) is off the 64-class critical path.  (Round-1 variants
+// with a cluster barrier per class or shared-memory-staged rows were measured slower and removed.)
 template <int R>
 struct WinTermsFlags32 : WinTerms<R> {
     // the candidate's delta0 / delta1 rows straight from global memory (read once: no L1 allocation)
@@ -2426,94 +1265,6 @@ __device__ __forceinline__ void st_async_u32(uint32_t local_addr, uint32_t local
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(local_bar), "r"(cta));
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(ra), "r"(v), "r"(rb)
                  : "memory");
-}
-
-template <int R, int mode>
-__global__ void __launch_bounds__(512, 1) k_decide_cl2(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
-                                                       const DTabs T, uint8_t* __restrict__ acc,
-                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log) {
-    constexpr int WN = WinTerms<R>::WN;
-    constexpr uint32_t ROWB = 2 * WN * 8;   // one slot: WN {delta0, delta1} int64 pairs
-    constexpr uint32_t NSW = mode ? 2 : 1;  // slots per warp (SWAP: the candidate and its partner)
-    extern __shared__ __align__(16) uint8_t dsm[];
-    __shared__ uint8_t sDelta[8 * 16];
-    __shared__ uint32_t sKappa[64];
-    __shared__ __align__(8) uint64_t sbar[2 + 2 * 16];  // mailboxes [2], staging [warp][buffer]
-    const uint32_t nb = L / 8, M = nb * nb, P = L * L;
-    const uint32_t ncta = gridDim.x, first = blockIdx.x * cpc;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t buf_bytes = cpc * NSW * ROWB;
-    uint32_t* sflags = reinterpret_cast<uint32_t*>(dsm + 2 * buf_bytes);  // [P]
-    uint32_t* sSlot = sflags + P;                                          // [64][cpc * NSW]
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(dsm);
-    const uint32_t sflags_addr = sbase + 2 * buf_bytes;
-    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
-    auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
-    auto stbar = [&](uint32_t b) { return bar0 + 8 * (2 + 2 * warp + b); };
-    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
-    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
-        sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
-    if (mode)
-        for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sKappa[j] = swap_kappa(seed, pass_t, j, M);
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < 2 + 2 * 16; ++i)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uint32_t per_class = cpc * NSW;
-    for (uint32_t j = threadIdx.x; j < 64 * per_class; j += blockDim.x) {
-        const uint32_t s = j / per_class, i = j - s * per_class;
-        const uint32_t m = i < cpc ? first + i : ((first + i - cpc) ^ sKappa[s]);
-        sSlot[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
-    }
-    __syncthreads();
-    // warp `warp` stages its slot(s) of class s into buffer b (lane 0 issues the bulk copies)
-    auto stage = [&](uint32_t s, uint32_t b) {
-        __syncwarp();  // the warp's reads of buffer b (class s-2) are done
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const uint32_t bar = stbar(b);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(NSW * ROWB)
-                         : "memory");
-#pragma unroll
-            for (uint32_t i = 0; i < NSW; ++i) {
-                const uint32_t pix = sSlot[s * per_class + (i ? cpc : 0) + warp];
-                const uint32_t dst = sbase + b * buf_bytes + (warp * NSW + i) * ROWB;
-                bulk_g2s(dst, T.d + (size_t)pix * WN, 2 * WN * 8, bar);
-            }
-        }
-    };
-    stage(0, 0);
-    LaneOffsets<R> off;
-    off.init();
-    cluster_sync_all();  // every CTA's barriers and flags are initialised before any remote st.async
-    for (uint32_t s = 0; s < 64; ++s) {
-        const uint32_t b = s & 1;
-        if (s + 1 < 64) stage(s + 1, b ^ 1);
-        if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
-        if (threadIdx.x == 0)  // this CTA expects M flags of class s (the phase of class s-2 is complete)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
-                         : "memory");
-        tc::mbar_wait(stbar(b), (s >> 1) & 1);  // this warp's rows of class s
-        const uint32_t m = first + warp, mm = m ^ (mode ? sKappa[s] : 0u);
-        const uint32_t p = sSlot[s * per_class + warp], p2 = mode ? sSlot[s * per_class + cpc + warp] : p;
-        const long long* rows = reinterpret_cast<const long long*>(dsm + b * buf_bytes) + (size_t)warp * NSW * 2 * WN;
-        WinTermsFlags32<R> A, B;
-        A.load_smem(rows);
-        if (mode) B.load_smem(rows + 2 * WN);
-        i128 sum = A.sum_flags(sflags, L, p, off, T);
-        if (mode) sum += B.sum_flags(sflags, L, p2, off, T);
-        const bool ok = 2 * sum < 0;
-        if (lane < ncta) st_async_u32(sflags_addr + 4 * p, mailbox(s), lane, ok ? 1u : 0u);
-        if (lane == 0) {  // bookkeeping for commit/stats
-            acc[p] = ok;
-            dEp[p] = (ok && (!mode || m < mm)) ? 2 * sum : (i128)0;
-            if (log) log[(size_t)s * M + m] = ok;
-        }
-    }
-    tc::mbar_wait(mailbox(63), (63 >> 1) & 1);  // every flag sent to this CTA has landed
-    cluster_sync_all();
 }
 
 // Cluster decision kernel v3: as v2 (st.async flag mailboxes, no cluster barrier) but every warp
@@ -3466,6 +2217,179 @@ __global__ void k_counts_export(const uint8_t* __restrict__ c, uint32_t P, uint3
     const uint32_t lp = blockIdx.x, l = lp / P, p = lp - l * P;
     for (uint32_t i = threadIdx.x; i < Ts; i += blockDim.x)
         out[(size_t)lp * Ts + i] = c[((size_t)p * nl + l) * Tp + i];
+}
+
+// ------------------------------------------------------------- narrow count rows (f3)
+// Per (level, integrand) offsets off[l][i] = round(N_l * I_ref,i) clamped to [0, N_l] (0 for the
+// padding integrands); any integer offset keeps every distance exact, this one makes |delta| small
+// (observed |c - N I_ref| <= 6 at N = 64).
+__global__ void k_narrow_offsets(const double* __restrict__ iref, uint32_t Ts, uint32_t Tp, uint4 lo, uint4 hi,
+                                 uint32_t nl, uint8_t* __restrict__ off) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Tp) return;
+    const uint32_t lv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    for (uint32_t l = 0; l < nl; ++l) {
+        long long o = 0;
+        if (i < Ts) {
+            o = __double2ll_rn((double)lv[l] * iref[i]);
+            o = o < 0 ? 0 : o > (long long)lv[l] ? (long long)lv[l] : o;
+        }
+        off[(size_t)l * Tp + i] = (uint8_t)o;  // N_l <= 128
+    }
+}
+// max over the tile of |c - off| per level -> rng[l] (atomicMax); one warp per pixel row.
+__global__ void __launch_bounds__(256) k_narrow_range(const uint8_t* __restrict__ c, uint32_t P, uint32_t Tp, uint32_t nl,
+                                                      const uint8_t* __restrict__ off, int* __restrict__ rng) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (p >= P) return;
+    for (uint32_t l = 0; l < nl; ++l) {
+        const uint8_t* row = c + ((size_t)p * nl + l) * Tp;
+        const uint8_t* o = off + (size_t)l * Tp;
+        int m = 0;
+        for (uint32_t i = 16 * lane; i < Tp; i += 512) {
+            const uint4 cv = *reinterpret_cast<const uint4*>(row + i);
+            const uint4 ov = *reinterpret_cast<const uint4*>(o + i);
+            const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cv);
+            const uint8_t* ob = reinterpret_cast<const uint8_t*>(&ov);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) m = max(m, abs((int)cb[j] - (int)ob[j]));
+        }
+        m = __reduce_max_sync(0xffffffffu, (unsigned)m);
+        if (lane == 0 && m) atomicMax(rng + l, m);
+    }
+}
+__device__ __forceinline__ uint32_t enc_e2m1(int d) {  // |d| <= 4: 0 1 2 3 4 -> 0x0 0x2 0x4 0x5 0x6
+    const int a = d < 0 ? -d : d;
+    const uint32_t m = a == 0 ? 0x0u : a == 1 ? 0x2u : a == 2 ? 0x4u : a == 3 ? 0x5u : 0x6u;
+    return m | (d < 0 ? 0x8u : 0u);
+}
+__device__ __forceinline__ uint32_t enc_e3m2(int d) {  // |d| <= 8: 1 + mantissa/4 times 2^(e-3)
+    const int a = d < 0 ? -d : d;
+    const uint32_t m = a == 0 ? 0x00u : a == 1 ? 0x0Cu : a < 4 ? 0x10u | (uint32_t)(2 * (a - 2))
+                     : a < 8 ? 0x14u | (uint32_t)(a - 4) : 0x18u;
+    return m | (d < 0 ? 0x20u : 0u);
+}
+__device__ __forceinline__ int dec_e2m1(uint32_t c) {
+    const uint32_t m = c & 7u;
+    const int a = m == 0 ? 0 : m == 2 ? 1 : m == 4 ? 2 : m == 5 ? 3 : 4;
+    return (c & 8u) ? -a : a;
+}
+__device__ __forceinline__ int dec_e3m2(uint32_t c) {
+    const uint32_t e = (c >> 2) & 7u, mt = c & 3u;
+    const int a = e == 0 ? 0 : (int)((4u + mt) << e) >> 5;  // 2^(e-3) (1 + mt/4) for e >= 3
+    return (c & 0x20u) ? -a : a;
+}
+// Row layout of a level: byte offset lb[l] in the row, format fmt[l].  One warp per pixel row;
+// lane j packs the 16-integrand groups j, j + 32, ...: e2m1 16 x 4 bit in 8 bytes, e3m2 16 x 6 bit
+// in 12 bytes (element k at bit bits * k of its group, little-endian), u8 copied; norms |delta|^2
+// (|c|^2 for u8 levels) per level.
+struct NarrowLayout {
+    uint32_t fmt[8], lb[8];
+};
+__global__ void __launch_bounds__(256) k_narrow_pack(const uint8_t* __restrict__ c, uint32_t P, uint32_t Tp, uint32_t nl,
+                                                     const uint8_t* __restrict__ off, NarrowLayout lay, uint32_t rowBn,
+                                                     uint8_t* __restrict__ out, int* __restrict__ norms) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (p >= P) return;
+    for (uint32_t l = 0; l < nl; ++l) {
+        const uint8_t* row = c + ((size_t)p * nl + l) * Tp;
+        const uint8_t* o = off + (size_t)l * Tp;
+        uint8_t* dst = out + (size_t)p * rowBn + lay.lb[l];
+        const uint32_t f = lay.fmt[l];
+        int nrm = 0;
+        for (uint32_t g = lane; g < Tp / 16; g += 32) {
+            const uint4 cv = *reinterpret_cast<const uint4*>(row + 16 * g);
+            const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cv);
+            if (f == BN_FMT_U8) {
+                *reinterpret_cast<uint4*>(dst + 16 * g) = cv;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) nrm += (int)cb[j] * (int)cb[j];
+                continue;
+            }
+            const uint4 ov = *reinterpret_cast<const uint4*>(o + 16 * g);
+            const uint8_t* ob = reinterpret_cast<const uint8_t*>(&ov);
+            if (f == BN_FMT_E2M1) {
+                uint32_t w[2] = {0, 0};
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int d = (int)cb[j] - (int)ob[j];
+                    nrm += d * d;
+                    w[j >> 3] |= enc_e2m1(d) << (4 * (j & 7));
+                }
+                *reinterpret_cast<uint2*>(dst + 8 * g) = make_uint2(w[0], w[1]);
+            } else {
+                unsigned long long lo = 0, hi = 0;  // 96 bits
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int d = (int)cb[j] - (int)ob[j];
+                    nrm += d * d;
+                    const unsigned long long e = enc_e3m2(d);
+                    const int b = 6 * j;  // element j at bits b .. b+5 of the 96-bit group
+                    if (b < 64) {
+                        lo |= e << b;
+                        if (b + 6 > 64) hi |= e >> (64 - b);
+                    } else {
+                        hi |= e << (b - 64);
+                    }
+                }
+                uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + 12 * g);
+                d32[0] = (uint32_t)lo;
+                d32[1] = (uint32_t)(lo >> 32);
+                d32[2] = (uint32_t)hi;
+            }
+        }
+        nrm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nrm);
+        if (lane == 0) norms[(size_t)p * nl + l] = nrm;
+    }
+}
+// Inverse of k_narrow_pack: counts c = delta + off (u8 rows [p][l][Tp]) and their norms |c|^2.
+__global__ void __launch_bounds__(256) k_narrow_unpack(const uint8_t* __restrict__ in, uint32_t P, uint32_t Tp, uint32_t nl,
+                                                       const uint8_t* __restrict__ off, NarrowLayout lay, uint32_t rowBn,
+                                                       uint8_t* __restrict__ c, int* __restrict__ norms) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (p >= P) return;
+    for (uint32_t l = 0; l < nl; ++l) {
+        uint8_t* row = c + ((size_t)p * nl + l) * Tp;
+        const uint8_t* o = off + (size_t)l * Tp;
+        const uint8_t* src = in + (size_t)p * rowBn + lay.lb[l];
+        const uint32_t f = lay.fmt[l];
+        int nrm = 0;
+        for (uint32_t g = lane; g < Tp / 16; g += 32) {
+            uint4 cv;
+            uint8_t* cb = reinterpret_cast<uint8_t*>(&cv);
+            if (f == BN_FMT_U8) {
+                cv = *reinterpret_cast<const uint4*>(src + 16 * g);
+            } else {
+                const uint4 ov = *reinterpret_cast<const uint4*>(o + 16 * g);
+                const uint8_t* ob = reinterpret_cast<const uint8_t*>(&ov);
+                if (f == BN_FMT_E2M1) {
+                    const uint2 w = *reinterpret_cast<const uint2*>(src + 8 * g);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        cb[j] = (uint8_t)(dec_e2m1(((j < 8 ? w.x : w.y) >> (4 * (j & 7))) & 0xFu) + ob[j]);
+                } else {
+                    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src + 12 * g);
+                    const unsigned long long lo = (unsigned long long)s32[0] | ((unsigned long long)s32[1] << 32);
+                    const unsigned long long hi = s32[2];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int b = 6 * j;
+                        unsigned long long e = b < 64 ? lo >> b : hi >> (b - 64);
+                        if (b < 64 && b + 6 > 64) e |= hi << (64 - b);
+                        cb[j] = (uint8_t)(dec_e3m2((uint32_t)e & 0x3Fu) + ob[j]);
+                    }
+                }
+            }
+            *reinterpret_cast<uint4*>(row + 16 * g) = cv;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) nrm += (int)cb[j] * (int)cb[j];
+        }
+        nrm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nrm);
+        if (lane == 0) norms[(size_t)p * nl + l] = nrm;
+    }
 }
 
 // Accept-log scatter is written directly by k_decide.

@@ -108,12 +108,10 @@ def test_c1_shape_full_run(bn, oracle_mod, mode):
     assert st[-1]["E_fixed"] < st[0]["E_fixed"] + (-st[0]["dE_sum"])
 
 
-@pytest.mark.parametrize("gather", ["", "old", "nofuse"])
+@pytest.mark.parametrize("gather", ["", "nofuse"])
 def test_c2_shape_swap(bn, oracle_mod, monkeypatch, gather):
     """C2 shape (SWAP, 4 spp) at 32x32, T=100 (ragged): commit fused with the next pass's partner
-    gather (default), separate partner-map gather + commit (BN_FUSE=0), one-CTA-per-pixel gather
-    (BN_GATHER=old)."""
-    monkeypatch.setenv("BN_GATHER", "old" if gather == "old" else "")
+    gather (default), separate partner-map gather + commit (BN_FUSE=0)."""
     monkeypatch.setenv("BN_FUSE", "0" if gather == "nofuse" else "1")
     s, o, U = make(bn, oracle_mod, 32, 100, (4,))
     _check_run(s, o, U, 6, 1, seed=5)
@@ -225,42 +223,47 @@ def test_concurrent_contexts_match_sequential(bn, oracle_mod):
         assert np.array_equal(a_, b_)
 
 
-# ------------------------------------------------------------------ window-Gram variants
-@pytest.mark.parametrize("L,T,levels", [(16, 64, (16,)), (32, 300, (1, 4, 16, 64)), (64, 512, (4,))])
-def test_gram_variants_bit_identical(bn, oracle_mod, L, T, levels, monkeypatch):
-    """tcgen05 (UMMA/TMEM), IMMA v2, IMMA v1 and dp4a window Grams give identical distances,
-    equal to the plain definition on the oracle's counts."""
+# ------------------------------------------------- window Gram, narrow row formats (f3)
+@pytest.mark.parametrize("narrow", ["auto", "e3m2", "u8", "0"])
+@pytest.mark.parametrize("L,T,levels", [(16, 64, (16,)), (32, 300, (1, 4, 16, 64)), (64, 512, (4,)), (32, 130, (128,))])
+def test_narrow_rows_window_distances(bn, oracle_mod, L, T, levels, narrow, monkeypatch):
+    """The window Gram on every row format -- narrow e2m1 / e3m2 deltas chosen per level from the
+    tile's range (auto), e3m2 forced, the u8 layout through the narrow path, plain u8 rows (0) --
+    gives the plain definition on the oracle's counts, after SWAP passes through the C-ABI equal to
+    the oracle's (counts exported from the packed rows bit-exact)."""
     from tests.test_dist_cpu import _partial_distances
 
-    a, b, px, py = synth.make_bank(T, 31)
-    U = synth.make_tile(L, 32)
-    outs = {}
-    for variant in ("", "tc", "tc2", "tc3", "tc5", "imma2", "imma1", "simt"):
-        monkeypatch.setenv("BN_GRAM", variant)
-        s, o, _ = make(bn, oracle_mod, L, T, levels, bank=(a, b, px, py), U=U)
-        outs[variant] = s.window_distances()
-    co = o.counts(U)
+    monkeypatch.setenv("BN_NARROW", narrow)
+    s, o, U = make(bn, oracle_mod, L, T, levels, tile_seed=32, bank_seed=31)
+    _check_run(s, o, U, 2, 1, seed=13)
+    co = s.eval_counts()
+    D = s.window_distances()
     for li in range(len(levels)):
-        assert np.array_equal(outs[""][li], _partial_distances(co[li], L))
-    for k in ("tc", "tc2", "tc3", "tc5", "imma2", "imma1", "simt"):
-        assert np.array_equal(outs[k], outs[""]), k
+        assert np.array_equal(D[li], _partial_distances(co[li], L))
 
 
-@pytest.mark.parametrize("variant", ["tc", "tc2", "tc3", "tc4", "tc5"])
-def test_tc_gram_optimize_parity(bn, oracle_mod, monkeypatch, variant):
-    """Full passes with the tcgen05 window Grams against the oracle (C3 shape, ragged T)."""
-    monkeypatch.setenv("BN_GRAM", variant)
+@pytest.mark.parametrize("narrow", ["auto", "e3m2", "0"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_narrow_rows_mode_switches(bn, oracle_mod, monkeypatch, narrow, mode):
+    """Mode switches across narrow and u8 rows: SWAP (packs), REDRAW (unpacks), SWAP again,
+    against the oracle pass by pass (C3 shape, ragged T)."""
+    monkeypatch.setenv("BN_NARROW", narrow)
     s, o, U = make(bn, oracle_mod, 32, 130, (1, 4, 16, 64))
-    _check_run(s, o, U, 2, 0, seed=7)
+    st, _ = s.optimize(2, 7, mode=mode, log=True)
+    Uo, co, _, _ = o.optimize(U, mode=mode, passes=2, seed=7)
+    assert np.array_equal(s.get_tile(), Uo)
+    st, lg = s.optimize(2, 7, mode=1 - mode, first_pass=2, log=True)
+    Uo, co, sto, lgo = o.optimize(Uo, co, mode=1 - mode, passes=2, first_pass=2, seed=7, log=True)
+    assert np.array_equal(lg, lgo) and np.array_equal(s.get_tile(), Uo) and np.array_equal(s.eval_counts(), co)
+    assert [x["E_fixed"] for x in st] == [x["E_fixed"] for x in sto]
 
 
-@pytest.mark.parametrize("decide", ["", "cluster2", "cluster1", "flags", "per_class", "swap3"])
+@pytest.mark.parametrize("decide", ["", "flags", "per_class", "swap3"])
 @pytest.mark.parametrize("L,mode", [(16, 0), (16, 1), (32, 1), (64, 1), (128, 0), (128, 1)])
 def test_decide_kernels_parity(bn, oracle_mod, monkeypatch, decide, L, mode):
-    """Every persistent decision kernel (register-prefetched cluster v3 = default, SWAP per-member
-    cluster kernel = default for SWAP, v3 one-warp-per-couple SWAP (swap3), shared-memory-staged v2,
-    cluster v1 with a cluster barrier per class, cooperative flag kernel) against the oracle, both
-    modes, tile sides from 2 to 16 active indices per band."""
+    """Every persistent decision kernel (register-prefetched cluster kernel = REDRAW default, SWAP
+    per-member cluster kernel = SWAP default, one-warp-per-couple SWAP (swap3), cooperative flag
+    kernel, per-class launches) against the oracle, both modes, 2 to 16 active indices per band."""
     monkeypatch.setenv("BN_DECIDE", decide)
     s, o, U = make(bn, oracle_mod, L, 40, (4, 16))
     _check_run(s, o, U, 2, mode, seed=21 + L + mode)
