@@ -27,7 +27,7 @@ SYMBOLS = ("bn_create", "bn_destroy", "bn_last_error", "bn_version", "bn_set_lat
            "bn_optimize", "bn_comm_init", "bn_comm_unique_id", "bn_launch_count", "bn_profile_enable",
            "bn_profile_get", "bn_window_distances", "bn_set_permutation",
            "bn_set_energy_form", "bn_eval_quality", "bn_check")
-KERNELS = ("counts", "gather", "gram", "lut", "decide", "stats", "commit")
+KERNELS = ("counts", "gather", "gram", "lut", "decide", "stats", "commit", "tail")
 
 
 class BNError(RuntimeError):

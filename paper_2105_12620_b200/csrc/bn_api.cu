@@ -188,6 +188,12 @@ struct bn_ctx {
     bool no_big = false;  // BN_DECIDE=nobig: L > 128 tiles use the cooperative flag kernel
     bool no_cluster = false;  // BN_DECIDE=flags: skip the cluster decide kernel
     bool no_fuse = false;          // BN_FUSE=0: separate SWAP commit (k_finish) and gather kernels
+    bool no_tail = false;          // BN_TAIL=0: separate decision and commit kernels (no k_pass_tail)
+    uint32_t nEpart = 0;           // energy partials written by the last Gram / k_lut launch
+
+    bool tail_attr_set[8] = {false};
+    int tail_clusters = -1;        // clusters of the fused pass tail that fit (cached)
+    DevBuf<TailCounters> tailc;
     bool swap_v3 = false;     // BN_DECIDE=swap3: SWAP on k_decide_cl3 (one warp per couple) instead of k_decide_swap
     // narrow count rows: in the SWAP / paper modes, where a pass only
     // permutes rows, the rows are stored as packed deltas c - round(N I_ref) (e2m1 / e3m2 per level,
@@ -406,8 +412,10 @@ int ensure_work(bn_ctx* ctx) {
 template <int R>
 int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn);
 template <int R>
-int launch_lut_only(bn_ctx* ctx, int write_deltas);
+int launch_lut_only(bn_ctx* ctx, int write_deltas, bool exchange = true);
 
+// The Gram and the energy terms of a pass (with a communicator, the exchange of the partial
+// distances in between, inside launch_lut_only).
 template <int R>
 int launch_gram_lut(bn_ctx* ctx, const uint8_t* cn, const int* nn, int write_deltas,
                     const std::function<int()>* after_gram) {
@@ -546,8 +554,8 @@ int ensure_narrow(bn_ctx* ctx) {
 }
 
 template <int R>
-int launch_lut_only(bn_ctx* ctx, int write_deltas) {
-    if (ctx->comm) {
+int launch_lut_only(bn_ctx* ctx, int write_deltas, bool exchange) {
+    if (ctx->comm && exchange) {
         const size_t n = (size_t)ctx->P * half_count_padded(R) * ctx->nl * 4;
         int r = g_nccl.allreduce(ctx->Dt.p, ctx->Dt.p, n, NCCL_INT32, NCCL_SUM, ctx->comm, ctx->ls);
         if (r) return fail(ctx, BN_ENCCL, "ncclAllReduce: %s", g_nccl.errstr(r));
@@ -558,6 +566,7 @@ int launch_lut_only(bn_ctx* ctx, int write_deltas) {
         la.Dmax[l] = l < ctx->nl ? ctx->Dmax[l] : 0;
     }
     const size_t nthr = (size_t)ctx->P * half_count_padded(R);
+    ctx->nEpart = (uint32_t)((nthr + 255) / 256);
     KSTART(BN_K_LUT);
     {
         auto fn = ctx->nl == 4 ? k_lut<R, 4> : ctx->nl == 1 ? k_lut<R, 1> : k_lut<R, 0>;
@@ -810,6 +819,99 @@ int paper_decide(bn_ctx* ctx, uint32_t t, uint64_t seed, uint32_t ncp, uint8_t* 
     }
 }
 
+// Fused pass tail (k_pass_tail, SWAP, L <= 128): one cooperative launch of clusters of `ncta` CTAs,
+// cluster 0 deciding, the others committing (and gathering the next pass's candidates) behind it.
+// Returns BN_OK with *done = false when the configuration does not fit (separate kernels then).
+template <int R>
+int launch_pass_tail(bn_ctx* ctx, uint32_t t, uint64_t seed, uint8_t* log, uint32_t rb, const uint2* Un,
+                     const uint8_t* cn, const int* nn, uint2* Un2, uint8_t* cn2, int* nn2, int gather_next,
+                     PassStatsDev* out, int check_prev, bool* done) {
+    *done = false;
+    const uint32_t nb = ctx->L / 8, M = nb * nb, P = ctx->P;
+    if (ctx->no_tail || nb > 16) return BN_OK;
+    uint32_t cpc = 16;
+    while (cpc > M) cpc /= 2;
+    const uint32_t ncta = M / cpc;
+    const size_t smem = 4 * (size_t)P + (size_t)64 * cpc * 6;
+    if (!ctx->tail_attr_set[R]) {
+        CUDA_TRY(cudaFuncSetAttribute(k_pass_tail<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(k_pass_tail<R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        ctx->tail_attr_set[R] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(32 * (cpc + 1));  // + the publisher warp of the deciding CTAs
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->ls;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ncta;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (ctx->tail_clusters < 0) {
+        cfg.gridDim = dim3(ncta);
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_pass_tail<R>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            ncl = 0;
+        }
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
+        const int cap = nsm / (int)ncta;  // one CTA per SM at most
+        ctx->tail_clusters = ncl < cap ? ncl : cap;
+    }
+    if (ctx->tail_clusters < 2) return BN_OK;
+    const uint32_t ncl = (uint32_t)ctx->tail_clusters, nh = (ncl - 1) * ncta;
+    cfg.gridDim = dim3(ncl * ncta);
+    if (!ctx->tailc.p) {
+        CUDA_TRY(ctx->tailc.ensure(1));
+        CUDA_TRY(cudaMemsetAsync(ctx->tailc.p, 0, sizeof(TailCounters), ctx->stream));
+    }
+    CUDA_TRY(ctx->fparts.ensure(nh));
+    uint32_t L = ctx->L, nl = ctx->nl;
+    uint32_t nE = ctx->nEpart;
+    longlong2* dterms = ctx->d0.p;
+    uint8_t* acc = ctx->acc.p;
+    i128* dEp = ctx->dEp.p;
+    const u128* Epart = ctx->Epart.p;
+    int* err = ctx->derr.p;
+    uint2* U = ctx->U.p;
+    uint8_t* c = ctx->c.p;
+    int* nc = ctx->nc.p;
+    FinishPart* parts = ctx->fparts.p;
+    TailCounters* tc = ctx->tailc.p;
+    void* args[] = {&t, &seed, &L, &cpc, &dterms, &acc, &dEp, &log, (void*)&Epart, &nE, &nl, &err, &rb,
+                    (void*)&Un, &U, (void*)&cn, &c, (void*)&nn, &nc, &Un2, &cn2, &nn2, &gather_next, &parts, &out,
+                    &check_prev, &tc};
+    KSTART(BN_K_TAIL);
+    cudaError_t e = cudaLaunchKernelExC(&cfg, (const void*)k_pass_tail<R>, args);
+    if (e != cudaSuccess) {
+        if (ctx->prof) ctx->prof_marks.pop_back();
+        cudaGetLastError();
+        ctx->tail_clusters = 0;  // does not fit: separate kernels from now on
+        return BN_OK;
+    }
+    LAUNCHED_K();
+    *done = true;
+    return BN_OK;
+}
+int pass_tail(bn_ctx* ctx, uint32_t t, uint64_t seed, uint8_t* log, uint32_t rb, const uint2* Un, const uint8_t* cn,
+              const int* nn, uint2* Un2, uint8_t* cn2, int* nn2, int gather_next, PassStatsDev* out, int check_prev,
+              bool* done) {
+    switch (ctx->R) {
+        case 1: return launch_pass_tail<1>(ctx, t, seed, log, rb, Un, cn, nn, Un2, cn2, nn2, gather_next, out, check_prev, done);
+        case 2: return launch_pass_tail<2>(ctx, t, seed, log, rb, Un, cn, nn, Un2, cn2, nn2, gather_next, out, check_prev, done);
+        case 3: return launch_pass_tail<3>(ctx, t, seed, log, rb, Un, cn, nn, Un2, cn2, nn2, gather_next, out, check_prev, done);
+        case 4: return launch_pass_tail<4>(ctx, t, seed, log, rb, Un, cn, nn, Un2, cn2, nn2, gather_next, out, check_prev, done);
+        case 5: return launch_pass_tail<5>(ctx, t, seed, log, rb, Un, cn, nn, Un2, cn2, nn2, gather_next, out, check_prev, done);
+        case 6: return launch_pass_tail<6>(ctx, t, seed, log, rb, Un, cn, nn, Un2, cn2, nn2, gather_next, out, check_prev, done);
+        default: return launch_pass_tail<7>(ctx, t, seed, log, rb, Un, cn, nn, Un2, cn2, nn2, gather_next, out, check_prev, done);
+    }
+}
+
 // The device error flag accumulates every invariant failure of every launch since it was last
 // read (bits: 1 window distance outside [0, T N^2], 2 dE term outside +-2^55, 4 a pass's
 // recomputed start energy != the previous pass's E + sum dE); reading it clears it.
@@ -862,8 +964,7 @@ int optimize_best_of_k(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* sta
     ctx->ls = ctx->stream;
     // exact energy of the starting tile (slot `passes`), then E_after = E_before + sum dE per pass
     if ((rc = gram_lut(ctx, ctx->c.p, ctx->nc.p, 0))) return rc;
-    const uint32_t nE = (uint32_t)(((size_t)P * half_count_padded(ctx->R) + 255) / 256);
-    k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, nullptr, nullptr, P, 0, ctx->pstats.p + prm->passes);
+    k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, ctx->nEpart, nullptr, nullptr, P, 0, ctx->pstats.p + prm->passes);
     LAUNCHED();
     LutArgs la;
     for (uint32_t l = 0; l < 8; ++l) {
@@ -949,6 +1050,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->no_cluster = dm && !strcmp(dm, "flags");
     ctx->swap_v3 = dm && !strcmp(dm, "swap3");
     ctx->no_big = dm && !strcmp(dm, "nobig");
+    const char* tl = getenv("BN_TAIL");
+    ctx->no_tail = tl && !strcmp(tl, "0");
     const char* fu = getenv("BN_FUSE");
     ctx->no_fuse = fu && !strcmp(fu, "0");
     const char* nw = getenv("BN_NARROW");
@@ -997,7 +1100,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->ev_out.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release(); ctx->rows_done.release();
-        ctx->noff.release(); ctx->nrng.release();
+        ctx->noff.release(); ctx->nrng.release(); ctx->tailc.release();
         if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
         if (ctx->hp) cudaStreamSynchronize(ctx->hp), cudaStreamDestroy(ctx->hp);
         for (cudaEvent_t e : {ctx->evA, ctx->evB, ctx->evC})
@@ -1180,8 +1283,7 @@ int bn_energy(bn_ctx* ctx, double* E, uint64_t E_fixed[2]) {
     if (rc) return rc;
     CUDA_TRY(ctx->pstats.ensure(1));
     if ((rc = gram_lut(ctx, ctx->c.p, ctx->nc.p, 0))) return rc;
-    const uint32_t nE = (uint32_t)(((size_t)ctx->P * half_count_padded(ctx->R) + 255) / 256);
-    k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, nullptr, nullptr, ctx->P, 0, ctx->pstats.p);
+    k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, ctx->nEpart, nullptr, nullptr, ctx->P, 0, ctx->pstats.p);
     LAUNCHED();
     PassStatsDev h;
     CUDA_TRY(cudaMemcpyAsync(&h, ctx->pstats.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1211,7 +1313,6 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     const uint32_t rb = row_bytes(ctx);
     const uint32_t P = ctx->P, M = (ctx->L / 8) * (ctx->L / 8), nl = ctx->nl;
     const int R = ctx->R;
-    const uint32_t nE = (uint32_t)(((size_t)P * half_count_padded(R) + 255) / 256);
     const bool paper = prm->mode == BN_PAPER_SWAP;
     const uint32_t budget = paper ? (prm->budget ? prm->budget : P / 4) : 0, ncp = budget / 2;
     if (paper) {
@@ -1344,6 +1445,19 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             if (rowflags && pi > 0) CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evC, 0));
             return BN_OK;
         };
+        if (prm->mode == BN_SWAP && !ctx->no_tail && ctx->tail_clusters != 0 && ctx->L <= 128) {
+            // fused pass tail: Gram (+ exchange), then dE terms, decisions and commit in one launch
+            uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
+            const bool nxt = fuse && pi + 1 < prm->passes;
+            if ((rc = gram_lut(ctx, buf_c(pi), buf_n(pi), 1))) return rc;
+            bool done = false;
+            if ((rc = pass_tail(ctx, t, prm->seed, log, rb, buf_U(pi), buf_c(pi), buf_n(pi), nxt ? buf_U(pi + 1) : nullptr,
+                                nxt ? buf_c(pi + 1) : nullptr, nxt ? buf_n(pi + 1) : nullptr, (int)nxt,
+                                ctx->pstats.p + pi, (int)(pi > 0), &done)))
+                return rc;
+            if (done) continue;
+            goto decisions;  // the tail does not fit this device: the separate kernels
+        }
         if (pf && ctx->prefetch_at == 0 && (rc = prefetch())) return rc;
         ctx->gram_rows = rowflags ? ctx->rows_done.p : nullptr;
         ctx->gram_rows_target = rows_target[pi & 1];
@@ -1351,6 +1465,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         ctx->gram_rows = nullptr;
         if (rc) return rc;
         if (pf && ctx->prefetch_at == 2 && (rc = prefetch())) return rc;
+    decisions:
         uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
         bool done = false;
         if (paper) {
@@ -1367,7 +1482,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             KSTART(BN_K_COMMIT);
             CUDA_TRY(launch_k(ctx, k_finish_gather, dim3(nfin_g), dim3(BN_FG_THREADS), 0, cs, ctx->acc.p, P, rb, nl,
                               (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
-                              ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, ctx->fparts.p,
+                              ctx->nc.p, (const u128*)ctx->Epart.p, ctx->nEpart, (const i128*)ctx->dEp.p, ctx->fparts.p,
                               ctx->ticket.p, ctx->pstats.p + pi, (const uint32_t*)nullptr, buf_U(pi + 1),
                               buf_c(pi + 1), buf_n(pi + 1), ctx->L, prm->seed, t + 1,
                               paper ? (const uint32_t*)ctx->perm.p : (const uint32_t*)nullptr,
@@ -1379,7 +1494,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         KSTART(BN_K_COMMIT);
         CUDA_TRY(launch_k(ctx, k_finish, dim3(nfin), dim3(256), 0, cs, (const uint8_t*)ctx->acc.p, P, rb, nl,
                           (const uint2*)buf_U(pi), ctx->U.p, (const uint8_t*)buf_c(pi), ctx->c.p, (const int*)buf_n(pi),
-                          ctx->nc.p, (const u128*)ctx->Epart.p, nE, (const i128*)ctx->dEp.p, (int)(prm->mode != BN_REDRAW),
+                          ctx->nc.p, (const u128*)ctx->Epart.p, ctx->nEpart, (const i128*)ctx->dEp.p, (int)(prm->mode != BN_REDRAW),
                           ctx->fparts.p, ctx->ticket.p, ctx->pstats.p + pi, (int)paper, (int)(!paper && pi > 0),
                           ctx->derr.p));
         LAUNCHED_K();
@@ -1393,7 +1508,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
         // the paper's concurrent swaps do not add up (E may rise): the energy after pass pi is the
         // pass-start energy of pass pi + 1, and after the last pass one more energy evaluation
         if ((rc = gram_lut(ctx, ctx->c.p, ctx->nc.p, 0))) return rc;
-        k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, nE, nullptr, nullptr, P, 0,
+        k_pass_stats<<<1, 1024, 0, ctx->stream>>>(ctx->Epart.p, ctx->nEpart, nullptr, nullptr, P, 0,
                                                   ctx->pstats.p + prm->passes);
         LAUNCHED();
     }

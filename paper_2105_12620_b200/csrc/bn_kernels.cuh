@@ -534,6 +534,165 @@ __device__ __forceinline__ void st_v8(int2* dst, const int* x, const int* y) {
                  : "memory");
 }
 
+// -------------------------------------------------------------------------- energy terms
+// q(o, D) = rn_u64(2^52 * W[o] * G_l[D]); W and G are host-built fp64 tables (exp/sqrt of the
+// host libm), the product is one IEEE multiply (no contraction possible), the scaling by 2^52
+// is exact (reading R15).  With q < 2^52, every dE term (a sum over <= 8 levels of differences of
+// two q's) satisfies |term| < 2^55, and every window sum of <= 224 terms |sum| < 2^63: int64 is
+// exact throughout the decisions.
+constexpr int BN_FIX_BITS = 52;  // E = E_fixed * 2^-52
+__device__ __forceinline__ unsigned long long qterm(double w, const double* __restrict__ G, int D) {
+    return __double2ull_rn(__dmul_rn(__dmul_rn(w, __ldg(G + D)), 4503599627370496.0));
+}
+
+// dE terms are int64 (exact, see above).  The int128 escape machinery of earlier versions (a
+// sentinel plus a side table for terms beyond int64) is unreachable with the 2^52 scale; the
+// invariant |term| < 2^55 is checked here (err flag 2).
+constexpr long long DT_ESC = (long long)0x8000000000000000ull;
+constexpr long long TERM_MAX = 1ll << 55;
+__device__ __forceinline__ void put_terms(longlong2* d, size_t idx, long long v0, long long v1, int* err) {
+    if (v0 >= TERM_MAX || v0 <= -TERM_MAX || v1 >= TERM_MAX || v1 <= -TERM_MAX) atomicOr(err, 2);
+    d[idx] = make_longlong2(v0, v1);
+}
+__device__ __forceinline__ i128 get_term(long long v, const longlong2* __restrict__ x, size_t idx) {
+    if (v != DT_ESC) return (i128)v;
+    const longlong2 e = x[idx];
+    return ((i128)e.y << 64) | (u128)(unsigned long long)e.x;
+}
+struct DTabs {
+    const longlong2* d;  // {delta0, delta1} interleaved per (pixel, offset): one 16-B access per term
+    const longlong2* x0;
+    const longlong2* x1;
+};
+
+// Exact warp sum of an int128 (two's complement, mod 2^128) with 8 REDUX.SUM instructions:
+// split into 16-bit limbs (each warp sum < 2^21 fits 32 bits), then recombine with carries.
+__device__ __forceinline__ i128 warp_sum_i128_redux(unsigned long long lo, unsigned long long hi) {
+    uint32_t s[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[i] = __reduce_add_sync(0xffffffffu, (uint32_t)(lo >> (16 * i)) & 0xffffu);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[4 + i] = __reduce_add_sync(0xffffffffu, (uint32_t)(hi >> (16 * i)) & 0xffffu);
+    u128 r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += (u128)s[i] << (16 * i);
+    return (i128)r;
+}
+
+// Exact warp sum of a u128 (or an int128 mod 2^128) by a 5-step shuffle butterfly.
+__device__ __forceinline__ u128 warp_sum_u128(u128 v) {
+    unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
+        const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+        const unsigned long long nlo = lo + olo;
+        hi += ohi + (nlo < lo);
+        lo = nlo;
+    }
+    return ((u128)hi << 64) | lo;
+}
+
+// Exact warp sum of int64 partials whose total fits int64: four independent REDUX.SUM over 16-bit
+// limbs of the two's-complement value (each limb sum < 2^21), recombined mod 2^64.
+#ifndef BN_I64_REDUX
+#define BN_I64_REDUX 1  // 0: 5-step shuffle butterfly (C3 decide 0.073 vs 0.070 ms, C2 0.068 vs 0.058)
+#endif
+__device__ __forceinline__ long long warp_sum_i64(long long v) {
+    if (BN_I64_REDUX) {
+        const unsigned long long u = (unsigned long long)v;
+        unsigned long long r = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            r += (unsigned long long)__reduce_add_sync(0xffffffffu, (uint32_t)(u >> (16 * i)) & 0xffffu) << (16 * i);
+        return (long long)r;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+struct LutArgs {
+    const double* G[8];  // per-level G tables
+    int Dmax[8];         // largest legal D per level (guards corrupted distances)
+};
+
+// NL > 0: compile-time level count (all distance loads issued up front); NL = 0: runtime nl.
+template <int R, int NL>
+__global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32_t L, uint32_t nl_rt,
+                                             const double* __restrict__ W, LutArgs lut, int write_deltas,
+                                             longlong2* __restrict__ d, u128* __restrict__ Epart, int* __restrict__ err) {
+    constexpr int HP = half_count_padded(R), R0 = ru4(R), RW = ru4(2 * R + 1);
+    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
+    const uint32_t P = L * L;
+#ifndef BN_LUT_REVERSE
+#define BN_LUT_REVERSE 1
+#endif
+    // (p, padded offset hp); BN_LUT_REVERSE: last-written window distances first (still in L2)
+    const size_t idx = BN_LUT_REVERSE ? (size_t)(gridDim.x - 1 - blockIdx.x) * blockDim.x + threadIdx.x
+                                      : (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long e = 0;  // < 2 * 8 * 2^52 = 2^56 per thread, < 2^61 per warp
+    const uint32_t p = (uint32_t)(idx / HP), hp = (uint32_t)(idx - (size_t)p * HP);
+    int ox, oy;
+    if (hp < (uint32_t)R0) {
+        oy = 0;
+        ox = (int)hp + 1;
+    } else {
+        oy = 1 + (int)(hp - R0) / RW;
+        ox = (int)(hp - R0) % RW - R;
+    }
+    if (idx < (size_t)P * HP && ox <= R) {  // pads (ox > R) are skipped
+        const uint32_t x = p % L, y = p / L;
+        const uint32_t q = ((y + oy) & (L - 1)) * L + ((x + ox + L) & (L - 1));
+        const int wi = win_index(ox, oy, R), wm = win_index(-ox, -oy, R);
+        const double w = W[wi];
+        // q < 2^52: per-level differences and their sums over <= 8 levels are exact in int64 (R15)
+        long long a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+        const uint32_t nl = NL ? NL : nl_rt;
+        int4 Dv[NL ? NL : 1];
+        if (NL) {
+#pragma unroll
+            for (int l = 0; l < (NL ? NL : 1); ++l) Dv[l] = dt_get(Dt, (size_t)nl * P * HP, (size_t)l * P * HP + idx);
+        }
+#pragma unroll
+        for (uint32_t l = 0; l < nl; ++l) {
+            const int4 D = NL ? Dv[NL ? l : 0] : dt_get(Dt, (size_t)nl * P * HP, (size_t)l * P * HP + idx);
+            const int dm = lut.Dmax[l];
+            if ((unsigned)D.x > (unsigned)dm || (unsigned)D.y > (unsigned)dm || (unsigned)D.z > (unsigned)dm ||
+                (unsigned)D.w > (unsigned)dm) {
+                atomicOr(err, 1);
+                continue;
+            }
+            const double* G = lut.G[l];
+            const long long qcc = (long long)qterm(w, G, D.x), qcn = (long long)qterm(w, G, D.y);
+            const long long qnc = (long long)qterm(w, G, D.z), qnn = (long long)qterm(w, G, D.w);
+            e += (unsigned long long)qcc;
+            a0 += qnc - qcc;  // p takes cn_p, q still c_q
+            a1 += qnn - qcn;  // p takes cn_p, q already cn_q
+            b0 += qcn - qcc;  // q takes cn_q, p still c_p
+            b1 += qnn - qnc;  // q takes cn_q, p already cn_p
+        }
+        e *= 2;  // ordered pairs (p,q) and (q,p)
+        if (write_deltas) {
+            put_terms(d, (size_t)p * WN + wi, a0, a1, err);
+            put_terms(d, (size_t)q * WN + wm, b0, b1, err);
+        }
+    }
+    // block reduction of e: exact warp sums of 16-bit limbs (REDUX), then the 8 warp partials
+    __shared__ unsigned long long swarp[8];
+    unsigned long long ws = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        ws += (unsigned long long)__reduce_add_sync(0xffffffffu, (uint32_t)(e >> (16 * i)) & 0xffffu) << (16 * i);
+    if ((threadIdx.x & 31) == 0) swarp[threadIdx.x >> 5] = ws;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u128 t = 0;
+        for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += swarp[j];
+        Epart[blockIdx.x] = t;
+    }
+}
+
 // Row formats of a level's count rows (SURVEY §8 f3 narrow storage).  BN_FMT_U8:
 // the counts c (uint8, kind::i8, exact s32 accumulation).  BN_FMT_E2M1 / BN_FMT_E3M2: the deltas
 // delta = c - off_i (off_i = round(N_l I_ref,i), one integer per integrand and level) packed 16 per
@@ -793,165 +952,6 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-    }
-}
-
-// -------------------------------------------------------------------------- energy terms
-// q(o, D) = rn_u64(2^52 * W[o] * G_l[D]); W and G are host-built fp64 tables (exp/sqrt of the
-// host libm), the product is one IEEE multiply (no contraction possible), the scaling by 2^52
-// is exact (reading R15).  With q < 2^52, every dE term (a sum over <= 8 levels of differences of
-// two q's) satisfies |term| < 2^55, and every window sum of <= 224 terms |sum| < 2^63: int64 is
-// exact throughout the decisions.
-constexpr int BN_FIX_BITS = 52;  // E = E_fixed * 2^-52
-__device__ __forceinline__ unsigned long long qterm(double w, const double* __restrict__ G, int D) {
-    return __double2ull_rn(__dmul_rn(__dmul_rn(w, __ldg(G + D)), 4503599627370496.0));
-}
-
-// dE terms are int64 (exact, see above).  The int128 escape machinery of earlier versions (a
-// sentinel plus a side table for terms beyond int64) is unreachable with the 2^52 scale; the
-// invariant |term| < 2^55 is checked here (err flag 2).
-constexpr long long DT_ESC = (long long)0x8000000000000000ull;
-constexpr long long TERM_MAX = 1ll << 55;
-__device__ __forceinline__ void put_terms(longlong2* d, size_t idx, long long v0, long long v1, int* err) {
-    if (v0 >= TERM_MAX || v0 <= -TERM_MAX || v1 >= TERM_MAX || v1 <= -TERM_MAX) atomicOr(err, 2);
-    d[idx] = make_longlong2(v0, v1);
-}
-__device__ __forceinline__ i128 get_term(long long v, const longlong2* __restrict__ x, size_t idx) {
-    if (v != DT_ESC) return (i128)v;
-    const longlong2 e = x[idx];
-    return ((i128)e.y << 64) | (u128)(unsigned long long)e.x;
-}
-struct DTabs {
-    const longlong2* d;  // {delta0, delta1} interleaved per (pixel, offset): one 16-B access per term
-    const longlong2* x0;
-    const longlong2* x1;
-};
-
-// Exact warp sum of an int128 (two's complement, mod 2^128) with 8 REDUX.SUM instructions:
-// split into 16-bit limbs (each warp sum < 2^21 fits 32 bits), then recombine with carries.
-__device__ __forceinline__ i128 warp_sum_i128_redux(unsigned long long lo, unsigned long long hi) {
-    uint32_t s[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s[i] = __reduce_add_sync(0xffffffffu, (uint32_t)(lo >> (16 * i)) & 0xffffu);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s[4 + i] = __reduce_add_sync(0xffffffffu, (uint32_t)(hi >> (16 * i)) & 0xffffu);
-    u128 r = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r += (u128)s[i] << (16 * i);
-    return (i128)r;
-}
-
-// Exact warp sum of a u128 (or an int128 mod 2^128) by a 5-step shuffle butterfly.
-__device__ __forceinline__ u128 warp_sum_u128(u128 v) {
-    unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
-        const unsigned long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
-        const unsigned long long nlo = lo + olo;
-        hi += ohi + (nlo < lo);
-        lo = nlo;
-    }
-    return ((u128)hi << 64) | lo;
-}
-
-// Exact warp sum of int64 partials whose total fits int64: four independent REDUX.SUM over 16-bit
-// limbs of the two's-complement value (each limb sum < 2^21), recombined mod 2^64.
-#ifndef BN_I64_REDUX
-#define BN_I64_REDUX 1  // 0: 5-step shuffle butterfly (C3 decide 0.073 vs 0.070 ms, C2 0.068 vs 0.058)
-#endif
-__device__ __forceinline__ long long warp_sum_i64(long long v) {
-    if (BN_I64_REDUX) {
-        const unsigned long long u = (unsigned long long)v;
-        unsigned long long r = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            r += (unsigned long long)__reduce_add_sync(0xffffffffu, (uint32_t)(u >> (16 * i)) & 0xffffu) << (16 * i);
-        return (long long)r;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-struct LutArgs {
-    const double* G[8];  // per-level G tables
-    int Dmax[8];         // largest legal D per level (guards corrupted distances)
-};
-
-// NL > 0: compile-time level count (all distance loads issued up front); NL = 0: runtime nl.
-template <int R, int NL>
-__global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32_t L, uint32_t nl_rt,
-                                             const double* __restrict__ W, LutArgs lut, int write_deltas,
-                                             longlong2* __restrict__ d, u128* __restrict__ Epart, int* __restrict__ err) {
-    constexpr int HP = half_count_padded(R), R0 = ru4(R), RW = ru4(2 * R + 1);
-    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
-    const uint32_t P = L * L;
-#ifndef BN_LUT_REVERSE
-#define BN_LUT_REVERSE 1
-#endif
-    // (p, padded offset hp); BN_LUT_REVERSE: last-written window distances first (still in L2)
-    const size_t idx = BN_LUT_REVERSE ? (size_t)(gridDim.x - 1 - blockIdx.x) * blockDim.x + threadIdx.x
-                                      : (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long e = 0;  // < 2 * 8 * 2^52 = 2^56 per thread, < 2^61 per warp
-    const uint32_t p = (uint32_t)(idx / HP), hp = (uint32_t)(idx - (size_t)p * HP);
-    int ox, oy;
-    if (hp < (uint32_t)R0) {
-        oy = 0;
-        ox = (int)hp + 1;
-    } else {
-        oy = 1 + (int)(hp - R0) / RW;
-        ox = (int)(hp - R0) % RW - R;
-    }
-    if (idx < (size_t)P * HP && ox <= R) {  // pads (ox > R) are skipped
-        const uint32_t x = p % L, y = p / L;
-        const uint32_t q = ((y + oy) & (L - 1)) * L + ((x + ox + L) & (L - 1));
-        const int wi = win_index(ox, oy, R), wm = win_index(-ox, -oy, R);
-        const double w = W[wi];
-        // q < 2^52: per-level differences and their sums over <= 8 levels are exact in int64 (R15)
-        long long a0 = 0, a1 = 0, b0 = 0, b1 = 0;
-        const uint32_t nl = NL ? NL : nl_rt;
-        int4 Dv[NL ? NL : 1];
-        if (NL) {
-#pragma unroll
-            for (int l = 0; l < (NL ? NL : 1); ++l) Dv[l] = dt_get(Dt, (size_t)nl * P * HP, (size_t)l * P * HP + idx);
-        }
-#pragma unroll
-        for (uint32_t l = 0; l < nl; ++l) {
-            const int4 D = NL ? Dv[NL ? l : 0] : dt_get(Dt, (size_t)nl * P * HP, (size_t)l * P * HP + idx);
-            const int dm = lut.Dmax[l];
-            if ((unsigned)D.x > (unsigned)dm || (unsigned)D.y > (unsigned)dm || (unsigned)D.z > (unsigned)dm ||
-                (unsigned)D.w > (unsigned)dm) {
-                atomicOr(err, 1);
-                continue;
-            }
-            const double* G = lut.G[l];
-            const long long qcc = (long long)qterm(w, G, D.x), qcn = (long long)qterm(w, G, D.y);
-            const long long qnc = (long long)qterm(w, G, D.z), qnn = (long long)qterm(w, G, D.w);
-            e += (unsigned long long)qcc;
-            a0 += qnc - qcc;  // p takes cn_p, q still c_q
-            a1 += qnn - qcn;  // p takes cn_p, q already cn_q
-            b0 += qcn - qcc;  // q takes cn_q, p still c_p
-            b1 += qnn - qnc;  // q takes cn_q, p already cn_p
-        }
-        e *= 2;  // ordered pairs (p,q) and (q,p)
-        if (write_deltas) {
-            put_terms(d, (size_t)p * WN + wi, a0, a1, err);
-            put_terms(d, (size_t)q * WN + wm, b0, b1, err);
-        }
-    }
-    // block reduction of e: exact warp sums of 16-bit limbs (REDUX), then the 8 warp partials
-    __shared__ unsigned long long swarp[8];
-    unsigned long long ws = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-        ws += (unsigned long long)__reduce_add_sync(0xffffffffu, (uint32_t)(e >> (16 * i)) & 0xffffu) << (16 * i);
-    if ((threadIdx.x & 31) == 0) swarp[threadIdx.x >> 5] = ws;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        u128 t = 0;
-        for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += swarp[j];
-        Epart[blockIdx.x] = t;
     }
 }
 
@@ -1235,6 +1235,20 @@ struct WinTermsFlags32 : WinTerms<R> {
                              : "l"(r + w));
         }
     }
+    // the same rows while other CTAs of the running kernel may still be writing other rows of the
+    // table (k_pass_tail): L2-coherent loads, ordered after the producer's release by an acquire
+    __device__ __forceinline__ void load_global_cg(const DTabs T, uint32_t pix) {
+        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
+        const int lane = threadIdx.x & 31;
+        const longlong2* r = T.d + (size_t)pix * WN;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int w = lane + 32 * j;
+            if (w < WN)
+                asm volatile("ld.global.cg.v2.b64 {%0, %1}, [%2];" : "=l"(this->v0[j]), "=l"(this->v1[j]) : "l"(r + w)
+                             : "memory");
+        }
+    }
     // exact int64 window sum (|term| < 2^55, <= 224 terms: |sum| < 2^63), warp-reduced in int64
     __device__ __forceinline__ i128 sum_flags(const uint32_t* sflags, uint32_t L, uint32_t p,
                                               const LaneOffsets<R>& off, const DTabs T) const {
@@ -1351,16 +1365,42 @@ __device__ __forceinline__ uint32_t couple_member(uint32_t c, uint32_t kappa, ui
     const uint32_t m = ((c >> h) << (h + 1)) | (c & ((1u << h) - 1u));
     return upper ? m ^ kappa : m;
 }
+// Progress counters of the fused pass tail (k_pass_tail): lut[s] counts the finished dE-term units
+// of class s, dec[s] the decided members of class s; reset by the kernel's last CTA.
+struct TailCounters {
+    unsigned int lut[64], dec[64];
+    unsigned int lut_next, com_next, ticket, pad;
+};
+__device__ __forceinline__ void wait_count(const unsigned int* c, unsigned int target) {
+    for (uint32_t n = 0;; ++n) {
+        unsigned int v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+        if (v >= target) break;
+        if (n > (1u << 28)) __trap();  // never hang the GPU on a protocol bug
+        if (n > 8) __nanosleep(32);
+    }
+}
+__device__ __forceinline__ void red_release_add(unsigned int* c, unsigned int v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(c), "r"(v) : "memory");
+}
+
+// Body of k_decide_swap.  With `tc` (the fused pass tail) the CTA has one extra warp, the publisher:
+// the deciding warps count their class-s members in shared memory (release, CTA scope) after
+// writing acc / dEp, and the publisher, once all of the CTA's members of class s are counted, makes
+// them visible at GPU scope (fence) and adds them to tc->dec[s] -- so no deciding warp ever waits on
+// a GPU-scope fence (which would also drain its in-flight row prefetch).  With upc > 0 the rows of
+// class s are only loaded once tc->lut[s] reaches upc.
 template <int R>
-__global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
-                                                        const DTabs T, uint8_t* __restrict__ acc,
-                                                        i128* __restrict__ dEp, uint8_t* __restrict__ log) {
-    extern __shared__ __align__(16) uint8_t dsm[];
+__device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
+                                                 const DTabs T, uint8_t* __restrict__ acc, i128* __restrict__ dEp,
+                                                 uint8_t* __restrict__ log, TailCounters* tc, uint32_t upc) {
     __shared__ uint8_t sDelta[8 * 16];
     __shared__ __align__(8) uint64_t sbar[2];
     __shared__ __align__(16) unsigned long long sPart[16][2];
+    __shared__ unsigned int sDecCnt[64];
     const uint32_t nb = L / 8, M = nb * nb, P = L * L;
-    const uint32_t ncta = gridDim.x, first = blockIdx.x * cpc;  // first slot of this CTA
+    const uint32_t ncta = cpc ? (M / cpc) : 0, first = (blockIdx.x % ncta) * cpc;  // first slot of this CTA
+    const uint32_t cta = blockIdx.x % ncta;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* sflags = reinterpret_cast<uint32_t*>(dsm);        // [P]
     uint32_t* sSlot = sflags + P;                                // [64][cpc] pixels
@@ -1371,6 +1411,7 @@ __global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_
     for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
     for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
         sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
+    for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sDecCnt[j] = 0;
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1383,14 +1424,41 @@ __global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_
         sIdx[j] = (uint16_t)m;
     }
     __syncthreads();
+    if (tc && warp == cpc) {  // the publisher warp (fused pass tail)
+        cluster_sync_all();
+        if (lane == 0) {
+            const uint32_t cnt_addr = (uint32_t)__cvta_generic_to_shared(sDecCnt);
+            for (uint32_t s = 0; s < 64; ++s) {
+                for (uint32_t n = 0;; ++n) {
+                    unsigned int v;
+                    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(cnt_addr + 4 * s) : "memory");
+                    if (v >= cpc) break;
+                    if (n > (1u << 28)) __trap();
+                }
+                red_release_add(tc->dec + s, cpc);  // fence.acq_rel.gpu + add: the members' writes first
+            }
+        }
+        __syncwarp();
+        cluster_sync_all();
+        return;
+    }
     WinTermsFlags32<R> A, An;
-    A.load_global(T, sSlot[warp]);
+    auto load_rows = [&](WinTermsFlags32<R>& X, uint32_t s) {
+        if (tc && upc) {
+            if (lane == 0) wait_count(tc->lut + s, upc);
+            __syncwarp();
+            X.load_global_cg(T, sSlot[s * cpc + warp]);
+        } else {
+            X.load_global(T, sSlot[s * cpc + warp]);
+        }
+    };
+    load_rows(A, 0);
     LaneOffsets<R> off;
     off.init();
     cluster_sync_all();  // every CTA's barriers and flags are initialised before any remote st.async
     const uint32_t upper = (first + warp) & 1, pair_bar = 1 + (warp >> 1);
     for (uint32_t s = 0; s < 64; ++s) {
-        if (s + 1 < 64) An.load_global(T, sSlot[(s + 1) * cpc + warp]);
+        if (s + 1 < 64) load_rows(An, s + 1);
         if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
         if (threadIdx.x == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
@@ -1411,11 +1479,23 @@ __global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_
             acc[p] = ok;
             dEp[p] = (ok && !upper) ? 2 * sum : (i128)0;
             if (log) log[(size_t)s * M + sIdx[s * cpc + warp]] = ok;
+            if (tc)  // counted for the publisher warp (release at CTA scope: acc / dEp written first)
+                asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(
+                                 (uint32_t)__cvta_generic_to_shared(sDecCnt + s))
+                             : "memory");
         }
         A = An;
     }
+    (void)cta;
     tc::mbar_wait(mailbox(63), (63 >> 1) & 1);
     cluster_sync_all();
+}
+template <int R>
+__global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
+                                                        const DTabs T, uint8_t* __restrict__ acc,
+                                                        i128* __restrict__ dEp, uint8_t* __restrict__ log) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    decide_swap_body<R>(dsm, pass_t, seed, L, cpc, T, acc, dEp, log, nullptr, 0);
 }
 
 // Cluster decisions for tiles with more candidates per class than one 16 x 16-warp cluster has
@@ -2014,6 +2094,142 @@ __global__ void __launch_bounds__(BN_FG_THREADS, BN_FG_MINB) k_finish_gather(uin
         if (check_prev && (__ldcg(&out[-1].E_after[0]) != tot.e[0] || __ldcg(&out[-1].E_after[1]) != tot.e[1]))
             atomicOr(err, 4);
         *ticket = 0;
+    }
+}
+
+// ------------------------------------------------------------ fused pass tail (SWAP, L <= 128)
+// One cooperative launch of clusters of `ncta` CTAs replaces k_decide_swap + k_finish_gather
+// (DESIGN.md §5.8).  Cluster 0 decides the 64 colour classes exactly as k_decide_swap and publishes
+// every decided member in tc->dec[s]; the other clusters commit in class order behind it: once all
+// M members of class s are decided, each member q's final row (acc ? cn_q : c_q) is committed and
+// gathered into the next pass's candidate buffer at its next-pass partner, and the pass's exact
+// sums are accumulated (the last helper reduces them).  Co-residency of the decision cluster and
+// the helpers (which wait on it) is guaranteed by the cooperative launch.  Bit-identical to the
+// separate kernels: the same decisions, the same copies, the same exact sums.
+template <int R>
+__global__ void __launch_bounds__(544, 1) k_pass_tail(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
+                                                      longlong2* __restrict__ dterms, uint8_t* __restrict__ acc,
+                                                      i128* __restrict__ dEp, uint8_t* __restrict__ log,
+                                                      const u128* __restrict__ Epart, uint32_t nEpart, uint32_t nl,
+                                                      int* __restrict__ err,
+                                                      uint32_t rowB, const uint2* __restrict__ Un, uint2* __restrict__ U,
+                                                      const uint8_t* __restrict__ cn, uint8_t* __restrict__ c,
+                                                      const int* __restrict__ nn, int* __restrict__ nc,
+                                                      uint2* __restrict__ Un2, uint8_t* __restrict__ cn2,
+                                                      int* __restrict__ nn2, int gather_next,
+                                                      FinishPart* __restrict__ parts, PassStatsDev* __restrict__ out,
+                                                      int check_prev, TailCounters* __restrict__ tc) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    constexpr int WN = (2 * R + 1) * (2 * R + 1) - 1;
+    const uint32_t nb = L / 8, M = nb * nb, P = L * L;
+    const uint32_t ncta = M / cpc;
+    const DTabs T = {dterms, nullptr, nullptr};
+    if (blockIdx.x < ncta) {  // cluster 0: the decisions
+        decide_swap_body<R>(dsm, pass_t, seed, L, cpc, T, acc, dEp, log, tc, 0);
+        return;
+    }
+    // ------------------------------------------------------------------------ helpers
+    __shared__ uint8_t sD[8 * 16];
+    __shared__ uint32_t sUnit;
+    __shared__ FinishPart s_w[32];
+    __shared__ bool last;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nh = gridDim.x - ncta, hb = blockIdx.x - ncta;
+    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
+        sD[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
+    __syncthreads();
+    auto cls = [&](uint32_t q) -> uint32_t {  // colour class of pixel q in pass t
+        const uint32_t x = q & (L - 1), y = q / L;
+        const uint32_t along = (pass_t & 1) ? y : x, across = (pass_t & 1) ? x : y;
+        const uint32_t r = across & 7;
+        return 8 * r + ((along - sD[r * nb + (across >> 3)]) & 7);
+    };
+    // pass-start energy: this helper's share of the k_lut block partials
+    u128 e = 0;
+    const uint32_t e0 = (uint32_t)((uint64_t)nEpart * hb / nh), e1 = (uint32_t)((uint64_t)nEpart * (hb + 1) / nh);
+    for (uint32_t j = e0 + threadIdx.x; j < e1; j += blockDim.x) e += Epart[j];
+    // commit + next-pass gather in class order (unit = hw members, one per warp), exact sums
+    const uint32_t hw = (blockDim.x >> 5) < 16 ? (blockDim.x >> 5) : 16;
+    const uint32_t cpu_ = (M + hw - 1) / hw, ncunits = 64 * cpu_;
+    i128 dsum = 0;
+    unsigned na = 0;
+    const uint32_t n16 = rowB / 16;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            sUnit = atomicAdd(&tc->com_next, 1u);
+            if (sUnit < ncunits) wait_count(tc->dec + sUnit / cpu_, M);
+        }
+        __syncthreads();
+        const uint32_t u = sUnit;
+        __syncthreads();
+        if (u >= ncunits) break;
+        const uint32_t s = u / cpu_, m = (u - s * cpu_) * hw + warp;
+        if (warp >= hw || m >= M) continue;
+        const uint32_t q = class_pixel_tab(sD, L, pass_t, s, m);
+        const bool a = __ldcg(acc + q) != 0;
+        const uint4* src = reinterpret_cast<const uint4*>((a ? cn : c) + (size_t)q * rowB);
+        uint32_t p2 = 0;
+        if (gather_next) {
+            if (lane == 0) p2 = swap_partner(L, seed, pass_t + 1, q);
+            p2 = __shfl_sync(0xffffffffu, p2, 0);
+        }
+        uint4* dst_c = reinterpret_cast<uint4*>(c + (size_t)q * rowB);
+        uint4* dst_n = reinterpret_cast<uint4*>(cn2 + (size_t)p2 * rowB);
+        for (uint32_t j = lane; j < n16; j += 32) {
+            const uint4 v = src[j];
+            if (a) dst_c[j] = v;
+            if (gather_next) dst_n[j] = v;
+        }
+        if (lane == 0) {
+            const uint2 uq = a ? Un[q] : U[q];
+            if (a) U[q] = uq;
+            if (gather_next) Un2[p2] = uq;
+            const unsigned long long lo = __ldcg(reinterpret_cast<const unsigned long long*>(dEp + q));
+            const unsigned long long hi = __ldcg(reinterpret_cast<const unsigned long long*>(dEp + q) + 1);
+            dsum += (i128)(((u128)hi << 64) | lo);
+            na += a;
+            acc[q] = 0;  // the next pass starts from all-zero accept flags
+        }
+        if (lane < nl) {
+            const int nv = a ? nn[(size_t)q * nl + lane] : nc[(size_t)q * nl + lane];
+            if (a) nc[(size_t)q * nl + lane] = nv;
+            if (gather_next) nn2[(size_t)p2 * nl + lane] = nv;
+        }
+    }
+    // this helper's partial sums; the last helper reduces them and resets the counters
+    const FinishPart mine = block_sum_parts(e, (u128)dsum, na, s_w);
+    if (threadIdx.x == 0) {
+        parts[hb] = mine;
+        __threadfence();
+        last = atomicAdd(&tc->ticket, 1u) == nh - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    u128 E = 0, D = 0;
+    unsigned A = 0;
+    for (uint32_t j = threadIdx.x; j < nh; j += blockDim.x) {
+        const unsigned long long* qq = reinterpret_cast<const unsigned long long*>(parts + j);
+        E += ((u128)__ldcg(qq + 1) << 64) | __ldcg(qq + 0);
+        D += ((u128)__ldcg(qq + 3) << 64) | __ldcg(qq + 2);
+        A += (unsigned)__ldcg(qq + 4);
+    }
+    const FinishPart tot = block_sum_parts(E, D, A, s_w);
+    for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) tc->dec[j] = 0;
+    if (threadIdx.x == 0) {
+        const u128 Et = ((u128)tot.e[1] << 64) | tot.e[0], Dd = ((u128)tot.d[1] << 64) | tot.d[0];
+        const u128 Ea = Et + Dd;
+        out->E_before[0] = tot.e[0];
+        out->E_before[1] = tot.e[1];
+        out->E_after[0] = (unsigned long long)Ea;
+        out->E_after[1] = (unsigned long long)(Ea >> 64);
+        out->dE_sum[0] = tot.d[0];
+        out->dE_sum[1] = tot.d[1];
+        out->accepted = tot.a / 2;
+        if (check_prev && (__ldcg(&out[-1].E_after[0]) != tot.e[0] || __ldcg(&out[-1].E_after[1]) != tot.e[1]))
+            atomicOr(err, 4);
+        tc->com_next = 0;
+        tc->ticket = 0;
     }
 }
 
