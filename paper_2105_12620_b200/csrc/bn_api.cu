@@ -198,14 +198,18 @@ struct bn_ctx {
     // narrow count rows: in the SWAP / paper modes, where a pass only
     // permutes rows, the rows are stored as packed deltas c - round(N I_ref) (e2m1 / e3m2 per level,
     // chosen from the tile's measured range); every other consumer unpacks them first (ensure_u8)
-    int narrow_mode = -1;  // BN_NARROW: -1 auto (default), 0 off, 1 force e2m1, 2 force e3m2, 3 force u8 layout
+    int narrow_mode = -1;  // BN_NARROW: -1 auto (default: narrow when Tp >= 2048), 0 off, 1 narrow (range-chosen formats),
+                           // 2 e3m2 / u8 only, 3 the u8 layout through the narrow path
     bool packed = false;   // c holds narrow rows (layout fmt / lb / rowBn)
     uint32_t fmt[8] = {0}, lb[8] = {0}, rowBn = 0;
     DevBuf<uint8_t> noff;  // offsets [l][Tp]
     bool noff_dirty = true;
     DevBuf<int> nrng;      // per-level max |delta|
-    uint32_t layout_epoch = 0;  // bumped whenever the row layout changes (tensor-map cache)
-    struct MapEntry { const void* base; uint32_t epoch; CountMaps m[8]; };
+    int* nrng_host = nullptr;  // pinned copy, valid when nrng_epoch == layout_epoch (filled by bn_set_tile)
+    uint32_t nrng_epoch = 0xffffffffu;
+    uint32_t layout_epoch = 0;  // bumped whenever the rows are rewritten (range validity)
+    // tensor-map cache, keyed by buffer and layout (the layout is the same for every tile of a bank)
+    struct MapEntry { const void* base; uint64_t key; CountMaps m[8]; };
     std::vector<MapEntry> map_cache;
     // per-kernel event timing (bn_profile_*)
     bool prof = false;
@@ -430,15 +434,21 @@ uint32_t row_bytes(const bn_ctx* ctx) { return ctx->packed ? ctx->rowBn : ctx->r
 // Tensor maps of the rows at `base` in the current layout, cached per (buffer, layout epoch): the
 // candidate buffers alternate between a few pointers, and encoding 3 maps per level per launch
 // would cost tens of microseconds of host time per pass.
+uint64_t layout_key(const bn_ctx* ctx) {
+    uint64_t k = ((uint64_t)row_bytes(ctx) << 32) ^ ((uint64_t)ctx->L << 20) ^ ((uint64_t)ctx->Tp << 4) ^ ctx->nl;
+    for (uint32_t l = 0; l < ctx->nl; ++l) k = k * 1000003u + (ctx->packed ? 1 + ctx->fmt[l] : 0);
+    return k;
+}
 bool level_maps(bn_ctx* ctx, const void* base, CountMaps* out) {
+    const uint64_t key = layout_key(ctx);
     for (const auto& e : ctx->map_cache)
-        if (e.base == base && e.epoch == ctx->layout_epoch) {
+        if (e.base == base && e.key == key) {
             for (uint32_t l = 0; l < ctx->nl; ++l) out[l] = e.m[l];
             return true;
         }
     bn_ctx::MapEntry ent;
     ent.base = base;
-    ent.epoch = ctx->layout_epoch;
+    ent.key = key;
     for (uint32_t l = 0; l < ctx->nl; ++l) {
         const uint32_t f = ctx->packed ? ctx->fmt[l] : BN_FMT_U8;
         const uint64_t lb = ctx->packed ? ctx->lb[l] : (uint64_t)l * ctx->Tp;
@@ -507,8 +517,8 @@ int ensure_u8(bn_ctx* ctx) {
 // Narrow rows for the permuting modes: per level, the tile's max |c - round(N I_ref)| selects e2m1
 // (<= 4), e3m2 (<= 8) or u8; the rows are packed into that layout (norms |delta|^2).  One host
 // synchronisation (the range) per new tile.
-int ensure_narrow(bn_ctx* ctx) {
-    if (ctx->packed || ctx->narrow_mode == 0) return BN_OK;
+// Per-level max |c - off| of the current u8 rows into the pinned host buffer (asynchronous).
+int narrow_range_async(bn_ctx* ctx) {
     const uint32_t P = ctx->P, nl = ctx->nl, Tp = ctx->Tp;
     const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
     const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
@@ -521,13 +531,28 @@ int ensure_narrow(bn_ctx* ctx) {
         LAUNCHED();
         ctx->noff_dirty = false;
     }
+    if (!ctx->nrng_host) CUDA_TRY(cudaMallocHost(&ctx->nrng_host, 8 * sizeof(int)));
     CUDA_TRY(ctx->nrng.ensure(8));
     CUDA_TRY(cudaMemsetAsync(ctx->nrng.p, 0, 8 * sizeof(int), ctx->stream));
-    k_narrow_range<<<(P + 7) / 8, 256, 0, ctx->stream>>>(ctx->c.p, P, Tp, nl, ctx->noff.p, ctx->nrng.p);
+    k_narrow_range<<<4 * 148, 256, 0, ctx->stream>>>(ctx->c.p, P, Tp, nl, ctx->noff.p, ctx->nrng.p);
     LAUNCHED();
+    CUDA_TRY(cudaMemcpyAsync(ctx->nrng_host, ctx->nrng.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->nrng_epoch = ctx->layout_epoch;
+    return BN_OK;
+}
+
+// Narrow rows pay off where the Gram's K loop is long (C5: T = 8192, 0.84 -> 0.74 ms per Gram); with
+// T <= 1024 per level the Gram is bound by the TMA row rate, not bytes, and the pack is overhead.
+bool narrow_wanted(const bn_ctx* ctx) { return ctx->narrow_mode > 0 || (ctx->narrow_mode < 0 && ctx->Tp >= 2048); }
+
+int ensure_narrow(bn_ctx* ctx) {
+    if (ctx->packed || !narrow_wanted(ctx)) return BN_OK;
+    const uint32_t P = ctx->P, nl = ctx->nl, Tp = ctx->Tp;
+    int rc;
+    if (ctx->nrng_epoch != ctx->layout_epoch && (rc = narrow_range_async(ctx))) return rc;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // immediate when bn_set_tile already waited for it
     int rng[8];
-    CUDA_TRY(cudaMemcpyAsync(rng, ctx->nrng.p, sizeof rng, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    memcpy(rng, ctx->nrng_host, sizeof rng);
     NarrowLayout lay;
     uint32_t off = 0;
     for (uint32_t l = 0; l < 8; ++l) {
@@ -543,8 +568,9 @@ int ensure_narrow(bn_ctx* ctx) {
         if (l < nl) off += Tp * fmt_bits(f) / 8;
     }
     ctx->rowBn = off;
-    k_narrow_pack<<<(P + 7) / 8, 256, 0, ctx->stream>>>(ctx->c.p, P, Tp, nl, ctx->noff.p, lay, ctx->rowBn, ctx->cn.p,
-                                                       ctx->nn.p);
+    CUDA_TRY(cudaMemsetAsync(ctx->nn.p, 0, (size_t)P * nl * sizeof(int), ctx->stream));
+    k_narrow_pack<<<8 * 148, 256, 0, ctx->stream>>>(ctx->c.p, P, Tp, nl, ctx->noff.p, lay, ctx->rowBn, ctx->cn.p,
+                                                   ctx->nn.p);
     LAUNCHED();
     std::swap(ctx->c, ctx->cn);
     std::swap(ctx->nc, ctx->nn);
@@ -1055,7 +1081,7 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     const char* fu = getenv("BN_FUSE");
     ctx->no_fuse = fu && !strcmp(fu, "0");
     const char* nw = getenv("BN_NARROW");
-    ctx->narrow_mode = !nw || !*nw || !strcmp(nw, "auto") ? -1 : !strcmp(nw, "0") ? 0 : !strcmp(nw, "e2m1") ? 1
+    ctx->narrow_mode = !nw || !*nw || !strcmp(nw, "auto") ? -1 : !strcmp(nw, "0") ? 0 : !strcmp(nw, "1") ? 1
                      : !strcmp(nw, "e3m2") ? 2 : !strcmp(nw, "u8") ? 3 : -1;
     const char* ov = getenv("BN_OVERLAP");
     ctx->no_overlap = ov && !strcmp(ov, "0");
@@ -1101,6 +1127,7 @@ void bn_destroy(bn_ctx* ctx) {
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release(); ctx->rows_done.release();
         ctx->noff.release(); ctx->nrng.release(); ctx->tailc.release();
+        if (ctx->nrng_host) cudaFreeHost(ctx->nrng_host);
         if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
         if (ctx->hp) cudaStreamSynchronize(ctx->hp), cudaStreamDestroy(ctx->hp);
         for (cudaEvent_t e : {ctx->evA, ctx->evB, ctx->evC})
@@ -1238,6 +1265,8 @@ int bn_set_tile(bn_ctx* ctx, uint32_t L, const uint32_t* u_xy, int is_device) {
     ctx->counts_dirty = true;
     int rc = ensure_counts(ctx);
     if (rc) return rc;
+    // the narrow-row range of the new counts, ready (pinned) when the permuting optimiser packs them
+    if (narrow_wanted(ctx) && (rc = narrow_range_async(ctx))) return rc;
     if (!is_device) CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // host buffer may be reused
     return BN_OK;
 }

@@ -2453,38 +2453,42 @@ __global__ void k_narrow_offsets(const double* __restrict__ iref, uint32_t Ts, u
         off[(size_t)l * Tp + i] = (uint8_t)o;  // N_l <= 128
     }
 }
-// max over the tile of |c - off| per level -> rng[l] (atomicMax); one warp per pixel row.
+// max over the tile of |c - off| per level -> rng[l] (atomicMax).  One thread per 16-byte chunk of
+// the rows (grid-stride, fully parallel), one atomic per warp.
 __global__ void __launch_bounds__(256) k_narrow_range(const uint8_t* __restrict__ c, uint32_t P, uint32_t Tp, uint32_t nl,
                                                       const uint8_t* __restrict__ off, int* __restrict__ rng) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (p >= P) return;
-    for (uint32_t l = 0; l < nl; ++l) {
-        const uint8_t* row = c + ((size_t)p * nl + l) * Tp;
-        const uint8_t* o = off + (size_t)l * Tp;
+    const uint32_t g16 = Tp / 16, n = P * nl * g16;  // chunks; a warp's chunks lie in one (pixel, level) row
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < n; i += gridDim.x * blockDim.x) {
         int m = 0;
-        for (uint32_t i = 16 * lane; i < Tp; i += 512) {
-            const uint4 cv = *reinterpret_cast<const uint4*>(row + i);
-            const uint4 ov = *reinterpret_cast<const uint4*>(o + i);
-            const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cv);
-            const uint8_t* ob = reinterpret_cast<const uint8_t*>(&ov);
+        uint32_t l = 0;
+        if (i < n) {
+            const uint32_t row = i / g16, g = i - row * g16;
+            l = row % nl;
+            const uint4 cv = __ldcs(reinterpret_cast<const uint4*>(c) + i);
+            const uint4 ov = __ldg(reinterpret_cast<const uint4*>(off + (size_t)l * Tp) + g);
+            const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, ow[4] = {ov.x, ov.y, ov.z, ov.w};
 #pragma unroll
-            for (int j = 0; j < 16; ++j) m = max(m, abs((int)cb[j] - (int)ob[j]));
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t d = __vabsdiffu4(cw[k], ow[k]);  // four |c - off| bytes
+                m = max(m, (int)max(max(d & 0xff, (d >> 8) & 0xff), max((d >> 16) & 0xff, d >> 24)));
+            }
         }
-        m = __reduce_max_sync(0xffffffffu, (unsigned)m);
-        if (lane == 0 && m) atomicMax(rng + l, m);
+        // lanes of a warp share the level when g16 >= 32; otherwise reduce per lane
+        if (g16 % 32 == 0) {
+            m = (int)__reduce_max_sync(0xffffffffu, (unsigned)m);
+            if ((threadIdx.x & 31) == 0 && m && i < n) atomicMax(rng + l, m);
+        } else if (m && i < n) {
+            atomicMax(rng + l, m);
+        }
     }
 }
 __device__ __forceinline__ uint32_t enc_e2m1(int d) {  // |d| <= 4: 0 1 2 3 4 -> 0x0 0x2 0x4 0x5 0x6
-    const int a = d < 0 ? -d : d;
-    const uint32_t m = a == 0 ? 0x0u : a == 1 ? 0x2u : a == 2 ? 0x4u : a == 3 ? 0x5u : 0x6u;
-    return m | (d < 0 ? 0x8u : 0u);
+    const uint32_t a = (uint32_t)abs(d);
+    return (a < 3 ? 2 * a : a + 2) | (d < 0 ? 0x8u : 0u);
 }
-__device__ __forceinline__ uint32_t enc_e3m2(int d) {  // |d| <= 8: 1 + mantissa/4 times 2^(e-3)
-    const int a = d < 0 ? -d : d;
-    const uint32_t m = a == 0 ? 0x00u : a == 1 ? 0x0Cu : a < 4 ? 0x10u | (uint32_t)(2 * (a - 2))
-                     : a < 8 ? 0x14u | (uint32_t)(a - 4) : 0x18u;
-    return m | (d < 0 ? 0x20u : 0u);
+__device__ __forceinline__ uint32_t enc_e3m2(int d) {  // |d| <= 8: (1 + mantissa/4) 2^(e-3)
+    const uint32_t a = (uint32_t)abs(d);
+    return (a == 0 ? 0u : a == 1 ? 0x0Cu : a < 4 ? 0x0Cu + 2 * a : a < 8 ? 0x10u + a : 0x18u) | (d < 0 ? 0x20u : 0u);
 }
 __device__ __forceinline__ int dec_e2m1(uint32_t c) {
     const uint32_t m = c & 7u;
@@ -2503,61 +2507,61 @@ __device__ __forceinline__ int dec_e3m2(uint32_t c) {
 struct NarrowLayout {
     uint32_t fmt[8], lb[8];
 };
+// One thread per 16-integrand group (grid-stride); the row norms accumulate per warp in `norms`
+// (zeroed before the launch) with one atomic per warp and row.
 __global__ void __launch_bounds__(256) k_narrow_pack(const uint8_t* __restrict__ c, uint32_t P, uint32_t Tp, uint32_t nl,
                                                      const uint8_t* __restrict__ off, NarrowLayout lay, uint32_t rowBn,
                                                      uint8_t* __restrict__ out, int* __restrict__ norms) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (p >= P) return;
-    for (uint32_t l = 0; l < nl; ++l) {
-        const uint8_t* row = c + ((size_t)p * nl + l) * Tp;
-        const uint8_t* o = off + (size_t)l * Tp;
-        uint8_t* dst = out + (size_t)p * rowBn + lay.lb[l];
-        const uint32_t f = lay.fmt[l];
+    const uint32_t g16 = Tp / 16, n = P * nl * g16;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < n; i += gridDim.x * blockDim.x) {
         int nrm = 0;
-        for (uint32_t g = lane; g < Tp / 16; g += 32) {
-            const uint4 cv = *reinterpret_cast<const uint4*>(row + 16 * g);
+        uint32_t row = 0;
+        if (i < n) {
+            row = i / g16;
+            const uint32_t g = i - row * g16, p = row / nl, l = row - p * nl;
+            const uint4 cv = __ldcs(reinterpret_cast<const uint4*>(c) + i);
             const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cv);
+            uint8_t* dst = out + (size_t)p * rowBn + lay.lb[l];
+            const uint32_t f = lay.fmt[l];
             if (f == BN_FMT_U8) {
-                *reinterpret_cast<uint4*>(dst + 16 * g) = cv;
+                reinterpret_cast<uint4*>(dst)[g] = cv;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) nrm += (int)cb[j] * (int)cb[j];
-                continue;
-            }
-            const uint4 ov = *reinterpret_cast<const uint4*>(o + 16 * g);
-            const uint8_t* ob = reinterpret_cast<const uint8_t*>(&ov);
-            if (f == BN_FMT_E2M1) {
-                uint32_t w[2] = {0, 0};
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int d = (int)cb[j] - (int)ob[j];
-                    nrm += d * d;
-                    w[j >> 3] |= enc_e2m1(d) << (4 * (j & 7));
-                }
-                *reinterpret_cast<uint2*>(dst + 8 * g) = make_uint2(w[0], w[1]);
             } else {
-                unsigned long long lo = 0, hi = 0;  // 96 bits
+                const uint4 ov = __ldg(reinterpret_cast<const uint4*>(off + (size_t)l * Tp) + g);
+                const uint8_t* ob = reinterpret_cast<const uint8_t*>(&ov);
+                if (f == BN_FMT_E2M1) {
+                    uint32_t w[2] = {0, 0};
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int d = (int)cb[j] - (int)ob[j];
-                    nrm += d * d;
-                    const unsigned long long e = enc_e3m2(d);
-                    const int b = 6 * j;  // element j at bits b .. b+5 of the 96-bit group
-                    if (b < 64) {
-                        lo |= e << b;
-                        if (b + 6 > 64) hi |= e >> (64 - b);
-                    } else {
-                        hi |= e << (b - 64);
+                    for (int j = 0; j < 16; ++j) {
+                        const int d = (int)cb[j] - (int)ob[j];
+                        nrm += d * d;
+                        w[j >> 3] |= enc_e2m1(d) << (4 * (j & 7));
                     }
+                    reinterpret_cast<uint2*>(dst)[g] = make_uint2(w[0], w[1]);
+                } else {
+                    uint32_t w[3] = {0, 0, 0};  // 96 bits, element j at bits 6j .. 6j+5
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int d = (int)cb[j] - (int)ob[j];
+                        nrm += d * d;
+                        const uint32_t e = enc_e3m2(d), b = 6 * j;
+                        w[b >> 5] |= e << (b & 31);
+                        if ((b & 31) > 26) w[(b >> 5) + 1] |= e >> (32 - (b & 31));
+                    }
+                    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + 12 * g);
+                    d32[0] = w[0];
+                    d32[1] = w[1];
+                    d32[2] = w[2];
                 }
-                uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + 12 * g);
-                d32[0] = (uint32_t)lo;
-                d32[1] = (uint32_t)(lo >> 32);
-                d32[2] = (uint32_t)hi;
             }
         }
-        nrm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nrm);
-        if (lane == 0) norms[(size_t)p * nl + l] = nrm;
+        if (g16 % 32 == 0) {  // the warp's 32 groups belong to one row
+            nrm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nrm);
+            if ((threadIdx.x & 31) == 0 && i < n) atomicAdd(norms + row, nrm);
+        } else if (i < n) {
+            atomicAdd(norms + row, nrm);
+        }
     }
 }
 // Inverse of k_narrow_pack: counts c = delta + off (u8 rows [p][l][Tp]) and their norms |c|^2.

@@ -63,9 +63,12 @@ def _compare(s, g, st, lg):
     s.check()  # no device invariant failed in any launch
 
 
-@pytest.mark.parametrize("job", ["C2_swap", "C3_swap", "C3_redraw"])
-def test_full_passes_vs_oracle(bn, job):
-    """C2 (20 SWAP passes), C3 (2 SWAP passes; 2 REDRAW passes): every class of every pass."""
+@pytest.mark.parametrize("job,narrow", [("C2_swap", "auto"), ("C3_swap", "auto"), ("C3_swap", "1"),
+                                        ("C3_redraw", "auto")])
+def test_full_passes_vs_oracle(bn, job, narrow, monkeypatch):
+    """C2 (20 SWAP passes), C3 (2 SWAP passes, also on narrow rows; 2 REDRAW passes): every class of
+    every pass."""
+    monkeypatch.setenv("BN_NARROW", narrow)
     g = load(job)
     s = _sampler(bn, g)
     assert sha(s.eval_counts()) == g["counts0_sha256"], "initial counts differ"

@@ -224,11 +224,11 @@ def test_concurrent_contexts_match_sequential(bn, oracle_mod):
 
 
 # ------------------------------------------------- window Gram, narrow row formats (f3)
-@pytest.mark.parametrize("narrow", ["auto", "e3m2", "u8", "0"])
+@pytest.mark.parametrize("narrow", ["1", "e3m2", "u8", "0"])
 @pytest.mark.parametrize("L,T,levels", [(16, 64, (16,)), (32, 300, (1, 4, 16, 64)), (64, 512, (4,)), (32, 130, (128,))])
 def test_narrow_rows_window_distances(bn, oracle_mod, L, T, levels, narrow, monkeypatch):
     """The window Gram on every row format -- narrow e2m1 / e3m2 deltas chosen per level from the
-    tile's range (auto), e3m2 forced, the u8 layout through the narrow path, plain u8 rows (0) --
+    tile's range (1), e3m2 forced, the u8 layout through the narrow path, plain u8 rows (0) --
     gives the plain definition on the oracle's counts, after SWAP passes through the C-ABI equal to
     the oracle's (counts exported from the packed rows bit-exact)."""
     from tests.test_dist_cpu import _partial_distances
@@ -242,7 +242,7 @@ def test_narrow_rows_window_distances(bn, oracle_mod, L, T, levels, narrow, monk
         assert np.array_equal(D[li], _partial_distances(co[li], L))
 
 
-@pytest.mark.parametrize("narrow", ["auto", "e3m2", "0"])
+@pytest.mark.parametrize("narrow", ["1", "e3m2", "0"])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_narrow_rows_mode_switches(bn, oracle_mod, monkeypatch, narrow, mode):
     """Mode switches across narrow and u8 rows: SWAP (packs), REDRAW (unpacks), SWAP again,
