@@ -6,9 +6,13 @@
 A step is one optimisation pass over the whole tile (all 64 colour classes: candidate counts,
 windowed distances, energy terms, decisions, commit) = L*L pixel-update evaluations.
 N = 1 runs BASELINE's metric workload C3 (128x128 tile, T = 1024, 1/4/16/64 spp).  N > 1
-(torchrun, one process per GPU) gives every rank its own independent dimension-pair tile of
-the same shape (pair j = rank, seeds XOR j; reading R13): no data-path collective, weak
-scaling, value = all ranks' evals / max-over-ranks device time.
+(torchrun, one process per GPU) runs, unless --config is given, the sharded workload C4: the 8
+independent dimension-pair tiles (128^2, T = 1024) split over the ranks (pair j on rank j mod N;
+reading R13), no data-path collective, strong scaling, value = all evals / max-over-ranks device
+time.  Every line also carries secondary keys measured the same way (device time, max over
+ranks): "redraw" (C3 with the REDRAW optimiser, which counts new candidates every pass), "c4"
+(the 8 pairs over the N ranks) and "c5" (C5, one tile; at N > 1 bank-sharded over the ranks with
+one NCCL int32 all-reduce of the partial window distances per pass).
 
 --impl reference times the CPU oracle (oracle/, single-threaded C) on bounded samples of the
 same workload; under torchrun only rank 0 runs it.
@@ -48,7 +52,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default=None, help="workload (default: C3 at N = 1, C4 at N > 1)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the redraw / c4 / c5 secondary keys")
     ap.add_argument("--mode", choices=["config", "redraw", "swap", "paper"], default="config",
                     help="optimiser mode (default: the config's); paper = PAPER.md §3.4 snapshot couples, N/4 budget")
     ap.add_argument("--K", type=int, default=1, help="best-of-K re-draws (REDRAW only; K candidates per pixel)")
@@ -147,35 +152,52 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------- roofline
+def method_macs_per_eval(cfg):
+    """one pixel-update eval compares one new count row with the 224 rows of its
+    window at every level: 224 * T * levels int8 multiply-accumulates (C3: 917,504 MAC)."""
+    return 224 * cfg.T * len(cfg.levels)
+
+
+def row_bytes(cfg):
+    return len(cfg.levels) * (-(-cfg.T // 256) * 256)
+
+
 def algorithmic(kernel, cfg):
     """(units per launch, unit, bound) of each kernel class -- DESIGN.md §7."""
     P, T, nl, R = cfg.L * cfg.L, cfg.T, len(cfg.levels), 7
     H = 2 * R * R + 2 * R
+    WN = (2 * R + 1) ** 2 - 1
     if kernel == "gram":
-        # 4 int8 dot products per unordered window pair and level, T-long: 2 ops per MAC
-        return 2.0 * P * H * 4 * nl * T, "ops", "tensor"
+        # §8(d) method work: 224 T levels MAC per eval (2 ops per MAC) for every eval of the pass
+        return 2.0 * method_macs_per_eval(cfg) * evals_per_pass(cfg), "ops", "tensor"
     if kernel == "counts":
         # one half-plane test per (pixel, integrand, sample) = 2 FFMA (fp32 filter, exact fallback)
         return 2.0 * P * T * max(cfg.levels), "ffma", "alu"
     if kernel == "lut":
-        # bytes: read the 4 int32 distances per (p, h, level) (two int2 planes); write the 4 int64
-        # dE terms per (p, h) (p side and q side; the int128 escapes are rare)
+        # read the 4 int32 distances per (p, h, level) (two int2 planes); write the 4 int64 dE terms per (p, h)
         return float(P * H * (16 * nl + 32)), "bytes", "hbm"
     if kernel == "decide":
         if cfg.mode == 2:  # paper mode: the snapshot dE term (int64) of each couple member's window
-            return float(evals_per_pass(cfg) * ((2 * R + 1) ** 2 - 1) * 8), "bytes", "hbm"
-        # bytes: both int64 dE terms per (candidate, window offset), all 64 classes in one launch
-        return float(P * ((2 * R + 1) ** 2 - 1) * 16), "bytes", "hbm"
-    if kernel == "gather":
-        # bytes: read and write every pixel's count rows (partner rows -> candidate buffer)
-        return float(2 * P * nl * (-(-T // 256) * 256)), "bytes", "hbm"
+            return float(evals_per_pass(cfg) * WN * 8), "bytes", "hbm"
+        return float(P * WN * 16), "bytes", "hbm"  # both int64 dE terms per (candidate, window offset)
+    if kernel == "tail":
+        # the decisions' dE terms + the commit / next-pass gather of every row (read + write)
+        return float(P * WN * 16 + 2 * P * row_bytes(cfg)), "bytes", "hbm"
+    if kernel in ("gather", "commit"):
+        return float(2 * P * row_bytes(cfg)), "bytes", "hbm"  # read and write every pixel's rows
     return None, None, None
+
+
+def ncu_traffic():
+    try:
+        return json.load(open(TRAFFIC_FILE))
+    except (OSError, ValueError):
+        return {}
 
 
 def roofline(prof, cfg, peaks, sm_clock_mhz, name=None):
     """Roofline line of one kernel class; default: the kernel with the largest device time per
-    step (C3: k_counts, which runs beside the energy terms and decisions and, with the Gram,
-    sets the pass time -- DESIGN.md 7)."""
+    step (C3: the window Gram)."""
     if name is None:
         name = max(prof, key=lambda k: prof[k][0])
     ms, n = prof[name]
@@ -185,13 +207,15 @@ def roofline(prof, cfg, peaks, sm_clock_mhz, name=None):
     if units is None:
         out.update(bound="latency", achieved=None, peak=None, unit=None, frac=None, traffic=None)
         return out
-    per_s = units / (ms / max(n, 1) / 1e3)
+    sec = ms / max(n, 1) / 1e3
+    per_s = units / sec
     if bound == "hbm":
         peak = peaks.get("hbm_gbs", 6650.0)
         out.update(bound="hbm", achieved=per_s / 1e9, peak=peak, unit="GB/s")
         out["peak_source"] = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
     elif bound == "tensor":
-        # int8 dense tensor peak = measured bf16 dense (cuBLAS) x nominal int8/bf16 ratio 4.5/2.25
+        # int8 (and the f8f6f4 narrow rows) dense tensor peak = measured bf16 dense (cuBLAS) x the
+        # nominal ratio 4.5 / 2.25 PFLOP/s (B200_PROFILING.md)
         bf16 = peaks.get("bf16_tflops", 1590.0)
         peak = 2.0 * bf16
         out.update(bound="tensor", achieved=per_s / 1e12, peak=peak, unit="TOP/s (int8)")
@@ -199,41 +223,60 @@ def roofline(prof, cfg, peaks, sm_clock_mhz, name=None):
                               if "bf16_tflops" in peaks else "fallback 1.59 PF bf16 x 2")
     else:
         clk = peaks.get("sm_max_mhz", 1965.0)
-        if kind == "ops":
-            peak = SMS * DP4A_PER_CLK_SM * 8 * clk * 1e6 / 1e12  # TOP/s (dp4a: 4 MAC = 8 ops)
-            out.update(bound="alu", achieved=per_s / 1e12, peak=peak, unit="TOP/s")
-        else:
-            peak = SMS * 128 * clk * 1e6 / 1e12                  # T FFMA/s: 128 lanes/clk/SM
-            out.update(bound="alu", achieved=per_s / 1e12, peak=peak, unit="T FFMA/s")
-        lanes = "64 dp4a" if kind == "ops" else "128 FFMA"
-        out["peak_source"] = f"derived: 148 SM x {lanes} lanes/clk x clocks.max.sm {clk:.0f} MHz (DESIGN.md §7)"
+        peak = SMS * 128 * clk * 1e6 / 1e12                  # T FFMA/s: 128 lanes/clk/SM
+        out.update(bound="alu", achieved=per_s / 1e12, peak=peak, unit="T FFMA/s")
+        out["peak_source"] = f"derived: 148 SM x 128 FFMA lanes/clk x clocks.max.sm {clk:.0f} MHz (DESIGN.md §7)"
     out["frac"] = out["achieved"] / out["peak"]
     out["traffic"] = None
-    try:
-        tr = json.load(open(TRAFFIC_FILE)).get(f"{cfg.name}:{name}")
-        if tr:
-            out["traffic"] = tr["dram_bytes_per_launch"]
-            out["traffic_source"] = tr.get("source", TRAFFIC_FILE)
-    except (OSError, ValueError):
-        pass
+    tr = ncu_traffic().get(f"{cfg.name}:{name}")
+    if tr:
+        out["traffic"] = tr["dram_bytes_per_launch"]
+        out["traffic_source"] = tr.get("source", TRAFFIC_FILE)
     if sm_clock_mhz:
         out["sm_mhz_during_run"] = sm_clock_mhz
-    if name == "gram" and cfg.name in ("C3", "C4", "C5"):
-        out["limiter"] = ("L2->SM operand streaming: the UMMA pipe runs at its peak MAC rate when fed "
-                          "(tools/umma_bench.cu), a run without the epilogue takes ~80% of the kernel "
-                          "time; 31% of the issued MACs are useful (dense 128x240 tiles, DESIGN.md 5.1)")
-        # TMA operand bytes per launch: every (8x8 block, level) item streams 3 neighbour chunks x Tp/128
-        # K-slices of one 46 KB stage (A: 128 rows, B: 240 rows of 128 B)
+    if name == "gram":
+        out["units"] = (f"SURVEY §8(d) method work: {method_macs_per_eval(cfg)} MAC per eval x "
+                        f"{evals_per_pass(cfg)} evals per launch, 2 ops per MAC")
+        # what the tensor pipe is actually issued: dense 128 x 240 tiles, every (8x8 block, level)
+        # item x 3 neighbour chunks x T: the 4 state combinations of the half window plus the
+        # pixels outside every window (DESIGN.md 5.0 / 5.1)
         items = (cfg.L // 8) ** 2 * len(cfg.levels)
-        stream = items * 3 * (-(-cfg.T // 256) * 256 // 128) * (128 + 240) * 128
-        gbs = stream / (ms / max(n, 1) / 1e3) / 1e9
-        out["operand_stream"] = {"bytes_per_launch": stream, "achieved_GBs": gbs, "l2_read_peak_GBs": L2_PEAK_GBS,
-                                 "frac": gbs / L2_PEAK_GBS,
-                                 "peak_source": "tools/l2bw.cu on this pool (L2-resident 48 MB, 16-B loads, all SMs)"}
+        issued = 2.0 * items * 3 * (-(-cfg.T // 256) * 256) * 128 * 240
+        out["issued"] = {"ops_per_launch": issued, "achieved": issued / sec / 1e12, "frac": issued / sec / 1e12 / out["peak"],
+                         "note": "dense UMMA tiles as issued (4 state combinations x half window, padded)"}
+        out["limiter"] = ("TMA row rate: removing the epilogue or the MMAs leaves ~90% of the time, halving the "
+                          "operand bytes (narrow rows) does not shorten it; the K loop is row-request bound "
+                          "(DESIGN.md 5.1, tools/kernel_times.py probes)")
     if name == "counts":
         out["limiter"] = ("ALU-pipe issue: per test 1 FFMA2 (fma pipe) + ~1.75 half-rate ALU ops (sign "
                           "count, |t| filter); the FFMA-lane peak is the reported denominator (DESIGN.md 5.1)")
     return out
+
+
+def pass_dram(cfg, ms_per_pass, peaks, kernels):
+    """Pass-level DRAM fraction: the DRAM bytes of one pass's kernels from the committed ncu capture
+    (profiles/ncu_traffic.json) / the measured pass time / HBM peak."""
+    tr = ncu_traffic()
+    parts = {k: tr[f"{cfg.name}:{k}"]["dram_bytes_per_launch"] for k in kernels if f"{cfg.name}:{k}" in tr}
+    if not parts:
+        return None
+    total = float(sum(parts.values()))
+    gbs = total / (ms_per_pass / 1e3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    return {"bytes_per_pass": total, "per_kernel": parts, "achieved_GBs": gbs, "peak_GBs": peak, "frac": gbs / peak,
+            "source": TRAFFIC_FILE}
+
+
+def host_cpu():
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
 
 
 # --------------------------------------------------------------------------- oracle sample
@@ -288,25 +331,121 @@ def run_reference(args, cfg):
         tt += dt
         per.append(dt)
     v = ev / tt
+    model, nproc = host_cpu()
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": config_json(cfg, 1),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": cpu_sample_desc(cfg, classes) + " per step"},
+                         "sample": cpu_sample_desc(cfg, classes) + " per step", "cpu_model": model, "nproc": nproc},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------------ ours
+class Workload:
+    """The contexts of one workload on this rank: C4's pairs split over the ranks (strong scaling),
+    C5 at N > 1 bank-sharded (one NCCL all-reduce of the partial distances per pass, strong
+    scaling), otherwise one independent pair tile per rank (weak scaling)."""
+
+    def __init__(self, cfg, args, rank, world, local, stream):
+        import torch
+
+        from paper_2105_12620_b200 import bn
+        from paper_2105_12620_b200.dist import make_bank_sharded, pairs_of_rank
+
+        self.cfg, self.stream = cfg, stream
+        self.banksharded = cfg.name == "C5" and world > 1
+        if cfg.pairs > 1:
+            self.pairs, self.scaling = pairs_of_rank(cfg.pairs, rank, world), "strong"
+        elif self.banksharded:
+            self.pairs, self.scaling = [0], "strong"
+        else:
+            self.pairs, self.scaling = [rank], "weak"
+        P = cfg.L * cfg.L
+        self.samplers, self.streams, self.seeds = [], [], []
+        for j in self.pairs:
+            U, (a, b, px, py) = synth.problem_inputs(cfg, j)
+            st_j = torch.cuda.Stream() if len(self.pairs) > 1 else stream
+            s = bn.Sampler(local, st_j.cuda_stream)
+            s.set_lattice(synth.D1, synth.D2, cfg.levels)
+            if self.banksharded:
+                make_bank_sharded(s, a, b, px, py, rank, world)
+            else:
+                s.set_bank(a, b, px, py)
+            s.set_energy(2.1, 1.0, 7)
+            s.set_energy_form({"gf": 0, "eq1": 1, "eq1max": 2}[args.energy])
+            s.set_tile(cfg.L, U)
+            if cfg.mode == 2:
+                s.set_permutation(synth.make_permutation(P, synth.opt_seed(cfg, j)))
+            self.samplers.append(s)
+            self.streams.append(st_j)
+            self.seeds.append(synth.opt_seed(cfg, j))
+        EP = evals_per_pass(cfg)
+        # evals of one step summed over all ranks
+        self.units_per_step = EP * cfg.pairs if cfg.pairs > 1 else EP * (1 if self.banksharded else world)
+
+    def run(self, passes, first):
+        """Enqueue `passes` passes on every local pair (each on its own stream), joined to `stream`."""
+        import torch
+
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        for sj, stj, sd in zip(self.samplers, self.streams, self.seeds):
+            if stj is not self.stream:
+                stj.wait_event(ev)
+            sj.optimize(passes, sd, mode=self.cfg.mode, first_pass=first, stats=False, K=self.cfg.extra.get("K", 1))
+        for stj in self.streams:
+            if stj is not self.stream:
+                e = torch.cuda.Event()
+                e.record(stj)
+                self.stream.wait_event(e)
+
+    def launches(self):
+        return sum(x.launch_count() for x in self.samplers)
+
+    def check(self):
+        for x in self.samplers:  # every device invariant of the timed passes held (exact E chain, ranges)
+            x.check()
+
+    def close(self):
+        for x in self.samplers:
+            x.close()
+
+
+def timed(wl, steps, warmup, barrier, clock_index=None):
+    """W untimed warm-up passes, then `steps` passes between barriers and CUDA events on the
+    workload's stream; returns (device ms of this rank, launches, clock summary or None)."""
+    import torch
+
+    wl.run(warmup, 0)
+    barrier()
+    l0 = wl.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(clock_index) if clock_index is not None else None
+    if clk:
+        clk.__enter__()
+    barrier()
+    e0.record(wl.stream)
+    wl.run(steps, warmup)
+    e1.record(wl.stream)
+    barrier()
+    if clk:
+        clk.__exit__()
+    wl.check()
+    return e0.elapsed_time(e1), wl.launches() - l0, clk.summary() if clk else None
+
+
 def run_ours(args, cfg):
+    import dataclasses
+
     import torch
     import torch.distributed as dist
 
     from paper_2105_12620_b200 import bn
-    from paper_2105_12620_b200.dist import max_over_ranks, pairs_of_rank, sum_over_ranks
+    from paper_2105_12620_b200.dist import max_over_ranks, sum_over_ranks
 
     rank, local, world = dist_env()
     if world != args.gpus:
@@ -322,75 +461,13 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
-    # Work decomposition:
-    #  C4: the 8 independent dimension pairs are split over ranks (strong scaling, fixed total);
-    #  C5 with N > 1: one tile, bank shards + one int32 all-reduce per pass (strong scaling);
-    #  otherwise: one independent pair tile per rank (weak scaling).
-    banksharded = cfg.name == "C5" and world > 1
-    if cfg.pairs > 1:
-        pairs, scaling = pairs_of_rank(cfg.pairs, rank, world), "strong"
-    elif banksharded:
-        pairs, scaling = [0], "strong"
-    else:
-        pairs, scaling = [rank], "weak"
-    P = cfg.L * cfg.L
-    samplers, streams, seeds = [], [], []
-    for j in pairs:
-        U, (a, b, px, py) = synth.problem_inputs(cfg, j)
-        st_j = torch.cuda.Stream() if len(pairs) > 1 else stream
-        s = bn.Sampler(local, st_j.cuda_stream)
-        s.set_lattice(synth.D1, synth.D2, cfg.levels)
-        if banksharded:
-            from paper_2105_12620_b200.dist import make_bank_sharded
-
-            make_bank_sharded(s, a, b, px, py, rank, world)
-        else:
-            s.set_bank(a, b, px, py)
-        s.set_energy(2.1, 1.0, 7)
-        s.set_energy_form({"gf": 0, "eq1": 1, "eq1max": 2}[args.energy])
-        s.set_tile(cfg.L, U)
-        if cfg.mode == 2:
-            s.set_permutation(synth.make_permutation(P, synth.opt_seed(cfg, j)))
-        samplers.append(s)
-        streams.append(st_j)
-        seeds.append(synth.opt_seed(cfg, j))
-    s = samplers[0]
-    U0 = synth.problem_inputs(cfg, pairs[0])[0]
-
-    def run_all(passes, first):
-        """Enqueue `passes` passes on every local pair (each on its own stream), joined to `stream`."""
-        ev = torch.cuda.Event()
-        ev.record(stream)
-        for sj, stj, sd in zip(samplers, streams, seeds):
-            if stj is not stream:
-                stj.wait_event(ev)
-            sj.optimize(passes, sd, mode=cfg.mode, first_pass=first, stats=False, K=cfg.extra.get("K", 1))
-        for stj in streams:
-            if stj is not stream:
-                e = torch.cuda.Event()
-                e.record(stj)
-                stream.wait_event(e)
-
-    # warm-up passes (W >= 3 by contract)
-    run_all(args.warmup, 0)
-    barrier()
-    l0 = sum(x.launch_count() for x in samplers)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        e0.record(stream)
-        run_all(args.steps, args.warmup)
-        e1.record(stream)
-        barrier()
-    ms = e0.elapsed_time(e1)
-    launches = sum(x.launch_count() for x in samplers) - l0
-    for x in samplers:  # every device invariant of the timed passes held (exact E chain, ranges)
-        x.check()
+    wl = Workload(cfg, args, rank, world, local, stream)
+    ms, launches, clocks = timed(wl, args.steps, args.warmup, barrier, clock_index=local)
     ms_max = max_over_ranks(ms)
+    value = wl.units_per_step * args.steps / (ms_max / 1e3)
+    s, seeds, pairs = wl.samplers[0], wl.seeds, wl.pairs
+    P = cfg.L * cfg.L
     EP = evals_per_pass(cfg)
-    units_per_step = EP * (1 if banksharded else len(pairs) * world) if cfg.pairs == 1 else EP * cfg.pairs
-    value = units_per_step * args.steps / (ms_max / 1e3)
-    clocks = clk.summary()
 
     # per-kernel device time on the context stream (one pair alone, events around each launch)
     s.profile_enable(True)
@@ -404,6 +481,10 @@ def run_ours(args, cfg):
     for k in active:
         r = roofline(active, cfg, peaks, None, name=k)
         roof_all[k] = {x: r.get(x) for x in ("bound", "achieved", "peak", "unit", "frac", "avg_launch_ms")}
+    # pass-level DRAM fraction: the steady-state pass kernels as captured under ncu (where the fused
+    # tail runs as its two constituents, k_decide_* + k_finish_gather), over the live pass time
+    ms_pass_single = sum(v[0] for v in active.values()) / args.steps
+    pdram = pass_dram(cfg, ms_pass_single, peaks, ["gram", "lut", "decide", "commit"])
 
     # end to end through the public API with host buffers: per step, H2D of a tile from pinned host
     # memory (bn_set_tile, which rebuilds its counts), one pass (bn_optimize) and D2H of the resulting
@@ -417,7 +498,7 @@ def run_ours(args, cfg):
         e_stream = torch.cuda.Stream()
         s_b = bn.Sampler(local, e_stream.cuda_stream)
         s_b.set_lattice(synth.D1, synth.D2, cfg.levels)
-        if banksharded:
+        if wl.banksharded:
             from paper_2105_12620_b200.dist import make_bank_sharded
 
             make_bank_sharded(s_b, ea, eb, epx, epy, rank, world)
@@ -450,7 +531,7 @@ def run_ours(args, cfg):
     first += 2
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(streams[0])
+    f0.record(wl.streams[0])
     for es in e_streams:
         es.wait_event(f0)
     for k in range(min(NT - 1, args.e2e_steps)):
@@ -462,26 +543,49 @@ def run_ours(args, cfg):
     for es in e_streams:
         ej = torch.cuda.Event()
         ej.record(es)
-        streams[0].wait_event(ej)
-    f1.record(streams[0])
+        wl.streams[0].wait_event(ej)
+    f1.record(wl.streams[0])
     barrier()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
     E_after = s.energy()[1]
     for s_b in extra:
         s_b.close()
-    e2e_units = EP * (1 if banksharded else world)
+    e2e_units = EP * (1 if wl.banksharded else world)
     e2e = {"value": e2e_units * args.e2e_steps / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": P * 8, "d2h_bytes_per_step": P * 8,
            "path": ("per step: bn_set_tile(pinned host tile) + bn_optimize(1 pass) + bn_get_tile(pinned host), "
                     f"{NT} independent tiles on {NT} streams, steps up to k+{NT - 1} enqueued before step k's result is read")}
-    del U0
+    wl.close()
+
+    # secondary workloads, measured the same way (device time, max over ranks, invariants checked)
+    secondary = {}
+    if not args.no_secondary:
+        sec = []
+        if cfg.name == "C3" and cfg.mode != 0:
+            sec.append(("redraw", dataclasses.replace(cfg, mode=0), 10))
+        if cfg.name != "C4":
+            sec.append(("c4", synth.CONFIGS["C4"], 10))
+        if cfg.name != "C5":
+            sec.append(("c5", synth.CONFIGS["C5"], 5))
+        for key, c2, st2 in sec:
+            w2 = Workload(c2, args, rank, world, local, stream)
+            ms2, _, _ = timed(w2, st2, 3, barrier)
+            ms2 = max_over_ranks(ms2)
+            secondary[key] = {"value": w2.units_per_step * st2 / (ms2 / 1e3), "unit": UNIT, "steps": st2, "warmup": 3,
+                              "ms_per_step": ms2 / st2, "scaling": w2.scaling,
+                              "workload": workload(c2)["workload"] + f" [{workload(c2)['mode']}]",
+                              "per_rank": (f"{len(w2.pairs)} of the {c2.pairs} pair tiles" if c2.pairs > 1 else
+                                           f"bank shard {world}-way, NCCL int32 all-reduce per pass" if w2.banksharded
+                                           else "one independent tile")}
+            w2.close()
 
     launches = sum_over_ranks(launches)  # total over all ranks
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ev, dt, _ = oracle_sample(cfg, 0, args.cpu_classes)
+        model, nproc = host_cpu()
         cpu = {"value": ev / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": cpu_sample_desc(cfg, args.cpu_classes), "seconds": dt}
+               "sample": cpu_sample_desc(cfg, args.cpu_classes), "seconds": dt, "cpu_model": model, "nproc": nproc}
 
     if rank == 0:
         cfgj = config_json(cfg, world)
@@ -490,22 +594,23 @@ def run_ours(args, cfg):
         if cfg.pairs > 1:
             cfgj["per_rank"] = f"{len(pairs)} of the {cfg.pairs} independent dimension-pair tiles, one stream each"
             cfgj["global_tiles"] = cfg.pairs
-        elif banksharded:
+        elif wl.banksharded:
             cfgj["per_rank"] = f"bank shard {world}-way, one int32 NCCL all-reduce of window distances per pass"
             cfgj["global_tiles"] = 1
+        if pdram:
+            roof["pass_dram"] = pdram
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "scaling": wl.scaling, "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": cfgj, "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
             "roofline": roof, "cpu_baseline": cpu,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
             "roofline_per_kernel": roof_all,
             "final_energy": E_after,
+            **secondary,
         }
         print(json.dumps(line), flush=True)
-    for x in samplers:
-        x.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -514,6 +619,8 @@ def main():
     args = parse()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if args.config is None:
+        args.config = "C3" if dist_env()[2] == 1 else "C4"
     cfg = synth.CONFIGS[args.config]
     if args.mode != "config":
         import dataclasses

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <functional>
 #include <string>
 #include <vector>
@@ -534,7 +535,9 @@ int narrow_range_async(bn_ctx* ctx) {
     if (!ctx->nrng_host) CUDA_TRY(cudaMallocHost(&ctx->nrng_host, 8 * sizeof(int)));
     CUDA_TRY(ctx->nrng.ensure(8));
     CUDA_TRY(cudaMemsetAsync(ctx->nrng.p, 0, 8 * sizeof(int), ctx->stream));
-    k_narrow_range<<<4 * 148, 256, 0, ctx->stream>>>(ctx->c.p, P, Tp, nl, ctx->noff.p, ctx->nrng.p);
+    const size_t nch = (size_t)P * nl * (Tp / 16);  // 16-byte chunks; ~4 per thread
+    k_narrow_range<<<(unsigned)std::min<size_t>((nch + 1023) / 1024, 148 * 64), 256, 0, ctx->stream>>>(
+        ctx->c.p, P, Tp, nl, ctx->noff.p, ctx->nrng.p);
     LAUNCHED();
     CUDA_TRY(cudaMemcpyAsync(ctx->nrng_host, ctx->nrng.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     ctx->nrng_epoch = ctx->layout_epoch;
@@ -569,8 +572,9 @@ int ensure_narrow(bn_ctx* ctx) {
     }
     ctx->rowBn = off;
     CUDA_TRY(cudaMemsetAsync(ctx->nn.p, 0, (size_t)P * nl * sizeof(int), ctx->stream));
-    k_narrow_pack<<<8 * 148, 256, 0, ctx->stream>>>(ctx->c.p, P, Tp, nl, ctx->noff.p, lay, ctx->rowBn, ctx->cn.p,
-                                                   ctx->nn.p);
+    const size_t nch = (size_t)P * nl * (Tp / 16);
+    k_narrow_pack<<<(unsigned)std::min<size_t>((nch + 1023) / 1024, 148 * 64), 256, 0, ctx->stream>>>(
+        ctx->c.p, P, Tp, nl, ctx->noff.p, lay, ctx->rowBn, ctx->cn.p, ctx->nn.p);
     LAUNCHED();
     std::swap(ctx->c, ctx->cn);
     std::swap(ctx->nc, ctx->nn);
@@ -1078,6 +1082,12 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->no_big = dm && !strcmp(dm, "nobig");
     const char* tl = getenv("BN_TAIL");
     ctx->no_tail = tl && !strcmp(tl, "0");
+    // Nsight Compute cannot replay the cooperative cluster launch of the fused tail: under a
+    // profiler (injection library present) the pass runs the separate kernels instead
+    for (const char* v : {"NV_COMPUTE_PROFILER_PERFWORKS_DIR", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE", "CUDA_INJECTION64_PATH"}) {
+        const char* inj = getenv(v);
+        if (inj && *inj) ctx->no_tail = true;
+    }
     const char* fu = getenv("BN_FUSE");
     ctx->no_fuse = fu && !strcmp(fu, "0");
     const char* nw = getenv("BN_NARROW");
