@@ -565,6 +565,9 @@ def run_ours(args, cfg):
             sec.append(("redraw", dataclasses.replace(cfg, mode=0), 10))
         if cfg.name != "C4":
             sec.append(("c4", synth.CONFIGS["C4"], 10))
+        if world == 1:
+            # what every rank of an 8-GPU C4 run does: one pair tile alone (no exchange between ranks)
+            sec.append(("c4_one_pair", dataclasses.replace(synth.CONFIGS["C4"], pairs=1), 20))
         if cfg.name != "C5":
             sec.append(("c5", synth.CONFIGS["C5"], 5))
         for key, c2, st2 in sec:
@@ -572,6 +575,7 @@ def run_ours(args, cfg):
             ms2, _, _ = timed(w2, st2, 3, barrier)
             ms2 = max_over_ranks(ms2)
             secondary[key] = {"value": w2.units_per_step * st2 / (ms2 / 1e3), "unit": UNIT, "steps": st2, "warmup": 3,
+                              "n_gpus": world,
                               "ms_per_step": ms2 / st2, "scaling": w2.scaling,
                               "workload": workload(c2)["workload"] + f" [{workload(c2)['mode']}]",
                               "per_rank": (f"{len(w2.pairs)} of the {c2.pairs} pair tiles" if c2.pairs > 1 else

@@ -26,6 +26,19 @@
 
 namespace bn {
 
+// Debug build (-DBN_DEBUG_BOUNDS, tools/gpu_debug.sh): device bounds checks at the index
+// computations of the pass kernels; a failed check traps (the launch fails with an error).
+#ifdef BN_DEBUG_BOUNDS
+#define BN_ASSERT(c)          \
+    do {                      \
+        if (!(c)) __trap();   \
+    } while (0)
+#else
+#define BN_ASSERT(c) \
+    do {             \
+    } while (0)
+#endif
+
 typedef __int128 i128;
 typedef unsigned __int128 u128;
 
@@ -645,6 +658,7 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
         const uint32_t x = p % L, y = p / L;
         const uint32_t q = ((y + oy) & (L - 1)) * L + ((x + ox + L) & (L - 1));
         const int wi = win_index(ox, oy, R), wm = win_index(-ox, -oy, R);
+        BN_ASSERT(p < P && q < P && wi >= 0 && wi < WN && wm >= 0 && wm < WN);
         const double w = W[wi];
         // q < 2^52: per-level differences and their sums over <= 8 levels are exact in int64 (R15)
         long long a0 = 0, a1 = 0, b0 = 0, b1 = 0;
@@ -890,6 +904,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
             }
             named_bar(2, 128);
             const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
+            BN_ASSERT(p < P && l < nl);
             const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
             int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
             for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
@@ -1337,6 +1352,7 @@ __global__ void __launch_bounds__(mode ? 256 : 512, 1) k_decide_cl3(uint32_t pas
                          : "memory");
         const uint32_t m = first + warp, mm = m ^ (mode ? sKappa[s] : 0u);
         const uint32_t p = sSlot[s * per_class + warp], p2 = mode ? sSlot[s * per_class + cpc + warp] : p;
+        BN_ASSERT(p < P && p2 < P);
         i128 sum = A.sum_flags(sflags, L, p, off, T);
         if (mode) sum += B.sum_flags(sflags, L, p2, off, T);
         const bool ok = 2 * sum < 0;
@@ -1464,6 +1480,7 @@ __device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, 
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
                          : "memory");
         const uint32_t p = sSlot[s * cpc + warp];
+        BN_ASSERT(p < P);
         const i128 mine = A.sum_flags(sflags, L, p, off, T);
         if (lane == 0) {
             sPart[warp][0] = (unsigned long long)mine;
@@ -1581,6 +1598,7 @@ __global__ void __launch_bounds__(512, 1) k_decide_big(uint32_t pass_t, uint64_t
             const bool more = k + 1 < spw || s + 1 < 64;
             if (more) An.load_global(T, sSlot[k + 1 < spw ? s * cpc + w0 + k + 1 : (s + 1) * cpc + w0]);
             const uint32_t slot = s * cpc + w0 + k, p = sSlot[slot];
+            BN_ASSERT(p < P && slot < 64 * cpc);
             const long long mine = A.sum_bits(sbits, L, p, off);
             if (mode && !(k & 1)) {
                 prev = mine;
@@ -2039,6 +2057,7 @@ __global__ void __launch_bounds__(BN_FG_THREADS, BN_FG_MINB) k_finish_gather(uin
                 : perm    ? paper_partner(perm, invperm, paper_key(seed, pass_next, P), budget, p)
                           : swap_partner(L, seed, pass_next, p);
         q = __shfl_sync(0xffffffffu, q, 0);
+        BN_ASSERT(q < P);
         const bool a = acc[q] != 0;
         const uint4* src = reinterpret_cast<const uint4*>((a ? cn : c) + (size_t)q * rowB);
         uint4* dst = reinterpret_cast<uint4*>(cn2 + (size_t)p * rowB);
@@ -2166,12 +2185,14 @@ __global__ void __launch_bounds__(544, 1) k_pass_tail(uint32_t pass_t, uint64_t 
         const uint32_t s = u / cpu_, m = (u - s * cpu_) * hw + warp;
         if (warp >= hw || m >= M) continue;
         const uint32_t q = class_pixel_tab(sD, L, pass_t, s, m);
+        BN_ASSERT(q < P && s < 64);
         const bool a = __ldcg(acc + q) != 0;
         const uint4* src = reinterpret_cast<const uint4*>((a ? cn : c) + (size_t)q * rowB);
         uint32_t p2 = 0;
         if (gather_next) {
             if (lane == 0) p2 = swap_partner(L, seed, pass_t + 1, q);
             p2 = __shfl_sync(0xffffffffu, p2, 0);
+            BN_ASSERT(p2 < P);
         }
         uint4* dst_c = reinterpret_cast<uint4*>(c + (size_t)q * rowB);
         uint4* dst_n = reinterpret_cast<uint4*>(cn2 + (size_t)p2 * rowB);
