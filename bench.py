@@ -264,7 +264,7 @@ def pass_dram(cfg, ms_per_pass, peaks, kernels):
     gbs = total / (ms_per_pass / 1e3) / 1e9
     peak = peaks.get("hbm_gbs", 6650.0)
     return {"bytes_per_pass": total, "per_kernel": parts, "achieved_GBs": gbs, "peak_GBs": peak, "frac": gbs / peak,
-            "source": TRAFFIC_FILE}
+            "source": os.path.relpath(TRAFFIC_FILE, ROOT)}
 
 
 def host_cpu():

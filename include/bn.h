@@ -216,7 +216,7 @@ enum bn_kernel_id {
     BN_K_DECIDE = 4, /* colour-class decisions                        */
     BN_K_STATS = 5,  /* exact per-pass reductions                     */
     BN_K_COMMIT = 6, /* commit accepted rows / shifts                 */
-    BN_K_TAIL = 7,   /* fused pass tail: dE terms + decisions + commit (SWAP, L <= 128) */
+    BN_K_TAIL = 7,   /* fused pass tail: decisions + commit / next gather (SWAP, 64 <= L <= 128) */
     BN_K_COUNT_IDS = 8
 };
 int bn_profile_enable(bn_ctx *ctx, int enable);

@@ -858,7 +858,7 @@ int launch_pass_tail(bn_ctx* ctx, uint32_t t, uint64_t seed, uint8_t* log, uint3
                      PassStatsDev* out, int check_prev, bool* done) {
     *done = false;
     const uint32_t nb = ctx->L / 8, M = nb * nb, P = ctx->P;
-    if (ctx->no_tail || nb > 16) return BN_OK;
+    if (ctx->no_tail || nb > 16 || nb < 8) return BN_OK;  // 64 <= L <= 128 (C1-size tiles: measured slower)
     uint32_t cpc = 16;
     while (cpc > M) cpc /= 2;
     const uint32_t ncta = M / cpc;
@@ -890,7 +890,9 @@ int launch_pass_tail(bn_ctx* ctx, uint32_t t, uint64_t seed, uint8_t* log, uint3
         }
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
-        const int cap = nsm / (int)ncta;  // one CTA per SM at most
+        int cap = nsm / (int)ncta;  // one CTA per SM at most
+        const char* tcl = getenv("BN_TAIL_CLUSTERS");  // cap (A/B measurements, concurrent contexts)
+        if (tcl && atoi(tcl) >= 2) cap = std::min(cap, atoi(tcl));
         ctx->tail_clusters = ncl < cap ? ncl : cap;
     }
     if (ctx->tail_clusters < 2) return BN_OK;
@@ -1484,7 +1486,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             if (rowflags && pi > 0) CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evC, 0));
             return BN_OK;
         };
-        if (prm->mode == BN_SWAP && !ctx->no_tail && ctx->tail_clusters != 0 && ctx->L <= 128) {
+        if (prm->mode == BN_SWAP && !ctx->no_tail && ctx->tail_clusters != 0 && ctx->L <= 128 && ctx->L >= 64) {
             // fused pass tail: Gram (+ exchange), then dE terms, decisions and commit in one launch
             uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
             const bool nxt = fuse && pi + 1 < prm->passes;
