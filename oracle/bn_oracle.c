@@ -671,3 +671,113 @@ int orc_error_spectrum(const orc_problem *pb, const uint8_t *c, uint32_t l, doub
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * Smooth (low-frequency) test integrands -- evaluation only (§3.5
+ * l.309-313 "achieves blue-noise distribution of integrand noise even for low frequency
+ * integrands"; a Gaussian-bump family used only to EVALUATE a tile
+ * optimised on Heavisides, with exact references by separable error-function products).
+ *   f(x, y) = exp(-(x - cx)^2 / (2 sx^2) - (y - cy)^2 / (2 sy^2))      on [0,1)^2
+ *   I       = X(cx, sx) X(cy, sy),  X(c, s) = s sqrt(pi/2) (erf((1 - c)/(s sqrt 2)) + erf(c/(s sqrt 2)))
+ *   e_i(p)  = 1/N sum_{k<N} f_i(s^k_p) - I_i       (the pixel's estimate error, fp64)
+ * bumps: [nb][4] = (cx, cy, sx, sy).
+ * ---------------------------------------------------------------------------------------- */
+static double erf_axis(double c, double s) {
+    const double r2 = 1.4142135623730950488016887242097;
+    return s * 1.2533141373155002512078826424055 * (erf((1.0 - c) / (s * r2)) + erf(c / (s * r2)));
+}
+double orc_bump_integral(double cx, double cy, double sx, double sy) { return erf_axis(cx, sx) * erf_axis(cy, sy); }
+
+int orc_smooth_errors(const orc_problem *pb, const uint32_t *U, uint32_t l, uint32_t nb, const double *bumps,
+                      double *e /* [nb][P] */) {
+    const uint32_t L = pb->L, P = L * L;
+    if (l >= pb->n_levels || nb == 0) return -1;
+    const uint32_t N = pb->levels[l];
+    for (uint32_t i = 0; i < nb; ++i) {
+        const double cx = bumps[4 * i], cy = bumps[4 * i + 1], sx = bumps[4 * i + 2], sy = bumps[4 * i + 3];
+        if (!(sx > 0) || !(sy > 0)) return -1;
+        const double ref = orc_bump_integral(cx, cy, sx, sy);
+        for (uint32_t p = 0; p < P; ++p) {
+            double acc = 0.0;
+            for (uint32_t k = 0; k < N; ++k) {
+                uint32_t xy[2];
+                orc_sample(pb->d1, pb->d2, U[2 * p], U[2 * p + 1], k, xy);
+                const double x = (double)xy[0] / 4294967296.0, y = (double)xy[1] / 4294967296.0;
+                acc += exp(-(x - cx) * (x - cx) / (2.0 * sx * sx) - (y - cy) * (y - cy) / (2.0 * sy * sy));
+            }
+            e[(size_t)i * P + p] = acc / (double)N - ref;
+        }
+    }
+    return 0;
+}
+
+/* The evaluation criterion (§3.3) on error images e[ni][P] (same definitions as
+ * orc_denoised_rmse / orc_error_spectrum, which form the images from counts). */
+int orc_denoised_rmse_images(uint32_t L, uint32_t ni, const double *e, const double *sigmas, uint32_t n_sigmas,
+                             double *rmse) {
+    const uint32_t P = L * L;
+    for (uint32_t s = 0; s < n_sigmas; ++s) {
+        int r = (int)ceil(4.0 * sigmas[s]);
+        int kw = 2 * r + 1;
+        double *k = malloc(sizeof(double) * kw * kw);
+        if (orc_gauss_kernel(sigmas[s], k, kw * kw) < 0) { free(k); return -1; }
+        double acc = 0.0;
+        for (uint32_t i = 0; i < ni; ++i) {
+            double ss = 0.0;
+            for (uint32_t y = 0; y < L; ++y)
+                for (uint32_t x = 0; x < L; ++x) {
+                    double v = 0.0;   /* (e (*) k_sigma)(p) */
+                    for (int dy = -r; dy <= r; ++dy)
+                        for (int dx = -r; dx <= r; ++dx) {
+                            uint32_t q = wrap((int64_t)y + dy, L) * L + wrap((int64_t)x + dx, L);
+                            v += k[(dy + r) * kw + (dx + r)] * e[(size_t)i * P + q];
+                        }
+                    ss += v * v;
+                }
+            acc += sqrt(ss / (double)P);
+        }
+        rmse[s] = acc / (double)ni;
+        free(k);
+    }
+    return 0;
+}
+
+int orc_error_spectrum_images(uint32_t L, uint32_t ni, const double *e, double *S /* [ky][kx] */,
+                              double *profile /* [L/2] or NULL */) {
+    const uint32_t P = L * L;
+    const double two_pi = 6.283185307179586476925286766559;
+    memset(S, 0, sizeof(double) * P);
+    for (uint32_t i = 0; i < ni; ++i) {
+        const double *ei = e + (size_t)i * P;
+        double mean = 0.0;
+        for (uint32_t p = 0; p < P; ++p) mean += ei[p];
+        mean /= (double)P;
+        for (uint32_t ky = 0; ky < L; ++ky)
+            for (uint32_t kx = 0; kx < L; ++kx) {
+                double re = 0.0, im = 0.0;
+                for (uint32_t y = 0; y < L; ++y)
+                    for (uint32_t x = 0; x < L; ++x) {
+                        double ph = -two_pi * (double)((kx * x + ky * y) % L) / (double)L;
+                        re += (ei[y * L + x] - mean) * cos(ph);
+                        im += (ei[y * L + x] - mean) * sin(ph);
+                    }
+                S[ky * L + kx] += (re * re + im * im) / (double)ni;
+            }
+    }
+    if (profile) {
+        double *sum = calloc(L / 2, sizeof(double));
+        uint32_t *cnt = calloc(L / 2, sizeof(uint32_t));
+        for (uint32_t ky = 0; ky < L; ++ky)
+            for (uint32_t kx = 0; kx < L; ++kx) {
+                int fx = kx <= L / 2 ? (int)kx : (int)kx - (int)L;
+                int fy = ky <= L / 2 ? (int)ky : (int)ky - (int)L;
+                int j = (int)floor(sqrt((double)(fx * fx + fy * fy)));
+                if (j < 1 || j > (int)L / 2) continue;
+                sum[j - 1] += S[ky * L + kx];
+                cnt[j - 1] += 1;
+            }
+        for (uint32_t j = 0; j < L / 2; ++j) profile[j] = cnt[j] ? sum[j] / cnt[j] : 0.0;
+        free(sum); free(cnt);
+    }
+    return 0;
+}

@@ -120,6 +120,17 @@ def lib():
                                             ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
                                             ctypes.c_void_p, ctypes.c_void_p]
         _lib.orc_paper_optimize.restype = ctypes.c_int
+        _lib.orc_bump_integral.argtypes = [ctypes.c_double] * 4
+        _lib.orc_bump_integral.restype = ctypes.c_double
+        _lib.orc_smooth_errors.argtypes = [P(Problem), ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                                           ctypes.c_void_p]
+        _lib.orc_smooth_errors.restype = ctypes.c_int
+        _lib.orc_denoised_rmse_images.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                                                  ctypes.c_uint32, ctypes.c_void_p]
+        _lib.orc_denoised_rmse_images.restype = ctypes.c_int
+        _lib.orc_error_spectrum_images.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p,
+                                                   ctypes.c_void_p]
+        _lib.orc_error_spectrum_images.restype = ctypes.c_int
     return _lib
 
 
@@ -187,6 +198,33 @@ def gauss_kernel(sigma: float) -> np.ndarray:
 def iref(a: int, b: int, px: int, py: int) -> float:
     """Exact half-plane area inside [0,1]^2 (teaser 'I_ref')."""
     return lib().orc_iref(a, b, px, py)
+
+
+def bump_integral(cx: float, cy: float, sx: float, sy: float) -> float:
+    """Exact integral over [0,1]^2 of the Gaussian bump (separable erf product)."""
+    return lib().orc_bump_integral(cx, cy, sx, sy)
+
+
+def denoised_rmse_images(e: np.ndarray, sigmas) -> np.ndarray:
+    """Evaluation criterion (§3.3) on error images e[ni][L][L] (plain convolution)."""
+    e = np.ascontiguousarray(e, dtype=np.float64)
+    ni, L = e.shape[0], e.shape[-1]
+    sg = np.ascontiguousarray(sigmas, dtype=np.float64)
+    out = np.zeros(len(sg), np.float64)
+    if lib().orc_denoised_rmse_images(L, ni, e.ctypes.data, sg.ctypes.data, len(sg), out.ctypes.data):
+        raise ValueError("bad arguments")
+    return out
+
+
+def error_spectrum_images(e: np.ndarray):
+    """(S [L, L] mean power spectrum of the mean-subtracted images, radial profile [L/2])."""
+    e = np.ascontiguousarray(e, dtype=np.float64)
+    ni, L = e.shape[0], e.shape[-1]
+    S = np.zeros((L, L), np.float64)
+    prof = np.zeros(L // 2, np.float64)
+    if lib().orc_error_spectrum_images(L, ni, e.ctypes.data, S.ctypes.data, prof.ctypes.data):
+        raise ValueError("bad arguments")
+    return S, prof
 
 
 @dataclass
@@ -265,6 +303,16 @@ class OracleProblem:
         sg = np.ascontiguousarray(sigmas, dtype=np.float64)
         out = np.zeros(len(sg), np.float64)
         if lib().orc_denoised_rmse(self.ref(), c.ctypes.data, level, sg.ctypes.data, len(sg), out.ctypes.data):
+            raise ValueError("bad arguments")
+        return out
+
+    def smooth_errors(self, U: np.ndarray, level: int, bumps) -> np.ndarray:
+        """Errors e_i(p) [nb][L][L] of the Gaussian-bump integrands (cx, cy, sx, sy) at progressive
+        level `level` of the tile U: 1/N sum_k f_i(s^k_p) - I_i (§3.5 l.309-313)."""
+        U = np.ascontiguousarray(U, dtype=np.uint32).reshape(-1, 2)
+        bm = np.ascontiguousarray(bumps, dtype=np.float64).reshape(-1, 4)
+        out = np.zeros((len(bm), self.L, self.L), np.float64)
+        if lib().orc_smooth_errors(self.ref(), U.ctypes.data, level, len(bm), bm.ctypes.data, out.ctypes.data):
             raise ValueError("bad arguments")
         return out
 

@@ -57,6 +57,16 @@ def make_permutation(P: int, seed: int) -> np.ndarray:
     return rng.permutation(P).astype(np.uint32)
 
 
+def make_bumps(n: int, seed: int) -> np.ndarray:
+    """Smooth (low-frequency) evaluation integrands, Gaussian bumps [n][4] = (cx, cy, sx, sy)
+    (§3.5 l.309-313; evaluation only).  Reading R34: centres uniform in
+    [0,1)^2, widths i.i.d. log-uniform in [0.05, 0.25]."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    c = rng.random((n, 2))
+    w = np.exp(rng.uniform(np.log(0.05), np.log(0.25), size=(n, 2)))
+    return np.ascontiguousarray(np.concatenate([c, w], axis=1), dtype=np.float64)
+
+
 def axis_cut_bank(N: int, js, axis: str = "x"):
     """Lattice-aligned axis steps f = [x >= j/N] (or y): the exact-integral pin bank."""
     js = np.asarray(js, dtype=np.int64)
