@@ -180,6 +180,19 @@ int bn_check(bn_ctx *ctx);
 int bn_eval_quality(bn_ctx *ctx, uint32_t level, const double *sigmas, uint32_t n_sigmas,
                     double *rmse, double *spectrum, double *profile);
 
+/* The same criterion for the smooth (low-frequency) evaluation integrands (§3.5
+ * l.309-313 "blue-noise distribution of integrand noise even for low frequency integrands";
+ * SURVEY §8 f4; used to evaluate a tile optimised on Heavisides, never to optimise):
+ *   f_i(x, y) = exp(-(x - cx)^2 / (2 sx^2) - (y - cy)^2 / (2 sy^2)),  bumps [n_bumps][4] = (cx, cy, sx, sy)
+ *   e_i(p)    = 1/N_l sum_{k < N_l} f_i(s^k_p) - I_i   (fp64 at the tile's samples),
+ *   I_i       = the exact integral over [0,1]^2 (separable erf product, host libm), also returned
+ *               in iref [n_bumps] if non-NULL;
+ * rmse / spectrum / profile as bn_eval_quality over the n_bumps error images.  Host outputs;
+ * synchronises.  EINVAL on level >= n_levels, no bumps, a width <= 0 or not finite, bad sigmas or
+ * L > 256. */
+int bn_eval_smooth(bn_ctx *ctx, uint32_t level, uint32_t n_bumps, const double *bumps, const double *sigmas,
+                   uint32_t n_sigmas, double *rmse, double *spectrum, double *profile, double *iref);
+
 /* Precomputed permutation of the pixel indices used by BN_PAPER_SWAP (PAPER.md l.303-304:
  * "we precompute a permutation of pixel indices that we store in a linear array").
  * perm: host uint32 [n], n = L*L of the tile the optimiser will run on, every index in [0, n)

@@ -26,7 +26,7 @@ SYMBOLS = ("bn_create", "bn_destroy", "bn_last_error", "bn_version", "bn_set_lat
            "bn_get_references", "bn_set_energy", "bn_set_tile", "bn_get_tile", "bn_eval_counts", "bn_energy",
            "bn_optimize", "bn_comm_init", "bn_comm_unique_id", "bn_launch_count", "bn_profile_enable",
            "bn_profile_get", "bn_window_distances", "bn_set_permutation",
-           "bn_set_energy_form", "bn_eval_quality", "bn_check")
+           "bn_set_energy_form", "bn_eval_quality", "bn_check", "bn_eval_smooth")
 KERNELS = ("counts", "gather", "gram", "lut", "decide", "stats", "commit", "tail")
 
 
@@ -77,6 +77,7 @@ def load_library(path: str = LIB_PATH):
         "bn_comm_init": ([vp, vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "bn_comm_unique_id": ([vp], ctypes.c_int),
         "bn_check": ([vp], ctypes.c_int),
+        "bn_eval_smooth": ([vp, u32, u32, vp, vp, u32, vp, vp, vp, vp], ctypes.c_int),
         "bn_launch_count": ([vp], u64),
         "bn_profile_enable": ([vp, ctypes.c_int], ctypes.c_int),
         "bn_window_distances": ([vp, vp, ctypes.c_int], ctypes.c_int),
@@ -252,6 +253,22 @@ class Sampler:
                                               S.ctypes.data if S is not None else None,
                                               prof.ctypes.data if prof is not None else None))
         return r, S, prof
+
+    def eval_smooth(self, bumps, level: int = 0, sigmas=None, spectrum: bool = True):
+        """Evaluation criterion for the smooth Gaussian-bump integrands (§3.5): (denoised RMSE
+        per sigma, spectrum [L, L] or None, radial profile [L/2] or None, exact references [n]).
+        bumps: [n][4] = (cx, cy, sx, sy); default sigmas: 16 log-spaced in [0.25, 20]."""
+        bm = np.ascontiguousarray(bumps, dtype=np.float64).reshape(-1, 4)
+        sg = np.geomspace(0.25, 20.0, 16) if sigmas is None else np.ascontiguousarray(sigmas, dtype=np.float64)
+        sg = np.ascontiguousarray(sg, dtype=np.float64)
+        r = np.zeros(len(sg), np.float64)
+        S = np.zeros((self.L, self.L), np.float64) if spectrum else None
+        prof = np.zeros(self.L // 2, np.float64) if spectrum else None
+        ref = np.zeros(len(bm), np.float64)
+        self._check(self._lib.bn_eval_smooth(self._ctx, level, len(bm), bm.ctypes.data, sg.ctypes.data, len(sg),
+                                             r.ctypes.data, S.ctypes.data if S is not None else None,
+                                             prof.ctypes.data if prof is not None else None, ref.ctypes.data))
+        return r, S, prof, ref
 
     def window_distances(self, out=None):
         """Partial (this bank shard) window distances D_l(p, p+o), [levels, P, H] int32,

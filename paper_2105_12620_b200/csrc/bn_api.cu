@@ -153,7 +153,7 @@ struct bn_ctx {
     DevBuf<unsigned long long> kpart;  // best-of-K partial window sums [M][8]
     DevBuf<unsigned int> kticket;
     DevBuf<double2> ev_tw, ev_X1;  // bn_eval_quality work buffers
-    DevBuf<double> ev_h, ev_rm, ev_sp, ev_out;  // BN_PAPER_SWAP: precomputed permutation, per-pass partner map
+    DevBuf<double> ev_h, ev_rm, ev_sp, ev_out, ev_bump, ev_img;  // BN_PAPER_SWAP: precomputed permutation, per-pass partner map
     uint32_t perm_n = 0;
     DevBuf<int4> Dt;
     DevBuf<longlong2> d0;        // int64 dE terms {delta0, delta1} per (pixel, offset) (DT_ESC = see escape tables)
@@ -1135,7 +1135,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->d0.release(); ctx->x0.release(); ctx->x1.release(); ctx->dEp.release(); ctx->Epart.release(); ctx->pstats.release(); ctx->fparts.release(); ctx->ticket.release();
         ctx->W.release(); ctx->G.release(); ctx->iref.release(); ctx->perm.release(); ctx->part.release(); ctx->invperm.release(); ctx->cnK.release(); ctx->UnK.release(); ctx->nnK.release(); ctx->kpart.release(); ctx->kticket.release();
         ctx->ev_tw.release(); ctx->ev_X1.release(); ctx->ev_h.release(); ctx->ev_rm.release(); ctx->ev_sp.release();
-        ctx->ev_out.release();
+        ctx->ev_out.release(); ctx->ev_bump.release(); ctx->ev_img.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release(); ctx->rows_done.release();
         ctx->noff.release(); ctx->nrng.release(); ctx->tailc.release();
@@ -1592,24 +1592,21 @@ int bn_check(bn_ctx* ctx) {
     return read_err_flag(ctx);
 }
 
-int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t ns, double* rmse, double* spectrum,
-                    double* profile) {
-    if (!ctx) return BN_EINVAL;
-    int rc;
-    if ((rc = check_ready(ctx))) return rc;
-    if (level >= ctx->nl) return fail(ctx, BN_EINVAL, "level %u >= %u levels", level, ctx->nl);
-    if (ns > 64 || (ns && (!sigmas || !rmse))) return fail(ctx, BN_EINVAL, "bad sigma list (at most 64)");
-    for (uint32_t s = 0; s < ns; ++s)
-        if (!(sigmas[s] > 0) || !std::isfinite(sigmas[s]) || sigmas[s] > 1e4)
-            return fail(ctx, BN_EINVAL, "sigma[%u] = %g outside (0, 1e4]", s, sigmas[s]);
-    const uint32_t L = ctx->L, P = ctx->P, Ts = ctx->Ts;
-    if (L > 256) return fail(ctx, BN_EINVAL, "bn_eval_quality supports L <= 256 (L = %u)", L);
-    DeviceGuard g(ctx->dev);
-    if ((rc = ensure_counts(ctx))) return rc;
-    const uint8_t* rows = u8_rows(ctx);
-    CUDA_TRY(ctx->iref.ensure(Ts));
-    k_iref<<<(Ts + 127) / 128, 128, 0, ctx->stream>>>(ctx->ab.p, ctx->pxy.p, Ts, ctx->iref.p);
-    LAUNCHED();
+}  // extern "C"
+
+namespace {
+// The evaluation criterion's pipeline (§3.3): row DFT, column DFT + power + Parseval sums
+// per sigma, fixed-order reductions.  Error images from the counts of `level` (img == nullptr) or
+// given on the device (img [ni][P], the smooth family).
+int eval_pipeline(bn_ctx* ctx, uint32_t level, uint32_t ni, const double* img, const double* sigmas, uint32_t ns,
+                  double* rmse, double* spectrum, double* profile) {
+    const uint32_t L = ctx->L, P = ctx->P;
+    const uint8_t* rows = img ? nullptr : u8_rows(ctx);
+    if (!img) {
+        CUDA_TRY(ctx->iref.ensure(ctx->Ts));
+        k_iref<<<(ctx->Ts + 127) / 128, 128, 0, ctx->stream>>>(ctx->ab.p, ctx->pxy.p, ctx->Ts, ctx->iref.p);
+        LAUNCHED();
+    }
     // twiddles w^m = exp(-2 pi i m / L) and the 1D kernel spectra h_s(k) = sum_d g(d) cos(2 pi k d / L) / sum_d g(d)
     // (g = exp(-d^2 / (2 sigma^2)), |d| <= ceil(4 sigma)): host libm, like the energy tables
     const double two_pi = 6.283185307179586476925286766559;
@@ -1629,11 +1626,11 @@ int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t 
             h[(size_t)s * L + k] = acc / Z;
         }
     }
-    const uint32_t chunk = 1024, ngroups = (Ts + EV_II - 1) / EV_II;
+    const uint32_t chunk = 1024, ngroups = (ni + EV_II - 1) / EV_II;
     CUDA_TRY(ctx->ev_tw.ensure(L));
     CUDA_TRY(ctx->ev_h.ensure(h.size()));
-    CUDA_TRY(ctx->ev_X1.ensure((size_t)std::min(chunk, Ts) * P));
-    CUDA_TRY(ctx->ev_rm.ensure((size_t)Ts * L * nsk));
+    CUDA_TRY(ctx->ev_X1.ensure((size_t)std::min(chunk, ni) * P));
+    CUDA_TRY(ctx->ev_rm.ensure((size_t)ni * L * nsk));
     CUDA_TRY(ctx->ev_sp.ensure((size_t)ngroups * P));
     CUDA_TRY(ctx->ev_out.ensure(64 + P + L / 2));
     CUDA_TRY(cudaMemcpyAsync(ctx->ev_tw.p, tw.data(), L * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
@@ -1642,11 +1639,11 @@ int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t 
     CUDA_TRY(cudaFuncSetAttribute(k_ev_dft_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
     CUDA_TRY(cudaFuncSetAttribute(k_ev_dft_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
     const double invN = 1.0 / (double)ctx->levels[level];
-    for (uint32_t i0 = 0; i0 < Ts; i0 += chunk) {
-        const uint32_t ci = std::min(chunk, Ts - i0);
+    for (uint32_t i0 = 0; i0 < ni; i0 += chunk) {
+        const uint32_t ci = std::min(chunk, ni - i0);
         const dim3 grid(L, (ci + EV_II - 1) / EV_II);
         k_ev_dft_rows<<<grid, 256, sm1, ctx->stream>>>(rows, L, ctx->rowB, level * ctx->Tp, invN, ctx->iref.p, i0,
-                                                        ci, ctx->ev_tw.p, ctx->ev_X1.p);
+                                                        ci, ctx->ev_tw.p, ctx->ev_X1.p, img);
         LAUNCHED();
         k_ev_dft_cols<<<grid, 256, sm2, ctx->stream>>>(ctx->ev_X1.p, L, i0, ci, ctx->ev_tw.p, ctx->ev_h.p, nsk,
                                                         ctx->ev_rm.p, ctx->ev_sp.p);
@@ -1656,12 +1653,12 @@ int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t 
     double* dS = dr + 64;
     double* dprof = dS + P;
     if (ns) {
-        k_ev_rmse<<<ns, 256, 0, ctx->stream>>>(ctx->ev_rm.p, L, Ts, nsk, dr);
+        k_ev_rmse<<<ns, 256, 0, ctx->stream>>>(ctx->ev_rm.p, L, ni, nsk, dr);
         LAUNCHED();
         CUDA_TRY(cudaMemcpyAsync(rmse, dr, ns * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     }
     if (spectrum || profile) {
-        k_ev_spectrum<<<1, 256, 0, ctx->stream>>>(ctx->ev_sp.p, L, ngroups, Ts, dS, dprof);
+        k_ev_spectrum<<<1, 256, 0, ctx->stream>>>(ctx->ev_sp.p, L, ngroups, ni, dS, dprof);
         LAUNCHED();
         if (spectrum) CUDA_TRY(cudaMemcpyAsync(spectrum, dS, (size_t)P * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         if (profile)
@@ -1669,6 +1666,64 @@ int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t 
     }
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return BN_OK;
+}
+
+int check_eval_args(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t ns, const double* rmse) {
+    int rc;
+    if ((rc = check_ready(ctx))) return rc;
+    if (level >= ctx->nl) return fail(ctx, BN_EINVAL, "level %u >= %u levels", level, ctx->nl);
+    if (ns > 64 || (ns && (!sigmas || !rmse))) return fail(ctx, BN_EINVAL, "bad sigma list (at most 64)");
+    for (uint32_t s = 0; s < ns; ++s)
+        if (!(sigmas[s] > 0) || !std::isfinite(sigmas[s]) || sigmas[s] > 1e4)
+            return fail(ctx, BN_EINVAL, "sigma[%u] = %g outside (0, 1e4]", s, sigmas[s]);
+    if (ctx->L > 256) return fail(ctx, BN_EINVAL, "the evaluation criterion supports L <= 256 (L = %u)", ctx->L);
+    return BN_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int bn_eval_quality(bn_ctx* ctx, uint32_t level, const double* sigmas, uint32_t ns, double* rmse, double* spectrum,
+                    double* profile) {
+    if (!ctx) return BN_EINVAL;
+    int rc;
+    if ((rc = check_eval_args(ctx, level, sigmas, ns, rmse))) return rc;
+    DeviceGuard g(ctx->dev);
+    if ((rc = ensure_counts(ctx))) return rc;
+    return eval_pipeline(ctx, level, ctx->Ts, nullptr, sigmas, ns, rmse, spectrum, profile);
+}
+
+int bn_eval_smooth(bn_ctx* ctx, uint32_t level, uint32_t n_bumps, const double* bumps, const double* sigmas,
+                   uint32_t ns, double* rmse, double* spectrum, double* profile, double* iref) {
+    if (!ctx) return BN_EINVAL;
+    int rc;
+    if ((rc = check_eval_args(ctx, level, sigmas, ns, rmse))) return rc;
+    if (n_bumps == 0 || !bumps) return fail(ctx, BN_EINVAL, "empty bump list");
+    std::vector<double> ref(n_bumps);
+    const double r2 = 1.4142135623730950488016887242097, sqrt_half_pi = 1.2533141373155002512078826424055;
+    for (uint32_t i = 0; i < n_bumps; ++i) {
+        const double cx = bumps[4 * i], cy = bumps[4 * i + 1], sx = bumps[4 * i + 2], sy = bumps[4 * i + 3];
+        if (!(sx > 0) || !(sy > 0) || !std::isfinite(sx) || !std::isfinite(sy) || !std::isfinite(cx) || !std::isfinite(cy))
+            return fail(ctx, BN_EINVAL, "bump %u: widths must be positive and finite", i);
+        // exact reference: separable erf product over [0,1]^2 (host libm)
+        ref[i] = sx * sqrt_half_pi * (std::erf((1.0 - cx) / (sx * r2)) + std::erf(cx / (sx * r2))) *
+                 (sy * sqrt_half_pi * (std::erf((1.0 - cy) / (sy * r2)) + std::erf(cy / (sy * r2))));
+    }
+    if (iref) memcpy(iref, ref.data(), n_bumps * sizeof(double));
+    DeviceGuard g(ctx->dev);
+    const uint32_t P = ctx->P;
+    CUDA_TRY(ctx->ev_bump.ensure((size_t)n_bumps * 5));
+    CUDA_TRY(ctx->ev_img.ensure((size_t)n_bumps * P));
+    double* dref = ctx->ev_bump.p + 4 * (size_t)n_bumps;
+    CUDA_TRY(cudaMemcpyAsync(ctx->ev_bump.p, bumps, (size_t)n_bumps * 4 * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(dref, ref.data(), n_bumps * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    const size_t n = (size_t)n_bumps * P;
+    k_ev_smooth_err<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+        ctx->U.p, ctx->S.p, ctx->levels[level], reinterpret_cast<const double4*>(ctx->ev_bump.p), dref, n_bumps, P,
+        ctx->ev_img.p);
+    LAUNCHED();
+    return eval_pipeline(ctx, level, n_bumps, ctx->ev_img.p, sigmas, ns, rmse, spectrum, profile);
 }
 
 int bn_set_permutation(bn_ctx* ctx, const uint32_t* perm, uint32_t n) {

@@ -1890,7 +1890,7 @@ constexpr int EV_II = 32;  // integrands per CTA
 __global__ void __launch_bounds__(256) k_ev_dft_rows(const uint8_t* __restrict__ c, uint32_t L, uint32_t rowB,
                                                      uint32_t loff, double invN, const double* __restrict__ iref,
                                                      uint32_t i0, uint32_t ni, const double2* __restrict__ tw,
-                                                     double2* __restrict__ X1) {
+                                                     double2* __restrict__ X1, const double* __restrict__ img) {
     extern __shared__ double ev_smem[];
     double* E = ev_smem;                                         // [L][EV_II]
     double2* w = reinterpret_cast<double2*>(E + (size_t)L * EV_II);  // [L]
@@ -1898,7 +1898,10 @@ __global__ void __launch_bounds__(256) k_ev_dft_rows(const uint8_t* __restrict__
     for (uint32_t j = threadIdx.x; j < L; j += blockDim.x) w[j] = tw[j];
     for (uint32_t j = threadIdx.x; j < L * EV_II; j += blockDim.x) {
         const uint32_t x = j / EV_II, ii = j % EV_II, i = ic + ii;
-        E[j] = i < ni ? (double)c[(size_t)(y * L + x) * rowB + loff + i0 + i] * invN - iref[i0 + i] : 0.0;
+        // error image: from the counts (c / N - I_ref) or given (img [ni][P], the smooth family)
+        E[j] = i >= ni ? 0.0
+               : img  ? img[(size_t)(i0 + i) * L * L + y * L + x]
+                      : (double)c[(size_t)(y * L + x) * rowB + loff + i0 + i] * invN - iref[i0 + i];
     }
     __syncthreads();
     for (uint32_t o = threadIdx.x; o < L * EV_II; o += blockDim.x) {
@@ -2631,6 +2634,28 @@ __global__ void __launch_bounds__(256) k_narrow_unpack(const uint8_t* __restrict
         nrm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nrm);
         if (lane == 0) norms[(size_t)p * nl + l] = nrm;
     }
+}
+
+// Smooth evaluation integrands (§3.5 l.309-313): the estimate error of
+// every (bump i, pixel p) at N samples, e = 1/N sum_k exp(-(x_k - cx)^2/(2 sx^2) - (y_k - cy)^2/(2 sy^2))
+// - I_i, samples x_k = ((s^k.x + u_p.x) mod 2^32) 2^-32 in fp64; I_i host-built (erf products).
+__global__ void __launch_bounds__(256) k_ev_smooth_err(const uint2* __restrict__ U, const uint2* __restrict__ S,
+                                                       uint32_t N, const double4* __restrict__ bumps,
+                                                       const double* __restrict__ ref, uint32_t nb, uint32_t P,
+                                                       double* __restrict__ out) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (size_t)nb * P) return;
+    const uint32_t i = (uint32_t)(t / P), p = (uint32_t)(t - (size_t)i * P);
+    const double4 b = bumps[i];
+    const double ax = 2.0 * b.z * b.z, ay = 2.0 * b.w * b.w;
+    const uint2 u = U[p];
+    double acc = 0.0;
+    for (uint32_t k = 0; k < N; ++k) {
+        const uint2 sk = S[k];
+        const double x = (double)(sk.x + u.x) * 2.3283064365386963e-10, y = (double)(sk.y + u.y) * 2.3283064365386963e-10;
+        acc += exp(-(x - b.x) * (x - b.x) / ax - (y - b.y) * (y - b.y) / ay);
+    }
+    out[t] = acc / (double)N - ref[i];
 }
 
 // Accept-log scatter is written directly by k_decide.

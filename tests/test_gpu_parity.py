@@ -385,6 +385,36 @@ def test_eval_quality_after_gpu_passes(bn, oracle_mod):
         s.eval_quality(0, [0.0])
 
 
+@pytest.mark.parametrize("L,T,levels,level,nb", [(16, 8, (16,), 0, 5), (32, 20, (4, 16, 64), 2, 12),
+                                                  (64, 12, (16,), 0, 40)])
+def test_eval_smooth_parity(bn, oracle_mod, L, T, levels, level, nb):
+    """Smooth Gaussian-bump evaluation integrands (§3.5, f4): the GPU's denoised RMSE,
+    spectrum and profile equal the oracle's plain per-sample estimates + convolution / DFT."""
+    s, o, U = make(bn, oracle_mod, L, T, levels)
+    bumps = synth.make_bumps(nb, L + nb)
+    sig = [0.25, 1.0, 2.0, 6.0]
+    r, S, prof, ref = s.eval_smooth(bumps, level, sig)
+    e = o.smooth_errors(U, level, bumps)
+    np.testing.assert_allclose(ref, [oracle_mod.bump_integral(*b) for b in bumps], rtol=1e-14)
+    np.testing.assert_allclose(r, oracle_mod.denoised_rmse_images(e, sig), rtol=1e-9)
+    So, po = oracle_mod.error_spectrum_images(e)
+    np.testing.assert_allclose(S, So, rtol=1e-8, atol=1e-12 * So.max())
+    np.testing.assert_allclose(prof, po, rtol=1e-8, atol=1e-12 * po.max())
+    with pytest.raises(bn.BNError):
+        s.eval_smooth(np.array([[0.5, 0.5, 0.0, 0.1]]), level, sig)
+
+
+def test_eval_smooth_versatility_on_gpu_tiles(bn, oracle_mod):
+    """PAPER.md §3.5: a tile optimised on Heavisides only (GPU SWAP passes) has lower low-frequency
+    error power for the smooth family than the random tile (SPEC acceptance 8: <= 0.7x)."""
+    s, o, U = make(bn, oracle_mod, 64, 64, (16,))
+    bumps = synth.make_bumps(32, 3)
+    _, _, p0, _ = s.eval_smooth(bumps, 0, [2.0])
+    s.optimize(10, 2, mode=1, stats=False)
+    _, _, p1, _ = s.eval_smooth(bumps, 0, [2.0])
+    assert p1[:3].mean() <= 0.7 * p0[:3].mean()
+
+
 @pytest.mark.parametrize("decide", ["", "nobig"])
 @pytest.mark.parametrize("L,mode", [(256, 0), (256, 1), (512, 1)])
 def test_decide_large_tiles(bn, oracle_mod, monkeypatch, decide, L, mode):

@@ -4,8 +4,10 @@ For one tile problem it runs, on the GPU, the random initial tile ("random scram
 noise baseline of Fig. 1(c)) and the tiles left by P passes of each optimiser mode (greedy SWAP,
 paper-verbatim snapshot couples, greedy REDRAW), and reports the denoised-RMSE curve (16
 log-spaced sigmas in [0.25, 20]) and the radial error power profile of each, plus the time of the
-bn_eval_quality call.  The paper prints no numbers for this figure (parity unpinned); the output
-is the qualitative ordering.
+bn_eval_quality call.  With --smooth N it also evaluates every tile on N smooth Gaussian-bump
+integrands (§3.5 "even for low frequency integrands"; bn_eval_smooth), which no optimiser
+sees.  The paper prints no numbers for this figure (parity unpinned); the output is the
+qualitative ordering.
 
     python tools/eval_curve.py [--L 64] [--T 256] [--spp 16] [--passes 40] [--out profiles/...json]
 """
@@ -32,6 +34,7 @@ def main():
     ap.add_argument("--T", type=int, default=256)
     ap.add_argument("--spp", type=int, default=16)
     ap.add_argument("--passes", type=int, default=40)
+    ap.add_argument("--smooth", type=int, default=0, help="smooth Gaussian-bump evaluation integrands")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "eval_curve.json"))
     args = ap.parse_args()
     import torch
@@ -61,6 +64,12 @@ def main():
         dt = time.perf_counter() - t0
         res["curves"][name] = {"passes": passes, "E_before": E0, "E_after": s.energy()[1], "rmse": r.tolist(),
                                "radial_profile": prof.tolist(), "eval_ms": 1e3 * dt}
+        if args.smooth:
+            rs, _, ps, _ = s.eval_smooth(synth.make_bumps(args.smooth, 5), 0, sig)
+            res["curves"][name]["smooth"] = {"n_bumps": args.smooth, "bump_seed": 5, "rmse": rs.tolist(),
+                                             "radial_profile": ps.tolist()}
+            print(f"        smooth: rmse(1, 2, 5) = " + ", ".join(f"{rs[np.argmin(abs(sig - v))]:.3e}" for v in (1, 2, 5))
+                  + f"   low/mid power {np.mean(ps[:L // 16]) / np.mean(ps[L // 4:3 * L // 8]):.3f}", flush=True)
         s.close()
         print(f"{name:7s} passes {passes:4d}  E {E0:.1f} -> {res['curves'][name]['E_after']:.1f}  "
               f"rmse(0.25, 1, 2, 5, 20) = " + ", ".join(f"{r[np.argmin(abs(sig - v))]:.3e}" for v in (0.25, 1, 2, 5, 20))
