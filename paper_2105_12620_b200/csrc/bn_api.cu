@@ -191,6 +191,11 @@ struct bn_ctx {
     bool no_fuse = false;          // BN_FUSE=0: separate SWAP commit (k_finish) and gather kernels
     bool no_tail = false;          // BN_TAIL=0: separate decision and commit kernels (no k_pass_tail)
     uint32_t nEpart = 0;           // energy partials written by the last Gram / k_lut launch
+    DevBuf<uint16_t> border;       // block order of the Gram (wrapping blocks first)
+    uint32_t border_L = 0;
+    bool no_border = false;        // BN_GRAM_ORDER=raster: plain raster block order
+    DevBuf<unsigned int> gsched;   // Gram work counter + CTA exit counter (dynamic item scheduling)
+    bool static_sched = false;     // BN_GRAM_SCHED=static: round-robin items instead
 
     bool tail_attr_set[8] = {false};
     int tail_clusters = -1;        // clusters of the fused pass tail that fit (cached)
@@ -480,8 +485,31 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
     const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
     KSTART(BN_K_GRAM);
+    // block order: toroidally wrapping blocks (x0 = 0, x0 = L - 8, last block row) first
+    const uint32_t nbx = ctx->L / 8;
+    if (ctx->border_L != ctx->L && !ctx->no_border) {
+        std::vector<uint16_t> ord;
+        for (int pass = 0; pass < 2; ++pass)
+            for (uint32_t b = 0; b < nbx * nbx; ++b) {
+                const uint32_t bx = b % nbx, by = b / nbx;
+                const bool wraps = bx == 0 || bx == nbx - 1 || by == nbx - 1;
+                if (wraps == (pass == 0)) ord.push_back((uint16_t)b);
+            }
+        CUDA_TRY(ctx->border.ensure(ord.size()));
+        CUDA_TRY(cudaMemcpyAsync(ctx->border.p, ord.data(), ord.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        ctx->border_L = ctx->L;
+    }
+    // dynamic scheduling only pays when a CTA gets more than one item (C1: 128 items, ~1 us dearer)
+    const bool dyn = !ctx->static_sched && items > grid;
+    if (dyn && !ctx->gsched.p) {  // zero once; the kernel's last CTA re-zeroes it
+        CUDA_TRY(ctx->gsched.ensure(2));
+        CUDA_TRY(cudaMemsetAsync(ctx->gsched.p, 0, 2 * sizeof(unsigned int), ctx->ls));
+    }
     CUDA_TRY(launch_k(ctx, k_gram_tc4<R>, dim3(grid), dim3(tc3::THREADS), smem, ctx->ls, gm, ctx->nc.p, nn, ctx->L,
-                      ctx->Tp, ctx->nl, ctx->Dt.p, ctx->gram_rows, ctx->gram_rows_target));
+                      ctx->Tp, ctx->nl, ctx->Dt.p, ctx->gram_rows, ctx->gram_rows_target,
+                      (const uint16_t*)(ctx->no_border ? nullptr : ctx->border.p),
+                      dyn ? ctx->gsched.p : nullptr));
     LAUNCHED_K();
     return BN_OK;
 }
@@ -1082,6 +1110,10 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->no_cluster = dm && !strcmp(dm, "flags");
     ctx->swap_v3 = dm && !strcmp(dm, "swap3");
     ctx->no_big = dm && !strcmp(dm, "nobig");
+    const char* go = getenv("BN_GRAM_ORDER");
+    ctx->no_border = go && !strcmp(go, "raster");
+    const char* gs = getenv("BN_GRAM_SCHED");
+    ctx->static_sched = gs && !strcmp(gs, "static");
     const char* tl = getenv("BN_TAIL");
     ctx->no_tail = tl && !strcmp(tl, "0");
     // Nsight Compute cannot replay the cooperative cluster launch of the fused tail: under a
@@ -1138,7 +1170,7 @@ void bn_destroy(bn_ctx* ctx) {
         ctx->ev_out.release(); ctx->ev_bump.release(); ctx->ev_img.release();
         for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         ctx->Un2.release(); ctx->cn2.release(); ctx->nn2.release(); ctx->rows_done.release();
-        ctx->noff.release(); ctx->nrng.release(); ctx->tailc.release();
+        ctx->noff.release(); ctx->nrng.release(); ctx->tailc.release(); ctx->border.release(); ctx->gsched.release();
         if (ctx->nrng_host) cudaFreeHost(ctx->nrng_host);
         if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
         if (ctx->hp) cudaStreamSynchronize(ctx->hp), cudaStreamDestroy(ctx->hp);

@@ -746,7 +746,9 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                                                               uint32_t L, uint32_t Tp, uint32_t nl,
                                                               int4* __restrict__ Dt,
                                                               const unsigned int* __restrict__ rows_done,
-                                                              uint32_t rows_target) {
+                                                              uint32_t rows_target,
+                                                              const uint16_t* __restrict__ border,
+                                                              unsigned int* __restrict__ sched) {
     using tc3::NBR; using tc3::NBX; using tc3::GRP; using tc3::CH_ROWS; using tc3::NCHUNK; using tc3::N;
     using tc3::A_BYTES; using tc3::STAGE; using tc3::NSTAGE; using tc3::SCR;
     constexpr int RW = ru4(2 * R + 1), R0 = ru4(R), NV = RW > R + 1 + R0 ? RW : R + 1 + R0;
@@ -756,10 +758,12 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     uint8_t* gring = smem_raw + (sring - raw);
     int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);  // [4 warps][32][SCR]
     int* snorm = scratch + 4 * 32 * SCR;                              // [2][NBR][NBX], x from x0-8
-    __shared__ __align__(8) uint64_t bars[2 * NSTAGE + 4];
-    __shared__ uint32_t tmem_sh;
+    constexpr int IQ = 4;  // item ring (dynamic scheduling): producer -> MMA warp and epilogue
+    __shared__ __align__(8) uint64_t bars[2 * NSTAGE + 4 + 2 * IQ];
+    __shared__ uint32_t tmem_sh, sItem[IQ];
     const uint32_t b_full = (uint32_t)__cvta_generic_to_shared(&bars[0]);
     const uint32_t b_empty = b_full + 8 * NSTAGE, b_tfull = b_full + 16 * NSTAGE, b_tempty = b_tfull + 16;
+    const uint32_t i_full = b_tempty + 16, i_empty = i_full + 8 * IQ;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nbx = L / 8, nitems = nbx * nbx * nl, P = L * L;
     const uint32_t nk = Tp / 128;
@@ -771,6 +775,10 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
         for (int i = 0; i < 2; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_tfull + 8 * i) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(b_tempty + 8 * i) : "memory");
+        }
+        for (int i = 0; i < IQ; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(i_full + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(i_empty + 8 * i) : "memory");
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -786,9 +794,11 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     const uint32_t tmem = tmem_sh;
     // Items block-major (the levels of a block consecutive) so that the window distances written last
     // are whole pixels' rows, which k_lut (BN_LUT_REVERSE) reads first while they are still in L2.
+    // Block order `border` (host-built): the blocks whose chunks wrap the torus (more, smaller TMA
+    // boxes: the slowest items) first, so the static round-robin spreads them over the CTAs.
     auto item_xyl = [&](uint32_t it, uint32_t& x0, uint32_t& y0, uint32_t& l) {
         l = it % nl;
-        const uint32_t b = it / nl;
+        const uint32_t b = border ? (uint32_t)border[it / nl] : it / nl;
         x0 = 8 * (b % nbx);
         y0 = 8 * (b / nbx);
     };
@@ -809,11 +819,35 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
         asm volatile("fence.proxy.async.global;" ::: "memory");
     };
 
+    // Dynamic scheduling (sched != null): the producer claims the next item from the global counter
+    // sched[0] and hands it to the MMA warp and the epilogue through the ring sItem (slot full /
+    // empty mbarriers; the empty barrier collects the MMA warp's and the epilogue's release), so a CTA
+    // that drew slow (wrapping) items simply takes fewer; the last CTA resets the counters.  Static
+    // round robin (it = cta, cta + G, ...) otherwise.
+    auto next_item = [&](uint32_t j, uint32_t prev) -> uint32_t {  // j-th item of this CTA (consumer side)
+        if (!sched) return j == 0 ? blockIdx.x : prev + gridDim.x;
+        const uint32_t slot = j % IQ;
+        tc::mbar_wait(i_full + 8 * slot, (j / IQ) & 1);
+        return sItem[slot];
+    };
+    auto release_item = [&](uint32_t j) {
+        if (sched) mbar_arrive(i_empty + 8 * (j % IQ));
+    };
     if (warp == 4) {
         // --------------------------------------------------------------- TMA producer
         if (lane == 0) {
-            uint32_t g = 0;
-            for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+            uint32_t g = 0, j = 0;
+            for (uint32_t it = blockIdx.x;; ++j) {
+                if (sched) {
+                    const uint32_t slot = j % IQ;
+                    if (j >= (uint32_t)IQ) tc::mbar_wait(i_empty + 8 * slot, ((j / IQ) - 1) & 1);
+                    it = atomicAdd(sched, 1u);
+                    sItem[slot] = it;
+                    mbar_arrive(i_full + 8 * slot);  // release (CTA scope): sItem written first
+                } else if (j > 0) {
+                    it += gridDim.x;
+                }
+                if (it >= nitems) break;
                 uint32_t x0, y0, l;
                 item_xyl(it, x0, y0, l);
                 wait_rows(y0);
@@ -853,7 +887,11 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     } else if (warp == 5) {
         // --------------------------------------------------------------- UMMA issuer
         uint32_t g = 0, cc = 0;  // stage counter, chunk counter (accumulator ring)
-        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        for (uint32_t ji = 0, it = 0;; ++ji) {
+            it = next_item(ji, it);
+            __syncwarp();
+            if (lane == 0) release_item(ji);
+            if (it >= nitems) break;
             uint32_t x0, y0, l;
             item_xyl(it, x0, y0, l);
             const uint32_t f = gm.fmt[l];
@@ -891,12 +929,16 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
         const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
         int* scr = scratch + (warp * 32 + lane) * SCR;
         uint32_t cc = 0;
-        for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        for (uint32_t ji = 0, it = 0;; ++ji) {
+            it = next_item(ji, it);
+            named_bar(2, 128);  // every epilogue thread read the slot (and the previous item's norms are done)
+            if (threadIdx.x == 0) release_item(ji);
+            if (it >= nitems) break;
             uint32_t x0, y0, l;
             item_xyl(it, x0, y0, l);
             const bool fp = gm.fmt[l] != BN_FMT_U8;  // fp32 accumulator (exact integers)
             if (threadIdx.x == 0) wait_rows(y0);  // the candidates' norms come from k_counts too
-            named_bar(2, 128);  // previous item's norms are no longer read
+            named_bar(2, 128);
             for (int j = threadIdx.x; j < 2 * NBR * NBX; j += 128) {
                 const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;
                 const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - 8) & (L - 1);
@@ -967,6 +1009,13 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+    if (sched && threadIdx.x == 0) {  // the last CTA out resets the work counter for the next launch
+        __threadfence();
+        if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+            sched[0] = 0;
+            sched[1] = 0;
+        }
     }
 }
 
