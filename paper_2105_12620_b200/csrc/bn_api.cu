@@ -95,7 +95,9 @@ bool make_level_maps(CountMaps* m, const void* base, uint64_t rowB, uint64_t lb,
                      uint64_t L) {
     return make_level_map(&m->a, base, rowB, lb, elems, fmt, L, 8, 8) &&
            make_level_map(&m->b, base, rowB, lb, elems, fmt, L, 24, 5) &&
-           make_level_map(&m->s, base, rowB, lb, elems, fmt, L, 8, 1);
+           make_level_map(&m->s, base, rowB, lb, elems, fmt, L, 8, 1) &&
+           make_level_map(&m->g, base, rowB, lb, elems, fmt, L, 8, 5) &&
+           make_level_map(&m->r, base, rowB, lb, elems, fmt, L, 24, 1);
 }
 
 template <class T>

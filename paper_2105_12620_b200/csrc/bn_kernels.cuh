@@ -475,6 +475,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     for (uint32_t i = 0; !mbar_try(bar, parity); ++i)
         if (i > (1u << 26)) __trap();  // never hang the GPU on a protocol bug
 }
+__device__ __forceinline__ void ld8(uint32_t taddr, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t* r) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -536,8 +541,11 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int
 // Tensor maps over the [y][x][K] count tensor (3D, K innermost): box A = {128, 8, 8} (a whole
 // 8x8 block = 64 rows), box B = {128, 24, 5} (a whole neighbour chunk, no wrap), box S =
 // {128, 8, 1} (8 pixels of one row, used where a toroidal wrap splits a chunk).
+// Per level and operand: a = the block's A rows {128, 8 px, 8 rows}; b = a whole neighbour chunk
+// {128, 24 px, 5 rows}; g = one 8-pixel group of a chunk {128, 8, 5} (x-wrapping chunks, group-major
+// in shared memory); r = one chunk row {128, 24, 1} (y-wrapping chunks); s = {128, 8, 1} (corners).
 struct CountMaps {
-    CUtensorMap a, b, s;
+    CUtensorMap a, b, s, g, r;
 };
 
 // 256-bit store of four int2 records {(x[0], y[0]) .. (x[3], y[3])} (one whole 32-byte sector).
@@ -865,13 +873,25 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx)
                                      : "memory");
                         const int kx = (int)(ks * 128);
-                        const bool whole = x0 >= 8 && x0 + 16 <= L && y0 + CH_ROWS * (ch + 1) <= L;
+#ifdef BN_GRAM_PROBE_WHOLE  // timing probe (not product): wrapping chunks as one (zero-filled) box
+                        const bool xw = false, yw = false;
+#else
+                        const bool xw = x0 < 8 || x0 + 16 > L, yw = y0 + CH_ROWS * (ch + 1) > L;
+#endif
                         for (int v = 0; v < 2; ++v) {
                             const CountMaps& m = v ? gm.n[l] : gm.c[l];
                             tma_3d(buf + v * 8192, &m.a, kx, (int)x0, (int)y0, bar);  // 64 block rows
                             const uint32_t bdst = buf + A_BYTES + v * CH_ROWS * GRP * 1024;
-                            if (whole) {
+                            if (!xw && !yw) {
                                 tma_3d(bdst, &m.b, kx, (int)x0 - 8, (int)(y0 + CH_ROWS * ch), bar);
+                            } else if (!yw) {  // x wrap: three 8-pixel groups, group-major [gx][row][px]
+                                for (int gx = 0; gx < GRP; ++gx)
+                                    tma_3d(bdst + gx * CH_ROWS * 1024, &m.g, kx, (int)((x0 + 8 * gx + L - 8) & (L - 1)),
+                                           (int)(y0 + CH_ROWS * ch), bar);
+                            } else if (!xw) {  // y wrap: five rows of 24 pixels
+                                for (int nyl = 0; nyl < CH_ROWS; ++nyl)
+                                    tma_3d(bdst + nyl * GRP * 1024, &m.r, kx, (int)x0 - 8,
+                                           (int)((y0 + CH_ROWS * ch + nyl) & (L - 1)), bar);
                             } else {
                                 for (int nyl = 0; nyl < CH_ROWS; ++nyl)
                                     for (int gx = 0; gx < GRP; ++gx) {
@@ -960,12 +980,24 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                     continue;
                 }
 #endif
+                // x-wrapping chunks (not y-wrapping) hold their B rows group-major: column (gx, row, px)
+                const bool gmaj = (x0 < 8 || x0 + 16 > L) && y0 + CH_ROWS * (ch + 1) <= L;
                 for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
                     const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
                     uint32_t rc[32], rn[32];
-                    const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub + nyl * NBX;
-                    tc::ld32(ta, rc);                       // <v_p, c_q>, q in x0-8 .. x0+23 of row ny
-                    tc::ld32(ta + CH_ROWS * NBX, rn);       // <v_p, cn_q>
+                    const uint32_t tb = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub;
+                    if (!gmaj) {
+                        const uint32_t ta = tb + nyl * NBX;
+                        tc::ld32(ta, rc);                       // <v_p, c_q>, q in x0-8 .. x0+23 of row ny
+                        tc::ld32(ta + CH_ROWS * NBX, rn);       // <v_p, cn_q>
+                    } else {
+#pragma unroll
+                        for (int gx = 0; gx < GRP; ++gx) {
+                            const uint32_t ta = tb + (gx * CH_ROWS + nyl) * 8;
+                            tc::ld8(ta, rc + 8 * gx);
+                            tc::ld8(ta + CH_ROWS * NBX, rn + 8 * gx);
+                        }
+                    }
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     if (oy < 0 || oy > R) continue;
                     int dc[2 * R + 1], dn[2 * R + 1];
