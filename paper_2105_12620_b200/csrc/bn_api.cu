@@ -80,10 +80,9 @@ bool make_level_map(CUtensorMap* m, const void* base, uint64_t rowB, uint64_t lb
                     uint64_t L, uint32_t bx, uint32_t by) {
     encode_tiled_t enc = get_encode_tiled();
     if (!enc) return false;
-    const CUtensorMapDataType dt = fmt == BN_FMT_U8     ? CU_TENSOR_MAP_DATA_TYPE_UINT8
-                                   : fmt == BN_FMT_E2M1 ? CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B
-                                                        : CU_TENSOR_MAP_DATA_TYPE_16U6_ALIGN16B;
-    cuuint64_t dims[3] = {elems, L, L};
+    // e2m1 rows stay packed (plain bytes, kind::mxf4); e3m2 rows are unpacked by the TMA (f8f6f4)
+    const CUtensorMapDataType dt = fmt == BN_FMT_E3M2 ? CU_TENSOR_MAP_DATA_TYPE_16U6_ALIGN16B : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+    cuuint64_t dims[3] = {fmt == BN_FMT_E2M1 ? elems / 2 : elems, L, L};
     cuuint64_t strides[2] = {rowB, L * rowB};
     cuuint32_t box[3] = {128, bx, by};
     cuuint32_t es[3] = {1, 1, 1};

@@ -729,6 +729,21 @@ __host__ __device__ constexpr uint32_t idesc_f8(uint32_t f, int M, int N) {  // 
     return (1u << 4) | ((f == BN_FMT_E2M1 ? 5u : 4u) << 7) | ((f == BN_FMT_E2M1 ? 5u : 4u) << 10) |
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// e2m1 rows left packed (two values per byte, 256 per 128-B row) for kind::mxf4 (block32, every
+// ue8m0 scale factor 2^0 = 0x7F, so the products are the plain integer products; exact fp32 sums,
+// tools/narrow_mma_check.cu): K = 64 per instruction, twice the f8f6f4 rate and half the TMA rows.
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+    return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_mxf4(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum,
+                                         uint32_t tmem_sf) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accum), "r"(tmem_sf));
+}
+// K elements per 128-B row of a stage: packed e2m1 (mxf4) holds 256
+__host__ __device__ constexpr uint32_t stage_k(uint32_t f) { return f == BN_FMT_E2M1 ? 256 : 128; }
 __device__ __forceinline__ void mma_f8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -774,7 +789,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     const uint32_t i_full = b_tempty + 16, i_empty = i_full + 8 * IQ;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nbx = L / 8, nitems = nbx * nbx * nl, P = L * L;
-    const uint32_t nk = Tp / 128;
+    constexpr uint32_t SF_COL = 240;  // scale factors (mxf4) in the unused columns 240..247 of accumulator 0
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b_full + 8 * i) : "memory");
@@ -800,6 +815,14 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = tmem_sh;
+    if (warp < 4) {  // ue8m0 scale factors 2^0 for the mxf4 levels (all 128 lanes, 8 columns)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                         tmem + ((uint32_t)(32 * warp) << 16) + SF_COL), "r"(0x7F7F7F7Fu) : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // Items block-major (the levels of a block consecutive) so that the window distances written last
     // are whole pixels' rows, which k_lut (BN_LUT_REVERSE) reads first while they are still in L2.
     // Block order `border` (host-built): the blocks whose chunks wrap the torus (more, smaller TMA
@@ -860,7 +883,8 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                 item_xyl(it, x0, y0, l);
                 wait_rows(y0);
                 // transaction bytes = the packed global bytes the boxes read (128 + 240 rows)
-                const uint32_t tx = (uint32_t)(128 + N) * 128 * fmt_bits(gm.fmt[l]) / 8;
+                const uint32_t f = gm.fmt[l], nk = Tp / stage_k(f);
+                const uint32_t tx = (uint32_t)(128 + N) * 128 * (f == BN_FMT_E2M1 ? 8 : fmt_bits(f)) / 8;
                 for (int ch = 0; ch < NCHUNK; ++ch)
                     for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
                         const uint32_t b = g % NSTAGE, use = g / NSTAGE;
@@ -914,8 +938,8 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
             if (it >= nitems) break;
             uint32_t x0, y0, l;
             item_xyl(it, x0, y0, l);
-            const uint32_t f = gm.fmt[l];
-            const uint32_t idesc = f == BN_FMT_U8 ? tc::idesc_u8(128, N) : idesc_f8(f, 128, N);
+            const uint32_t f = gm.fmt[l], nk = Tp / stage_k(f);
+            const uint32_t idesc = f == BN_FMT_U8 ? tc::idesc_u8(128, N) : f == BN_FMT_E2M1 ? idesc_mxf4(128, N) : idesc_f8(f, 128, N);
             for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
                 const uint32_t ub = cc & 1, uu = cc >> 1;
                 if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
@@ -932,6 +956,9 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                             if (f == BN_FMT_U8)
                                 tc::mma(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk), idesc,
                                         (ks > 0 || kk > 0) ? 1u : 0u);
+                            else if (f == BN_FMT_E2M1)
+                                mma_mxf4(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk), idesc,
+                                         (ks > 0 || kk > 0) ? 1u : 0u, tmem + SF_COL);
                             else
                                 mma_f8(tmem + 256 * ub, tc::sdesc(sa + 32 * kk), tc::sdesc(sb + 32 * kk), idesc,
                                        (ks > 0 || kk > 0) ? 1u : 0u);
