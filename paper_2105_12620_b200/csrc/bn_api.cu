@@ -199,7 +199,8 @@ struct bn_ctx {
     bool static_sched = false;     // BN_GRAM_SCHED=static: round-robin items instead
 
     bool tail_attr_set[8] = {false};
-    int tail_clusters = -1;        // clusters of the fused pass tail that fit (cached)
+    int tail_clusters = -1;        // clusters of the fused pass tail that fit (cached for tail_L)
+    uint32_t tail_L = 0;
     DevBuf<TailCounters> tailc;
     bool swap_v3 = false;     // BN_DECIDE=swap3: SWAP on k_decide_cl3 (one warp per couple) instead of k_decide_swap
     // narrow count rows: in the SWAP / paper modes, where a pass only
@@ -887,18 +888,30 @@ int launch_pass_tail(bn_ctx* ctx, uint32_t t, uint64_t seed, uint8_t* log, uint3
                      PassStatsDev* out, int check_prev, bool* done) {
     *done = false;
     const uint32_t nb = ctx->L / 8, M = nb * nb, P = ctx->P;
-    if (ctx->no_tail || nb > 16 || nb < 8) return BN_OK;  // 64 <= L <= 128 (C1-size tiles: measured slower)
-    uint32_t cpc = 16;
+    if (ctx->no_tail || nb > 64 || nb < 8) return BN_OK;  // 64 <= L <= 512 (C1-size tiles: measured slower)
+    // L <= 128: k_decide_swap's shape (one warp per member, flags as words); L = 256, 512:
+    // k_decide_big's (16 warps x M / 256 slots, flags as bits)
+    const bool big = nb > 16;
+    if (big && (M % 512 || ctx->no_big)) return BN_OK;  // whole couples per warp
+    uint32_t cpc = big ? M / 16 : 16;
     while (cpc > M) cpc /= 2;
     const uint32_t ncta = M / cpc;
-    const size_t smem = 4 * (size_t)P + (size_t)64 * cpc * 6;
+    const size_t smem = (big ? (size_t)P / 8 : 4 * (size_t)P) + (size_t)64 * cpc * 6;
+    if (smem > 220 * 1024) return BN_OK;
+    const void* fn = big ? (const void*)k_pass_tail<R, true> : (const void*)k_pass_tail<R, false>;
     if (!ctx->tail_attr_set[R]) {
-        CUDA_TRY(cudaFuncSetAttribute(k_pass_tail<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(k_pass_tail<R>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        for (const void* f : {(const void*)k_pass_tail<R, true>, (const void*)k_pass_tail<R, false>}) {
+            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        }
         ctx->tail_attr_set[R] = true;
     }
+    if (ctx->tail_L != ctx->L) {  // the fitting cluster count depends on the variant and its smem
+        ctx->tail_clusters = -1;
+        ctx->tail_L = ctx->L;
+    }
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(32 * (cpc + 1));  // + the publisher warp of the deciding CTAs
+    cfg.blockDim = dim3(32 * ((big ? 16 : cpc) + 1));  // + the publisher warp of the deciding CTAs
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->ls;
     cudaLaunchAttribute at[2];
@@ -913,7 +926,7 @@ int launch_pass_tail(bn_ctx* ctx, uint32_t t, uint64_t seed, uint8_t* log, uint3
     if (ctx->tail_clusters < 0) {
         cfg.gridDim = dim3(ncta);
         int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_pass_tail<R>, &cfg) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess) {
             cudaGetLastError();
             ncl = 0;
         }
@@ -948,7 +961,7 @@ int launch_pass_tail(bn_ctx* ctx, uint32_t t, uint64_t seed, uint8_t* log, uint3
                     (void*)&Un, &U, (void*)&cn, &c, (void*)&nn, &nc, &Un2, &cn2, &nn2, &gather_next, &parts, &out,
                     &check_prev, &tc};
     KSTART(BN_K_TAIL);
-    cudaError_t e = cudaLaunchKernelExC(&cfg, (const void*)k_pass_tail<R>, args);
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
     if (e != cudaSuccess) {
         if (ctx->prof) ctx->prof_marks.pop_back();
         cudaGetLastError();
@@ -1519,7 +1532,8 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
             if (rowflags && pi > 0) CUDA_TRY(cudaStreamWaitEvent(cs, ctx->evC, 0));
             return BN_OK;
         };
-        if (prm->mode == BN_SWAP && !ctx->no_tail && ctx->tail_clusters != 0 && ctx->L <= 128 && ctx->L >= 64) {
+        if (prm->mode == BN_SWAP && !ctx->no_tail && (ctx->tail_clusters != 0 || ctx->tail_L != ctx->L) &&
+            ctx->L <= 512 && ctx->L >= 64) {
             // fused pass tail: Gram (+ exchange), then dE terms, decisions and commit in one launch
             uint8_t* log = accept_log ? ctx->log.p + (size_t)pi * 64 * M : nullptr;
             const bool nxt = fuse && pi + 1 < prm->passes;

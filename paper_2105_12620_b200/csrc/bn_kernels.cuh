@@ -1657,26 +1657,33 @@ struct WinTermsBits : WinTermsFlags32<R> {
         return warp_sum_i64(acc);
     }
 };
+// Body of k_decide_big.  With `tc` (the fused pass tail, SWAP) the CTA has one extra warp (warp
+// nw), the publisher, exactly as in decide_swap_body: every lane that wrote a member's acc / dEp
+// counts it in shared memory (release, CTA scope), and the publisher adds the CTA's cpc members of
+// class s to tc->dec[s] at GPU scope once all are counted.
 template <int R, int mode>
-__global__ void __launch_bounds__(512, 1) k_decide_big(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t spw,
-                                                       const DTabs T, uint8_t* __restrict__ acc,
-                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log) {
-    extern __shared__ __align__(16) uint8_t dsm[];
+__device__ __forceinline__ void decide_big_body(uint8_t* dsm, uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t spw,
+                                                uint32_t nw, const DTabs T, uint8_t* __restrict__ acc,
+                                                i128* __restrict__ dEp, uint8_t* __restrict__ log, TailCounters* tc) {
     __shared__ uint8_t sDelta[8 * 64];
     __shared__ __align__(8) uint64_t sbar[2];
+    __shared__ unsigned int sDecCnt[64];
     const uint32_t nb = L / 8, M = nb * nb, P = L * L;
-    const uint32_t ncta = gridDim.x, nw = blockDim.x >> 5, cpc = nw * spw;
-    const uint32_t first = blockIdx.x * cpc;  // first slot of this CTA
+    const uint32_t ncta = M / (nw * spw), cpc = nw * spw;
+    const uint32_t cta = blockIdx.x % ncta;
+    const uint32_t first = cta * cpc;  // first slot of this CTA
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* sbits = reinterpret_cast<uint32_t*>(dsm);                 // [P / 32]
     uint32_t* sSlot = sbits + P / 32;                                   // [64][cpc] pixels
     uint16_t* sIdx = reinterpret_cast<uint16_t*>(sSlot + 64 * cpc);     // [64][cpc] active indices
     const uint32_t sbits_addr = (uint32_t)__cvta_generic_to_shared(dsm);
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
+    const uint32_t cnt_addr = (uint32_t)__cvta_generic_to_shared(sDecCnt);
     auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
     for (uint32_t j = threadIdx.x; j < P / 32; j += blockDim.x) sbits[j] = 0;
     for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
         sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
+    for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sDecCnt[j] = 0;
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1689,6 +1696,23 @@ __global__ void __launch_bounds__(512, 1) k_decide_big(uint32_t pass_t, uint64_t
         sIdx[j] = (uint16_t)m;
     }
     __syncthreads();
+    if (tc && warp == nw) {  // the publisher warp (fused pass tail)
+        cluster_sync_all();
+        if (lane == 0) {
+            for (uint32_t s = 0; s < 64; ++s) {
+                for (uint32_t n = 0;; ++n) {
+                    unsigned int v;
+                    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(cnt_addr + 4 * s) : "memory");
+                    if (v >= cpc) break;
+                    if (n > (1u << 28)) __trap();
+                }
+                red_release_add(tc->dec + s, cpc);  // fence.acq_rel.gpu + add: the members' writes first
+            }
+        }
+        __syncwarp();
+        cluster_sync_all();
+        return;
+    }
     const uint32_t w0 = warp * spw;  // this warp's first slot within the CTA's slots of a class
     WinTermsBits<R> A, An;
     A.load_global(T, sSlot[w0]);
@@ -1724,6 +1748,8 @@ __global__ void __launch_bounds__(512, 1) k_decide_big(uint32_t pass_t, uint64_t
                     acc[pk] = ok;
                     dEp[pk] = (ok && lane == 0) ? 2 * sum : (i128)0;
                     if (log) log[(size_t)s * M + sIdx[sl]] = ok;
+                    if (tc)  // counted for the publisher warp (release at CTA scope: acc / dEp written first)
+                        asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(cnt_addr + 4 * s) : "memory");
                 }
             }
             if (more) A = An;
@@ -1731,6 +1757,13 @@ __global__ void __launch_bounds__(512, 1) k_decide_big(uint32_t pass_t, uint64_t
     }
     tc::mbar_wait(mailbox(63), (63 >> 1) & 1);
     cluster_sync_all();
+}
+template <int R, int mode>
+__global__ void __launch_bounds__(512, 1) k_decide_big(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t spw,
+                                                       const DTabs T, uint8_t* __restrict__ acc,
+                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    decide_big_body<R, mode>(dsm, pass_t, seed, L, spw, blockDim.x >> 5, T, acc, dEp, log, nullptr);
 }
 
 // ------------------------------------------------------------------------------- pass sums
@@ -2227,7 +2260,7 @@ __global__ void __launch_bounds__(BN_FG_THREADS, BN_FG_MINB) k_finish_gather(uin
     }
 }
 
-// ------------------------------------------------------------ fused pass tail (SWAP, L <= 128)
+// ------------------------------------------------------------ fused pass tail (SWAP, 64 <= L <= 512)
 // One cooperative launch of clusters of `ncta` CTAs replaces k_decide_swap + k_finish_gather
 // (DESIGN.md §5.8).  Cluster 0 decides the 64 colour classes exactly as k_decide_swap and publishes
 // every decided member in tc->dec[s]; the other clusters commit in class order behind it: once all
@@ -2236,7 +2269,7 @@ __global__ void __launch_bounds__(BN_FG_THREADS, BN_FG_MINB) k_finish_gather(uin
 // sums are accumulated (the last helper reduces them).  Co-residency of the decision cluster and
 // the helpers (which wait on it) is guaranteed by the cooperative launch.  Bit-identical to the
 // separate kernels: the same decisions, the same copies, the same exact sums.
-template <int R>
+template <int R, bool BIG>
 __global__ void __launch_bounds__(544, 1) k_pass_tail(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
                                                       longlong2* __restrict__ dterms, uint8_t* __restrict__ acc,
                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log,
@@ -2255,11 +2288,14 @@ __global__ void __launch_bounds__(544, 1) k_pass_tail(uint32_t pass_t, uint64_t 
     const uint32_t ncta = M / cpc;
     const DTabs T = {dterms, nullptr, nullptr};
     if (blockIdx.x < ncta) {  // cluster 0: the decisions
-        decide_swap_body<R>(dsm, pass_t, seed, L, cpc, T, acc, dEp, log, tc, 0);
+        if (BIG)  // L = 256, 512: cpc / 16 slots per warp (k_decide_big)
+            decide_big_body<R, 1>(dsm, pass_t, seed, L, cpc / 16, 16, T, acc, dEp, log, tc);
+        else
+            decide_swap_body<R>(dsm, pass_t, seed, L, cpc, T, acc, dEp, log, tc, 0);
         return;
     }
     // ------------------------------------------------------------------------ helpers
-    __shared__ uint8_t sD[8 * 16];
+    __shared__ uint8_t sD[8 * 64];  // nb <= 64
     __shared__ uint32_t sUnit;
     __shared__ FinishPart s_w[32];
     __shared__ bool last;

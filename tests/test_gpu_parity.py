@@ -415,15 +415,18 @@ def test_eval_smooth_versatility_on_gpu_tiles(bn, oracle_mod):
     assert p1[:3].mean() <= 0.7 * p0[:3].mean()
 
 
-@pytest.mark.parametrize("decide", ["", "nobig"])
+@pytest.mark.parametrize("decide", ["", "notail", "nobig"])
 @pytest.mark.parametrize("L,mode", [(256, 0), (256, 1), (512, 1)])
 def test_decide_large_tiles(bn, oracle_mod, monkeypatch, decide, L, mode):
-    """Tiles beyond one cluster's warps (L = 256, 512): the bit-flag cluster kernel with several
-    slots per warp (default) and, with nobig, the cooperative neighbour-band flag kernel (REDRAW) or
-    the per-class launches (SWAP), one full pass against the oracle."""
-    monkeypatch.setenv("BN_DECIDE", decide)
+    """Tiles beyond one cluster's warps (L = 256, 512): SWAP through the fused pass tail with the
+    bit-flag decisions (default), the bit-flag cluster kernel with several slots per warp (notail;
+    REDRAW always), and with nobig the cooperative neighbour-band flag kernel (REDRAW) or the
+    per-class launches (SWAP); full passes against the oracle (SWAP: 2, so the tail also gathers the
+    next pass's candidates)."""
+    monkeypatch.setenv("BN_DECIDE", "nobig" if decide == "nobig" else "")
+    monkeypatch.setenv("BN_TAIL", "0" if decide == "notail" else "1")
     s, o, U = make(bn, oracle_mod, L, 16, (4,))
-    _check_run(s, o, U, 1, mode, seed=5 + L + mode)
+    _check_run(s, o, U, 2 if mode else 1, mode, seed=5 + L + mode)
 
 
 # --------------------------------------------------------------- best-of-K REDRAW (f3, K > 1)
