@@ -1521,7 +1521,7 @@ __device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, 
     __shared__ uint8_t sDelta[8 * 16];
     __shared__ __align__(8) uint64_t sbar[2];
     __shared__ __align__(16) unsigned long long sPart[16][2];
-    __shared__ unsigned int sDecCnt[64];
+    __shared__ unsigned int sDecCnt[64], sKap[64];
     const uint32_t nb = L / 8, M = nb * nb, P = L * L;
     const uint32_t ncta = cpc ? (M / cpc) : 0, first = (blockIdx.x % ncta) * cpc;  // first slot of this CTA
     const uint32_t cta = blockIdx.x % ncta;
@@ -1535,7 +1535,10 @@ __device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, 
     for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
     for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
         sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
-    for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sDecCnt[j] = 0;
+    for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) {
+        sDecCnt[j] = 0;
+        sKap[j] = swap_kappa(seed, pass_t, j, M);  // one Philox per class, not per slot
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1543,7 +1546,7 @@ __device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, 
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < 64 * cpc; j += blockDim.x) {
         const uint32_t s = j / cpc, i = first + (j - s * cpc);
-        const uint32_t m = couple_member(i >> 1, swap_kappa(seed, pass_t, s, M), i & 1);
+        const uint32_t m = couple_member(i >> 1, sKap[s], i & 1);
         sSlot[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
         sIdx[j] = (uint16_t)m;
     }
@@ -1667,7 +1670,7 @@ __device__ __forceinline__ void decide_big_body(uint8_t* dsm, uint32_t pass_t, u
                                                 i128* __restrict__ dEp, uint8_t* __restrict__ log, TailCounters* tc) {
     __shared__ uint8_t sDelta[8 * 64];
     __shared__ __align__(8) uint64_t sbar[2];
-    __shared__ unsigned int sDecCnt[64];
+    __shared__ unsigned int sDecCnt[64], sKap[64];
     const uint32_t nb = L / 8, M = nb * nb, P = L * L;
     const uint32_t ncta = M / (nw * spw), cpc = nw * spw;
     const uint32_t cta = blockIdx.x % ncta;
@@ -1683,7 +1686,10 @@ __device__ __forceinline__ void decide_big_body(uint8_t* dsm, uint32_t pass_t, u
     for (uint32_t j = threadIdx.x; j < P / 32; j += blockDim.x) sbits[j] = 0;
     for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
         sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
-    for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sDecCnt[j] = 0;
+    for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) {
+        sDecCnt[j] = 0;
+        if (mode) sKap[j] = swap_kappa(seed, pass_t, j, M);  // one Philox per class, not per slot
+    }
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1691,7 +1697,7 @@ __device__ __forceinline__ void decide_big_body(uint8_t* dsm, uint32_t pass_t, u
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < 64 * cpc; j += blockDim.x) {
         const uint32_t s = j / cpc, i = first + (j - s * cpc);
-        const uint32_t m = mode ? couple_member(i >> 1, swap_kappa(seed, pass_t, s, M), i & 1) : i;
+        const uint32_t m = mode ? couple_member(i >> 1, sKap[s], i & 1) : i;
         sSlot[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
         sIdx[j] = (uint16_t)m;
     }
