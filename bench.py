@@ -244,9 +244,9 @@ def roofline(prof, cfg, peaks, sm_clock_mhz, name=None):
         issued = 2.0 * items * 3 * (-(-cfg.T // 256) * 256) * 128 * 240
         out["issued"] = {"ops_per_launch": issued, "achieved": issued / sec / 1e12, "frac": issued / sec / 1e12 / out["peak"],
                          "note": "dense UMMA tiles as issued (4 state combinations x half window, padded)"}
-        out["limiter"] = ("TMA row rate: removing the epilogue or the MMAs leaves ~90% of the time, halving the "
-                          "operand bytes (narrow rows) does not shorten it; the K loop is row-request bound "
-                          "(DESIGN.md 5.1, tools/kernel_times.py probes)")
+        out["limiter"] = ("balanced pipeline: removing the epilogue, the MMAs or the operand loads leaves 83-91% "
+                          "of the time (C3); the TMA stream runs at 31% of the xbar peak and the tensor pipe is "
+                          "active 16% (C3) / 37% (C5, mxf4) -- DESIGN.md 5.1, profiles/r02_ncu_full_gram.md")
     if name == "counts":
         out["limiter"] = ("ALU-pipe issue: per test 1 FFMA2 (fma pipe) + ~1.75 half-rate ALU ops (sign "
                           "count, |t| filter); the FFMA-lane peak is the reported denominator (DESIGN.md 5.1)")
