@@ -517,9 +517,11 @@ constexpr int STAGE = A_BYTES + B_BYTES;  // 47104 = 46 KB
 #define BN_GRAM_NSTAGE 4
 #endif
 constexpr int NSTAGE = BN_GRAM_NSTAGE;
-constexpr int THREADS = 192;
+// warps 0-7: two epilogue groups (group g drains TMEM accumulator g, i.e. every other neighbour
+// chunk; warp & 3 = its TMEM lane quadrant), warp 8: TMA producer, warp 9: MMA issuer
+constexpr int THREADS = 320;
 constexpr int SCR = 25;  // odd row stride: conflict-free scratch writes
-constexpr int SMEM = NSTAGE * STAGE + 4 * 32 * SCR * 4 + 2 * NBR * NBX * 4 + 1024;
+constexpr int SMEM = NSTAGE * STAGE + 2 * (4 * 32 * SCR * 4 + 2 * NBR * NBX * 4) + 1024;
 constexpr int H = 2 * R * R + 2 * R;
 }  // namespace tc3
 
@@ -779,8 +781,8 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     const uint32_t raw = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t sring = (raw + 1023) & ~1023u;
     uint8_t* gring = smem_raw + (sring - raw);
-    int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);  // [4 warps][32][SCR]
-    int* snorm = scratch + 4 * 32 * SCR;                              // [2][NBR][NBX], x from x0-8
+    int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);  // [2 groups][4 warps][32][SCR]
+    int* snorm_all = scratch + 2 * 4 * 32 * SCR;                      // [2 groups][2][NBR][NBX], x from x0-8
     constexpr int IQ = 4;  // item ring (dynamic scheduling): producer -> MMA warp and epilogue
     __shared__ __align__(8) uint64_t bars[2 * NSTAGE + 4 + 2 * IQ];
     __shared__ uint32_t tmem_sh, sItem[IQ];
@@ -801,7 +803,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
         }
         for (int i = 0; i < IQ; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(i_full + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(i_empty + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 3;" ::"r"(i_empty + 8 * i) : "memory");
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -864,7 +866,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     auto release_item = [&](uint32_t j) {
         if (sched) mbar_arrive(i_empty + 8 * (j % IQ));
     };
-    if (warp == 4) {
+    if (warp == 8) {
         // --------------------------------------------------------------- TMA producer
         if (lane == 0) {
             uint32_t g = 0, j = 0;
@@ -928,7 +930,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                     }
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         // --------------------------------------------------------------- UMMA issuer
         uint32_t g = 0, cc = 0;  // stage counter, chunk counter (accumulator ring)
         for (uint32_t ji = 0, it = 0;; ++ji) {
@@ -971,33 +973,36 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                 }
             }
         }
-    } else if (warp < 4) {
-        // --------------------------------------------------------------- epilogue
-        const int arow = 32 * warp + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
-        int* scr = scratch + (warp * 32 + lane) * SCR;
+    } else if (warp < 8) {
+        // --------------------------------------------------------------- epilogue (2 groups)
+        const int grp = warp >> 2, wq = warp & 3, tg = threadIdx.x & 127, gbar = 2 + grp;
+        const int arow = 32 * wq + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
+        int* scr = scratch + ((grp * 4 + wq) * 32 + lane) * SCR;
+        int* snorm = snorm_all + grp * 2 * NBR * NBX;
         uint32_t cc = 0;
         for (uint32_t ji = 0, it = 0;; ++ji) {
             it = next_item(ji, it);
-            named_bar(2, 128);  // every epilogue thread read the slot (and the previous item's norms are done)
-            if (threadIdx.x == 0) release_item(ji);
+            named_bar(gbar, 128);  // every thread of the group read the slot (and the previous item's norms are done)
+            if (tg == 0) release_item(ji);
             if (it >= nitems) break;
             uint32_t x0, y0, l;
             item_xyl(it, x0, y0, l);
             const bool fp = gm.fmt[l] != BN_FMT_U8;  // fp32 accumulator (exact integers)
-            if (threadIdx.x == 0) wait_rows(y0);  // the candidates' norms come from k_counts too
-            named_bar(2, 128);
-            for (int j = threadIdx.x; j < 2 * NBR * NBX; j += 128) {
+            if (tg == 0) wait_rows(y0);  // the candidates' norms come from k_counts too
+            named_bar(gbar, 128);
+            for (int j = tg; j < 2 * NBR * NBX; j += 128) {
                 const int nx = j % NBX, vr = j / NBX, vv = vr >= NBR, r = vr - vv * NBR;
                 const uint32_t qy = (y0 + r) & (L - 1), qx = (x0 + nx + L - 8) & (L - 1);
                 snorm[j] = (vv ? nn : nc)[(size_t)(qy * L + qx) * nl + l];
             }
-            named_bar(2, 128);
+            named_bar(gbar, 128);
             const uint32_t p = ((y0 + dy) & (L - 1)) * L + ((x0 + dx) & (L - 1));
             BN_ASSERT(p < P && l < nl);
             const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
             int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
             for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
                 const uint32_t ub = cc & 1, uu = cc >> 1;
+                if ((int)ub != grp) continue;  // the other group's accumulator
                 tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #ifdef BN_GRAM_PROBE_NOEPI  // timing probe (not product): no TMEM reads, no stores
@@ -1012,7 +1017,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                 for (int nyl = 0; nyl < CH_ROWS; ++nyl) {
                     const int ny = CH_ROWS * ch + nyl, oy = ny - dy;
                     uint32_t rc[32], rn[32];
-                    const uint32_t tb = tmem + ((uint32_t)(32 * warp) << 16) + 256 * ub;
+                    const uint32_t tb = tmem + ((uint32_t)(32 * wq) << 16) + 256 * ub;
                     if (!gmaj) {
                         const uint32_t ta = tb + nyl * NBX;
                         tc::ld32(ta, rc);                       // <v_p, c_q>, q in x0-8 .. x0+23 of row ny
