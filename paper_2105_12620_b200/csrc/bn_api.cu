@@ -174,6 +174,7 @@ struct bn_ctx {
     // (candidate prefetch) and `hp` (high-priority decisions) are internal, joined by events.
     cudaStream_t ls = nullptr, aux = nullptr, hp = nullptr;
     cudaEvent_t evA = nullptr, evB = nullptr, evC = nullptr;
+    cudaEvent_t ev_h2d = nullptr;  // bn_set_tile: the upload of a host tile is complete
     bool no_overlap = false;  // BN_OVERLAP=0: no candidate prefetch on the aux stream
     // per-row publication of the next pass's candidate counts (k_counts -> k_gram_tc4 follows them)
     DevBuf<unsigned int> rows_done;
@@ -549,24 +550,16 @@ int ensure_u8(bn_ctx* ctx) {
 // (<= 4), e3m2 (<= 8) or u8; the rows are packed into that layout (norms |delta|^2).  One host
 // synchronisation (the range) per new tile.
 // Per-level max |c - off| of the current u8 rows into the pinned host buffer (asynchronous).
+int ensure_noff(bn_ctx* ctx);
 int narrow_range_async(bn_ctx* ctx) {
     const uint32_t P = ctx->P, nl = ctx->nl, Tp = ctx->Tp;
-    const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
-    const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
-    if (ctx->noff_dirty) {
-        CUDA_TRY(ctx->iref.ensure(ctx->Ts));
-        k_iref<<<(ctx->Ts + 127) / 128, 128, 0, ctx->stream>>>(ctx->ab.p, ctx->pxy.p, ctx->Ts, ctx->iref.p);
-        LAUNCHED();
-        CUDA_TRY(ctx->noff.ensure((size_t)nl * Tp));
-        k_narrow_offsets<<<(Tp + 255) / 256, 256, 0, ctx->stream>>>(ctx->iref.p, ctx->Ts, Tp, lo, hi, nl, ctx->noff.p);
-        LAUNCHED();
-        ctx->noff_dirty = false;
-    }
+    int rc;
+    if ((rc = ensure_noff(ctx))) return rc;
     if (!ctx->nrng_host) CUDA_TRY(cudaMallocHost(&ctx->nrng_host, 8 * sizeof(int)));
     CUDA_TRY(ctx->nrng.ensure(8));
     CUDA_TRY(cudaMemsetAsync(ctx->nrng.p, 0, 8 * sizeof(int), ctx->stream));
-    const size_t nch = (size_t)P * nl * (Tp / 16);  // 16-byte chunks; ~4 per thread
-    k_narrow_range<<<(unsigned)std::min<size_t>((nch + 1023) / 1024, 148 * 64), 256, 0, ctx->stream>>>(
+    const size_t nchl = (size_t)P * (Tp / 16);  // 16-byte chunks per level; >= 8 per thread
+    k_narrow_range<<<dim3((unsigned)std::min<size_t>((nchl + 2047) / 2048, 148 * 8), nl), 256, 0, ctx->stream>>>(
         ctx->c.p, P, Tp, nl, ctx->noff.p, ctx->nrng.p);
     LAUNCHED();
     CUDA_TRY(cudaMemcpyAsync(ctx->nrng_host, ctx->nrng.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -577,6 +570,24 @@ int narrow_range_async(bn_ctx* ctx) {
 // Narrow rows pay off where the Gram's K loop is long (C5: T = 8192, 0.84 -> 0.74 ms per Gram); with
 // T <= 1024 per level the Gram is bound by the TMA row rate, not bytes, and the pack is overhead.
 bool narrow_wanted(const bn_ctx* ctx) { return ctx->narrow_mode > 0 || (ctx->narrow_mode < 0 && ctx->Tp >= 2048); }
+
+// Offsets off[l][i] = round(N_l I_ref,i) of the current bank (once per bank)
+int ensure_noff(bn_ctx* ctx) {
+    if (!ctx->noff_dirty) return BN_OK;
+    const uint32_t nl = ctx->nl, Tp = ctx->Tp;
+    const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
+    const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
+    CUDA_TRY(ctx->iref.ensure(ctx->Ts));
+    k_iref<<<(ctx->Ts + 127) / 128, 128, 0, ctx->stream>>>(ctx->ab.p, ctx->pxy.p, ctx->Ts, ctx->iref.p);
+    LAUNCHED();
+    CUDA_TRY(ctx->noff.ensure((size_t)nl * Tp));
+    k_narrow_offsets<<<(Tp + 255) / 256, 256, 0, ctx->stream>>>(ctx->iref.p, ctx->Ts, Tp, lo, hi, nl, ctx->noff.p);
+    LAUNCHED();
+    ctx->noff_dirty = false;
+    return BN_OK;
+}
+
+
 
 int ensure_narrow(bn_ctx* ctx) {
     if (ctx->packed || !narrow_wanted(ctx)) return BN_OK;
@@ -1188,6 +1199,7 @@ void bn_destroy(bn_ctx* ctx) {
         if (ctx->nrng_host) cudaFreeHost(ctx->nrng_host);
         if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
         if (ctx->hp) cudaStreamSynchronize(ctx->hp), cudaStreamDestroy(ctx->hp);
+        if (ctx->ev_h2d) cudaEventDestroy(ctx->ev_h2d);
         for (cudaEvent_t e : {ctx->evA, ctx->evB, ctx->evC})
             if (e) cudaEventDestroy(e);
     }
@@ -1319,13 +1331,18 @@ int bn_set_tile(bn_ctx* ctx, uint32_t L, const uint32_t* u_xy, int is_device) {
     CUDA_TRY(ctx->U.ensure(ctx->P));
     CUDA_TRY(cudaMemcpyAsync(ctx->U.p, u_xy, (size_t)ctx->P * sizeof(uint2),
                              is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+    if (!is_device) {
+        if (!ctx->ev_h2d) CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_h2d, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(ctx->ev_h2d, ctx->stream));
+    }
     ctx->have_tile = true;
     ctx->counts_dirty = true;
     int rc = ensure_counts(ctx);
     if (rc) return rc;
     // the narrow-row range of the new counts, ready (pinned) when the permuting optimiser packs them
     if (narrow_wanted(ctx) && (rc = narrow_range_async(ctx))) return rc;
-    if (!is_device) CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // host buffer may be reused
+    // the host buffer may be reused once it is copied; the counts stay asynchronous
+    if (!is_device) CUDA_TRY(cudaEventSynchronize(ctx->ev_h2d));
     return BN_OK;
 }
 

@@ -109,6 +109,81 @@ __host__ __device__ __forceinline__ int hpad_index(int ox, int oy, int R) {
     return oy == 0 ? ox - 1 : ru4(R) + (oy - 1) * ru4(2 * R + 1) + (ox + R);
 }
 
+// ---------------------------------------------------------------------------- narrow row formats
+// Row formats of a level's count rows (SURVEY §8 f3 narrow storage): see the Gram.
+enum : uint32_t { BN_FMT_U8 = 0, BN_FMT_E2M1 = 1, BN_FMT_E3M2 = 2 };
+__host__ __device__ constexpr uint32_t fmt_bits(uint32_t f) { return f == BN_FMT_U8 ? 8 : f == BN_FMT_E2M1 ? 4 : 6; }
+__device__ __forceinline__ uint32_t enc_e2m1(int d) {  // |d| <= 4: 0 1 2 3 4 -> 0x0 0x2 0x4 0x5 0x6
+    const uint32_t a = (uint32_t)abs(d);
+    return (a < 3 ? 2 * a : a + 2) | (d < 0 ? 0x8u : 0u);
+}
+__device__ __forceinline__ uint32_t enc_e3m2(int d) {  // |d| <= 8: (1 + mantissa/4) 2^(e-3)
+    const uint32_t a = (uint32_t)abs(d);
+    return (a == 0 ? 0u : a == 1 ? 0x0Cu : a < 4 ? 0x0Cu + 2 * a : a < 8 ? 0x10u + a : 0x18u) | (d < 0 ? 0x20u : 0u);
+}
+__device__ __forceinline__ int dec_e2m1(uint32_t c) {
+    const uint32_t m = c & 7u;
+    const int a = m == 0 ? 0 : m == 2 ? 1 : m == 4 ? 2 : m == 5 ? 3 : 4;
+    return (c & 8u) ? -a : a;
+}
+__device__ __forceinline__ int dec_e3m2(uint32_t c) {
+    const uint32_t e = (c >> 2) & 7u, mt = c & 3u;
+    const int a = e == 0 ? 0 : (int)((4u + mt) << e) >> 5;  // 2^(e-3) (1 + mt/4) for e >= 3
+    return (c & 0x20u) ? -a : a;
+}
+// Row layout of a level: byte offset lb[l] in the row, format fmt[l].  One warp per pixel row;
+// lane j packs the 16-integrand groups j, j + 32, ...: e2m1 16 x 4 bit in 8 bytes, e3m2 16 x 6 bit
+// in 12 bytes (element k at bit bits * k of its group, little-endian), u8 copied; norms |delta|^2
+// (|c|^2 for u8 levels) per level.
+struct NarrowLayout {
+    uint32_t fmt[8], lb[8];
+};
+// Pack one 16-integrand chunk of a level row (16 counts cv, offsets ov) in format f at group g of
+// the level's packed row dst; adds sum delta^2 (sum c^2 for u8) to nrm, returns max |delta| (u8: 0).
+__device__ __forceinline__ uint32_t pack_chunk16(uint4 cv, uint4 ov, uint32_t f, uint8_t* dst, uint32_t g, int& nrm) {
+    const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, ow[4] = {ov.x, ov.y, ov.z, ov.w};
+    if (f == BN_FMT_U8) {
+        reinterpret_cast<uint4*>(dst)[g] = cv;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nrm = (int)__dp4a(cw[k], cw[k], (unsigned)nrm);
+        return 0;
+    }
+    uint32_t mx = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mx = __vmaxu4(mx, __vabsdiffu4(cw[k], ow[k]));
+    mx = max(max(mx & 0xffu, (mx >> 8) & 0xffu), max((mx >> 16) & 0xffu, mx >> 24));
+    if (f == BN_FMT_E2M1) {  // byte-parallel; |d| <= 4 where the format is valid (range checked)
+        uint32_t w[2] = {0, 0};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t ad = __vabsdiffu4(cw[k], ow[k]);  // |d| per byte
+            // e2m1 code per byte: magnitude a + min(a, 2) (0 1 2 3 4 -> 0 2 4 5 6), sign 0x8
+            const uint32_t code = (ad + __vminu4(ad, 0x02020202u)) | (__vcmpltu4(cw[k], ow[k]) & 0x08080808u);
+            nrm = (int)__dp4a(ad, ad, (unsigned)nrm);
+            const uint32_t t = code | (code >> 4);  // byte 0 = n0 | n1 << 4, byte 2 = n2 | n3 << 4
+            w[k >> 1] |= __byte_perm(t, 0, 0x4420) << (16 * (k & 1));
+        }
+        reinterpret_cast<uint2*>(dst)[g] = make_uint2(w[0], w[1]);
+    } else {
+        const uint8_t* cb = reinterpret_cast<const uint8_t*>(cw);
+        const uint8_t* ob = reinterpret_cast<const uint8_t*>(ow);
+        uint32_t w[3] = {0, 0, 0};  // 96 bits, element j at bits 6j .. 6j+5
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int d = (int)cb[j] - (int)ob[j];
+            nrm += d * d;
+            const uint32_t e = enc_e3m2(d), b = 6 * j;
+            w[b >> 5] |= e << (b & 31);
+            if ((b & 31) > 26) w[(b >> 5) + 1] |= e >> (32 - (b & 31));
+        }
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + 12 * g);
+        d32[0] = w[0];
+        d32[1] = w[1];
+        d32[2] = w[2];
+    }
+    return mx;
+}
+
 // ---------------------------------------------------------------------------- error vectors
 // Heaviside counts for every pixel of a tile (set_tile) or for the REDRAW candidates of pass t.
 //   c_l,p,i = #{k < N_l : a_i (X_k - PX_i) + b_i (Y_k - PY_i) >= 0},  X_k = S_k.x + u_p.x mod 2^32.
@@ -725,8 +800,6 @@ __global__ void __launch_bounds__(256) k_lut(const int4* __restrict__ Dt, uint32
 // multiplies them with kind::f8f6f4 into fp32 (exact: |<x,y>| < 2^24; tools/narrow_mma_check.cu).
 // The offsets cancel in every distance: D = sum (c_p - c_q)^2 = sum (delta_p - delta_q)^2, and the
 // norms stored beside the rows are |delta|^2.
-enum : uint32_t { BN_FMT_U8 = 0, BN_FMT_E2M1 = 1, BN_FMT_E3M2 = 2 };
-__host__ __device__ constexpr uint32_t fmt_bits(uint32_t f) { return f == BN_FMT_U8 ? 8 : f == BN_FMT_E2M1 ? 4 : 6; }
 __host__ __device__ constexpr uint32_t idesc_f8(uint32_t f, int M, int N) {  // f32 += e2m1 / e3m2, K-major
     return (1u << 4) | ((f == BN_FMT_E2M1 ? 5u : 4u) << 7) | ((f == BN_FMT_E2M1 ? 5u : 4u) << 10) |
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -2632,60 +2705,34 @@ __global__ void k_narrow_offsets(const double* __restrict__ iref, uint32_t Ts, u
         off[(size_t)l * Tp + i] = (uint8_t)o;  // N_l <= 128
     }
 }
-// max over the tile of |c - off| per level -> rng[l] (atomicMax).  One thread per 16-byte chunk of
-// the rows (grid-stride, fully parallel), one atomic per warp.
+// max over the tile of |c - off| per level -> rng[l].  Grid (blocks, nl): block (b, l) scans level l
+// (16-byte chunks, grid-stride) keeping a per-byte running max (VABSDIFF4 / VMAX4), then one warp
+// reduction and ONE atomicMax per block (a per-warp atomic on the single address rng[l] serialised
+// 1M atomics for C5: 0.86 ms).
 __global__ void __launch_bounds__(256) k_narrow_range(const uint8_t* __restrict__ c, uint32_t P, uint32_t Tp, uint32_t nl,
                                                       const uint8_t* __restrict__ off, int* __restrict__ rng) {
-    const uint32_t g16 = Tp / 16, n = P * nl * g16;  // chunks; a warp's chunks lie in one (pixel, level) row
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i - (threadIdx.x & 31) < n; i += gridDim.x * blockDim.x) {
-        int m = 0;
-        uint32_t l = 0;
-        if (i < n) {
-            const uint32_t row = i / g16, g = i - row * g16;
-            l = row % nl;
-            const uint4 cv = __ldcs(reinterpret_cast<const uint4*>(c) + i);
-            const uint4 ov = __ldg(reinterpret_cast<const uint4*>(off + (size_t)l * Tp) + g);
-            const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, ow[4] = {ov.x, ov.y, ov.z, ov.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t d = __vabsdiffu4(cw[k], ow[k]);  // four |c - off| bytes
-                m = max(m, (int)max(max(d & 0xff, (d >> 8) & 0xff), max((d >> 16) & 0xff, d >> 24)));
-            }
-        }
-        // lanes of a warp share the level when g16 >= 32; otherwise reduce per lane
-        if (g16 % 32 == 0) {
-            m = (int)__reduce_max_sync(0xffffffffu, (unsigned)m);
-            if ((threadIdx.x & 31) == 0 && m && i < n) atomicMax(rng + l, m);
-        } else if (m && i < n) {
-            atomicMax(rng + l, m);
-        }
+    const uint32_t l = blockIdx.y, g16 = Tp / 16;
+    const size_t n = (size_t)P * g16;  // chunks of level l
+    const uint4* cv4 = reinterpret_cast<const uint4*>(c);
+    const uint4* ov4 = reinterpret_cast<const uint4*>(off + (size_t)l * Tp);
+    uint32_t m = 0;  // four byte lanes
+    for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (size_t)gridDim.x * blockDim.x) {
+        const size_t p = j / g16, g = j - p * g16;
+        const uint4 cv = __ldcs(cv4 + (p * nl + l) * g16 + g);
+        const uint4 ov = __ldg(ov4 + g);
+        m = __vmaxu4(m, __vmaxu4(__vmaxu4(__vabsdiffu4(cv.x, ov.x), __vabsdiffu4(cv.y, ov.y)),
+                                 __vmaxu4(__vabsdiffu4(cv.z, ov.z), __vabsdiffu4(cv.w, ov.w))));
+    }
+    unsigned mm = max(max(m & 0xffu, (m >> 8) & 0xffu), max((m >> 16) & 0xffu, m >> 24));
+    mm = __reduce_max_sync(0xffffffffu, mm);
+    __shared__ unsigned sm[8];
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t w = 1; w < (blockDim.x >> 5); ++w) mm = max(mm, sm[w]);
+        if (mm) atomicMax(rng + l, (int)mm);
     }
 }
-__device__ __forceinline__ uint32_t enc_e2m1(int d) {  // |d| <= 4: 0 1 2 3 4 -> 0x0 0x2 0x4 0x5 0x6
-    const uint32_t a = (uint32_t)abs(d);
-    return (a < 3 ? 2 * a : a + 2) | (d < 0 ? 0x8u : 0u);
-}
-__device__ __forceinline__ uint32_t enc_e3m2(int d) {  // |d| <= 8: (1 + mantissa/4) 2^(e-3)
-    const uint32_t a = (uint32_t)abs(d);
-    return (a == 0 ? 0u : a == 1 ? 0x0Cu : a < 4 ? 0x0Cu + 2 * a : a < 8 ? 0x10u + a : 0x18u) | (d < 0 ? 0x20u : 0u);
-}
-__device__ __forceinline__ int dec_e2m1(uint32_t c) {
-    const uint32_t m = c & 7u;
-    const int a = m == 0 ? 0 : m == 2 ? 1 : m == 4 ? 2 : m == 5 ? 3 : 4;
-    return (c & 8u) ? -a : a;
-}
-__device__ __forceinline__ int dec_e3m2(uint32_t c) {
-    const uint32_t e = (c >> 2) & 7u, mt = c & 3u;
-    const int a = e == 0 ? 0 : (int)((4u + mt) << e) >> 5;  // 2^(e-3) (1 + mt/4) for e >= 3
-    return (c & 0x20u) ? -a : a;
-}
-// Row layout of a level: byte offset lb[l] in the row, format fmt[l].  One warp per pixel row;
-// lane j packs the 16-integrand groups j, j + 32, ...: e2m1 16 x 4 bit in 8 bytes, e3m2 16 x 6 bit
-// in 12 bytes (element k at bit bits * k of its group, little-endian), u8 copied; norms |delta|^2
-// (|c|^2 for u8 levels) per level.
-struct NarrowLayout {
-    uint32_t fmt[8], lb[8];
-};
 // One thread per 16-integrand group (grid-stride); the row norms accumulate per warp in `norms`
 // (zeroed before the launch) with one atomic per warp and row.
 __global__ void __launch_bounds__(256) k_narrow_pack(const uint8_t* __restrict__ c, uint32_t P, uint32_t Tp, uint32_t nl,
@@ -2699,41 +2746,9 @@ __global__ void __launch_bounds__(256) k_narrow_pack(const uint8_t* __restrict__
             row = i / g16;
             const uint32_t g = i - row * g16, p = row / nl, l = row - p * nl;
             const uint4 cv = __ldcs(reinterpret_cast<const uint4*>(c) + i);
-            const uint8_t* cb = reinterpret_cast<const uint8_t*>(&cv);
-            uint8_t* dst = out + (size_t)p * rowBn + lay.lb[l];
             const uint32_t f = lay.fmt[l];
-            if (f == BN_FMT_U8) {
-                reinterpret_cast<uint4*>(dst)[g] = cv;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) nrm += (int)cb[j] * (int)cb[j];
-            } else {
-                const uint4 ov = __ldg(reinterpret_cast<const uint4*>(off + (size_t)l * Tp) + g);
-                const uint8_t* ob = reinterpret_cast<const uint8_t*>(&ov);
-                if (f == BN_FMT_E2M1) {
-                    uint32_t w[2] = {0, 0};
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int d = (int)cb[j] - (int)ob[j];
-                        nrm += d * d;
-                        w[j >> 3] |= enc_e2m1(d) << (4 * (j & 7));
-                    }
-                    reinterpret_cast<uint2*>(dst)[g] = make_uint2(w[0], w[1]);
-                } else {
-                    uint32_t w[3] = {0, 0, 0};  // 96 bits, element j at bits 6j .. 6j+5
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int d = (int)cb[j] - (int)ob[j];
-                        nrm += d * d;
-                        const uint32_t e = enc_e3m2(d), b = 6 * j;
-                        w[b >> 5] |= e << (b & 31);
-                        if ((b & 31) > 26) w[(b >> 5) + 1] |= e >> (32 - (b & 31));
-                    }
-                    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + 12 * g);
-                    d32[0] = w[0];
-                    d32[1] = w[1];
-                    d32[2] = w[2];
-                }
-            }
+            const uint4 ov = f == BN_FMT_U8 ? make_uint4(0, 0, 0, 0) : __ldg(reinterpret_cast<const uint4*>(off + (size_t)l * Tp) + g);
+            pack_chunk16(cv, ov, f, out + (size_t)p * rowBn + lay.lb[l], g, nrm);
         }
         if (g16 % 32 == 0) {  // the warp's 32 groups belong to one row
             nrm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nrm);
