@@ -380,6 +380,10 @@ int check_ready(bn_ctx* ctx) {
     return BN_OK;
 }
 
+// Dynamic shared memory of k_counts: the CTA's samples (float2 + int2 per pixel and sample)
+size_t counts_smem(const bn_ctx* ctx) {
+    return (size_t)COUNT_PIX * ((ctx->levels[ctx->nl - 1] + 3) & ~3u) * 16;
+}
 // (Re)build counts of the current tile when lattice or bank changed after bn_set_tile.
 int ensure_counts(bn_ctx* ctx) {
     if (!ctx->counts_dirty) return BN_OK;
@@ -394,7 +398,7 @@ int ensure_counts(bn_ctx* ctx) {
     const uint4 lo = make_uint4(ctx->levels[0], ctx->levels[1], ctx->levels[2], ctx->levels[3]);
     const uint4 hi = make_uint4(ctx->levels[4], ctx->levels[5], ctx->levels[6], ctx->levels[7]);
     KSTART(BN_K_COUNTS);
-    k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->ls>>>(
+    k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, counts_smem(ctx), ctx->ls>>>(
         ctx->U.p, nullptr, 0, 0, 0, P, ctx->ab.p, ctx->Cc.p, ctx->cgrp.p, ctx->Tp, ctx->S.p, Nmax, lo, hi, ctx->nl, ctx->c.p,
         ctx->nc.p, nullptr, ctx->L);
     LAUNCHED_K();
@@ -1062,7 +1066,7 @@ int optimize_best_of_k(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* sta
         const uint32_t t = prm->first_pass + pi;
         for (uint32_t j = 0; j < K; ++j) {
             KSTART(BN_K_COUNTS);
-            k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->stream>>>(
+            k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, counts_smem(ctx), ctx->stream>>>(
                 nullptr, ctx->UnK.p + (size_t)j * P, (int)(1 + j), prm->seed, t, P, ctx->ab.p, ctx->Cc.p, ctx->cgrp.p,
                 ctx->Tp, ctx->S.p, ctx->levels[nl - 1], lo, hi, nl, ctx->cnK.p + (size_t)j * P * ctx->rowB,
                 ctx->nnK.p + (size_t)j * P * nl, nullptr, ctx->L);
@@ -1477,7 +1481,7 @@ int bn_optimize(bn_ctx* ctx, const bn_opt_params* prm, bn_pass_stats* stats, uin
     }
     auto launch_counts = [&](uint32_t pi) -> int {
         KSTART(BN_K_COUNTS);
-        k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, 0, ctx->ls>>>(
+        k_counts<<<(P + COUNT_PIX - 1) / COUNT_PIX, 256, counts_smem(ctx), ctx->ls>>>(
             nullptr, buf_U(pi), 1, prm->seed, prm->first_pass + pi, P, ctx->ab.p, ctx->Cc.p, ctx->cgrp.p, ctx->Tp, ctx->S.p,
             ctx->levels[nl - 1], lo, hi, nl, buf_c(pi), buf_n(pi), rowflags ? ctx->rows_done.p : nullptr, ctx->L);
         LAUNCHED_K();

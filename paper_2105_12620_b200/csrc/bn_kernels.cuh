@@ -309,7 +309,7 @@ __global__ void k_count_prep(const int2* __restrict__ ab, const long long* __res
 // norms, and the warp-cooperative exact recount of ambiguous pairs (see k_counts).
 template <int NI, int NPX>
 __device__ __forceinline__ void count_pixels(uint32_t pp0, uint32_t nsub, uint32_t p0, const CountGroup& gq, uint32_t q,
-                                             float2 (*sXYf)[128], int2 (*sXY)[128], const uint32_t* levels,
+                                             const float2* sXYf, const int2* sXY, uint32_t ns, const uint32_t* levels,
                                              uint32_t nl, uint32_t Tp, uint32_t Nmax, uint8_t* __restrict__ out,
                                              const int2* __restrict__ ab, const long long* __restrict__ Cc,
                                              int (*sNorm)[8]) {
@@ -319,7 +319,7 @@ __device__ __forceinline__ void count_pixels(uint32_t pp0, uint32_t nsub, uint32
     const float2* xyf[NPX];
 #pragma unroll
     for (int x = 0; x < NPX; ++x) {
-        xyf[x] = sXYf[pp0 + x * nsub];
+        xyf[x] = sXYf + (pp0 + x * nsub) * ns;
 #pragma unroll
         for (int j = 0; j < NI / 2; ++j) acc[x][j] = 0, mn[x][j] = 3.0e38f;
     }
@@ -374,7 +374,7 @@ __device__ __forceinline__ void count_pixels(uint32_t pp0, uint32_t nsub, uint32
                         const uint32_t k = lane + 32 * r;
                         bool pos = false;
                         if (k < Nmax) {
-                            const int2 xy = sXY[pp][k];
+                            const int2 xy = sXY[pp * ns + k];
                             pos = ((long long)abj.x * xy.x + (long long)abj.y * xy.y - cj) >= 0;
                         }
                         bits[r] = __ballot_sync(0xffffffffu, pos);
@@ -401,10 +401,12 @@ __device__ __forceinline__ void count_pixels(uint32_t pp0, uint32_t nsub, uint32
     }
 }
 
-#ifndef BN_COUNT_MINB
-#define BN_COUNT_MINB 2
+// <= 120 registers: a counts CTA (8 warps) then fits beside a persistent Gram CTA (10 warps x 104)
+// in one SM's 64 K registers, so another tile's counts overlap the Gram (the e2e serving loop)
+#ifndef BN_COUNT_MAXREG
+#define BN_COUNT_MAXREG 120
 #endif
-__global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __restrict__ U, uint2* __restrict__ Uout, int redraw,
+__global__ void __maxnreg__(BN_COUNT_MAXREG) k_counts(const uint2* __restrict__ U, uint2* __restrict__ Uout, int redraw,
                                                 uint64_t seed, uint32_t pass_t, uint32_t P,
                                                 const int2* __restrict__ ab, const long long* __restrict__ Cc,
                                                 const CountGroup* __restrict__ grp, uint32_t Tp,
@@ -413,8 +415,12 @@ __global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __re
                                                 int* __restrict__ norms, unsigned int* __restrict__ rows_done,
                                                 uint32_t L) {
     constexpr int NI = COUNT_NI;
-    __shared__ int2 sXY[COUNT_PIX][128];
-    __shared__ float2 sXYf[COUNT_PIX][128];
+    // the CTA's samples, [COUNT_PIX][ns] each (dynamic, ns = Nmax rounded up to 4: a small footprint
+    // lets a counts CTA of another tile co-reside with a persistent Gram CTA on the same SM)
+    extern __shared__ __align__(16) uint8_t kc_smem[];
+    const uint32_t ns = (Nmax + 3) & ~3u;
+    float2* sXYf = reinterpret_cast<float2*>(kc_smem);
+    int2* sXY = reinterpret_cast<int2*>(sXYf + COUNT_PIX * ns);
     __shared__ int sNorm[COUNT_PIX][8];
     __shared__ uint32_t levels[8];
     if (threadIdx.x == 0) {
@@ -447,8 +453,8 @@ __global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __re
         for (uint32_t k = threadIdx.x & 31; k < Nmax; k += 32) {
             const uint2 sk = S[k];
             const int2 xy = make_int2((int)((sk.x + u.x) ^ 0x80000000u), (int)((sk.y + u.y) ^ 0x80000000u));
-            sXY[pp][k] = xy;
-            sXYf[pp][k] = make_float2(__int2float_rn(xy.x), __int2float_rn(xy.y));
+            sXY[pp * ns + k] = xy;
+            sXYf[pp * ns + k] = make_float2(__int2float_rn(xy.x), __int2float_rn(xy.y));
         }
     }
     __syncthreads();
@@ -458,9 +464,9 @@ __global__ void __launch_bounds__(256, BN_COUNT_MINB) k_counts(const uint2* __re
         for (uint32_t pp = sub; pp < COUNT_PIX; pp += 2 * nsub) {
             if (p0 + pp >= P) break;
             if (pp + nsub < COUNT_PIX && p0 + pp + nsub < P)  // two of the thread's pixels at once
-                count_pixels<NI, 2>(pp, nsub, p0, gq, q, sXYf, sXY, levels, nl, Tp, Nmax, out, ab, Cc, sNorm);
+                count_pixels<NI, 2>(pp, nsub, p0, gq, q, sXYf, sXY, ns, levels, nl, Tp, Nmax, out, ab, Cc, sNorm);
             else
-                count_pixels<NI, 1>(pp, nsub, p0, gq, q, sXYf, sXY, levels, nl, Tp, Nmax, out, ab, Cc, sNorm);
+                count_pixels<NI, 1>(pp, nsub, p0, gq, q, sXYf, sXY, ns, levels, nl, Tp, Nmax, out, ab, Cc, sNorm);
         }
     }
     __syncthreads();
@@ -594,9 +600,13 @@ constexpr int STAGE = A_BYTES + B_BYTES;  // 47104 = 46 KB
 constexpr int NSTAGE = BN_GRAM_NSTAGE;
 // warps 0-7: two epilogue groups (group g drains TMEM accumulator g, i.e. every other neighbour
 // chunk; warp & 3 = its TMEM lane quadrant), warp 8: TMA producer, warp 9: MMA issuer
-constexpr int THREADS = 320;
+#ifndef BN_GRAM_EPI_GROUPS
+#define BN_GRAM_EPI_GROUPS 2
+#endif
+constexpr int EPI = BN_GRAM_EPI_GROUPS;  // epilogue groups of 4 warps (1 or 2)
+constexpr int THREADS = 32 * (4 * EPI + 2);
 constexpr int SCR = 25;  // odd row stride: conflict-free scratch writes
-constexpr int SMEM = NSTAGE * STAGE + 2 * (4 * 32 * SCR * 4 + 2 * NBR * NBX * 4) + 1024;
+constexpr int SMEM = NSTAGE * STAGE + EPI * (4 * 32 * SCR * 4 + 2 * NBR * NBX * 4) + 1024;
 constexpr int H = 2 * R * R + 2 * R;
 }  // namespace tc3
 
@@ -855,7 +865,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     const uint32_t sring = (raw + 1023) & ~1023u;
     uint8_t* gring = smem_raw + (sring - raw);
     int* scratch = reinterpret_cast<int*>(gring + NSTAGE * STAGE);  // [2 groups][4 warps][32][SCR]
-    int* snorm_all = scratch + 2 * 4 * 32 * SCR;                      // [2 groups][2][NBR][NBX], x from x0-8
+    int* snorm_all = scratch + tc3::EPI * 4 * 32 * SCR;                // [groups][2][NBR][NBX], x from x0-8
     constexpr int IQ = 4;  // item ring (dynamic scheduling): producer -> MMA warp and epilogue
     __shared__ __align__(8) uint64_t bars[2 * NSTAGE + 4 + 2 * IQ];
     __shared__ uint32_t tmem_sh, sItem[IQ];
@@ -876,7 +886,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
         }
         for (int i = 0; i < IQ; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(i_full + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 3;" ::"r"(i_empty + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(i_empty + 8 * i), "r"(1 + tc3::EPI) : "memory");
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -939,7 +949,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     auto release_item = [&](uint32_t j) {
         if (sched) mbar_arrive(i_empty + 8 * (j % IQ));
     };
-    if (warp == 8) {
+    if (warp == 4 * tc3::EPI) {
         // --------------------------------------------------------------- TMA producer
         if (lane == 0) {
             uint32_t g = 0, j = 0;
@@ -1003,7 +1013,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                     }
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == 4 * tc3::EPI + 1) {
         // --------------------------------------------------------------- UMMA issuer
         uint32_t g = 0, cc = 0;  // stage counter, chunk counter (accumulator ring)
         for (uint32_t ji = 0, it = 0;; ++ji) {
@@ -1046,7 +1056,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                 }
             }
         }
-    } else if (warp < 8) {
+    } else if (warp < 4 * tc3::EPI) {
         // --------------------------------------------------------------- epilogue (2 groups)
         const int grp = warp >> 2, wq = warp & 3, tg = threadIdx.x & 127, gbar = 2 + grp;
         const int arow = 32 * wq + lane, v = arow >> 6, pp = arow & 63, dy = pp >> 3, dx = pp & 7;
@@ -1075,7 +1085,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
             int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
             for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
                 const uint32_t ub = cc & 1, uu = cc >> 1;
-                if ((int)ub != grp) continue;  // the other group's accumulator
+                if (tc3::EPI == 2 && (int)ub != grp) continue;  // the other group's accumulator
                 tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #ifdef BN_GRAM_PROBE_NOEPI  // timing probe (not product): no TMEM reads, no stores
