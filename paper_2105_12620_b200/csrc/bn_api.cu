@@ -198,6 +198,7 @@ struct bn_ctx {
     bool no_border = false;        // BN_GRAM_ORDER=raster: plain raster block order
     DevBuf<unsigned int> gsched;   // Gram work counter + CTA exit counter (dynamic item scheduling)
     bool static_sched = false;     // BN_GRAM_SCHED=static: round-robin items instead
+    bool no_csplit = false;        // BN_GRAM_CSPLIT=0: small tiles keep whole (block, level) items
 
     bool tail_attr_set[8] = {false};
     int tail_clusters = -1;        // clusters of the fused pass tail that fit (cached for tail_L)
@@ -489,7 +490,9 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     }
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
-    const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl;
+    // small tiles (fewer (block, level) items than SMs): one item per neighbour chunk
+    const uint32_t csplit = (ctx->L / 8) * (ctx->L / 8) * ctx->nl < (uint32_t)nsm && !ctx->no_csplit ? tc3::NCHUNK : 1;
+    const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl * csplit;
     const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
     KSTART(BN_K_GRAM);
     // block order: toroidally wrapping blocks (x0 = 0, x0 = L - 8, last block row) first
@@ -516,7 +519,7 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     CUDA_TRY(launch_k(ctx, k_gram_tc4<R>, dim3(grid), dim3(tc3::THREADS), smem, ctx->ls, gm, ctx->nc.p, nn, ctx->L,
                       ctx->Tp, ctx->nl, ctx->Dt.p, ctx->gram_rows, ctx->gram_rows_target,
                       (const uint16_t*)(ctx->no_border ? nullptr : ctx->border.p),
-                      dyn ? ctx->gsched.p : nullptr));
+                      dyn ? ctx->gsched.p : nullptr, csplit));
     LAUNCHED_K();
     return BN_OK;
 }
@@ -1141,6 +1144,8 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->no_big = dm && !strcmp(dm, "nobig");
     const char* go = getenv("BN_GRAM_ORDER");
     ctx->no_border = go && !strcmp(go, "raster");
+    const char* csp = getenv("BN_GRAM_CSPLIT");
+    ctx->no_csplit = csp && !strcmp(csp, "0");
     const char* gs = getenv("BN_GRAM_SCHED");
     ctx->static_sched = gs && !strcmp(gs, "static");
     const char* tl = getenv("BN_TAIL");

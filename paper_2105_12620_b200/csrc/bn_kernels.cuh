@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                                                               const unsigned int* __restrict__ rows_done,
                                                               uint32_t rows_target,
                                                               const uint16_t* __restrict__ border,
-                                                              unsigned int* __restrict__ sched) {
+                                                              unsigned int* __restrict__ sched, uint32_t csplit) {
     using tc3::NBR; using tc3::NBX; using tc3::GRP; using tc3::CH_ROWS; using tc3::NCHUNK; using tc3::N;
     using tc3::A_BYTES; using tc3::STAGE; using tc3::NSTAGE; using tc3::SCR;
     constexpr int RW = ru4(2 * R + 1), R0 = ru4(R), NV = RW > R + 1 + R0 ? RW : R + 1 + R0;
@@ -873,7 +873,9 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     const uint32_t b_empty = b_full + 8 * NSTAGE, b_tfull = b_full + 16 * NSTAGE, b_tempty = b_tfull + 16;
     const uint32_t i_full = b_tempty + 16, i_empty = i_full + 8 * IQ;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t nbx = L / 8, nitems = nbx * nbx * nl, P = L * L;
+    // csplit = NCHUNK (small tiles: fewer (block, level) pairs than SMs): an item is one neighbour
+    // chunk of a (block, level), so three CTAs share a block instead of one walking its chunks
+    const uint32_t nbx = L / 8, nitems = nbx * nbx * nl * csplit, P = L * L;
     constexpr uint32_t SF_COL = 240;  // scale factors (mxf4) in the unused columns 240..247 of accumulator 0
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
@@ -913,10 +915,16 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
     // Block order `border` (host-built): the blocks whose chunks wrap the torus (more, smaller TMA
     // boxes: the slowest items) first, so the static round-robin spreads them over the CTAs.
     auto item_xyl = [&](uint32_t it, uint32_t& x0, uint32_t& y0, uint32_t& l) {
+        it /= csplit;
         l = it % nl;
         const uint32_t b = border ? (uint32_t)border[it / nl] : it / nl;
         x0 = 8 * (b % nbx);
         y0 = 8 * (b / nbx);
+    };
+    // the item's chunks [ch0, ch1)
+    auto item_ch = [&](uint32_t it, int& ch0, int& ch1) {
+        ch0 = csplit == 1 ? 0 : (int)(it % csplit);
+        ch1 = csplit == 1 ? NCHUNK : ch0 + 1;
     };
     // wait until every tile row y0 .. y0 + 14 (mod L) of this pass's candidates is published by
     // k_counts (acquire), then order the following TMA (async-proxy) reads after it
@@ -966,11 +974,13 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                 if (it >= nitems) break;
                 uint32_t x0, y0, l;
                 item_xyl(it, x0, y0, l);
+                int chb, che;
+                item_ch(it, chb, che);
                 wait_rows(y0);
                 // transaction bytes = the packed global bytes the boxes read (128 + 240 rows)
                 const uint32_t f = gm.fmt[l], nk = Tp / stage_k(f);
                 const uint32_t tx = (uint32_t)(128 + N) * 128 * (f == BN_FMT_E2M1 ? 8 : fmt_bits(f)) / 8;
-                for (int ch = 0; ch < NCHUNK; ++ch)
+                for (int ch = chb; ch < che; ++ch)
                     for (uint32_t ks = 0; ks < nk; ++ks, ++g) {
                         const uint32_t b = g % NSTAGE, use = g / NSTAGE;
                         if (use > 0) tc::mbar_wait(b_empty + 8 * b, (use - 1) & 1);
@@ -1025,7 +1035,9 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
             item_xyl(it, x0, y0, l);
             const uint32_t f = gm.fmt[l], nk = Tp / stage_k(f);
             const uint32_t idesc = f == BN_FMT_U8 ? tc::idesc_u8(128, N) : f == BN_FMT_E2M1 ? idesc_mxf4(128, N) : idesc_f8(f, 128, N);
-            for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
+            int chb, che;
+            item_ch(it, chb, che);
+            for (int ch = chb; ch < che; ++ch, ++cc) {
                 const uint32_t ub = cc & 1, uu = cc >> 1;
                 if (uu > 0) tc::mbar_wait(b_tempty + 8 * ub, (uu - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1083,7 +1095,9 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
             BN_ASSERT(p < P && l < nl);
             const int np = snorm[(v * NBR + dy) * NBX + dx + 8];
             int2* out2 = dt_plane(Dt, (size_t)nl * P * half_count_padded(R), v) + ((size_t)l * P + p) * half_count_padded(R);
-            for (int ch = 0; ch < NCHUNK; ++ch, ++cc) {
+            int chb, che;
+            item_ch(it, chb, che);
+            for (int ch = chb; ch < che; ++ch, ++cc) {
                 const uint32_t ub = cc & 1, uu = cc >> 1;
                 if (tc3::EPI == 2 && (int)ub != grp) continue;  // the other group's accumulator
                 tc::mbar_wait(b_tfull + 8 * ub, uu & 1);
