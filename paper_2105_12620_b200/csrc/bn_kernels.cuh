@@ -113,14 +113,9 @@ __host__ __device__ __forceinline__ int hpad_index(int ox, int oy, int R) {
 // Row formats of a level's count rows (SURVEY §8 f3 narrow storage): see the Gram.
 enum : uint32_t { BN_FMT_U8 = 0, BN_FMT_E2M1 = 1, BN_FMT_E3M2 = 2 };
 __host__ __device__ constexpr uint32_t fmt_bits(uint32_t f) { return f == BN_FMT_U8 ? 8 : f == BN_FMT_E2M1 ? 4 : 6; }
-__device__ __forceinline__ uint32_t enc_e2m1(int d) {  // |d| <= 4: 0 1 2 3 4 -> 0x0 0x2 0x4 0x5 0x6
-    const uint32_t a = (uint32_t)abs(d);
-    return (a < 3 ? 2 * a : a + 2) | (d < 0 ? 0x8u : 0u);
-}
-__device__ __forceinline__ uint32_t enc_e3m2(int d) {  // |d| <= 8: (1 + mantissa/4) 2^(e-3)
-    const uint32_t a = (uint32_t)abs(d);
-    return (a == 0 ? 0u : a == 1 ? 0x0Cu : a < 4 ? 0x0Cu + 2 * a : a < 8 ? 0x10u + a : 0x18u) | (d < 0 ? 0x20u : 0u);
-}
+// Codes (the encoders are byte-parallel, in pack_chunk16): e2m1 |d| <= 4: 0 1 2 3 4 -> 0x0 0x2 0x4 0x5
+// 0x6, sign 0x8; e3m2 |d| <= 8: (1 + mantissa/4) 2^(e-3): 0 1 2 3 4 5 6 7 8 -> 0x00 0x0C 0x10 0x12
+// 0x14 0x15 0x16 0x17 0x18, sign 0x20.
 __device__ __forceinline__ int dec_e2m1(uint32_t c) {
     const uint32_t m = c & 7u;
     const int a = m == 0 ? 0 : m == 2 ? 1 : m == 4 ? 2 : m == 5 ? 3 : 4;
@@ -164,22 +159,24 @@ __device__ __forceinline__ uint32_t pack_chunk16(uint4 cv, uint4 ov, uint32_t f,
             w[k >> 1] |= __byte_perm(t, 0, 0x4420) << (16 * (k & 1));
         }
         reinterpret_cast<uint2*>(dst)[g] = make_uint2(w[0], w[1]);
-    } else {
-        const uint8_t* cb = reinterpret_cast<const uint8_t*>(cw);
-        const uint8_t* ob = reinterpret_cast<const uint8_t*>(ow);
-        uint32_t w[3] = {0, 0, 0};  // 96 bits, element j at bits 6j .. 6j+5
+    } else {  // e3m2, byte-parallel; |d| <= 8 where the format is valid (range checked)
+        uint32_t v[4];  // four 24-bit runs of four 6-bit codes
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int d = (int)cb[j] - (int)ob[j];
-            nrm += d * d;
-            const uint32_t e = enc_e3m2(d), b = 6 * j;
-            w[b >> 5] |= e << (b & 31);
-            if ((b & 31) > 26) w[(b >> 5) + 1] |= e >> (32 - (b & 31));
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t ad = __vabsdiffu4(cw[k], ow[k]);  // |d| per byte, 0..8
+            nrm = (int)__dp4a(ad, ad, (unsigned)nrm);
+            const uint32_t t = ad | (ad >> 4);
+            const uint32_t sel = __byte_perm(t, 0, 0x4420);  // selector nibbles |d0| .. |d3| (mod 8)
+            // codes of 0..7: 00 0C 10 12 | 14 15 16 17; |d| = 8: 0x18; sign 0x20
+            const uint32_t eq8 = __vcmpeq4(ad, 0x08080808u);
+            uint32_t code = (__byte_perm(0x12100C00u, 0x17161514u, sel) & ~eq8) | (0x18181818u & eq8);
+            code |= __vcmpltu4(cw[k], ow[k]) & 0x20202020u;
+            v[k] = (code & 0x3Fu) | ((code >> 2) & 0xFC0u) | ((code >> 4) & 0x3F000u) | ((code >> 6) & 0xFC0000u);
         }
-        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + 12 * g);
-        d32[0] = w[0];
-        d32[1] = w[1];
-        d32[2] = w[2];
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + 12 * g);  // element j at bits 6j .. 6j+5
+        d32[0] = v[0] | (v[1] << 24);
+        d32[1] = (v[1] >> 8) | (v[2] << 16);
+        d32[2] = (v[2] >> 16) | (v[3] << 8);
     }
     return mx;
 }
