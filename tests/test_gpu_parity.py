@@ -167,10 +167,13 @@ def test_errors(bn, oracle_mod):
 
 
 # ------------------------------------------------------------- bank-shard decomposition (C5)
-def test_window_distances_and_shard_decomposition(bn, oracle_mod):
+@pytest.mark.parametrize("csplit", ["", "0"])
+def test_window_distances_and_shard_decomposition(bn, oracle_mod, monkeypatch, csplit):
     """The multi-GPU (C5) exchange sums partial window distances over bank shards.  On one GPU:
     the full-bank distances equal the plain definition on the oracle's counts, and the shard
-    contexts' partial distances (T split 3 ways, ragged) add up to them exactly."""
+    contexts' partial distances (T split 3 ways, ragged) add up to them exactly.  Small tiles run
+    one Gram item per neighbour chunk by default; BN_GRAM_CSPLIT=0 keeps whole items."""
+    monkeypatch.setenv("BN_GRAM_CSPLIT", csplit)
     from paper_2105_12620_b200.dist import shard_range
     from tests.test_dist_cpu import _partial_distances
 
