@@ -92,7 +92,7 @@ int bn_set_energy(bn_ctx *ctx, double sigma_i, double sigma_s, int32_t radius);
 enum bn_energy_form { BN_E_GF = 0, BN_E_EQ1 = 1, BN_E_EQ1_MAX = 2 };
 int bn_set_energy_form(bn_ctx *ctx, uint32_t form);
 
-/* Load the tile U (L*L pixels, L a power of two >= 16, L > 2R) and build its counts.
+/* Load the tile U (L*L pixels, L a power of two in [16, 2048], L > 2R) and build its counts.
  * u_xy: [2 L L] uint32, host (is_device = 0) or device.  Requires lattice and bank.
  * Returns once a host u_xy has been copied (it may then be reused); the counts are built
  * asynchronously on the context's stream, ordered before every later call on it. */

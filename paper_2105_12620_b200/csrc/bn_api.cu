@@ -193,7 +193,7 @@ struct bn_ctx {
     bool no_fuse = false;          // BN_FUSE=0: separate SWAP commit (k_finish) and gather kernels
     bool no_tail = false;          // BN_TAIL=0: separate decision and commit kernels (no k_pass_tail)
     uint32_t nEpart = 0;           // energy partials written by the last Gram / k_lut launch
-    DevBuf<uint16_t> border;       // block order of the Gram (wrapping blocks first)
+    DevBuf<uint32_t> border;       // block order of the Gram (wrapping blocks first)
     uint32_t border_L = 0;
     bool no_border = false;        // BN_GRAM_ORDER=raster: plain raster block order
     DevBuf<unsigned int> gsched;   // Gram work counter + CTA exit counter (dynamic item scheduling)
@@ -498,15 +498,15 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     // block order: toroidally wrapping blocks (x0 = 0, x0 = L - 8, last block row) first
     const uint32_t nbx = ctx->L / 8;
     if (ctx->border_L != ctx->L && !ctx->no_border) {
-        std::vector<uint16_t> ord;
+        std::vector<uint32_t> ord;
         for (int pass = 0; pass < 2; ++pass)
             for (uint32_t b = 0; b < nbx * nbx; ++b) {
                 const uint32_t bx = b % nbx, by = b / nbx;
                 const bool wraps = bx == 0 || bx == nbx - 1 || by == nbx - 1;
-                if (wraps == (pass == 0)) ord.push_back((uint16_t)b);
+                if (wraps == (pass == 0)) ord.push_back(b);
             }
         CUDA_TRY(ctx->border.ensure(ord.size()));
-        CUDA_TRY(cudaMemcpyAsync(ctx->border.p, ord.data(), ord.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(ctx->border.p, ord.data(), ord.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         ctx->border_L = ctx->L;
     }
@@ -518,7 +518,7 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     }
     CUDA_TRY(launch_k(ctx, k_gram_tc4<R>, dim3(grid), dim3(tc3::THREADS), smem, ctx->ls, gm, ctx->nc.p, nn, ctx->L,
                       ctx->Tp, ctx->nl, ctx->Dt.p, ctx->gram_rows, ctx->gram_rows_target,
-                      (const uint16_t*)(ctx->no_border ? nullptr : ctx->border.p),
+                      (const uint32_t*)(ctx->no_border ? nullptr : ctx->border.p),
                       dyn ? ctx->gsched.p : nullptr, csplit));
     LAUNCHED_K();
     return BN_OK;
@@ -1332,7 +1332,7 @@ int bn_set_energy(bn_ctx* ctx, double sigma_i, double sigma_s, int32_t radius) {
 int bn_set_tile(bn_ctx* ctx, uint32_t L, const uint32_t* u_xy, int is_device) {
     if (!ctx) return BN_EINVAL;
     if (!u_xy) return fail(ctx, BN_EINVAL, "null tile");
-    if (!pow2(L) || L < 16 || L > 4096) return fail(ctx, BN_EINVAL, "L = %u must be a power of two in [16, 4096]", L);
+    if (!pow2(L) || L < 16 || L > 2048) return fail(ctx, BN_EINVAL, "L = %u must be a power of two in [16, 2048]", L);
     if (!ctx->have_lattice || !ctx->have_bank) return fail(ctx, BN_ESTATE, "set lattice and bank before the tile");
     DeviceGuard g(ctx->dev);
     ctx->L = L;

@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(tc3::THREADS, 1) k_gram_tc4(const __grid_const
                                                               int4* __restrict__ Dt,
                                                               const unsigned int* __restrict__ rows_done,
                                                               uint32_t rows_target,
-                                                              const uint16_t* __restrict__ border,
+                                                              const uint32_t* __restrict__ border,
                                                               unsigned int* __restrict__ sched, uint32_t csplit) {
     using tc3::NBR; using tc3::NBX; using tc3::GRP; using tc3::CH_ROWS; using tc3::NCHUNK; using tc3::N;
     using tc3::A_BYTES; using tc3::STAGE; using tc3::NSTAGE; using tc3::SCR;

@@ -18,6 +18,7 @@ import numpy as np
 import pytest
 
 import synth
+from tests.golden import make_bigtile
 from tests.golden.make_fullsize import load, unpack_log
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
@@ -127,3 +128,27 @@ def test_nccl_one_rank_small_runs_vs_oracle(bn, oracle_mod):
         assert np.array_equal(lg, lgo) and np.array_equal(s.get_tile(), Uo)
         assert [x["E_fixed"] for x in st] == [x["E_fixed"] for x in sto]
         s.close()
+
+
+@pytest.mark.parametrize("name", sorted(make_bigtile.JOBS))
+def test_largest_tiles_vs_oracle(bn, name):
+    """The largest tiles the API accepts (L = 1024, 2048; T = 8, 4 spp): one REDRAW and one SWAP
+    pass (the cooperative band-flag decisions / per-class launches beyond one cluster) against
+    oracle goldens: counts before and after, the accept log of all 64 classes, the tile, E_fixed
+    and dE_sum, all bit-exact."""
+    g = make_bigtile.load(name)
+    U, (a, b, px, py) = make_bigtile.inputs(g["L"])
+    s = bn.Sampler(0)
+    s.set_lattice(synth.D1, synth.D2, g["levels"])
+    s.set_bank(a, b, px, py)
+    s.set_energy(2.1, 1.0, 7)
+    s.set_tile(g["L"], U)
+    assert sha(s.eval_counts()) == g["counts0_sha256"]
+    st, lg = s.optimize(1, g["seed"], mode=g["mode"], log=True)
+    assert sha(np.asarray(lg[0], np.uint8)) == g["log_sha256"], "accept log differs"
+    assert st[0]["accepted"] == g["accepted"] and st[0]["proposed"] == g["proposed"]
+    assert st[0]["E_fixed"] == int(g["E_fixed"]) and st[0]["dE_sum"] == int(g["dE_sum"])
+    assert sha(s.get_tile()) == g["U_sha256"], "tile differs"
+    assert sha(s.eval_counts()) == g["counts_final_sha256"], "counts differ"
+    s.check()
+    s.close()

@@ -463,6 +463,10 @@ def test_edge_cases_empty_and_degenerate(bn, oracle_mod):
     with pytest.raises(bn.BNError) as e:
         s.set_bank(a, b, px, py, 5, 5)
     assert e.value.code == bn.BN_EINVAL
+    s.set_bank(a, b, px, py)
+    with pytest.raises(bn.BNError) as e:  # beyond the largest parity-tested tile side (2048)
+        s.set_tile(4096, np.zeros((4096 * 4096, 2), np.uint32))
+    assert e.value.code == bn.BN_EINVAL
     with pytest.raises(bn.BNError) as e:
         s.set_bank(np.full(8, 1 << 16, np.int32), b, px, py)
     assert e.value.code == bn.BN_EINVAL
