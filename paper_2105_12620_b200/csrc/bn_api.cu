@@ -610,9 +610,12 @@ int ensure_narrow(bn_ctx* ctx) {
         uint32_t f = BN_FMT_U8;
         if (l < nl) {
             const int m = rng[l];
+            // the fp32 accumulator of the narrow MMAs is exact while every dot product stays below
+            // 2^24: Tp * 4^2 (e2m1) and Tp * 8^2 (e3m2) bound them
+            const bool e2 = (uint64_t)Tp * 16 < (1ull << 24), e3 = (uint64_t)Tp * 64 < (1ull << 24);
             f = ctx->narrow_mode == 3 ? BN_FMT_U8
-                : m <= 4 && ctx->narrow_mode != 2 ? BN_FMT_E2M1
-                : m <= 8 ? BN_FMT_E3M2 : BN_FMT_U8;
+                : m <= 4 && ctx->narrow_mode != 2 && e2 ? BN_FMT_E2M1
+                : m <= 8 && e3 ? BN_FMT_E3M2 : BN_FMT_U8;
         }
         ctx->fmt[l] = lay.fmt[l] = f;
         ctx->lb[l] = lay.lb[l] = off;
