@@ -1588,6 +1588,36 @@ __device__ __forceinline__ uint32_t couple_member(uint32_t c, uint32_t kappa, ui
     const uint32_t m = ((c >> h) << (h + 1)) | (c & ((1u << h) - 1u));
     return upper ? m ^ kappa : m;
 }
+__device__ __forceinline__ void red_async_or(uint32_t local_addr, uint32_t local_bar, uint32_t cta, uint32_t v) {
+    uint32_t ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(cta));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(local_bar), "r"(cta));
+    asm volatile("red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.or.b32 [%0], %1, [%2];" ::"r"(ra),
+                 "r"(v), "r"(rb)
+                 : "memory");
+}
+template <int R>
+struct WinTermsBits : WinTermsFlags32<R> {
+    __device__ __forceinline__ long long sum_bits(const uint32_t* sbits, uint32_t L, uint32_t p,
+                                                  const LaneOffsets<R>& off) const {
+        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
+        const int lane = threadIdx.x & 31;
+        const uint32_t x = p & (L - 1), y = p & ~(L - 1);
+        long long acc = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int w = lane + 32 * j;
+            if (w < WN) {
+                const uint32_t q = ((y + (uint32_t)off.oy[j] * L) & (L * L - 1)) + ((x + off.ox[j]) & (L - 1));
+                acc += (sbits[q >> 5] >> (q & 31)) & 1u ? this->v1[j] : this->v0[j];
+            }
+        }
+        return warp_sum_i64(acc);
+    }
+};
+#ifndef BN_SWAP_BITS
+#define BN_SWAP_BITS 1  // SWAP decisions with the accept flags as bits (fewer shared-memory bank conflicts)
+#endif
 // Progress counters of the fused pass tail (k_pass_tail): lut[s] counts the finished dE-term units
 // of class s, dec[s] the decided members of class s; reset by the kernel's last CTA.
 struct TailCounters {
@@ -1631,7 +1661,7 @@ __device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, 
     const uint32_t sflags_addr = (uint32_t)__cvta_generic_to_shared(dsm);
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
     auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
-    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
+    for (uint32_t j = threadIdx.x; j < (BN_SWAP_BITS ? P / 32 : P); j += blockDim.x) sflags[j] = 0;
     for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
         sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
     for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) {
@@ -1668,7 +1698,11 @@ __device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, 
         cluster_sync_all();
         return;
     }
+#if BN_SWAP_BITS
+    WinTermsBits<R> A, An;
+#else
     WinTermsFlags32<R> A, An;
+#endif
     auto load_rows = [&](WinTermsFlags32<R>& X, uint32_t s) {
         if (tc && upc) {
             if (lane == 0) wait_count(tc->lut + s, upc);
@@ -1691,7 +1725,11 @@ __device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, 
                          : "memory");
         const uint32_t p = sSlot[s * cpc + warp];
         BN_ASSERT(p < P);
+#if BN_SWAP_BITS
+        const i128 mine = (i128)A.sum_bits(sflags, L, p, off);
+#else
         const i128 mine = A.sum_flags(sflags, L, p, off, T);
+#endif
         if (lane == 0) {
             sPart[warp][0] = (unsigned long long)mine;
             sPart[warp][1] = (unsigned long long)((u128)mine >> 64);
@@ -1701,7 +1739,11 @@ __device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, 
         const i128 other = (i128)(((u128)sPart[o][1] << 64) | sPart[o][0]);
         const i128 sum = upper ? other + mine : mine + other;
         const bool ok = 2 * sum < 0;
+#if BN_SWAP_BITS
+        if (lane < ncta) red_async_or(sflags_addr + 4 * (p >> 5), mailbox(s), lane, ok ? 1u << (p & 31) : 0u);
+#else
         if (lane < ncta) st_async_u32(sflags_addr + 4 * p, mailbox(s), lane, ok ? 1u : 0u);
+#endif
         if (lane == 0) {
             acc[p] = ok;
             dEp[p] = (ok && !upper) ? 2 * sum : (i128)0;
@@ -1732,33 +1774,6 @@ __global__ void __launch_bounds__(512, 1) k_decide_swap(uint32_t pass_t, uint64_
 // flags are BITS in shared memory (P/8 bytes: 8 KB for 256^2), broadcast with
 // red.async.or.b32 ... mbarrier::complete_tx (4 bytes of transaction per candidate and CTA, sent
 // whether 0 or 1).  Same mailbox protocol as k_decide_cl3.
-__device__ __forceinline__ void red_async_or(uint32_t local_addr, uint32_t local_bar, uint32_t cta, uint32_t v) {
-    uint32_t ra, rb;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(cta));
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(local_bar), "r"(cta));
-    asm volatile("red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.or.b32 [%0], %1, [%2];" ::"r"(ra),
-                 "r"(v), "r"(rb)
-                 : "memory");
-}
-template <int R>
-struct WinTermsBits : WinTermsFlags32<R> {
-    __device__ __forceinline__ long long sum_bits(const uint32_t* sbits, uint32_t L, uint32_t p,
-                                                  const LaneOffsets<R>& off) const {
-        constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
-        const int lane = threadIdx.x & 31;
-        const uint32_t x = p & (L - 1), y = p & ~(L - 1);
-        long long acc = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const int w = lane + 32 * j;
-            if (w < WN) {
-                const uint32_t q = ((y + (uint32_t)off.oy[j] * L) & (L * L - 1)) + ((x + off.ox[j]) & (L - 1));
-                acc += (sbits[q >> 5] >> (q & 31)) & 1u ? this->v1[j] : this->v0[j];
-            }
-        }
-        return warp_sum_i64(acc);
-    }
-};
 // Body of k_decide_big.  With `tc` (the fused pass tail, SWAP) the CTA has one extra warp (warp
 // nw), the publisher, exactly as in decide_swap_body: every lane that wrote a member's acc / dEp
 // counts it in shared memory (release, CTA scope), and the publisher adds the CTA's cpc members of
