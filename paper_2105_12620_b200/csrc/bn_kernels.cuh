@@ -1503,91 +1503,6 @@ __device__ __forceinline__ void st_async_u32(uint32_t local_addr, uint32_t local
                  : "memory");
 }
 
-// Cluster decision kernel v3: as v2 (st.async flag mailboxes, no cluster barrier) but every warp
-// loads its candidate's dE-term rows for the next class straight into registers (issued one
-// class ahead, so the L2 latency hides behind the current class) instead of staging them in
-// shared memory: the shared-memory pipe, which bounds v2's window sums (57 KB of rows written and
-// read back per class and SM), only serves the accept flags.
-template <int R, int mode>
-__global__ void __launch_bounds__(mode ? 256 : 512, 1) k_decide_cl3(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
-                                                       const DTabs T, uint8_t* __restrict__ acc,
-                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log) {
-    constexpr uint32_t NSW = mode ? 2 : 1;  // candidates per warp (SWAP: the candidate and its partner)
-    extern __shared__ __align__(16) uint8_t dsm[];
-    __shared__ uint8_t sDelta[8 * 16];
-    __shared__ uint32_t sKappa[64];
-    __shared__ __align__(8) uint64_t sbar[2];  // mailboxes by class parity
-    const uint32_t nb = L / 8, M = nb * nb, P = L * L;
-    const uint32_t ncta = gridDim.x, first = blockIdx.x * cpc;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* sflags = reinterpret_cast<uint32_t*>(dsm);  // [P]
-    uint32_t* sSlot = sflags + P;                          // [64][cpc * NSW]
-    const uint32_t sflags_addr = (uint32_t)__cvta_generic_to_shared(dsm);
-    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
-    auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
-    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) sflags[j] = 0;
-    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
-        sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
-    if (mode)
-        for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sKappa[j] = swap_kappa(seed, pass_t, j, M);
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uint32_t per_class = cpc * NSW;
-    for (uint32_t j = threadIdx.x; j < 64 * per_class; j += blockDim.x) {
-        const uint32_t s = j / per_class, i = j - s * per_class;
-        const uint32_t m = i < cpc ? first + i : ((first + i - cpc) ^ sKappa[s]);
-        sSlot[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
-    }
-    __syncthreads();
-    WinTermsFlags32<R> A, B, An, Bn;
-    A.load_global(T, sSlot[warp]);
-    if (mode) B.load_global(T, sSlot[cpc + warp]);
-    LaneOffsets<R> off;
-    off.init();
-    cluster_sync_all();  // every CTA's barriers and flags are initialised before any remote st.async
-    for (uint32_t s = 0; s < 64; ++s) {
-        if (s + 1 < 64) {  // next class's rows: in flight while this class waits and sums
-            An.load_global(T, sSlot[(s + 1) * per_class + warp]);
-            if (mode) Bn.load_global(T, sSlot[(s + 1) * per_class + cpc + warp]);
-        }
-        if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
-        if (threadIdx.x == 0)  // this CTA expects M flags of class s (the phase of class s-2 is complete)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
-                         : "memory");
-        const uint32_t m = first + warp, mm = m ^ (mode ? sKappa[s] : 0u);
-        const uint32_t p = sSlot[s * per_class + warp], p2 = mode ? sSlot[s * per_class + cpc + warp] : p;
-        BN_ASSERT(p < P && p2 < P);
-        i128 sum = A.sum_flags(sflags, L, p, off, T);
-        if (mode) sum += B.sum_flags(sflags, L, p2, off, T);
-        const bool ok = 2 * sum < 0;
-        if (lane < ncta) st_async_u32(sflags_addr + 4 * p, mailbox(s), lane, ok ? 1u : 0u);
-        if (lane == 0) {  // bookkeeping for commit/stats
-            acc[p] = ok;
-            dEp[p] = (ok && (!mode || m < mm)) ? 2 * sum : (i128)0;
-            if (log) log[(size_t)s * M + m] = ok;
-        }
-        A = An;
-        if (mode) B = Bn;
-    }
-    tc::mbar_wait(mailbox(63), (63 >> 1) & 1);  // every flag sent to this CTA has landed
-    cluster_sync_all();
-}
-
-// SWAP cluster decision kernel: one warp per couple MEMBER (not per couple), so SWAP decisions
-// run with the same 16 warps x 16 CTAs shape and register budget as REDRAW.  The couples
-// {m, m ^ kappa} of class s are listed by their lower member (bit h = msb(kappa) of m clear), two
-// consecutive slots per couple, so both members of a couple sit in the same CTA, in warps 2j and
-// 2j+1: each warp sums its own member's window (acc-dependent terms, as in v3), the pair exchanges
-// the two int128 sums through shared memory under a 64-thread named barrier, and both decide on
-// the identical total.  Flags are broadcast exactly as in v3 (one st.async per member).
-__device__ __forceinline__ uint32_t couple_member(uint32_t c, uint32_t kappa, uint32_t upper) {
-    const uint32_t h = 31u - __clz(kappa);
-    const uint32_t m = ((c >> h) << (h + 1)) | (c & ((1u << h) - 1u));
-    return upper ? m ^ kappa : m;
-}
 __device__ __forceinline__ void red_async_or(uint32_t local_addr, uint32_t local_bar, uint32_t cta, uint32_t v) {
     uint32_t ra, rb;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(cta));
@@ -1615,6 +1530,91 @@ struct WinTermsBits : WinTermsFlags32<R> {
         return warp_sum_i64(acc);
     }
 };
+// Cluster decision kernel v3: as v2 (st.async flag mailboxes, no cluster barrier) but every warp
+// loads its candidate's dE-term rows for the next class straight into registers (issued one
+// class ahead, so the L2 latency hides behind the current class) instead of staging them in
+// shared memory: the shared-memory pipe, which bounds v2's window sums (57 KB of rows written and
+// read back per class and SM), only serves the accept flags.
+template <int R, int mode>
+__global__ void __launch_bounds__(mode ? 256 : 512, 1) k_decide_cl3(uint32_t pass_t, uint64_t seed, uint32_t L, uint32_t cpc,
+                                                       const DTabs T, uint8_t* __restrict__ acc,
+                                                       i128* __restrict__ dEp, uint8_t* __restrict__ log) {
+    constexpr uint32_t NSW = mode ? 2 : 1;  // candidates per warp (SWAP: the candidate and its partner)
+    extern __shared__ __align__(16) uint8_t dsm[];
+    __shared__ uint8_t sDelta[8 * 16];
+    __shared__ uint32_t sKappa[64];
+    __shared__ __align__(8) uint64_t sbar[2];  // mailboxes by class parity
+    const uint32_t nb = L / 8, M = nb * nb, P = L * L;
+    const uint32_t ncta = gridDim.x, first = blockIdx.x * cpc;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* sflags = reinterpret_cast<uint32_t*>(dsm);  // [P]
+    uint32_t* sSlot = sflags + P;                          // [64][cpc * NSW]
+    const uint32_t sflags_addr = (uint32_t)__cvta_generic_to_shared(dsm);
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
+    auto mailbox = [&](uint32_t s) { return bar0 + 8 * (s & 1); };
+    for (uint32_t j = threadIdx.x; j < P / 32; j += blockDim.x) sflags[j] = 0;  // accept bits
+    for (uint32_t j = threadIdx.x; j < 8 * nb; j += blockDim.x)
+        sDelta[j] = (uint8_t)(philox_seeded(seed, j % nb, pass_t, j / nb, 2).x & 7);
+    if (mode)
+        for (uint32_t j = threadIdx.x; j < 64; j += blockDim.x) sKappa[j] = swap_kappa(seed, pass_t, j, M);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * i) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t per_class = cpc * NSW;
+    for (uint32_t j = threadIdx.x; j < 64 * per_class; j += blockDim.x) {
+        const uint32_t s = j / per_class, i = j - s * per_class;
+        const uint32_t m = i < cpc ? first + i : ((first + i - cpc) ^ sKappa[s]);
+        sSlot[j] = class_pixel_tab(sDelta, L, pass_t, s, m);
+    }
+    __syncthreads();
+    WinTermsBits<R> A, B, An, Bn;
+    A.load_global(T, sSlot[warp]);
+    if (mode) B.load_global(T, sSlot[cpc + warp]);
+    LaneOffsets<R> off;
+    off.init();
+    cluster_sync_all();  // every CTA's barriers and flags are initialised before any remote st.async
+    for (uint32_t s = 0; s < 64; ++s) {
+        if (s + 1 < 64) {  // next class's rows: in flight while this class waits and sums
+            An.load_global(T, sSlot[(s + 1) * per_class + warp]);
+            if (mode) Bn.load_global(T, sSlot[(s + 1) * per_class + cpc + warp]);
+        }
+        if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
+        if (threadIdx.x == 0)  // this CTA expects M flags of class s (the phase of class s-2 is complete)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mailbox(s)), "r"(4 * M)
+                         : "memory");
+        const uint32_t m = first + warp, mm = m ^ (mode ? sKappa[s] : 0u);
+        const uint32_t p = sSlot[s * per_class + warp], p2 = mode ? sSlot[s * per_class + cpc + warp] : p;
+        BN_ASSERT(p < P && p2 < P);
+        i128 sum = (i128)A.sum_bits(sflags, L, p, off);
+        if (mode) sum += (i128)B.sum_bits(sflags, L, p2, off);
+        const bool ok = 2 * sum < 0;
+        if (lane < ncta) red_async_or(sflags_addr + 4 * (p >> 5), mailbox(s), lane, ok ? 1u << (p & 31) : 0u);
+        if (lane == 0) {  // bookkeeping for commit/stats
+            acc[p] = ok;
+            dEp[p] = (ok && (!mode || m < mm)) ? 2 * sum : (i128)0;
+            if (log) log[(size_t)s * M + m] = ok;
+        }
+        A = An;
+        if (mode) B = Bn;
+    }
+    tc::mbar_wait(mailbox(63), (63 >> 1) & 1);  // every flag sent to this CTA has landed
+    cluster_sync_all();
+}
+
+// SWAP cluster decision kernel: one warp per couple MEMBER (not per couple), so SWAP decisions
+// run with the same 16 warps x 16 CTAs shape and register budget as REDRAW.  The couples
+// {m, m ^ kappa} of class s are listed by their lower member (bit h = msb(kappa) of m clear), two
+// consecutive slots per couple, so both members of a couple sit in the same CTA, in warps 2j and
+// 2j+1: each warp sums its own member's window (acc-dependent terms, as in v3), the pair exchanges
+// the two int128 sums through shared memory under a 64-thread named barrier, and both decide on
+// the identical total.  Flags are broadcast exactly as in v3 (one st.async per member).
+__device__ __forceinline__ uint32_t couple_member(uint32_t c, uint32_t kappa, uint32_t upper) {
+    const uint32_t h = 31u - __clz(kappa);
+    const uint32_t m = ((c >> h) << (h + 1)) | (c & ((1u << h) - 1u));
+    return upper ? m ^ kappa : m;
+}
 #ifndef BN_SWAP_BITS
 #define BN_SWAP_BITS 1  // SWAP decisions with the accept flags as bits (fewer shared-memory bank conflicts)
 #endif
