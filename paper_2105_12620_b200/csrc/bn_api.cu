@@ -752,6 +752,8 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     const bool swap_v4 = mode && !ctx->swap_v3;  // SWAP: one warp per couple member (k_decide_swap)
     uint32_t cpc = mode && !swap_v4 ? 8 : 16;
     while (cpc > nb * nb / (swap_v4 ? 1 : nb)) cpc /= 2;  // at most M slots (SWAP v4) / nb per CTA
+    if (swap_v4)  // the full cluster, whole couples (one CTA for M <= 16: C1)
+        cpc = nb * nb <= 16 ? nb * nb : std::max(2u, std::min(16u, nb * nb / 16));
     const uint32_t ncta = nb * nb / cpc;
     *done = false;
     if (ctx->no_cluster) return BN_OK;
@@ -914,8 +916,10 @@ int launch_pass_tail(bn_ctx* ctx, uint32_t t, uint64_t seed, uint8_t* log, uint3
     // k_decide_big's (16 warps x M / 256 slots, flags as bits)
     const bool big = nb > 16;
     if (big && (M % 512 || ctx->no_big)) return BN_OK;  // whole couples per warp
-    uint32_t cpc = big ? M / 16 : 16;
-    while (cpc > M) cpc /= 2;
+    // members per deciding CTA: spread each class over the full 16-CTA cluster (C2: 4 members per
+    // CTA, tail 0.069 -> 0.057 ms; fewer warps per SM issue the window sums faster), whole couples;
+    // tiny classes (M <= 16) stay in one CTA
+    uint32_t cpc = big ? M / 16 : M <= 16 ? M : std::max(2u, std::min(16u, M / 16));
     const uint32_t ncta = M / cpc;
     const size_t smem = (big ? (size_t)P / 8 : 4 * (size_t)P) + (size_t)64 * cpc * 6;
     if (smem > 220 * 1024) return BN_OK;
