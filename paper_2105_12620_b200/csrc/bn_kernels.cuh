@@ -1420,7 +1420,8 @@ template <int R>
 struct LaneOffsets {
     static constexpr int WN = WinTerms<R>::WN, PER = WinTerms<R>::PER;
     int oy[PER], ox[PER];
-    __device__ __forceinline__ void init() {
+    int d[PER];  // oy * L + ox: the neighbour's pixel offset when the window does not wrap
+    __device__ __forceinline__ void init(uint32_t L = 0) {
         const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
@@ -1428,6 +1429,7 @@ struct LaneOffsets {
             const int ww = w >= R * (2 * R + 1) + R ? w + 1 : w;
             oy[j] = w < WN ? ww / (2 * R + 1) - R : 0;
             ox[j] = w < WN ? ww % (2 * R + 1) - R : 0;
+            d[j] = oy[j] * (int)L + ox[j];
         }
     }
 };
@@ -1519,12 +1521,25 @@ struct WinTermsBits : WinTermsFlags32<R> {
         const int lane = threadIdx.x & 31;
         const uint32_t x = p & (L - 1), y = p & ~(L - 1);
         long long acc = 0;
+        // the window does not wrap (warp-uniform): neighbour = p + oy L + ox, one add per term
+        const bool inner = x >= (uint32_t)R && x + R < L && y >= (uint32_t)R * L && y + R * L < L * L;
+        if (inner) {
 #pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const int w = lane + 32 * j;
-            if (w < WN) {
-                const uint32_t q = ((y + (uint32_t)off.oy[j] * L) & (L * L - 1)) + ((x + off.ox[j]) & (L - 1));
-                acc += (sbits[q >> 5] >> (q & 31)) & 1u ? this->v1[j] : this->v0[j];
+            for (int j = 0; j < PER; ++j) {
+                const int w = lane + 32 * j;
+                if (w < WN) {
+                    const uint32_t q = p + (uint32_t)off.d[j];
+                    acc += (sbits[q >> 5] >> (q & 31)) & 1u ? this->v1[j] : this->v0[j];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int w = lane + 32 * j;
+                if (w < WN) {
+                    const uint32_t q = ((y + (uint32_t)off.oy[j] * L) & (L * L - 1)) + ((x + off.ox[j]) & (L - 1));
+                    acc += (sbits[q >> 5] >> (q & 31)) & 1u ? this->v1[j] : this->v0[j];
+                }
             }
         }
         return warp_sum_i64(acc);
@@ -1573,7 +1588,7 @@ __global__ void __launch_bounds__(mode ? 256 : 512, 1) k_decide_cl3(uint32_t pas
     A.load_global(T, sSlot[warp]);
     if (mode) B.load_global(T, sSlot[cpc + warp]);
     LaneOffsets<R> off;
-    off.init();
+    off.init(L);
     cluster_sync_all();  // every CTA's barriers and flags are initialised before any remote st.async
     for (uint32_t s = 0; s < 64; ++s) {
         if (s + 1 < 64) {  // next class's rows: in flight while this class waits and sums
@@ -1714,7 +1729,7 @@ __device__ __forceinline__ void decide_swap_body(uint8_t* dsm, uint32_t pass_t, 
     };
     load_rows(A, 0);
     LaneOffsets<R> off;
-    off.init();
+    off.init(L);
     cluster_sync_all();  // every CTA's barriers and flags are initialised before any remote st.async
     const uint32_t upper = (first + warp) & 1, pair_bar = 1 + (warp >> 1);
     for (uint32_t s = 0; s < 64; ++s) {
@@ -1837,7 +1852,7 @@ __device__ __forceinline__ void decide_big_body(uint8_t* dsm, uint32_t pass_t, u
     WinTermsBits<R> A, An;
     A.load_global(T, sSlot[w0]);
     LaneOffsets<R> off;
-    off.init();
+    off.init(L);
     cluster_sync_all();
     for (uint32_t s = 0; s < 64; ++s) {
         if (s > 0) tc::mbar_wait(mailbox(s - 1), ((s - 1) >> 1) & 1);  // all flags of class s-1
