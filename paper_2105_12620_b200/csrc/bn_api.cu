@@ -754,6 +754,8 @@ int launch_decide_cluster(bn_ctx* ctx, uint32_t t, uint64_t seed, int mode, uint
     while (cpc > nb * nb / (swap_v4 ? 1 : nb)) cpc /= 2;  // at most M slots (SWAP v4) / nb per CTA
     if (swap_v4)  // the full cluster, whole couples (one CTA for M <= 16: C1)
         cpc = nb * nb <= 16 ? nb * nb : std::max(2u, std::min(16u, nb * nb / 16));
+    else if (!mode)  // REDRAW: the same spread (C2 REDRAW decide 0.042 -> 0.038 ms)
+        cpc = nb * nb <= 16 ? nb * nb : std::max(1u, std::min(16u, nb * nb / 16));
     const uint32_t ncta = nb * nb / cpc;
     *done = false;
     if (ctx->no_cluster) return BN_OK;
