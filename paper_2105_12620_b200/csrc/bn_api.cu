@@ -199,6 +199,7 @@ struct bn_ctx {
     DevBuf<unsigned int> gsched;   // Gram work counter + CTA exit counter (dynamic item scheduling)
     bool static_sched = false;     // BN_GRAM_SCHED=static: round-robin items instead
     bool no_csplit = false;        // BN_GRAM_CSPLIT=0: small tiles keep whole (block, level) items
+    bool force_csplit = false;     // BN_GRAM_CSPLIT=1: every tile splits its items into chunks
 
     bool tail_attr_set[8] = {false};
     int tail_clusters = -1;        // clusters of the fused pass tail that fit (cached for tail_L)
@@ -491,7 +492,12 @@ int launch_gram(bn_ctx* ctx, const uint8_t* cn, const int* nn) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
     // small tiles (fewer (block, level) items than SMs): one item per neighbour chunk
-    const uint32_t csplit = (ctx->L / 8) * (ctx->L / 8) * ctx->nl < (uint32_t)nsm && !ctx->no_csplit ? tc3::NCHUNK : 1;
+    // ... and long rows (Tp >= 2048: operands beyond L2): the three chunk items of a block run
+    // concurrently on three SMs and share its A rows in L2 (C5 Gram DRAM reads 1.02 -> 0.62 GB,
+    // 0.337 -> 0.329 ms; C3 would lose: 0.105 -> 0.117 ms)
+    const uint32_t csplit = ctx->force_csplit || (((ctx->L / 8) * (ctx->L / 8) * ctx->nl < (uint32_t)nsm || ctx->Tp >= 2048) &&
+                                                  !ctx->no_csplit)
+                                ? tc3::NCHUNK : 1;
     const uint32_t items = (ctx->L / 8) * (ctx->L / 8) * ctx->nl * csplit;
     const uint32_t grid = items < (uint32_t)nsm ? items : (uint32_t)nsm;
     KSTART(BN_K_GRAM);
@@ -1155,6 +1161,7 @@ int bn_create(bn_ctx** out, int cuda_device, uintptr_t cuda_stream) {
     ctx->no_border = go && !strcmp(go, "raster");
     const char* csp = getenv("BN_GRAM_CSPLIT");
     ctx->no_csplit = csp && !strcmp(csp, "0");
+    ctx->force_csplit = csp && !strcmp(csp, "1");
     const char* gs = getenv("BN_GRAM_SCHED");
     ctx->static_sched = gs && !strcmp(gs, "static");
     const char* tl = getenv("BN_TAIL");
